@@ -1,0 +1,177 @@
+/*
+ * avd.h — C ABI of the B200-native activation outlier-attribution pass
+ * (arXiv 2603.10444, section "Mean Bias as the Dominant Source of Activation Outliers",
+ * PAPER.md:1-27).  Library: paper_2603_10444_b200/libavd.so (sm_100a only).
+ *
+ * For an fp32 activation matrix X (l = b*s tokens x m hidden, row-major) the pass computes
+ *   mu      = (1/l) X^T 1
+ *   Xc      = X - 1 mu^T
+ *   spike   = rank-k truncated SVD of Xc, k = floor(0.01 m)
+ *             (V_k, sigma_k from the top-k eigenpairs of G = Xc^T Xc)
+ *   tail    = Xc - spike
+ *   energies ||X||^2 = ||M||^2 + ||spike||^2 + ||tail||^2
+ *   E_top   = top 0.1% entries by |X_ij|
+ *   rho     = M_ij^2/X_ij^2, spike_ij^2/X_ij^2, tail_ij^2/X_ij^2
+ *   cross   = 1 - sum(rho)   (the "minor cross-terms")
+ * Readings of the paper where it is silent are listed in DESIGN.md ("Readings" R1..R13).
+ *
+ * Conventions (all entry points):
+ *   - Pointers named *_dev are CUDA device pointers on the context's device; *_host are host.
+ *   - Every output buffer is caller-owned; the library keeps no caller pointer after return.
+ *   - The library owns its workspace (device memory allocated in avd_create, freed in
+ *     avd_destroy); avd_plan reports its size before creation.
+ *   - All device work is stream-ordered on the context's stream.  Entry points that return
+ *     host scalars synchronise that stream before returning.
+ *   - Errors are status codes (never aborts or exceptions); avd_last_error() gives a
+ *     thread-local message for the last failing call.
+ *   - Results are deterministic for fixed (X, seed, world size): the Gram is accumulated
+ *     exactly in integers, and every floating-point reduction has a fixed order.
+ *   - Row sharding (world > 1): rank r owns rows [row_offset, row_offset + l_local) of the
+ *     global matrix; linear indices are global (i * m + j).  Between the stage entry points
+ *     the caller all-reduces the buffers avd_buffer() exposes (see paper_2603_10444_b200/
+ *     distributed.py); with world == 1 avd_decompose runs the whole pass.
+ */
+#ifndef AVD_H_
+#define AVD_H_
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  AVD_OK = 0,
+  AVD_EINVAL = 1,      /* bad sizes / fractions / pointers / alignment / workspace        */
+  AVD_ENONFINITE = 2,  /* X contains NaN or Inf (R5)               */
+  AVD_ENOCONV = 3,     /* eigensolver hit max_iters before eig_tol; outputs still written */
+  AVD_ECUDA = 4,       /* a CUDA runtime / driver call failed                             */
+  AVD_ENOMEM = 6,      /* device allocation failed                                       */
+  AVD_ESTATE = 8       /* stage called out of order                                      */
+} avd_status;
+
+/* Sizes derived from (l, m, fractions) — DESIGN.md R1, R2:
+ *   k     = max(1, floor(k_frac * m))          ("k = floor(0.01 m)")
+ *   n_top = max(1, floor(top_frac * l * m))    ("top 0.1%")
+ * floor(f*n) is taken as round(f*n) when |f*n - round(f*n)| < 1e-9.                     */
+typedef struct {
+  int32_t k;               /* spike rank                                                    */
+  int32_t p;               /* subspace-iteration block size = roundup16(k + 8)              */
+  int64_t n_top;           /* |E_top| requested (global)                                    */
+  int32_t digits;          /* int8 digit planes per centred entry in the Gram (2 or 3)      */
+  size_t workspace_bytes;  /* device bytes avd_create will allocate                         */
+} avd_plan_t;
+
+typedef struct {
+  int64_t l_global;        /* global rows l (>= 2)                                           */
+  int64_t l_local;         /* rows held by this rank (== l_global when world == 1)           */
+  int64_t row_offset;      /* first global row of this rank                                  */
+  int64_t m;               /* columns (>= 2)                                                 */
+  double k_frac;           /* 0.01; used when k_override == 0                  */
+  double top_frac;         /* 0.001; used when n_top_override == 0             */
+  int32_t k_override;      /* > 0: use this k                                                */
+  int64_t n_top_override;  /* > 0: use this |E_top|                                          */
+  uint64_t seed;           /* start block of the subspace iteration + Gram dither            */
+  int32_t max_iters;       /* subspace iterations cap (0 -> 200)                             */
+  double eig_tol;          /* Ritz residual tolerance relative to lambda_1 (0 -> 1e-10)      */
+  int32_t digits;          /* 0 -> 3; Gram operand = centred X in `digits` int8 digit planes */
+  int32_t world;           /* ranks sharing the rows (1 = single GPU)                        */
+  int32_t device;          /* CUDA device ordinal                                            */
+  void* stream;            /* cudaStream_t (NULL = legacy default stream)                    */
+} avd_config;
+
+/* Outputs.  Device arrays caller-owned, sized from the plan (cap = n_top). */
+typedef struct {
+  double* mu_dev;          /* [m] feature-wise mean mu                          */
+  double* V_dev;           /* [m*k] row-major: V[j*k + r] = component j of v_r */
+  double* sigma_dev;       /* [k] singular values of Xc, descending                          */
+  int64_t* top_idx_dev;    /* [n_top] global linear indices i*m+j of THIS rank's part of
+                              E_top, ascending (ties by smaller index, zeros excluded; R3,R4)*/
+  double* rho_dev;         /* [n_top*4]: rho_mean, rho_spike, rho_tail, cross per entry      */
+  /* host scalars written on return */
+  int64_t n_top_local;     /* entries of E_top owned by this rank                            */
+  int64_t top_offset;      /* position of this rank's slice inside the global E_top          */
+  int64_t n_top_global;    /* |E_top| (< requested only if X has fewer nonzeros)             */
+  double energy_cf[4];     /* closed forms: total = sum x^2, mean = l||mu||^2,
+                              spike = sum_{r<k} sigma_r^2, tail = tr(G) - spike*/
+  double energy_el[4];     /* elementwise: sum x^2, sum M^2, sum spike^2, sum tail^2         */
+  double cross_el[3];      /* <M,spike>, <M,tail>, <spike,tail> Frobenius inner products     */
+  double colmean_absmax[2];/* max_j |mean_i spike_ij|, max_j |mean_i tail_ij|  */
+  double rho_mean_aggr[4]; /* mean over E_top of rho_mean, rho_spike, rho_tail, cross (R10)  */
+  double rho_energy_aggr[3]; /* sum_E c^2 / sum_E x^2, c = M, spike, tail                    */
+  double sigma_next;       /* sigma_{k+1} (Ritz estimate; 0 when unavailable)                */
+  double trace_g;          /* tr(G) = ||Xc||_F^2                                             */
+  int32_t iters;           /* subspace iterations used                                       */
+  double max_resid;        /* max_r<k ||G v_r - lambda_r v_r|| / lambda_1                     */
+} avd_outputs;
+
+typedef struct avd_ctx avd_ctx;
+
+/* Sizes and workspace for a configuration (no device work).  AVD_EINVAL when l_global < 2,
+ * m < 2, k > min(l, m), a fraction outside (0, 1], p > 112, or the row
+ * shard is inconsistent.                                                                    */
+avd_status avd_plan(const avd_config* cfg, avd_plan_t* plan);
+
+/* Allocate the workspace on cfg->device and bind cfg->stream.  *ctx is NULL on failure.     */
+avd_status avd_create(const avd_config* cfg, avd_ctx** ctx);
+void avd_destroy(avd_ctx* ctx);
+avd_status avd_get_plan(const avd_ctx* ctx, avd_plan_t* plan);
+
+/* The whole pass on one GPU (cfg.world == 1).  X_dev: device, row-major l x m fp32, 16-byte
+ * aligned, read only, not retained.  out: device arrays (see avd_outputs) + host scalars.
+ * Blocks until outputs are ready.  AVD_ENONFINITE if X has NaN/Inf (outputs untouched);
+ * AVD_ENOCONV if the eigensolver hit max_iters (outputs written, iters/max_resid tell).     */
+avd_status avd_decompose(avd_ctx* ctx, const float* X_dev, avd_outputs* out);
+
+/* Same pass from HOST memory: X_host (l x m fp32, pinned or pageable) is copied to an
+ * internal device buffer (allocated on first use, freed by avd_destroy); out's array fields
+ * are HOST pointers here and receive the results by device-to-host copy.                   */
+avd_status avd_decompose_host(avd_ctx* ctx, const float* X_host, avd_outputs* out);
+
+/* ---- stage entry points (row-sharded, world >= 1) -------------------------------------
+ * Call in this order; after each stage the caller all-reduces (over all ranks, in place)
+ * the buffers listed, then calls the next stage.  With world == 1 no exchange is needed.
+ *   avd_stage_stats    (K1 column sums, sum x^2, column max/min, |x| histogram)
+ *       exchange: AVD_BUF_STATS (f64, SUM), AVD_BUF_COLMAX (f32, MAX),
+ *                 AVD_BUF_COLMIN (f32, MIN), AVD_BUF_HIST1 (i64, SUM)
+ *   avd_stage_split    (mu, column scales, K2 centred int8 digit planes + top-set candidates)
+ *   avd_stage_gram     (K3 tcgen05 int8 Gram, exact int64)   exchange: AVD_BUF_GRAM (i64, SUM)
+ *   avd_stage_eig      (K4 subspace iteration + Rayleigh-Ritz; replicated on every rank)
+ *   avd_stage_project  (K5+K8 projections P = Xc V_k and elementwise energies)
+ *       exchange: AVD_BUF_ENERGY (f64, SUM)
+ *   avd_stage_select(level 0)  (K6 second-level histogram)    exchange: AVD_BUF_HIST2 (i64, SUM)
+ *   avd_stage_select(level 1)  (K6 third-level histogram)     exchange: AVD_BUF_HIST3 (i64, SUM)
+ *   avd_stage_select(level 2)  (K6 mark + per-rank tie count) exchange: AVD_BUF_TIES (i64, SUM)
+ *   avd_stage_gather   (K6 ordered compaction with the rank's tie quota, K7 rho gather)
+ *       exchange: AVD_BUF_AGG (f64, SUM)
+ *   avd_stage_report   (host scalars into out)                                            */
+typedef enum {
+  AVD_BUF_STATS = 0, AVD_BUF_COLMAX = 1, AVD_BUF_COLMIN = 2, AVD_BUF_HIST1 = 3,
+  AVD_BUF_GRAM = 4, AVD_BUF_ENERGY = 5, AVD_BUF_HIST2 = 6, AVD_BUF_HIST3 = 7,
+  AVD_BUF_TIES = 8, AVD_BUF_AGG = 9,
+  /* read-only views for tests / diagnostics (not exchanged) */
+  AVD_BUF_MU = 16, AVD_BUF_G = 17, AVD_BUF_P = 18, AVD_BUF_DIGITS = 19, AVD_BUF_SCALE = 20
+} avd_buffer_id;
+
+/* Device pointer and byte size of a workspace buffer (valid until avd_destroy). */
+avd_status avd_buffer(avd_ctx* ctx, int32_t which, void** dev_ptr, size_t* bytes);
+
+avd_status avd_stage_stats(avd_ctx* ctx, const float* X_dev);
+avd_status avd_stage_split(avd_ctx* ctx, const float* X_dev);
+avd_status avd_stage_gram(avd_ctx* ctx);
+avd_status avd_stage_eig(avd_ctx* ctx);
+avd_status avd_stage_project(avd_ctx* ctx, const float* X_dev);
+avd_status avd_stage_select(avd_ctx* ctx, const float* X_dev, int32_t level, int32_t rank);
+avd_status avd_stage_gather(avd_ctx* ctx, const float* X_dev, int32_t rank, avd_outputs* out);
+avd_status avd_stage_report(avd_ctx* ctx, avd_outputs* out);
+
+/* Number of kernels this context launched since creation (for the bench's gpu_launches). */
+int64_t avd_launch_count(const avd_ctx* ctx);
+
+const char* avd_strerror(avd_status s);
+const char* avd_last_error(void); /* thread-local message of the last failing call */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AVD_H_ */

@@ -1,0 +1,183 @@
+"""Thin ctypes binding of libavd.so (include/avd.h) — argument marshalling only.
+
+Same names as the C ABI.  Every numerical step runs in the library's CUDA kernels; this module
+never falls back to anything else: if libavd.so is missing or cannot load, it raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libavd.so")
+
+AVD_OK, AVD_EINVAL, AVD_ENONFINITE, AVD_ENOCONV, AVD_ECUDA, AVD_ENOMEM, AVD_ESTATE = 0, 1, 2, 3, 4, 6, 8
+BUF = dict(STATS=0, COLMAX=1, COLMIN=2, HIST1=3, GRAM=4, ENERGY=5, HIST2=6, HIST3=7, TIES=8, AGG=9,
+           MU=16, G=17, P=18, DIGITS=19, SCALE=20)
+
+# every symbol include/avd.h declares
+EXPORTS = ["avd_plan", "avd_create", "avd_destroy", "avd_get_plan", "avd_decompose",
+           "avd_decompose_host", "avd_buffer", "avd_stage_stats", "avd_stage_split",
+           "avd_stage_gram", "avd_stage_eig", "avd_stage_project", "avd_stage_select",
+           "avd_stage_gather", "avd_stage_report", "avd_launch_count", "avd_strerror",
+           "avd_last_error"]
+
+
+class avd_plan_t(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_int32), ("p", ctypes.c_int32), ("n_top", ctypes.c_int64),
+                ("digits", ctypes.c_int32), ("workspace_bytes", ctypes.c_size_t)]
+
+
+class avd_config(ctypes.Structure):
+    _fields_ = [("l_global", ctypes.c_int64), ("l_local", ctypes.c_int64),
+                ("row_offset", ctypes.c_int64), ("m", ctypes.c_int64),
+                ("k_frac", ctypes.c_double), ("top_frac", ctypes.c_double),
+                ("k_override", ctypes.c_int32), ("n_top_override", ctypes.c_int64),
+                ("seed", ctypes.c_uint64), ("max_iters", ctypes.c_int32),
+                ("eig_tol", ctypes.c_double), ("digits", ctypes.c_int32),
+                ("world", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("stream", ctypes.c_void_p)]
+
+
+class avd_outputs(ctypes.Structure):
+    _fields_ = [("mu_dev", ctypes.c_void_p), ("V_dev", ctypes.c_void_p),
+                ("sigma_dev", ctypes.c_void_p), ("top_idx_dev", ctypes.c_void_p),
+                ("rho_dev", ctypes.c_void_p),
+                ("n_top_local", ctypes.c_int64), ("top_offset", ctypes.c_int64),
+                ("n_top_global", ctypes.c_int64),
+                ("energy_cf", ctypes.c_double * 4), ("energy_el", ctypes.c_double * 4),
+                ("cross_el", ctypes.c_double * 3), ("colmean_absmax", ctypes.c_double * 2),
+                ("rho_mean_aggr", ctypes.c_double * 4), ("rho_energy_aggr", ctypes.c_double * 3),
+                ("sigma_next", ctypes.c_double), ("trace_g", ctypes.c_double),
+                ("iters", ctypes.c_int32), ("max_resid", ctypes.c_double)]
+
+
+_lib = None
+
+
+class AvdError(RuntimeError):
+    def __init__(self, status: int, where: str, msg: str):
+        super().__init__(f"{where}: status {status} ({msg})")
+        self.status = status
+
+
+def lib() -> ctypes.CDLL:
+    """Load libavd.so (raises if it is missing — there is no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built; run paper_2603_10444_b200/build.py "
+                              "(or __graft_entry__.build())")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I32, I64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+        L.avd_plan.argtypes = [ctypes.POINTER(avd_config), ctypes.POINTER(avd_plan_t)]
+        L.avd_create.argtypes = [ctypes.POINTER(avd_config), ctypes.POINTER(P)]
+        L.avd_destroy.argtypes = [P]
+        L.avd_destroy.restype = None
+        L.avd_get_plan.argtypes = [P, ctypes.POINTER(avd_plan_t)]
+        L.avd_decompose.argtypes = [P, P, ctypes.POINTER(avd_outputs)]
+        L.avd_decompose_host.argtypes = [P, P, ctypes.POINTER(avd_outputs)]
+        L.avd_buffer.argtypes = [P, I32, ctypes.POINTER(P), ctypes.POINTER(ctypes.c_size_t)]
+        L.avd_stage_stats.argtypes = [P, P]
+        L.avd_stage_split.argtypes = [P, P]
+        L.avd_stage_gram.argtypes = [P]
+        L.avd_stage_eig.argtypes = [P]
+        L.avd_stage_project.argtypes = [P, P]
+        L.avd_stage_select.argtypes = [P, P, I32, I32]
+        L.avd_stage_gather.argtypes = [P, P, I32, ctypes.POINTER(avd_outputs)]
+        L.avd_stage_report.argtypes = [P, ctypes.POINTER(avd_outputs)]
+        L.avd_launch_count.argtypes = [P]
+        L.avd_launch_count.restype = I64
+        L.avd_strerror.argtypes = [ctypes.c_int]
+        L.avd_strerror.restype = ctypes.c_char_p
+        L.avd_last_error.argtypes = []
+        L.avd_last_error.restype = ctypes.c_char_p
+        for name in EXPORTS:
+            if name not in ("avd_destroy", "avd_launch_count", "avd_strerror", "avd_last_error"):
+                getattr(L, name).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def check(status: int, where: str, ok=(AVD_OK,)) -> int:
+    if status not in ok:
+        L = lib()
+        raise AvdError(status, where, f"{L.avd_strerror(status).decode()}: {L.avd_last_error().decode()}")
+    return status
+
+
+# ---- same-name wrappers -------------------------------------------------------------------
+def avd_plan(cfg: avd_config) -> avd_plan_t:
+    p = avd_plan_t()
+    check(lib().avd_plan(ctypes.byref(cfg), ctypes.byref(p)), "avd_plan")
+    return p
+
+
+def avd_create(cfg: avd_config) -> ctypes.c_void_p:
+    h = ctypes.c_void_p()
+    check(lib().avd_create(ctypes.byref(cfg), ctypes.byref(h)), "avd_create")
+    return h
+
+
+def avd_destroy(h) -> None:
+    lib().avd_destroy(h)
+
+
+def avd_get_plan(h) -> avd_plan_t:
+    p = avd_plan_t()
+    check(lib().avd_get_plan(h, ctypes.byref(p)), "avd_get_plan")
+    return p
+
+
+def avd_decompose(h, X_ptr: int, out: avd_outputs) -> int:
+    return check(lib().avd_decompose(h, ctypes.c_void_p(X_ptr), ctypes.byref(out)), "avd_decompose",
+                 ok=(AVD_OK, AVD_ENOCONV))
+
+
+def avd_decompose_host(h, X_ptr: int, out: avd_outputs) -> int:
+    return check(lib().avd_decompose_host(h, ctypes.c_void_p(X_ptr), ctypes.byref(out)),
+                 "avd_decompose_host", ok=(AVD_OK, AVD_ENOCONV))
+
+
+def avd_buffer(h, which: int):
+    p = ctypes.c_void_p()
+    n = ctypes.c_size_t()
+    check(lib().avd_buffer(h, which, ctypes.byref(p), ctypes.byref(n)), "avd_buffer")
+    return p.value, n.value
+
+
+def avd_stage_stats(h, X_ptr: int):
+    return check(lib().avd_stage_stats(h, ctypes.c_void_p(X_ptr)), "avd_stage_stats")
+
+
+def avd_stage_split(h, X_ptr: int):
+    return check(lib().avd_stage_split(h, ctypes.c_void_p(X_ptr)), "avd_stage_split")
+
+
+def avd_stage_gram(h):
+    return check(lib().avd_stage_gram(h), "avd_stage_gram")
+
+
+def avd_stage_eig(h):
+    return check(lib().avd_stage_eig(h), "avd_stage_eig", ok=(AVD_OK, AVD_ENOCONV))
+
+
+def avd_stage_project(h, X_ptr: int):
+    return check(lib().avd_stage_project(h, ctypes.c_void_p(X_ptr)), "avd_stage_project")
+
+
+def avd_stage_select(h, X_ptr: int, level: int, rank: int):
+    return check(lib().avd_stage_select(h, ctypes.c_void_p(X_ptr), level, rank), "avd_stage_select")
+
+
+def avd_stage_gather(h, X_ptr: int, rank: int, out: avd_outputs):
+    return check(lib().avd_stage_gather(h, ctypes.c_void_p(X_ptr), rank, ctypes.byref(out)),
+                 "avd_stage_gather")
+
+
+def avd_stage_report(h, out: avd_outputs):
+    return check(lib().avd_stage_report(h, ctypes.byref(out)), "avd_stage_report")
+
+
+def avd_launch_count(h) -> int:
+    return int(lib().avd_launch_count(h))

@@ -1,0 +1,477 @@
+// avd.cu — C ABI (include/avd.h): plan, workspace, stage orchestration and the one-call pass.
+// Every numerical step runs in the kernels of k_*.cu; this file only validates arguments,
+// carves the workspace, launches, and copies the final scalars.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace avd {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+namespace {
+
+int64_t floor_frac(double f, int64_t n) {
+  const double v = f * (double)n;
+  const double r = std::nearbyint(v);
+  return std::fabs(v - r) < 1e-9 ? (int64_t)r : (int64_t)std::floor(v);
+}
+
+struct Layout {
+  // byte offsets inside the single workspace allocation
+  size_t off[64];
+  size_t total = 0;
+  int n = 0;
+  size_t add(size_t bytes) {
+    total = (total + 255) & ~size_t(255);
+    off[n] = total;
+    total += bytes;
+    return (size_t)n++;
+  }
+};
+
+avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* lay) {
+  if (!cfg || !plan) { set_error("null argument"); return AVD_EINVAL; }
+  const int64_t l = cfg->l_global, m = cfg->m;
+  if (l < 2 || m < 2) { set_error("l and m must be >= 2 (SPEC.md:225)"); return AVD_EINVAL; }
+  const int world = cfg->world <= 0 ? 1 : cfg->world;
+  if (cfg->l_local < 1 || cfg->row_offset < 0 || cfg->row_offset + cfg->l_local > l ||
+      (world == 1 && (cfg->l_local != l || cfg->row_offset != 0))) {
+    set_error("inconsistent row shard");
+    return AVD_EINVAL;
+  }
+  if (cfg->k_override <= 0 && !(cfg->k_frac > 0.0 && cfg->k_frac <= 1.0)) { set_error("k_frac must be in (0,1]"); return AVD_EINVAL; }
+  if (cfg->n_top_override <= 0 && !(cfg->top_frac > 0.0 && cfg->top_frac <= 1.0)) { set_error("top_frac must be in (0,1]"); return AVD_EINVAL; }
+  const int64_t k = cfg->k_override > 0 ? cfg->k_override : std::max<int64_t>(1, floor_frac(cfg->k_frac, m));
+  if (k > std::min(l, m)) { set_error("k > min(l, m) (SPEC.md:227)"); return AVD_EINVAL; }
+  const int64_t p = ((k + 8 + 15) / 16) * 16;
+  if (p > kMaxP || k > 96) { set_error("k too large for this build (p <= 112, k <= 96)"); return AVD_EINVAL; }
+  const int64_t n_top = cfg->n_top_override > 0 ? cfg->n_top_override : std::max<int64_t>(1, floor_frac(cfg->top_frac, l * m));
+  const int nd = cfg->digits == 0 ? 3 : cfg->digits;
+  if (nd != 2 && nd != 3) { set_error("digits must be 2 or 3"); return AVD_EINVAL; }
+  plan->k = (int32_t)k;
+  plan->p = (int32_t)p;
+  plan->n_top = n_top;
+  plan->digits = nd;
+
+  Ctx tmp;
+  Ctx* C = c ? c : &tmp;
+  C->cfg = *cfg;
+  C->cfg.world = world;
+  C->k = (int)k;
+  C->p = (int)p;
+  C->k_pad = (int)(((k + 15) / 16) * 16);
+  C->nd = nd;
+  C->m_pad = round_up(m, kGramTile);
+  C->l_pad = round_up(cfg->l_local, kGramK);
+  const int64_t ll = cfg->l_local;
+  const int ncb = (int)ceil_div(m, 256LL * ((m % 4 == 0) ? 4 : 1));
+  C->r1 = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(4LL * C->num_sms, ncb), ceil_div(ll, 4)));
+  C->cand_cap = std::min<int64_t>(ll * m, std::max<int64_t>(4 * n_top, 1 << 20));
+  C->n_red = (int)ceil_div(m, 32);
+  C->n_proj_ctas = (int)ceil_div(ll, 32);
+  C->nwords = ceil_div(ll * m, 32);
+  C->nblk = ceil_div(C->nwords, 1024);
+  C->n_gather_ctas = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_top, 256), 4LL * C->num_sms));
+
+  Layout L;
+  L.add(sizeof(double) * C->r1 * m);            // 0 colsum_part
+  L.add(sizeof(float) * C->r1 * m);             // 1 colmax_part
+  L.add(sizeof(float) * C->r1 * m);             // 2 colmin_part
+  L.add(sizeof(double) * C->r1 * ncb);          // 3 sq_part
+  L.add(sizeof(double) * (m + 2));              // 4 stats
+  L.add(sizeof(float) * m);                     // 5 colmax
+  L.add(sizeof(float) * m);                     // 6 colmin
+  L.add(sizeof(unsigned long long) * kHistBins);// 7 hist1
+  L.add(sizeof(double) * m);                    // 8 mu
+  L.add(sizeof(int32_t) * C->m_pad);            // 9 shift
+  L.add(sizeof(DevPlan));                       // 10 dplan
+  L.add((size_t)nd * C->m_pad * C->l_pad);      // 11 digits
+  L.add(sizeof(uint32_t) * C->cand_cap);        // 12 cand_key
+  L.add(sizeof(uint64_t) * C->cand_cap);        // 13 cand_idx
+  L.add(sizeof(unsigned long long));            // 14 cand_cnt
+  L.add(sizeof(long long) * C->m_pad * C->m_pad);// 15 gram_i
+  L.add(sizeof(double) * m * m);                // 16 G
+  L.add(sizeof(double) * m * p);                // 17 Q
+  L.add(sizeof(double) * m * p);                // 18 Y
+  L.add(sizeof(double) * m * p);                // 19 Z
+  L.add(sizeof(double) * m * p);                // 20 U
+  L.add(sizeof(double) * p * p);                // 21 H
+  L.add(sizeof(double) * p * p);                // 22 W
+  L.add(sizeof(double) * 2 * p);                // 23 theta
+  L.add(sizeof(double) * C->n_red * p * p);     // 24 red_part
+  L.add(sizeof(double) * 2 * p);                // 25 resid
+  L.add(sizeof(double));                        // 26 trace
+  L.add(sizeof(double) * m * k);                // 27 V
+  L.add(sizeof(double) * k);                    // 28 sigma
+  L.add(sizeof(float) * m * C->k_pad);          // 29 V32
+  L.add(sizeof(float) * ll * C->k_pad);         // 30 P
+  L.add(sizeof(double) * C->n_proj_ctas * 4);   // 31 en_part
+  L.add(sizeof(double) * C->n_proj_ctas * C->k_pad);  // 32 colsumP_part
+  L.add(sizeof(double) * (4 + C->k_pad));       // 33 energy
+  L.add(sizeof(unsigned long long) * kHistBins);// 34 hist2
+  L.add(sizeof(unsigned long long) * kHist3Bins);// 35 hist3
+  L.add(sizeof(long long) * 2 * world);         // 36 ties
+  L.add(sizeof(uint32_t) * C->nwords);          // 37 bm_sel
+  L.add(sizeof(uint32_t) * C->nwords);          // 38 bm_tie
+  L.add(sizeof(int64_t) * (2 * C->nblk + 2));   // 39 blk_cnt
+  L.add(sizeof(double) * 8);                    // 40 agg
+  L.add(sizeof(double) * 8 * C->n_gather_ctas); // 41 agg_part
+  L.add(sizeof(double) * 16);                   // 42 report
+  plan->workspace_bytes = L.total;
+  if (lay) *lay = L;
+  return AVD_OK;
+}
+
+// colmean maxima and <M,spike>, <M,tail>, l||mu||^2 (one CTA, fixed-order reductions)
+__global__ void report_kernel(const double* __restrict__ energy, const double* __restrict__ stats,
+                              const double* __restrict__ mu, const double* __restrict__ V, int64_t m, int k,
+                              int64_t l_global, double* __restrict__ rep) {
+  __shared__ double s_ms[256], s_mt[256], s_as[256], s_at[256], s_mu2[256];
+  double ms = 0, mt = 0, as = 0, at = 0, mu2 = 0;
+  const double inv_l = 1.0 / (double)l_global;
+  for (int64_t j = threadIdx.x; j < m; j += 256) {
+    double cs = 0.0;  // sum_i spike_ij = sum_r (1^T P)_r V_jr
+    for (int r = 0; r < k; ++r) cs = fma(energy[4 + r], V[j * k + r], cs);
+    const double cxc = stats[j] - (double)l_global * mu[j];  // sum_i xc_ij
+    const double ct = cxc - cs;                              // sum_i tail_ij
+    ms = fma(mu[j], cs, ms);
+    mt = fma(mu[j], ct, mt);
+    as = fmax(as, fabs(cs * inv_l));
+    at = fmax(at, fabs(ct * inv_l));
+    mu2 = fma(mu[j], mu[j], mu2);
+  }
+  s_ms[threadIdx.x] = ms; s_mt[threadIdx.x] = mt; s_as[threadIdx.x] = as; s_at[threadIdx.x] = at; s_mu2[threadIdx.x] = mu2;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0, b = 0, c = 0, d = 0, e = 0;
+    for (int t = 0; t < 256; ++t) { a += s_ms[t]; b += s_mt[t]; c = fmax(c, s_as[t]); d = fmax(d, s_at[t]); e += s_mu2[t]; }
+    rep[0] = a; rep[1] = b; rep[2] = c; rep[3] = d; rep[4] = (double)l_global * e;
+  }
+}
+
+// assemble the user's device outputs
+__global__ void copy_outputs_kernel(const double* __restrict__ mu, const double* __restrict__ V,
+                                    const double* __restrict__ sigma, int64_t m, int k, double* __restrict__ mu_o,
+                                    double* __restrict__ V_o, double* __restrict__ sigma_o) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (mu_o && t < m) mu_o[t] = mu[t];
+  if (V_o && t < m * k) V_o[t] = V[t];
+  if (sigma_o && t < k) sigma_o[t] = sigma[t];
+}
+
+}  // namespace
+}  // namespace avd
+
+using namespace avd;
+
+struct avd_ctx : public Ctx {
+  void* ws = nullptr;
+  // device outputs for the host path
+  double *o_mu = nullptr, *o_V = nullptr, *o_sigma = nullptr, *o_rho = nullptr;
+  int64_t* o_idx = nullptr;
+  double* report = nullptr;
+};
+
+extern "C" {
+
+const char* avd_strerror(avd_status s) {
+  switch (s) {
+    case AVD_OK: return "ok";
+    case AVD_EINVAL: return "invalid argument";
+    case AVD_ENONFINITE: return "input contains NaN or Inf";
+    case AVD_ENOCONV: return "eigensolver did not converge";
+    case AVD_ECUDA: return "CUDA error";
+    case AVD_ENOMEM: return "out of device memory";
+    case AVD_ESTATE: return "stage called out of order";
+  }
+  return "unknown status";
+}
+
+const char* avd_last_error(void) { return avd::g_err.c_str(); }
+
+avd_status avd_plan(const avd_config* cfg, avd_plan_t* plan) { return make_plan(cfg, plan, nullptr, nullptr); }
+
+avd_status avd_create(const avd_config* cfg, avd_ctx** out) {
+  if (!out) { set_error("null ctx pointer"); return AVD_EINVAL; }
+  *out = nullptr;
+  avd_ctx* c = new (std::nothrow) avd_ctx();
+  if (!c) return AVD_ENOMEM;
+  AVD_CUDA(cudaSetDevice(cfg ? cfg->device : 0));
+  int dev = 0, sms = 148, major = 0, minor = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (major != 10 || minor != 0) {
+    set_error("libavd is built for sm_100a (B200); device is sm_" + std::to_string(major) + std::to_string(minor));
+    delete c;
+    return AVD_ECUDA;
+  }
+  c->num_sms = sms;
+  Layout L;
+  avd_status st = make_plan(cfg, &c->plan, c, &L);
+  if (st != AVD_OK) { delete c; return st; }
+  c->stream = (cudaStream_t)cfg->stream;
+  if (cudaMalloc(&c->ws, L.total) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("cudaMalloc of " + std::to_string(L.total) + " workspace bytes failed");
+    delete c;
+    return AVD_ENOMEM;
+  }
+  c->ws_bytes = L.total;
+  char* b = (char*)c->ws;
+  int i = 0;
+#define BIND(field, T) c->field = reinterpret_cast<T>(b + L.off[i++])
+  BIND(colsum_part, double*); BIND(colmax_part, float*); BIND(colmin_part, float*); BIND(sq_part, double*);
+  BIND(stats, double*); BIND(colmax, float*); BIND(colmin, float*); BIND(hist1, unsigned long long*);
+  BIND(mu, double*); BIND(shift, int32_t*); BIND(dplan, DevPlan*); BIND(digits, int8_t*);
+  BIND(cand_key, uint32_t*); BIND(cand_idx, uint64_t*); BIND(cand_cnt, unsigned long long*);
+  BIND(gram_i, long long*); BIND(G, double*); BIND(Q, double*); BIND(Y, double*); BIND(Z, double*); BIND(U, double*);
+  BIND(H, double*); BIND(W, double*); BIND(theta, double*); BIND(red_part, double*); BIND(resid, double*);
+  BIND(trace, double*); BIND(V, double*); BIND(sigma, double*); BIND(V32, float*); BIND(P, float*);
+  BIND(en_part, double*); BIND(colsumP_part, double*); BIND(energy, double*); BIND(hist2, unsigned long long*);
+  BIND(hist3, unsigned long long*); BIND(ties, long long*); BIND(bm_sel, uint32_t*); BIND(bm_tie, uint32_t*);
+  BIND(blk_cnt, int64_t*); BIND(agg, double*); BIND(agg_part, double*); BIND(report, double*);
+#undef BIND
+  if (cudaMallocHost(&c->eig_host, sizeof(double) * 4 * kMaxP) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(c->ws);
+    delete c;
+    set_error("cudaMallocHost failed");
+    return AVD_ENOMEM;
+  }
+  st = gram_make_tmap(c);
+  if (st != AVD_OK) { cudaFree(c->ws); cudaFreeHost(c->eig_host); delete c; return st; }
+  c->stage = 0;
+  *out = c;
+  return AVD_OK;
+}
+
+void avd_destroy(avd_ctx* c) {
+  if (!c) return;
+  cudaFree(c->ws);
+  cudaFreeHost(c->eig_host);
+  cudaFree(c->X_stage);
+  cudaFree(c->o_mu); cudaFree(c->o_V); cudaFree(c->o_sigma); cudaFree(c->o_rho); cudaFree(c->o_idx);
+  delete c;
+}
+
+avd_status avd_get_plan(const avd_ctx* c, avd_plan_t* plan) {
+  if (!c || !plan) return AVD_EINVAL;
+  *plan = c->plan;
+  return AVD_OK;
+}
+
+int64_t avd_launch_count(const avd_ctx* c) { return c ? c->launches : 0; }
+
+avd_status avd_buffer(avd_ctx* c, int32_t which, void** ptr, size_t* bytes) {
+  if (!c || !ptr || !bytes) return AVD_EINVAL;
+  const int64_t m = c->cfg.m;
+  switch (which) {
+    case AVD_BUF_STATS: *ptr = c->stats; *bytes = sizeof(double) * (m + 2); break;
+    case AVD_BUF_COLMAX: *ptr = c->colmax; *bytes = sizeof(float) * m; break;
+    case AVD_BUF_COLMIN: *ptr = c->colmin; *bytes = sizeof(float) * m; break;
+    case AVD_BUF_HIST1: *ptr = c->hist1; *bytes = sizeof(long long) * kHistBins; break;
+    case AVD_BUF_GRAM: *ptr = c->gram_i; *bytes = sizeof(long long) * c->m_pad * c->m_pad; break;
+    case AVD_BUF_ENERGY: *ptr = c->energy; *bytes = sizeof(double) * (4 + c->k_pad); break;
+    case AVD_BUF_HIST2: *ptr = c->hist2; *bytes = sizeof(long long) * kHistBins; break;
+    case AVD_BUF_HIST3: *ptr = c->hist3; *bytes = sizeof(long long) * kHist3Bins; break;
+    case AVD_BUF_TIES: *ptr = c->ties; *bytes = sizeof(long long) * 2 * c->cfg.world; break;
+    case AVD_BUF_AGG: *ptr = c->agg; *bytes = sizeof(double) * 8; break;
+    case AVD_BUF_MU: *ptr = c->mu; *bytes = sizeof(double) * m; break;
+    case AVD_BUF_G: *ptr = c->G; *bytes = sizeof(double) * m * m; break;
+    case AVD_BUF_P: *ptr = c->P; *bytes = sizeof(float) * c->cfg.l_local * c->k_pad; break;
+    case AVD_BUF_DIGITS: *ptr = c->digits; *bytes = (size_t)c->nd * c->m_pad * c->l_pad; break;
+    case AVD_BUF_SCALE: *ptr = c->shift; *bytes = sizeof(int32_t) * c->m_pad; break;
+    default: set_error("unknown buffer id"); return AVD_EINVAL;
+  }
+  return AVD_OK;
+}
+
+#define STAGE_CHECK(c, want)                                                              \
+  do {                                                                                    \
+    if (!(c)) { set_error("null ctx"); return AVD_EINVAL; }                               \
+    if ((c)->stage != (want)) {                                                           \
+      set_error("stage order: expected stage " + std::to_string(want) + ", ctx is at " +  \
+                std::to_string((c)->stage));                                              \
+      return AVD_ESTATE;                                                                  \
+    }                                                                                     \
+  } while (0)
+
+avd_status avd_stage_stats(avd_ctx* c, const float* X) {
+  if (!c || !X) { set_error("null argument"); return AVD_EINVAL; }
+  c->stage = 0;  // a new pass may start at any time
+  AVD_TRY(launch_stats(c, X));
+  c->stage = 1;
+  return AVD_OK;
+}
+
+avd_status avd_stage_split(avd_ctx* c, const float* X) {
+  STAGE_CHECK(c, 1);
+  AVD_TRY(launch_prepare(c));
+  AVD_CUDA(cudaMemcpyAsync(&c->hplan, c->dplan, sizeof(DevPlan), cudaMemcpyDeviceToHost, c->stream));
+  AVD_CUDA(cudaStreamSynchronize(c->stream));
+  if (c->hplan.nonfinite > 0) {
+    set_error(std::to_string(c->hplan.nonfinite) + " non-finite entries in X");
+    c->stage = 0;
+    return AVD_ENONFINITE;
+  }
+  AVD_TRY(launch_split(c, X));
+  c->stage = 2;
+  return AVD_OK;
+}
+
+avd_status avd_stage_gram(avd_ctx* c) {
+  STAGE_CHECK(c, 2);
+  AVD_TRY(launch_gram(c));
+  c->stage = 3;
+  return AVD_OK;
+}
+
+avd_status avd_stage_eig(avd_ctx* c) {
+  STAGE_CHECK(c, 3);
+  AVD_TRY(launch_gram_finalize(c));
+  avd_status st = run_eig(c);
+  if (st != AVD_OK && st != AVD_ENOCONV) return st;
+  c->stage = 4;
+  return st;
+}
+
+avd_status avd_stage_project(avd_ctx* c, const float* X) {
+  STAGE_CHECK(c, 4);
+  AVD_TRY(launch_project(c, X));
+  c->stage = 5;
+  return AVD_OK;
+}
+
+avd_status avd_stage_select(avd_ctx* c, const float* X, int32_t level, int32_t rank) {
+  STAGE_CHECK(c, 5 + level);
+  if (level < 0 || level > 2 || rank < 0 || rank >= c->cfg.world) { set_error("bad level/rank"); return AVD_EINVAL; }
+  if (level == 0) {
+    unsigned long long cnt = 0;
+    AVD_CUDA(cudaMemcpyAsync(&cnt, c->cand_cnt, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
+    AVD_CUDA(cudaStreamSynchronize(c->stream));
+    c->hplan.cand_count = (int64_t)cnt;
+    c->cand_overflow = (int64_t)cnt > c->cand_cap;
+  }
+  AVD_TRY(launch_select(c, X, level, rank));
+  c->stage = 6 + level;
+  return AVD_OK;
+}
+
+avd_status avd_stage_gather(avd_ctx* c, const float* X, int32_t rank, avd_outputs* out) {
+  STAGE_CHECK(c, 8);
+  if (!out || !out->top_idx_dev || !out->rho_dev) { set_error("null output arrays"); return AVD_EINVAL; }
+  AVD_TRY(launch_gather(c, X, rank, out->top_idx_dev, out->rho_dev));
+  c->stage = 9;
+  return AVD_OK;
+}
+
+avd_status avd_stage_report(avd_ctx* c, avd_outputs* out) {
+  STAGE_CHECK(c, 9);
+  if (!out) { set_error("null outputs"); return AVD_EINVAL; }
+  const int64_t m = c->cfg.m;
+  const int k = c->k;
+  report_kernel<<<1, 256, 0, c->stream>>>(c->energy, c->stats, c->mu, c->V, m, k, c->cfg.l_global, c->report);
+  AVD_LAUNCHED(c);
+  if (out->mu_dev || out->V_dev || out->sigma_dev) {
+    copy_outputs_kernel<<<(unsigned)ceil_div(std::max<int64_t>(m * k, m), 256), 256, 0, c->stream>>>(
+        c->mu, c->V, c->sigma, m, k, out->mu_dev, out->V_dev, out->sigma_dev);
+    AVD_LAUNCHED(c);
+  }
+  double h[64];
+  const int kp = c->k_pad;
+  AVD_CUDA(cudaMemcpyAsync(h, c->report, sizeof(double) * 5, cudaMemcpyDeviceToHost, c->stream));
+  AVD_CUDA(cudaMemcpyAsync(h + 8, c->agg, sizeof(double) * 8, cudaMemcpyDeviceToHost, c->stream));
+  AVD_CUDA(cudaMemcpyAsync(h + 16, c->energy, sizeof(double) * 4, cudaMemcpyDeviceToHost, c->stream));
+  AVD_CUDA(cudaMemcpyAsync(h + 20, c->stats + m, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  AVD_CUDA(cudaMemcpyAsync(h + 21, c->trace, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  std::vector<double> sig(k);
+  AVD_CUDA(cudaMemcpyAsync(sig.data(), c->sigma, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
+  AVD_CUDA(cudaMemcpyAsync(&c->hplan, c->dplan, sizeof(DevPlan), cudaMemcpyDeviceToHost, c->stream));
+  AVD_CUDA(cudaStreamSynchronize(c->stream));
+  (void)kp;
+  double spike = 0.0;
+  for (int r = 0; r < k; ++r) spike += sig[r] * sig[r];
+  const double total = h[20], trace = h[21];
+  out->energy_cf[0] = total;
+  out->energy_cf[1] = h[4];
+  out->energy_cf[2] = spike;
+  out->energy_cf[3] = trace - spike;
+  out->energy_el[0] = total;
+  out->energy_el[1] = h[4];
+  out->energy_el[2] = h[16];
+  out->energy_el[3] = h[17];
+  out->cross_el[0] = h[0];
+  out->cross_el[1] = h[1];
+  out->cross_el[2] = h[18];
+  out->colmean_absmax[0] = h[2];
+  out->colmean_absmax[1] = h[3];
+  const double nt = (double)c->hplan.n_eff;
+  for (int q = 0; q < 4; ++q) out->rho_mean_aggr[q] = nt > 0 ? h[8 + q] / nt : 0.0;
+  for (int q = 0; q < 3; ++q) out->rho_energy_aggr[q] = h[15] > 0 ? h[12 + q] / h[15] : 0.0;
+  out->sigma_next = c->sigma_next;
+  out->trace_g = trace;
+  out->iters = c->iters;
+  out->max_resid = c->max_resid;
+  out->n_top_local = c->hplan.sel_local;
+  out->top_offset = c->hplan.top_offset;
+  out->n_top_global = c->hplan.n_eff;
+  c->stage = 10;
+  return AVD_OK;
+}
+
+avd_status avd_decompose(avd_ctx* c, const float* X, avd_outputs* out) {
+  if (!c || !X || !out) { set_error("null argument"); return AVD_EINVAL; }
+  if (c->cfg.world != 1) { set_error("avd_decompose needs world == 1 (use the stage API)"); return AVD_EINVAL; }
+  if ((reinterpret_cast<uintptr_t>(X) & 15) != 0) { set_error("X must be 16-byte aligned"); return AVD_EINVAL; }
+  AVD_TRY(avd_stage_stats(c, X));
+  AVD_TRY(avd_stage_split(c, X));
+  AVD_TRY(avd_stage_gram(c));
+  const avd_status eig = avd_stage_eig(c);
+  if (eig != AVD_OK && eig != AVD_ENOCONV) return eig;
+  AVD_TRY(avd_stage_project(c, X));
+  for (int lv = 0; lv < 3; ++lv) AVD_TRY(avd_stage_select(c, X, lv, 0));
+  AVD_TRY(avd_stage_gather(c, X, 0, out));
+  AVD_TRY(avd_stage_report(c, out));
+  return eig;
+}
+
+avd_status avd_decompose_host(avd_ctx* c, const float* X_host, avd_outputs* out) {
+  if (!c || !X_host || !out) { set_error("null argument"); return AVD_EINVAL; }
+  const int64_t l = c->cfg.l_local, m = c->cfg.m, k = c->k, n = c->plan.n_top;
+  if (!c->X_stage) {
+    AVD_CUDA(cudaMalloc(&c->X_stage, sizeof(float) * l * m));
+    AVD_CUDA(cudaMalloc(&c->o_mu, sizeof(double) * m));
+    AVD_CUDA(cudaMalloc(&c->o_V, sizeof(double) * m * k));
+    AVD_CUDA(cudaMalloc(&c->o_sigma, sizeof(double) * k));
+    AVD_CUDA(cudaMalloc(&c->o_idx, sizeof(int64_t) * n));
+    AVD_CUDA(cudaMalloc(&c->o_rho, sizeof(double) * 4 * n));
+  }
+  AVD_CUDA(cudaMemcpyAsync(c->X_stage, X_host, sizeof(float) * l * m, cudaMemcpyHostToDevice, c->stream));
+  avd_outputs d = *out;
+  d.mu_dev = c->o_mu; d.V_dev = c->o_V; d.sigma_dev = c->o_sigma; d.top_idx_dev = c->o_idx; d.rho_dev = c->o_rho;
+  const avd_status st = avd_decompose(c, c->X_stage, &d);
+  if (st != AVD_OK && st != AVD_ENOCONV) return st;
+  if (out->mu_dev) AVD_CUDA(cudaMemcpyAsync(out->mu_dev, c->o_mu, sizeof(double) * m, cudaMemcpyDeviceToHost, c->stream));
+  if (out->V_dev) AVD_CUDA(cudaMemcpyAsync(out->V_dev, c->o_V, sizeof(double) * m * k, cudaMemcpyDeviceToHost, c->stream));
+  if (out->sigma_dev) AVD_CUDA(cudaMemcpyAsync(out->sigma_dev, c->o_sigma, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
+  if (out->top_idx_dev) AVD_CUDA(cudaMemcpyAsync(out->top_idx_dev, c->o_idx, sizeof(int64_t) * d.n_top_local, cudaMemcpyDeviceToHost, c->stream));
+  if (out->rho_dev) AVD_CUDA(cudaMemcpyAsync(out->rho_dev, c->o_rho, sizeof(double) * 4 * d.n_top_local, cudaMemcpyDeviceToHost, c->stream));
+  AVD_CUDA(cudaStreamSynchronize(c->stream));
+  double* keep[5] = {out->mu_dev, out->V_dev, out->sigma_dev, out->rho_dev, nullptr};
+  int64_t* keep_idx = out->top_idx_dev;
+  *out = d;
+  out->mu_dev = keep[0]; out->V_dev = keep[1]; out->sigma_dev = keep[2]; out->rho_dev = keep[3];
+  out->top_idx_dev = keep_idx;
+  return st;
+}
+
+}  // extern "C"

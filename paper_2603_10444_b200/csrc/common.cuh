@@ -1,0 +1,160 @@
+// common.cuh — shared context, error handling and launch helpers of libavd (product code).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "../../include/avd.h"
+
+namespace avd {
+
+constexpr int kHistBins = 4096;   // first/second level: 12 key bits
+constexpr int kHist3Bins = 128;   // third level: 7 key bits
+constexpr int kGramTile = 128;    // Gram tile edge (rows of A / B panels)
+constexpr int kGramK = 128;       // K rows per pipeline stage (one 128-byte swizzle row of int8)
+constexpr int kMaxP = 112;        // subspace block size cap (two p x p fp64 matrices in smem)
+
+// Device-side "plan2": values decided on the device after the stats exchange.
+struct DevPlan {
+  int64_t n_eff;        // min(n_top, #nonzero entries)
+  int64_t cnt_gt;       // #entries with key strictly above the current bin prefix
+  int64_t cand_count;   // candidates appended by K2
+  int64_t nonfinite;    // #non-finite entries seen by K1
+  int32_t b1, b2;       // selected first/second level bins
+  uint32_t T;           // exact 31-bit key threshold (n_top-th largest |x| bits)
+  int32_t empty;        // 1 when n_eff == 0
+  int64_t cnt_gt_T;     // #entries with key > T (global)
+  int64_t q;            // ties (key == T) to take, globally
+  int64_t ties_local;   // ties held by this rank
+  int64_t quota;        // ties this rank takes
+  int64_t sel_local;    // entries of E_top held by this rank
+  int64_t top_offset;   // global position of this rank's first entry
+};
+
+struct Ctx {
+  avd_config cfg;
+  avd_plan_t plan;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  int64_t m_pad = 0;     // m rounded up to kGramTile
+  int64_t l_pad = 0;     // l_local rounded up to kGramK
+  int k = 0, p = 0, k_pad = 0;
+  int nd = 3;
+  int64_t launches = 0;
+  int stage = 0;         // last completed stage (ordering check)
+  // K1
+  int r1 = 1;                 // row chunks of the stats kernel
+  double* colsum_part = nullptr;  // [r1][m]
+  float* colmax_part = nullptr;   // [r1][m]
+  float* colmin_part = nullptr;   // [r1][m]
+  double* sq_part = nullptr;      // [r1 * ncb]
+  double* stats = nullptr;        // [m + 2]: colsum[m], sum x^2, nonfinite count  (exchange)
+  float* colmax = nullptr;        // [m] (exchange MAX)
+  float* colmin = nullptr;        // [m] (exchange MIN)
+  unsigned long long* hist1 = nullptr;  // [4096] (exchange SUM)
+  // prepare
+  double* mu = nullptr;           // [m]
+  int32_t* shift = nullptr;       // [m_pad] digit scale exponent per column
+  DevPlan* dplan = nullptr;
+  DevPlan hplan{};
+  // K2
+  int8_t* digits = nullptr;       // [nd][m_pad][l_pad]
+  uint32_t* cand_key = nullptr;   // [cand_cap]
+  uint64_t* cand_idx = nullptr;   // [cand_cap]
+  unsigned long long* cand_cnt = nullptr;
+  int64_t cand_cap = 0;
+  bool cand_overflow = false;
+  // K3
+  long long* gram_i = nullptr;    // [m_pad * m_pad] int64 (upper tiles) (exchange SUM)
+  double* G = nullptr;            // [m * m] fp64 symmetric
+  CUtensorMap tmap_digits{};
+  int gram_split = 1;
+  // K4
+  double *Q = nullptr, *Y = nullptr, *Z = nullptr, *U = nullptr;  // [m][p]
+  double *H = nullptr, *W = nullptr, *theta = nullptr;          // [p][p], [p][p], [p]
+  double* red_part = nullptr;     // [n_red_chunks][p*p]
+  int n_red = 1;
+  double* resid = nullptr;        // [p]
+  double* trace = nullptr;        // [1]
+  double* eig_host = nullptr;     // pinned: theta[p] + resid[p]
+  double* V = nullptr;            // [m][k] output copy (row-major)
+  double* sigma = nullptr;        // [k]
+  float* V32 = nullptr;           // [m][k_pad] fp32 copy for K5/K8
+  int iters = 0;
+  double max_resid = 0;
+  double sigma_next = 0;
+  // K5/K8
+  float* P = nullptr;             // [l_local][k_pad]
+  double* en_part = nullptr;      // [n_proj_ctas][4]
+  double* colsumP_part = nullptr; // [n_proj_ctas][k_pad]
+  int n_proj_ctas = 1;
+  double* energy = nullptr;       // [4 + k_pad + m] exchange SUM: x^2, S^2, T^2, ST, colsumP[k_pad], colsumXc[m]
+  // K6
+  unsigned long long* hist2 = nullptr;  // [4096] (exchange)
+  unsigned long long* hist3 = nullptr;  // [128] (exchange)
+  long long* ties = nullptr;            // [world] (exchange)
+  uint32_t* bm_sel = nullptr;           // bitmap [nwords]
+  uint32_t* bm_tie = nullptr;
+  int64_t nwords = 0;
+  int64_t* blk_cnt = nullptr;           // [2 * nblk + 2] scan scratch
+  int64_t nblk = 0;
+  // K7
+  double* agg = nullptr;                // [8] exchange: sum rho(4), sum_E M^2, S^2, T^2, X^2
+  double* agg_part = nullptr;
+  int n_gather_ctas = 1;
+  // host path
+  float* X_stage = nullptr;             // device copy for avd_decompose_host
+  size_t ws_bytes = 0;
+};
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+
+#define AVD_CUDA(call)                                                                \
+  do {                                                                                \
+    cudaError_t e__ = (call);                                                         \
+    if (e__ != cudaSuccess) {                                                         \
+      ::avd::set_error(std::string(#call) + " failed: " + cudaGetErrorString(e__) +   \
+                       " (" + __FILE__ + ":" + std::to_string(__LINE__) + ")");       \
+      return AVD_ECUDA;                                                               \
+    }                                                                                 \
+  } while (0)
+
+#define AVD_LAUNCHED(ctx)                                                             \
+  do {                                                                                \
+    (ctx)->launches++;                                                                \
+    cudaError_t e__ = cudaGetLastError();                                             \
+    if (e__ != cudaSuccess) {                                                         \
+      ::avd::set_error(std::string("kernel launch failed: ") + cudaGetErrorString(e__) + \
+                       " (" + __FILE__ + ":" + std::to_string(__LINE__) + ")");       \
+      return AVD_ECUDA;                                                               \
+    }                                                                                 \
+  } while (0)
+
+#define AVD_TRY(expr)                        \
+  do {                                       \
+    avd_status s__ = (expr);                 \
+    if (s__ != AVD_OK) return s__;           \
+  } while (0)
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+// ---------------------------------------------------------------- kernels (per file)
+avd_status launch_stats(Ctx* c, const float* X);           // k_stats.cu
+avd_status launch_stats_reduce(Ctx* c);                    // k_stats.cu
+avd_status launch_prepare(Ctx* c);                         // k_stats.cu
+avd_status launch_split(Ctx* c, const float* X);           // k_split.cu
+avd_status launch_gram(Ctx* c);                            // k_gram.cu
+avd_status gram_make_tmap(Ctx* c);                         // k_gram.cu
+avd_status launch_gram_finalize(Ctx* c);                   // k_eig.cu
+avd_status run_eig(Ctx* c);                                // k_eig.cu
+avd_status launch_project(Ctx* c, const float* X);         // k_project.cu
+avd_status launch_select(Ctx* c, const float* X, int level, int rank);  // k_select.cu
+avd_status launch_gather(Ctx* c, const float* X, int rank, int64_t* top_idx, double* rho);
+avd_status launch_project_reduce(Ctx* c);                  // k_project.cu
+avd_status launch_agg_reduce(Ctx* c);                      // k_select.cu
+
+}  // namespace avd

@@ -1,0 +1,265 @@
+// k_gram.cu — K3: the centred Gram G = Xc^T Xc (right singular vectors of Xc are its
+// eigenvectors, sigma^2 its eigenvalues: the truncated SVD of PAPER.md:11-14) as a dense
+// contraction on the 5th-generation tensor cores.
+//
+// Operands: the nd int8 digit planes D_d[j][i] written by K2 (K-major, row j = column j of Xc),
+// q_ij = sum_d 128^(nd-1-d) D_d[j][i].  The Gram of the fixed-point matrix is accumulated
+// EXACTLY:  sum_i q_ia q_ib = sum_{d,e} 128^(2nd-2-d-e) sum_i D_d[a][i] D_e[b][i]
+//   nd = 2: all four digit products, classes 2^14 / 2^7 / 2^0           (exact)
+//   nd = 3: classes 2^28 / 2^21 / 2^14 (6 products; classes <= 2^7 dropped, rel. <= 2^-21)
+// Each class is one int32 TMEM accumulator (tcgen05.mma kind::i8, M=128, N=128, K=32), so no
+// floating-point rounding happens inside the contraction (the fp32 TMEM accumulation of the
+// tf32 path truncates; see profiles/r01_umma_probe.txt).  Per (tile, K-range) work unit the
+// epilogue combines the classes into int64 and atomically adds them into G_int (integer adds
+// commute: the result is bit-identical for any unit order, split or rank count).
+//
+// Warp roles (192 threads, 1 CTA/SM, persistent over work units):
+//   warp 0: TMA producer (cp.async.bulk.tensor 2D, SWIZZLE_128B, mbarrier ring)
+//   warp 1: TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2-5: epilogue (tcgen05.ld 32x32b -> int64 -> global atomics)
+#include <cudaTypedefs.h>
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace avd {
+
+namespace {
+using namespace sm100;
+
+constexpr int kGramThreads = 192;
+constexpr uint32_t kBox = 128 * 128;  // bytes of one TMA box (128 rows x 128 int8)
+
+// kind::i8 instruction descriptor: c_format S32 (2), a/b format signed int8 (1), K-major.
+__host__ __device__ constexpr uint32_t idesc_i8(uint32_t M, uint32_t N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void unit_coords(int64_t u, int n_tiles, int T, int S, int64_t NK, int& ta,
+                                            int& tb, int64_t& ks0, int64_t& ks1) {
+  const int s = (int)(u / n_tiles);
+  int t = (int)(u - (int64_t)s * n_tiles);
+  int a = 0;
+  while (t >= T - a) { t -= T - a; ++a; }
+  ta = a;
+  tb = a + t;
+  ks0 = NK * s / S;
+  ks1 = NK * (s + 1) / S;
+}
+
+template <int ND, int NS>
+__global__ void __launch_bounds__(kGramThreads, 1) gram_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                               int64_t m_pad, int64_t NK, int T, int S,
+                                                               long long* __restrict__ G) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr uint32_t kStageBytes = 2 * ND * kBox;
+  __shared__ uint64_t full_bar[NS], empty_bar[NS], tfull_bar, tempty_bar;
+  __shared__ uint32_t tmem_base_sh;
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int n_tiles = T * (T + 1) / 2;
+  const int64_t n_units = (int64_t)n_tiles * S;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
+    mbar_init(&tfull_bar, 1);
+    mbar_init(&tempty_bar, 4);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) tma_prefetch(&tmap);
+  if (warp == 1) tmem_alloc<512>(&tmem_base_sh);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp == 0) {
+    // ================= TMA producer
+    if (elect_one()) {
+      uint32_t it = 0;
+      for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+        int ta, tb;
+        int64_t ks0, ks1;
+        unit_coords(u, n_tiles, T, S, NK, ta, tb, ks0, ks1);
+        const bool diag = ta == tb;
+        for (int64_t ks = ks0; ks < ks1; ++ks, ++it) {
+          const uint32_t s = it % NS, r = it / NS;
+          mbar_wait(&empty_bar[s], (r & 1) ^ 1);
+          uint8_t* st = smem + s * kStageBytes;
+          mbar_arrive_expect_tx(&full_bar[s], diag ? ND * kBox : 2 * ND * kBox);
+#pragma unroll
+          for (int d = 0; d < ND; ++d)
+            tma_load_2d(st + d * kBox, &tmap, &full_bar[s], (int32_t)(ks * 128), (int32_t)(d * m_pad + ta * 128));
+          if (!diag) {
+#pragma unroll
+            for (int d = 0; d < ND; ++d)
+              tma_load_2d(st + (ND + d) * kBox, &tmap, &full_bar[s], (int32_t)(ks * 128),
+                          (int32_t)(d * m_pad + tb * 128));
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer
+    constexpr uint32_t idesc = idesc_i8(128, 128);
+    uint32_t it = 0, ui = 0;
+    for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++ui) {
+      int ta, tb;
+      int64_t ks0, ks1;
+      unit_coords(u, n_tiles, T, S, NK, ta, tb, ks0, ks1);
+      const bool diag = ta == tb;
+      mbar_wait(&tempty_bar, (ui & 1) ^ 1);
+      tc_fence_after();
+      for (int64_t ks = ks0; ks < ks1; ++ks, ++it) {
+        const uint32_t s = it % NS, r = it / NS;
+        mbar_wait(&full_bar[s], r & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t abase = smem_u32(smem + s * kStageBytes);
+          const uint32_t bbase = diag ? abase : abase + ND * kBox;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            uint64_t a[ND], b[ND];
+#pragma unroll
+            for (int d = 0; d < ND; ++d) {
+              a[d] = smem_desc(abase + d * kBox + kk * 32, 16, 1024, 2);
+              b[d] = smem_desc(bbase + d * kBox + kk * 32, 16, 1024, 2);
+            }
+            const uint32_t acc = (ks > ks0 || kk > 0) ? 1u : 0u;
+            if (ND == 2) {
+              mma_i8(tmem + 0, a[0], b[0], idesc, acc);
+              mma_i8(tmem + 128, a[0], b[1], idesc, acc);
+              mma_i8(tmem + 128, a[1], b[0], idesc, 1u);
+              mma_i8(tmem + 256, a[1], b[1], idesc, acc);
+            } else {
+              mma_i8(tmem + 0, a[0], b[0], idesc, acc);
+              mma_i8(tmem + 128, a[0], b[1], idesc, acc);
+              mma_i8(tmem + 128, a[1], b[0], idesc, 1u);
+              mma_i8(tmem + 256, a[0], b[ND - 1], idesc, acc);
+              mma_i8(tmem + 256, a[1], b[1], idesc, 1u);
+              mma_i8(tmem + 256, a[ND - 1], b[0], idesc, 1u);
+            }
+          }
+          mma_commit(&empty_bar[s]);
+        }
+        __syncwarp();
+      }
+      if (elect_one()) mma_commit(&tfull_bar);
+      __syncwarp();
+    }
+  } else {
+    // ================= epilogue: warps 2..5 -> TMEM lane quadrant (warp % 4)
+    const uint32_t q = warp & 3;
+    uint32_t ui = 0;
+    for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++ui) {
+      int ta, tb;
+      int64_t ks0, ks1;
+      unit_coords(u, n_tiles, T, S, NK, ta, tb, ks0, ks1);
+      mbar_wait(&tfull_bar, ui & 1);
+      tc_fence_after();
+      const int64_t row = (int64_t)ta * 128 + q * 32 + lane;
+      unsigned long long* grow = reinterpret_cast<unsigned long long*>(G + row * m_pad + (int64_t)tb * 128);
+      const uint32_t tbase = tmem + ((q * 32) << 16);
+#pragma unroll 1
+      for (int c0 = 0; c0 < 128; c0 += 16) {
+        uint32_t r0[16], r1[16], r2[16];
+        tmem_ld16(tbase + c0, r0);
+        tmem_ld16(tbase + 128 + c0, r1);
+        tmem_ld16(tbase + 256 + c0, r2);
+        tmem_ld_wait();
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          const long long v = ((long long)(int32_t)r0[t] << 14) + ((long long)(int32_t)r1[t] << 7) +
+                              (long long)(int32_t)r2[t];
+          if (v != 0) atomicAdd(grow + c0 + t, (unsigned long long)v);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+int choose_split(int n_tiles, int64_t NK, int sms) {
+  // balance waves over the SMs; every unit <= 1024 stages (131072 rows: int32-exact bound)
+  int best = 1;
+  double best_eff = -1.0;
+  const int smin = (int)ceil_div(NK, 1024);
+  for (int S = std::max(1, smin); S <= std::max(smin, 16) && S <= NK; ++S) {
+    const int64_t units = (int64_t)n_tiles * S;
+    const double waves = (double)ceil_div(units, sms);
+    const double eff = (double)units / (waves * sms) - 0.004 * S;  // small per-unit overhead
+    if (eff > best_eff + 1e-9) { best_eff = eff; best = S; }
+  }
+  return best;
+}
+
+}  // namespace
+
+avd_status gram_make_tmap(Ctx* c) {
+  auto enc = get_encode();
+  if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return AVD_ECUDA; }
+  uint64_t dims[2] = {(uint64_t)c->l_pad, (uint64_t)(c->nd * c->m_pad)};
+  uint64_t strides[1] = {(uint64_t)c->l_pad};
+  uint32_t box[2] = {128, 128};
+  uint32_t es[2] = {1, 1};
+  CUresult r = enc(&c->tmap_digits, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, c->digits, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r)); return AVD_ECUDA; }
+  const int T = (int)(c->m_pad / 128);
+  c->gram_split = choose_split(T * (T + 1) / 2, c->l_pad / 128, c->num_sms);
+  return AVD_OK;
+}
+
+avd_status launch_gram(Ctx* c) {
+  const int T = (int)(c->m_pad / 128);
+  const int n_tiles = T * (T + 1) / 2;
+  const int64_t NK = c->l_pad / 128;
+  const int S = c->gram_split;
+  const int64_t units = (int64_t)n_tiles * S;
+  const int grid = (int)std::min<int64_t>(units, c->num_sms);
+  AVD_CUDA(cudaMemsetAsync(c->gram_i, 0, sizeof(long long) * c->m_pad * c->m_pad, c->stream));
+  if (c->nd == 2) {
+    constexpr int NS = 3;
+    const size_t smem = (size_t)NS * 2 * 2 * kBox + 1024;
+    AVD_CUDA(cudaFuncSetAttribute(gram_kernel<2, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    gram_kernel<2, NS><<<grid, kGramThreads, smem, c->stream>>>(c->tmap_digits, c->m_pad, NK, T, S, c->gram_i);
+  } else {
+    constexpr int NS = 2;
+    const size_t smem = (size_t)NS * 2 * 3 * kBox + 1024;
+    AVD_CUDA(cudaFuncSetAttribute(gram_kernel<3, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    gram_kernel<3, NS><<<grid, kGramThreads, smem, c->stream>>>(c->tmap_digits, c->m_pad, NK, T, S, c->gram_i);
+  }
+  AVD_LAUNCHED(c);
+  return AVD_OK;
+}
+
+}  // namespace avd

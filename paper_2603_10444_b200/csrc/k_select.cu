@@ -1,0 +1,370 @@
+// k_select.cu — K6: exact top-0.1% set E_top by |X_ij|, ties broken by the
+// smaller global linear index i*m+j, zeros excluded (R3, R4); K7: rho gather
+// (PAPER.md:23-27).
+//
+// Keys are the 31-bit magnitude bit patterns of the fp32 entries (ordering of |x| == ordering of
+// the bits).  Radix levels: bits [30:19] (hist1, K1) -> [18:7] (hist2) -> [6:0] (hist3) give
+// the exact threshold key T, count_gt(T) and the tie quota q = n_eff - count_gt(T).  Entries
+// with key > T and the first q entries with key == T (in linear order) form E_top.  They are
+// marked in two bitmaps over this rank's linear index range and emitted in ascending order by
+// a two-level ordered compaction, so the output needs no sort and is deterministic.
+// Rank r takes the ties left after ranks < r (rows are sharded in rank order).
+// The histogram and mark passes read the K2 candidate list (entries with key>>19 >= b1), or,
+// if it overflowed its capacity, stream X directly.
+#include "common.cuh"
+
+namespace avd {
+
+namespace {
+
+constexpr int kSelThreads = 256;
+constexpr int kWordsPerBlk = 1024;  // bitmap words per compaction block
+
+template <bool FROM_X>
+__device__ __forceinline__ bool fetch(int64_t t, const uint32_t* __restrict__ ckey, const uint64_t* __restrict__ cidx,
+                                      const float* __restrict__ X, int64_t base, uint32_t& key, uint64_t& lidx) {
+  if (FROM_X) {
+    const float x = __ldg(X + t);
+    key = __float_as_uint(x) & 0x7FFFFFFFu;
+    lidx = (uint64_t)t;
+    return key != 0 && key < 0x7F800000u;
+  } else {
+    key = ckey[t];
+    lidx = cidx[t] - (uint64_t)base;
+    return true;
+  }
+}
+
+// level 0: hist2 of bits [18:7] over key>>19 == b1 ; level 1: hist3 of bits [6:0] over key>>7 == prefix
+template <bool FROM_X>
+__global__ void __launch_bounds__(kSelThreads) hist_kernel(int level, int64_t n, const uint32_t* __restrict__ ckey,
+                                                           const uint64_t* __restrict__ cidx, const float* __restrict__ X,
+                                                           const DevPlan* __restrict__ dp, unsigned long long* __restrict__ out) {
+  __shared__ unsigned int sh[kHistBins];
+  const int nb = level == 0 ? kHistBins : kHist3Bins;
+  for (int b = threadIdx.x; b < nb; b += kSelThreads) sh[b] = 0;
+  __syncthreads();
+  const uint32_t pre = level == 0 ? (uint32_t)dp->b1 : (((uint32_t)dp->b1 << 12) | (uint32_t)dp->b2);
+  const int shiftp = level == 0 ? 19 : 7;
+  for (int64_t t = (int64_t)blockIdx.x * kSelThreads + threadIdx.x; t < n; t += (int64_t)gridDim.x * kSelThreads) {
+    uint32_t key;
+    uint64_t li;
+    if (!fetch<FROM_X>(t, ckey, cidx, X, 0, key, li)) continue;
+    if ((key >> shiftp) != pre) continue;
+    const uint32_t bin = level == 0 ? ((key >> 7) & 0xFFFu) : (key & 0x7Fu);
+    atomicAdd(&sh[bin], 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb; b += kSelThreads)
+    if (sh[b]) atomicAdd(&out[b], (unsigned long long)sh[b]);
+}
+
+// Find the bin of the next level that contains the n_eff-th largest key (one warp).
+__global__ void find_bin_kernel(int level, const unsigned long long* __restrict__ h, DevPlan* __restrict__ dp) {
+  const int lane = threadIdx.x;
+  const int nb = level == 0 ? kHistBins : kHist3Bins;
+  const int per = nb / 32;
+  const long long need = dp->n_eff - dp->cnt_gt;  // rank inside the current prefix (>= 1)
+  const int hi = nb - 1 - lane * per;
+  unsigned long long mine = 0;
+  for (int b = hi; b > hi - per; --b) mine += h[b];
+  unsigned long long incl = mine;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const unsigned long long excl = incl - mine;
+  if (dp->empty) return;
+  if (excl < (unsigned long long)need && incl >= (unsigned long long)need) {
+    unsigned long long cum = excl;
+    int b = hi;
+    for (; b > hi - per; --b) {
+      if (cum + h[b] >= (unsigned long long)need) break;
+      cum += h[b];
+    }
+    if (level == 0) {
+      dp->b2 = b;
+      dp->cnt_gt = dp->cnt_gt + (long long)cum;
+    } else {
+      dp->T = ((uint32_t)dp->b1 << 19) | ((uint32_t)dp->b2 << 7) | (uint32_t)b;
+      dp->cnt_gt_T = dp->cnt_gt + (long long)cum;
+      dp->q = dp->n_eff - dp->cnt_gt_T;
+    }
+  }
+}
+
+// mark entries with key > T (sel) and key == T (tie); count both for this rank
+template <bool FROM_X>
+__global__ void __launch_bounds__(kSelThreads) mark_kernel(int64_t n, const uint32_t* __restrict__ ckey,
+                                                           const uint64_t* __restrict__ cidx, const float* __restrict__ X,
+                                                           int64_t base, const DevPlan* __restrict__ dp,
+                                                           uint32_t* __restrict__ bm_sel, uint32_t* __restrict__ bm_tie,
+                                                           unsigned long long* __restrict__ counts) {
+  __shared__ unsigned int c_sel, c_tie;
+  if (threadIdx.x == 0) { c_sel = 0; c_tie = 0; }
+  __syncthreads();
+  const uint32_t T = dp->T;
+  const bool empty = dp->empty != 0;
+  unsigned int ns = 0, nt = 0;
+  if (!empty) {
+    for (int64_t t = (int64_t)blockIdx.x * kSelThreads + threadIdx.x; t < n; t += (int64_t)gridDim.x * kSelThreads) {
+      uint32_t key;
+      uint64_t li;
+      if (!fetch<FROM_X>(t, ckey, cidx, X, base, key, li)) continue;
+      if (key > T) {
+        atomicOr(&bm_sel[li >> 5], 1u << (li & 31));
+        ++ns;
+      } else if (key == T) {
+        atomicOr(&bm_tie[li >> 5], 1u << (li & 31));
+        ++nt;
+      }
+    }
+  }
+  if (ns) atomicAdd(&c_sel, ns);
+  if (nt) atomicAdd(&c_tie, nt);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (c_sel) atomicAdd(&counts[0], (unsigned long long)c_sel);
+    if (c_tie) atomicAdd(&counts[1], (unsigned long long)c_tie);
+  }
+}
+
+// counts[0..1] (this rank) -> ties[rank] (sel) and ties[world + rank] (tie) for the exchange
+__global__ void publish_counts_kernel(const unsigned long long* __restrict__ counts, long long* __restrict__ ties,
+                                      int world, int rank) {
+  const int t = threadIdx.x;
+  if (t < 2 * world) ties[t] = 0;
+  __syncthreads();
+  if (t == 0) { ties[rank] = (long long)counts[0]; ties[world + rank] = (long long)counts[1]; }
+}
+
+__global__ void __launch_bounds__(kSelThreads) blk_count_kernel(const uint32_t* __restrict__ bs, const uint32_t* __restrict__ bt,
+                                                                int64_t nwords, int64_t nblk, int64_t* __restrict__ blk) {
+  __shared__ int s1[kSelThreads], s2[kSelThreads];
+  const int64_t w0 = (int64_t)blockIdx.x * kWordsPerBlk;
+  int a = 0, b = 0;
+  for (int64_t w = w0 + threadIdx.x; w < min(nwords, w0 + kWordsPerBlk); w += kSelThreads) {
+    a += __popc(bs[w]);
+    b += __popc(bt[w]);
+  }
+  s1[threadIdx.x] = a;
+  s2[threadIdx.x] = b;
+  __syncthreads();
+  for (int o = kSelThreads / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) { s1[threadIdx.x] += s1[threadIdx.x + o]; s2[threadIdx.x] += s2[threadIdx.x + o]; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { blk[blockIdx.x] = s1[0]; blk[nblk + blockIdx.x] = s2[0]; }
+}
+
+// exclusive scan of block counts (one CTA) + this rank's tie quota and offsets
+__global__ void blk_scan_kernel(int64_t* __restrict__ blk, int64_t nblk, const long long* __restrict__ ties, int world,
+                                int rank, DevPlan* __restrict__ dp) {
+  __shared__ int64_t carry[2];
+  if (threadIdx.x == 0) { carry[0] = 0; carry[1] = 0; }
+  __syncthreads();
+  for (int which = 0; which < 2; ++which) {
+    int64_t* a = blk + which * nblk;
+    for (int64_t base = 0; base < nblk; base += blockDim.x) {
+      const int64_t i = base + threadIdx.x;
+      int64_t v = i < nblk ? a[i] : 0;
+      // inclusive block scan (Hillis-Steele in smem)
+      __shared__ int64_t sh[1024];
+      sh[threadIdx.x] = v;
+      __syncthreads();
+      for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+        int64_t t = threadIdx.x >= (unsigned)o ? sh[threadIdx.x - o] : 0;
+        __syncthreads();
+        sh[threadIdx.x] += t;
+        __syncthreads();
+      }
+      const int64_t incl = sh[threadIdx.x];
+      if (i < nblk) a[i] = carry[which] + incl - v;
+      __syncthreads();
+      if (threadIdx.x == blockDim.x - 1) carry[which] += incl;
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) {
+    long long before_ties = 0, before_sel = 0;
+    for (int r = 0; r < rank; ++r) { before_ties += ties[world + r]; before_sel += ties[r]; }
+    const long long q = dp->empty ? 0 : dp->q;
+    long long quota = q - before_ties;
+    quota = quota < 0 ? 0 : quota;
+    quota = quota > ties[world + rank] ? ties[world + rank] : quota;
+    // global offset: all sel of ranks < r plus their quotas
+    long long off = before_sel;
+    long long rem = q;
+    for (int r = 0; r < rank; ++r) {
+      const long long qr = rem < ties[world + r] ? (rem < 0 ? 0 : rem) : ties[world + r];
+      off += qr;
+      rem -= ties[world + r];
+    }
+    dp->ties_local = ties[world + rank];
+    dp->quota = quota;
+    dp->sel_local = carry[0] + quota;
+    dp->top_offset = off;
+  }
+}
+
+__global__ void __launch_bounds__(kSelThreads) emit_kernel(const uint32_t* __restrict__ bs, const uint32_t* __restrict__ bt,
+                                                           int64_t nwords, int64_t nblk, const int64_t* __restrict__ blk,
+                                                           const DevPlan* __restrict__ dp, int64_t base_idx,
+                                                           int64_t* __restrict__ out) {
+  __shared__ int ps[kSelThreads + 1], pt[kSelThreads + 1];
+  const int64_t w0 = (int64_t)blockIdx.x * kWordsPerBlk;
+  const int64_t quota = dp->quota;
+  int64_t sel_before = blk[blockIdx.x], tie_before = blk[nblk + blockIdx.x];
+  constexpr int WPT = kWordsPerBlk / kSelThreads;  // 4 consecutive words per thread
+  uint32_t ws[WPT], wt[WPT];
+  int a = 0, b = 0;
+#pragma unroll
+  for (int q = 0; q < WPT; ++q) {
+    const int64_t w = w0 + threadIdx.x * WPT + q;
+    ws[q] = w < nwords ? bs[w] : 0u;
+    wt[q] = w < nwords ? bt[w] : 0u;
+    a += __popc(ws[q]);
+    b += __popc(wt[q]);
+  }
+  ps[threadIdx.x] = a;
+  pt[threadIdx.x] = b;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int sa = 0, sb = 0;
+    for (int t = 0; t < kSelThreads; ++t) {
+      const int x = ps[t], y = pt[t];
+      ps[t] = sa; pt[t] = sb;
+      sa += x; sb += y;
+    }
+  }
+  __syncthreads();
+  int64_t sb4 = sel_before + ps[threadIdx.x];
+  int64_t tb4 = tie_before + pt[threadIdx.x];
+#pragma unroll
+  for (int q = 0; q < WPT; ++q) {
+    const int64_t w = w0 + threadIdx.x * WPT + q;
+    uint32_t s = ws[q], t = wt[q];
+    while (s | t) {
+      const uint32_t ls = s & (0u - s), lt = t & (0u - t);
+      // next set bit in linear order among both masks
+      const bool take_sel = ls && (!lt || ls < lt);
+      const uint32_t bit = take_sel ? ls : lt;
+      const int pos_in_word = __ffs(bit) - 1;
+      if (take_sel) {
+        out[sb4 + min(tb4, quota)] = base_idx + w * 32 + pos_in_word;
+        ++sb4;
+        s &= s - 1;
+      } else {
+        if (tb4 < quota) out[sb4 + tb4] = base_idx + w * 32 + pos_in_word;
+        ++tb4;
+        t &= t - 1;
+      }
+    }
+  }
+}
+
+// rho per selected entry + per-CTA aggregate partials
+__global__ void __launch_bounds__(kSelThreads) gather_kernel(const int64_t* __restrict__ top_idx, const DevPlan* __restrict__ dp,
+                                                             const float* __restrict__ X, int64_t m, int64_t row_offset,
+                                                             const double* __restrict__ mu, const float* __restrict__ P,
+                                                             const double* __restrict__ V, int k, int k_pad,
+                                                             double* __restrict__ rho, double* __restrict__ agg_part) {
+  __shared__ double red[kSelThreads / 32][8];
+  const int64_t n = dp->sel_local;
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int64_t t = (int64_t)blockIdx.x * kSelThreads + threadIdx.x; t < n; t += (int64_t)gridDim.x * kSelThreads) {
+    const int64_t g = top_idx[t];
+    const int64_t i = g / m - row_offset, j = g % m;
+    const double x = (double)X[i * m + j];
+    const double M = mu[j];
+    const double xc = x - M;
+    double S = 0.0;
+    for (int r = 0; r < k; ++r) S = fma((double)P[i * k_pad + r], V[j * k + r], S);
+    const double T = xc - S;
+    const double x2 = x * x;
+    const double rm = M * M / x2, rs = S * S / x2, rt = T * T / x2;
+    const double cr = 1.0 - (rm + rs + rt);
+    rho[t * 4 + 0] = rm; rho[t * 4 + 1] = rs; rho[t * 4 + 2] = rt; rho[t * 4 + 3] = cr;
+    acc[0] += rm; acc[1] += rs; acc[2] += rt; acc[3] += cr;
+    acc[4] += M * M; acc[5] += S * S; acc[6] += T * T; acc[7] += x2;
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xFFFFFFFFu, acc[q], o);
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) red[threadIdx.x >> 5][q] = acc[q];
+  __syncthreads();
+  if (threadIdx.x < 8) {
+    double s = 0.0;
+    for (int w = 0; w < kSelThreads / 32; ++w) s += red[w][threadIdx.x];
+    agg_part[(int64_t)blockIdx.x * 8 + threadIdx.x] = s;
+  }
+}
+
+__global__ void agg_reduce_kernel(const double* __restrict__ part, int nparts, double* __restrict__ agg) {
+  const int t = threadIdx.x;
+  if (t < 8) {
+    double s = 0.0;
+    for (int q = 0; q < nparts; ++q) s += part[(int64_t)q * 8 + t];
+    agg[t] = s;
+  }
+}
+
+}  // namespace
+
+// level 0: hist2 ; level 1: find b2, hist3 ; level 2: find T, mark, publish counts
+avd_status launch_select(Ctx* c, const float* X, int level, int rank) {
+  const bool fromX = c->cand_overflow;
+  const int64_t n = fromX ? c->cfg.l_local * c->cfg.m : c->hplan.cand_count;
+  const int64_t base = c->cfg.row_offset * c->cfg.m;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, kSelThreads), 4LL * c->num_sms));
+  if (level == 0) {
+    AVD_CUDA(cudaMemsetAsync(c->hist2, 0, sizeof(unsigned long long) * kHistBins, c->stream));
+    if (fromX) hist_kernel<true><<<grid, kSelThreads, 0, c->stream>>>(0, n, nullptr, nullptr, X, c->dplan, c->hist2);
+    else hist_kernel<false><<<grid, kSelThreads, 0, c->stream>>>(0, n, c->cand_key, c->cand_idx, nullptr, c->dplan, c->hist2);
+    AVD_LAUNCHED(c);
+  } else if (level == 1) {
+    find_bin_kernel<<<1, 32, 0, c->stream>>>(0, c->hist2, c->dplan);
+    AVD_LAUNCHED(c);
+    AVD_CUDA(cudaMemsetAsync(c->hist3, 0, sizeof(unsigned long long) * kHist3Bins, c->stream));
+    if (fromX) hist_kernel<true><<<grid, kSelThreads, 0, c->stream>>>(1, n, nullptr, nullptr, X, c->dplan, c->hist3);
+    else hist_kernel<false><<<grid, kSelThreads, 0, c->stream>>>(1, n, c->cand_key, c->cand_idx, nullptr, c->dplan, c->hist3);
+    AVD_LAUNCHED(c);
+  } else {
+    find_bin_kernel<<<1, 32, 0, c->stream>>>(1, c->hist3, c->dplan);
+    AVD_LAUNCHED(c);
+    AVD_CUDA(cudaMemsetAsync(c->bm_sel, 0, sizeof(uint32_t) * c->nwords, c->stream));
+    AVD_CUDA(cudaMemsetAsync(c->bm_tie, 0, sizeof(uint32_t) * c->nwords, c->stream));
+    unsigned long long* counts = reinterpret_cast<unsigned long long*>(c->blk_cnt + 2 * c->nblk);
+    AVD_CUDA(cudaMemsetAsync(counts, 0, 2 * sizeof(unsigned long long), c->stream));
+    if (fromX)
+      mark_kernel<true><<<grid, kSelThreads, 0, c->stream>>>(n, nullptr, nullptr, X, base, c->dplan, c->bm_sel,
+                                                             c->bm_tie, counts);
+    else
+      mark_kernel<false><<<grid, kSelThreads, 0, c->stream>>>(n, c->cand_key, c->cand_idx, nullptr, base, c->dplan,
+                                                              c->bm_sel, c->bm_tie, counts);
+    AVD_LAUNCHED(c);
+    publish_counts_kernel<<<1, 256, 0, c->stream>>>(counts, c->ties, c->cfg.world, rank);
+    AVD_LAUNCHED(c);
+  }
+  return AVD_OK;
+}
+
+avd_status launch_gather(Ctx* c, const float* X, int rank, int64_t* top_idx, double* rho) {
+  blk_count_kernel<<<(unsigned)c->nblk, kSelThreads, 0, c->stream>>>(c->bm_sel, c->bm_tie, c->nwords, c->nblk, c->blk_cnt);
+  AVD_LAUNCHED(c);
+  blk_scan_kernel<<<1, 1024, 0, c->stream>>>(c->blk_cnt, c->nblk, c->ties, c->cfg.world, rank, c->dplan);
+  AVD_LAUNCHED(c);
+  emit_kernel<<<(unsigned)c->nblk, kSelThreads, 0, c->stream>>>(c->bm_sel, c->bm_tie, c->nwords, c->nblk, c->blk_cnt,
+                                                                 c->dplan, c->cfg.row_offset * c->cfg.m, top_idx);
+  AVD_LAUNCHED(c);
+  gather_kernel<<<(unsigned)c->n_gather_ctas, kSelThreads, 0, c->stream>>>(top_idx, c->dplan, X, c->cfg.m, c->cfg.row_offset,
+                                                                           c->mu, c->P, c->V, c->k, c->k_pad, rho, c->agg_part);
+  AVD_LAUNCHED(c);
+  agg_reduce_kernel<<<1, 32, 0, c->stream>>>(c->agg_part, c->n_gather_ctas, c->agg);
+  AVD_LAUNCHED(c);
+  return AVD_OK;
+}
+
+}  // namespace avd

@@ -1,0 +1,133 @@
+// k_split.cu — K2: centring X_c = X - 1 mu^T fused with the operand encoding of
+// the Gram and the top-set candidate pass.
+//   * every centred entry x_c is scaled by the column's power of two 2^shift_j and rounded with
+//     a deterministic dither u ~ U[0,1): q = floor(x_c 2^shift_j + u)  (|q| <= 2^(7 nd - 1));
+//     q is written as nd balanced base-128 int8 digits into TRANSPOSED planes
+//     D_d[j][i] (K-major operands of the tcgen05 kind::i8 Gram);
+//   * entries whose |x| bit pattern falls in a first-level bin >= b1 are appended as
+//     (key, global linear index) candidates of E_top.
+// One read of X (4 B/entry), nd bytes written per entry.
+#include "common.cuh"
+
+namespace avd {
+
+namespace {
+
+constexpr int kSplitRows = 128;   // rows i per CTA tile (= one 128-byte digit row)
+constexpr int kSplitCols = 64;    // columns j per CTA tile
+constexpr int kSplitThreads = 256;
+constexpr int kSW = 33;           // padded smem row stride in 32-bit words
+
+__device__ __forceinline__ uint32_t mix32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7FEB352Du;
+  x ^= x >> 15;
+  x *= 0x846CA68Bu;
+  x ^= x >> 16;
+  return x;
+}
+
+template <int ND>
+__global__ void __launch_bounds__(kSplitThreads) split_kernel(
+    const float* __restrict__ X, int64_t l_local, int64_t m, int64_t m_pad, int64_t l_pad,
+    int64_t row_offset, const double* __restrict__ mu, const int32_t* __restrict__ shift,
+    uint32_t seed32, int8_t* __restrict__ digits, const DevPlan* __restrict__ dp,
+    uint32_t* __restrict__ cand_key, uint64_t* __restrict__ cand_idx,
+    unsigned long long* __restrict__ cand_cnt, int64_t cand_cap) {
+  __shared__ uint32_t sD[ND][kSplitCols * kSW];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t i0 = (int64_t)blockIdx.x * kSplitRows;
+  const int64_t j0 = (int64_t)blockIdx.y * kSplitCols;
+  const int jl = (warp & 1) * 32 + lane;
+  const int64_t j = j0 + jl;
+  const int rg = warp >> 1;  // 32-row group
+  const uint32_t b1 = (uint32_t)dp->b1;
+  const bool colok = j < m;
+  const double muj = colok ? mu[j] : 0.0;
+  const double scale = colok ? ldexp(1.0, shift[j]) : 0.0;
+
+#pragma unroll 1
+  for (int t = 0; t < 8; ++t) {
+    uint32_t packed[ND];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) packed[d] = 0;
+    float xs[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = i0 + rg * 32 + t * 4 + u;
+      xs[u] = (colok && i < l_local) ? __ldcs(X + i * m + j) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = i0 + rg * 32 + t * 4 + u;
+      const bool ok = colok && i < l_local;
+      const float x = xs[u];
+      const uint32_t key = __float_as_uint(x) & 0x7FFFFFFFu;
+      const uint64_t gidx = (uint64_t)(row_offset + i) * (uint64_t)m + (uint64_t)j;
+      // ---- candidate append (warp aggregated)
+      const bool cand = ok && key != 0 && key < 0x7F800000u && (key >> 19) >= b1;
+      const uint32_t ballot = __ballot_sync(0xFFFFFFFFu, cand);
+      if (ballot) {
+        unsigned long long base = 0;
+        if (lane == __ffs(ballot) - 1) base = atomicAdd(cand_cnt, (unsigned long long)__popc(ballot));
+        base = __shfl_sync(0xFFFFFFFFu, base, __ffs(ballot) - 1);
+        if (cand) {
+          const unsigned long long pos = base + __popc(ballot & ((1u << lane) - 1u));
+          if (pos < (unsigned long long)cand_cap) {
+            cand_key[pos] = key;
+            cand_idx[pos] = gidx;
+          }
+        }
+      }
+      // ---- dithered fixed-point digits of the centred entry
+      if (ok) {
+        const double xc = (double)x - muj;
+        const uint32_t h = mix32((uint32_t)gidx ^ mix32((uint32_t)(gidx >> 32) ^ seed32));
+        const double dith = (double)(h >> 8) * (1.0 / 16777216.0);
+        int32_t q = (int32_t)floor(fma(xc, scale, dith));
+        int32_t dg[ND];
+#pragma unroll
+        for (int d = ND - 1; d >= 1; --d) {
+          const int32_t s = ((q + 64) & 127) - 64;
+          dg[d] = s;
+          q = (q - s) >> 7;
+        }
+        dg[0] = q;
+#pragma unroll
+        for (int d = 0; d < ND; ++d) packed[d] |= ((uint32_t)(uint8_t)(int8_t)dg[d]) << (8 * u);
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < ND; ++d) sD[d][jl * kSW + rg * 8 + t] = packed[d];
+  }
+  __syncthreads();
+  // write-out: plane d, row j0+jr, 32 words (128 rows of i) per row -> one 128 B line per warp
+#pragma unroll
+  for (int d = 0; d < ND; ++d) {
+    for (int jr = warp; jr < kSplitCols; jr += kSplitThreads / 32) {
+      const uint32_t w = sD[d][jr * kSW + lane];
+      uint32_t* dst = reinterpret_cast<uint32_t*>(digits + ((int64_t)d * m_pad + j0 + jr) * l_pad + i0);
+      __stcs(dst + lane, w);
+    }
+  }
+}
+
+}  // namespace
+
+avd_status launch_split(Ctx* c, const float* X) {
+  AVD_CUDA(cudaMemsetAsync(c->cand_cnt, 0, sizeof(unsigned long long), c->stream));
+  dim3 grid((unsigned)(c->l_pad / kSplitRows), (unsigned)(c->m_pad / kSplitCols));
+  const uint32_t seed32 = (uint32_t)(c->cfg.seed * 0x9E3779B97F4A7C15ull >> 32) ^ 0xA5A5A5A5u;
+  if (c->nd == 2)
+    split_kernel<2><<<grid, kSplitThreads, 0, c->stream>>>(
+        X, c->cfg.l_local, c->cfg.m, c->m_pad, c->l_pad, c->cfg.row_offset, c->mu, c->shift, seed32,
+        c->digits, c->dplan, c->cand_key, c->cand_idx, c->cand_cnt, c->cand_cap);
+  else
+    split_kernel<3><<<grid, kSplitThreads, 0, c->stream>>>(
+        X, c->cfg.l_local, c->cfg.m, c->m_pad, c->l_pad, c->cfg.row_offset, c->mu, c->shift, seed32,
+        c->digits, c->dplan, c->cand_key, c->cand_idx, c->cand_cnt, c->cand_cap);
+  AVD_LAUNCHED(c);
+  return AVD_OK;
+}
+
+}  // namespace avd

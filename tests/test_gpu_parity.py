@@ -1,0 +1,120 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 CPU oracle on the same seeded
+inputs.  Tolerances are the north star's (BASELINE.json:5) with DESIGN.md R14-R16 readings:
+  mu            ||d mu||_inf <= 1e-6 ||mu||_inf
+  E_top         bit-exact set (ties by linear index)
+  sigma_k       1e-4 relative (inputs have a planted spectral gap at k)
+  energy shares |d s| <= 1e-5 s + 1e-12
+  rho           1e-3 absolute
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from synth.gen import SynthSpec, generate
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu(X, **kw):
+    from paper_2603_10444_b200 import Decomposer
+    Xd = X.cuda()
+    dec = Decomposer(X.shape[0], X.shape[1], **kw)
+    r = dec(Xd)
+    torch.cuda.synchronize()
+    out = dict(mu=r.mu.cpu().numpy(), V=r.V.cpu().numpy(), sigma=r.sigma.cpu().numpy(),
+               top_idx=r.top_idx.cpu().numpy(), rho=r.rho.cpu().numpy(), res=r,
+               launches=dec.launches())
+    dec.close()
+    return out
+
+
+def assert_parity(g, o, sigma_tol=1e-4, share_tol=1e-5, rho_tol=1e-3, check_sigma=True):
+    r = g["res"]
+    mu_o = o["mu"]
+    assert np.max(np.abs(g["mu"] - mu_o)) <= 1e-6 * max(np.max(np.abs(mu_o)), 1e-300)
+    np.testing.assert_array_equal(g["top_idx"], o["top_idx"])
+    assert r.n_top_global == o["n_top"]
+    if check_sigma:
+        np.testing.assert_allclose(g["sigma"], o["sigma"], rtol=sigma_tol, atol=1e-9 * max(o["sigma"][0], 1e-300))
+    s_g = np.array(r.energy_cf[1:]) / r.energy_cf[0]
+    s_o = np.array(o["energy_cf"][1:]) / o["energy_cf"][0]
+    assert np.all(np.abs(s_g - s_o) <= share_tol * s_o + 1e-12), (s_g, s_o)
+    if len(o["rho"]):
+        assert np.max(np.abs(g["rho"] - o["rho"])) <= rho_tol
+    # elementwise energies agree with the closed forms
+    e_el, e_cf = np.array(r.energy_el), np.array(r.energy_cf)
+    assert np.all(np.abs(e_el - e_cf) <= 1e-5 * e_cf[0] + 1e-12), (e_el, e_cf)
+
+
+@pytest.mark.parametrize("digits", [2, 3])
+def test_c1_parity(cuda_device, digits):
+    """BASELINE.json configs[0]: 512 x 256, k = 2, |E_top| = 131."""
+    X = generate(SynthSpec(512, 256, seed=0))
+    o = O.decompose(X.numpy())
+    g = _gpu(X, digits=digits)
+    assert g["res"].n_top_global == 131
+    assert_parity(g, o)
+    assert g["launches"] > 10
+
+
+@pytest.mark.parametrize("l,m,seed", [(3000, 300, 1), (1024, 1024, 2), (777, 130, 3), (4096, 512, 4)])
+def test_ragged_parity(cuda_device, l, m, seed):
+    """Sizes that are not multiples of the 128-tiles / vector width (padding + scalar paths)."""
+    X = generate(SynthSpec(l, m, seed=seed, f_mean=0.8))
+    o = O.decompose(X.numpy())
+    g = _gpu(X)
+    assert_parity(g, o)
+
+
+def test_planted_exact(cuda_device):
+    """sigma_t = 0 dyadic planted data: the digit planes are exact, so the Gram is exact."""
+    spec = SynthSpec(1024, 256, seed=5, exact=True, k_s=4)
+    X = generate(spec)
+    o = O.decompose(X.numpy(), k=2)
+    g = _gpu(X, k=2)
+    assert_parity(g, o, sigma_tol=1e-12)
+
+
+def test_pure_mean_massive_ties(cuda_device):
+    """X = 1 mu^T: G = 0, rho_mean = 1, the top set is whole columns in row-major order."""
+    spec = SynthSpec(512, 128, seed=7, exact=True, k_s=1, spike_scale=0.0)
+    X = generate(spec)
+    o = O.decompose(X.numpy())
+    g = _gpu(X)
+    np.testing.assert_array_equal(g["top_idx"], o["top_idx"])
+    np.testing.assert_allclose(g["rho"][:, 0], 1.0, atol=1e-12)
+    np.testing.assert_array_equal(g["sigma"], 0.0)
+    assert abs(g["res"].energy_cf[1] - g["res"].energy_cf[0]) <= 1e-12 * g["res"].energy_cf[0]
+
+
+def test_nonfinite_rejected(cuda_device):
+    from paper_2603_10444_b200 import Decomposer
+    from paper_2603_10444_b200._lib import AvdError, AVD_ENONFINITE
+    X = generate(SynthSpec(256, 64, seed=1)).cuda()
+    X[17, 5] = float("nan")
+    dec = Decomposer(256, 64)
+    with pytest.raises(AvdError) as e:
+        dec(X)
+    assert e.value.status == AVD_ENONFINITE
+    dec.close()
+
+
+def test_deterministic_and_host_path(cuda_device):
+    from paper_2603_10444_b200 import Decomposer
+    X = generate(SynthSpec(2048, 256, seed=11))
+    dec = Decomposer(2048, 256)
+    a = dec(X.cuda())
+    ta = (a.mu.clone(), a.V.clone(), a.sigma.clone(), a.top_idx.clone(), a.rho.clone(), list(a.energy_cf))
+    b = dec(X.cuda())
+    assert torch.equal(ta[0], b.mu) and torch.equal(ta[1], b.V) and torch.equal(ta[2], b.sigma)
+    assert torch.equal(ta[3], b.top_idx) and torch.equal(ta[4], b.rho) and ta[5] == list(b.energy_cf)
+    h = dec.run_host(X.pin_memory())
+    assert torch.equal(h.mu, ta[0].cpu()) and torch.equal(h.top_idx, ta[3].cpu())
+    assert torch.equal(h.rho, ta[4].cpu()) and torch.equal(h.sigma, ta[2].cpu())
+    dec.close()
+
+
+def test_generator_bit_identical_on_cuda(cuda_device):
+    spec = SynthSpec(1000, 96, seed=3)
+    assert torch.equal(generate(spec), generate(spec, device="cuda").cpu())
