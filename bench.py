@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""Benchmark of the activation outlier-attribution pass (arXiv 2603.10444).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+
+One step = the whole hot path (stats+histogram, centre+digits,
+Gram, eigensolve, projections+energies, exact top set, rho gather) over one synthetic matrix
+(synth/gen.py; default c4 = 131072 x 4096, k = 40, |E_top| = 536870; BASELINE.json configs[3],
+the configuration the metric is quoted on at 1/2/4/8 B200).  X (2.1 GB) is larger than L2, so no
+flush is needed between steps.  N > 1: torchrun, one process per GPU, rows sharded in rank
+order, NCCL all-reduces of the exchange buffers (strong scaling of one matrix); time is the max
+over ranks.  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth.gen import config_spec, generate  # noqa: E402
+
+METRIC = "activation entries decomposed/sec (l*m/s)"
+UNIT = "entries/s"
+WORKLOADS = {
+    "c1": "c1: single matrix l=512, m=256 (k=2, |E_top|=131)",
+    "c2": "c2: single layer l=8192, m=2048 (k=20)",
+    "c4": "c4: single matrix l=131072, m=4096 (k=40), row-sharded over the GPUs",
+    "c5": "c5: single matrix l=1048576, m=8192 (k=81), row-sharded over the GPUs",
+}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ------------------------------------------------------------------ clocks during the timed region
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thr = threading.Thread(target=self._read, daemon=True)
+            self.thr.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ timed stage wrapper
+class TimedBackend:
+    """Wraps the library stage backend and records CUDA events around every stage (on the
+    stream the library launches on, which is torch's current stream)."""
+
+    STAGES = ["stage_stats", "stage_split", "stage_gram", "stage_eig", "stage_project",
+              "stage_select", "stage_gather", "stage_report"]
+
+    def __init__(self, inner):
+        self.inner = inner
+        self.events = []  # (name, start, end)
+        self.record = False
+
+    def exchange_buffer(self, name, dtype):
+        return self.inner.exchange_buffer(name, dtype)
+
+    def __getattr__(self, name):
+        fn = getattr(self.inner, name)
+        if name not in self.STAGES:
+            return fn
+
+        def wrapped(*a, **k):
+            if not self.record:
+                return fn(*a, **k)
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            r = fn(*a, **k)
+            e.record()
+            self.events.append((name, s, e))
+            return r
+        return wrapped
+
+    def stage_ms(self, steps):
+        torch.cuda.synchronize()
+        acc = {}
+        for name, s, e in self.events:
+            acc[name] = acc.get(name, 0.0) + s.elapsed_time(e)
+        return {k.replace("stage_", ""): v / steps for k, v in acc.items()}
+
+
+class LocalComm:
+    rank, world = 0, 1
+
+    def all_reduce(self, t, op):  # pragma: no cover - world 1 never exchanges
+        pass
+
+
+# ------------------------------------------------------------------ CPU baseline (the oracle)
+def cpu_baseline(spec, rows: int, cols: int):
+    from oracle import oracle as O
+    O.build()
+    Xs = generate(spec, 0, rows)[:, :cols].contiguous().numpy()
+    t0 = time.perf_counter()
+    O.decompose(Xs)
+    dt = time.perf_counter() - t0
+    return {"value": rows * cols / dt, "unit": UNIT, "cores": O.host_cores(), "kind": "oracle",
+            "sample": f"rows [0,{rows}) x cols [0,{cols}) of the {spec.l}x{spec.m} matrix "
+                      f"(full oracle pass: two-pass mean, explicit Xc, fp64 Gram, cyclic Jacobi "
+                      f"(single thread), full sort, rho); {dt:.2f} s",
+            "seconds": dt}
+
+
+def run_reference(args):
+    """--impl reference: the fp64 CPU oracle as it stands, on a bounded sample per step."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    O.build()
+    spec = config_spec(args.config)
+    rows, cols = 2048, 256
+    Xs = generate(spec, 0, rows)[:, :cols].contiguous().numpy()
+    for _ in range(args.warmup):
+        O.decompose(Xs)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.decompose(Xs)
+    dt = (time.perf_counter() - t0) / args.steps
+    v = rows * cols / dt
+    sample = (f"rows [0,{rows}) x cols [0,{cols}) of the {args.config} matrix per step "
+              f"(oracle: fp64 two-pass mean, Gram, cyclic Jacobi, full sort, rho)")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": WORKLOADS.get(args.config, args.config),
+                                            "sample_rows": rows, "sample_cols": cols},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": O.host_cores(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--digits", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2603_10444_b200.distributed import ShardedDecomposer, TorchComm, _LibBackend, run_stages, shard_rows
+    from paper_2603_10444_b200.api import Decomposer
+
+    spec = config_spec(args.config)
+    l, m = spec.l, spec.m
+    r0, lloc = shard_rows(l, world, rank)
+    X = generate(spec, r0, lloc, device="cuda")
+    torch.cuda.synchronize()
+
+    if world == 1:
+        dec = Decomposer(l, m, digits=args.digits, seed=0)
+        comm = LocalComm()
+    else:
+        sd = ShardedDecomposer(l, m, digits=args.digits, seed=0)
+        dec, comm = sd.dec, sd.comm
+    backend = TimedBackend(_LibBackend(dec))
+
+    def step():
+        return run_stages(backend, comm, X)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    for _ in range(args.warmup):
+        res = step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.15)
+    launches0 = dec.launches()
+    backend.record = True
+    t_s, t_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_s.record()
+    for _ in range(args.steps):
+        res = step()
+    t_e.record()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    backend.record = False
+    launches = dec.launches() - launches0
+    clocks = sampler.stop()
+    ms = t_s.elapsed_time(t_e)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    stage_ms = backend.stage_ms(args.steps)
+    ms_step = ms / args.steps
+    value = l * m / (ms_step * 1e-3)
+
+    # ---------------- e2e: host buffers through the public API, copies inside the timed region
+    e2e = None
+    Xh = X.cpu().pin_memory()
+    n_loc = int(res.top_idx.numel())
+    d2h = 8 * (m + m * dec.k + dec.k) + 8 * n_loc + 32 * n_loc
+    if world == 1:
+        for _ in range(1):
+            dec.run_host(Xh)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            dec.run_host(Xh)
+        torch.cuda.synchronize()
+        e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
+    else:
+        Xd = torch.empty_like(X)
+        outs = None
+
+        def e2e_step():
+            Xd.copy_(Xh, non_blocking=True)
+            r = run_stages(_LibBackend(dec), comm, Xd)
+            return [t.cpu() for t in (r.mu, r.V, r.sigma, r.top_idx, r.rho)]
+        outs = e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            outs = e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
+        t = torch.tensor([e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item())
+        del outs
+    e2e = {"value": l * m / (e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(lloc * m * 4),
+           "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms}
+
+    # ---------------- roofline of the dominant kernel (the tcgen05 Gram, stage "gram")
+    peaks, which = _peaks()
+    nd = dec.plan.digits
+    t_gram = stage_ms.get("gram", float("nan")) * 1e-3
+    alg_ops = lloc * m * (m + 1)                       # symmetric Gram, SURVEY §8(d) K3
+    T = (m + 127) // 128
+    lpad = (lloc + 127) // 128 * 128
+    exec_ops = (4 if nd == 2 else 6) * 2 * lpad * 128 * 128 * (T * (T + 1) // 2)
+    int8_peak = 2.0 * peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))  # i8 = 2x bf16 (nominal)
+    achieved = alg_ops / t_gram / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(f"{args.config}_gram_nd{nd}")
+    except OSError:
+        pass
+    roofline = {"bound": "tensor", "kernel": "gram_kernel (K3, tcgen05.mma kind::i8)",
+                "achieved": achieved, "peak": int8_peak, "unit": "TFLOP/s",
+                "frac": achieved / int8_peak, "traffic": traffic,
+                "peak_source": f"{which}: 2 x bf16_tflops_sustained (int8 dense = 2x bf16 nominal)",
+                "algorithmic_ops_per_launch": alg_ops, "executed_int8_ops_per_launch": exec_ops,
+                "executed_frac": exec_ops / t_gram / 1e12 / int8_peak,
+                "launch_ms": t_gram * 1e3}
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    streams = {
+        "stats (K1)": (lloc * m * 4, stage_ms.get("stats")),
+        "split (K2)": (lloc * m * (4 + nd), stage_ms.get("split")),
+        "project+energy (K5/K8)": (lloc * m * 4, stage_ms.get("project")),
+    }
+    stream_roof = {k: {"GB/s": b / (t * 1e-3) / 1e9, "frac_hbm": b / (t * 1e-3) / 1e9 / hbm}
+                   for k, (b, t) in streams.items() if t}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "i8/i32 Gram + f64 eig + f32 projection",
+        "data": "synthetic (planted mean bias + rank-k Walsh spike + Irwin-Hall tail, synth/gen.py seed 0)",
+        "config": {"workload": WORKLOADS[args.config], "l": l, "m": m, "k": dec.k,
+                   "n_top": dec.n_top, "digits": nd, "l2": "inputs larger than L2 (X is "
+                   f"{l * m * 4 / 1e9:.2f} GB > 126 MB); no flush",
+                   "parallelism": f"row-shard x{world}"},
+        "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches),
+        "roofline": roofline, "stage_ms": stage_ms, "streaming_roofline": stream_roof,
+        "eig_iters": res.iters, "eig_max_resid": res.max_resid,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(spec, 2048, 512)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -165,6 +165,15 @@ avd_status avd_stage_select(avd_ctx* ctx, const float* X_dev, int32_t level, int
 avd_status avd_stage_gather(avd_ctx* ctx, const float* X_dev, int32_t rank, avd_outputs* out);
 avd_status avd_stage_report(avd_ctx* ctx, avd_outputs* out);
 
+/* Tie quota of `rank` (R3): E_top takes the first q entries with key == T in global
+ * linear order and rows are sharded in rank order, so rank r takes
+ *   quota_r  = clamp(q - sum_{r'<r} tie_counts[r'], 0, tie_counts[r])
+ *   offset_r = sum_{r'<r} (sel_counts[r'] + quota_r')   (position of its slice in E_top).
+ * sel_counts / tie_counts: host arrays [world] of per-rank counts of key > T / key == T.
+ * Host-only integer logic (no device work); used by avd_stage_gather.                       */
+avd_status avd_tie_quota(const int64_t* sel_counts, const int64_t* tie_counts, int32_t world,
+                         int32_t rank, int64_t q, int64_t* quota, int64_t* offset);
+
 /* Number of kernels this context launched since creation (for the bench's gpu_launches). */
 int64_t avd_launch_count(const avd_ctx* ctx);
 

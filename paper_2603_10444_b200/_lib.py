@@ -19,7 +19,7 @@ BUF = dict(STATS=0, COLMAX=1, COLMIN=2, HIST1=3, GRAM=4, ENERGY=5, HIST2=6, HIST
 EXPORTS = ["avd_plan", "avd_create", "avd_destroy", "avd_get_plan", "avd_decompose",
            "avd_decompose_host", "avd_buffer", "avd_stage_stats", "avd_stage_split",
            "avd_stage_gram", "avd_stage_eig", "avd_stage_project", "avd_stage_select",
-           "avd_stage_gather", "avd_stage_report", "avd_launch_count", "avd_strerror",
+           "avd_stage_gather", "avd_stage_report", "avd_tie_quota", "avd_launch_count", "avd_strerror",
            "avd_last_error"]
 
 
@@ -86,6 +86,7 @@ def lib() -> ctypes.CDLL:
         L.avd_stage_select.argtypes = [P, P, I32, I32]
         L.avd_stage_gather.argtypes = [P, P, I32, ctypes.POINTER(avd_outputs)]
         L.avd_stage_report.argtypes = [P, ctypes.POINTER(avd_outputs)]
+        L.avd_tie_quota.argtypes = [P, P, I32, I32, I64, P, P]
         L.avd_launch_count.argtypes = [P]
         L.avd_launch_count.restype = I64
         L.avd_strerror.argtypes = [ctypes.c_int]
@@ -181,3 +182,14 @@ def avd_stage_report(h, out: avd_outputs):
 
 def avd_launch_count(h) -> int:
     return int(lib().avd_launch_count(h))
+
+
+def avd_tie_quota(sel_counts, tie_counts, rank: int, q: int):
+    """(quota, offset) of `rank` — host-only integer logic of the library (no GPU needed)."""
+    world = len(sel_counts)
+    S = (ctypes.c_int64 * world)(*[int(x) for x in sel_counts])
+    T = (ctypes.c_int64 * world)(*[int(x) for x in tie_counts])
+    quota, off = ctypes.c_int64(), ctypes.c_int64()
+    check(lib().avd_tie_quota(S, T, world, rank, int(q), ctypes.byref(quota), ctypes.byref(off)),
+          "avd_tie_quota")
+    return quota.value, off.value

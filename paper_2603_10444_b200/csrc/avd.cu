@@ -271,6 +271,22 @@ avd_status avd_get_plan(const avd_ctx* c, avd_plan_t* plan) {
 
 int64_t avd_launch_count(const avd_ctx* c) { return c ? c->launches : 0; }
 
+avd_status avd_tie_quota(const int64_t* sel_counts, const int64_t* tie_counts, int32_t world, int32_t rank,
+                         int64_t q, int64_t* quota, int64_t* offset) {
+  if (!sel_counts || !tie_counts || !quota || !offset || world < 1 || rank < 0 || rank >= world || q < 0) {
+    set_error("avd_tie_quota: bad arguments");
+    return AVD_EINVAL;
+  }
+  int64_t rem = q, off = 0;
+  for (int r = 0; r < world; ++r) {
+    const int64_t qr = std::min<int64_t>(std::max<int64_t>(rem, 0), tie_counts[r]);
+    if (r == rank) { *quota = qr; *offset = off; return AVD_OK; }
+    off += sel_counts[r] + qr;
+    rem -= tie_counts[r];
+  }
+  return AVD_OK;
+}
+
 avd_status avd_buffer(avd_ctx* c, int32_t which, void** ptr, size_t* bytes) {
   if (!c || !ptr || !bytes) return AVD_EINVAL;
   const int64_t m = c->cfg.m;

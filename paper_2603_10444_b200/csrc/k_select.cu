@@ -11,6 +11,7 @@
 // Rank r takes the ties left after ranks < r (rows are sharded in rank order).
 // The histogram and mark passes read the K2 candidate list (entries with key>>19 >= b1), or,
 // if it overflowed its capacity, stream X directly.
+#include <vector>
 #include "common.cuh"
 
 namespace avd {
@@ -157,23 +158,22 @@ __global__ void __launch_bounds__(kSelThreads) blk_count_kernel(const uint32_t* 
   if (threadIdx.x == 0) { blk[blockIdx.x] = s1[0]; blk[nblk + blockIdx.x] = s2[0]; }
 }
 
-// exclusive scan of block counts (one CTA) + this rank's tie quota and offsets
-__global__ void blk_scan_kernel(int64_t* __restrict__ blk, int64_t nblk, const long long* __restrict__ ties, int world,
-                                int rank, DevPlan* __restrict__ dp) {
+// exclusive scan of block counts (one CTA); quota / offset come from avd_tie_quota (host)
+__global__ void blk_scan_kernel(int64_t* __restrict__ blk, int64_t nblk, int64_t quota, int64_t offset,
+                                int64_t ties_local, DevPlan* __restrict__ dp) {
   __shared__ int64_t carry[2];
+  __shared__ int64_t sh[1024];
   if (threadIdx.x == 0) { carry[0] = 0; carry[1] = 0; }
   __syncthreads();
   for (int which = 0; which < 2; ++which) {
     int64_t* a = blk + which * nblk;
     for (int64_t base = 0; base < nblk; base += blockDim.x) {
       const int64_t i = base + threadIdx.x;
-      int64_t v = i < nblk ? a[i] : 0;
-      // inclusive block scan (Hillis-Steele in smem)
-      __shared__ int64_t sh[1024];
+      const int64_t v = i < nblk ? a[i] : 0;
       sh[threadIdx.x] = v;
       __syncthreads();
       for (int o = 1; o < (int)blockDim.x; o <<= 1) {
-        int64_t t = threadIdx.x >= (unsigned)o ? sh[threadIdx.x - o] : 0;
+        const int64_t t = threadIdx.x >= (unsigned)o ? sh[threadIdx.x - o] : 0;
         __syncthreads();
         sh[threadIdx.x] += t;
         __syncthreads();
@@ -186,24 +186,10 @@ __global__ void blk_scan_kernel(int64_t* __restrict__ blk, int64_t nblk, const l
     }
   }
   if (threadIdx.x == 0) {
-    long long before_ties = 0, before_sel = 0;
-    for (int r = 0; r < rank; ++r) { before_ties += ties[world + r]; before_sel += ties[r]; }
-    const long long q = dp->empty ? 0 : dp->q;
-    long long quota = q - before_ties;
-    quota = quota < 0 ? 0 : quota;
-    quota = quota > ties[world + rank] ? ties[world + rank] : quota;
-    // global offset: all sel of ranks < r plus their quotas
-    long long off = before_sel;
-    long long rem = q;
-    for (int r = 0; r < rank; ++r) {
-      const long long qr = rem < ties[world + r] ? (rem < 0 ? 0 : rem) : ties[world + r];
-      off += qr;
-      rem -= ties[world + r];
-    }
-    dp->ties_local = ties[world + rank];
+    dp->ties_local = ties_local;
     dp->quota = quota;
     dp->sel_local = carry[0] + quota;
-    dp->top_offset = off;
+    dp->top_offset = offset;
   }
 }
 
@@ -352,9 +338,19 @@ avd_status launch_select(Ctx* c, const float* X, int level, int rank) {
 }
 
 avd_status launch_gather(Ctx* c, const float* X, int rank, int64_t* top_idx, double* rho) {
+  // exchanged per-rank counts -> this rank's tie quota and global offset (host integer logic)
+  const int world = c->cfg.world;
+  std::vector<long long> tc(2 * world);
+  AVD_CUDA(cudaMemcpyAsync(tc.data(), c->ties, sizeof(long long) * 2 * world, cudaMemcpyDeviceToHost, c->stream));
+  AVD_CUDA(cudaMemcpyAsync(&c->hplan, c->dplan, sizeof(DevPlan), cudaMemcpyDeviceToHost, c->stream));
+  AVD_CUDA(cudaStreamSynchronize(c->stream));
+  std::vector<int64_t> sel(world), tie(world);
+  for (int r = 0; r < world; ++r) { sel[r] = tc[r]; tie[r] = tc[world + r]; }
+  int64_t quota = 0, offset = 0;
+  AVD_TRY(avd_tie_quota(sel.data(), tie.data(), world, rank, c->hplan.empty ? 0 : c->hplan.q, &quota, &offset));
   blk_count_kernel<<<(unsigned)c->nblk, kSelThreads, 0, c->stream>>>(c->bm_sel, c->bm_tie, c->nwords, c->nblk, c->blk_cnt);
   AVD_LAUNCHED(c);
-  blk_scan_kernel<<<1, 1024, 0, c->stream>>>(c->blk_cnt, c->nblk, c->ties, c->cfg.world, rank, c->dplan);
+  blk_scan_kernel<<<1, 1024, 0, c->stream>>>(c->blk_cnt, c->nblk, quota, offset, tie[rank], c->dplan);
   AVD_LAUNCHED(c);
   emit_kernel<<<(unsigned)c->nblk, kSelThreads, 0, c->stream>>>(c->bm_sel, c->bm_tie, c->nwords, c->nblk, c->blk_cnt,
                                                                  c->dplan, c->cfg.row_offset * c->cfg.m, top_idx);

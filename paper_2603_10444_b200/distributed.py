@@ -1,0 +1,146 @@
+"""Row-sharded pass over P GPUs: one process per GPU, NCCL collectives via torch.distributed.
+
+Rank r owns the contiguous rows [row_offset_r, row_offset_r + l_r) of the global matrix (rank
+order == row order, which makes the tie quota of E_top a rank-ordered prefix).  Every numerical
+step runs in libavd's kernels through the stage entry points of include/avd.h; between them this
+module all-reduces exactly the exchange buffers the header lists:
+
+  stats   : column sums + sum x^2 + non-finite count (SUM f64), column max (MAX), min (MIN),
+            |x| histogram level 1 (SUM i64)
+  gram    : the exact int64 Gram partials (SUM i64)  -> identical G on every rank
+  eig     : replicated (same G, same seed -> bit-identical V_k, sigma_k on every rank)
+  project : elementwise energy sums + column sums of P (SUM f64)
+  select  : histogram levels 2, 3 (SUM i64), per-rank sel/tie counts (SUM = all-gather)
+  gather  : rho aggregates (SUM f64)
+
+The exchange logic is written against a tiny `Comm` interface so the CPU tests can drive the
+same orchestration with the gloo backend (tests/test_distributed_gloo.py).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import _lib as L
+from .api import Decomposer, Result
+
+# (stage, buffer name, dtype, reduce op) in call order
+EXCHANGES = {
+    "stats": [("STATS", torch.float64, "sum"), ("COLMAX", torch.float32, "max"),
+              ("COLMIN", torch.float32, "min"), ("HIST1", torch.int64, "sum")],
+    "gram": [("GRAM", torch.int64, "sum")],
+    "project": [("ENERGY", torch.float64, "sum")],
+    "select0": [("HIST2", torch.int64, "sum")],
+    "select1": [("HIST3", torch.int64, "sum")],
+    "select2": [("TIES", torch.int64, "sum")],
+    "gather": [("AGG", torch.float64, "sum")],
+}
+
+_OPS = {"sum": dist.ReduceOp.SUM, "max": dist.ReduceOp.MAX, "min": dist.ReduceOp.MIN}
+
+
+def shard_rows(l_global: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous near-equal row shard of `rank`: (row_offset, l_local)."""
+    r0 = l_global * rank // world
+    r1 = l_global * (rank + 1) // world
+    return r0, r1 - r0
+
+
+class TorchComm:
+    """all_reduce over a torch.distributed process group (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def all_reduce(self, t: torch.Tensor, op: str) -> None:
+        dist.all_reduce(t, op=_OPS[op], group=self.group)
+
+
+def run_stages(backend, comm, X) -> object:
+    """The sharded pass: stage calls of `backend` interleaved with `comm` exchanges."""
+    rank = comm.rank
+
+    def exchange(stage):
+        if comm.world == 1:
+            return
+        for name, dtype, op in EXCHANGES[stage]:
+            comm.all_reduce(backend.exchange_buffer(name, dtype), op)
+
+    backend.stage_stats(X)
+    exchange("stats")
+    backend.stage_split(X)
+    backend.stage_gram()
+    exchange("gram")
+    backend.stage_eig()
+    backend.stage_project(X)
+    exchange("project")
+    for lv in range(3):
+        backend.stage_select(X, lv, rank)
+        exchange(f"select{lv}")
+    backend.stage_gather(X, rank)
+    exchange("gather")
+    return backend.stage_report()
+
+
+class _LibBackend:
+    """Stage calls into libavd (device pointers of torch tensors)."""
+
+    def __init__(self, dec: Decomposer):
+        self.dec = dec
+        self.h = dec.h
+        self.out = None
+        self._views = {}
+
+    def exchange_buffer(self, name, dtype):
+        if name not in self._views:
+            self._views[name] = self.dec.buffer(name, dtype)
+        return self._views[name]
+
+    def stage_stats(self, X):
+        L.avd_stage_stats(self.h, X.data_ptr())
+
+    def stage_split(self, X):
+        L.avd_stage_split(self.h, X.data_ptr())
+
+    def stage_gram(self):
+        L.avd_stage_gram(self.h)
+
+    def stage_eig(self):
+        self.eig_status = L.avd_stage_eig(self.h)
+
+    def stage_project(self, X):
+        L.avd_stage_project(self.h, X.data_ptr())
+
+    def stage_select(self, X, level, rank):
+        L.avd_stage_select(self.h, X.data_ptr(), level, rank)
+
+    def stage_gather(self, X, rank):
+        self.out = self.dec._outputs()
+        L.avd_stage_gather(self.h, X.data_ptr(), rank, self.out)
+
+    def stage_report(self) -> Result:
+        L.avd_stage_report(self.h, self.out)
+        return self.dec._result(self.out, self.eig_status)
+
+
+class ShardedDecomposer:
+    """Decomposer of a row-sharded matrix: call on this rank's [l_local, m] CUDA block."""
+
+    def __init__(self, l_global: int, m: int, group=None, **kw):
+        self.comm = TorchComm(group)
+        self.row_offset, self.l_local = shard_rows(l_global, self.comm.world, self.comm.rank)
+        self.dec = Decomposer(l_global, m, world=self.comm.world, l_local=self.l_local,
+                              row_offset=self.row_offset, **kw)
+        self.backend = _LibBackend(self.dec)
+
+    def __call__(self, X_local: torch.Tensor) -> Result:
+        self.dec._check_X(X_local)
+        return run_stages(self.backend, self.comm, X_local)
+
+    def launches(self) -> int:
+        return self.dec.launches()
+
+    def close(self):
+        self.dec.close()
