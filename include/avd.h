@@ -78,7 +78,11 @@ typedef struct {
   int32_t world;           /* ranks sharing the rows (1 = single GPU)                        */
   int32_t device;          /* CUDA device ordinal                                            */
   void* stream;            /* cudaStream_t (NULL = legacy default stream)                    */
+  int32_t flags;           /* AVD_FLAG_* bits (0 = defaults)                                 */
 } avd_config;
+
+/* avd_config.flags: select E_top by streaming X even when the candidate list would do (tests) */
+#define AVD_FLAG_STREAM_SELECT 1
 
 /* Outputs.  Device arrays caller-owned, sized from the plan (cap = n_top). */
 typedef struct {
@@ -131,24 +135,31 @@ avd_status avd_decompose_host(avd_ctx* ctx, const float* X_host, avd_outputs* ou
 /* ---- stage entry points (row-sharded, world >= 1) -------------------------------------
  * Call in this order; after each stage the caller all-reduces (over all ranks, in place)
  * the buffers listed, then calls the next stage.  With world == 1 no exchange is needed.
- *   avd_stage_stats    (K1 column sums, sum x^2, column max/min, |x| histogram)
+ *   avd_stage_stats    (K1 column sums, sum x^2, #nonzero, column max/min, row-sampled |x|
+ *                       histogram)
  *       exchange: AVD_BUF_STATS (f64, SUM), AVD_BUF_COLMAX (f32, MAX),
  *                 AVD_BUF_COLMIN (f32, MIN), AVD_BUF_HIST1 (i64, SUM)
- *   avd_stage_split    (mu, column scales, K2 centred int8 digit planes + top-set candidates)
- *   avd_stage_gram     (K3 tcgen05 int8 Gram, exact int64)   exchange: AVD_BUF_GRAM (i64, SUM)
+ *   avd_stage_split    (mu, column scales, candidate bin b0, K2 centred int8 digit planes +
+ *                       top-set candidates)
+ *   avd_stage_gram     (K3 tcgen05 int8 Gram, exact int64)
+ *       exchange: AVD_BUF_GRAM (i64, SUM), AVD_BUF_CAND (i64, SUM)
  *   avd_stage_eig      (K4 subspace iteration + Rayleigh-Ritz; replicated on every rank)
  *   avd_stage_project  (K5+K8 projections P = Xc V_k and elementwise energies)
  *       exchange: AVD_BUF_ENERGY (f64, SUM)
- *   avd_stage_select(level 0)  (K6 second-level histogram)    exchange: AVD_BUF_HIST2 (i64, SUM)
- *   avd_stage_select(level 1)  (K6 third-level histogram)     exchange: AVD_BUF_HIST3 (i64, SUM)
- *   avd_stage_select(level 2)  (K6 mark + per-rank tie count) exchange: AVD_BUF_TIES (i64, SUM)
+ *   avd_stage_select(level 0)  (K6 exact |x| histogram, bits 30:19)  exchange: AVD_BUF_HIST0 (i64, SUM)
+ *   avd_stage_select(level 1)  (K6 bits 18:7 inside bin b1)          exchange: AVD_BUF_HIST2 (i64, SUM)
+ *   avd_stage_select(level 2)  (K6 bits 6:0 inside (b1, b2))         exchange: AVD_BUF_HIST3 (i64, SUM)
+ *   avd_stage_select(level 3)  (K6 threshold T, mark, per-rank counts) exchange: AVD_BUF_TIES (i64, SUM)
  *   avd_stage_gather   (K6 ordered compaction with the rank's tie quota, K7 rho gather)
  *       exchange: AVD_BUF_AGG (f64, SUM)
- *   avd_stage_report   (host scalars into out)                                            */
+ *   avd_stage_report   (host scalars into out)
+ * The K6 histograms read the K2 candidate list (entries with |x| bits >= bin b0 chosen from the
+ * row-sampled histogram), or stream X itself when the exchanged candidate count does not cover
+ * |E_top| or a rank overflowed its candidate capacity; both give the exact same E_top.        */
 typedef enum {
   AVD_BUF_STATS = 0, AVD_BUF_COLMAX = 1, AVD_BUF_COLMIN = 2, AVD_BUF_HIST1 = 3,
   AVD_BUF_GRAM = 4, AVD_BUF_ENERGY = 5, AVD_BUF_HIST2 = 6, AVD_BUF_HIST3 = 7,
-  AVD_BUF_TIES = 8, AVD_BUF_AGG = 9,
+  AVD_BUF_TIES = 8, AVD_BUF_AGG = 9, AVD_BUF_HIST0 = 10, AVD_BUF_CAND = 11,
   /* read-only views for tests / diagnostics (not exchanged) */
   AVD_BUF_MU = 16, AVD_BUF_G = 17, AVD_BUF_P = 18, AVD_BUF_DIGITS = 19, AVD_BUF_SCALE = 20
 } avd_buffer_id;

@@ -13,6 +13,7 @@ LIB_PATH = os.path.join(HERE, "libavd.so")
 
 AVD_OK, AVD_EINVAL, AVD_ENONFINITE, AVD_ENOCONV, AVD_ECUDA, AVD_ENOMEM, AVD_ESTATE = 0, 1, 2, 3, 4, 6, 8
 BUF = dict(STATS=0, COLMAX=1, COLMIN=2, HIST1=3, GRAM=4, ENERGY=5, HIST2=6, HIST3=7, TIES=8, AGG=9,
+           HIST0=10, CAND=11,
            MU=16, G=17, P=18, DIGITS=19, SCALE=20)
 
 # every symbol include/avd.h declares
@@ -36,7 +37,7 @@ class avd_config(ctypes.Structure):
                 ("seed", ctypes.c_uint64), ("max_iters", ctypes.c_int32),
                 ("eig_tol", ctypes.c_double), ("digits", ctypes.c_int32),
                 ("world", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("stream", ctypes.c_void_p)]
+                ("stream", ctypes.c_void_p), ("flags", ctypes.c_int32)]
 
 
 class avd_outputs(ctypes.Structure):

@@ -55,7 +55,7 @@ class Decomposer:
                  k_frac: float = 0.01, top_frac: float = 0.001, seed: int = 0, digits: int = 0,
                  max_iters: int = 0, eig_tol: float = 0.0, device: int | None = None,
                  world: int = 1, l_local: int | None = None, row_offset: int = 0,
-                 stream: torch.cuda.Stream | None = None):
+                 stream: torch.cuda.Stream | None = None, flags: int = 0):
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2603_10444_b200 needs a CUDA device (sm_100a); no CPU path")
         self.device = torch.cuda.current_device() if device is None else int(device)
@@ -71,6 +71,7 @@ class Decomposer:
         cfg.max_iters, cfg.eig_tol, cfg.digits = int(max_iters), float(eig_tol), int(digits)
         cfg.world, cfg.device = int(world), self.device
         cfg.stream = ctypes.c_void_p(self.stream.cuda_stream)
+        cfg.flags = int(flags)
         self.cfg = cfg
         with torch.cuda.device(self.device):
             self.h = L.avd_create(cfg)

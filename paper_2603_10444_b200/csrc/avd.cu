@@ -74,7 +74,8 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   const int ncb = (int)ceil_div(m, 256LL * ((m % 4 == 0) ? 4 : 1));
   C->r1 = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(4LL * C->num_sms, ncb), ceil_div(ll, 4)));
   C->cand_cap = std::min<int64_t>(ll * m, std::max<int64_t>(4 * n_top, 1 << 20));
-  C->n_red = (int)ceil_div(m, 32);
+  C->n_red = (int)ceil_div(m, kRedRowsC);
+  C->gemm_ks = (int)std::max<int64_t>(1, std::min<int64_t>(8, ceil_div(2LL * C->num_sms, ceil_div(m, 32))));
   C->n_proj_ctas = (int)ceil_div(ll, 32);
   C->nwords = ceil_div(ll * m, 32);
   C->nblk = ceil_div(C->nwords, 1024);
@@ -85,7 +86,7 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   L.add(sizeof(float) * C->r1 * m);             // 1 colmax_part
   L.add(sizeof(float) * C->r1 * m);             // 2 colmin_part
   L.add(sizeof(double) * C->r1 * ncb);          // 3 sq_part
-  L.add(sizeof(double) * (m + 2));              // 4 stats
+  L.add(sizeof(double) * (m + 3));              // 4 stats
   L.add(sizeof(float) * m);                     // 5 colmax
   L.add(sizeof(float) * m);                     // 6 colmin
   L.add(sizeof(unsigned long long) * kHistBins);// 7 hist1
@@ -124,6 +125,9 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   L.add(sizeof(double) * 8);                    // 40 agg
   L.add(sizeof(double) * 8 * C->n_gather_ctas); // 41 agg_part
   L.add(sizeof(double) * 16);                   // 42 report
+  L.add(sizeof(unsigned long long) * kHistBins);// 43 hist0
+  L.add(sizeof(long long) * 2);                 // 44 cand_x
+  L.add(sizeof(double) * C->gemm_ks * m * p);   // 45 Ypart
   plan->workspace_bytes = L.total;
   if (lay) *lay = L;
   return AVD_OK;
@@ -238,7 +242,7 @@ avd_status avd_create(const avd_config* cfg, avd_ctx** out) {
   BIND(trace, double*); BIND(V, double*); BIND(sigma, double*); BIND(V32, float*); BIND(P, float*);
   BIND(en_part, double*); BIND(colsumP_part, double*); BIND(energy, double*); BIND(hist2, unsigned long long*);
   BIND(hist3, unsigned long long*); BIND(ties, long long*); BIND(bm_sel, uint32_t*); BIND(bm_tie, uint32_t*);
-  BIND(blk_cnt, int64_t*); BIND(agg, double*); BIND(agg_part, double*); BIND(report, double*);
+  BIND(blk_cnt, int64_t*); BIND(agg, double*); BIND(agg_part, double*); BIND(report, double*); BIND(hist0, unsigned long long*); BIND(cand_x, long long*); BIND(Ypart, double*);
 #undef BIND
   if (cudaMallocHost(&c->eig_host, sizeof(double) * 4 * kMaxP) != cudaSuccess) {
     cudaGetLastError();
@@ -291,7 +295,9 @@ avd_status avd_buffer(avd_ctx* c, int32_t which, void** ptr, size_t* bytes) {
   if (!c || !ptr || !bytes) return AVD_EINVAL;
   const int64_t m = c->cfg.m;
   switch (which) {
-    case AVD_BUF_STATS: *ptr = c->stats; *bytes = sizeof(double) * (m + 2); break;
+    case AVD_BUF_STATS: *ptr = c->stats; *bytes = sizeof(double) * (m + 3); break;
+    case AVD_BUF_HIST0: *ptr = c->hist0; *bytes = sizeof(long long) * kHistBins; break;
+    case AVD_BUF_CAND: *ptr = c->cand_x; *bytes = sizeof(long long) * 2; break;
     case AVD_BUF_COLMAX: *ptr = c->colmax; *bytes = sizeof(float) * m; break;
     case AVD_BUF_COLMIN: *ptr = c->colmin; *bytes = sizeof(float) * m; break;
     case AVD_BUF_HIST1: *ptr = c->hist1; *bytes = sizeof(long long) * kHistBins; break;
@@ -369,13 +375,16 @@ avd_status avd_stage_project(avd_ctx* c, const float* X) {
 
 avd_status avd_stage_select(avd_ctx* c, const float* X, int32_t level, int32_t rank) {
   STAGE_CHECK(c, 5 + level);
-  if (level < 0 || level > 2 || rank < 0 || rank >= c->cfg.world) { set_error("bad level/rank"); return AVD_EINVAL; }
+  if (level < 0 || level > 3 || rank < 0 || rank >= c->cfg.world) { set_error("bad level/rank"); return AVD_EINVAL; }
   if (level == 0) {
+    // local count + globally exchanged [count, overflow] -> same decision on every rank
     unsigned long long cnt = 0;
+    long long gx[2] = {0, 0};
     AVD_CUDA(cudaMemcpyAsync(&cnt, c->cand_cnt, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
+    AVD_CUDA(cudaMemcpyAsync(gx, c->cand_x, sizeof(gx), cudaMemcpyDeviceToHost, c->stream));
     AVD_CUDA(cudaStreamSynchronize(c->stream));
     c->hplan.cand_count = (int64_t)cnt;
-    c->cand_overflow = (int64_t)cnt > c->cand_cap;
+    c->cand_overflow = gx[1] > 0 || gx[0] < c->hplan.n_eff || (c->cfg.flags & AVD_FLAG_STREAM_SELECT);
   }
   AVD_TRY(launch_select(c, X, level, rank));
   c->stage = 6 + level;
@@ -383,15 +392,15 @@ avd_status avd_stage_select(avd_ctx* c, const float* X, int32_t level, int32_t r
 }
 
 avd_status avd_stage_gather(avd_ctx* c, const float* X, int32_t rank, avd_outputs* out) {
-  STAGE_CHECK(c, 8);
+  STAGE_CHECK(c, 9);
   if (!out || !out->top_idx_dev || !out->rho_dev) { set_error("null output arrays"); return AVD_EINVAL; }
   AVD_TRY(launch_gather(c, X, rank, out->top_idx_dev, out->rho_dev));
-  c->stage = 9;
+  c->stage = 10;
   return AVD_OK;
 }
 
 avd_status avd_stage_report(avd_ctx* c, avd_outputs* out) {
-  STAGE_CHECK(c, 9);
+  STAGE_CHECK(c, 10);
   if (!out) { set_error("null outputs"); return AVD_EINVAL; }
   const int64_t m = c->cfg.m;
   const int k = c->k;
@@ -440,7 +449,7 @@ avd_status avd_stage_report(avd_ctx* c, avd_outputs* out) {
   out->n_top_local = c->hplan.sel_local;
   out->top_offset = c->hplan.top_offset;
   out->n_top_global = c->hplan.n_eff;
-  c->stage = 10;
+  c->stage = 11;
   return AVD_OK;
 }
 
@@ -454,7 +463,7 @@ avd_status avd_decompose(avd_ctx* c, const float* X, avd_outputs* out) {
   const avd_status eig = avd_stage_eig(c);
   if (eig != AVD_OK && eig != AVD_ENOCONV) return eig;
   AVD_TRY(avd_stage_project(c, X));
-  for (int lv = 0; lv < 3; ++lv) AVD_TRY(avd_stage_select(c, X, lv, 0));
+  for (int lv = 0; lv < 4; ++lv) AVD_TRY(avd_stage_select(c, X, lv, 0));
   AVD_TRY(avd_stage_gather(c, X, 0, out));
   AVD_TRY(avd_stage_report(c, out));
   return eig;

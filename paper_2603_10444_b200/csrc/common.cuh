@@ -15,6 +15,7 @@ constexpr int kHist3Bins = 128;   // third level: 7 key bits
 constexpr int kGramTile = 128;    // Gram tile edge (rows of A / B panels)
 constexpr int kGramK = 128;       // K rows per pipeline stage (one 128-byte swizzle row of int8)
 constexpr int kMaxP = 112;        // subspace block size cap (two p x p fp64 matrices in smem)
+constexpr int kRedRowsC = 64;     // rows per partial of the m-length p x p reductions (k_eig.cu)
 
 // Device-side "plan2": values decided on the device after the stats exchange.
 struct DevPlan {
@@ -22,6 +23,7 @@ struct DevPlan {
   int64_t cnt_gt;       // #entries with key strictly above the current bin prefix
   int64_t cand_count;   // candidates appended by K2
   int64_t nonfinite;    // #non-finite entries seen by K1
+  int32_t b0;           // candidate threshold bin (from the row-sampled histogram)
   int32_t b1, b2;       // selected first/second level bins
   uint32_t T;           // exact 31-bit key threshold (n_top-th largest |x| bits)
   int32_t empty;        // 1 when n_eff == 0
@@ -50,7 +52,8 @@ struct Ctx {
   float* colmax_part = nullptr;   // [r1][m]
   float* colmin_part = nullptr;   // [r1][m]
   double* sq_part = nullptr;      // [r1 * ncb]
-  double* stats = nullptr;        // [m + 2]: colsum[m], sum x^2, nonfinite count  (exchange)
+  double* stats = nullptr;        // [m + 3]: colsum[m], sum x^2, #nonfinite, #nonzero (exchange)
+  unsigned long long* hist0 = nullptr;  // [4096] exact first-level histogram over candidates (exchange)
   float* colmax = nullptr;        // [m] (exchange MAX)
   float* colmin = nullptr;        // [m] (exchange MIN)
   unsigned long long* hist1 = nullptr;  // [4096] (exchange SUM)
@@ -65,7 +68,8 @@ struct Ctx {
   uint64_t* cand_idx = nullptr;   // [cand_cap]
   unsigned long long* cand_cnt = nullptr;
   int64_t cand_cap = 0;
-  bool cand_overflow = false;
+  long long* cand_x = nullptr;    // [2] exchange SUM: candidate count, overflow flag
+  bool cand_overflow = false;     // true -> K6 streams X instead of the candidate list
   // K3
   long long* gram_i = nullptr;    // [m_pad * m_pad] int64 (upper tiles) (exchange SUM)
   double* G = nullptr;            // [m * m] fp64 symmetric
@@ -76,6 +80,8 @@ struct Ctx {
   double *H = nullptr, *W = nullptr, *theta = nullptr;          // [p][p], [p][p], [p]
   double* red_part = nullptr;     // [n_red_chunks][p*p]
   int n_red = 1;
+  int gemm_ks = 1;                // split-K of Y = G Q
+  double* Ypart = nullptr;        // [gemm_ks][m][p]
   double* resid = nullptr;        // [p]
   double* trace = nullptr;        // [1]
   double* eig_host = nullptr;     // pinned: theta[p] + resid[p]

@@ -3,11 +3,15 @@
 // values of Xc that define the rank-k spike.
 //
 //   Q_0 = orth(random m x p), p = roundup16(k + 8)
-//   repeat:  Y = G Q ; H = Q^T Y ; (W, theta) = eig(H)           (Rayleigh-Ritz)
-//            U = Q W ; Z = Y W (= G U)  ; res_r = ||Z_r - theta_r U_r|| / theta_1, r < k
-//            stop when max res_r <= tol ;  Q = orth(Z)              (SVQB, twice)
-// p x p symmetric eigenproblems are solved by a one-CTA parallel (round-robin) Jacobi.
-// Everything is fp64; every reduction has a fixed order (deterministic).
+//   repeat:  Y = G Q ; H = Q^T Y ; (W, theta) = eig(H)            (Rayleigh-Ritz)
+//            U = Q W ; Z = Y W (= G U) ; res_r = ||Z_r - theta_r U_r|| / theta_1, r < k
+//            stop when max res_r <= tol
+//            Q = orth(G Z)   (two products per orthonormalisation: G^2 U, Cholesky-QR2)
+// p x p problems run in one CTA each: parallel (round-robin) Jacobi for Rayleigh-Ritz,
+// Cholesky + triangular inverse for CholQR; the m-length reductions feeding them are
+// multi-CTA partial sums finished inside those one-CTA kernels in a fixed order.
+// Rank deficiency (G = 0, rank(G) < p, m < p) flags the failing columns, which are re-drawn at
+// random and re-orthonormalised (R11).  Everything is fp64 and deterministic.
 #include <cfloat>
 #include "common.cuh"
 
@@ -58,54 +62,73 @@ __global__ void rand_fill_kernel(double* __restrict__ Q, int64_t m, int p, uint3
   Q[t] = rnd_sym(seed, (uint32_t)(t / p), (uint32_t)c);
 }
 
-// ---------------------------------------------------------------- Y = G Q  (m x m) (m x p)
-constexpr int kGB = 32;  // rows of Y per CTA and K chunk
-template <int PC>  // PC = p / 16 column groups
-__global__ void __launch_bounds__(256) gemm_gq_kernel(const double* __restrict__ G, const double* __restrict__ Q,
-                                                      int64_t m, double* __restrict__ Y) {
+// ---------------------------------------------------------------- Y = G Q  (split-K partials)
+// CTA: 32 rows of Y x all p columns, K range [kz*kchunk, (kz+1)*kchunk); 128 threads, each a
+// 4-row x (p/16)-column register tile.  Ypart[kz][m][p].
+constexpr int kGM = 32;   // rows per CTA
+constexpr int kGK = 32;   // K per smem stage
+template <int PC>
+__global__ void __launch_bounds__(128) gemm_gq_kernel(const double* __restrict__ G, const double* __restrict__ Q,
+                                                      int64_t m, int64_t kchunk, double* __restrict__ Ypart) {
   constexpr int p = PC * 16;
-  __shared__ double sG[kGB][kGB + 1];
-  __shared__ double sQ[kGB][p];
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const int64_t r0 = (int64_t)blockIdx.x * kGB;
-  double acc[2][PC];
+  __shared__ __align__(16) double sGt[kGK][kGM + 2];  // transposed G tile [k][row]
+  __shared__ __align__(16) double sQ[kGK][p];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // rows 4ty..4ty+3, cols tx+16c
+  const int64_t r0 = (int64_t)blockIdx.x * kGM;
+  const int64_t kbeg = (int64_t)blockIdx.y * kchunk;
+  const int64_t kend = min(m, kbeg + kchunk);
+  double acc[4][PC];
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int c = 0; c < PC; ++c) acc[a][c] = 0.0;
-  for (int64_t k0 = 0; k0 < m; k0 += kGB) {
-    for (int t = threadIdx.x; t < kGB * kGB; t += 256) {
-      const int rr = t / kGB, kk = t % kGB;
-      sG[rr][kk] = (r0 + rr < m && k0 + kk < m) ? G[(r0 + rr) * m + k0 + kk] : 0.0;
+  for (int64_t k0 = kbeg; k0 < kend; k0 += kGK) {
+#pragma unroll
+    for (int e = 0; e < (kGM * kGK) / 128; ++e) {
+      const int t = threadIdx.x + e * 128;
+      const int rr = t / kGK, kk = t % kGK;
+      sGt[kk][rr] = (r0 + rr < m && k0 + kk < kend) ? G[(r0 + rr) * m + k0 + kk] : 0.0;
     }
-    for (int t = threadIdx.x; t < kGB * p; t += 256) {
+    for (int t = threadIdx.x; t < kGK * p; t += 128) {
       const int kk = t / p, cc = t % p;
-      sQ[kk][cc] = (k0 + kk < m) ? Q[(k0 + kk) * p + cc] : 0.0;
+      sQ[kk][cc] = (k0 + kk < kend) ? Q[(k0 + kk) * p + cc] : 0.0;
     }
     __syncthreads();
 #pragma unroll 4
-    for (int kk = 0; kk < kGB; ++kk) {
-      const double g0 = sG[ty * 2][kk], g1 = sG[ty * 2 + 1][kk];
+    for (int kk = 0; kk < kGK; ++kk) {
+      const double2 g01 = *reinterpret_cast<const double2*>(&sGt[kk][4 * ty]);
+      const double2 g23 = *reinterpret_cast<const double2*>(&sGt[kk][4 * ty + 2]);
 #pragma unroll
       for (int c = 0; c < PC; ++c) {
         const double qv = sQ[kk][tx + 16 * c];
-        acc[0][c] = fma(g0, qv, acc[0][c]);
-        acc[1][c] = fma(g1, qv, acc[1][c]);
+        acc[0][c] = fma(g01.x, qv, acc[0][c]);
+        acc[1][c] = fma(g01.y, qv, acc[1][c]);
+        acc[2][c] = fma(g23.x, qv, acc[2][c]);
+        acc[3][c] = fma(g23.y, qv, acc[3][c]);
       }
     }
     __syncthreads();
   }
+  double* Yp = Ypart + (int64_t)blockIdx.y * m * p;
 #pragma unroll
-  for (int a = 0; a < 2; ++a) {
-    const int64_t r = r0 + ty * 2 + a;
+  for (int a = 0; a < 4; ++a) {
+    const int64_t r = r0 + 4 * ty + a;
     if (r < m)
 #pragma unroll
-      for (int c = 0; c < PC; ++c) Y[r * p + tx + 16 * c] = acc[a][c];
+      for (int c = 0; c < PC; ++c) Yp[r * p + tx + 16 * c] = acc[a][c];
   }
 }
 
+__global__ void ksum_kernel(const double* __restrict__ part, int nparts, int64_t n, double* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  double s = part[t];
+  for (int q = 1; q < nparts; ++q) s += part[(int64_t)q * n + t];
+  out[t] = s;
+}
+
 // ---------------------------------------------------------------- C = A^T B partials (m x p)
-constexpr int kRedRows = 32;
+constexpr int kRedRows = kRedRowsC;
 __global__ void __launch_bounds__(256) atb_partial_kernel(const double* __restrict__ A, const double* __restrict__ B,
                                                           int64_t m, int p, double* __restrict__ part) {
   extern __shared__ double sm[];
@@ -127,18 +150,11 @@ __global__ void __launch_bounds__(256) atb_partial_kernel(const double* __restri
     part[(int64_t)blockIdx.x * p * p + t] = s;
   }
 }
-__global__ void red_sum_kernel(const double* __restrict__ part, int nparts, int n, double* __restrict__ out) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  double s = 0.0;
-  for (int q = 0; q < nparts; ++q) s += part[(int64_t)q * n + t];
-  out[t] = s;
-}
 
 // ---------------------------------------------------------------- Out = In * M (m x p)(p x p)
-__global__ void __launch_bounds__(256) matpp_kernel(const double* __restrict__ In0, double* __restrict__ Out0,
-                                                    const double* __restrict__ In1, double* __restrict__ Out1,
-                                                    const double* __restrict__ M, int64_t m, int p) {
+// in place allowed (each CTA stages its rows before writing them)
+__global__ void __launch_bounds__(256) matpp_kernel(const double* In0, double* Out0, const double* In1,
+                                                    double* Out1, const double* __restrict__ M, int64_t m, int p) {
   extern __shared__ double sm[];
   double* sM = sm;                 // p*p
   double* sI = sm + p * p;         // 16 rows x p
@@ -184,12 +200,27 @@ __global__ void resid_kernel(const double* __restrict__ Z, const double* __restr
   }
 }
 
+// sum nparts partials of a p x p matrix into smem A (ld), symmetrised
+__device__ void load_sym(const double* __restrict__ part, int nparts, int p, double* A, int ld) {
+  for (int t = threadIdx.x; t < p * p; t += blockDim.x) {
+    const int i = t / p, j = t % p;
+    if (j < i) continue;
+    double s = 0.0, s2 = 0.0;
+    for (int q = 0; q < nparts; ++q) {
+      s += part[(int64_t)q * p * p + i * p + j];
+      s2 += part[(int64_t)q * p * p + j * p + i];
+    }
+    const double v = 0.5 * (s + s2);
+    A[i * ld + j] = v;
+    A[j * ld + i] = v;
+  }
+}
+
 // ---------------------------------------------------------------- p x p symmetric Jacobi
-// mode 0: W = eigenvectors (columns, sorted by eigenvalue desc), evals = eigenvalues
-// mode 1: W = eigvecs * diag(d^-1/2) (0 for d <= 1e-13 d_max), bad[c] = 1 for zeroed columns
-__global__ void __launch_bounds__(512) jacobi_kernel(const double* __restrict__ Ain, int p, int mode,
+// W = eigenvectors (columns sorted by eigenvalue desc), evals = eigenvalues; stats[0] = sweeps
+__global__ void __launch_bounds__(512) jacobi_kernel(const double* __restrict__ part, int nparts, int p,
                                                      double* __restrict__ Wout, double* __restrict__ evals,
-                                                     int* __restrict__ bad) {
+                                                     int* __restrict__ stats) {
   extern __shared__ double sm[];
   const int ld = p + 1;
   double* A = sm;
@@ -200,14 +231,15 @@ __global__ void __launch_bounds__(512) jacobi_kernel(const double* __restrict__ 
   __shared__ double dsh[kMaxP];
   __shared__ int rank_sh[kMaxP];
   const int tid = threadIdx.x, nt = blockDim.x;
+  load_sym(part, nparts, p, A, ld);
   for (int t = tid; t < p * p; t += nt) {
     const int i = t / p, j = t % p;
-    A[i * ld + j] = 0.5 * (Ain[i * p + j] + Ain[j * p + i]);
     V[i * ld + j] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
   const int half = p / 2;
-  for (int sweep = 0; sweep < 40; ++sweep) {
+  int sweep = 0;
+  for (; sweep < 30; ++sweep) {
     if (tid == 0) rotated = 0;
     __syncthreads();
     for (int step = 0; step < p - 1; ++step) {
@@ -231,22 +263,22 @@ __global__ void __launch_bounds__(512) jacobi_kernel(const double* __restrict__ 
         cs[tid][0] = c; cs[tid][1] = s;
       }
       __syncthreads();
-      // rows: A <- J^T A
-      for (int t = tid; t < half * p; t += nt) {
+      for (int t = tid; t < half * p; t += nt) {  // rows: A <- J^T A
         const int i = t / p, col = t % p;
-        const double c = cs[i][0], s = cs[i][1];
+        const double s = cs[i][1];
         if (s == 0.0) continue;
+        const double c = cs[i][0];
         const int P_ = pq[i][0], Q_ = pq[i][1];
         const double ap = A[P_ * ld + col], aq = A[Q_ * ld + col];
         A[P_ * ld + col] = c * ap - s * aq;
         A[Q_ * ld + col] = s * ap + c * aq;
       }
       __syncthreads();
-      // columns: A <- A J, V <- V J
-      for (int t = tid; t < half * p; t += nt) {
+      for (int t = tid; t < half * p; t += nt) {  // columns: A <- A J, V <- V J
         const int i = t / p, row = t % p;
-        const double c = cs[i][0], s = cs[i][1];
+        const double s = cs[i][1];
         if (s == 0.0) continue;
+        const double c = cs[i][0];
         const int P_ = pq[i][0], Q_ = pq[i][1];
         const double ap = A[row * ld + P_], aq = A[row * ld + Q_];
         A[row * ld + P_] = c * ap - s * aq;
@@ -256,16 +288,9 @@ __global__ void __launch_bounds__(512) jacobi_kernel(const double* __restrict__ 
         V[row * ld + Q_] = s * vp + c * vq;
       }
       __syncthreads();
-      if (tid < half && cs[tid][1] != 0.0) {
-        const int P_ = pq[tid][0], Q_ = pq[tid][1];
-        A[P_ * ld + Q_] = 0.0;
-        A[Q_ * ld + P_] = 0.0;
-      }
-      __syncthreads();
     }
     if (!rotated) break;
   }
-  // sort eigenvalues descending (ties by index)
   if (tid < p) dsh[tid] = A[tid * ld + tid];
   __syncthreads();
   if (tid < p) {
@@ -275,18 +300,66 @@ __global__ void __launch_bounds__(512) jacobi_kernel(const double* __restrict__ 
     rank_sh[tid] = rk;
   }
   __syncthreads();
-  double dmax = 0.0;
-  for (int j = 0; j < p; ++j) dmax = fmax(dmax, dsh[j]);
   for (int t = tid; t < p * p; t += nt) {
-    const int row = t / p, i = t % p;  // source column i -> rank_sh[i]
-    double f = 1.0;
-    if (mode == 1) f = (dsh[i] > 1e-13 * dmax && dsh[i] > 0.0) ? 1.0 / sqrt(dsh[i]) : 0.0;
-    Wout[row * p + rank_sh[i]] = V[row * ld + i] * f;
+    const int row = t / p, i = t % p;
+    Wout[row * p + rank_sh[i]] = V[row * ld + i];
   }
-  if (tid < p) {
-    evals[rank_sh[tid]] = dsh[tid];
-    if (mode == 1 && bad) bad[rank_sh[tid]] = (dsh[tid] > 1e-13 * dmax && dsh[tid] > 0.0) ? 0 : 1;
+  if (tid < p) evals[rank_sh[tid]] = dsh[tid];
+  if (tid == 0 && stats) stats[0] = sweep + 1;
+}
+
+// ---------------------------------------------------------------- Cholesky-QR step
+// B = sum(part) (p x p) = R^T R; Rinv = R^{-1} (upper); columns whose pivot is <= 1e-13 of the
+// largest diagonal are flagged bad[c] = 1 and get a zero Rinv column.
+__global__ void __launch_bounds__(512) chol_inv_kernel(const double* __restrict__ part, int nparts, int p,
+                                                       double* __restrict__ Rinv, int* __restrict__ bad) {
+  extern __shared__ double sm[];
+  const int ld = p + 1;
+  double* B = sm;           // becomes R (upper)
+  double* X = sm + p * ld;  // Rinv
+  __shared__ int badsh[kMaxP];
+  __shared__ double dmax;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  load_sym(part, nparts, p, B, ld);
+  __syncthreads();
+  if (tid == 0) {
+    double d = 0.0;
+    for (int i = 0; i < p; ++i) d = fmax(d, B[i * ld + i]);
+    dmax = d;
   }
+  __syncthreads();
+  const double tol = 1e-13 * dmax;
+  for (int j = 0; j < p; ++j) {
+    const double d = B[j * ld + j];
+    const bool ok = d > tol && d > 0.0;
+    const double rjj = ok ? sqrt(d) : 0.0;
+    __syncthreads();  // everyone read d before row j is rewritten
+    if (tid == 0) { badsh[j] = ok ? 0 : 1; B[j * ld + j] = rjj; }
+    for (int k = j + 1 + tid; k < p; k += nt) B[j * ld + k] = ok ? B[j * ld + k] / rjj : 0.0;
+    __syncthreads();
+    const int rem = p - j - 1;
+    for (int t = tid; t < rem * rem; t += nt) {  // trailing update (upper part only)
+      const int i = j + 1 + t / rem, k = j + 1 + t % rem;
+      if (k >= i) B[i * ld + k] -= B[j * ld + i] * B[j * ld + k];
+    }
+    __syncthreads();
+  }
+  // Rinv: solve R x = e_c for every column c (one thread per column, back substitution)
+  for (int c = tid; c < p; c += nt) {
+    for (int i = 0; i < p; ++i) X[i * ld + c] = 0.0;
+    if (!badsh[c]) {
+      X[c * ld + c] = 1.0 / B[c * ld + c];
+      for (int i = c - 1; i >= 0; --i) {
+        if (badsh[i]) continue;
+        double s = 0.0;
+        for (int k = i + 1; k <= c; ++k) s = fma(B[i * ld + k], X[k * ld + c], s);
+        X[i * ld + c] = -s / B[i * ld + i];
+      }
+    }
+  }
+  __syncthreads();
+  for (int t = tid; t < p * p; t += nt) Rinv[t] = X[(t / p) * ld + (t % p)];
+  for (int c = tid; c < p; c += nt) bad[c] = badsh[c];
 }
 
 // V_out[j][r] = sign_r * U[j][r] (r < k), sign making the largest-|.| entry positive
@@ -335,40 +408,36 @@ avd_status launch_gram_finalize(Ctx* c) {
 
 namespace {
 
-avd_status launch_gemm_gq(Ctx* c) {
+// Y = G In (split-K partials summed in a fixed order)
+avd_status gemm_g(Ctx* c, const double* In, double* Out) {
   const int64_t m = c->cfg.m;
-  const unsigned grid = (unsigned)ceil_div(m, kGB);
+  const int ks = c->gemm_ks;
+  const int64_t kchunk = round_up(ceil_div(m, ks), kGK);
+  dim3 grid((unsigned)ceil_div(m, kGM), (unsigned)ks);
   switch (c->p / 16) {
-#define CASE(PC) case PC: gemm_gq_kernel<PC><<<grid, 256, 0, c->stream>>>(c->G, c->Q, m, c->Y); break;
+#define CASE(PC) case PC: gemm_gq_kernel<PC><<<grid, 128, 0, c->stream>>>(c->G, In, m, kchunk, c->Ypart); break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
     default: set_error("unsupported p"); return AVD_EINVAL;
   }
   AVD_LAUNCHED(c);
+  const int64_t n = m * c->p;
+  ksum_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c->stream>>>(c->Ypart, ks, n, Out);
+  AVD_LAUNCHED(c);
   return AVD_OK;
 }
 
-avd_status launch_atb(Ctx* c, const double* A, const double* B, double* out) {
+avd_status atb(Ctx* c, const double* A, const double* B) {
   const int64_t m = c->cfg.m;
   const int p = c->p;
   const size_t sm = 2 * kRedRows * p * sizeof(double);
   AVD_CUDA(cudaFuncSetAttribute(atb_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   atb_partial_kernel<<<c->n_red, 256, sm, c->stream>>>(A, B, m, p, c->red_part);
   AVD_LAUNCHED(c);
-  red_sum_kernel<<<(unsigned)ceil_div(p * p, 256), 256, 0, c->stream>>>(c->red_part, c->n_red, p * p, out);
-  AVD_LAUNCHED(c);
   return AVD_OK;
 }
 
-avd_status launch_jacobi(Ctx* c, const double* A, int mode, double* W, double* ev, int* bad) {
-  const size_t sm = 2 * (size_t)c->p * (c->p + 1) * sizeof(double);
-  AVD_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  jacobi_kernel<<<1, 512, sm, c->stream>>>(A, c->p, mode, W, ev, bad);
-  AVD_LAUNCHED(c);
-  return AVD_OK;
-}
-
-avd_status launch_matpp(Ctx* c, const double* In0, double* Out0, const double* In1, double* Out1, const double* M) {
+avd_status matpp(Ctx* c, const double* In0, double* Out0, const double* In1, double* Out1, const double* M) {
   const int p = c->p;
   const size_t sm = ((size_t)p * p + 16 * p) * sizeof(double);
   AVD_CUDA(cudaFuncSetAttribute(matpp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -377,19 +446,20 @@ avd_status launch_matpp(Ctx* c, const double* In0, double* Out0, const double* I
   return AVD_OK;
 }
 
-// Q <- orth(Z) by SVQB (twice); rank-deficient directions are re-drawn at random.
-avd_status svqb(Ctx* c, double* Z, double* Q, uint32_t seed) {
-  int* bad = reinterpret_cast<int*>(c->resid + c->p);  // scratch after resid[p]
-  double* ev = c->theta + c->p;                         // scratch evals
+// Q <- orth(Y) by Cholesky-QR2; rank-deficient columns are re-drawn at random between passes.
+avd_status orth(Ctx* c, const double* Y, double* Q, uint32_t seed) {
+  int* bad = reinterpret_cast<int*>(c->resid + c->p);
+  const int p = c->p;
+  const size_t sm = 2 * (size_t)p * (p + 1) * sizeof(double);
+  AVD_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   for (int pass = 0; pass < 2; ++pass) {
-    double* src = pass == 0 ? Z : Q;
-    AVD_TRY(launch_atb(c, src, src, c->H));
-    AVD_TRY(launch_jacobi(c, c->H, 1, c->W, ev, bad));
-    AVD_TRY(launch_matpp(c, src, c->U, nullptr, nullptr, c->W));  // U as temp
-    AVD_CUDA(cudaMemcpyAsync(Q, c->U, sizeof(double) * c->cfg.m * c->p, cudaMemcpyDeviceToDevice, c->stream));
+    const double* src = pass == 0 ? Y : Q;
+    AVD_TRY(atb(c, src, src));
+    chol_inv_kernel<<<1, 512, sm, c->stream>>>(c->red_part, c->n_red, p, c->W, bad);
+    AVD_LAUNCHED(c);
+    AVD_TRY(matpp(c, src, Q, nullptr, nullptr, c->W));
     if (pass == 0) {
-      rand_fill_kernel<<<(unsigned)ceil_div(c->cfg.m * c->p, 256), 256, 0, c->stream>>>(Q, c->cfg.m, c->p,
-                                                                                         seed, bad);
+      rand_fill_kernel<<<(unsigned)ceil_div(c->cfg.m * p, 256), 256, 0, c->stream>>>(Q, c->cfg.m, p, seed, bad);
       AVD_LAUNCHED(c);
     }
   }
@@ -402,19 +472,23 @@ avd_status run_eig(Ctx* c) {
   const int64_t m = c->cfg.m;
   const int p = c->p, k = c->k;
   const uint32_t seed = (uint32_t)(c->cfg.seed ^ (c->cfg.seed >> 32)) * 2654435761u + 12345u;
+  int* jstats = reinterpret_cast<int*>(c->theta + p);
+  const size_t jsm = 2 * (size_t)p * (p + 1) * sizeof(double);
+  AVD_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jsm));
   rand_fill_kernel<<<(unsigned)ceil_div(m * p, 256), 256, 0, c->stream>>>(c->Z, m, p, seed, nullptr);
   AVD_LAUNCHED(c);
-  AVD_TRY(svqb(c, c->Z, c->Q, seed + 1));
-  const int max_it = c->cfg.max_iters > 0 ? c->cfg.max_iters : 200;
-  const double tol = c->cfg.eig_tol > 0 ? c->cfg.eig_tol : 1e-10;
+  AVD_TRY(orth(c, c->Z, c->Q, seed + 1));
+  const int max_it = c->cfg.max_iters > 0 ? c->cfg.max_iters : 100;
+  const double tol = c->cfg.eig_tol > 0 ? c->cfg.eig_tol : 1e-9;
   int it = 0;
   double maxres = 0.0;
   bool conv = false;
   for (it = 1; it <= max_it; ++it) {
-    AVD_TRY(launch_gemm_gq(c));                              // Y = G Q
-    AVD_TRY(launch_atb(c, c->Q, c->Y, c->H));                // H = Q^T Y
-    AVD_TRY(launch_jacobi(c, c->H, 0, c->W, c->theta, nullptr));
-    AVD_TRY(launch_matpp(c, c->Y, c->Z, c->Q, c->U, c->W));  // Z = Y W, U = Q W
+    AVD_TRY(gemm_g(c, c->Q, c->Y));                         // Y = G Q
+    AVD_TRY(atb(c, c->Q, c->Y));                            // H = Q^T Y (partials)
+    jacobi_kernel<<<1, 512, jsm, c->stream>>>(c->red_part, c->n_red, p, c->W, c->theta, jstats);
+    AVD_LAUNCHED(c);
+    AVD_TRY(matpp(c, c->Y, c->Z, c->Q, c->U, c->W));        // Z = Y W, U = Q W
     resid_kernel<<<k, 256, 0, c->stream>>>(c->Z, c->U, c->theta, m, p, c->resid);
     AVD_LAUNCHED(c);
     AVD_CUDA(cudaMemcpyAsync(c->eig_host, c->theta, sizeof(double) * p, cudaMemcpyDeviceToHost, c->stream));
@@ -425,7 +499,8 @@ avd_status run_eig(Ctx* c) {
     if (!(c->eig_host[0] > 0.0)) { maxres = 0.0; conv = true; break; }  // G == 0: nothing to iterate
     if (maxres <= tol) { conv = true; break; }
     if (it == max_it) break;
-    AVD_TRY(svqb(c, c->Z, c->Q, seed + 7919u * (uint32_t)it));
+    AVD_TRY(gemm_g(c, c->Z, c->Y));                         // Y = G Z = G^2 U
+    AVD_TRY(orth(c, c->Y, c->Q, seed + 7919u * (uint32_t)it));
   }
   c->iters = std::min(it, max_it);
   c->max_resid = maxres;

@@ -132,18 +132,22 @@ __global__ void __launch_bounds__(kProjThreads) project_kernel(
 }
 
 // energy[0..4) = sum S^2, T^2, ST, xc^2 ; energy[4..4+KP) = column sums of P
+// one CTA per output value: strided partial sums + fixed-order tree (deterministic)
 __global__ void project_reduce_kernel(const double* __restrict__ en_part, const double* __restrict__ colsumP_part,
                                       int nparts, int KP, double* __restrict__ energy) {
-  const int t = threadIdx.x;
-  if (t < 4) {
-    double s = 0.0;
-    for (int q = 0; q < nparts; ++q) s += en_part[(int64_t)q * 4 + t];
-    energy[t] = s;
-  } else if (t < 4 + KP) {
-    double s = 0.0;
-    for (int q = 0; q < nparts; ++q) s += colsumP_part[(int64_t)q * KP + (t - 4)];
-    energy[t] = s;
+  __shared__ double sh[256];
+  const int o = blockIdx.x;
+  const double* src = o < 4 ? en_part + o : colsumP_part + (o - 4);
+  const int stride = o < 4 ? 4 : KP;
+  double s = 0.0;
+  for (int q = threadIdx.x; q < nparts; q += 256) s += src[(int64_t)q * stride];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
   }
+  if (threadIdx.x == 0) energy[o] = sh[0];
 }
 
 }  // namespace
@@ -161,7 +165,8 @@ avd_status launch_project(Ctx* c, const float* X) {
     default: set_error("unsupported k_pad"); return AVD_EINVAL;
   }
   AVD_LAUNCHED(c);
-  project_reduce_kernel<<<1, 128, 0, c->stream>>>(c->en_part, c->colsumP_part, c->n_proj_ctas, c->k_pad, c->energy);
+  project_reduce_kernel<<<4 + c->k_pad, 256, 0, c->stream>>>(c->en_part, c->colsumP_part, c->n_proj_ctas, c->k_pad,
+                                                              c->energy);
   AVD_LAUNCHED(c);
   return AVD_OK;
 }

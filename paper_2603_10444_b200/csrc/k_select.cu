@@ -36,23 +36,24 @@ __device__ __forceinline__ bool fetch(int64_t t, const uint32_t* __restrict__ ck
   }
 }
 
-// level 0: hist2 of bits [18:7] over key>>19 == b1 ; level 1: hist3 of bits [6:0] over key>>7 == prefix
+// radix level 0: bits [30:19] of every candidate (exact counts);
+// level 1: bits [18:7] over key>>19 == b1 ; level 2: bits [6:0] over key>>7 == (b1, b2)
 template <bool FROM_X>
 __global__ void __launch_bounds__(kSelThreads) hist_kernel(int level, int64_t n, const uint32_t* __restrict__ ckey,
                                                            const uint64_t* __restrict__ cidx, const float* __restrict__ X,
                                                            const DevPlan* __restrict__ dp, unsigned long long* __restrict__ out) {
   __shared__ unsigned int sh[kHistBins];
-  const int nb = level == 0 ? kHistBins : kHist3Bins;
+  const int nb = level < 2 ? kHistBins : kHist3Bins;
   for (int b = threadIdx.x; b < nb; b += kSelThreads) sh[b] = 0;
   __syncthreads();
-  const uint32_t pre = level == 0 ? (uint32_t)dp->b1 : (((uint32_t)dp->b1 << 12) | (uint32_t)dp->b2);
-  const int shiftp = level == 0 ? 19 : 7;
+  const uint32_t pre = level == 0 ? 0u : (level == 1 ? (uint32_t)dp->b1 : (((uint32_t)dp->b1 << 12) | (uint32_t)dp->b2));
+  const int shiftp = level == 0 ? 31 : (level == 1 ? 19 : 7);
   for (int64_t t = (int64_t)blockIdx.x * kSelThreads + threadIdx.x; t < n; t += (int64_t)gridDim.x * kSelThreads) {
     uint32_t key;
     uint64_t li;
     if (!fetch<FROM_X>(t, ckey, cidx, X, 0, key, li)) continue;
     if ((key >> shiftp) != pre) continue;
-    const uint32_t bin = level == 0 ? ((key >> 7) & 0xFFFu) : (key & 0x7Fu);
+    const uint32_t bin = level == 0 ? (key >> 19) : (level == 1 ? ((key >> 7) & 0xFFFu) : (key & 0x7Fu));
     atomicAdd(&sh[bin], 1u);
   }
   __syncthreads();
@@ -60,10 +61,10 @@ __global__ void __launch_bounds__(kSelThreads) hist_kernel(int level, int64_t n,
     if (sh[b]) atomicAdd(&out[b], (unsigned long long)sh[b]);
 }
 
-// Find the bin of the next level that contains the n_eff-th largest key (one warp).
+// Find the bin of radix level `level` that contains the n_eff-th largest key (one warp).
 __global__ void find_bin_kernel(int level, const unsigned long long* __restrict__ h, DevPlan* __restrict__ dp) {
   const int lane = threadIdx.x;
-  const int nb = level == 0 ? kHistBins : kHist3Bins;
+  const int nb = level < 2 ? kHistBins : kHist3Bins;
   const int per = nb / 32;
   const long long need = dp->n_eff - dp->cnt_gt;  // rank inside the current prefix (>= 1)
   const int hi = nb - 1 - lane * per;
@@ -84,6 +85,9 @@ __global__ void find_bin_kernel(int level, const unsigned long long* __restrict_
       cum += h[b];
     }
     if (level == 0) {
+      dp->b1 = b;
+      dp->cnt_gt = (long long)cum;
+    } else if (level == 1) {
       dp->b2 = b;
       dp->cnt_gt = dp->cnt_gt + (long long)cum;
     } else {
@@ -299,26 +303,25 @@ __global__ void agg_reduce_kernel(const double* __restrict__ part, int nparts, d
 
 }  // namespace
 
-// level 0: hist2 ; level 1: find b2, hist3 ; level 2: find T, mark, publish counts
+// level 0: radix level 0 histogram ; level 1: find b1, level-1 histogram ;
+// level 2: find b2, level-2 histogram ; level 3: find T, mark, publish per-rank counts
 avd_status launch_select(Ctx* c, const float* X, int level, int rank) {
   const bool fromX = c->cand_overflow;
   const int64_t n = fromX ? c->cfg.l_local * c->cfg.m : c->hplan.cand_count;
   const int64_t base = c->cfg.row_offset * c->cfg.m;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, kSelThreads), 4LL * c->num_sms));
-  if (level == 0) {
-    AVD_CUDA(cudaMemsetAsync(c->hist2, 0, sizeof(unsigned long long) * kHistBins, c->stream));
-    if (fromX) hist_kernel<true><<<grid, kSelThreads, 0, c->stream>>>(0, n, nullptr, nullptr, X, c->dplan, c->hist2);
-    else hist_kernel<false><<<grid, kSelThreads, 0, c->stream>>>(0, n, c->cand_key, c->cand_idx, nullptr, c->dplan, c->hist2);
-    AVD_LAUNCHED(c);
-  } else if (level == 1) {
-    find_bin_kernel<<<1, 32, 0, c->stream>>>(0, c->hist2, c->dplan);
-    AVD_LAUNCHED(c);
-    AVD_CUDA(cudaMemsetAsync(c->hist3, 0, sizeof(unsigned long long) * kHist3Bins, c->stream));
-    if (fromX) hist_kernel<true><<<grid, kSelThreads, 0, c->stream>>>(1, n, nullptr, nullptr, X, c->dplan, c->hist3);
-    else hist_kernel<false><<<grid, kSelThreads, 0, c->stream>>>(1, n, c->cand_key, c->cand_idx, nullptr, c->dplan, c->hist3);
+  if (level <= 2) {
+    unsigned long long* h = level == 0 ? c->hist0 : (level == 1 ? c->hist2 : c->hist3);
+    if (level > 0) {
+      find_bin_kernel<<<1, 32, 0, c->stream>>>(level - 1, level == 1 ? c->hist0 : c->hist2, c->dplan);
+      AVD_LAUNCHED(c);
+    }
+    AVD_CUDA(cudaMemsetAsync(h, 0, sizeof(unsigned long long) * (level < 2 ? kHistBins : kHist3Bins), c->stream));
+    if (fromX) hist_kernel<true><<<grid, kSelThreads, 0, c->stream>>>(level, n, nullptr, nullptr, X, c->dplan, h);
+    else hist_kernel<false><<<grid, kSelThreads, 0, c->stream>>>(level, n, c->cand_key, c->cand_idx, nullptr, c->dplan, h);
     AVD_LAUNCHED(c);
   } else {
-    find_bin_kernel<<<1, 32, 0, c->stream>>>(1, c->hist3, c->dplan);
+    find_bin_kernel<<<1, 32, 0, c->stream>>>(2, c->hist3, c->dplan);
     AVD_LAUNCHED(c);
     AVD_CUDA(cudaMemsetAsync(c->bm_sel, 0, sizeof(uint32_t) * c->nwords, c->stream));
     AVD_CUDA(cudaMemsetAsync(c->bm_tie, 0, sizeof(uint32_t) * c->nwords, c->stream));

@@ -4,7 +4,7 @@
 //     a deterministic dither u ~ U[0,1): q = floor(x_c 2^shift_j + u)  (|q| <= 2^(7 nd - 1));
 //     q is written as nd balanced base-128 int8 digits into TRANSPOSED planes
 //     D_d[j][i] (K-major operands of the tcgen05 kind::i8 Gram);
-//   * entries whose |x| bit pattern falls in a first-level bin >= b1 are appended as
+//   * entries whose |x| bit pattern falls in a first-level bin >= b0 are appended as
 //     (key, global linear index) candidates of E_top.
 // One read of X (4 B/entry), nd bytes written per entry.
 #include "common.cuh"
@@ -35,54 +35,61 @@ __global__ void __launch_bounds__(kSplitThreads) split_kernel(
     uint32_t* __restrict__ cand_key, uint64_t* __restrict__ cand_idx,
     unsigned long long* __restrict__ cand_cnt, int64_t cand_cap) {
   __shared__ uint32_t sD[ND][kSplitCols * kSW];
+  __shared__ uint32_t srow[kSplitRows];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t i0 = (int64_t)blockIdx.x * kSplitRows;
   const int64_t j0 = (int64_t)blockIdx.y * kSplitCols;
   const int jl = (warp & 1) * 32 + lane;
   const int64_t j = j0 + jl;
   const int rg = warp >> 1;  // 32-row group
-  const uint32_t b1 = (uint32_t)dp->b1;
+  if (threadIdx.x < kSplitRows)
+    srow[threadIdx.x] = mix32((uint32_t)(row_offset + i0 + threadIdx.x) * 0x9E3779B1u ^ seed32);
+  const uint32_t b0 = (uint32_t)dp->b0;
   const bool colok = j < m;
   const double muj = colok ? mu[j] : 0.0;
   const double scale = colok ? ldexp(1.0, shift[j]) : 0.0;
+  const uint32_t colh = mix32((uint32_t)j ^ 0x68E31DA4u);
+  // all 32 loads of this thread in flight at once
+  float xs[32];
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    const int64_t i = i0 + rg * 32 + r;
+    xs[r] = (colok && i < l_local) ? __ldcs(X + i * m + j) : 0.f;
+  }
+  __syncthreads();
 
-#pragma unroll 1
+#pragma unroll
   for (int t = 0; t < 8; ++t) {
     uint32_t packed[ND];
 #pragma unroll
     for (int d = 0; d < ND; ++d) packed[d] = 0;
-    float xs[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int64_t i = i0 + rg * 32 + t * 4 + u;
-      xs[u] = (colok && i < l_local) ? __ldcs(X + i * m + j) : 0.f;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t i = i0 + rg * 32 + t * 4 + u;
+      const int rl = rg * 32 + t * 4 + u;
+      const int64_t i = i0 + rl;
       const bool ok = colok && i < l_local;
-      const float x = xs[u];
+      const float x = xs[t * 4 + u];
       const uint32_t key = __float_as_uint(x) & 0x7FFFFFFFu;
-      const uint64_t gidx = (uint64_t)(row_offset + i) * (uint64_t)m + (uint64_t)j;
       // ---- candidate append (warp aggregated)
-      const bool cand = ok && key != 0 && key < 0x7F800000u && (key >> 19) >= b1;
+      const bool cand = ok && key != 0 && key < 0x7F800000u && (key >> 19) >= b0;
       const uint32_t ballot = __ballot_sync(0xFFFFFFFFu, cand);
       if (ballot) {
+        const int ldr = __ffs(ballot) - 1;
         unsigned long long base = 0;
-        if (lane == __ffs(ballot) - 1) base = atomicAdd(cand_cnt, (unsigned long long)__popc(ballot));
-        base = __shfl_sync(0xFFFFFFFFu, base, __ffs(ballot) - 1);
+        if (lane == ldr) base = atomicAdd(cand_cnt, (unsigned long long)__popc(ballot));
+        base = __shfl_sync(0xFFFFFFFFu, base, ldr);
         if (cand) {
           const unsigned long long pos = base + __popc(ballot & ((1u << lane) - 1u));
           if (pos < (unsigned long long)cand_cap) {
             cand_key[pos] = key;
-            cand_idx[pos] = gidx;
+            cand_idx[pos] = (uint64_t)(row_offset + i) * (uint64_t)m + (uint64_t)j;
           }
         }
       }
       // ---- dithered fixed-point digits of the centred entry
       if (ok) {
         const double xc = (double)x - muj;
-        const uint32_t h = mix32((uint32_t)gidx ^ mix32((uint32_t)(gidx >> 32) ^ seed32));
+        const uint32_t h = mix32(srow[rl] ^ colh);
         const double dith = (double)(h >> 8) * (1.0 / 16777216.0);
         int32_t q = (int32_t)floor(fma(xc, scale, dith));
         int32_t dg[ND];
@@ -112,6 +119,13 @@ __global__ void __launch_bounds__(kSplitThreads) split_kernel(
   }
 }
 
+// exchange slot for the global candidate decision: [count, overflowed]
+__global__ void cand_publish_kernel(const unsigned long long* __restrict__ cnt, int64_t cap,
+                                    long long* __restrict__ out) {
+  out[0] = (long long)*cnt;
+  out[1] = (long long)(*cnt > (unsigned long long)cap ? 1 : 0);
+}
+
 }  // namespace
 
 avd_status launch_split(Ctx* c, const float* X) {
@@ -126,6 +140,8 @@ avd_status launch_split(Ctx* c, const float* X) {
     split_kernel<3><<<grid, kSplitThreads, 0, c->stream>>>(
         X, c->cfg.l_local, c->cfg.m, c->m_pad, c->l_pad, c->cfg.row_offset, c->mu, c->shift, seed32,
         c->digits, c->dplan, c->cand_key, c->cand_idx, c->cand_cnt, c->cand_cap);
+  AVD_LAUNCHED(c);
+  cand_publish_kernel<<<1, 1, 0, c->stream>>>(c->cand_cnt, c->cand_cap, c->cand_x);
   AVD_LAUNCHED(c);
   return AVD_OK;
 }

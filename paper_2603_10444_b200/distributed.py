@@ -10,7 +10,8 @@ module all-reduces exactly the exchange buffers the header lists (SURVEY.md §2.
   gram    : the exact int64 Gram partials (SUM i64)  -> identical G on every rank
   eig     : replicated (same G, same seed -> bit-identical V_k, sigma_k on every rank)
   project : elementwise energy sums + column sums of P (SUM f64)
-  select  : histogram levels 2, 3 (SUM i64), per-rank sel/tie counts (SUM = all-gather)
+  gram    : + candidate count / overflow flag (SUM i64) -> same candidate-vs-stream decision
+  select  : radix histograms of |x| bits (SUM i64), per-rank sel/tie counts (SUM = all-gather)
   gather  : rho aggregates (SUM f64)
 
 The exchange logic is written against a tiny `Comm` interface so the CPU tests can drive the
@@ -28,11 +29,12 @@ from .api import Decomposer, Result
 EXCHANGES = {
     "stats": [("STATS", torch.float64, "sum"), ("COLMAX", torch.float32, "max"),
               ("COLMIN", torch.float32, "min"), ("HIST1", torch.int64, "sum")],
-    "gram": [("GRAM", torch.int64, "sum")],
+    "gram": [("GRAM", torch.int64, "sum"), ("CAND", torch.int64, "sum")],
     "project": [("ENERGY", torch.float64, "sum")],
-    "select0": [("HIST2", torch.int64, "sum")],
-    "select1": [("HIST3", torch.int64, "sum")],
-    "select2": [("TIES", torch.int64, "sum")],
+    "select0": [("HIST0", torch.int64, "sum")],
+    "select1": [("HIST2", torch.int64, "sum")],
+    "select2": [("HIST3", torch.int64, "sum")],
+    "select3": [("TIES", torch.int64, "sum")],
     "gather": [("AGG", torch.float64, "sum")],
 }
 
@@ -76,7 +78,7 @@ def run_stages(backend, comm, X) -> object:
     backend.stage_eig()
     backend.stage_project(X)
     exchange("project")
-    for lv in range(3):
+    for lv in range(4):
         backend.stage_select(X, lv, rank)
         exchange(f"select{lv}")
     backend.stage_gather(X, rank)

@@ -118,3 +118,26 @@ def test_deterministic_and_host_path(cuda_device):
 def test_generator_bit_identical_on_cuda(cuda_device):
     spec = SynthSpec(1000, 96, seed=3)
     assert torch.equal(generate(spec), generate(spec, device="cuda").cpu())
+
+
+@pytest.mark.parametrize("flags", [0, 1])
+def test_selection_paths_agree(cuda_device, flags):
+    """Candidate-list selection and the streaming-X fallback give the oracle's exact E_top,
+    including massive ties (two tied columns) and a tie quota inside the threshold key."""
+    spec = SynthSpec(2048, 192, seed=21, f_mean=0.8)
+    X = generate(spec)
+    X[:, 5] = 40.0    # 2048 tied entries of the largest magnitude (|E_top| = 393)
+    X[:, 77] = -40.0  # same magnitude, opposite sign
+    o = O.decompose(X.numpy())
+    g = _gpu(X, flags=flags)
+    np.testing.assert_array_equal(g["top_idx"], o["top_idx"])
+    assert np.max(np.abs(g["rho"] - o["rho"])) <= 1e-3
+
+
+def test_high_top_frac(cuda_device):
+    """|E_top| = 30% of the entries: b0 falls to the bottom of the sampled histogram."""
+    X = generate(SynthSpec(1024, 128, seed=4))
+    o = O.decompose(X.numpy(), n_top=int(0.3 * 1024 * 128))
+    g = _gpu(X, n_top=int(0.3 * 1024 * 128))
+    np.testing.assert_array_equal(g["top_idx"], o["top_idx"])
+    assert np.max(np.abs(g["rho"] - o["rho"])) <= 1e-3
