@@ -355,7 +355,8 @@ def main():
                    "parallelism": f"row-shard x{world}"},
         "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches),
         "roofline": roofline, "stage_ms": stage_ms, "streaming_roofline": stream_roof,
-        "eig_iters": res.iters, "eig_max_resid": res.max_resid,
+        "eig_iters": res.iters, "eig_max_resid": res.max_resid, "eig_rr_checks": res.rr_checks,
+        "eig_jacobi_sweeps": res.jacobi_sweeps,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(spec, 2048, 512)

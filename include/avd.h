@@ -107,6 +107,8 @@ typedef struct {
   double trace_g;          /* tr(G) = ||Xc||_F^2                                             */
   int32_t iters;           /* subspace iterations used                                       */
   double max_resid;        /* max_r<k ||G v_r - lambda_r v_r|| / lambda_1                     */
+  int32_t rr_checks;      /* Rayleigh-Ritz checks of the eigensolver (diagnostic)           */
+  int32_t jacobi_sweeps;   /* sweeps of the last p x p Jacobi (diagnostic)                   */
 } avd_outputs;
 
 typedef struct avd_ctx avd_ctx;

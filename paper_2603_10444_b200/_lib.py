@@ -50,7 +50,8 @@ class avd_outputs(ctypes.Structure):
                 ("cross_el", ctypes.c_double * 3), ("colmean_absmax", ctypes.c_double * 2),
                 ("rho_mean_aggr", ctypes.c_double * 4), ("rho_energy_aggr", ctypes.c_double * 3),
                 ("sigma_next", ctypes.c_double), ("trace_g", ctypes.c_double),
-                ("iters", ctypes.c_int32), ("max_resid", ctypes.c_double)]
+                ("iters", ctypes.c_int32), ("max_resid", ctypes.c_double),
+                ("rr_checks", ctypes.c_int32), ("jacobi_sweeps", ctypes.c_int32)]
 
 
 _lib = None

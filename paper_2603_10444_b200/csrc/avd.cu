@@ -69,12 +69,13 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   C->k_pad = (int)(((k + 15) / 16) * 16);
   C->nd = nd;
   C->m_pad = round_up(m, kGramTile);
+  C->m_pad32 = round_up(m, 32);
   C->l_pad = round_up(cfg->l_local, kGramK);
   const int64_t ll = cfg->l_local;
   const int ncb = (int)ceil_div(m, 256LL * ((m % 4 == 0) ? 4 : 1));
   C->r1 = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(4LL * C->num_sms, ncb), ceil_div(ll, 4)));
   C->cand_cap = std::min<int64_t>(ll * m, std::max<int64_t>(4 * n_top, 1 << 20));
-  C->n_red = (int)ceil_div(m, kRedRowsC);
+  C->n_red = (int)ceil_div(m, kRedRowsC);  // partials of the m-length p x p reductions
   C->gemm_ks = (int)std::max<int64_t>(1, std::min<int64_t>(8, ceil_div(2LL * C->num_sms, ceil_div(m, 32))));
   C->n_proj_ctas = (int)ceil_div(ll, 32);
   C->nwords = ceil_div(ll * m, 32);
@@ -128,6 +129,9 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   L.add(sizeof(unsigned long long) * kHistBins);// 43 hist0
   L.add(sizeof(long long) * 2);                 // 44 cand_x
   L.add(sizeof(double) * C->gemm_ks * m * p);   // 45 Ypart
+  L.add(sizeof(float) * 2 * C->l_pad * (((C->k_pad + 31) / 32) * 32));   // 46 P_hl
+  L.add(sizeof(float) * 2 * C->k_pad * round_up(m, 32));                 // 47 Vt_hl
+  L.add(sizeof(float) * 2 * C->m_pad * (((C->k_pad + 31) / 32) * 32));   // 48 V_hl
   plan->workspace_bytes = L.total;
   if (lay) *lay = L;
   return AVD_OK;
@@ -243,6 +247,7 @@ avd_status avd_create(const avd_config* cfg, avd_ctx** out) {
   BIND(en_part, double*); BIND(colsumP_part, double*); BIND(energy, double*); BIND(hist2, unsigned long long*);
   BIND(hist3, unsigned long long*); BIND(ties, long long*); BIND(bm_sel, uint32_t*); BIND(bm_tie, uint32_t*);
   BIND(blk_cnt, int64_t*); BIND(agg, double*); BIND(agg_part, double*); BIND(report, double*); BIND(hist0, unsigned long long*); BIND(cand_x, long long*); BIND(Ypart, double*);
+  BIND(P_hl, float*); BIND(Vt_hl, float*); BIND(V_hl, float*);
 #undef BIND
   if (cudaMallocHost(&c->eig_host, sizeof(double) * 4 * kMaxP) != cudaSuccess) {
     cudaGetLastError();
@@ -251,6 +256,7 @@ avd_status avd_create(const avd_config* cfg, avd_ctx** out) {
     set_error("cudaMallocHost failed");
     return AVD_ENOMEM;
   }
+  cudaMemset(c->P_hl, 0, sizeof(float) * 2 * c->l_pad * (((c->k_pad + 31) / 32) * 32));
   st = gram_make_tmap(c);
   if (st != AVD_OK) { cudaFree(c->ws); cudaFreeHost(c->eig_host); delete c; return st; }
   c->stage = 0;
@@ -446,6 +452,8 @@ avd_status avd_stage_report(avd_ctx* c, avd_outputs* out) {
   out->trace_g = trace;
   out->iters = c->iters;
   out->max_resid = c->max_resid;
+  out->rr_checks = c->rr_count;
+  out->jacobi_sweeps = c->jacobi_sweeps;
   out->n_top_local = c->hplan.sel_local;
   out->top_offset = c->hplan.top_offset;
   out->n_top_global = c->hplan.n_eff;

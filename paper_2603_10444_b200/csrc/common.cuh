@@ -15,7 +15,7 @@ constexpr int kHist3Bins = 128;   // third level: 7 key bits
 constexpr int kGramTile = 128;    // Gram tile edge (rows of A / B panels)
 constexpr int kGramK = 128;       // K rows per pipeline stage (one 128-byte swizzle row of int8)
 constexpr int kMaxP = 112;        // subspace block size cap (two p x p fp64 matrices in smem)
-constexpr int kRedRowsC = 64;     // rows per partial of the m-length p x p reductions (k_eig.cu)
+constexpr int kRedRowsC = 256;    // rows per partial of the m-length p x p reductions (k_eig.cu)
 
 // Device-side "plan2": values decided on the device after the stats exchange.
 struct DevPlan {
@@ -89,10 +89,16 @@ struct Ctx {
   double* sigma = nullptr;        // [k]
   float* V32 = nullptr;           // [m][k_pad] fp32 copy for K5/K8
   int iters = 0;
+  int rr_count = 0;               // Rayleigh-Ritz checks in the last solve
+  int jacobi_sweeps = 0;          // sweeps of the last Rayleigh-Ritz Jacobi
   double max_resid = 0;
   double sigma_next = 0;
   // K5/K8
   float* P = nullptr;             // [l_local][k_pad]
+  float* P_hl = nullptr;          // [2][l_pad][KP32] tf32 hi / lo planes of P (K8 A operand)
+  float* Vt_hl = nullptr;         // [2*k_pad][m_pad32] tf32 hi / lo of V^T (K5 B operand)
+  float* V_hl = nullptr;          // [2][m_pad][KP32] tf32 hi / lo of V (K8 B operand)
+  int64_t m_pad32 = 0;
   double* en_part = nullptr;      // [n_proj_ctas][4]
   double* colsumP_part = nullptr; // [n_proj_ctas][k_pad]
   int n_proj_ctas = 1;
@@ -145,8 +151,8 @@ void set_error(const std::string& msg);
     if (s__ != AVD_OK) return s__;           \
   } while (0)
 
-inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
-inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
 // ---------------------------------------------------------------- kernels (per file)
 avd_status launch_stats(Ctx* c, const float* X);           // k_stats.cu
@@ -161,6 +167,8 @@ avd_status launch_project(Ctx* c, const float* X);         // k_project.cu
 avd_status launch_select(Ctx* c, const float* X, int level, int rank);  // k_select.cu
 avd_status launch_gather(Ctx* c, const float* X, int rank, int64_t* top_idx, double* rho);
 avd_status launch_project_reduce(Ctx* c);                  // k_project.cu
+bool project_tc_supported(const Ctx* c, const float* X); // k_project_tc.cu
+avd_status launch_project_tc(Ctx* c, const float* X);    // k_project_tc.cu
 avd_status launch_agg_reduce(Ctx* c);                      // k_select.cu
 
 }  // namespace avd

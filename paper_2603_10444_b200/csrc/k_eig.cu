@@ -128,27 +128,43 @@ __global__ void ksum_kernel(const double* __restrict__ part, int nparts, int64_t
 }
 
 // ---------------------------------------------------------------- C = A^T B partials (m x p)
-constexpr int kRedRows = kRedRowsC;
+// CTA: kRedRowsC rows in 64-row smem chunks; thread owns PC^2 outputs (p^2 = 256 PC^2).
+constexpr int kRedChunk = 64;
+template <int PC>
 __global__ void __launch_bounds__(256) atb_partial_kernel(const double* __restrict__ A, const double* __restrict__ B,
-                                                          int64_t m, int p, double* __restrict__ part) {
+                                                          int64_t m, double* __restrict__ part) {
+  constexpr int p = PC * 16;
+  constexpr int U = PC * PC;
   extern __shared__ double sm[];
   double* sA = sm;
-  double* sB = sm + kRedRows * p;
-  const int64_t r0 = (int64_t)blockIdx.x * kRedRows;
-  for (int t = threadIdx.x; t < kRedRows * p; t += 256) {
-    const int rr = t / p;
-    const bool ok = r0 + rr < m;
-    sA[t] = ok ? A[r0 * p + t] : 0.0;
-    sB[t] = ok ? B[r0 * p + t] : 0.0;
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < p * p; t += 256) {
-    const int i = t / p, j = t % p;
-    double s = 0.0;
+  double* sB = sm + kRedChunk * p;
+  double acc[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) acc[u] = 0.0;
+  const int64_t rbase = (int64_t)blockIdx.x * kRedRowsC;
+  for (int ch = 0; ch < kRedRowsC / kRedChunk; ++ch) {
+    const int64_t r0 = rbase + ch * kRedChunk;
+    if (r0 >= m) break;
+    __syncthreads();
+    for (int t = threadIdx.x; t < kRedChunk * p; t += 256) {
+      const int rr = t / p;
+      const bool ok = r0 + rr < m;
+      sA[t] = ok ? A[r0 * p + t] : 0.0;
+      sB[t] = ok ? B[r0 * p + t] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = threadIdx.x + 256 * u;
+      const int i = t / p, j = t % p;
+      double s = acc[u];
 #pragma unroll 8
-    for (int rr = 0; rr < kRedRows; ++rr) s = fma(sA[rr * p + i], sB[rr * p + j], s);
-    part[(int64_t)blockIdx.x * p * p + t] = s;
+      for (int rr = 0; rr < kRedChunk; ++rr) s = fma(sA[rr * p + i], sB[rr * p + j], s);
+      acc[u] = s;
+    }
   }
+#pragma unroll
+  for (int u = 0; u < U; ++u) part[(int64_t)blockIdx.x * p * p + threadIdx.x + 256 * u] = acc[u];
 }
 
 // ---------------------------------------------------------------- Out = In * M (m x p)(p x p)
@@ -198,6 +214,20 @@ __global__ void resid_kernel(const double* __restrict__ Z, const double* __restr
     const double t0 = fabs(theta[0]) > 0 ? fabs(theta[0]) : 1.0;
     res[r] = sqrt(sh[0]) / t0;
   }
+}
+
+// out[t] = sum_q part[q][t] in a fixed order (independent loads, unrolled)
+__global__ void psum_kernel(const double* __restrict__ part, int nparts, int n, double* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int q = 0;
+  for (; q + 8 <= nparts; q += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] += part[(int64_t)(q + u) * n + t];
+  }
+  for (; q < nparts; ++q) a[0] += part[(int64_t)q * n + t];
+  out[t] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
 }
 
 // sum nparts partials of a p x p matrix into smem A (ld), symmetrised
@@ -344,20 +374,20 @@ __global__ void __launch_bounds__(512) chol_inv_kernel(const double* __restrict_
     }
     __syncthreads();
   }
-  // Rinv: solve R x = e_c for every column c (one thread per column, back substitution)
-  for (int c = tid; c < p; c += nt) {
-    for (int i = 0; i < p; ++i) X[i * ld + c] = 0.0;
-    if (!badsh[c]) {
-      X[c * ld + c] = 1.0 / B[c * ld + c];
-      for (int i = c - 1; i >= 0; --i) {
-        if (badsh[i]) continue;
-        double s = 0.0;
-        for (int k = i + 1; k <= c; ++k) s = fma(B[i * ld + k], X[k * ld + c], s);
-        X[i * ld + c] = -s / B[i * ld + i];
-      }
-    }
-  }
+  // Rinv = R^{-1} row by row from the bottom (X[i][.] accumulates sum_{k>i} R[i][k] Rinv[k][.])
+  for (int t = tid; t < p * p; t += nt) X[(t / p) * ld + (t % p)] = 0.0;
   __syncthreads();
+  for (int j = p - 1; j >= 0; --j) {
+    const bool okj = !badsh[j];
+    const double inv = okj ? 1.0 / B[j * ld + j] : 0.0;
+    for (int cc = tid; cc < p; cc += nt) X[j * ld + cc] = okj ? (((cc == j) ? 1.0 : 0.0) - X[j * ld + cc]) * inv : 0.0;
+    __syncthreads();
+    for (int t = tid; t < j * p; t += nt) {
+      const int i = t / p, cc = t % p;
+      X[i * ld + cc] = fma(B[i * ld + j], X[j * ld + cc], X[i * ld + cc]);
+    }
+    __syncthreads();
+  }
   for (int t = tid; t < p * p; t += nt) Rinv[t] = X[(t / p) * ld + (t % p)];
   for (int c = tid; c < p; c += nt) bad[c] = badsh[c];
 }
@@ -427,12 +457,23 @@ avd_status gemm_g(Ctx* c, const double* In, double* Out) {
   return AVD_OK;
 }
 
+// H = A^T B (m-length reduction): per-CTA partials, then a multi-CTA fixed-order sum into c->H
 avd_status atb(Ctx* c, const double* A, const double* B) {
   const int64_t m = c->cfg.m;
   const int p = c->p;
-  const size_t sm = 2 * kRedRows * p * sizeof(double);
-  AVD_CUDA(cudaFuncSetAttribute(atb_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  atb_partial_kernel<<<c->n_red, 256, sm, c->stream>>>(A, B, m, p, c->red_part);
+  const size_t sm = 2 * kRedChunk * p * sizeof(double);
+  switch (p / 16) {
+#define CASE(PC)                                                                                      \
+  case PC:                                                                                            \
+    AVD_CUDA(cudaFuncSetAttribute(atb_partial_kernel<PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+    atb_partial_kernel<PC><<<c->n_red, 256, sm, c->stream>>>(A, B, m, c->red_part);                   \
+    break;
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
+#undef CASE
+    default: set_error("unsupported p"); return AVD_EINVAL;
+  }
+  AVD_LAUNCHED(c);
+  psum_kernel<<<(unsigned)ceil_div(p * p, 128), 128, 0, c->stream>>>(c->red_part, c->n_red, p * p, c->H);
   AVD_LAUNCHED(c);
   return AVD_OK;
 }
@@ -455,7 +496,7 @@ avd_status orth(Ctx* c, const double* Y, double* Q, uint32_t seed) {
   for (int pass = 0; pass < 2; ++pass) {
     const double* src = pass == 0 ? Y : Q;
     AVD_TRY(atb(c, src, src));
-    chol_inv_kernel<<<1, 512, sm, c->stream>>>(c->red_part, c->n_red, p, c->W, bad);
+    chol_inv_kernel<<<1, 512, sm, c->stream>>>(c->H, 1, p, c->W, bad);
     AVD_LAUNCHED(c);
     AVD_TRY(matpp(c, src, Q, nullptr, nullptr, c->W));
     if (pass == 0) {
@@ -468,6 +509,9 @@ avd_status orth(Ctx* c, const double* Y, double* Q, uint32_t seed) {
 
 }  // namespace
 
+// Subspace iteration: every iteration applies G^2 (two GEMMs) and re-orthonormalises; a
+// Rayleigh-Ritz check runs on a schedule predicted from the observed residual decay (at most
+// every 4 iterations, always on the last one), so the p x p Jacobi runs ~3-4 times per solve.
 avd_status run_eig(Ctx* c) {
   const int64_t m = c->cfg.m;
   const int p = c->p, k = c->k;
@@ -480,31 +524,51 @@ avd_status run_eig(Ctx* c) {
   AVD_TRY(orth(c, c->Z, c->Q, seed + 1));
   const int max_it = c->cfg.max_iters > 0 ? c->cfg.max_iters : 100;
   const double tol = c->cfg.eig_tol > 0 ? c->cfg.eig_tol : 1e-9;
-  int it = 0;
-  double maxres = 0.0;
+  int it = 0, next_rr = 2, prev_it = 0, rr_count = 0;
+  double maxres = 0.0, prev_res = -1.0;
   bool conv = false;
   for (it = 1; it <= max_it; ++it) {
     AVD_TRY(gemm_g(c, c->Q, c->Y));                         // Y = G Q
-    AVD_TRY(atb(c, c->Q, c->Y));                            // H = Q^T Y (partials)
-    jacobi_kernel<<<1, 512, jsm, c->stream>>>(c->red_part, c->n_red, p, c->W, c->theta, jstats);
-    AVD_LAUNCHED(c);
-    AVD_TRY(matpp(c, c->Y, c->Z, c->Q, c->U, c->W));        // Z = Y W, U = Q W
-    resid_kernel<<<k, 256, 0, c->stream>>>(c->Z, c->U, c->theta, m, p, c->resid);
-    AVD_LAUNCHED(c);
-    AVD_CUDA(cudaMemcpyAsync(c->eig_host, c->theta, sizeof(double) * p, cudaMemcpyDeviceToHost, c->stream));
-    AVD_CUDA(cudaMemcpyAsync(c->eig_host + p, c->resid, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
-    AVD_CUDA(cudaStreamSynchronize(c->stream));
-    maxres = 0.0;
-    for (int r = 0; r < k; ++r) maxres = std::max(maxres, c->eig_host[p + r]);
-    if (!(c->eig_host[0] > 0.0)) { maxres = 0.0; conv = true; break; }  // G == 0: nothing to iterate
-    if (maxres <= tol) { conv = true; break; }
-    if (it == max_it) break;
-    AVD_TRY(gemm_g(c, c->Z, c->Y));                         // Y = G Z = G^2 U
+    if (it == next_rr || it == max_it) {
+      ++rr_count;
+      AVD_TRY(atb(c, c->Q, c->Y));                          // H = Q^T Y
+      jacobi_kernel<<<1, 512, jsm, c->stream>>>(c->H, 1, p, c->W, c->theta, jstats);
+      AVD_LAUNCHED(c);
+      AVD_TRY(matpp(c, c->Y, c->Z, c->Q, c->U, c->W));      // Z = Y W, U = Q W (Ritz vectors)
+      resid_kernel<<<k, 256, 0, c->stream>>>(c->Z, c->U, c->theta, m, p, c->resid);
+      AVD_LAUNCHED(c);
+      AVD_CUDA(cudaMemcpyAsync(c->eig_host, c->theta, sizeof(double) * p, cudaMemcpyDeviceToHost, c->stream));
+      AVD_CUDA(cudaMemcpyAsync(c->eig_host + p, c->resid, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
+      AVD_CUDA(cudaStreamSynchronize(c->stream));
+      maxres = 0.0;
+      for (int r = 0; r < k; ++r) maxres = std::max(maxres, c->eig_host[p + r]);
+      if (!(c->eig_host[0] > 0.0)) { maxres = 0.0; conv = true; break; }  // G == 0: nothing to iterate
+      if (maxres <= tol) { conv = true; break; }
+      if (it == max_it) break;
+      // predicted residual decay per G^2 step: observed, else (theta_p / theta_k)^2
+      double rate = -1.0;
+      if (prev_res > 0.0 && maxres < prev_res) rate = std::pow(maxres / prev_res, 1.0 / (double)(it - prev_it));
+      else if (c->eig_host[k - 1] > 0.0) rate = std::pow(std::max(c->eig_host[p - 1], 0.0) / c->eig_host[k - 1], 2.0);
+      int step = 1;
+      if (rate > 0.0 && rate < 0.95) {
+        const double need = std::log(tol / maxres) / std::log(rate);
+        step = (int)std::max(1.0, std::min(8.0, std::floor(need)));
+      }
+      prev_res = maxres;
+      prev_it = it;
+      next_rr = it + step;
+      AVD_TRY(gemm_g(c, c->Z, c->Y));                       // Y = G Z = G^2 U
+    } else {
+      AVD_TRY(gemm_g(c, c->Y, c->Z));                       // Z = G Y = G^2 Q
+      std::swap(c->Y, c->Z);
+    }
     AVD_TRY(orth(c, c->Y, c->Q, seed + 7919u * (uint32_t)it));
   }
   c->iters = std::min(it, max_it);
+  c->rr_count = rr_count;
   c->max_resid = maxres;
   c->sigma_next = (k < p) ? std::sqrt(std::max(c->eig_host[k], 0.0)) : 0.0;
+  AVD_CUDA(cudaMemcpyAsync(&c->jacobi_sweeps, jstats, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   AVD_CUDA(cudaMemsetAsync(c->V32, 0, sizeof(float) * m * c->k_pad, c->stream));
   finalize_vectors_kernel<<<k, 256, 0, c->stream>>>(c->U, c->theta, m, p, k, c->k_pad, c->V, c->sigma, c->V32);
   AVD_LAUNCHED(c);

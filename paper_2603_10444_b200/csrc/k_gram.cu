@@ -223,6 +223,8 @@ int choose_split(int n_tiles, int64_t NK, int sms) {
 
 }  // namespace
 
+PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() { return get_encode(); }
+
 avd_status gram_make_tmap(Ctx* c) {
   auto enc = get_encode();
   if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return AVD_ECUDA; }

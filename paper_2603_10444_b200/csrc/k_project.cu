@@ -153,6 +153,13 @@ __global__ void project_reduce_kernel(const double* __restrict__ en_part, const 
 }  // namespace
 
 avd_status launch_project(Ctx* c, const float* X) {
+  if (project_tc_supported(c, X)) {
+    AVD_TRY(launch_project_tc(c, X));
+    project_reduce_kernel<<<4 + c->k_pad, 256, 0, c->stream>>>(c->en_part, c->colsumP_part, c->n_proj_ctas, c->k_pad,
+                                                                c->energy);
+    AVD_LAUNCHED(c);
+    return AVD_OK;
+  }
   const unsigned grid = (unsigned)c->n_proj_ctas;
   switch (c->k_pad / 16) {
 #define CASE(K)                                                                                         \

@@ -141,3 +141,12 @@ def test_high_top_frac(cuda_device):
     g = _gpu(X, n_top=int(0.3 * 1024 * 128))
     np.testing.assert_array_equal(g["top_idx"], o["top_idx"])
     assert np.max(np.abs(g["rho"] - o["rho"])) <= 1e-3
+
+
+@pytest.mark.parametrize("k", [7, 33, 81])
+def test_large_k_parity(cuda_device, k):
+    """k padded to 16 / 48 / 96 (the K5 N-widths and the K8 64-column path)."""
+    X = generate(SynthSpec(2048, 512, seed=30 + k, k_s=k, f_mean=0.7))
+    o = O.decompose(X.numpy(), k=k)
+    g = _gpu(X, k=k)
+    assert_parity(g, o)
