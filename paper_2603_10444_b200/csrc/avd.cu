@@ -132,6 +132,7 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   L.add(sizeof(float) * 2 * C->l_pad * (((C->k_pad + 31) / 32) * 32));   // 46 P_hl
   L.add(sizeof(float) * 2 * C->k_pad * round_up(m, 32));                 // 47 Vt_hl
   L.add(sizeof(float) * 2 * C->m_pad * (((C->k_pad + 31) / 32) * 32));   // 48 V_hl
+  L.add(sizeof(float) * 2 * C->m_pad);                                   // 49 mu_hl
   plan->workspace_bytes = L.total;
   if (lay) *lay = L;
   return AVD_OK;
@@ -247,7 +248,7 @@ avd_status avd_create(const avd_config* cfg, avd_ctx** out) {
   BIND(en_part, double*); BIND(colsumP_part, double*); BIND(energy, double*); BIND(hist2, unsigned long long*);
   BIND(hist3, unsigned long long*); BIND(ties, long long*); BIND(bm_sel, uint32_t*); BIND(bm_tie, uint32_t*);
   BIND(blk_cnt, int64_t*); BIND(agg, double*); BIND(agg_part, double*); BIND(report, double*); BIND(hist0, unsigned long long*); BIND(cand_x, long long*); BIND(Ypart, double*);
-  BIND(P_hl, float*); BIND(Vt_hl, float*); BIND(V_hl, float*);
+  BIND(P_hl, float*); BIND(Vt_hl, float*); BIND(V_hl, float*); BIND(mu_hl, float*);
 #undef BIND
   if (cudaMallocHost(&c->eig_host, sizeof(double) * 4 * kMaxP) != cudaSuccess) {
     cudaGetLastError();

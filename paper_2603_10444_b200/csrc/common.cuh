@@ -59,6 +59,7 @@ struct Ctx {
   unsigned long long* hist1 = nullptr;  // [4096] (exchange SUM)
   // prepare
   double* mu = nullptr;           // [m]
+  float* mu_hl = nullptr;         // [2][m_pad]: mu = hi + lo (fp32 pair) for fp32 centring
   int32_t* shift = nullptr;       // [m_pad] digit scale exponent per column
   DevPlan* dplan = nullptr;
   DevPlan hplan{};

@@ -26,7 +26,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn();  // k_gram.cu
 namespace {
 using namespace sm100;
 
-constexpr int kPThreads = 192;
+constexpr int kPThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 convert / epilogue
 constexpr uint32_t kTile = 128 * 128;  // bytes of a 128-row x 32-fp32 swizzled tile
 
 __device__ __forceinline__ float rna_tf32(float x) {
@@ -57,7 +57,7 @@ __global__ void split_v_kernel(const double* __restrict__ V, int64_t m, int k, i
 template <int KP, int NS>
 __global__ void __launch_bounds__(kPThreads, 1) proj_tc_kernel(
     const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmVt, int64_t l_local, int64_t m,
-    const double* __restrict__ mu, float* __restrict__ P, float* __restrict__ P_hl, int64_t l_pad,
+    const float* __restrict__ mu_hl, int64_t m_pad, float* __restrict__ P, float* __restrict__ P_hl, int64_t l_pad,
     double* __restrict__ en_part, double* __restrict__ colsumP_part) {
   constexpr int KP32 = (KP + 31) / 32 * 32;
   constexpr int NSLOT_MAX = (512 / KP) < 8 ? (512 / KP) : 8;
@@ -67,8 +67,8 @@ __global__ void __launch_bounds__(kPThreads, 1) proj_tc_kernel(
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full_bar[NS], conv_bar[NS], empty_bar[NS], tfull_bar, tempty_bar;
   __shared__ uint32_t tmem_sh;
-  __shared__ double colsum_w[4][KP];
-  __shared__ double sq_w[4];
+  __shared__ double colsum_w[8][KP];
+  __shared__ double sq_w[8];
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int64_t nrb = ceil_div(l_local, 128);
@@ -76,9 +76,9 @@ __global__ void __launch_bounds__(kPThreads, 1) proj_tc_kernel(
   const int nslot = NC < NSLOT_MAX ? NC : NSLOT_MAX;  // every slot receives >= 1 chunk
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NS; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&conv_bar[s], 4); mbar_init(&empty_bar[s], 1); }
+    for (int s = 0; s < NS; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&conv_bar[s], 8); mbar_init(&empty_bar[s], 1); }
     mbar_init(&tfull_bar, 1);
-    mbar_init(&tempty_bar, 4);
+    mbar_init(&tempty_bar, 8);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) { tma_prefetch(&tmX); tma_prefetch(&tmVt); }
@@ -140,79 +140,89 @@ __global__ void __launch_bounds__(kPThreads, 1) proj_tc_kernel(
       __syncwarp();
     }
   } else {
-    // ================= converter + epilogue warps
-    const int ew = warp - 2;              // 0..3
+    // ================= converter + epilogue warps (8 warps, two per TMEM lane quadrant)
+    const int ew = warp - 2;              // 0..7
     const uint32_t q = warp & 3;          // TMEM lane quadrant
-    const int ct = threadIdx.x - 64;      // 0..127 converter thread
+    const int half = ew >> 2;             // epilogue column half
+    const int ct = threadIdx.x - 64;      // 0..255 converter thread
+    const int g = (ct & 7) ^ ((ct >> 3) & 7);  // logical 4-column group of this thread (SW128)
+    const int rbase = ct >> 3;            // rows rbase + 32 u, u < 4
     double sq = 0.0;
     uint32_t it = 0, ui = 0;
     for (int64_t rb = blockIdx.x; rb < nrb; rb += gridDim.x, ++ui) {
       const int64_t row0 = rb * 128;
       for (int c = 0; c < NC; ++c, ++it) {
         const uint32_t s = it % NS, r = it / NS;
+        const int64_t col = (int64_t)c * 32 + g * 4;
+        const float4 mh4 = __ldg(reinterpret_cast<const float4*>(mu_hl + col));
+        const float4 ml4 = __ldg(reinterpret_cast<const float4*>(mu_hl + m_pad + col));
+        const float mh[4] = {mh4.x, mh4.y, mh4.z, mh4.w}, ml[4] = {ml4.x, ml4.y, ml4.z, ml4.w};
+        bool cok[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) cok[e] = col + e < m;
         mbar_wait(&full_bar[s], r & 1);
         uint8_t* st = smem + s * kStage;
         const float4* xs = reinterpret_cast<const float4*>(st);
         float4* hs = reinterpret_cast<float4*>(st + kTile);
         float4* ls = reinterpret_cast<float4*>(st + 2 * kTile);
+        float s32 = 0.f;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int ch = ct + 128 * u;  // 16-byte chunk index in the tile
-          const int row = ch >> 3;
-          const int g = (ch & 7) ^ (row & 7);  // logical 4-column group (swizzle 128B)
-          const int64_t col = (int64_t)c * 32 + g * 4;
-          const bool rok = row0 + row < l_local;
+        for (int u = 0; u < 4; ++u) {
+          const int ch = ct + 256 * u;  // 16-byte chunk index in the tile
+          const bool rok = row0 + rbase + 32 * u < l_local;
           const float4 x = xs[ch];
-          float xv[4] = {x.x, x.y, x.z, x.w};
+          const float xv[4] = {x.x, x.y, x.z, x.w};
           float hv[4], lv[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            float xc = 0.f;
-            if (rok && col + e < m) xc = (float)((double)xv[e] - __ldg(mu + col + e));
-            sq = fma((double)xc, (double)xc, sq);
+            // fp32 centring with mu = hi + lo: (x - mu_hi) is exact or correctly rounded
+            const float xc = (rok && cok[e]) ? (xv[e] - mh[e]) - ml[e] : 0.f;
+            s32 = fmaf(xc, xc, s32);
             hv[e] = rna_tf32(xc);
             lv[e] = rna_tf32(xc - hv[e]);
           }
           hs[ch] = make_float4(hv[0], hv[1], hv[2], hv[3]);
           ls[ch] = make_float4(lv[0], lv[1], lv[2], lv[3]);
         }
+        sq += (double)s32;
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&conv_bar[s]);
       }
-      // ---- epilogue: P row = sum of slots
+      // ---- epilogue: P row = sum of slots (this warp: half of the KP columns)
       mbar_wait(&tfull_bar, ui & 1);
       tc_fence_after();
       const int64_t row = row0 + q * 32 + lane;
       const bool rok = row < l_local;
       const uint32_t tb = tmem + ((q * 32) << 16);
 #pragma unroll 1
-      for (int c0 = 0; c0 < KP; c0 += 16) {
-        float pv[16];
+      for (int c0 = half * (KP / 2); c0 < (half + 1) * (KP / 2); c0 += 8) {
+        float pv[8];
 #pragma unroll
-        for (int t = 0; t < 16; ++t) pv[t] = 0.f;
+        for (int t = 0; t < 8; ++t) pv[t] = 0.f;
         for (int sl = 0; sl < nslot; ++sl) {
-          uint32_t rv[16];
-          tmem_ld16(tb + sl * KP + c0, rv);
+          uint32_t rv[8];
+          tmem_ld8(tb + sl * KP + c0, rv);
           tmem_ld_wait();
 #pragma unroll
-          for (int t = 0; t < 16; ++t) pv[t] += __uint_as_float(rv[t]);
+          for (int t = 0; t < 8; ++t) pv[t] += __uint_as_float(rv[t]);
         }
         if (rok) {
           float4* dst = reinterpret_cast<float4*>(P + row * KP + c0);
+          dst[0] = make_float4(pv[0], pv[1], pv[2], pv[3]);
+          dst[1] = make_float4(pv[4], pv[5], pv[6], pv[7]);
+          float hv[8], lv[8];
 #pragma unroll
-          for (int t = 0; t < 4; ++t) dst[t] = make_float4(pv[4 * t], pv[4 * t + 1], pv[4 * t + 2], pv[4 * t + 3]);
-          float* hrow = P_hl + row * KP32 + c0;
-          float* lrow = P_hl + (l_pad + row) * KP32 + c0;
-#pragma unroll
-          for (int t = 0; t < 16; ++t) {
-            const float h = rna_tf32(pv[t]);
-            hrow[t] = h;
-            lrow[t] = rna_tf32(pv[t] - h);
-          }
+          for (int t = 0; t < 8; ++t) { hv[t] = rna_tf32(pv[t]); lv[t] = rna_tf32(pv[t] - hv[t]); }
+          float4* hrow = reinterpret_cast<float4*>(P_hl + row * KP32 + c0);
+          float4* lrow = reinterpret_cast<float4*>(P_hl + (l_pad + row) * KP32 + c0);
+          hrow[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
+          hrow[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
+          lrow[0] = make_float4(lv[0], lv[1], lv[2], lv[3]);
+          lrow[1] = make_float4(lv[4], lv[5], lv[6], lv[7]);
         }
 #pragma unroll
-        for (int t = 0; t < 16; ++t) {
+        for (int t = 0; t < 8; ++t) {
           double v = rok ? (double)pv[t] : 0.0;
           for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
           if (lane == 0) colsum_w[ew][c0 + t] += v;
@@ -227,10 +237,16 @@ __global__ void __launch_bounds__(kPThreads, 1) proj_tc_kernel(
   }
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x < KP)
-    colsumP_part[(int64_t)blockIdx.x * KP + threadIdx.x] =
-        ((colsum_w[0][threadIdx.x] + colsum_w[1][threadIdx.x]) + colsum_w[2][threadIdx.x]) + colsum_w[3][threadIdx.x];
-  if (threadIdx.x == 0) en_part[(int64_t)blockIdx.x * 4 + 3] = ((sq_w[0] + sq_w[1]) + sq_w[2]) + sq_w[3];
+  if (threadIdx.x < KP) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += colsum_w[w][threadIdx.x];
+    colsumP_part[(int64_t)blockIdx.x * KP + threadIdx.x] = t;
+  }
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += sq_w[w];
+    en_part[(int64_t)blockIdx.x * 4 + 3] = t;
+  }
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
@@ -238,7 +254,7 @@ __global__ void __launch_bounds__(kPThreads, 1) proj_tc_kernel(
 template <int KP32, int NCOL, int NS>
 __global__ void __launch_bounds__(kPThreads, 1) energy_tc_kernel(
     const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmV, const float* __restrict__ X,
-    int64_t l_local, int64_t m, int64_t l_pad, int64_t m_pad128, const double* __restrict__ mu,
+    int64_t l_local, int64_t m, int64_t l_pad, int64_t m_pad128, const float* __restrict__ mu_hl, int64_t m_pad,
     double* __restrict__ en_part) {
   constexpr int NA = KP32 / 32;                       // 32-wide K atoms
   constexpr uint32_t kATile = kTile;                  // 128 rows x 128 B
@@ -251,7 +267,7 @@ __global__ void __launch_bounds__(kPThreads, 1) energy_tc_kernel(
   uint8_t* sB = smem + kA;
   __shared__ uint64_t afull_bar, aempty_bar, full_bar[NS], empty_bar[NS], tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_sh;
-  __shared__ double red[4][3];
+  __shared__ double red[8][3];
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int64_t nrb = ceil_div(l_local, 128);
@@ -260,7 +276,7 @@ __global__ void __launch_bounds__(kPThreads, 1) energy_tc_kernel(
     mbar_init(&afull_bar, 1);
     mbar_init(&aempty_bar, 1);
     for (int s = 0; s < NS; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(&tfull_bar[b], 1); mbar_init(&tempty_bar[b], 4); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull_bar[b], 1); mbar_init(&tempty_bar[b], 8); }
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) { tma_prefetch(&tmP); tma_prefetch(&tmV); }
@@ -330,8 +346,10 @@ __global__ void __launch_bounds__(kPThreads, 1) energy_tc_kernel(
       }
     }
   } else {
+    // ================= epilogue warps (8: two per TMEM lane quadrant, each half of the columns)
     const int ew = warp - 2;
     const uint32_t q = warp & 3;
+    const int half = ew >> 2;
     double eS = 0.0, eT = 0.0, eST = 0.0;
     uint32_t ci = 0;
     for (int64_t rb = blockIdx.x; rb < nrb; rb += gridDim.x) {
@@ -343,12 +361,20 @@ __global__ void __launch_bounds__(kPThreads, 1) energy_tc_kernel(
         mbar_wait(&tfull_bar[b], br & 1);
         tc_fence_after();
         const uint32_t tb = tmem + ((q * 32) << 16) + b * NCOL;
+        float s2 = 0.f, t2 = 0.f, st = 0.f;
 #pragma unroll 1
-        for (int c0 = 0; c0 < NCOL; c0 += 16) {
+        for (int c0 = half * (NCOL / 2); c0 < (half + 1) * (NCOL / 2); c0 += 16) {
           uint32_t rv[16];
           tmem_ld16(tb + c0, rv);
           const int64_t j0 = (int64_t)c * NCOL + c0;
-          float xv[16];
+          float xv[16], mh[16], ml[16];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const float4 a = __ldg(reinterpret_cast<const float4*>(mu_hl + j0) + t);
+            const float4 bb = __ldg(reinterpret_cast<const float4*>(mu_hl + m_pad + j0) + t);
+            mh[4 * t] = a.x; mh[4 * t + 1] = a.y; mh[4 * t + 2] = a.z; mh[4 * t + 3] = a.w;
+            ml[4 * t] = bb.x; ml[4 * t + 1] = bb.y; ml[4 * t + 2] = bb.z; ml[4 * t + 3] = bb.w;
+          }
           if (rok && j0 + 16 <= m) {
             const float4* src = reinterpret_cast<const float4*>(xrow + j0);
 #pragma unroll
@@ -363,16 +389,18 @@ __global__ void __launch_bounds__(kPThreads, 1) energy_tc_kernel(
           tmem_ld_wait();
 #pragma unroll
           for (int t = 0; t < 16; ++t) {
-            if (rok && j0 + t < m) {
-              const double xc = (double)(float)((double)xv[t] - __ldg(mu + j0 + t));
-              const double S = (double)__uint_as_float(rv[t]);
-              const double T = xc - S;
-              eS = fma(S, S, eS);
-              eT = fma(T, T, eT);
-              eST = fma(S, T, eST);
-            }
+            const bool ok = rok && j0 + t < m;
+            const float xc = (xv[t] - mh[t]) - ml[t];
+            const float S = ok ? __uint_as_float(rv[t]) : 0.f;
+            const float T = ok ? xc - S : 0.f;
+            s2 = fmaf(S, S, s2);
+            t2 = fmaf(T, T, t2);
+            st = fmaf(S, T, st);
           }
         }
+        eS += (double)s2;
+        eT += (double)t2;
+        eST += (double)st;
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty_bar[b]);
@@ -387,9 +415,11 @@ __global__ void __launch_bounds__(kPThreads, 1) energy_tc_kernel(
   }
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x < 3)
-    en_part[(int64_t)blockIdx.x * 4 + threadIdx.x] =
-        ((red[0][threadIdx.x] + red[1][threadIdx.x]) + red[2][threadIdx.x]) + red[3][threadIdx.x];
+  if (threadIdx.x < 3) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w][threadIdx.x];
+    en_part[(int64_t)blockIdx.x * 4 + threadIdx.x] = t;
+  }
   if (warp == 1) tmem_dealloc<2 * NCOL>(tmem);
 }
 
@@ -410,8 +440,9 @@ avd_status launch_k5(Ctx* c, const CUtensorMap& tmX, const CUtensorMap& tmVt, in
   constexpr uint32_t kStage = 3 * kTile + ((2 * KP * 128 + 1023) / 1024) * 1024;
   const size_t smem = NS * kStage + 1024;
   AVD_CUDA(cudaFuncSetAttribute(proj_tc_kernel<KP, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  proj_tc_kernel<KP, NS><<<grid, kPThreads, smem, c->stream>>>(tmX, tmVt, c->cfg.l_local, c->cfg.m, c->mu, c->P,
-                                                               c->P_hl, c->l_pad, c->en_part, c->colsumP_part);
+  proj_tc_kernel<KP, NS><<<grid, kPThreads, smem, c->stream>>>(tmX, tmVt, c->cfg.l_local, c->cfg.m, c->mu_hl,
+                                                               c->m_pad, c->P, c->P_hl, c->l_pad, c->en_part,
+                                                               c->colsumP_part);
   AVD_LAUNCHED(c);
   return AVD_OK;
 }
@@ -425,7 +456,8 @@ avd_status launch_k8(Ctx* c, const float* X, const CUtensorMap& tmP, const CUten
   AVD_CUDA(cudaFuncSetAttribute(energy_tc_kernel<KP32, NCOL, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
   energy_tc_kernel<KP32, NCOL, NS><<<grid, kPThreads, smem, c->stream>>>(tmP, tmV, X, c->cfg.l_local, c->cfg.m,
-                                                                         c->l_pad, c->m_pad, c->mu, c->en_part);
+                                                                         c->l_pad, c->m_pad, c->mu_hl, c->m_pad,
+                                                                         c->en_part);
   AVD_LAUNCHED(c);
   return AVD_OK;
 }

@@ -30,7 +30,7 @@ __device__ __forceinline__ uint32_t mix32(uint32_t x) {
 template <int ND>
 __global__ void __launch_bounds__(kSplitThreads) split_kernel(
     const float* __restrict__ X, int64_t l_local, int64_t m, int64_t m_pad, int64_t l_pad,
-    int64_t row_offset, const double* __restrict__ mu, const int32_t* __restrict__ shift,
+    int64_t row_offset, const float* __restrict__ mu_hl, const int32_t* __restrict__ shift,
     uint32_t seed32, int8_t* __restrict__ digits, const DevPlan* __restrict__ dp,
     uint32_t* __restrict__ cand_key, uint64_t* __restrict__ cand_idx,
     unsigned long long* __restrict__ cand_cnt, int64_t cand_cap) {
@@ -46,20 +46,22 @@ __global__ void __launch_bounds__(kSplitThreads) split_kernel(
     srow[threadIdx.x] = mix32((uint32_t)(row_offset + i0 + threadIdx.x) * 0x9E3779B1u ^ seed32);
   const uint32_t b0 = (uint32_t)dp->b0;
   const bool colok = j < m;
-  const double muj = colok ? mu[j] : 0.0;
-  const double scale = colok ? ldexp(1.0, shift[j]) : 0.0;
+  // mu = hi + lo (fp32 pair); 2^shift as an exact fp32 power of two (shift clamped to the normal
+  // range: columns with max|xc| < 2^-100 quantise to zero)
+  const float mh = colok ? mu_hl[j] : 0.f, ml = colok ? mu_hl[m_pad + j] : 0.f;
+  const int sh = colok ? shift[j] : 0;
+  const float scale = (colok && sh <= 126 && sh >= -126) ? __int_as_float((sh + 127) << 23) : 0.f;
   const uint32_t colh = mix32((uint32_t)j ^ 0x68E31DA4u);
-  // all 32 loads of this thread in flight at once
-  float xs[32];
-#pragma unroll
-  for (int r = 0; r < 32; ++r) {
-    const int64_t i = i0 + rg * 32 + r;
-    xs[r] = (colok && i < l_local) ? __ldcs(X + i * m + j) : 0.f;
-  }
   __syncthreads();
 
-#pragma unroll
+#pragma unroll 1
   for (int t = 0; t < 8; ++t) {
+    float xs[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = i0 + rg * 32 + t * 4 + u;
+      xs[u] = (colok && i < l_local) ? __ldcs(X + i * m + j) : 0.f;
+    }
     uint32_t packed[ND];
 #pragma unroll
     for (int d = 0; d < ND; ++d) packed[d] = 0;
@@ -68,7 +70,7 @@ __global__ void __launch_bounds__(kSplitThreads) split_kernel(
       const int rl = rg * 32 + t * 4 + u;
       const int64_t i = i0 + rl;
       const bool ok = colok && i < l_local;
-      const float x = xs[t * 4 + u];
+      const float x = xs[u];
       const uint32_t key = __float_as_uint(x) & 0x7FFFFFFFu;
       // ---- candidate append (warp aggregated)
       const bool cand = ok && key != 0 && key < 0x7F800000u && (key >> 19) >= b0;
@@ -86,18 +88,20 @@ __global__ void __launch_bounds__(kSplitThreads) split_kernel(
           }
         }
       }
-      // ---- dithered fixed-point digits of the centred entry
+      // ---- dithered fixed-point digits of the centred entry: q = floor(xc 2^shift + u)
       if (ok) {
-        const double xc = (double)x - muj;
+        const float y = ((x - mh) - ml) * scale;     // exact power-of-two scaling, |y| < 2^(7nd-1)
+        const float yi = floorf(y);
+        const float f = y - yi;                       // exact fractional part
         const uint32_t h = mix32(srow[rl] ^ colh);
-        const double dith = (double)(h >> 8) * (1.0 / 16777216.0);
-        int32_t q = (int32_t)floor(fma(xc, scale, dith));
+        const float dith = (float)(h >> 8) * (1.0f / 16777216.0f);  // u in [0,1), 24 bits
+        int32_t q = (int32_t)yi + (dith >= 1.0f - f ? 1 : 0);
         int32_t dg[ND];
 #pragma unroll
         for (int d = ND - 1; d >= 1; --d) {
-          const int32_t s = ((q + 64) & 127) - 64;
-          dg[d] = s;
-          q = (q - s) >> 7;
+          const int32_t sdg = ((q + 64) & 127) - 64;
+          dg[d] = sdg;
+          q = (q - sdg) >> 7;
         }
         dg[0] = q;
 #pragma unroll
@@ -134,11 +138,11 @@ avd_status launch_split(Ctx* c, const float* X) {
   const uint32_t seed32 = (uint32_t)(c->cfg.seed * 0x9E3779B97F4A7C15ull >> 32) ^ 0xA5A5A5A5u;
   if (c->nd == 2)
     split_kernel<2><<<grid, kSplitThreads, 0, c->stream>>>(
-        X, c->cfg.l_local, c->cfg.m, c->m_pad, c->l_pad, c->cfg.row_offset, c->mu, c->shift, seed32,
+        X, c->cfg.l_local, c->cfg.m, c->m_pad, c->l_pad, c->cfg.row_offset, c->mu_hl, c->shift, seed32,
         c->digits, c->dplan, c->cand_key, c->cand_idx, c->cand_cnt, c->cand_cap);
   else
     split_kernel<3><<<grid, kSplitThreads, 0, c->stream>>>(
-        X, c->cfg.l_local, c->cfg.m, c->m_pad, c->l_pad, c->cfg.row_offset, c->mu, c->shift, seed32,
+        X, c->cfg.l_local, c->cfg.m, c->m_pad, c->l_pad, c->cfg.row_offset, c->mu_hl, c->shift, seed32,
         c->digits, c->dplan, c->cand_key, c->cand_idx, c->cand_cnt, c->cand_cap);
   AVD_LAUNCHED(c);
   cand_publish_kernel<<<1, 1, 0, c->stream>>>(c->cand_cnt, c->cand_cap, c->cand_x);

@@ -156,17 +156,23 @@ __global__ void stats_reduce_kernel(int64_t m, int r1, int nsq, const double* __
 __global__ void prepare_kernel(int64_t m, int64_t m_pad, int64_t l_global, int nd, int64_t n_top, int sample,
                                const double* __restrict__ stats, const float* __restrict__ colmax,
                                const float* __restrict__ colmin, const unsigned long long* __restrict__ hist1,
-                               double* __restrict__ mu, int32_t* __restrict__ shift, DevPlan* __restrict__ dp) {
+                               double* __restrict__ mu, float* __restrict__ mu_hl, int32_t* __restrict__ shift,
+                               DevPlan* __restrict__ dp) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j < m_pad) {
     int32_t sh = 0;
+    float mh = 0.f, ml = 0.f;
     if (j < m) {
       const double mj = stats[j] / (double)l_global;
       mu[j] = mj;
+      mh = (float)mj;
+      ml = (float)(mj - (double)mh);
       const double a = fmax((double)colmax[j] - mj, mj - (double)colmin[j]);
       if (a > 0.0 && a < 1e300) sh = (7 * nd - 1) - (ilogb(a) + 1);
     }
     shift[j] = sh;
+    mu_hl[j] = mh;
+    mu_hl[m_pad + j] = ml;
   }
   if (blockIdx.x == 0 && threadIdx.x < 32) {
     const int lane = threadIdx.x;
@@ -241,7 +247,7 @@ avd_status launch_stats(Ctx* c, const float* X) {
 avd_status launch_prepare(Ctx* c) {
   prepare_kernel<<<(unsigned)ceil_div(c->m_pad, 256), 256, 0, c->stream>>>(
       c->cfg.m, c->m_pad, c->cfg.l_global, c->nd, c->plan.n_top, stats_sample_step(c->cfg.l_global), c->stats,
-      c->colmax, c->colmin, c->hist1, c->mu, c->shift, c->dplan);
+      c->colmax, c->colmin, c->hist1, c->mu, c->mu_hl, c->shift, c->dplan);
   AVD_LAUNCHED(c);
   return AVD_OK;
 }
