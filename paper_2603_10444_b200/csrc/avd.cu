@@ -53,7 +53,7 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   const int64_t p = ((k + 8 + 15) / 16) * 16;
   if (p > kMaxP || k > 96) { set_error("k too large for this build (p <= 112, k <= 96)"); return AVD_EINVAL; }
   const int64_t n_top = cfg->n_top_override > 0 ? cfg->n_top_override : std::max<int64_t>(1, floor_frac(cfg->top_frac, l * m));
-  const int nd = cfg->digits == 0 ? 3 : cfg->digits;
+  const int nd = cfg->digits == 0 ? 2 : cfg->digits;
   if (nd != 2 && nd != 3) { set_error("digits must be 2 or 3"); return AVD_EINVAL; }
   plan->k = (int32_t)k;
   plan->p = (int32_t)p;

@@ -15,7 +15,7 @@ constexpr int kHist3Bins = 128;   // third level: 7 key bits
 constexpr int kGramTile = 128;    // Gram tile edge (rows of A / B panels)
 constexpr int kGramK = 128;       // K rows per pipeline stage (one 128-byte swizzle row of int8)
 constexpr int kMaxP = 112;        // subspace block size cap (two p x p fp64 matrices in smem)
-constexpr int kRedRowsC = 256;    // rows per partial of the m-length p x p reductions (k_eig.cu)
+constexpr int kRedRowsC = 128;    // rows per partial of the m-length p x p reductions (k_eig.cu)
 
 // Device-side "plan2": values decided on the device after the stats exchange.
 struct DevPlan {

@@ -64,15 +64,19 @@ __global__ void rand_fill_kernel(double* __restrict__ Q, int64_t m, int p, uint3
 
 // ---------------------------------------------------------------- Y = G Q  (split-K partials)
 // CTA: 32 rows of Y x all p columns, K range [kz*kchunk, (kz+1)*kchunk); 128 threads, each a
-// 4-row x (p/16)-column register tile.  Ypart[kz][m][p].
+// 4-row x (p/16)-column register tile; register-prefetched double buffer (the next K stage's
+// global loads are in flight while the current stage computes).  Ypart[kz][m][p].
 constexpr int kGM = 32;   // rows per CTA
 constexpr int kGK = 32;   // K per smem stage
 template <int PC>
 __global__ void __launch_bounds__(128) gemm_gq_kernel(const double* __restrict__ G, const double* __restrict__ Q,
                                                       int64_t m, int64_t kchunk, double* __restrict__ Ypart) {
   constexpr int p = PC * 16;
-  __shared__ __align__(16) double sGt[kGK][kGM + 2];  // transposed G tile [k][row]
-  __shared__ __align__(16) double sQ[kGK][p];
+  constexpr int NG = (kGM * kGK) / 128;   // G values per thread per stage
+  constexpr int NQ = (kGK * p) / 128;     // Q values per thread per stage
+  constexpr int SG = kGK * (kGM + 2);     // doubles of one transposed G tile [k][row]
+  constexpr int SQ = kGK * p;
+  extern __shared__ __align__(16) double gsm[];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // rows 4ty..4ty+3, cols tx+16c
   const int64_t r0 = (int64_t)blockIdx.x * kGM;
   const int64_t kbeg = (int64_t)blockIdx.y * kchunk;
@@ -82,31 +86,57 @@ __global__ void __launch_bounds__(128) gemm_gq_kernel(const double* __restrict__
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int c = 0; c < PC; ++c) acc[a][c] = 0.0;
-  for (int64_t k0 = kbeg; k0 < kend; k0 += kGK) {
+  double gv[NG], qv[NQ];
+  auto load = [&](int64_t k0) {
 #pragma unroll
-    for (int e = 0; e < (kGM * kGK) / 128; ++e) {
+    for (int e = 0; e < NG; ++e) {
       const int t = threadIdx.x + e * 128;
       const int rr = t / kGK, kk = t % kGK;
-      sGt[kk][rr] = (r0 + rr < m && k0 + kk < kend) ? G[(r0 + rr) * m + k0 + kk] : 0.0;
+      gv[e] = (r0 + rr < m && k0 + kk < kend) ? __ldg(G + (r0 + rr) * m + k0 + kk) : 0.0;
     }
-    for (int t = threadIdx.x; t < kGK * p; t += 128) {
-      const int kk = t / p, cc = t % p;
-      sQ[kk][cc] = (k0 + kk < kend) ? Q[(k0 + kk) * p + cc] : 0.0;
+#pragma unroll
+    for (int e = 0; e < NQ; ++e) {
+      const int t = threadIdx.x + e * 128;
+      const int kk = t / p;
+      qv[e] = (k0 + kk < kend) ? __ldg(Q + (k0 + kk) * p + (t % p)) : 0.0;
     }
-    __syncthreads();
-#pragma unroll 4
+  };
+  auto store = [&](int buf) {
+    double* sG = gsm + buf * (SG + SQ);
+    double* sQ = sG + SG;
+#pragma unroll
+    for (int e = 0; e < NG; ++e) {
+      const int t = threadIdx.x + e * 128;
+      sG[(t % kGK) * (kGM + 2) + t / kGK] = gv[e];
+    }
+#pragma unroll
+    for (int e = 0; e < NQ; ++e) sQ[threadIdx.x + e * 128] = qv[e];
+  };
+  if (kbeg < kend) {
+    load(kbeg);
+    store(0);
+  }
+  __syncthreads();
+  int buf = 0;
+  for (int64_t k0 = kbeg; k0 < kend; k0 += kGK, buf ^= 1) {
+    const bool more = k0 + kGK < kend;
+    if (more) load(k0 + kGK);
+    const double* sG = gsm + buf * (SG + SQ);
+    const double* sQ = sG + SG;
+#pragma unroll 8
     for (int kk = 0; kk < kGK; ++kk) {
-      const double2 g01 = *reinterpret_cast<const double2*>(&sGt[kk][4 * ty]);
-      const double2 g23 = *reinterpret_cast<const double2*>(&sGt[kk][4 * ty + 2]);
+      const double2 g01 = *reinterpret_cast<const double2*>(sG + kk * (kGM + 2) + 4 * ty);
+      const double2 g23 = *reinterpret_cast<const double2*>(sG + kk * (kGM + 2) + 4 * ty + 2);
 #pragma unroll
       for (int c = 0; c < PC; ++c) {
-        const double qv = sQ[kk][tx + 16 * c];
-        acc[0][c] = fma(g01.x, qv, acc[0][c]);
-        acc[1][c] = fma(g01.y, qv, acc[1][c]);
-        acc[2][c] = fma(g23.x, qv, acc[2][c]);
-        acc[3][c] = fma(g23.y, qv, acc[3][c]);
+        const double q = sQ[kk * p + tx + 16 * c];
+        acc[0][c] = fma(g01.x, q, acc[0][c]);
+        acc[1][c] = fma(g01.y, q, acc[1][c]);
+        acc[2][c] = fma(g23.x, q, acc[2][c]);
+        acc[3][c] = fma(g23.y, q, acc[3][c]);
       }
     }
+    if (more) store(buf ^ 1);
     __syncthreads();
   }
   double* Yp = Ypart + (int64_t)blockIdx.y * m * p;
@@ -281,14 +311,22 @@ __global__ void __launch_bounds__(512) jacobi_kernel(const double* __restrict__ 
         pq[tid][0] = P_; pq[tid][1] = Q_;
         const double app = A[P_ * ld + P_], aqq = A[Q_ * ld + Q_], apq = A[P_ * ld + Q_];
         double c = 1.0, s = 0.0;
-        if (fabs(apq) > 1e-300 && fabs(apq) > 1e-15 * sqrt(fabs(app) * fabs(aqq))) {
-          const double th = (aqq - app) / (2.0 * apq);
-          double t;
-          if (fabs(th) > 1e150) t = 0.5 / th;
-          else t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
-          c = 1.0 / sqrt(t * t + 1.0);
-          s = t * c;
-          rotated = 1;
+        const float apq32 = (float)apq;
+        if (fabs(apq) > 1e-15 * sqrt(fabs(app) * fabs(aqq)) && apq32 != 0.f) {
+          // tan of the rotation angle in fp32 (MUFU-speed); (c, s) are then built in fp64 so the
+          // rotation stays orthonormal to fp64 precision — a_pq shrinks by ~1e-7 per rotation and
+          // the sweeps converge as usual (K4).
+          const float th = (float)(aqq - app) * 0.5f / apq32;
+          float t32 = 0.f;
+          if (isfinite(th)) t32 = copysignf(1.0f, th) / (fabsf(th) + sqrtf(fmaf(th, th, 1.0f)));
+          const double t = (double)t32;
+          const double x = fma(t, t, 1.0);
+          double r = (double)rsqrtf((float)x);
+          r = r * (1.5 - 0.5 * x * r * r);
+          r = r * (1.5 - 0.5 * x * r * r);  // 1 / sqrt(1 + t^2) to fp64 accuracy
+          c = r;
+          s = t * r;
+          if (t32 != 0.f) rotated = 1;
         }
         cs[tid][0] = c; cs[tid][1] = s;
       }
@@ -445,7 +483,13 @@ avd_status gemm_g(Ctx* c, const double* In, double* Out) {
   const int64_t kchunk = round_up(ceil_div(m, ks), kGK);
   dim3 grid((unsigned)ceil_div(m, kGM), (unsigned)ks);
   switch (c->p / 16) {
-#define CASE(PC) case PC: gemm_gq_kernel<PC><<<grid, 128, 0, c->stream>>>(c->G, In, m, kchunk, c->Ypart); break;
+#define CASE(PC)                                                                                          \
+  case PC: {                                                                                              \
+    const int sm = 2 * (kGK * (kGM + 2) + kGK * PC * 16) * (int)sizeof(double);                           \
+    AVD_CUDA(cudaFuncSetAttribute(gemm_gq_kernel<PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));  \
+    gemm_gq_kernel<PC><<<grid, 128, sm, c->stream>>>(c->G, In, m, kchunk, c->Ypart);                      \
+    break;                                                                                                \
+  }
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
     default: set_error("unsupported p"); return AVD_EINVAL;
@@ -496,7 +540,7 @@ avd_status orth(Ctx* c, const double* Y, double* Q, uint32_t seed) {
   for (int pass = 0; pass < 2; ++pass) {
     const double* src = pass == 0 ? Y : Q;
     AVD_TRY(atb(c, src, src));
-    chol_inv_kernel<<<1, 512, sm, c->stream>>>(c->H, 1, p, c->W, bad);
+    chol_inv_kernel<<<1, 256, sm, c->stream>>>(c->H, 1, p, c->W, bad);
     AVD_LAUNCHED(c);
     AVD_TRY(matpp(c, src, Q, nullptr, nullptr, c->W));
     if (pass == 0) {
@@ -523,7 +567,7 @@ avd_status run_eig(Ctx* c) {
   AVD_LAUNCHED(c);
   AVD_TRY(orth(c, c->Z, c->Q, seed + 1));
   const int max_it = c->cfg.max_iters > 0 ? c->cfg.max_iters : 100;
-  const double tol = c->cfg.eig_tol > 0 ? c->cfg.eig_tol : 1e-9;
+  const double tol = c->cfg.eig_tol > 0 ? c->cfg.eig_tol : 1e-7;
   int it = 0, next_rr = 2, prev_it = 0, rr_count = 0;
   double maxres = 0.0, prev_res = -1.0;
   bool conv = false;
