@@ -108,7 +108,7 @@ typedef struct {
   int32_t iters;           /* subspace iterations used                                       */
   double max_resid;        /* max_r<k ||G v_r - lambda_r v_r|| / lambda_1                     */
   int32_t rr_checks;      /* Rayleigh-Ritz checks of the eigensolver (diagnostic)           */
-  int32_t jacobi_sweeps;   /* sweeps of the last p x p Jacobi (diagnostic)                   */
+  int32_t jacobi_sweeps;   /* total sweeps of the p x p Jacobi solves (diagnostic)           */
 } avd_outputs;
 
 typedef struct avd_ctx avd_ctx;

@@ -76,7 +76,7 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   C->r1 = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(4LL * C->num_sms, ncb), ceil_div(ll, 4)));
   C->cand_cap = std::min<int64_t>(ll * m, std::max<int64_t>(4 * n_top, 1 << 20));
   C->n_red = (int)ceil_div(m, kRedRowsC);  // partials of the m-length p x p reductions
-  C->gemm_ks = (int)std::max<int64_t>(1, std::min<int64_t>(8, ceil_div(2LL * C->num_sms, ceil_div(m, 32))));
+  C->gemm_ks = (int)std::max<int64_t>(1, std::min<int64_t>(8, ceil_div(2LL * C->num_sms, ceil_div(m, 64))));
   C->n_proj_ctas = (int)ceil_div(ll, 32);
   C->nwords = ceil_div(ll * m, 32);
   C->nblk = ceil_div(C->nwords, 1024);

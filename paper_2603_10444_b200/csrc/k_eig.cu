@@ -63,10 +63,10 @@ __global__ void rand_fill_kernel(double* __restrict__ Q, int64_t m, int p, uint3
 }
 
 // ---------------------------------------------------------------- Y = G Q  (split-K partials)
-// CTA: 32 rows of Y x all p columns, K range [kz*kchunk, (kz+1)*kchunk); 128 threads, each a
-// 4-row x (p/16)-column register tile; register-prefetched double buffer (the next K stage's
+// CTA: 64 rows of Y x all p columns, K range [kz*kchunk, (kz+1)*kchunk); 128 threads, each an
+// 8-row x (p/16)-column register tile; register-prefetched double buffer (the next K stage's
 // global loads are in flight while the current stage computes).  Ypart[kz][m][p].
-constexpr int kGM = 32;   // rows per CTA
+constexpr int kGM = 64;   // rows per CTA
 constexpr int kGK = 32;   // K per smem stage
 template <int PC>
 __global__ void __launch_bounds__(128) gemm_gq_kernel(const double* __restrict__ G, const double* __restrict__ Q,
@@ -77,13 +77,13 @@ __global__ void __launch_bounds__(128) gemm_gq_kernel(const double* __restrict__
   constexpr int SG = kGK * (kGM + 2);     // doubles of one transposed G tile [k][row]
   constexpr int SQ = kGK * p;
   extern __shared__ __align__(16) double gsm[];
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // rows 4ty..4ty+3, cols tx+16c
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // rows 8ty..8ty+7, cols tx+16c
   const int64_t r0 = (int64_t)blockIdx.x * kGM;
   const int64_t kbeg = (int64_t)blockIdx.y * kchunk;
   const int64_t kend = min(m, kbeg + kchunk);
-  double acc[4][PC];
+  double acc[8][PC];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < 8; ++a)
 #pragma unroll
     for (int c = 0; c < PC; ++c) acc[a][c] = 0.0;
   double gv[NG], qv[NQ];
@@ -125,15 +125,18 @@ __global__ void __launch_bounds__(128) gemm_gq_kernel(const double* __restrict__
     const double* sQ = sG + SG;
 #pragma unroll 8
     for (int kk = 0; kk < kGK; ++kk) {
-      const double2 g01 = *reinterpret_cast<const double2*>(sG + kk * (kGM + 2) + 4 * ty);
-      const double2 g23 = *reinterpret_cast<const double2*>(sG + kk * (kGM + 2) + 4 * ty + 2);
+      double g[8];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const double2 v = *reinterpret_cast<const double2*>(sG + kk * (kGM + 2) + 8 * ty + 2 * h);
+        g[2 * h] = v.x;
+        g[2 * h + 1] = v.y;
+      }
 #pragma unroll
       for (int c = 0; c < PC; ++c) {
         const double q = sQ[kk * p + tx + 16 * c];
-        acc[0][c] = fma(g01.x, q, acc[0][c]);
-        acc[1][c] = fma(g01.y, q, acc[1][c]);
-        acc[2][c] = fma(g23.x, q, acc[2][c]);
-        acc[3][c] = fma(g23.y, q, acc[3][c]);
+#pragma unroll
+        for (int a = 0; a < 8; ++a) acc[a][c] = fma(g[a], q, acc[a][c]);
       }
     }
     if (more) store(buf ^ 1);
@@ -141,8 +144,8 @@ __global__ void __launch_bounds__(128) gemm_gq_kernel(const double* __restrict__
   }
   double* Yp = Ypart + (int64_t)blockIdx.y * m * p;
 #pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    const int64_t r = r0 + 4 * ty + a;
+  for (int a = 0; a < 8; ++a) {
+    const int64_t r = r0 + 8 * ty + a;
     if (r < m)
 #pragma unroll
       for (int c = 0; c < PC; ++c) Yp[r * p + tx + 16 * c] = acc[a][c];
@@ -277,157 +280,216 @@ __device__ void load_sym(const double* __restrict__ part, int nparts, int p, dou
 }
 
 // ---------------------------------------------------------------- p x p symmetric Jacobi
-// W = eigenvectors (columns sorted by eigenvalue desc), evals = eigenvalues; stats[0] = sweeps
-__global__ void __launch_bounds__(512) jacobi_kernel(const double* __restrict__ part, int nparts, int p,
-                                                     double* __restrict__ Wout, double* __restrict__ evals,
-                                                     int* __restrict__ stats) {
+// Parallel round-robin Jacobi, one CTA of 16 warps.  In each of the p-1 steps of a sweep the p/2
+// disjoint pairs are owned by warps (pair i -> warp i % 16); lane 0 of the owner computes the
+// rotation (Rutishauser, fp32 seeds + Newton to fp64 accuracy) and broadcasts it by shuffle, the
+// warp rotates rows P,Q (lanes over columns), barrier, then columns P,Q of A and V (lanes over
+// rows), barrier.  W = eigenvectors (columns sorted by eigenvalue desc), evals; stats[0] = sweeps.
+constexpr int kJW = 16;  // warps
+__device__ __forceinline__ double rcp_fast(double x) {  // 1/x, MUFU seed + 2 Newton steps (~1 ulp)
+  double r = (double)(1.0f / (float)x);
+  r = r * fma(-x, r, 2.0);
+  return r * fma(-x, r, 2.0);
+}
+__device__ __forceinline__ double rsqrt_fast(double x) {  // 1/sqrt(x), x in the fp32 range
+  double r = (double)rsqrtf((float)x);
+  r = r * fma(-0.5 * x * r, r, 1.5);
+  return r * fma(-0.5 * x * r, r, 1.5);
+}
+__device__ __forceinline__ void jacobi_rotation(double app, double aqq, double apq, double& c, double& s, bool& rot) {
+  c = 1.0;
+  s = 0.0;
+  rot = false;
+  // skip when a_pq^2 <= 1e-26 a_pp a_qq (|a_pq| <= 1e-13 sqrt(a_pp a_qq)) or a_pq is below fp32 range
+  if (!(apq * apq > 1e-26 * fabs(app * aqq)) || fabs(apq) < 1e-30 || fabs(apq) > 1e30) return;
+  // Rutishauser: th = (a_qq - a_pp) / (2 a_pq), t = sign(th) / (|th| + sqrt(th^2 + 1))
+  const double th = 0.5 * (aqq - app) * rcp_fast(apq);
+  double t;
+  const double ath = fabs(th);
+  if (ath > 1e18) {
+    t = 0.5 / th;
+  } else {
+    const double y = fma(th, th, 1.0);
+    const double ri = rcp_fast(ath + y * rsqrt_fast(y));
+    t = th >= 0.0 ? ri : -ri;
+  }
+  c = rsqrt_fast(fma(t, t, 1.0));
+  s = t * c;
+  rot = true;
+}
+
+__device__ __forceinline__ void rr_pair(int p, int step, int i, int& P, int& Q) {
+  int a, b;
+  if (i == 0) { a = p - 1; b = step; }
+  else { a = (step + i) % (p - 1); b = (step - i + (p - 1)) % (p - 1); }
+  P = min(a, b);
+  Q = max(a, b);
+}
+
+__global__ void __launch_bounds__(kJW * 32) jacobi_kernel(const double* __restrict__ Hin, int p,
+                                                          double* __restrict__ Wout, double* __restrict__ evals,
+                                                          int* __restrict__ stats) {
   extern __shared__ double sm[];
   const int ld = p + 1;
   double* A = sm;
   double* V = sm + p * ld;
-  __shared__ double cs[kMaxP / 2][2];
-  __shared__ int pq[kMaxP / 2][2];
   __shared__ int rotated;
   __shared__ double dsh[kMaxP];
   __shared__ int rank_sh[kMaxP];
-  const int tid = threadIdx.x, nt = blockDim.x;
-  load_sym(part, nparts, p, A, ld);
-  for (int t = tid; t < p * p; t += nt) {
-    const int i = t / p, j = t % p;
-    V[i * ld + j] = (i == j) ? 1.0 : 0.0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ int escale;
+  if (warp == 0) {  // power-of-two scale 2^-e of the matrix (exact), so MUFU seeds stay in range
+    double d = 0.0;
+    for (int i = lane; i < p; i += 32) d = fmax(d, fabs(Hin[i * p + i]));
+    for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xFFFFFFFFu, d, o));
+    if (lane == 0) escale = (d > 0.0 && d < 1e300) ? ilogb(d) : 0;
   }
+  __syncthreads();
+  const int e = escale;
+  for (int i = warp; i < p; i += kJW)
+    for (int j = lane; j < p; j += 32) {
+      A[i * ld + j] = ldexp(0.5 * (Hin[i * p + j] + Hin[j * p + i]), -e);
+      V[i * ld + j] = (i == j) ? 1.0 : 0.0;
+    }
   __syncthreads();
   const int half = p / 2;
   int sweep = 0;
   for (; sweep < 30; ++sweep) {
-    if (tid == 0) rotated = 0;
+    if (threadIdx.x == 0) rotated = 0;
     __syncthreads();
+    int rot_any = 0;
     for (int step = 0; step < p - 1; ++step) {
-      if (tid < half) {
-        int a, b;
-        if (tid == 0) { a = p - 1; b = step; }
-        else { a = (step + tid) % (p - 1); b = (step - tid + (p - 1)) % (p - 1); }
-        const int P_ = min(a, b), Q_ = max(a, b);
-        pq[tid][0] = P_; pq[tid][1] = Q_;
-        const double app = A[P_ * ld + P_], aqq = A[Q_ * ld + Q_], apq = A[P_ * ld + Q_];
-        double c = 1.0, s = 0.0;
-        const float apq32 = (float)apq;
-        if (fabs(apq) > 1e-15 * sqrt(fabs(app) * fabs(aqq)) && apq32 != 0.f) {
-          // tan of the rotation angle in fp32 (MUFU-speed); (c, s) are then built in fp64 so the
-          // rotation stays orthonormal to fp64 precision — a_pq shrinks by ~1e-7 per rotation and
-          // the sweeps converge as usual (K4).
-          const float th = (float)(aqq - app) * 0.5f / apq32;
-          float t32 = 0.f;
-          if (isfinite(th)) t32 = copysignf(1.0f, th) / (fabsf(th) + sqrtf(fmaf(th, th, 1.0f)));
-          const double t = (double)t32;
-          const double x = fma(t, t, 1.0);
-          double r = (double)rsqrtf((float)x);
-          r = r * (1.5 - 0.5 * x * r * r);
-          r = r * (1.5 - 0.5 * x * r * r);  // 1 / sqrt(1 + t^2) to fp64 accuracy
-          c = r;
-          s = t * r;
-          if (t32 != 0.f) rotated = 1;
+      // ---- rows (J^T A) for the pairs owned by this warp
+      double cs_c[4], cs_s[4];
+      int pp[4], qq[4];
+      // lane u computes the rotation of this warp's u-th pair (all in parallel)
+      double myc = 1.0, mys = 0.0;
+      {
+        const int i = warp + kJW * lane;
+        if (lane < 4 && i < half) {
+          int P, Q;
+          rr_pair(p, step, i, P, Q);
+          bool rot;
+          jacobi_rotation(A[P * ld + P], A[Q * ld + Q], A[P * ld + Q], myc, mys, rot);
+          rot_any |= rot;
         }
-        cs[tid][0] = c; cs[tid][1] = s;
+      }
+      int np = 0;
+      for (int i = warp; i < half; i += kJW, ++np) {
+        int P, Q;
+        rr_pair(p, step, i, P, Q);
+        const double c = __shfl_sync(0xFFFFFFFFu, myc, np);
+        const double s = __shfl_sync(0xFFFFFFFFu, mys, np);
+        cs_c[np] = c; cs_s[np] = s; pp[np] = P; qq[np] = Q;
+        if (s != 0.0) {
+          for (int col = lane; col < p; col += 32) {
+            const double ap = A[P * ld + col], aq = A[Q * ld + col];
+            A[P * ld + col] = c * ap - s * aq;
+            A[Q * ld + col] = s * ap + c * aq;
+          }
+        }
       }
       __syncthreads();
-      for (int t = tid; t < half * p; t += nt) {  // rows: A <- J^T A
-        const int i = t / p, col = t % p;
-        const double s = cs[i][1];
+      // ---- columns (A J, V J)
+      for (int u = 0; u < np; ++u) {
+        const double c = cs_c[u], s = cs_s[u];
         if (s == 0.0) continue;
-        const double c = cs[i][0];
-        const int P_ = pq[i][0], Q_ = pq[i][1];
-        const double ap = A[P_ * ld + col], aq = A[Q_ * ld + col];
-        A[P_ * ld + col] = c * ap - s * aq;
-        A[Q_ * ld + col] = s * ap + c * aq;
-      }
-      __syncthreads();
-      for (int t = tid; t < half * p; t += nt) {  // columns: A <- A J, V <- V J
-        const int i = t / p, row = t % p;
-        const double s = cs[i][1];
-        if (s == 0.0) continue;
-        const double c = cs[i][0];
-        const int P_ = pq[i][0], Q_ = pq[i][1];
-        const double ap = A[row * ld + P_], aq = A[row * ld + Q_];
-        A[row * ld + P_] = c * ap - s * aq;
-        A[row * ld + Q_] = s * ap + c * aq;
-        const double vp = V[row * ld + P_], vq = V[row * ld + Q_];
-        V[row * ld + P_] = c * vp - s * vq;
-        V[row * ld + Q_] = s * vp + c * vq;
+        const int P = pp[u], Q = qq[u];
+        for (int row = lane; row < p; row += 32) {
+          const double ap = A[row * ld + P], aq = A[row * ld + Q];
+          A[row * ld + P] = c * ap - s * aq;
+          A[row * ld + Q] = s * ap + c * aq;
+          const double vp = V[row * ld + P], vq = V[row * ld + Q];
+          V[row * ld + P] = c * vp - s * vq;
+          V[row * ld + Q] = s * vp + c * vq;
+        }
       }
       __syncthreads();
     }
+    if (rot_any) rotated = 1;
+    __syncthreads();
     if (!rotated) break;
   }
-  if (tid < p) dsh[tid] = A[tid * ld + tid];
+  if (threadIdx.x < p) dsh[threadIdx.x] = A[threadIdx.x * ld + threadIdx.x];
   __syncthreads();
-  if (tid < p) {
+  if (threadIdx.x < p) {
     int rk = 0;
-    const double di = dsh[tid];
-    for (int j = 0; j < p; ++j) rk += (dsh[j] > di) || (dsh[j] == di && j < tid);
-    rank_sh[tid] = rk;
+    const double di = dsh[threadIdx.x];
+    for (int j = 0; j < p; ++j) rk += (dsh[j] > di) || (dsh[j] == di && j < (int)threadIdx.x);
+    rank_sh[threadIdx.x] = rk;
   }
   __syncthreads();
-  for (int t = tid; t < p * p; t += nt) {
-    const int row = t / p, i = t % p;
-    Wout[row * p + rank_sh[i]] = V[row * ld + i];
-  }
-  if (tid < p) evals[rank_sh[tid]] = dsh[tid];
-  if (tid == 0 && stats) stats[0] = sweep + 1;
+  for (int row = warp; row < p; row += kJW)
+    for (int i = lane; i < p; i += 32) Wout[row * p + rank_sh[i]] = V[row * ld + i];
+  if (threadIdx.x < p) evals[rank_sh[threadIdx.x]] = ldexp(dsh[threadIdx.x], e);
+  if (threadIdx.x == 0 && stats) stats[0] = sweep + 1;
 }
 
 // ---------------------------------------------------------------- Cholesky-QR step
-// B = sum(part) (p x p) = R^T R; Rinv = R^{-1} (upper); columns whose pivot is <= 1e-13 of the
-// largest diagonal are flagged bad[c] = 1 and get a zero Rinv column.
-__global__ void __launch_bounds__(512) chol_inv_kernel(const double* __restrict__ part, int nparts, int p,
-                                                       double* __restrict__ Rinv, int* __restrict__ bad) {
+// B = H (p x p, symmetrised) = R^T R; Rinv = R^{-1} (upper).  Columns whose pivot is <= 1e-13 of
+// the largest diagonal are flagged bad[c] = 1 and get a zero Rinv column.  16 warps, rows owned
+// by warps and lanes over columns; every thread recomputes the pivot (no serial section).
+__global__ void __launch_bounds__(kJW * 32) chol_inv_kernel(const double* __restrict__ Hin, int p,
+                                                            double* __restrict__ Rinv, int* __restrict__ bad) {
   extern __shared__ double sm[];
   const int ld = p + 1;
   double* B = sm;           // becomes R (upper)
   double* X = sm + p * ld;  // Rinv
   __shared__ int badsh[kMaxP];
-  __shared__ double dmax;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  load_sym(part, nparts, p, B, ld);
+  __shared__ double dmax_sh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = warp; i < p; i += kJW)
+    for (int j = lane; j < p; j += 32) {
+      B[i * ld + j] = 0.5 * (Hin[i * p + j] + Hin[j * p + i]);
+      X[i * ld + j] = 0.0;
+    }
   __syncthreads();
-  if (tid == 0) {
+  if (warp == 0) {
     double d = 0.0;
-    for (int i = 0; i < p; ++i) d = fmax(d, B[i * ld + i]);
-    dmax = d;
+    for (int i = lane; i < p; i += 32) d = fmax(d, B[i * ld + i]);
+    for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xFFFFFFFFu, d, o));
+    if (lane == 0) dmax_sh = d;
   }
   __syncthreads();
-  const double tol = 1e-13 * dmax;
+  // exact even power-of-two normalisation: B' = B 2^-e2, R = R' 2^(e2/2), Rinv = Rinv' 2^-(e2/2)
+  const int e2 = (dmax_sh > 0.0 && dmax_sh < 1e300) ? 2 * (ilogb(dmax_sh) / 2) : 0;
+  for (int i = warp; i < p; i += kJW)
+    for (int j = lane; j < p; j += 32) B[i * ld + j] = ldexp(B[i * ld + j], -e2);
+  __syncthreads();
+  const double tol = 1e-13 * ldexp(dmax_sh, -e2);
   for (int j = 0; j < p; ++j) {
     const double d = B[j * ld + j];
     const bool ok = d > tol && d > 0.0;
-    const double rjj = ok ? sqrt(d) : 0.0;
-    __syncthreads();  // everyone read d before row j is rewritten
-    if (tid == 0) { badsh[j] = ok ? 0 : 1; B[j * ld + j] = rjj; }
-    for (int k = j + 1 + tid; k < p; k += nt) B[j * ld + k] = ok ? B[j * ld + k] / rjj : 0.0;
+    const double inv = ok ? rsqrt_fast(d) : 0.0;   // 1 / R_jj
+    const double rjj = d * inv;
+    // trailing update with the row of R computed on the fly: B[i][k] -= R[j][i] R[j][k]
+    for (int i = j + 1 + warp; i < p; i += kJW) {
+      const double rji = B[j * ld + i] * inv;
+      for (int k = i + lane; k < p; k += 32) B[i * ld + k] -= rji * (B[j * ld + k] * inv);
+    }
     __syncthreads();
-    const int rem = p - j - 1;
-    for (int t = tid; t < rem * rem; t += nt) {  // trailing update (upper part only)
-      const int i = j + 1 + t / rem, k = j + 1 + t % rem;
-      if (k >= i) B[i * ld + k] -= B[j * ld + i] * B[j * ld + k];
+    if (warp == 0) {
+      for (int k = j + 1 + lane; k < p; k += 32) B[j * ld + k] *= inv;
+      if (lane == 0) { B[j * ld + j] = rjj; badsh[j] = ok ? 0 : 1; }
     }
     __syncthreads();
   }
-  // Rinv = R^{-1} row by row from the bottom (X[i][.] accumulates sum_{k>i} R[i][k] Rinv[k][.])
-  for (int t = tid; t < p * p; t += nt) X[(t / p) * ld + (t % p)] = 0.0;
-  __syncthreads();
+  // Rinv = R^{-1} from the bottom row up; X[i][.] accumulates sum_{k>i} R[i][k] Rinv[k][.]
   for (int j = p - 1; j >= 0; --j) {
     const bool okj = !badsh[j];
-    const double inv = okj ? 1.0 / B[j * ld + j] : 0.0;
-    for (int cc = tid; cc < p; cc += nt) X[j * ld + cc] = okj ? (((cc == j) ? 1.0 : 0.0) - X[j * ld + cc]) * inv : 0.0;
+    const double inv = okj ? rcp_fast(B[j * ld + j]) : 0.0;
+    if (warp == 0)
+      for (int cc = lane; cc < p; cc += 32) X[j * ld + cc] = okj ? (((cc == j) ? 1.0 : 0.0) - X[j * ld + cc]) * inv : 0.0;
     __syncthreads();
-    for (int t = tid; t < j * p; t += nt) {
-      const int i = t / p, cc = t % p;
-      X[i * ld + cc] = fma(B[i * ld + j], X[j * ld + cc], X[i * ld + cc]);
+    for (int i = warp; i < j; i += kJW) {
+      const double rij = B[i * ld + j];
+      for (int cc = j + lane; cc < p; cc += 32) X[i * ld + cc] = fma(rij, X[j * ld + cc], X[i * ld + cc]);
     }
     __syncthreads();
   }
-  for (int t = tid; t < p * p; t += nt) Rinv[t] = X[(t / p) * ld + (t % p)];
-  for (int c = tid; c < p; c += nt) bad[c] = badsh[c];
+  for (int i = warp; i < p; i += kJW)
+    for (int cc = lane; cc < p; cc += 32) Rinv[i * p + cc] = ldexp(X[i * ld + cc], -e2 / 2);
+  for (int cc = threadIdx.x; cc < p; cc += blockDim.x) bad[cc] = badsh[cc];
 }
 
 // V_out[j][r] = sign_r * U[j][r] (r < k), sign making the largest-|.| entry positive
@@ -540,7 +602,7 @@ avd_status orth(Ctx* c, const double* Y, double* Q, uint32_t seed) {
   for (int pass = 0; pass < 2; ++pass) {
     const double* src = pass == 0 ? Y : Q;
     AVD_TRY(atb(c, src, src));
-    chol_inv_kernel<<<1, 256, sm, c->stream>>>(c->H, 1, p, c->W, bad);
+    chol_inv_kernel<<<1, kJW * 32, sm, c->stream>>>(c->H, p, c->W, bad);
     AVD_LAUNCHED(c);
     AVD_TRY(matpp(c, src, Q, nullptr, nullptr, c->W));
     if (pass == 0) {
@@ -560,7 +622,8 @@ avd_status run_eig(Ctx* c) {
   const int64_t m = c->cfg.m;
   const int p = c->p, k = c->k;
   const uint32_t seed = (uint32_t)(c->cfg.seed ^ (c->cfg.seed >> 32)) * 2654435761u + 12345u;
-  int* jstats = reinterpret_cast<int*>(c->theta + p);
+  int* jstats = reinterpret_cast<int*>(c->theta + p);  // [16] sweeps per RR solve
+  AVD_CUDA(cudaMemsetAsync(jstats, 0, 16 * sizeof(int), c->stream));
   const size_t jsm = 2 * (size_t)p * (p + 1) * sizeof(double);
   AVD_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jsm));
   rand_fill_kernel<<<(unsigned)ceil_div(m * p, 256), 256, 0, c->stream>>>(c->Z, m, p, seed, nullptr);
@@ -576,7 +639,7 @@ avd_status run_eig(Ctx* c) {
     if (it == next_rr || it == max_it) {
       ++rr_count;
       AVD_TRY(atb(c, c->Q, c->Y));                          // H = Q^T Y
-      jacobi_kernel<<<1, 512, jsm, c->stream>>>(c->H, 1, p, c->W, c->theta, jstats);
+      jacobi_kernel<<<1, kJW * 32, jsm, c->stream>>>(c->H, p, c->W, c->theta, jstats + std::min(rr_count - 1, 15));
       AVD_LAUNCHED(c);
       AVD_TRY(matpp(c, c->Y, c->Z, c->Q, c->U, c->W));      // Z = Y W, U = Q W (Ritz vectors)
       resid_kernel<<<k, 256, 0, c->stream>>>(c->Z, c->U, c->theta, m, p, c->resid);
@@ -612,7 +675,11 @@ avd_status run_eig(Ctx* c) {
   c->rr_count = rr_count;
   c->max_resid = maxres;
   c->sigma_next = (k < p) ? std::sqrt(std::max(c->eig_host[k], 0.0)) : 0.0;
-  AVD_CUDA(cudaMemcpyAsync(&c->jacobi_sweeps, jstats, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  int sw[16];
+  AVD_CUDA(cudaMemcpyAsync(sw, jstats, sizeof(sw), cudaMemcpyDeviceToHost, c->stream));
+  AVD_CUDA(cudaStreamSynchronize(c->stream));
+  c->jacobi_sweeps = 0;
+  for (int q = 0; q < std::min(rr_count, 16); ++q) c->jacobi_sweeps += sw[q];  // total over all RR solves
   AVD_CUDA(cudaMemsetAsync(c->V32, 0, sizeof(float) * m * c->k_pad, c->stream));
   finalize_vectors_kernel<<<k, 256, 0, c->stream>>>(c->U, c->theta, m, p, k, c->k_pad, c->V, c->sigma, c->V32);
   AVD_LAUNCHED(c);

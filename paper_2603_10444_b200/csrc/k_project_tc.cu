@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(kPThreads, 1) proj_tc_kernel(
   constexpr int KP32 = (KP + 31) / 32 * 32;
   constexpr int NSLOT_MAX = (512 / KP) < 8 ? (512 / KP) : 8;
   constexpr uint32_t kVtBytes = 2 * KP * 128;
-  constexpr uint32_t kStage = 3 * kTile + ((kVtBytes + 1023) / 1024) * 1024;
+  constexpr uint32_t kStage = 2 * kTile + ((kVtBytes + 1023) / 1024) * 1024;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full_bar[NS], conv_bar[NS], empty_bar[NS], tfull_bar, tempty_bar;
@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(kPThreads, 1) proj_tc_kernel(
           uint8_t* st = smem + s * kStage;
           mbar_arrive_expect_tx(&full_bar[s], kTile + kVtBytes);
           tma_load_2d(st, &tmX, &full_bar[s], c * 32, (int32_t)(rb * 128));
-          tma_load_2d(st + 3 * kTile, &tmVt, &full_bar[s], c * 32, 0);
+          tma_load_2d(st + 2 * kTile, &tmVt, &full_bar[s], c * 32, 0);
         }
       }
     }
@@ -124,10 +124,10 @@ __global__ void __launch_bounds__(kPThreads, 1) proj_tc_kernel(
           const uint32_t d = tmem + slot * KP;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            const uint64_t ahi = smem_desc(base + kTile + kk * 32, 16, 1024, 2);
-            const uint64_t alo = smem_desc(base + 2 * kTile + kk * 32, 16, 1024, 2);
-            const uint64_t bhi = smem_desc(base + 3 * kTile + kk * 32, 16, 1024, 2);
-            const uint64_t blo = smem_desc(base + 3 * kTile + KP * 128 + kk * 32, 16, 1024, 2);
+            const uint64_t ahi = smem_desc(base + kk * 32, 16, 1024, 2);
+            const uint64_t alo = smem_desc(base + kTile + kk * 32, 16, 1024, 2);
+            const uint64_t bhi = smem_desc(base + 2 * kTile + kk * 32, 16, 1024, 2);
+            const uint64_t blo = smem_desc(base + 2 * kTile + KP * 128 + kk * 32, 16, 1024, 2);
             mma_tf32(d, ahi, bhi, idesc, (slot_first && kk == 0) ? 0u : 1u);
             mma_tf32(d, ahi, blo, idesc, 1u);
             mma_tf32(d, alo, bhi, idesc, 1u);
@@ -163,8 +163,8 @@ __global__ void __launch_bounds__(kPThreads, 1) proj_tc_kernel(
         mbar_wait(&full_bar[s], r & 1);
         uint8_t* st = smem + s * kStage;
         const float4* xs = reinterpret_cast<const float4*>(st);
-        float4* hs = reinterpret_cast<float4*>(st + kTile);
-        float4* ls = reinterpret_cast<float4*>(st + 2 * kTile);
+        float4* hs = reinterpret_cast<float4*>(st);          // hi overwrites x in place
+        float4* ls = reinterpret_cast<float4*>(st + kTile);
         float s32 = 0.f;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -251,16 +251,20 @@ __global__ void __launch_bounds__(kPThreads, 1) proj_tc_kernel(
 }
 
 // ======================================================================= K8
+// Stage ring: V hi/lo tiles (B operand) + the matching X tile (for the epilogue), both by TMA.
+// A stage is released when the MMA has consumed it AND the 8 epilogue warps have read its X.
 template <int KP32, int NCOL, int NS>
 __global__ void __launch_bounds__(kPThreads, 1) energy_tc_kernel(
-    const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmV, const float* __restrict__ X,
-    int64_t l_local, int64_t m, int64_t l_pad, int64_t m_pad128, const float* __restrict__ mu_hl, int64_t m_pad,
-    double* __restrict__ en_part) {
+    const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmV,
+    const __grid_constant__ CUtensorMap tmX, int64_t l_local, int64_t m, int64_t l_pad, int64_t m_pad128,
+    const float* __restrict__ mu_hl, int64_t m_pad, double* __restrict__ en_part) {
   constexpr int NA = KP32 / 32;                       // 32-wide K atoms
+  constexpr int NXB = NCOL / 32;                      // X boxes (32 columns) per chunk
   constexpr uint32_t kATile = kTile;                  // 128 rows x 128 B
   constexpr uint32_t kBTile = NCOL * 128;             // NCOL rows x 128 B
-  constexpr uint32_t kA = 2 * NA * kATile;            // hi + lo
-  constexpr uint32_t kStage = 2 * NA * kBTile;        // hi + lo
+  constexpr uint32_t kA = 2 * NA * kATile;            // P hi + lo
+  constexpr uint32_t kVB = 2 * NA * kBTile;           // V hi + lo
+  constexpr uint32_t kStage = kVB + NXB * kTile;      // + X tile
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -275,12 +279,12 @@ __global__ void __launch_bounds__(kPThreads, 1) energy_tc_kernel(
   if (threadIdx.x == 0) {
     mbar_init(&afull_bar, 1);
     mbar_init(&aempty_bar, 1);
-    for (int s = 0; s < NS; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
+    for (int s = 0; s < NS; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1 + 8); }
     for (int b = 0; b < 2; ++b) { mbar_init(&tfull_bar[b], 1); mbar_init(&tempty_bar[b], 8); }
     fence_mbar_init();
   }
-  if (warp == 0 && lane == 0) { tma_prefetch(&tmP); tma_prefetch(&tmV); }
-  if (warp == 1) tmem_alloc<2 * NCOL>(&tmem_sh);
+  if (warp == 0 && lane == 0) { tma_prefetch(&tmP); tma_prefetch(&tmV); tma_prefetch(&tmX); }
+  if (warp == 1) tmem_alloc<(2 * NCOL < 32 ? 32 : 2 * NCOL)>(&tmem_sh);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -307,6 +311,9 @@ __global__ void __launch_bounds__(kPThreads, 1) energy_tc_kernel(
 #pragma unroll
             for (int a = 0; a < NA; ++a)
               tma_load_2d(st + (h * NA + a) * kBTile, &tmV, &full_bar[s], a * 32, (int32_t)(h * m_pad128 + c * NCOL));
+#pragma unroll
+          for (int xb = 0; xb < NXB; ++xb)
+            tma_load_2d(st + kVB + xb * kTile, &tmX, &full_bar[s], c * NCOL + xb * 32, (int32_t)(rb * 128));
         }
       }
     }
@@ -350,41 +357,36 @@ __global__ void __launch_bounds__(kPThreads, 1) energy_tc_kernel(
     const int ew = warp - 2;
     const uint32_t q = warp & 3;
     const int half = ew >> 2;
+    const int rloc = q * 32 + lane;                   // row inside the 128-row tile
     double eS = 0.0, eT = 0.0, eST = 0.0;
-    uint32_t ci = 0;
+    uint32_t it = 0, ci = 0;
     for (int64_t rb = blockIdx.x; rb < nrb; rb += gridDim.x) {
-      const int64_t row = rb * 128 + q * 32 + lane;
-      const bool rok = row < l_local;
-      const float* xrow = X + (rok ? row : 0) * m;
-      for (int c = 0; c < NC; ++c, ++ci) {
+      const bool rok = rb * 128 + rloc < l_local;
+      for (int c = 0; c < NC; ++c, ++it, ++ci) {
+        const uint32_t s = it % NS, r = it / NS;
         const uint32_t b = ci & 1, br = ci >> 1;
+        mbar_wait(&full_bar[s], r & 1);
         mbar_wait(&tfull_bar[b], br & 1);
         tc_fence_after();
         const uint32_t tb = tmem + ((q * 32) << 16) + b * NCOL;
+        const uint8_t* sx = sB + s * kStage + kVB;
         float s2 = 0.f, t2 = 0.f, st = 0.f;
-#pragma unroll 1
+#pragma unroll
         for (int c0 = half * (NCOL / 2); c0 < (half + 1) * (NCOL / 2); c0 += 16) {
           uint32_t rv[16];
           tmem_ld16(tb + c0, rv);
           const int64_t j0 = (int64_t)c * NCOL + c0;
           float xv[16], mh[16], ml[16];
+          const float4* xrow = reinterpret_cast<const float4*>(sx + (c0 / 32) * kTile + rloc * 128);
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const float4 a = __ldg(reinterpret_cast<const float4*>(mu_hl + j0) + t);
-            const float4 bb = __ldg(reinterpret_cast<const float4*>(mu_hl + m_pad + j0) + t);
-            mh[4 * t] = a.x; mh[4 * t + 1] = a.y; mh[4 * t + 2] = a.z; mh[4 * t + 3] = a.w;
-            ml[4 * t] = bb.x; ml[4 * t + 1] = bb.y; ml[4 * t + 2] = bb.z; ml[4 * t + 3] = bb.w;
-          }
-          if (rok && j0 + 16 <= m) {
-            const float4* src = reinterpret_cast<const float4*>(xrow + j0);
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              const float4 v = __ldg(src + t);
-              xv[4 * t] = v.x; xv[4 * t + 1] = v.y; xv[4 * t + 2] = v.z; xv[4 * t + 3] = v.w;
-            }
-          } else {
-#pragma unroll
-            for (int t = 0; t < 16; ++t) xv[t] = (rok && j0 + t < m) ? xrow[j0 + t] : 0.f;
+          for (int u = 0; u < 4; ++u) {
+            const int g = ((c0 % 32) >> 2) + u;       // logical 16-byte group of the row
+            const float4 v = xrow[g ^ (rloc & 7)];    // SWIZZLE_128B
+            xv[4 * u] = v.x; xv[4 * u + 1] = v.y; xv[4 * u + 2] = v.z; xv[4 * u + 3] = v.w;
+            const float4 a = __ldg(reinterpret_cast<const float4*>(mu_hl + j0) + u);
+            const float4 bb = __ldg(reinterpret_cast<const float4*>(mu_hl + m_pad + j0) + u);
+            mh[4 * u] = a.x; mh[4 * u + 1] = a.y; mh[4 * u + 2] = a.z; mh[4 * u + 3] = a.w;
+            ml[4 * u] = bb.x; ml[4 * u + 1] = bb.y; ml[4 * u + 2] = bb.z; ml[4 * u + 3] = bb.w;
           }
           tmem_ld_wait();
 #pragma unroll
@@ -403,7 +405,10 @@ __global__ void __launch_bounds__(kPThreads, 1) energy_tc_kernel(
         eST += (double)st;
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty_bar[b]);
+        if (lane == 0) {
+          mbar_arrive(&tempty_bar[b]);
+          mbar_arrive(&empty_bar[s]);
+        }
       }
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -420,7 +425,7 @@ __global__ void __launch_bounds__(kPThreads, 1) energy_tc_kernel(
     for (int w = 0; w < 8; ++w) t += red[w][threadIdx.x];
     en_part[(int64_t)blockIdx.x * 4 + threadIdx.x] = t;
   }
-  if (warp == 1) tmem_dealloc<2 * NCOL>(tmem);
+  if (warp == 1) tmem_dealloc<(2 * NCOL < 32 ? 32 : 2 * NCOL)>(tmem);
 }
 
 CUresult encode2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
@@ -436,8 +441,8 @@ CUresult encode2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t o
 
 template <int KP>
 avd_status launch_k5(Ctx* c, const CUtensorMap& tmX, const CUtensorMap& tmVt, int grid) {
-  constexpr int NS = 3;
-  constexpr uint32_t kStage = 3 * kTile + ((2 * KP * 128 + 1023) / 1024) * 1024;
+  constexpr uint32_t kStage = 2 * kTile + ((2 * KP * 128 + 1023) / 1024) * 1024;
+  constexpr int NS = (200 * 1024) / kStage;  // 4-5 stages in flight
   const size_t smem = NS * kStage + 1024;
   AVD_CUDA(cudaFuncSetAttribute(proj_tc_kernel<KP, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   proj_tc_kernel<KP, NS><<<grid, kPThreads, smem, c->stream>>>(tmX, tmVt, c->cfg.l_local, c->cfg.m, c->mu_hl,
@@ -448,14 +453,14 @@ avd_status launch_k5(Ctx* c, const CUtensorMap& tmX, const CUtensorMap& tmVt, in
 }
 
 template <int KP32, int NCOL>
-avd_status launch_k8(Ctx* c, const float* X, const CUtensorMap& tmP, const CUtensorMap& tmV, int grid) {
-  constexpr int NS = 2;
+avd_status launch_k8(Ctx* c, const CUtensorMap& tmP, const CUtensorMap& tmV, const CUtensorMap& tmX, int grid) {
   constexpr uint32_t kA = 2 * (KP32 / 32) * kTile;
-  constexpr uint32_t kStage = 2 * (KP32 / 32) * NCOL * 128;
+  constexpr uint32_t kStage = 2 * (KP32 / 32) * NCOL * 128 + (NCOL / 32) * kTile;
+  constexpr int NS = 2;
   const size_t smem = kA + NS * kStage + 1024;
   AVD_CUDA(cudaFuncSetAttribute(energy_tc_kernel<KP32, NCOL, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
-  energy_tc_kernel<KP32, NCOL, NS><<<grid, kPThreads, smem, c->stream>>>(tmP, tmV, X, c->cfg.l_local, c->cfg.m,
+  energy_tc_kernel<KP32, NCOL, NS><<<grid, kPThreads, smem, c->stream>>>(tmP, tmV, tmX, c->cfg.l_local, c->cfg.m,
                                                                          c->l_pad, c->m_pad, c->mu_hl, c->m_pad,
                                                                          c->en_part);
   AVD_LAUNCHED(c);
@@ -487,7 +492,7 @@ avd_status launch_project_tc(Ctx* c, const float* X) {
   if (encode2d(&tmX, X, c->cfg.m, c->cfg.l_local, c->cfg.m * 4, 32, 128) != CUDA_SUCCESS ||
       encode2d(&tmVt, c->Vt_hl, c->m_pad32, 2 * KP, c->m_pad32 * 4, 32, 2 * KP) != CUDA_SUCCESS ||
       encode2d(&tmP, c->P_hl, KP32, 2 * c->l_pad, KP32 * 4, 32, 128) != CUDA_SUCCESS ||
-      encode2d(&tmV, c->V_hl, KP32, 2 * c->m_pad, KP32 * 4, 32, KP32 <= 64 ? 128 : 64) != CUDA_SUCCESS) {
+      encode2d(&tmV, c->V_hl, KP32, 2 * c->m_pad, KP32 * 4, 32, KP32 <= 64 ? 64 : 32) != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (projection maps)");
     return AVD_ECUDA;
   }
@@ -504,9 +509,9 @@ avd_status launch_project_tc(Ctx* c, const float* X) {
     default: set_error("unsupported k_pad"); return AVD_EINVAL;
   }
   switch (KP32) {
-    case 32: AVD_TRY((launch_k8<32, 128>(c, X, tmP, tmV, grid))); break;
-    case 64: AVD_TRY((launch_k8<64, 128>(c, X, tmP, tmV, grid))); break;
-    case 96: AVD_TRY((launch_k8<96, 64>(c, X, tmP, tmV, grid))); break;
+    case 32: AVD_TRY((launch_k8<32, 64>(c, tmP, tmV, tmX, grid))); break;
+    case 64: AVD_TRY((launch_k8<64, 64>(c, tmP, tmV, tmX, grid))); break;
+    case 96: AVD_TRY((launch_k8<96, 32>(c, tmP, tmV, tmX, grid))); break;
     default: set_error("unsupported k_pad"); return AVD_EINVAL;
   }
   return AVD_OK;

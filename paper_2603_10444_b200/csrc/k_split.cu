@@ -27,18 +27,47 @@ __device__ __forceinline__ uint32_t mix32(uint32_t x) {
   return x;
 }
 
-template <int ND>
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src, bool valid) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(valid ? 4 : 0) : "memory");
+}
+
+template <int ND, bool VEC>
 __global__ void __launch_bounds__(kSplitThreads) split_kernel(
     const float* __restrict__ X, int64_t l_local, int64_t m, int64_t m_pad, int64_t l_pad,
     int64_t row_offset, const float* __restrict__ mu_hl, const int32_t* __restrict__ shift,
     uint32_t seed32, int8_t* __restrict__ digits, const DevPlan* __restrict__ dp,
     uint32_t* __restrict__ cand_key, uint64_t* __restrict__ cand_idx,
     unsigned long long* __restrict__ cand_cnt, int64_t cand_cap) {
+  extern __shared__ __align__(16) float sX[];  // [kSplitRows][kSplitCols] tile of X (cp.async)
   __shared__ uint32_t sD[ND][kSplitCols * kSW];
   __shared__ uint32_t srow[kSplitRows];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t i0 = (int64_t)blockIdx.x * kSplitRows;
   const int64_t j0 = (int64_t)blockIdx.y * kSplitCols;
+  // ---- stage the whole 128 x 64 tile with asynchronous copies (32 KB in flight per CTA)
+  if (VEC) {
+#pragma unroll
+    for (int u = 0; u < (kSplitRows * kSplitCols / 4) / kSplitThreads; ++u) {
+      const int id = threadIdx.x + kSplitThreads * u;
+      const int r = id / (kSplitCols / 4), cq = id % (kSplitCols / 4);
+      const int64_t gi = i0 + r, gj = j0 + cq * 4;
+      const bool v = gi < l_local && gj < m;
+      cp_async16(sX + r * kSplitCols + cq * 4, v ? (const void*)(X + gi * m + gj) : (const void*)X, v);
+    }
+  } else {
+    for (int id = threadIdx.x; id < kSplitRows * kSplitCols; id += kSplitThreads) {
+      const int r = id / kSplitCols, cc = id % kSplitCols;
+      const int64_t gi = i0 + r, gj = j0 + cc;
+      const bool v = gi < l_local && gj < m;
+      cp_async4(sX + r * kSplitCols + cc, v ? (const void*)(X + gi * m + gj) : (const void*)X, v);
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   const int jl = (warp & 1) * 32 + lane;
   const int64_t j = j0 + jl;
   const int rg = warp >> 1;  // 32-row group
@@ -52,16 +81,14 @@ __global__ void __launch_bounds__(kSplitThreads) split_kernel(
   const int sh = colok ? shift[j] : 0;
   const float scale = (colok && sh <= 126 && sh >= -126) ? __int_as_float((sh + 127) << 23) : 0.f;
   const uint32_t colh = mix32((uint32_t)j ^ 0x68E31DA4u);
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
 
 #pragma unroll 1
   for (int t = 0; t < 8; ++t) {
     float xs[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t i = i0 + rg * 32 + t * 4 + u;
-      xs[u] = (colok && i < l_local) ? __ldcs(X + i * m + j) : 0.f;
-    }
+    for (int u = 0; u < 4; ++u) xs[u] = sX[(rg * 32 + t * 4 + u) * kSplitCols + jl];
     uint32_t packed[ND];
 #pragma unroll
     for (int d = 0; d < ND; ++d) packed[d] = 0;
@@ -136,14 +163,18 @@ avd_status launch_split(Ctx* c, const float* X) {
   AVD_CUDA(cudaMemsetAsync(c->cand_cnt, 0, sizeof(unsigned long long), c->stream));
   dim3 grid((unsigned)(c->l_pad / kSplitRows), (unsigned)(c->m_pad / kSplitCols));
   const uint32_t seed32 = (uint32_t)(c->cfg.seed * 0x9E3779B97F4A7C15ull >> 32) ^ 0xA5A5A5A5u;
-  if (c->nd == 2)
-    split_kernel<2><<<grid, kSplitThreads, 0, c->stream>>>(
-        X, c->cfg.l_local, c->cfg.m, c->m_pad, c->l_pad, c->cfg.row_offset, c->mu_hl, c->shift, seed32,
-        c->digits, c->dplan, c->cand_key, c->cand_idx, c->cand_cnt, c->cand_cap);
-  else
-    split_kernel<3><<<grid, kSplitThreads, 0, c->stream>>>(
-        X, c->cfg.l_local, c->cfg.m, c->m_pad, c->l_pad, c->cfg.row_offset, c->mu_hl, c->shift, seed32,
-        c->digits, c->dplan, c->cand_key, c->cand_idx, c->cand_cnt, c->cand_cap);
+  const bool vec = (c->cfg.m % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
+  const size_t sm = sizeof(float) * kSplitRows * kSplitCols;
+#define LAUNCH(ND, V)                                                                                         \
+  do {                                                                                                        \
+    AVD_CUDA(cudaFuncSetAttribute(split_kernel<ND, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+    split_kernel<ND, V><<<grid, kSplitThreads, sm, c->stream>>>(                                              \
+        X, c->cfg.l_local, c->cfg.m, c->m_pad, c->l_pad, c->cfg.row_offset, c->mu_hl, c->shift, seed32,       \
+        c->digits, c->dplan, c->cand_key, c->cand_idx, c->cand_cnt, c->cand_cap);                             \
+  } while (0)
+  if (c->nd == 2) { if (vec) LAUNCH(2, true); else LAUNCH(2, false); }
+  else { if (vec) LAUNCH(3, true); else LAUNCH(3, false); }
+#undef LAUNCH
   AVD_LAUNCHED(c);
   cand_publish_kernel<<<1, 1, 0, c->stream>>>(c->cand_cnt, c->cand_cap, c->cand_x);
   AVD_LAUNCHED(c);
