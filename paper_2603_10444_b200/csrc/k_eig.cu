@@ -69,7 +69,7 @@ __global__ void rand_fill_kernel(double* __restrict__ Q, int64_t m, int p, uint3
 constexpr int kGM = 64;   // rows per CTA
 constexpr int kGK = 32;   // K per smem stage
 template <int PC>
-__global__ void __launch_bounds__(128) gemm_gq_kernel(const double* __restrict__ G, const double* __restrict__ Q,
+__global__ void __launch_bounds__(128, (PC <= 4 ? 3 : 1)) gemm_gq_kernel(const double* __restrict__ G, const double* __restrict__ Q,
                                                       int64_t m, int64_t kchunk, double* __restrict__ Ypart) {
   constexpr int p = PC * 16;
   constexpr int NG = (kGM * kGK) / 128;   // G values per thread per stage
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(128) gemm_gq_kernel(const double* __restrict__
     if (more) load(k0 + kGK);
     const double* sG = gsm + buf * (SG + SQ);
     const double* sQ = sG + SG;
-#pragma unroll 8
+#pragma unroll 2
     for (int kk = 0; kk < kGK; ++kk) {
       double g[8];
 #pragma unroll

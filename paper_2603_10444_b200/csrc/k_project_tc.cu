@@ -149,14 +149,19 @@ __global__ void __launch_bounds__(kPThreads, 1) proj_tc_kernel(
     const int rbase = ct >> 3;            // rows rbase + 32 u, u < 4
     double sq = 0.0;
     uint32_t it = 0, ui = 0;
+    float4 mh4 = __ldg(reinterpret_cast<const float4*>(mu_hl + g * 4));
+    float4 ml4 = __ldg(reinterpret_cast<const float4*>(mu_hl + m_pad + g * 4));
     for (int64_t rb = blockIdx.x; rb < nrb; rb += gridDim.x, ++ui) {
       const int64_t row0 = rb * 128;
       for (int c = 0; c < NC; ++c, ++it) {
         const uint32_t s = it % NS, r = it / NS;
         const int64_t col = (int64_t)c * 32 + g * 4;
-        const float4 mh4 = __ldg(reinterpret_cast<const float4*>(mu_hl + col));
-        const float4 ml4 = __ldg(reinterpret_cast<const float4*>(mu_hl + m_pad + col));
         const float mh[4] = {mh4.x, mh4.y, mh4.z, mh4.w}, ml[4] = {ml4.x, ml4.y, ml4.z, ml4.w};
+        {  // prefetch mu of the next chunk (mu depends on the column only)
+          const int64_t ncol = (int64_t)(c + 1 < NC ? c + 1 : 0) * 32 + g * 4;
+          mh4 = __ldg(reinterpret_cast<const float4*>(mu_hl + ncol));
+          ml4 = __ldg(reinterpret_cast<const float4*>(mu_hl + m_pad + ncol));
+        }
         bool cok[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) cok[e] = col + e < m;
@@ -365,28 +370,33 @@ __global__ void __launch_bounds__(kPThreads, 1) energy_tc_kernel(
       for (int c = 0; c < NC; ++c, ++it, ++ci) {
         const uint32_t s = it % NS, r = it / NS;
         const uint32_t b = ci & 1, br = ci >> 1;
+        static_assert(NCOL == 32, "epilogue handles 16 columns per warp half");
+        const int c0 = half * 16;
+        const int64_t j0 = (int64_t)c * NCOL + c0;
+        float mh[16], ml[16];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {  // mu loads issued before the barrier waits
+          const float4 a = __ldg(reinterpret_cast<const float4*>(mu_hl + j0) + u);
+          const float4 bb = __ldg(reinterpret_cast<const float4*>(mu_hl + m_pad + j0) + u);
+          mh[4 * u] = a.x; mh[4 * u + 1] = a.y; mh[4 * u + 2] = a.z; mh[4 * u + 3] = a.w;
+          ml[4 * u] = bb.x; ml[4 * u + 1] = bb.y; ml[4 * u + 2] = bb.z; ml[4 * u + 3] = bb.w;
+        }
         mbar_wait(&full_bar[s], r & 1);
         mbar_wait(&tfull_bar[b], br & 1);
         tc_fence_after();
         const uint32_t tb = tmem + ((q * 32) << 16) + b * NCOL;
         const uint8_t* sx = sB + s * kStage + kVB;
         float s2 = 0.f, t2 = 0.f, st = 0.f;
-#pragma unroll
-        for (int c0 = half * (NCOL / 2); c0 < (half + 1) * (NCOL / 2); c0 += 16) {
+        {
           uint32_t rv[16];
           tmem_ld16(tb + c0, rv);
-          const int64_t j0 = (int64_t)c * NCOL + c0;
-          float xv[16], mh[16], ml[16];
-          const float4* xrow = reinterpret_cast<const float4*>(sx + (c0 / 32) * kTile + rloc * 128);
+          float xv[16];
+          const float4* xrow = reinterpret_cast<const float4*>(sx + rloc * 128);
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const int g = ((c0 % 32) >> 2) + u;       // logical 16-byte group of the row
+            const int g = (c0 >> 2) + u;              // logical 16-byte group of the row
             const float4 v = xrow[g ^ (rloc & 7)];    // SWIZZLE_128B
             xv[4 * u] = v.x; xv[4 * u + 1] = v.y; xv[4 * u + 2] = v.z; xv[4 * u + 3] = v.w;
-            const float4 a = __ldg(reinterpret_cast<const float4*>(mu_hl + j0) + u);
-            const float4 bb = __ldg(reinterpret_cast<const float4*>(mu_hl + m_pad + j0) + u);
-            mh[4 * u] = a.x; mh[4 * u + 1] = a.y; mh[4 * u + 2] = a.z; mh[4 * u + 3] = a.w;
-            ml[4 * u] = bb.x; ml[4 * u + 1] = bb.y; ml[4 * u + 2] = bb.z; ml[4 * u + 3] = bb.w;
           }
           tmem_ld_wait();
 #pragma unroll
@@ -456,7 +466,8 @@ template <int KP32, int NCOL>
 avd_status launch_k8(Ctx* c, const CUtensorMap& tmP, const CUtensorMap& tmV, const CUtensorMap& tmX, int grid) {
   constexpr uint32_t kA = 2 * (KP32 / 32) * kTile;
   constexpr uint32_t kStage = 2 * (KP32 / 32) * NCOL * 128 + (NCOL / 32) * kTile;
-  constexpr int NS = 2;
+  constexpr int NSF = (int)((200u * 1024u - kA) / kStage);
+  constexpr int NS = NSF > 6 ? 6 : (NSF < 2 ? 2 : NSF);
   const size_t smem = kA + NS * kStage + 1024;
   AVD_CUDA(cudaFuncSetAttribute(energy_tc_kernel<KP32, NCOL, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
@@ -492,7 +503,7 @@ avd_status launch_project_tc(Ctx* c, const float* X) {
   if (encode2d(&tmX, X, c->cfg.m, c->cfg.l_local, c->cfg.m * 4, 32, 128) != CUDA_SUCCESS ||
       encode2d(&tmVt, c->Vt_hl, c->m_pad32, 2 * KP, c->m_pad32 * 4, 32, 2 * KP) != CUDA_SUCCESS ||
       encode2d(&tmP, c->P_hl, KP32, 2 * c->l_pad, KP32 * 4, 32, 128) != CUDA_SUCCESS ||
-      encode2d(&tmV, c->V_hl, KP32, 2 * c->m_pad, KP32 * 4, 32, KP32 <= 64 ? 64 : 32) != CUDA_SUCCESS) {
+      encode2d(&tmV, c->V_hl, KP32, 2 * c->m_pad, KP32 * 4, 32, 32) != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (projection maps)");
     return AVD_ECUDA;
   }
@@ -509,8 +520,8 @@ avd_status launch_project_tc(Ctx* c, const float* X) {
     default: set_error("unsupported k_pad"); return AVD_EINVAL;
   }
   switch (KP32) {
-    case 32: AVD_TRY((launch_k8<32, 64>(c, tmP, tmV, tmX, grid))); break;
-    case 64: AVD_TRY((launch_k8<64, 64>(c, tmP, tmV, tmX, grid))); break;
+    case 32: AVD_TRY((launch_k8<32, 32>(c, tmP, tmV, tmX, grid))); break;
+    case 64: AVD_TRY((launch_k8<64, 32>(c, tmP, tmV, tmX, grid))); break;
     case 96: AVD_TRY((launch_k8<96, 32>(c, tmP, tmV, tmX, grid))); break;
     default: set_error("unsupported k_pad"); return AVD_EINVAL;
   }

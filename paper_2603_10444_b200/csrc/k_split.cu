@@ -74,6 +74,10 @@ __global__ void __launch_bounds__(kSplitThreads) split_kernel(
   if (threadIdx.x < kSplitRows)
     srow[threadIdx.x] = mix32((uint32_t)(row_offset + i0 + threadIdx.x) * 0x9E3779B1u ^ seed32);
   const uint32_t b0 = (uint32_t)dp->b0;
+  // candidate test as one unsigned compare: key in [max(1, b0 << 19), 0x7F800000)
+  const uint32_t klo = max(1u, b0 << 19);
+  const uint32_t kspan = 0x7F800000u - klo;
+  const int rows_here = (l_local - i0) < kSplitRows ? (int)(l_local - i0) : kSplitRows;  // valid rows of this tile
   const bool colok = j < m;
   // mu = hi + lo (fp32 pair); 2^shift as an exact fp32 power of two (shift clamped to the normal
   // range: columns with max|xc| < 2^-100 quantise to zero)
@@ -95,12 +99,11 @@ __global__ void __launch_bounds__(kSplitThreads) split_kernel(
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int rl = rg * 32 + t * 4 + u;
-      const int64_t i = i0 + rl;
-      const bool ok = colok && i < l_local;
+      const bool ok = colok && rl < rows_here;
       const float x = xs[u];
       const uint32_t key = __float_as_uint(x) & 0x7FFFFFFFu;
       // ---- candidate append (warp aggregated)
-      const bool cand = ok && key != 0 && key < 0x7F800000u && (key >> 19) >= b0;
+      const bool cand = ok && (key - klo) < kspan;
       const uint32_t ballot = __ballot_sync(0xFFFFFFFFu, cand);
       if (ballot) {
         const int ldr = __ffs(ballot) - 1;
@@ -111,28 +114,30 @@ __global__ void __launch_bounds__(kSplitThreads) split_kernel(
           const unsigned long long pos = base + __popc(ballot & ((1u << lane) - 1u));
           if (pos < (unsigned long long)cand_cap) {
             cand_key[pos] = key;
-            cand_idx[pos] = (uint64_t)(row_offset + i) * (uint64_t)m + (uint64_t)j;
+            cand_idx[pos] = (uint64_t)(row_offset + i0 + rl) * (uint64_t)m + (uint64_t)j;
           }
         }
       }
       // ---- dithered fixed-point digits of the centred entry: q = floor(xc 2^shift + u)
       if (ok) {
         const float y = ((x - mh) - ml) * scale;     // exact power-of-two scaling, |y| < 2^(7nd-1)
-        const float yi = floorf(y);
-        const float f = y - yi;                       // exact fractional part
-        const uint32_t h = mix32(srow[rl] ^ colh);
-        const float dith = (float)(h >> 8) * (1.0f / 16777216.0f);  // u in [0,1), 24 bits
-        int32_t q = (int32_t)yi + (dith >= 1.0f - f ? 1 : 0);
+        const uint32_t h = (srow[rl] ^ colh) * 0x9E3779B1u;  // row/column hashes are mix32-ed
+        // u in [0, 1 - ulp(2^(7nd-1))]: the clamp keeps fl(y + u) < y + 1 for integer y (exact data
+        // stays exact); it moves probability <= 2^-10 (nd=2) / 2^-3 (nd=3) of u to the clamp value
+        constexpr float kDithMax = ND == 2 ? 1.0f - 0x1p-10f : 1.0f - 0x1p-3f;
+        const float dith = fminf(__uint_as_float(0x3F800000u | (h >> 9)) - 1.0f, kDithMax);
+        int32_t q = __float2int_rd(y + dith);        // RN sum then floor: dithered rounding
+        // balanced base-128 digits, most significant first
         int32_t dg[ND];
 #pragma unroll
         for (int d = ND - 1; d >= 1; --d) {
-          const int32_t sdg = ((q + 64) & 127) - 64;
-          dg[d] = sdg;
-          q = (q - sdg) >> 7;
+          const int32_t hi = (q + 64) >> 7;
+          dg[d] = q - (hi << 7);                      // in [-64, 63]
+          q = hi;
         }
         dg[0] = q;
 #pragma unroll
-        for (int d = 0; d < ND; ++d) packed[d] |= ((uint32_t)(uint8_t)(int8_t)dg[d]) << (8 * u);
+        for (int d = 0; d < ND; ++d) packed[d] = __byte_perm(packed[d], (uint32_t)dg[d], u == 0 ? 0x3214 : (u == 1 ? 0x3240 : (u == 2 ? 0x3410 : 0x4210)));
       }
     }
 #pragma unroll

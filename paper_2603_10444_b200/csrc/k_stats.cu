@@ -63,16 +63,13 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const bool ok = active && (i + u < r1);
-      const bool sampled = ((row_offset + i + u) % sample) == 0;  // warp-uniform
+      const bool sampled = (((uint32_t)(row_offset + i + u)) & (uint32_t)(sample - 1)) == 0;  // warp-uniform; sample = 2^s
 #pragma unroll
       for (int v = 0; v < VEC; ++v) {
         const float xv = x[u][v];
         const uint32_t key = __float_as_uint(xv) & 0x7FFFFFFFu;
         const bool fin = key < 0x7F800000u;
         if (ok) {
-          const double d = (double)xv;
-          s[v] += d;
-          sq = fma(d, d, sq);
           mx[v] = fmaxf(mx[v], xv);
           mn[v] = fminf(mn[v], xv);
           nonfin += fin ? 0u : 1u;
@@ -80,6 +77,20 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(
         }
         if (sampled) hist_add(sh, key, ok && fin && key != 0);
       }
+    }
+    // fp64 accumulation of U-row fp32 partial sums (each partial rounds once, ~2^-24 relative)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      float ps = 0.f, pq = 0.f;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool ok = active && (i + u < r1);
+        const float xv = ok ? x[u][v] : 0.f;
+        ps += xv;
+        pq = fmaf(xv, xv, pq);
+      }
+      s[v] += (double)ps;
+      sq += (double)pq;
     }
   }
   if (active) {
@@ -217,7 +228,10 @@ __global__ void prepare_kernel(int64_t m, int64_t m_pad, int64_t l_global, int n
 }  // namespace
 
 int stats_sample_step(int64_t l_global) {
-  return (int)std::max<int64_t>(1, std::min<int64_t>(16, l_global / 4096));
+  const int64_t want = std::max<int64_t>(1, std::min<int64_t>(16, l_global / 4096));
+  int s = 1;
+  while (s * 2 <= want) s *= 2;  // power of two: the kernel tests row & (s - 1)
+  return s;
 }
 
 avd_status launch_stats(Ctx* c, const float* X) {
