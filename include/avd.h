@@ -73,7 +73,7 @@ typedef struct {
   int64_t n_top_override;  /* > 0: use this |E_top|                                          */
   uint64_t seed;           /* start block of the subspace iteration + Gram dither            */
   int32_t max_iters;       /* subspace iterations cap (0 -> 200)                             */
-  double eig_tol;          /* Ritz residual tolerance relative to lambda_1 (0 -> 1e-7)       */
+  double eig_tol;          /* Ritz residual tolerance relative to lambda_1 (0 -> 1e-6)       */
   int32_t digits;          /* 0 -> 2; Gram operand = centred X in `digits` int8 digit planes */
   int32_t world;           /* ranks sharing the rows (1 = single GPU)                        */
   int32_t device;          /* CUDA device ordinal                                            */

@@ -138,31 +138,50 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   return AVD_OK;
 }
 
-// colmean maxima and <M,spike>, <M,tail>, l||mu||^2 (one CTA, fixed-order reductions)
-__global__ void report_kernel(const double* __restrict__ energy, const double* __restrict__ stats,
-                              const double* __restrict__ mu, const double* __restrict__ V, int64_t m, int k,
-                              int64_t l_global, double* __restrict__ rep) {
-  __shared__ double s_ms[256], s_mt[256], s_as[256], s_at[256], s_mu2[256];
+// colmean maxima and <M,spike>, <M,tail>, l||mu||^2: one thread per column, per-CTA partials
+// (fixed order) + a one-CTA finish
+__global__ void report_part_kernel(const double* __restrict__ energy, const double* __restrict__ stats,
+                                   const double* __restrict__ mu, const double* __restrict__ V, int64_t m, int k,
+                                   int64_t l_global, double* __restrict__ part) {
+  __shared__ double sh[5][256];
+  const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
   double ms = 0, mt = 0, as = 0, at = 0, mu2 = 0;
-  const double inv_l = 1.0 / (double)l_global;
-  for (int64_t j = threadIdx.x; j < m; j += 256) {
+  if (j < m) {
+    const double inv_l = 1.0 / (double)l_global;
     double cs = 0.0;  // sum_i spike_ij = sum_r (1^T P)_r V_jr
     for (int r = 0; r < k; ++r) cs = fma(energy[4 + r], V[j * k + r], cs);
     const double cxc = stats[j] - (double)l_global * mu[j];  // sum_i xc_ij
     const double ct = cxc - cs;                              // sum_i tail_ij
-    ms = fma(mu[j], cs, ms);
-    mt = fma(mu[j], ct, mt);
-    as = fmax(as, fabs(cs * inv_l));
-    at = fmax(at, fabs(ct * inv_l));
-    mu2 = fma(mu[j], mu[j], mu2);
+    ms = mu[j] * cs;
+    mt = mu[j] * ct;
+    as = fabs(cs * inv_l);
+    at = fabs(ct * inv_l);
+    mu2 = mu[j] * mu[j];
   }
-  s_ms[threadIdx.x] = ms; s_mt[threadIdx.x] = mt; s_as[threadIdx.x] = as; s_at[threadIdx.x] = at; s_mu2[threadIdx.x] = mu2;
+  sh[0][threadIdx.x] = ms; sh[1][threadIdx.x] = mt; sh[2][threadIdx.x] = as; sh[3][threadIdx.x] = at;
+  sh[4][threadIdx.x] = mu2;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double a = 0, b = 0, c = 0, d = 0, e = 0;
-    for (int t = 0; t < 256; ++t) { a += s_ms[t]; b += s_mt[t]; c = fmax(c, s_as[t]); d = fmax(d, s_at[t]); e += s_mu2[t]; }
-    rep[0] = a; rep[1] = b; rep[2] = c; rep[3] = d; rep[4] = (double)l_global * e;
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      sh[0][threadIdx.x] += sh[0][threadIdx.x + o];
+      sh[1][threadIdx.x] += sh[1][threadIdx.x + o];
+      sh[2][threadIdx.x] = fmax(sh[2][threadIdx.x], sh[2][threadIdx.x + o]);
+      sh[3][threadIdx.x] = fmax(sh[3][threadIdx.x], sh[3][threadIdx.x + o]);
+      sh[4][threadIdx.x] += sh[4][threadIdx.x + o];
+    }
+    __syncthreads();
   }
+  if (threadIdx.x < 5) part[(int64_t)blockIdx.x * 5 + threadIdx.x] = sh[threadIdx.x][0];
+}
+__global__ void report_final_kernel(const double* __restrict__ part, int nparts, int64_t l_global,
+                                    double* __restrict__ rep) {
+  if (threadIdx.x != 0) return;
+  double a = 0, b = 0, c = 0, d = 0, e = 0;
+  for (int q = 0; q < nparts; ++q) {
+    a += part[q * 5]; b += part[q * 5 + 1]; c = fmax(c, part[q * 5 + 2]); d = fmax(d, part[q * 5 + 3]);
+    e += part[q * 5 + 4];
+  }
+  rep[0] = a; rep[1] = b; rep[2] = c; rep[3] = d; rep[4] = (double)l_global * e;
 }
 
 // assemble the user's device outputs
@@ -411,7 +430,11 @@ avd_status avd_stage_report(avd_ctx* c, avd_outputs* out) {
   if (!out) { set_error("null outputs"); return AVD_EINVAL; }
   const int64_t m = c->cfg.m;
   const int k = c->k;
-  report_kernel<<<1, 256, 0, c->stream>>>(c->energy, c->stats, c->mu, c->V, m, k, c->cfg.l_global, c->report);
+  const int nrep = (int)ceil_div(m, 256);
+  report_part_kernel<<<nrep, 256, 0, c->stream>>>(c->energy, c->stats, c->mu, c->V, m, k, c->cfg.l_global,
+                                                  c->red_part);  // eig scratch is free here
+  AVD_LAUNCHED(c);
+  report_final_kernel<<<1, 32, 0, c->stream>>>(c->red_part, nrep, c->cfg.l_global, c->report);
   AVD_LAUNCHED(c);
   if (out->mu_dev || out->V_dev || out->sigma_dev) {
     copy_outputs_kernel<<<(unsigned)ceil_div(std::max<int64_t>(m * k, m), 256), 256, 0, c->stream>>>(

@@ -630,7 +630,7 @@ avd_status run_eig(Ctx* c) {
   AVD_LAUNCHED(c);
   AVD_TRY(orth(c, c->Z, c->Q, seed + 1));
   const int max_it = c->cfg.max_iters > 0 ? c->cfg.max_iters : 100;
-  const double tol = c->cfg.eig_tol > 0 ? c->cfg.eig_tol : 1e-7;
+  const double tol = c->cfg.eig_tol > 0 ? c->cfg.eig_tol : 1e-6;  // V angle <~ tol * lambda_1 / gap_k
   int it = 0, next_rr = 2, prev_it = 0, rr_count = 0;
   double maxres = 0.0, prev_res = -1.0;
   bool conv = false;

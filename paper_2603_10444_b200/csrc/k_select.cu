@@ -163,36 +163,61 @@ __global__ void __launch_bounds__(kSelThreads) blk_count_kernel(const uint32_t* 
 }
 
 // exclusive scan of block counts (one CTA); quota / offset come from avd_tie_quota (host)
-__global__ void blk_scan_kernel(int64_t* __restrict__ blk, int64_t nblk, int64_t quota, int64_t offset,
-                                int64_t ties_local, DevPlan* __restrict__ dp) {
-  __shared__ int64_t carry[2];
-  __shared__ int64_t sh[1024];
-  if (threadIdx.x == 0) { carry[0] = 0; carry[1] = 0; }
+// block-wide exclusive scan helpers (warp shuffles + one smem pass)
+template <typename T, int NT>
+__device__ __forceinline__ T block_exclusive_scan(T v, T* warp_tot, T& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
   __syncthreads();
+  if (warp == 0) {
+    T w = lane < NT / 32 ? warp_tot[lane] : T(0);
+    T wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const T t = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+      if (lane >= o) wi += t;
+    }
+    if (lane < NT / 32) warp_tot[lane] = wi - w;  // exclusive warp offsets
+    if (lane == NT / 32 - 1) warp_tot[NT / 32] = wi;
+  }
+  __syncthreads();
+  total = warp_tot[NT / 32];
+  const T r = warp_tot[warp] + incl - v;
+  __syncthreads();
+  return r;
+}
+
+// exclusive scan of the per-block (sel, tie) counts in one CTA (each thread owns a contiguous
+// run of blocks); quota / offset come from avd_tie_quota (host)
+__global__ void __launch_bounds__(1024) blk_scan_kernel(int64_t* __restrict__ blk, int64_t nblk, int64_t quota,
+                                                        int64_t offset, int64_t ties_local, DevPlan* __restrict__ dp) {
+  __shared__ int64_t wt[1024 / 32 + 1];
+  const int64_t per = (nblk + 1023) / 1024;
+  const int64_t b0 = threadIdx.x * per, b1 = min(nblk, b0 + per);
+  int64_t sel_total = 0;
   for (int which = 0; which < 2; ++which) {
     int64_t* a = blk + which * nblk;
-    for (int64_t base = 0; base < nblk; base += blockDim.x) {
-      const int64_t i = base + threadIdx.x;
-      const int64_t v = i < nblk ? a[i] : 0;
-      sh[threadIdx.x] = v;
-      __syncthreads();
-      for (int o = 1; o < (int)blockDim.x; o <<= 1) {
-        const int64_t t = threadIdx.x >= (unsigned)o ? sh[threadIdx.x - o] : 0;
-        __syncthreads();
-        sh[threadIdx.x] += t;
-        __syncthreads();
-      }
-      const int64_t incl = sh[threadIdx.x];
-      if (i < nblk) a[i] = carry[which] + incl - v;
-      __syncthreads();
-      if (threadIdx.x == blockDim.x - 1) carry[which] += incl;
-      __syncthreads();
+    int64_t run = 0;
+    for (int64_t i = b0; i < b1; ++i) run += a[i];
+    int64_t total;
+    int64_t acc = block_exclusive_scan<int64_t, 1024>(run, wt, total);
+    for (int64_t i = b0; i < b1; ++i) {
+      const int64_t v = a[i];
+      a[i] = acc;
+      acc += v;
     }
+    if (which == 0) sel_total = total;
   }
   if (threadIdx.x == 0) {
     dp->ties_local = ties_local;
     dp->quota = quota;
-    dp->sel_local = carry[0] + quota;
+    dp->sel_local = sel_total + quota;
     dp->top_offset = offset;
   }
 }
@@ -201,7 +226,7 @@ __global__ void __launch_bounds__(kSelThreads) emit_kernel(const uint32_t* __res
                                                            int64_t nwords, int64_t nblk, const int64_t* __restrict__ blk,
                                                            const DevPlan* __restrict__ dp, int64_t base_idx,
                                                            int64_t* __restrict__ out) {
-  __shared__ int ps[kSelThreads + 1], pt[kSelThreads + 1];
+  __shared__ int ps[kSelThreads / 32 + 1], pt[kSelThreads / 32 + 1];
   const int64_t w0 = (int64_t)blockIdx.x * kWordsPerBlk;
   const int64_t quota = dp->quota;
   int64_t sel_before = blk[blockIdx.x], tie_before = blk[nblk + blockIdx.x];
@@ -216,20 +241,11 @@ __global__ void __launch_bounds__(kSelThreads) emit_kernel(const uint32_t* __res
     a += __popc(ws[q]);
     b += __popc(wt[q]);
   }
-  ps[threadIdx.x] = a;
-  pt[threadIdx.x] = b;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int sa = 0, sb = 0;
-    for (int t = 0; t < kSelThreads; ++t) {
-      const int x = ps[t], y = pt[t];
-      ps[t] = sa; pt[t] = sb;
-      sa += x; sb += y;
-    }
-  }
-  __syncthreads();
-  int64_t sb4 = sel_before + ps[threadIdx.x];
-  int64_t tb4 = tie_before + pt[threadIdx.x];
+  int tot;
+  const int ea = block_exclusive_scan<int, kSelThreads>(a, ps, tot);
+  const int eb = block_exclusive_scan<int, kSelThreads>(b, pt, tot);
+  int64_t sb4 = sel_before + ea;
+  int64_t tb4 = tie_before + eb;
 #pragma unroll
   for (int q = 0; q < WPT; ++q) {
     const int64_t w = w0 + threadIdx.x * WPT + q;
