@@ -7,9 +7,13 @@
 //   * entries whose |x| bit pattern falls in a first-level bin >= b0 are appended as
 //     (key, global linear index) candidates of E_top.
 // One read of X (4 B/entry), nd bytes written per entry.
+#include <cudaTypedefs.h>
 #include "common.cuh"
+#include "sm100.cuh"
 
 namespace avd {
+
+PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn();  // k_gram.cu
 
 namespace {
 
@@ -38,26 +42,27 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src, bool valid
 
 template <int ND, bool VEC>
 __global__ void __launch_bounds__(kSplitThreads) split_kernel(
-    const float* __restrict__ X, int64_t l_local, int64_t m, int64_t m_pad, int64_t l_pad,
+    const __grid_constant__ CUtensorMap tmX, const float* __restrict__ X, int64_t l_local, int64_t m, int64_t m_pad, int64_t l_pad,
     int64_t row_offset, const float* __restrict__ mu_hl, const int32_t* __restrict__ shift,
     uint32_t seed32, int8_t* __restrict__ digits, const DevPlan* __restrict__ dp,
     uint32_t* __restrict__ cand_key, uint64_t* __restrict__ cand_idx,
     unsigned long long* __restrict__ cand_cnt, int64_t cand_cap) {
-  extern __shared__ __align__(16) float sX[];  // [kSplitRows][kSplitCols] tile of X (cp.async)
+  extern __shared__ __align__(128) float sX_raw[];  // [kSplitRows][kSplitCols] tile of X
+  float* sX = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(sX_raw) + 127) & ~uintptr_t(127));
   __shared__ uint32_t sD[ND][kSplitCols * kSW];
   __shared__ uint32_t srow[kSplitRows];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t i0 = (int64_t)blockIdx.x * kSplitRows;
   const int64_t j0 = (int64_t)blockIdx.y * kSplitCols;
-  // ---- stage the whole 128 x 64 tile with asynchronous copies (32 KB in flight per CTA)
+  // ---- stage the whole 128 x 64 tile asynchronously (32 KB in flight per CTA): one TMA
+  //      (out-of-range rows / columns zero-filled), or per-thread cp.async when m % 4 != 0
+  __shared__ __align__(8) uint64_t tbar;
   if (VEC) {
-#pragma unroll
-    for (int u = 0; u < (kSplitRows * kSplitCols / 4) / kSplitThreads; ++u) {
-      const int id = threadIdx.x + kSplitThreads * u;
-      const int r = id / (kSplitCols / 4), cq = id % (kSplitCols / 4);
-      const int64_t gi = i0 + r, gj = j0 + cq * 4;
-      const bool v = gi < l_local && gj < m;
-      cp_async16(sX + r * kSplitCols + cq * 4, v ? (const void*)(X + gi * m + gj) : (const void*)X, v);
+    if (threadIdx.x == 0) {
+      sm100::mbar_init(&tbar, 1);
+      sm100::fence_mbar_init();
+      sm100::mbar_arrive_expect_tx(&tbar, kSplitRows * kSplitCols * 4);
+      sm100::tma_load_2d(sX, &tmX, &tbar, (int32_t)j0, (int32_t)i0);
     }
   } else {
     for (int id = threadIdx.x; id < kSplitRows * kSplitCols; id += kSplitThreads) {
@@ -67,7 +72,7 @@ __global__ void __launch_bounds__(kSplitThreads) split_kernel(
       cp_async4(sX + r * kSplitCols + cc, v ? (const void*)(X + gi * m + gj) : (const void*)X, v);
     }
   }
-  asm volatile("cp.async.commit_group;" ::: "memory");
+  if (!VEC) asm volatile("cp.async.commit_group;" ::: "memory");
   const int jl = (warp & 1) * 32 + lane;
   const int64_t j = j0 + jl;
   const int rg = warp >> 1;  // 32-row group
@@ -85,8 +90,13 @@ __global__ void __launch_bounds__(kSplitThreads) split_kernel(
   const int sh = colok ? shift[j] : 0;
   const float scale = (colok && sh <= 126 && sh >= -126) ? __int_as_float((sh + 127) << 23) : 0.f;
   const uint32_t colh = mix32((uint32_t)j ^ 0x68E31DA4u);
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  __syncthreads();
+  if (VEC) {
+    __syncthreads();  // barrier initialised before anyone waits on it
+    sm100::mbar_wait(&tbar, 0);
+  } else {
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+  }
 
 #pragma unroll 1
   for (int t = 0; t < 8; ++t) {
@@ -169,12 +179,25 @@ avd_status launch_split(Ctx* c, const float* X) {
   dim3 grid((unsigned)(c->l_pad / kSplitRows), (unsigned)(c->m_pad / kSplitCols));
   const uint32_t seed32 = (uint32_t)(c->cfg.seed * 0x9E3779B97F4A7C15ull >> 32) ^ 0xA5A5A5A5u;
   const bool vec = (c->cfg.m % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
-  const size_t sm = sizeof(float) * kSplitRows * kSplitCols;
+  const size_t sm = sizeof(float) * kSplitRows * kSplitCols + 128;
+  CUtensorMap tmX{};
+  if (vec) {
+    uint64_t dims[2] = {(uint64_t)c->cfg.m, (uint64_t)c->cfg.l_local};
+    uint64_t strides[1] = {(uint64_t)c->cfg.m * 4};
+    uint32_t box[2] = {kSplitCols, kSplitRows};
+    uint32_t es[2] = {1, 1};
+    if (tma_encode_fn()(&tmX, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(X), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      set_error("cuTensorMapEncodeTiled failed (split)");
+      return AVD_ECUDA;
+    }
+  }
 #define LAUNCH(ND, V)                                                                                         \
   do {                                                                                                        \
     AVD_CUDA(cudaFuncSetAttribute(split_kernel<ND, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
     split_kernel<ND, V><<<grid, kSplitThreads, sm, c->stream>>>(                                              \
-        X, c->cfg.l_local, c->cfg.m, c->m_pad, c->l_pad, c->cfg.row_offset, c->mu_hl, c->shift, seed32,       \
+        tmX, X, c->cfg.l_local, c->cfg.m, c->m_pad, c->l_pad, c->cfg.row_offset, c->mu_hl, c->shift, seed32,       \
         c->digits, c->dplan, c->cand_key, c->cand_idx, c->cand_cnt, c->cand_cap);                             \
   } while (0)
   if (c->nd == 2) { if (vec) LAUNCH(2, true); else LAUNCH(2, false); }
