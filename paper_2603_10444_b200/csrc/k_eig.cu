@@ -25,8 +25,9 @@ __global__ void gram_finalize_kernel(const long long* __restrict__ Gi, int64_t m
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t a = blockIdx.y;
   if (b >= m) return;
+  // K3 adds tile (A, B), A <= B, transposed: element (a, b) of an upper tile sits at Gi[b][a]
   const bool upper = (a / 128) <= (b / 128);
-  const long long v = upper ? Gi[a * m_pad + b] : Gi[b * m_pad + a];
+  const long long v = upper ? Gi[b * m_pad + a] : Gi[a * m_pad + b];
   G[a * m + b] = ldexp((double)v * unit, -(shift[a] + shift[b]));
 }
 

@@ -16,7 +16,11 @@
 // Warp roles (192 threads, 1 CTA/SM, persistent over work units):
 //   warp 0: TMA producer (cp.async.bulk.tensor 2D, SWIZZLE_128B, mbarrier ring)
 //   warp 1: TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2-5: epilogue (tcgen05.ld 32x32b -> int64 -> global atomics)
+//   warps 2-9: epilogue (tcgen05.ld 32x32b -> int64 -> global atomics); warp w reads TMEM lane
+//              quadrant w % 4 and column half (w - 2) / 4.  Tile (a, b) is added TRANSPOSED,
+//              G_int[b-block col][a-block row], so a warp's 32 lanes (32 consecutive rows of
+//              the tile) hit 32 consecutive int64 (one 256-B segment per instruction); the
+//              upper-tile Gram is therefore held in the lower 128-tiles (k_eig.cu reads it so).
 #include <cudaTypedefs.h>
 #include "common.cuh"
 #include "sm100.cuh"
@@ -26,7 +30,7 @@ namespace avd {
 namespace {
 using namespace sm100;
 
-constexpr int kGramThreads = 192;
+constexpr int kGramThreads = 320;
 constexpr uint32_t kBox = 128 * 128;  // bytes of one TMA box (128 rows x 128 int8)
 
 // kind::i8 instruction descriptor: c_format S32 (2), a/b format signed int8 (1), K-major.
@@ -74,7 +78,7 @@ __global__ void __launch_bounds__(kGramThreads, 1) gram_kernel(const __grid_cons
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
     mbar_init(&tfull_bar, 1);
-    mbar_init(&tempty_bar, 4);
+    mbar_init(&tempty_bar, 8);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) tma_prefetch(&tmap);
@@ -159,8 +163,8 @@ __global__ void __launch_bounds__(kGramThreads, 1) gram_kernel(const __grid_cons
       __syncwarp();
     }
   } else {
-    // ================= epilogue: warps 2..5 -> TMEM lane quadrant (warp % 4)
-    const uint32_t q = warp & 3;
+    // ================= epilogue: warps 2..9 -> TMEM lane quadrant (warp % 4), column half
+    const uint32_t q = warp & 3, h = (warp - 2) >> 2;
     uint32_t ui = 0;
     for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++ui) {
       int ta, tb;
@@ -169,10 +173,11 @@ __global__ void __launch_bounds__(kGramThreads, 1) gram_kernel(const __grid_cons
       mbar_wait(&tfull_bar, ui & 1);
       tc_fence_after();
       const int64_t row = (int64_t)ta * 128 + q * 32 + lane;
-      unsigned long long* grow = reinterpret_cast<unsigned long long*>(G + row * m_pad + (int64_t)tb * 128);
-      const uint32_t tbase = tmem + ((q * 32) << 16);
+      unsigned long long* gcol =
+          reinterpret_cast<unsigned long long*>(G + ((int64_t)tb * 128 + h * 64) * m_pad + row);
+      const uint32_t tbase = tmem + ((q * 32) << 16) + h * 64;
 #pragma unroll 1
-      for (int c0 = 0; c0 < 128; c0 += 16) {
+      for (int c0 = 0; c0 < 64; c0 += 16) {
         uint32_t r0[16], r1[16], r2[16];
         tmem_ld16(tbase + c0, r0);
         tmem_ld16(tbase + 128 + c0, r1);
@@ -182,7 +187,7 @@ __global__ void __launch_bounds__(kGramThreads, 1) gram_kernel(const __grid_cons
         for (int t = 0; t < 16; ++t) {
           const long long v = ((long long)(int32_t)r0[t] << 14) + ((long long)(int32_t)r1[t] << 7) +
                               (long long)(int32_t)r2[t];
-          if (v != 0) atomicAdd(grow + c0 + t, (unsigned long long)v);
+          if (v != 0) atomicAdd(gcol + (int64_t)(c0 + t) * m_pad, (unsigned long long)v);
         }
       }
       tc_fence_before();
@@ -238,6 +243,10 @@ avd_status gram_make_tmap(Ctx* c) {
   if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r)); return AVD_ECUDA; }
   const int T = (int)(c->m_pad / 128);
   c->gram_split = choose_split(T * (T + 1) / 2, c->l_pad / 128, c->num_sms);
+  if (const char* e = getenv("AVD_GRAM_SPLIT")) {
+    const int v = atoi(e);
+    if (v >= (int)ceil_div(c->l_pad / 128, 1024) && v <= c->l_pad / 128) c->gram_split = v;
+  }
   return AVD_OK;
 }
 
