@@ -76,7 +76,6 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   C->r1 = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(4LL * C->num_sms, ncb), ceil_div(ll, 4)));
   C->cand_cap = std::min<int64_t>(ll * m, std::max<int64_t>(4 * n_top, 1 << 20));
   C->n_red = (int)ceil_div(m, kRedRowsC);  // partials of the m-length p x p reductions
-  C->gemm_ks = (int)std::max<int64_t>(1, std::min<int64_t>(8, ceil_div(2LL * C->num_sms, ceil_div(m, 64))));
   C->n_proj_ctas = (int)ceil_div(ll, 32);
   C->nwords = ceil_div(ll * m, 32);
   C->nblk = ceil_div(C->nwords, 1024);
@@ -99,7 +98,7 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   L.add(sizeof(uint64_t) * C->cand_cap);        // 13 cand_idx
   L.add(sizeof(unsigned long long));            // 14 cand_cnt
   L.add(sizeof(long long) * C->m_pad * C->m_pad);// 15 gram_i
-  L.add(sizeof(double) * m * m);                // 16 G
+  L.add(sizeof(double) * C->m_pad * C->m_pad);  // 16 G
   L.add(sizeof(double) * m * p);                // 17 Q
   L.add(sizeof(double) * m * p);                // 18 Y
   L.add(sizeof(double) * m * p);                // 19 Z
@@ -128,11 +127,17 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   L.add(sizeof(double) * 16);                   // 42 report
   L.add(sizeof(unsigned long long) * kHistBins);// 43 hist0
   L.add(sizeof(long long) * 2);                 // 44 cand_x
-  L.add(sizeof(double) * C->gemm_ks * m * p);   // 45 Ypart
+  L.add(gemm_part_bytes(C->m_pad, (int)p, C->num_sms));  // 45 gemm_part
   L.add(sizeof(float) * 2 * C->l_pad * (((C->k_pad + 31) / 32) * 32));   // 46 P_hl
   L.add(sizeof(float) * 2 * C->k_pad * round_up(m, 32));                 // 47 Vt_hl
   L.add(sizeof(float) * 2 * C->m_pad * (((C->k_pad + 31) / 32) * 32));   // 48 V_hl
   L.add(sizeof(float) * 2 * C->m_pad);                                   // 49 mu_hl
+  L.add(sizeof(float) * C->m_pad * C->m_pad);                            // 50 G32
+  L.add(sizeof(long long) * C->m_pad);                                   // 51 qsum
+  L.add(sizeof(float) * m * p);                                          // 52 Q32
+  L.add(sizeof(float) * m * p);                                          // 53 Z32
+  L.add(sizeof(unsigned) * 4);                                           // 54 ticket
+  L.add(sizeof(double));                                                 // 55 gmax
   plan->workspace_bytes = L.total;
   if (lay) *lay = L;
   return AVD_OK;
@@ -266,8 +271,9 @@ avd_status avd_create(const avd_config* cfg, avd_ctx** out) {
   BIND(trace, double*); BIND(V, double*); BIND(sigma, double*); BIND(V32, float*); BIND(P, float*);
   BIND(en_part, double*); BIND(colsumP_part, double*); BIND(energy, double*); BIND(hist2, unsigned long long*);
   BIND(hist3, unsigned long long*); BIND(ties, long long*); BIND(bm_sel, uint32_t*); BIND(bm_tie, uint32_t*);
-  BIND(blk_cnt, int64_t*); BIND(agg, double*); BIND(agg_part, double*); BIND(report, double*); BIND(hist0, unsigned long long*); BIND(cand_x, long long*); BIND(Ypart, double*);
+  BIND(blk_cnt, int64_t*); BIND(agg, double*); BIND(agg_part, double*); BIND(report, double*); BIND(hist0, unsigned long long*); BIND(cand_x, long long*); BIND(gemm_part, void*);
   BIND(P_hl, float*); BIND(Vt_hl, float*); BIND(V_hl, float*); BIND(mu_hl, float*);
+  BIND(G32, float*); BIND(qsum, long long*); BIND(Q32, float*); BIND(Z32, float*); BIND(ticket, unsigned*); BIND(gmax, double*);
 #undef BIND
   if (cudaMallocHost(&c->eig_host, sizeof(double) * 4 * kMaxP) != cudaSuccess) {
     cudaGetLastError();
@@ -334,7 +340,7 @@ avd_status avd_buffer(avd_ctx* c, int32_t which, void** ptr, size_t* bytes) {
     case AVD_BUF_TIES: *ptr = c->ties; *bytes = sizeof(long long) * 2 * c->cfg.world; break;
     case AVD_BUF_AGG: *ptr = c->agg; *bytes = sizeof(double) * 8; break;
     case AVD_BUF_MU: *ptr = c->mu; *bytes = sizeof(double) * m; break;
-    case AVD_BUF_G: *ptr = c->G; *bytes = sizeof(double) * m * m; break;
+    case AVD_BUF_G: *ptr = c->G; *bytes = sizeof(double) * c->m_pad * c->m_pad; break;
     case AVD_BUF_P: *ptr = c->P; *bytes = sizeof(float) * c->cfg.l_local * c->k_pad; break;
     case AVD_BUF_DIGITS: *ptr = c->digits; *bytes = (size_t)c->nd * c->m_pad * c->l_pad; break;
     case AVD_BUF_SCALE: *ptr = c->shift; *bytes = sizeof(int32_t) * c->m_pad; break;

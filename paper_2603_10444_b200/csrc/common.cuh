@@ -73,7 +73,9 @@ struct Ctx {
   bool cand_overflow = false;     // true -> K6 streams X instead of the candidate list
   // K3
   long long* gram_i = nullptr;    // [m_pad * m_pad] int64 (upper tiles) (exchange SUM)
-  double* G = nullptr;            // [m * m] fp64 symmetric
+  double* G = nullptr;            // [m_pad][m_pad] fp64 symmetric (zero beyond m)
+  float* G32 = nullptr;           // [m_pad][m_pad] fp32 copy (power steps of K4)
+  long long* qsum = nullptr;      // [m_pad] column sums of the quantised operand (exchange SUM)
   CUtensorMap tmap_digits{};
   int gram_split = 1;
   // K4
@@ -81,8 +83,10 @@ struct Ctx {
   double *H = nullptr, *W = nullptr, *theta = nullptr;          // [p][p], [p][p], [p]
   double* red_part = nullptr;     // [n_red_chunks][p*p]
   int n_red = 1;
-  int gemm_ks = 1;                // split-K of Y = G Q
-  double* Ypart = nullptr;        // [gemm_ks][m][p]
+  void* gemm_part = nullptr;      // Yfix: int64 [m_pad][p] fixed-point accumulator of Y = G Q
+  float *Q32 = nullptr, *Z32 = nullptr;  // [m][p] fp32 mirrors of Q, Z
+  unsigned* ticket = nullptr;     // last-CTA ticket of the fused reductions
+  double* gmax = nullptr;         // max |G| (fixed-point scale of the Y = G Q accumulation)
   double* resid = nullptr;        // [p]
   double* trace = nullptr;        // [1]
   double* eig_host = nullptr;     // pinned: theta[p] + resid[p]
@@ -164,6 +168,8 @@ avd_status launch_gram(Ctx* c);                            // k_gram.cu
 avd_status gram_make_tmap(Ctx* c);                         // k_gram.cu
 avd_status launch_gram_finalize(Ctx* c);                   // k_eig.cu
 avd_status run_eig(Ctx* c);                                // k_eig.cu
+void gemm_geometry(int64_t m_pad, int p, int num_sms, bool fp32, int* BM, int* ncta, int64_t* U, int* KT);
+size_t gemm_part_bytes(int64_t m_pad, int p, int num_sms);
 avd_status launch_project(Ctx* c, const float* X);         // k_project.cu
 avd_status launch_select(Ctx* c, const float* X, int level, int rank);  // k_select.cu
 avd_status launch_gather(Ctx* c, const float* X, int rank, int64_t* top_idx, double* rho);

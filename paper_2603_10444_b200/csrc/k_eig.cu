@@ -1,46 +1,77 @@
-// k_eig.cu — K4: top-k eigenpairs of the centred Gram G (fp64, on device) by block subspace
-// iteration with Rayleigh-Ritz: V_k, sigma_k = sqrt(lambda_k) are the right singular vectors /
-// values of Xc that define the rank-k spike.
+// k_eig.cu — K4: top-k eigenpairs of the centred Gram G (on device) by block subspace iteration
+// with Rayleigh-Ritz: V_k, sigma_k = sqrt(lambda_k) are the right singular vectors / values of
+// Xc that define the rank-k spike.
 //
 //   Q_0 = orth(random m x p), p = roundup16(k + 8)
-//   repeat:  Y = G Q ; H = Q^T Y ; (W, theta) = eig(H)            (Rayleigh-Ritz)
-//            U = Q W ; Z = Y W (= G U) ; res_r = ||Z_r - theta_r U_r|| / theta_1, r < k
-//            stop when max res_r <= tol
-//            Q = orth(G Z)   (two products per orthonormalisation: G^2 U, Cholesky-QR2)
-// p x p problems run in one CTA each: parallel (round-robin) Jacobi for Rayleigh-Ritz,
-// Cholesky + triangular inverse for CholQR; the m-length reductions feeding them are
-// multi-CTA partial sums finished inside those one-CTA kernels in a fixed order.
+//   power step:  Q <- orth(G (G Q))                    G in fp32 (L2-resident copy), fp32 FMA
+//   RR check:    Y = G Q (fp64) ; H = Q^T Y ; (W, theta) = eig(H)           (Rayleigh-Ritz)
+//                U = Q W ; Z = Y W (= G U) ; res_r = ||Z_r - theta_r U_r|| / theta_1, r < k
+//                stop when max res_r <= tol, else Q <- orth(G Z)
+// The power steps only steer the subspace; every reported quantity (theta, U, the residual
+// that decides convergence) comes from the fp64 product with the exact G, so the fp32 operator
+// perturbs nothing that is returned (its ~1e-8 relative error sits far below tol).
+//
+// Kernels: Y = G Q is a stream-K SIMT GEMM (fp32 or fp64; every CTA gets the same number of
+// 32-row K units, partial row-block segments are summed by a fixup kernel in a fixed order);
+// the m-length p x p reductions (Q^T Y, Y^T Y) are per-CTA partials whose LAST CTA (atomic
+// ticket) sums them in a fixed order and then runs the p x p step in place: Cholesky + triangular
+// inverse for CholQR, or the parallel Jacobi eigensolver for Rayleigh-Ritz.
 // Rank deficiency (G = 0, rank(G) < p, m < p) flags the failing columns, which are re-drawn at
-// random and re-orthonormalised (R11).  Everything is fp64 and deterministic.
+// random and re-orthonormalised (R11).  Deterministic: no floating-point atomics.
 #include <cfloat>
 #include "common.cuh"
 
 namespace avd {
 
+#ifdef AVD_EIG_PROBE
+__device__ long long g_probe_clk[16];  // tools/eig_micro.cu: phase timestamps of one-CTA kernels
+#define PROBE(i) do { if (threadIdx.x == 0 && blockIdx.x == gridDim.x - 1) g_probe_clk[i] = clock64(); } while (0)
+#else
+#define PROBE(i) do { } while (0)
+#endif
+
 namespace {
 
-// ---------------------------------------------------------------- G_int -> G (fp64)
+// ---------------------------------------------------------------- G_int -> G (fp64), G32 (fp32)
+// Both with leading dimension m_pad; rows/columns >= m are zero.
 __global__ void gram_finalize_kernel(const long long* __restrict__ Gi, int64_t m, int64_t m_pad,
-                                     const int32_t* __restrict__ shift, double unit, double* __restrict__ G) {
+                                     const int32_t* __restrict__ shift, const long long* __restrict__ qsum,
+                                     double inv_l, double unit, double* __restrict__ G, float* __restrict__ G32) {
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t a = blockIdx.y;
-  if (b >= m) return;
-  // K3 adds tile (A, B), A <= B, transposed: element (a, b) of an upper tile sits at Gi[b][a]
-  const bool upper = (a / 128) <= (b / 128);
-  const long long v = upper ? Gi[b * m_pad + a] : Gi[a * m_pad + b];
-  G[a * m + b] = ldexp((double)v * unit, -(shift[a] + shift[b]));
+  if (b >= m_pad) return;
+  double g = 0.0;
+  if (a < m && b < m) {
+    // K3 adds tile (A, B), A <= B, transposed: element (a, b) of an upper tile sits at Gi[b][a]
+    const bool upper = (a / 128) <= (b / 128);
+    const long long v = upper ? Gi[b * m_pad + a] : Gi[a * m_pad + b];
+    // exact centring of the quantised matrix: sum_i (q_ia - qbar_a)(q_ib - qbar_b)
+    //   = sum_i q_ia q_ib - S_a S_b / l   (S = column sums of q, exact integers)
+    const double corr = qsum ? ((double)qsum[a] * (double)qsum[b]) * inv_l : 0.0;
+    g = ldexp(((double)v - corr) * unit, -(shift[a] + shift[b]));
+  }
+  G[a * m_pad + b] = g;
+  G32[a * m_pad + b] = (float)g;
 }
 
-__global__ void trace_kernel(const double* __restrict__ G, int64_t m, double* __restrict__ out) {
-  __shared__ double sh[256];
-  double s = 0.0;
-  for (int64_t j = threadIdx.x; j < m; j += 256) s += G[j * m + j];
+// tr(G) and max_a G_aa (= max |G_ab| for the positive semidefinite G)
+__global__ void trace_kernel(const double* __restrict__ G, int64_t m, int64_t ld, double* __restrict__ out,
+                             double* __restrict__ gmax) {
+  __shared__ double sh[256], shm[256];
+  double s = 0.0, mx = 0.0;
+  for (int64_t j = threadIdx.x; j < m; j += 256) {
+    const double g = G[j * ld + j];
+    s += g;
+    mx = fmax(mx, fabs(g));
+  }
   sh[threadIdx.x] = s;
+  shm[threadIdx.x] = mx;
   __syncthreads();
   if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int i = 0; i < 256; ++i) t += sh[i];
+    double t = 0.0, u = 0.0;
+    for (int i = 0; i < 256; ++i) { t += sh[i]; u = fmax(u, shm[i]); }
     *out = t;
+    *gmax = u;
   }
 }
 
@@ -53,158 +84,594 @@ __device__ __forceinline__ double rnd_sym(uint32_t seed, uint32_t a, uint32_t b)
   return ((double)(h >> 8) + 0.5) * (2.0 / 16777216.0) - 1.0;
 }
 
-// Q[j][c] = U(-1,1) for columns with flag (or all when flags == nullptr)
-__global__ void rand_fill_kernel(double* __restrict__ Q, int64_t m, int p, uint32_t seed,
+// Q[j][c] = U(-1,1) for columns with flag (or all when flags == nullptr); Q32 mirrors it
+__global__ void rand_fill_kernel(double* __restrict__ Q, float* __restrict__ Q32, int64_t m, int p, uint32_t seed,
                                  const int* __restrict__ flags) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= m * p) return;
   const int c = (int)(t % p);
   if (flags && !flags[c]) return;
-  Q[t] = rnd_sym(seed, (uint32_t)(t / p), (uint32_t)c);
+  const double v = rnd_sym(seed, (uint32_t)(t / p), (uint32_t)c);
+  Q[t] = v;
+  if (Q32) Q32[t] = (float)v;
 }
 
-// ---------------------------------------------------------------- Y = G Q  (split-K partials)
-// CTA: 64 rows of Y x all p columns, K range [kz*kchunk, (kz+1)*kchunk); 128 threads, each an
-// 8-row x (p/16)-column register tile; register-prefetched double buffer (the next K stage's
-// global loads are in flight while the current stage computes).  Ypart[kz][m][p].
-constexpr int kGM = 64;   // rows per CTA
-constexpr int kGK = 32;   // K per smem stage
-template <int PC>
-__global__ void __launch_bounds__(128, (PC <= 4 ? 3 : 1)) gemm_gq_kernel(const double* __restrict__ G, const double* __restrict__ Q,
-                                                      int64_t m, int64_t kchunk, double* __restrict__ Ypart) {
-  constexpr int p = PC * 16;
-  constexpr int NG = (kGM * kGK) / 128;   // G values per thread per stage
-  constexpr int NQ = (kGK * p) / 128;     // Q values per thread per stage
-  constexpr int SG = kGK * (kGM + 2);     // doubles of one transposed G tile [k][row]
-  constexpr int SQ = kGK * p;
-  extern __shared__ __align__(16) double gsm[];
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // rows 8ty..8ty+7, cols tx+16c
-  const int64_t r0 = (int64_t)blockIdx.x * kGM;
-  const int64_t kbeg = (int64_t)blockIdx.y * kchunk;
-  const int64_t kend = min(m, kbeg + kchunk);
-  double acc[8][PC];
-#pragma unroll
-  for (int a = 0; a < 8; ++a)
-#pragma unroll
-    for (int c = 0; c < PC; ++c) acc[a][c] = 0.0;
-  double gv[NG], qv[NQ];
-  auto load = [&](int64_t k0) {
-#pragma unroll
-    for (int e = 0; e < NG; ++e) {
-      const int t = threadIdx.x + e * 128;
-      const int rr = t / kGK, kk = t % kGK;
-      gv[e] = (r0 + rr < m && k0 + kk < kend) ? __ldg(G + (r0 + rr) * m + k0 + kk) : 0.0;
+// ---------------------------------------------------------------- Y = G Q, stream-K
+// Unit = (row block rb of BM rows, K tile kt of 32).  U = RB * KT units are split evenly over
+// ncta CTAs (CTA c: [c U / n, (c+1) U / n)); a CTA's range covers at most two row blocks
+// (ncta >= RB), each written as a partial segment part[c][seg][BM][p].  G is symmetric, so the
+// (rows r0.., K k0..) tile is read as G[k][r0..] (contiguous rows, no transpose).
+// 128 threads: ty = tid / 8 owns rows ty*NR .. +NR, tx = tid % 8 owns column pairs 16 c2 + 2 tx.
+constexpr int kSkBK = 32;
+constexpr int kSkThreads = 128;
+constexpr int kSkStages = 3;
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Fixed-point scale of the Y accumulation: |partial sums of Y = G In| <= ||G||_inf max|In| <=
+// (m max|G|)^(level+1) =: Bnd for In orthonormal-ish (level 0) or In = G * orthonormal (level 1);
+// scale = 2^(61 - e), 2^e >= Bnd, so every running sum fits an int64 with resolution Bnd 2^-60.
+__device__ __forceinline__ double fix_scale(const double* gmax, int64_t m, int level) {
+  const double g = *gmax * (double)m;
+  if (!(g > 0.0) || !(g < 1e150)) return 1.0;
+  const double b = level ? g * g : g;
+  return ldexp(1.0, 61 - (ilogb(b) + 1));
+}
+
+template <typename T, int NR, int NC>
+__global__ void __launch_bounds__(kSkThreads) gemm_sk_kernel(const T* __restrict__ G, int64_t ldg,
+                                                             const T* __restrict__ Qin, int64_t m, int64_t U,
+                                                             int KT, int ncta, unsigned long long* __restrict__ Yfix,
+                                                             const double* __restrict__ gmax, int level) {
+  constexpr int BM = 16 * NR;
+  constexpr int p = 8 * NC;
+  constexpr int SG = kSkBK * BM;          // elements of one G stage
+  constexpr int SQ = kSkBK * p;           // elements of one Q stage
+  constexpr int EPC = 16 / sizeof(T);     // elements per 16-B chunk
+  extern __shared__ __align__(16) unsigned char sk_raw[];
+  T* sm = reinterpret_cast<T*>(sk_raw);
+  const int tid = threadIdx.x;
+  const int ty = tid >> 3, tx = tid & 7;
+  const int c = blockIdx.x;
+  const int64_t u0 = ((int64_t)c * U) / ncta, u1 = ((int64_t)(c + 1) * U) / ncta;
+
+  auto load_stage = [&](int slot, int64_t rb, int kt) {
+    T* sG = sm + slot * (SG + SQ);
+    T* sQ = sG + SG;
+    const int64_t k0 = (int64_t)kt * kSkBK;
+    const int64_t r0 = rb * BM;
+    constexpr int GCH = SG / EPC;  // 16-B chunks of the G tile
+    for (int ch = tid; ch < GCH; ch += kSkThreads) {
+      const int kk = ch / (BM / EPC), cc = ch % (BM / EPC);
+      const bool ok = k0 + kk < m;
+      const T* src = ok ? G + (k0 + kk) * ldg + r0 + cc * EPC : G;
+      cp_async16((uint32_t)__cvta_generic_to_shared(sG + kk * BM + cc * EPC), src, ok);
     }
-#pragma unroll
-    for (int e = 0; e < NQ; ++e) {
-      const int t = threadIdx.x + e * 128;
-      const int kk = t / p;
-      qv[e] = (k0 + kk < kend) ? __ldg(Q + (k0 + kk) * p + (t % p)) : 0.0;
+    constexpr int QCH = SQ / EPC;
+    for (int ch = tid; ch < QCH; ch += kSkThreads) {
+      const int kk = ch / (p / EPC);
+      const bool ok = k0 + kk < m;
+      const T* src = ok ? Qin + k0 * p + ch * EPC : Qin;
+      cp_async16((uint32_t)__cvta_generic_to_shared(sQ + ch * EPC), src, ok);
     }
   };
-  auto store = [&](int buf) {
-    double* sG = gsm + buf * (SG + SQ);
-    double* sQ = sG + SG;
+
+  int seg = 0;
+  for (int64_t u = u0; u < u1; ++seg) {
+    const int64_t rb = u / KT;
+    const int64_t uend = min(u1, (rb + 1) * KT);
+    const int n = (int)(uend - u);
+    const int kt0 = (int)(u - rb * KT);
+    T acc[NR][NC];
 #pragma unroll
-    for (int e = 0; e < NG; ++e) {
-      const int t = threadIdx.x + e * 128;
-      sG[(t % kGK) * (kGM + 2) + t / kGK] = gv[e];
+    for (int r = 0; r < NR; ++r)
+#pragma unroll
+      for (int q = 0; q < NC; ++q) acc[r][q] = T(0);
+    __syncthreads();  // previous segment's readers are done with every slot
+#pragma unroll
+    for (int s = 0; s < kSkStages - 1; ++s) {
+      if (s < n) load_stage(s, rb, kt0 + s);
+      cp_commit();
     }
+    for (int i = 0; i < n; ++i) {
+      cp_wait<kSkStages - 2>();
+      __syncthreads();
+      if (i + kSkStages - 1 < n) load_stage((i + kSkStages - 1) % kSkStages, rb, kt0 + i + kSkStages - 1);
+      cp_commit();
+      const T* sG = sm + (i % kSkStages) * (SG + SQ);
+      const T* sQ = sG + SG;
+#pragma unroll 4
+      for (int kk = 0; kk < kSkBK; ++kk) {
+        T g[NR], q[NC];
 #pragma unroll
-    for (int e = 0; e < NQ; ++e) sQ[threadIdx.x + e * 128] = qv[e];
-  };
-  if (kbeg < kend) {
-    load(kbeg);
-    store(0);
-  }
-  __syncthreads();
-  int buf = 0;
-  for (int64_t k0 = kbeg; k0 < kend; k0 += kGK, buf ^= 1) {
-    const bool more = k0 + kGK < kend;
-    if (more) load(k0 + kGK);
-    const double* sG = gsm + buf * (SG + SQ);
-    const double* sQ = sG + SG;
-#pragma unroll 2
-    for (int kk = 0; kk < kGK; ++kk) {
-      double g[8];
+        for (int r = 0; r < NR; r += EPC) {
+          if constexpr (sizeof(T) == 4) {
+            const float4 v = *reinterpret_cast<const float4*>(sG + kk * BM + ty * NR + r);
+            g[r] = v.x; g[r + 1] = v.y; g[r + 2] = v.z; g[r + 3] = v.w;
+          } else {
+            const double2 v = *reinterpret_cast<const double2*>(sG + kk * BM + ty * NR + r);
+            g[r] = v.x; g[r + 1] = v.y;
+          }
+        }
 #pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        const double2 v = *reinterpret_cast<const double2*>(sG + kk * (kGM + 2) + 8 * ty + 2 * h);
-        g[2 * h] = v.x;
-        g[2 * h + 1] = v.y;
-      }
+        for (int c2 = 0; c2 < NC / 2; ++c2) {
+          if constexpr (sizeof(T) == 4) {
+            const float2 v = *reinterpret_cast<const float2*>(sQ + kk * p + 16 * c2 + 2 * tx);
+            q[2 * c2] = v.x; q[2 * c2 + 1] = v.y;
+          } else {
+            const double2 v = *reinterpret_cast<const double2*>(sQ + kk * p + 16 * c2 + 2 * tx);
+            q[2 * c2] = v.x; q[2 * c2 + 1] = v.y;
+          }
+        }
 #pragma unroll
-      for (int c = 0; c < PC; ++c) {
-        const double q = sQ[kk * p + tx + 16 * c];
+        for (int r = 0; r < NR; ++r)
 #pragma unroll
-        for (int a = 0; a < 8; ++a) acc[a][c] = fma(g[a], q, acc[a][c]);
+          for (int q2 = 0; q2 < NC; ++q2) acc[r][q2] = fma(g[r], q[q2], acc[r][q2]);
       }
     }
-    if (more) store(buf ^ 1);
-    __syncthreads();
-  }
-  double* Yp = Ypart + (int64_t)blockIdx.y * m * p;
+    cp_wait<0>();
+    // exact integer accumulation of this segment into Yfix (order-independent, deterministic)
+    const double scale = fix_scale(gmax, m, level);
 #pragma unroll
-  for (int a = 0; a < 8; ++a) {
-    const int64_t r = r0 + 8 * ty + a;
-    if (r < m)
+    for (int r = 0; r < NR; ++r) {
+      const int64_t row = rb * BM + ty * NR + r;
+      if (row < m)
 #pragma unroll
-      for (int c = 0; c < PC; ++c) Yp[r * p + tx + 16 * c] = acc[a][c];
+        for (int q2 = 0; q2 < NC; ++q2) {
+          const long long v = __double2ll_rn((double)acc[r][q2] * scale);
+          if (v) atomicAdd(Yfix + row * p + 16 * (q2 / 2) + 2 * tx + (q2 & 1), (unsigned long long)v);
+        }
+    }
+    u = uend;
   }
 }
 
-__global__ void ksum_kernel(const double* __restrict__ part, int nparts, int64_t n, double* __restrict__ out) {
+// Y = Yfix / scale (fp64, optional fp32 mirror); Yfix re-zeroed for the next product
+__global__ void fix_convert_kernel(unsigned long long* __restrict__ Yfix, int64_t n, int64_t m,
+                                   const double* __restrict__ gmax, int level, double* __restrict__ Y,
+                                   float* __restrict__ Y32) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
-  double s = part[t];
-  for (int q = 1; q < nparts; ++q) s += part[(int64_t)q * n + t];
-  out[t] = s;
+  const double inv = 1.0 / fix_scale(gmax, m, level);
+  const double v = (double)(long long)Yfix[t] * inv;
+  Yfix[t] = 0ull;
+  Y[t] = v;
+  if (Y32) Y32[t] = (float)v;
 }
 
-// ---------------------------------------------------------------- C = A^T B partials (m x p)
-// CTA: kRedRowsC rows in 64-row smem chunks; thread owns PC^2 outputs (p^2 = 256 PC^2).
-constexpr int kRedChunk = 64;
-template <int PC>
-__global__ void __launch_bounds__(256) atb_partial_kernel(const double* __restrict__ A, const double* __restrict__ B,
-                                                          int64_t m, double* __restrict__ part) {
-  constexpr int p = PC * 16;
-  constexpr int U = PC * PC;
-  extern __shared__ double sm[];
-  double* sA = sm;
-  double* sB = sm + kRedChunk * p;
-  double acc[U];
-#pragma unroll
-  for (int u = 0; u < U; ++u) acc[u] = 0.0;
-  const int64_t rbase = (int64_t)blockIdx.x * kRedRowsC;
-  for (int ch = 0; ch < kRedRowsC / kRedChunk; ++ch) {
-    const int64_t r0 = rbase + ch * kRedChunk;
-    if (r0 >= m) break;
-    __syncthreads();
-    for (int t = threadIdx.x; t < kRedChunk * p; t += 256) {
-      const int rr = t / p;
-      const bool ok = r0 + rr < m;
-      sA[t] = ok ? A[r0 * p + t] : 0.0;
-      sB[t] = ok ? B[r0 * p + t] : 0.0;
+// ---------------------------------------------------------------- p x p helpers (one CTA)
+__device__ __forceinline__ double rcp_fast(double x) {  // 1/x, MUFU seed + 2 Newton steps (~1 ulp)
+  double r = (double)(1.0f / (float)x);
+  r = r * fma(-x, r, 2.0);
+  return r * fma(-x, r, 2.0);
+}
+__device__ __forceinline__ double rsqrt_fast(double x) {  // 1/sqrt(x), x in the fp32 range
+  double r = (double)rsqrtf((float)x);
+  r = r * fma(-0.5 * x * r, r, 1.5);
+  return r * fma(-0.5 * x * r, r, 1.5);
+}
+// Jacobi rotation (c, s) for the pair (p, q) of a symmetric matrix scaled to ~1.  The angle is
+// computed in fp32 (Rutishauser: th = (a_qq - a_pp) / (2 a_pq), t = sign(th) / (|th| + sqrt(th^2+1)))
+// — the rotation only has to shrink a_pq, which a 2^-24-accurate angle does by ~1e-7 per visit —
+// while (c, s) are made orthogonal to fp64 accuracy: c^2 + s^2 = 1 + d from the fp32 pair, scaled by
+// (1 + d)^(-1/2) = 1 - d/2 + 3d^2/8 (|d| <~ 1e-7), so every applied transform is an exact-in-fp64
+// similarity and the eigenvalues keep fp64 accuracy.  Skipped when |a_pq| <= 1e-13 sqrt(a_pp a_qq).
+__device__ __forceinline__ void jacobi_rotation(double app, double aqq, double apq, double& c, double& s, bool& rot) {
+  c = 1.0;
+  s = 0.0;
+  rot = false;
+  if (!(apq * apq > 1e-26 * fabs(app * aqq)) || fabs(apq) < 1e-30 || fabs(apq) > 1e30) return;
+  const float th = __fdividef(0.5f * (float)(aqq - app), (float)apq);
+  const float ath = fabsf(th);
+  if (!(ath < 1e18f)) return;  // |a_pq| below 1e-18 |a_qq - a_pp|: nothing left to rotate
+  float t = __frcp_rn(ath + sqrtf(fmaf(th, th, 1.0f)));
+  t = th >= 0.f ? t : -t;
+  const float c32 = rsqrtf(fmaf(t, t, 1.0f));
+  const double c0 = (double)c32, s0 = (double)(t * c32);
+  const double d = fma(c0, c0, s0 * s0) - 1.0;
+  const double r = fma(d, fma(0.375, d, -0.5), 1.0);
+  c = c0 * r;
+  s = s0 * r;
+  rot = true;
+}
+__device__ __forceinline__ void rr_pair(int p, int step, int i, int& P, int& Q) {
+  int a, b;
+  if (i == 0) { a = p - 1; b = step; }
+  else { a = (step + i) % (p - 1); b = (step - i + (p - 1)) % (p - 1); }
+  P = min(a, b);
+  Q = max(a, b);
+}
+
+// Parallel (round-robin) Jacobi on the symmetric A (P x P, ld LDA, scaled so max|a_ii| ~ 1) with
+// V^T (ld P).  Per step: warp u computes the rotation J_u of its pair (P_u, Q_u) (lane 0), then,
+// after one barrier, rewrites ITS two rows of A as rows of J_u^T A J (lane w takes the column
+// pair (P_w, Q_w) of the step, so each 2x2 block sees both rotations) and its two rows of
+// V^T (V <- V J).  Every row belongs to exactly one pair: no two warps touch the same element.
+// Two barriers per step.  Returns the number of sweeps.
+template <int P, int LDA>
+__device__ int jacobi_block(double* A, double* Vt, double* rc, double* rs, int* rp, int* rq, int* flag) {
+  constexpr int half = P / 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  int sweep = 0;
+  for (; sweep < 40; ++sweep) {
+    if (threadIdx.x == 0) *flag = 0;
+    for (int step = 0; step < P - 1; ++step) {
+      __syncthreads();
+#ifdef AVD_EIG_PROBE
+      long long t_a = clock64();
+#endif
+      if (warp == 0) {
+        bool any = false;
+        for (int u = lane; u < half; u += 32) {  // all rotations of the step, one lane each
+          int p0, q0;
+          rr_pair(P, step, u, p0, q0);
+          double c, s;
+          bool rot;
+          jacobi_rotation(A[p0 * LDA + p0], A[q0 * LDA + q0], A[p0 * LDA + q0], c, s, rot);
+          rc[u] = c;
+          rs[u] = s;
+          rp[u] = p0;
+          rq[u] = q0;
+          any |= rot;
+        }
+        if (__any_sync(0xFFFFFFFFu, any) && lane == 0) *flag = 1;
+      }
+#ifdef AVD_EIG_PROBE
+      long long t_b = clock64();
+#endif
+      __syncthreads();
+#ifdef AVD_EIG_PROBE
+      long long t_c = clock64();
+      if (threadIdx.x == 0) { g_probe_clk[8] += t_b - t_a; g_probe_clk[9] += t_c - t_b; }
+#endif
+      for (int u = warp; u < half; u += nwarps) {
+        const double cu = rc[u], su = rs[u];
+        const int p1 = rp[u], q1 = rq[u];
+        for (int w = lane; w < half; w += 32) {
+          const double cw = rc[w], sw = rs[w];
+          if (su == 0.0 && sw == 0.0) continue;
+          const int p2 = rp[w], q2 = rq[w];
+          const double a = A[p1 * LDA + p2], b = A[p1 * LDA + q2], c_ = A[q1 * LDA + p2], d = A[q1 * LDA + q2];
+          // rows: J_u^T, then columns: J_w
+          const double a1 = cu * a - su * c_, b1 = cu * b - su * d;
+          const double c1 = su * a + cu * c_, d1 = su * b + cu * d;
+          const double a2 = cw * a1 - sw * b1, b2 = sw * a1 + cw * b1;
+          const double c2 = cw * c1 - sw * d1, d2 = sw * c1 + cw * d1;
+          A[p1 * LDA + p2] = a2;
+          A[p1 * LDA + q2] = b2;
+          A[q1 * LDA + p2] = c2;
+          A[q1 * LDA + q2] = d2;
+        }
+        if (su != 0.0) {
+          // V <- V J_u: rows p1, q1 of V^T, two columns per lane
+          for (int j = 2 * lane; j < P; j += 64) {
+            double2* vp = reinterpret_cast<double2*>(Vt + p1 * P + j);
+            double2* vq = reinterpret_cast<double2*>(Vt + q1 * P + j);
+            const double2 x = *vp, y = *vq;
+            *vp = make_double2(cu * x.x - su * y.x, cu * x.y - su * y.y);
+            *vq = make_double2(su * x.x + cu * y.x, su * x.y + cu * y.y);
+          }
+        }
+      }
     }
     __syncthreads();
+    const int any = *flag;
+    __syncthreads();
+    if (!any) break;
+  }
+  return sweep + 1;
+}
+
+// Cholesky B = R^T R (upper; B scaled so max diag ~ 1).  Each thread keeps its entries of the
+// upper triangle in registers for the whole factorisation; at step j the owners of row j
+// publish it (double-buffered row), one barrier, and every owner of an entry (i, k), i > j,
+// applies b_ik -= b_ji b_jk / b_jj.  Outputs R into B (upper, zero below), dinv[j] = 1 / R_jj and
+// bad[j] = 1 for pivots <= 1e-13 of the largest diagonal (zero row).
+template <int P, int LDA, int NT>
+__device__ void chol_block(double* B, double* dinv, int* bad) {
+  constexpr int NU = P * (P + 1) / 2;
+  constexpr int E = (NU + NT - 1) / NT;
+  __shared__ double rowbuf[2][P];
+  __shared__ double dmax_sh;
+  int ei[E], ek[E];
+  double v[E];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int t = threadIdx.x + 256 * u;
-      const int i = t / p, j = t % p;
-      double s = acc[u];
-#pragma unroll 8
-      for (int rr = 0; rr < kRedChunk; ++rr) s = fma(sA[rr * p + i], sB[rr * p + j], s);
-      acc[u] = s;
+  for (int q = 0; q < E; ++q) {
+    const int e = threadIdx.x + NT * q;
+    ei[q] = P;  // none
+    ek[q] = P;
+    v[q] = 0.0;
+    if (e < NU) {
+      // packed upper triangle, row-major: row i holds P - i entries
+      int i = 0, rem = e;
+      while (rem >= P - i) { rem -= P - i; ++i; }
+      ei[q] = i;
+      ek[q] = i + rem;
+      v[q] = B[i * LDA + i + rem];
     }
   }
+  if (threadIdx.x < 32) {
+    double d = 0.0;
+    for (int i = threadIdx.x; i < P; i += 32) d = fmax(d, B[i * LDA + i]);
+    for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xFFFFFFFFu, d, o));
+    if (threadIdx.x == 0) dmax_sh = d;
+  }
+  __syncthreads();
+  const double tol = 1e-13 * dmax_sh;
+  for (int j = 0; j < P; ++j) {
+    double* row = rowbuf[j & 1];
 #pragma unroll
-  for (int u = 0; u < U; ++u) part[(int64_t)blockIdx.x * p * p + threadIdx.x + 256 * u] = acc[u];
+    for (int q = 0; q < E; ++q)
+      if (ei[q] == j) row[ek[q]] = v[q];
+    __syncthreads();
+    const double d = row[j];
+    const bool ok = d > tol && d > 0.0;
+    const double inv = ok ? rsqrt_fast(d) : 0.0;
+    const double invd = inv * inv;
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      if (ei[q] > j && ei[q] < P) v[q] = fma(-row[ei[q]] * invd, row[ek[q]], v[q]);
+      else if (ei[q] == j) v[q] = (ek[q] == j) ? (ok ? d * inv : 0.0) : v[q] * inv;  // R row j (final)
+    }
+    if (threadIdx.x == 0) { dinv[j] = inv; bad[j] = ok ? 0 : 1; }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < P * P; t += NT) B[(t / P) * LDA + t % P] = 0.0;
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < E; ++q)
+    if (ei[q] < P) B[ei[q] * LDA + ek[q]] = v[q];
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- fused m-length reduction
+// ticket += 1 with acq_rel semantics at GPU scope (no full sequentially-consistent fence)
+__device__ __forceinline__ unsigned ticket_acq_rel(unsigned* t) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(t) : "memory");
+  return old;
+}
+constexpr int kRedRows = kRedRowsC;  // rows per partial
+template <int PC>
+struct RedCfg {
+  static constexpr int threads = PC <= 4 ? 1024 : 512;  // register budget of the PC^2 accumulators
+  static constexpr int chunk = PC <= 3 ? kRedRows : 64;  // rows staged in smem at a time (one load wave)
+};
+// part[blk] = A[rows of blk]^T B[rows of blk] (p x p), register-tiled over the first 256 threads
+// (thread (ti, tj) owns outputs (ti + 16a, tj + 16b)); the last CTA to finish sums the partials
+// in block order (symmetrised) and then:
+//   MODE 0: H = the sum (out0)
+//   MODE 1: Cholesky -> R (out0, upper, p x p), 1/R_jj (out1), bad flags (ibad); stats[0] = 1 when
+//           a second CholQR pass is needed (a bad column, or cond(R)^2 > 1e6 from its diagonal)
+//   MODE 2: Jacobi -> W (out0, eigenvectors sorted by eigenvalue desc), theta (out1), sweeps
+// gate != nullptr && *gate == 0: nothing to do (second CholQR pass not needed).
+// The partial sum reads each partial once (two adjacent elements per load) and symmetrises in smem.
+template <int MODE, int PC>
+__global__ void __launch_bounds__(RedCfg<PC>::threads) atb_fused_kernel(
+    const double* __restrict__ A, const double* __restrict__ B, int64_t m, double* __restrict__ part,
+    unsigned* __restrict__ ticket, double* __restrict__ out0, double* __restrict__ out1, int* __restrict__ ibad,
+    int* __restrict__ stats, const int* __restrict__ gate) {
+  constexpr int p = PC * 16;
+  constexpr int NT = RedCfg<PC>::threads;
+  constexpr int kRedChunk = RedCfg<PC>::chunk;
+  if (gate && *gate == 0) return;
+  extern __shared__ __align__(16) double fsm[];
+  __shared__ unsigned last_sh;
+  PROBE(0);
+  {
+    double* sA = fsm;
+    double* sB = fsm + kRedChunk * p;
+    const int ti = threadIdx.x >> 4, tj = threadIdx.x & 15;
+    const bool comp = threadIdx.x < 256;
+    double acc[PC][PC];
+#pragma unroll
+    for (int a = 0; a < PC; ++a)
+#pragma unroll
+      for (int b = 0; b < PC; ++b) acc[a][b] = 0.0;
+    const int64_t rbase = (int64_t)blockIdx.x * kRedRows;
+    for (int ch = 0; ch < kRedRows / kRedChunk; ++ch) {
+      const int64_t r0 = rbase + ch * kRedChunk;
+      if (r0 >= m) break;
+      __syncthreads();
+      for (int t = threadIdx.x; t < kRedChunk * p / 2; t += NT) {
+        const int rr = (2 * t) / p;
+        const bool ok = r0 + rr < m;
+        const double2 va = ok ? reinterpret_cast<const double2*>(A + r0 * p)[t] : make_double2(0.0, 0.0);
+        const double2 vb = ok ? reinterpret_cast<const double2*>(B + r0 * p)[t] : make_double2(0.0, 0.0);
+        reinterpret_cast<double2*>(sA)[t] = va;
+        reinterpret_cast<double2*>(sB)[t] = vb;
+      }
+      __syncthreads();
+      if (comp) {
+#pragma unroll 4
+        for (int rr = 0; rr < kRedChunk; ++rr) {
+          double av[PC], bv[PC];
+#pragma unroll
+          for (int a = 0; a < PC; ++a) av[a] = sA[rr * p + ti + 16 * a];
+#pragma unroll
+          for (int b = 0; b < PC; ++b) bv[b] = sB[rr * p + tj + 16 * b];
+#pragma unroll
+          for (int a = 0; a < PC; ++a)
+#pragma unroll
+            for (int b = 0; b < PC; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+        }
+      }
+    }
+    if (comp) {
+      double* dst = part + (int64_t)blockIdx.x * p * p;
+#pragma unroll
+      for (int a = 0; a < PC; ++a)
+#pragma unroll
+        for (int b = 0; b < PC; ++b) dst[(ti + 16 * a) * p + tj + 16 * b] = acc[a][b];
+    }
+  }
+  // CTA's partial stores -> barrier -> one acq_rel ticket (release of the CTA's stores, acquire
+  // of every other CTA's for the last one) -> barrier
+  PROBE(1);
+  __syncthreads();
+  if (threadIdx.x == 0) last_sh = (ticket_acq_rel(ticket) == gridDim.x - 1) ? 1u : 0u;
+  __syncthreads();
+  if (!last_sh) return;
+  PROBE(2);
+  const int nparts = gridDim.x;
+  constexpr int ld = p + 1;
+  double* S = fsm;            // p x ld
+  double* X = fsm + p * ld;   // p x p (V^T for MODE 2)
+  __shared__ double aux[p];
+  __shared__ double rcs[2][p / 2];
+  __shared__ int rpq[2][p / 2];
+  __shared__ int flag_sh, badsh[p], rank_sh[p], escale;
+  // fixed-order sum of the partials: thread t owns the element pair (2t, 2t+1), all loads of a
+  // batch of 8 partials in flight at once
+  for (int t = threadIdx.x; t < p * p / 2; t += NT) {
+    double2 a[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] = make_double2(0.0, 0.0);
+    int q = 0;
+    for (; q + 8 <= nparts; q += 8) {
+      double2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(reinterpret_cast<const double2*>(part + (int64_t)(q + u) * p * p) + t);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { a[u].x += v[u].x; a[u].y += v[u].y; }
+    }
+    for (; q < nparts; ++q) {
+      const double2 v = __ldcg(reinterpret_cast<const double2*>(part + (int64_t)q * p * p) + t);
+      a[0].x += v.x;
+      a[0].y += v.y;
+    }
+    const double vx = ((a[0].x + a[1].x) + (a[2].x + a[3].x)) + ((a[4].x + a[5].x) + (a[6].x + a[7].x));
+    const double vy = ((a[0].y + a[1].y) + (a[2].y + a[3].y)) + ((a[4].y + a[5].y) + (a[6].y + a[7].y));
+    const int e0 = 2 * t;
+    X[e0] = vx;  // staging (X is free until the solve)
+    X[e0 + 1] = vy;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < p * p; t += NT) {
+    const int i = t / p, j = t % p;
+    S[i * ld + j] = 0.5 * (X[i * p + j] + X[j * p + i]);
+  }
+  if (threadIdx.x == 0) *ticket = 0u;  // re-arm for the next launch (stream-ordered)
+  __syncthreads();
+  PROBE(3);
+  if (MODE == 0) {
+    for (int t = threadIdx.x; t < p * p; t += NT) out0[t] = S[(t / p) * ld + t % p];
+    return;
+  }
+  // exact power-of-two normalisation (keeps MUFU seeds in range): S' = S 2^-e
+  if (threadIdx.x < 32) {
+    double d = 0.0;
+    for (int i = threadIdx.x; i < p; i += 32) d = fmax(d, fabs(S[i * ld + i]));
+    for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xFFFFFFFFu, d, o));
+    if (threadIdx.x == 0) {
+      int e = (d > 0.0 && d < 1e300) ? ilogb(d) : 0;
+      if (MODE == 1) e = 2 * (e / 2);  // even, so R scales by 2^(e/2)
+      escale = e;
+    }
+  }
+  __syncthreads();
+  const int e = escale;
+  const double sc = ldexp(1.0, -e);
+  for (int t = threadIdx.x; t < p * p; t += NT) S[(t / p) * ld + t % p] *= sc;
+  __syncthreads();
+  if (MODE == 1) {
+    PROBE(4);
+    chol_block<p, ld, NT>(S, aux, badsh);
+    PROBE(5);
+    const double rs = ldexp(1.0, e / 2), ri = ldexp(1.0, -e / 2);
+    for (int t = threadIdx.x; t < p * p; t += NT) out0[t] = S[(t / p) * ld + t % p] * rs;
+    for (int t = threadIdx.x; t < p; t += NT) {
+      out1[t] = aux[t] * ri;
+      ibad[t] = badsh[t];
+    }
+    if (stats && threadIdx.x < 32) {
+      double lo = 1e300, hi = 0.0;
+      int nb = 0;
+      for (int j = threadIdx.x; j < p; j += 32) {
+        if (badsh[j]) { ++nb; continue; }
+        lo = fmin(lo, aux[j]);
+        hi = fmax(hi, aux[j]);
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xFFFFFFFFu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xFFFFFFFFu, hi, o));
+        nb += __shfl_xor_sync(0xFFFFFFFFu, nb, o);
+      }
+      if (threadIdx.x == 0) stats[0] = (nb > 0 || !(hi <= 1e4 * lo)) ? 1 : 0;
+    }
+    return;
+  }
+  // MODE 2: Rayleigh-Ritz eigensolve (X holds V^T, ld p)
+  for (int t = threadIdx.x; t < p * p; t += NT) X[t] = (t / p == t % p) ? 1.0 : 0.0;
+  PROBE(4);
+  const int sweeps = jacobi_block<p, ld>(S, X, rcs[0], rcs[1], rpq[0], rpq[1], &flag_sh);
+  PROBE(5);
+  if (threadIdx.x < p) aux[threadIdx.x] = S[threadIdx.x * ld + threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x < p) {
+    int rk = 0;
+    const double di = aux[threadIdx.x];
+    for (int j = 0; j < p; ++j) rk += (aux[j] > di) || (aux[j] == di && j < (int)threadIdx.x);
+    rank_sh[threadIdx.x] = rk;
+  }
+  __syncthreads();
+  // W[row][rank(col)] = V[row][col] = V^T[col][row]
+  for (int t = threadIdx.x; t < p * p; t += NT) {
+    const int col = t / p, row = t % p;
+    out0[row * p + rank_sh[col]] = X[col * p + row];
+  }
+  if (threadIdx.x < p) out1[rank_sh[threadIdx.x]] = aux[threadIdx.x] * ldexp(1.0, e);
+  if (threadIdx.x == 0 && stats) stats[0] = sweeps;
+}
+
+// Q = Y R^{-1} (R upper from CholQR) by row-wise forward substitution, one thread per row,
+// right-looking so every q_k finalises after one multiply: acc_c -= q_k R_kc (c > k).
+// Columns flagged bad come out zero (re-drawn at random afterwards).  Q32 mirrors Q.
+template <int P>
+__global__ void __launch_bounds__(32) trsm_kernel(const double* Y, const double* __restrict__ R,
+                                                  const double* __restrict__ dinv, const int* __restrict__ bad,
+                                                  const int* __restrict__ gate, int64_t m, double* Q,
+                                                  float* __restrict__ Q32) {
+  if (gate && *gate == 0) return;
+  extern __shared__ double sR[];  // [P * P]
+  __shared__ double sd[P];
+  for (int t = threadIdx.x; t < P * P / 2; t += blockDim.x)
+    reinterpret_cast<double2*>(sR)[t] = reinterpret_cast<const double2*>(R)[t];
+  for (int t = threadIdx.x; t < P; t += blockDim.x) sd[t] = bad[t] ? 0.0 : dinv[t];
+  __syncthreads();
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  double acc[P];
+#pragma unroll
+  for (int c = 0; c < P; c += 2) {
+    const double2 v = reinterpret_cast<const double2*>(Y + r * P)[c / 2];
+    acc[c] = v.x;
+    acc[c + 1] = v.y;
+  }
+#pragma unroll
+  for (int k = 0; k < P; ++k) {
+    const double qk = acc[k] * sd[k];
+    acc[k] = qk;
+#pragma unroll
+    for (int c = k + 1; c < P; ++c) acc[c] = fma(-qk, sR[k * P + c], acc[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < P; c += 2) {
+    reinterpret_cast<double2*>(Q + r * P)[c / 2] = make_double2(acc[c], acc[c + 1]);
+    if (Q32) reinterpret_cast<float2*>(Q32 + r * P)[c / 2] = make_float2((float)acc[c], (float)acc[c + 1]);
+  }
 }
 
 // ---------------------------------------------------------------- Out = In * M (m x p)(p x p)
-// in place allowed (each CTA stages its rows before writing them)
-__global__ void __launch_bounds__(256) matpp_kernel(const double* In0, double* Out0, const double* In1,
-                                                    double* Out1, const double* __restrict__ M, int64_t m, int p) {
+// in place allowed (each CTA stages its rows before writing them); optional fp32 mirrors
+__global__ void __launch_bounds__(256) matpp_kernel(const double* In0, double* Out0, float* Out0f, const double* In1,
+                                                    double* Out1, float* Out1f, const double* __restrict__ M, int64_t m, int p) {
   extern __shared__ double sm[];
   double* sM = sm;                 // p*p
   double* sI = sm + p * p;         // 16 rows x p
@@ -213,6 +680,7 @@ __global__ void __launch_bounds__(256) matpp_kernel(const double* In0, double* O
   for (int w = 0; w < 2; ++w) {
     const double* In = w ? In1 : In0;
     double* Out = w ? Out1 : Out0;
+    float* Outf = w ? Out1f : Out0f;
     if (!In) continue;
     __syncthreads();
     for (int t = threadIdx.x; t < 16 * p; t += 256) sI[t] = (r0 + t / p < m) ? In[r0 * p + t] : 0.0;
@@ -220,9 +688,16 @@ __global__ void __launch_bounds__(256) matpp_kernel(const double* In0, double* O
     for (int t = threadIdx.x; t < 16 * p; t += 256) {
       const int rr = t / p, cc = t % p;
       if (r0 + rr >= m) continue;
-      double s = 0.0;
-      for (int q = 0; q < p; ++q) s = fma(sI[rr * p + q], sM[q * p + cc], s);
+      double s0 = 0.0, s1 = 0.0;
+      int q = 0;
+      for (; q + 1 < p; q += 2) {
+        s0 = fma(sI[rr * p + q], sM[q * p + cc], s0);
+        s1 = fma(sI[rr * p + q + 1], sM[(q + 1) * p + cc], s1);
+      }
+      if (q < p) s0 = fma(sI[rr * p + q], sM[q * p + cc], s0);
+      const double s = s0 + s1;
       Out[(r0 + rr) * p + cc] = s;
+      if (Outf) Outf[(r0 + rr) * p + cc] = (float)s;
     }
   }
 }
@@ -248,249 +723,6 @@ __global__ void resid_kernel(const double* __restrict__ Z, const double* __restr
     const double t0 = fabs(theta[0]) > 0 ? fabs(theta[0]) : 1.0;
     res[r] = sqrt(sh[0]) / t0;
   }
-}
-
-// out[t] = sum_q part[q][t] in a fixed order (independent loads, unrolled)
-__global__ void psum_kernel(const double* __restrict__ part, int nparts, int n, double* __restrict__ out) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  int q = 0;
-  for (; q + 8 <= nparts; q += 8) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u) a[u] += part[(int64_t)(q + u) * n + t];
-  }
-  for (; q < nparts; ++q) a[0] += part[(int64_t)q * n + t];
-  out[t] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
-}
-
-// sum nparts partials of a p x p matrix into smem A (ld), symmetrised
-__device__ void load_sym(const double* __restrict__ part, int nparts, int p, double* A, int ld) {
-  for (int t = threadIdx.x; t < p * p; t += blockDim.x) {
-    const int i = t / p, j = t % p;
-    if (j < i) continue;
-    double s = 0.0, s2 = 0.0;
-    for (int q = 0; q < nparts; ++q) {
-      s += part[(int64_t)q * p * p + i * p + j];
-      s2 += part[(int64_t)q * p * p + j * p + i];
-    }
-    const double v = 0.5 * (s + s2);
-    A[i * ld + j] = v;
-    A[j * ld + i] = v;
-  }
-}
-
-// ---------------------------------------------------------------- p x p symmetric Jacobi
-// Parallel round-robin Jacobi, one CTA of 16 warps.  In each of the p-1 steps of a sweep the p/2
-// disjoint pairs are owned by warps (pair i -> warp i % 16); lane 0 of the owner computes the
-// rotation (Rutishauser, fp32 seeds + Newton to fp64 accuracy) and broadcasts it by shuffle, the
-// warp rotates rows P,Q (lanes over columns), barrier, then columns P,Q of A and V (lanes over
-// rows), barrier.  W = eigenvectors (columns sorted by eigenvalue desc), evals; stats[0] = sweeps.
-constexpr int kJW = 16;  // warps
-__device__ __forceinline__ double rcp_fast(double x) {  // 1/x, MUFU seed + 2 Newton steps (~1 ulp)
-  double r = (double)(1.0f / (float)x);
-  r = r * fma(-x, r, 2.0);
-  return r * fma(-x, r, 2.0);
-}
-__device__ __forceinline__ double rsqrt_fast(double x) {  // 1/sqrt(x), x in the fp32 range
-  double r = (double)rsqrtf((float)x);
-  r = r * fma(-0.5 * x * r, r, 1.5);
-  return r * fma(-0.5 * x * r, r, 1.5);
-}
-__device__ __forceinline__ void jacobi_rotation(double app, double aqq, double apq, double& c, double& s, bool& rot) {
-  c = 1.0;
-  s = 0.0;
-  rot = false;
-  // skip when a_pq^2 <= 1e-26 a_pp a_qq (|a_pq| <= 1e-13 sqrt(a_pp a_qq)) or a_pq is below fp32 range
-  if (!(apq * apq > 1e-26 * fabs(app * aqq)) || fabs(apq) < 1e-30 || fabs(apq) > 1e30) return;
-  // Rutishauser: th = (a_qq - a_pp) / (2 a_pq), t = sign(th) / (|th| + sqrt(th^2 + 1))
-  const double th = 0.5 * (aqq - app) * rcp_fast(apq);
-  double t;
-  const double ath = fabs(th);
-  if (ath > 1e18) {
-    t = 0.5 / th;
-  } else {
-    const double y = fma(th, th, 1.0);
-    const double ri = rcp_fast(ath + y * rsqrt_fast(y));
-    t = th >= 0.0 ? ri : -ri;
-  }
-  c = rsqrt_fast(fma(t, t, 1.0));
-  s = t * c;
-  rot = true;
-}
-
-__device__ __forceinline__ void rr_pair(int p, int step, int i, int& P, int& Q) {
-  int a, b;
-  if (i == 0) { a = p - 1; b = step; }
-  else { a = (step + i) % (p - 1); b = (step - i + (p - 1)) % (p - 1); }
-  P = min(a, b);
-  Q = max(a, b);
-}
-
-__global__ void __launch_bounds__(kJW * 32) jacobi_kernel(const double* __restrict__ Hin, int p,
-                                                          double* __restrict__ Wout, double* __restrict__ evals,
-                                                          int* __restrict__ stats) {
-  extern __shared__ double sm[];
-  const int ld = p + 1;
-  double* A = sm;
-  double* V = sm + p * ld;
-  __shared__ int rotated;
-  __shared__ double dsh[kMaxP];
-  __shared__ int rank_sh[kMaxP];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __shared__ int escale;
-  if (warp == 0) {  // power-of-two scale 2^-e of the matrix (exact), so MUFU seeds stay in range
-    double d = 0.0;
-    for (int i = lane; i < p; i += 32) d = fmax(d, fabs(Hin[i * p + i]));
-    for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xFFFFFFFFu, d, o));
-    if (lane == 0) escale = (d > 0.0 && d < 1e300) ? ilogb(d) : 0;
-  }
-  __syncthreads();
-  const int e = escale;
-  for (int i = warp; i < p; i += kJW)
-    for (int j = lane; j < p; j += 32) {
-      A[i * ld + j] = ldexp(0.5 * (Hin[i * p + j] + Hin[j * p + i]), -e);
-      V[i * ld + j] = (i == j) ? 1.0 : 0.0;
-    }
-  __syncthreads();
-  const int half = p / 2;
-  int sweep = 0;
-  for (; sweep < 30; ++sweep) {
-    if (threadIdx.x == 0) rotated = 0;
-    __syncthreads();
-    int rot_any = 0;
-    for (int step = 0; step < p - 1; ++step) {
-      // ---- rows (J^T A) for the pairs owned by this warp
-      double cs_c[4], cs_s[4];
-      int pp[4], qq[4];
-      // lane u computes the rotation of this warp's u-th pair (all in parallel)
-      double myc = 1.0, mys = 0.0;
-      {
-        const int i = warp + kJW * lane;
-        if (lane < 4 && i < half) {
-          int P, Q;
-          rr_pair(p, step, i, P, Q);
-          bool rot;
-          jacobi_rotation(A[P * ld + P], A[Q * ld + Q], A[P * ld + Q], myc, mys, rot);
-          rot_any |= rot;
-        }
-      }
-      int np = 0;
-      for (int i = warp; i < half; i += kJW, ++np) {
-        int P, Q;
-        rr_pair(p, step, i, P, Q);
-        const double c = __shfl_sync(0xFFFFFFFFu, myc, np);
-        const double s = __shfl_sync(0xFFFFFFFFu, mys, np);
-        cs_c[np] = c; cs_s[np] = s; pp[np] = P; qq[np] = Q;
-        if (s != 0.0) {
-          for (int col = lane; col < p; col += 32) {
-            const double ap = A[P * ld + col], aq = A[Q * ld + col];
-            A[P * ld + col] = c * ap - s * aq;
-            A[Q * ld + col] = s * ap + c * aq;
-          }
-        }
-      }
-      __syncthreads();
-      // ---- columns (A J, V J)
-      for (int u = 0; u < np; ++u) {
-        const double c = cs_c[u], s = cs_s[u];
-        if (s == 0.0) continue;
-        const int P = pp[u], Q = qq[u];
-        for (int row = lane; row < p; row += 32) {
-          const double ap = A[row * ld + P], aq = A[row * ld + Q];
-          A[row * ld + P] = c * ap - s * aq;
-          A[row * ld + Q] = s * ap + c * aq;
-          const double vp = V[row * ld + P], vq = V[row * ld + Q];
-          V[row * ld + P] = c * vp - s * vq;
-          V[row * ld + Q] = s * vp + c * vq;
-        }
-      }
-      __syncthreads();
-    }
-    if (rot_any) rotated = 1;
-    __syncthreads();
-    if (!rotated) break;
-  }
-  if (threadIdx.x < p) dsh[threadIdx.x] = A[threadIdx.x * ld + threadIdx.x];
-  __syncthreads();
-  if (threadIdx.x < p) {
-    int rk = 0;
-    const double di = dsh[threadIdx.x];
-    for (int j = 0; j < p; ++j) rk += (dsh[j] > di) || (dsh[j] == di && j < (int)threadIdx.x);
-    rank_sh[threadIdx.x] = rk;
-  }
-  __syncthreads();
-  for (int row = warp; row < p; row += kJW)
-    for (int i = lane; i < p; i += 32) Wout[row * p + rank_sh[i]] = V[row * ld + i];
-  if (threadIdx.x < p) evals[rank_sh[threadIdx.x]] = ldexp(dsh[threadIdx.x], e);
-  if (threadIdx.x == 0 && stats) stats[0] = sweep + 1;
-}
-
-// ---------------------------------------------------------------- Cholesky-QR step
-// B = H (p x p, symmetrised) = R^T R; Rinv = R^{-1} (upper).  Columns whose pivot is <= 1e-13 of
-// the largest diagonal are flagged bad[c] = 1 and get a zero Rinv column.  16 warps, rows owned
-// by warps and lanes over columns; every thread recomputes the pivot (no serial section).
-__global__ void __launch_bounds__(kJW * 32) chol_inv_kernel(const double* __restrict__ Hin, int p,
-                                                            double* __restrict__ Rinv, int* __restrict__ bad) {
-  extern __shared__ double sm[];
-  const int ld = p + 1;
-  double* B = sm;           // becomes R (upper)
-  double* X = sm + p * ld;  // Rinv
-  __shared__ int badsh[kMaxP];
-  __shared__ double dmax_sh;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = warp; i < p; i += kJW)
-    for (int j = lane; j < p; j += 32) {
-      B[i * ld + j] = 0.5 * (Hin[i * p + j] + Hin[j * p + i]);
-      X[i * ld + j] = 0.0;
-    }
-  __syncthreads();
-  if (warp == 0) {
-    double d = 0.0;
-    for (int i = lane; i < p; i += 32) d = fmax(d, B[i * ld + i]);
-    for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xFFFFFFFFu, d, o));
-    if (lane == 0) dmax_sh = d;
-  }
-  __syncthreads();
-  // exact even power-of-two normalisation: B' = B 2^-e2, R = R' 2^(e2/2), Rinv = Rinv' 2^-(e2/2)
-  const int e2 = (dmax_sh > 0.0 && dmax_sh < 1e300) ? 2 * (ilogb(dmax_sh) / 2) : 0;
-  for (int i = warp; i < p; i += kJW)
-    for (int j = lane; j < p; j += 32) B[i * ld + j] = ldexp(B[i * ld + j], -e2);
-  __syncthreads();
-  const double tol = 1e-13 * ldexp(dmax_sh, -e2);
-  for (int j = 0; j < p; ++j) {
-    const double d = B[j * ld + j];
-    const bool ok = d > tol && d > 0.0;
-    const double inv = ok ? rsqrt_fast(d) : 0.0;   // 1 / R_jj
-    const double rjj = d * inv;
-    // trailing update with the row of R computed on the fly: B[i][k] -= R[j][i] R[j][k]
-    for (int i = j + 1 + warp; i < p; i += kJW) {
-      const double rji = B[j * ld + i] * inv;
-      for (int k = i + lane; k < p; k += 32) B[i * ld + k] -= rji * (B[j * ld + k] * inv);
-    }
-    __syncthreads();
-    if (warp == 0) {
-      for (int k = j + 1 + lane; k < p; k += 32) B[j * ld + k] *= inv;
-      if (lane == 0) { B[j * ld + j] = rjj; badsh[j] = ok ? 0 : 1; }
-    }
-    __syncthreads();
-  }
-  // Rinv = R^{-1} from the bottom row up; X[i][.] accumulates sum_{k>i} R[i][k] Rinv[k][.]
-  for (int j = p - 1; j >= 0; --j) {
-    const bool okj = !badsh[j];
-    const double inv = okj ? rcp_fast(B[j * ld + j]) : 0.0;
-    if (warp == 0)
-      for (int cc = lane; cc < p; cc += 32) X[j * ld + cc] = okj ? (((cc == j) ? 1.0 : 0.0) - X[j * ld + cc]) * inv : 0.0;
-    __syncthreads();
-    for (int i = warp; i < j; i += kJW) {
-      const double rij = B[i * ld + j];
-      for (int cc = j + lane; cc < p; cc += 32) X[i * ld + cc] = fma(rij, X[j * ld + cc], X[i * ld + cc]);
-    }
-    __syncthreads();
-  }
-  for (int i = warp; i < p; i += kJW)
-    for (int cc = lane; cc < p; cc += 32) Rinv[i * p + cc] = ldexp(X[i * ld + cc], -e2 / 2);
-  for (int cc = threadIdx.x; cc < p; cc += blockDim.x) bad[cc] = badsh[cc];
 }
 
 // V_out[j][r] = sign_r * U[j][r] (r < k), sign making the largest-|.| entry positive
@@ -529,85 +761,136 @@ __global__ void finalize_vectors_kernel(const double* __restrict__ U, const doub
 avd_status launch_gram_finalize(Ctx* c) {
   const int64_t m = c->cfg.m;
   const double unit = (c->nd == 3) ? 16384.0 : 1.0;
-  dim3 grid((unsigned)ceil_div(m, 256), (unsigned)m);
-  gram_finalize_kernel<<<grid, 256, 0, c->stream>>>(c->gram_i, m, c->m_pad, c->shift, unit, c->G);
+  dim3 grid((unsigned)ceil_div(c->m_pad, 256), (unsigned)c->m_pad);
+  gram_finalize_kernel<<<grid, 256, 0, c->stream>>>(c->gram_i, m, c->m_pad, c->shift, c->qsum,
+                                                    1.0 / (double)c->cfg.l_global, unit, c->G, c->G32);
   AVD_LAUNCHED(c);
-  trace_kernel<<<1, 256, 0, c->stream>>>(c->G, m, c->trace);
+  trace_kernel<<<1, 256, 0, c->stream>>>(c->G, m, c->m_pad, c->trace, c->gmax);
   AVD_LAUNCHED(c);
   return AVD_OK;
+}
+
+// stream-K geometry shared by the plan (workspace) and the launches
+void gemm_geometry(int64_t m_pad, int p, int num_sms, bool fp32, int* BM, int* ncta, int64_t* U, int* KT) {
+  *BM = (fp32 && p <= 64) ? 128 : 64;  // = 16 * NR of the gemm32 / gemm64 instantiations
+  const int64_t RB = m_pad / *BM;
+  *KT = (int)ceil_div(m_pad, kSkBK);
+  *U = RB * (int64_t)(*KT);
+  int64_t n = (int64_t)num_sms * (fp32 ? 3 : 2);
+  n = std::max<int64_t>(n, RB);
+  n = std::min<int64_t>(n, *U);
+  *ncta = (int)n;
+}
+size_t gemm_part_bytes(int64_t m_pad, int p, int num_sms) {
+  (void)num_sms;
+  return sizeof(unsigned long long) * (size_t)m_pad * p;  // Yfix
 }
 
 namespace {
 
-// Y = G In (split-K partials summed in a fixed order)
-avd_status gemm_g(Ctx* c, const double* In, double* Out) {
-  const int64_t m = c->cfg.m;
-  const int ks = c->gemm_ks;
-  const int64_t kchunk = round_up(ceil_div(m, ks), kGK);
-  dim3 grid((unsigned)ceil_div(m, kGM), (unsigned)ks);
-  switch (c->p / 16) {
-#define CASE(PC)                                                                                          \
-  case PC: {                                                                                              \
-    const int sm = 2 * (kGK * (kGM + 2) + kGK * PC * 16) * (int)sizeof(double);                           \
-    AVD_CUDA(cudaFuncSetAttribute(gemm_gq_kernel<PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));  \
-    gemm_gq_kernel<PC><<<grid, 128, sm, c->stream>>>(c->G, In, m, kchunk, c->Ypart);                      \
-    break;                                                                                                \
-  }
-    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
-#undef CASE
-    default: set_error("unsupported p"); return AVD_EINVAL;
-  }
+// Y = G In (fp64 G, fp64 math) or Y = G32 In32 (fp32); Y fp64 (+ optional fp32 mirror)
+template <typename T, int NR, int NC>
+avd_status gemm_launch(Ctx* c, const T* Gm, const T* In, int level, double* Y, float* Y32) {
+  int BM, ncta, KT;
+  int64_t U;
+  const int p = 8 * NC;
+  gemm_geometry(c->m_pad, p, c->num_sms, sizeof(T) == 4, &BM, &ncta, &U, &KT);
+  if (BM != 16 * NR) { set_error("gemm geometry mismatch"); return AVD_EINVAL; }
+  const int sm = kSkStages * (kSkBK * BM + kSkBK * p) * (int)sizeof(T);
+  AVD_CUDA(cudaFuncSetAttribute(gemm_sk_kernel<T, NR, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  auto* yfix = reinterpret_cast<unsigned long long*>(c->gemm_part);
+  gemm_sk_kernel<T, NR, NC><<<ncta, kSkThreads, sm, c->stream>>>(Gm, c->m_pad, In, c->cfg.m, U, KT, ncta, yfix,
+                                                                  c->gmax, level);
   AVD_LAUNCHED(c);
-  const int64_t n = m * c->p;
-  ksum_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c->stream>>>(c->Ypart, ks, n, Out);
+  const int64_t n = c->cfg.m * p;
+  fix_convert_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c->stream>>>(yfix, n, c->cfg.m, c->gmax, level, Y, Y32);
   AVD_LAUNCHED(c);
   return AVD_OK;
 }
 
-// H = A^T B (m-length reduction): per-CTA partials, then a multi-CTA fixed-order sum into c->H
-avd_status atb(Ctx* c, const double* A, const double* B) {
-  const int64_t m = c->cfg.m;
+avd_status gemm64(Ctx* c, const double* In, int level, double* Y, float* Y32) {
+  switch (c->p / 16) {
+#define CASE(PC) case PC: return gemm_launch<double, 4, 2 * PC>(c, c->G, In, level, Y, Y32);
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
+#undef CASE
+  }
+  set_error("unsupported p");
+  return AVD_EINVAL;
+}
+avd_status gemm32(Ctx* c, const float* In, int level, double* Y, float* Y32) {
+  switch (c->p / 16) {
+#define CASE(PC) case PC: return gemm_launch<float, (PC <= 4 ? 8 : 4), 2 * PC>(c, c->G32, In, level, Y, Y32);
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
+#undef CASE
+  }
+  set_error("unsupported p");
+  return AVD_EINVAL;
+}
+
+template <int MODE>
+avd_status atb_fused(Ctx* c, const double* A, const double* B, double* out0, double* out1, int* ibad, int* stats,
+                     const int* gate = nullptr) {
   const int p = c->p;
-  const size_t sm = 2 * kRedChunk * p * sizeof(double);
+  const int n_red = (int)ceil_div(c->cfg.m, kRedRows);
+  const int chunk = p <= 48 ? kRedRows : 64;
+  const size_t sm = std::max<size_t>(2 * (size_t)chunk * p, (size_t)p * (p + 1) + (size_t)p * p) * sizeof(double);
   switch (p / 16) {
-#define CASE(PC)                                                                                      \
-  case PC:                                                                                            \
-    AVD_CUDA(cudaFuncSetAttribute(atb_partial_kernel<PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
-    atb_partial_kernel<PC><<<c->n_red, 256, sm, c->stream>>>(A, B, m, c->red_part);                   \
+#define CASE(PC)                                                                                                \
+  case PC:                                                                                                      \
+    AVD_CUDA(cudaFuncSetAttribute(atb_fused_kernel<MODE, PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+    atb_fused_kernel<MODE, PC><<<n_red, RedCfg<PC>::threads, sm, c->stream>>>(A, B, c->cfg.m, c->red_part, c->ticket, out0, out1,  \
+                                                              ibad, stats, gate);                               \
     break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
     default: set_error("unsupported p"); return AVD_EINVAL;
   }
   AVD_LAUNCHED(c);
-  psum_kernel<<<(unsigned)ceil_div(p * p, 128), 128, 0, c->stream>>>(c->red_part, c->n_red, p * p, c->H);
-  AVD_LAUNCHED(c);
   return AVD_OK;
 }
 
-avd_status matpp(Ctx* c, const double* In0, double* Out0, const double* In1, double* Out1, const double* M) {
+avd_status matpp(Ctx* c, const double* In0, double* Out0, float* Out0f, const double* In1, double* Out1,
+                 float* Out1f, const double* M) {
   const int p = c->p;
   const size_t sm = ((size_t)p * p + 16 * p) * sizeof(double);
   AVD_CUDA(cudaFuncSetAttribute(matpp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  matpp_kernel<<<(unsigned)ceil_div(c->cfg.m, 16), 256, sm, c->stream>>>(In0, Out0, In1, Out1, M, c->cfg.m, p);
+  matpp_kernel<<<(unsigned)ceil_div(c->cfg.m, 16), 256, sm, c->stream>>>(In0, Out0, Out0f, In1, Out1, Out1f, M,
+                                                                         c->cfg.m, p);
   AVD_LAUNCHED(c);
   return AVD_OK;
 }
 
-// Q <- orth(Y) by Cholesky-QR2; rank-deficient columns are re-drawn at random between passes.
-avd_status orth(Ctx* c, const double* Y, double* Q, uint32_t seed) {
+avd_status trsm(Ctx* c, const double* Y, const double* R, const double* dinv, const int* bad, const int* gate) {
+  const unsigned grid = (unsigned)ceil_div(c->cfg.m, 32);
+  switch (c->p / 16) {
+#define CASE(PC)                                                                                              \
+  case PC:                                                                                                    \
+    AVD_CUDA(cudaFuncSetAttribute(trsm_kernel<16 * PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * PC * PC * 8)); \
+    trsm_kernel<16 * PC><<<grid, 32, 256 * PC * PC * 8, c->stream>>>(Y, R, dinv, bad, gate, c->cfg.m, c->Q, c->Q32); \
+    break;
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
+#undef CASE
+    default: set_error("unsupported p"); return AVD_EINVAL;
+  }
+  AVD_LAUNCHED(c);
+  return AVD_OK;
+}
+
+// Q <- orth(Y) by Cholesky-QR (Q32 mirrors Q).  The second pass (CholQR2) runs only when the
+// first one flagged it (a rank-deficient column, re-drawn at random in between, or
+// cond(R)^2 > 1e6, where one pass leaves orthogonality errors above ~1e-10); otherwise its two
+// kernels exit at once.
+avd_status orth(Ctx* c, const double* Y, uint32_t seed) {
   int* bad = reinterpret_cast<int*>(c->resid + c->p);
+  int* need2 = bad + c->p;
   const int p = c->p;
-  const size_t sm = 2 * (size_t)p * (p + 1) * sizeof(double);
-  AVD_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   for (int pass = 0; pass < 2; ++pass) {
-    const double* src = pass == 0 ? Y : Q;
-    AVD_TRY(atb(c, src, src));
-    chol_inv_kernel<<<1, kJW * 32, sm, c->stream>>>(c->H, p, c->W, bad);
-    AVD_LAUNCHED(c);
-    AVD_TRY(matpp(c, src, Q, nullptr, nullptr, c->W));
+    const double* src = pass == 0 ? Y : c->Q;
+    const int* gate = pass == 0 ? nullptr : need2;
+    AVD_TRY(atb_fused<1>(c, src, src, c->W, c->H, bad, pass == 0 ? need2 : nullptr, gate));  // R -> W, 1/R_jj -> H
+    AVD_TRY(trsm(c, src, c->W, c->H, bad, gate));                   // in place allowed (row-wise)
     if (pass == 0) {
-      rand_fill_kernel<<<(unsigned)ceil_div(c->cfg.m * p, 256), 256, 0, c->stream>>>(Q, c->cfg.m, p, seed, bad);
+      rand_fill_kernel<<<(unsigned)ceil_div(c->cfg.m * p, 256), 256, 0, c->stream>>>(c->Q, c->Q32, c->cfg.m, p, seed, bad);
       AVD_LAUNCHED(c);
     }
   }
@@ -616,33 +899,31 @@ avd_status orth(Ctx* c, const double* Y, double* Q, uint32_t seed) {
 
 }  // namespace
 
-// Subspace iteration: every iteration applies G^2 (two GEMMs) and re-orthonormalises; a
-// Rayleigh-Ritz check runs on a schedule predicted from the observed residual decay (at most
-// every 4 iterations, always on the last one), so the p x p Jacobi runs ~3-4 times per solve.
+// Subspace iteration: power steps Q <- orth(G^2 Q) in fp32; a Rayleigh-Ritz check (fp64) runs
+// on a schedule predicted from the observed residual decay (at most every 8 steps, always on the
+// last one), so the p x p Jacobi runs ~2-3 times per solve.
 avd_status run_eig(Ctx* c) {
   const int64_t m = c->cfg.m;
   const int p = c->p, k = c->k;
   const uint32_t seed = (uint32_t)(c->cfg.seed ^ (c->cfg.seed >> 32)) * 2654435761u + 12345u;
   int* jstats = reinterpret_cast<int*>(c->theta + p);  // [16] sweeps per RR solve
   AVD_CUDA(cudaMemsetAsync(jstats, 0, 16 * sizeof(int), c->stream));
-  const size_t jsm = 2 * (size_t)p * (p + 1) * sizeof(double);
-  AVD_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jsm));
-  rand_fill_kernel<<<(unsigned)ceil_div(m * p, 256), 256, 0, c->stream>>>(c->Z, m, p, seed, nullptr);
+  AVD_CUDA(cudaMemsetAsync(c->ticket, 0, sizeof(unsigned), c->stream));
+  AVD_CUDA(cudaMemsetAsync(c->gemm_part, 0, gemm_part_bytes(c->m_pad, p, c->num_sms), c->stream));
+  rand_fill_kernel<<<(unsigned)ceil_div(m * p, 256), 256, 0, c->stream>>>(c->Z, nullptr, m, p, seed, nullptr);
   AVD_LAUNCHED(c);
-  AVD_TRY(orth(c, c->Z, c->Q, seed + 1));
+  AVD_TRY(orth(c, c->Z, seed + 1));
   const int max_it = c->cfg.max_iters > 0 ? c->cfg.max_iters : 100;
   const double tol = c->cfg.eig_tol > 0 ? c->cfg.eig_tol : 1e-6;  // V angle <~ tol * lambda_1 / gap_k
   int it = 0, next_rr = 2, prev_it = 0, rr_count = 0;
   double maxres = 0.0, prev_res = -1.0;
   bool conv = false;
   for (it = 1; it <= max_it; ++it) {
-    AVD_TRY(gemm_g(c, c->Q, c->Y));                         // Y = G Q
     if (it == next_rr || it == max_it) {
       ++rr_count;
-      AVD_TRY(atb(c, c->Q, c->Y));                          // H = Q^T Y
-      jacobi_kernel<<<1, kJW * 32, jsm, c->stream>>>(c->H, p, c->W, c->theta, jstats + std::min(rr_count - 1, 15));
-      AVD_LAUNCHED(c);
-      AVD_TRY(matpp(c, c->Y, c->Z, c->Q, c->U, c->W));      // Z = Y W, U = Q W (Ritz vectors)
+      AVD_TRY(gemm64(c, c->Q, 0, c->Y, nullptr));           // Y = G Q (exact G, fp64)
+      AVD_TRY(atb_fused<2>(c, c->Q, c->Y, c->W, c->theta, nullptr, jstats + std::min(rr_count - 1, 15)));
+      AVD_TRY(matpp(c, c->Y, c->Z, c->Z32, c->Q, c->U, nullptr, c->W));  // Z = Y W, U = Q W (Ritz vectors)
       resid_kernel<<<k, 256, 0, c->stream>>>(c->Z, c->U, c->theta, m, p, c->resid);
       AVD_LAUNCHED(c);
       AVD_CUDA(cudaMemcpyAsync(c->eig_host, c->theta, sizeof(double) * p, cudaMemcpyDeviceToHost, c->stream));
@@ -660,17 +941,17 @@ avd_status run_eig(Ctx* c) {
       int step = 1;
       if (rate > 0.0 && rate < 0.95) {
         const double need = std::log(tol / maxres) / std::log(rate);
-        step = (int)std::max(1.0, std::min(8.0, std::floor(need)));
+        step = (int)std::max(1.0, std::min(8.0, std::ceil(need)));
       }
       prev_res = maxres;
       prev_it = it;
       next_rr = it + step;
-      AVD_TRY(gemm_g(c, c->Z, c->Y));                       // Y = G Z = G^2 U
+      AVD_TRY(gemm32(c, c->Z32, 1, c->Y, nullptr));        // Y = G Z = G^2 U
     } else {
-      AVD_TRY(gemm_g(c, c->Y, c->Z));                       // Z = G Y = G^2 Q
-      std::swap(c->Y, c->Z);
+      AVD_TRY(gemm32(c, c->Q32, 0, c->Z, c->Z32));         // Z = G Q
+      AVD_TRY(gemm32(c, c->Z32, 1, c->Y, nullptr));        // Y = G Z = G^2 Q
     }
-    AVD_TRY(orth(c, c->Y, c->Q, seed + 7919u * (uint32_t)it));
+    AVD_TRY(orth(c, c->Y, seed + 7919u * (uint32_t)it));
   }
   c->iters = std::min(it, max_it);
   c->rr_count = rr_count;
