@@ -335,10 +335,12 @@ def main():
                 "executed_frac": exec_ops / t_gram / 1e12 / int8_peak,
                 "launch_ms": t_gram * 1e3}
     hbm = peaks.get("hbm_gbs", 6650.0)
+    samp = max(1, min(16, l // 4096))
+    samp = 1 << (samp.bit_length() - 1)
     streams = {
-        "stats (K1)": (lloc * m * 4, stage_ms.get("stats")),
-        "split (K2)": (lloc * m * (4 + nd), stage_ms.get("split")),
-        "project+energy (K5/K8)": (lloc * m * 4, stage_ms.get("project")),
+        "row sample (K1s, 1/%d of the rows)" % samp: (lloc * m * 4 // samp, stage_ms.get("stats")),
+        "fused pass (K1+K2: read X, write digits)": (lloc * m * (4 + nd), stage_ms.get("split")),
+        "project+energy (K5/K8: read X twice)": (2 * lloc * m * 4, stage_ms.get("project")),
     }
     stream_roof = {k: {"GB/s": b / (t * 1e-3) / 1e9, "frac_hbm": b / (t * 1e-3) / 1e9 / hbm}
                    for k, (b, t) in streams.items() if t}

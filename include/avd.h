@@ -83,6 +83,9 @@ typedef struct {
 
 /* avd_config.flags: select E_top by streaming X even when the candidate list would do (tests) */
 #define AVD_FLAG_STREAM_SELECT 1
+/* avd_config.flags: quantise the Gram operand with the exact column ranges (the fallback taken
+ * when the row-sampled ranges overflow the digit range; forced here for tests)               */
+#define AVD_FLAG_EXACT_SCALE 2
 
 /* Outputs.  Device arrays caller-owned, sized from the plan (cap = n_top). */
 typedef struct {
@@ -109,6 +112,7 @@ typedef struct {
   double max_resid;        /* max_r<k ||G v_r - lambda_r v_r|| / lambda_1                     */
   int32_t rr_checks;      /* Rayleigh-Ritz checks of the eigensolver (diagnostic)           */
   int32_t jacobi_sweeps;   /* total sweeps of the p x p Jacobi solves (diagnostic)           */
+  int32_t requantised;     /* 1 if the Gram operand was re-quantised with exact column ranges */
 } avd_outputs;
 
 typedef struct avd_ctx avd_ctx;
@@ -137,15 +141,22 @@ avd_status avd_decompose_host(avd_ctx* ctx, const float* X_host, avd_outputs* ou
 /* ---- stage entry points (row-sharded, world >= 1) -------------------------------------
  * Call in this order; after each stage the caller all-reduces (over all ranks, in place)
  * the buffers listed, then calls the next stage.  With world == 1 no exchange is needed.
- *   avd_stage_stats    (K1 column sums, sum x^2, #nonzero, column max/min, row-sampled |x|
- *                       histogram)
- *       exchange: AVD_BUF_STATS (f64, SUM), AVD_BUF_COLMAX (f32, MAX),
- *                 AVD_BUF_COLMIN (f32, MIN), AVD_BUF_HIST1 (i64, SUM)
- *   avd_stage_split    (mu, column scales, candidate bin b0, K2 centred int8 digit planes +
- *                       top-set candidates)
- *   avd_stage_gram     (K3 tcgen05 int8 Gram, exact int64)
- *       exchange: AVD_BUF_GRAM (i64, SUM), AVD_BUF_CAND (i64, SUM)
- *   avd_stage_eig      (K4 subspace iteration + Rayleigh-Ritz; replicated on every rank)
+ *   avd_stage_stats    (row sample, global rows i % s == 0, s = 16 at l >= 64k: column sums,
+ *                       max, min, and on every 4th sampled row the |x| histogram bits 30:19;
+ *                       they seed the quantiser centre / scale and the candidate bin b0)
+ *       exchange: AVD_BUF_SAMPLE (f64, SUM), AVD_BUF_SMAX (f32, MAX), AVD_BUF_SMIN (f32, MIN),
+ *                 AVD_BUF_HIST1 (i64, SUM)
+ *   avd_stage_split    (the fused pass over X: fp64 column sums, sum x^2, #nonzero, the exact
+ *                       column range about the quantiser centre, the centred int8 digit planes of
+ *                       the Gram operand with their integer column sums and squared rounding
+ *                       errors, the top-set candidates)
+ *       exchange: AVD_BUF_STATS (f64, SUM), AVD_BUF_COLMAX (f32, MAX: max |x - quantiser centre|)
+ *   avd_stage_gram     (mu; AVD_ENONFINITE if X has NaN/Inf; re-quantisation with the exact
+ *                       ranges if any rank's digits overflowed; K3 tcgen05 int8 Gram, exact int64)
+ *       exchange: AVD_BUF_GRAM (i64, SUM), AVD_BUF_CAND (i64, SUM), AVD_BUF_QSUM (i64, SUM),
+ *                 AVD_BUF_QERR (f64, SUM)
+ *   avd_stage_eig      (exact centring of the Gram, K4 subspace iteration + Rayleigh-Ritz;
+ *                       replicated on every rank)
  *   avd_stage_project  (K5+K8 projections P = Xc V_k and elementwise energies)
  *       exchange: AVD_BUF_ENERGY (f64, SUM)
  *   avd_stage_select(level 0)  (K6 exact |x| histogram, bits 30:19)  exchange: AVD_BUF_HIST0 (i64, SUM)
@@ -155,13 +166,14 @@ avd_status avd_decompose_host(avd_ctx* ctx, const float* X_host, avd_outputs* ou
  *   avd_stage_gather   (K6 ordered compaction with the rank's tie quota, K7 rho gather)
  *       exchange: AVD_BUF_AGG (f64, SUM)
  *   avd_stage_report   (host scalars into out)
- * The K6 histograms read the K2 candidate list (entries with |x| bits >= bin b0 chosen from the
+ * The K6 histograms read the candidate list (entries with |x| bits >= bin b0 chosen from the
  * row-sampled histogram), or stream X itself when the exchanged candidate count does not cover
  * |E_top| or a rank overflowed its candidate capacity; both give the exact same E_top.        */
 typedef enum {
   AVD_BUF_STATS = 0, AVD_BUF_COLMAX = 1, AVD_BUF_COLMIN = 2, AVD_BUF_HIST1 = 3,
   AVD_BUF_GRAM = 4, AVD_BUF_ENERGY = 5, AVD_BUF_HIST2 = 6, AVD_BUF_HIST3 = 7,
   AVD_BUF_TIES = 8, AVD_BUF_AGG = 9, AVD_BUF_HIST0 = 10, AVD_BUF_CAND = 11,
+  AVD_BUF_SAMPLE = 12, AVD_BUF_SMAX = 13, AVD_BUF_SMIN = 14, AVD_BUF_QSUM = 15, AVD_BUF_QERR = 21,
   /* read-only views for tests / diagnostics (not exchanged) */
   AVD_BUF_MU = 16, AVD_BUF_G = 17, AVD_BUF_P = 18, AVD_BUF_DIGITS = 19, AVD_BUF_SCALE = 20
 } avd_buffer_id;
@@ -171,7 +183,7 @@ avd_status avd_buffer(avd_ctx* ctx, int32_t which, void** dev_ptr, size_t* bytes
 
 avd_status avd_stage_stats(avd_ctx* ctx, const float* X_dev);
 avd_status avd_stage_split(avd_ctx* ctx, const float* X_dev);
-avd_status avd_stage_gram(avd_ctx* ctx);
+avd_status avd_stage_gram(avd_ctx* ctx, const float* X_dev);
 avd_status avd_stage_eig(avd_ctx* ctx);
 avd_status avd_stage_project(avd_ctx* ctx, const float* X_dev);
 avd_status avd_stage_select(avd_ctx* ctx, const float* X_dev, int32_t level, int32_t rank);

@@ -11,9 +11,10 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libavd.so")
 
+AVD_FLAG_STREAM_SELECT, AVD_FLAG_EXACT_SCALE = 1, 2
 AVD_OK, AVD_EINVAL, AVD_ENONFINITE, AVD_ENOCONV, AVD_ECUDA, AVD_ENOMEM, AVD_ESTATE = 0, 1, 2, 3, 4, 6, 8
 BUF = dict(STATS=0, COLMAX=1, COLMIN=2, HIST1=3, GRAM=4, ENERGY=5, HIST2=6, HIST3=7, TIES=8, AGG=9,
-           HIST0=10, CAND=11,
+           HIST0=10, CAND=11, SAMPLE=12, SMAX=13, SMIN=14, QSUM=15, QERR=21,
            MU=16, G=17, P=18, DIGITS=19, SCALE=20)
 
 # every symbol include/avd.h declares
@@ -51,7 +52,8 @@ class avd_outputs(ctypes.Structure):
                 ("rho_mean_aggr", ctypes.c_double * 4), ("rho_energy_aggr", ctypes.c_double * 3),
                 ("sigma_next", ctypes.c_double), ("trace_g", ctypes.c_double),
                 ("iters", ctypes.c_int32), ("max_resid", ctypes.c_double),
-                ("rr_checks", ctypes.c_int32), ("jacobi_sweeps", ctypes.c_int32)]
+                ("rr_checks", ctypes.c_int32), ("jacobi_sweeps", ctypes.c_int32),
+                ("requantised", ctypes.c_int32)]
 
 
 _lib = None
@@ -82,7 +84,7 @@ def lib() -> ctypes.CDLL:
         L.avd_buffer.argtypes = [P, I32, ctypes.POINTER(P), ctypes.POINTER(ctypes.c_size_t)]
         L.avd_stage_stats.argtypes = [P, P]
         L.avd_stage_split.argtypes = [P, P]
-        L.avd_stage_gram.argtypes = [P]
+        L.avd_stage_gram.argtypes = [P, P]
         L.avd_stage_eig.argtypes = [P]
         L.avd_stage_project.argtypes = [P, P]
         L.avd_stage_select.argtypes = [P, P, I32, I32]
@@ -157,8 +159,8 @@ def avd_stage_split(h, X_ptr: int):
     return check(lib().avd_stage_split(h, ctypes.c_void_p(X_ptr)), "avd_stage_split")
 
 
-def avd_stage_gram(h):
-    return check(lib().avd_stage_gram(h), "avd_stage_gram")
+def avd_stage_gram(h, X_dev: int):
+    return check(lib().avd_stage_gram(h, X_dev), "avd_stage_gram")
 
 
 def avd_stage_eig(h):

@@ -39,6 +39,7 @@ class Result:
     status: int
     rr_checks: int = 0
     jacobi_sweeps: int = 0
+    requantised: int = 0        # 1: Gram operand re-quantised with the exact column ranges
 
     @property
     def shares_cf(self):
@@ -114,7 +115,8 @@ class Decomposer:
                       rho_mean_aggr=_to_list(o.rho_mean_aggr),
                       rho_energy_aggr=_to_list(o.rho_energy_aggr), sigma_next=float(o.sigma_next),
                       trace_g=float(o.trace_g), iters=int(o.iters), max_resid=float(o.max_resid),
-                      status=st, rr_checks=int(o.rr_checks), jacobi_sweeps=int(o.jacobi_sweeps))
+                      status=st, rr_checks=int(o.rr_checks), jacobi_sweeps=int(o.jacobi_sweeps),
+                      requantised=int(o.requantised))
 
     def _check_X(self, X: torch.Tensor):
         if not (X.is_cuda and X.dtype == torch.float32 and X.is_contiguous()):

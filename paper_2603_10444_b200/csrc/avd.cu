@@ -25,10 +25,11 @@ int64_t floor_frac(double f, int64_t n) {
 
 struct Layout {
   // byte offsets inside the single workspace allocation
-  size_t off[64];
+  size_t off[128];
   size_t total = 0;
   int n = 0;
   size_t add(size_t bytes) {
+    if (n >= 128) return (size_t)n;  // make_plan checks n against the bound below
     total = (total + 255) & ~size_t(255);
     off[n] = total;
     total += bytes;
@@ -74,6 +75,7 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   const int64_t ll = cfg->l_local;
   const int ncb = (int)ceil_div(m, 256LL * ((m % 4 == 0) ? 4 : 1));
   C->r1 = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(4LL * C->num_sms, ncb), ceil_div(ll, 4)));
+  C->r1 = (int)std::max<int64_t>(C->r1, ceil_div(ll, 65536));  // int32 per-chunk sums of q (k_pass1.cu)
   C->cand_cap = std::min<int64_t>(ll * m, std::max<int64_t>(4 * n_top, 1 << 20));
   C->n_red = (int)ceil_div(m, kRedRowsC);  // partials of the m-length p x p reductions
   C->n_proj_ctas = (int)ceil_div(ll, 32);
@@ -86,7 +88,7 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   L.add(sizeof(float) * C->r1 * m);             // 1 colmax_part
   L.add(sizeof(float) * C->r1 * m);             // 2 colmin_part
   L.add(sizeof(double) * C->r1 * ncb);          // 3 sq_part
-  L.add(sizeof(double) * (m + 3));              // 4 stats
+  L.add(sizeof(double) * (m + 4));              // 4 stats
   L.add(sizeof(float) * m);                     // 5 colmax
   L.add(sizeof(float) * m);                     // 6 colmin
   L.add(sizeof(unsigned long long) * kHistBins);// 7 hist1
@@ -133,11 +135,24 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   L.add(sizeof(float) * 2 * C->m_pad * (((C->k_pad + 31) / 32) * 32));   // 48 V_hl
   L.add(sizeof(float) * 2 * C->m_pad);                                   // 49 mu_hl
   L.add(sizeof(float) * C->m_pad * C->m_pad);                            // 50 G32
-  L.add(sizeof(long long) * C->m_pad);                                   // 51 qsum
+  L.add(sizeof(long long) * 2 * C->m_pad);                               // 51 qsum
   L.add(sizeof(float) * m * p);                                          // 52 Q32
   L.add(sizeof(float) * m * p);                                          // 53 Z32
   L.add(sizeof(unsigned) * 4);                                           // 54 ticket
   L.add(sizeof(double));                                                 // 55 gmax
+  L.add(sizeof(double) * (m + 1));                                       // 56 samp
+  L.add(sizeof(float) * m);                                              // 57 smax
+  L.add(sizeof(float) * m);                                              // 58 smin
+  L.add(sizeof(float) * C->m_pad);                                       // 59 qscale
+  L.add(sizeof(float) * C->m_pad);                                       // 60 qoff
+  L.add(sizeof(long long) * C->r1 * m);                                  // 61 qsum_part
+  L.add(sizeof(long long) * 2 * C->m_pad);                               // 62 qsum_local
+  L.add(sizeof(float) * C->r1 * m);                                      // 63 qerr_part
+  L.add(sizeof(double) * C->m_pad);                                      // 64 qerr_local
+  L.add(sizeof(double) * C->m_pad);                                      // 65 qerr
+  L.add(sizeof(float) * C->m_pad);                                       // 66 mu0
+  L.add(sizeof(long long) * C->r1 * m);                                  // 67 qsq_part
+  if (L.n >= 128) { set_error("workspace layout table overflow"); return AVD_EINVAL; }
   plan->workspace_bytes = L.total;
   if (lay) *lay = L;
   return AVD_OK;
@@ -274,6 +289,9 @@ avd_status avd_create(const avd_config* cfg, avd_ctx** out) {
   BIND(blk_cnt, int64_t*); BIND(agg, double*); BIND(agg_part, double*); BIND(report, double*); BIND(hist0, unsigned long long*); BIND(cand_x, long long*); BIND(gemm_part, void*);
   BIND(P_hl, float*); BIND(Vt_hl, float*); BIND(V_hl, float*); BIND(mu_hl, float*);
   BIND(G32, float*); BIND(qsum, long long*); BIND(Q32, float*); BIND(Z32, float*); BIND(ticket, unsigned*); BIND(gmax, double*);
+  BIND(samp, double*); BIND(smax, float*); BIND(smin, float*); BIND(qscale, float*); BIND(qoff, float*);
+  BIND(qsum_part, long long*); BIND(qsum_local, long long*); BIND(qerr_part, float*); BIND(qerr_local, double*);
+  BIND(qerr, double*); BIND(mu0, float*); BIND(qsq_part, long long*);
 #undef BIND
   if (cudaMallocHost(&c->eig_host, sizeof(double) * 4 * kMaxP) != cudaSuccess) {
     cudaGetLastError();
@@ -327,7 +345,12 @@ avd_status avd_buffer(avd_ctx* c, int32_t which, void** ptr, size_t* bytes) {
   if (!c || !ptr || !bytes) return AVD_EINVAL;
   const int64_t m = c->cfg.m;
   switch (which) {
-    case AVD_BUF_STATS: *ptr = c->stats; *bytes = sizeof(double) * (m + 3); break;
+    case AVD_BUF_STATS: *ptr = c->stats; *bytes = sizeof(double) * (m + 4); break;
+    case AVD_BUF_SAMPLE: *ptr = c->samp; *bytes = sizeof(double) * (m + 1); break;
+    case AVD_BUF_SMAX: *ptr = c->smax; *bytes = sizeof(float) * m; break;
+    case AVD_BUF_SMIN: *ptr = c->smin; *bytes = sizeof(float) * m; break;
+    case AVD_BUF_QSUM: *ptr = c->qsum; *bytes = sizeof(long long) * 2 * m; break;
+    case AVD_BUF_QERR: *ptr = c->qerr; *bytes = sizeof(double) * m; break;
     case AVD_BUF_HIST0: *ptr = c->hist0; *bytes = sizeof(long long) * kHistBins; break;
     case AVD_BUF_CAND: *ptr = c->cand_x; *bytes = sizeof(long long) * 2; break;
     case AVD_BUF_COLMAX: *ptr = c->colmax; *bytes = sizeof(float) * m; break;
@@ -362,28 +385,36 @@ avd_status avd_buffer(avd_ctx* c, int32_t which, void** ptr, size_t* bytes) {
 avd_status avd_stage_stats(avd_ctx* c, const float* X) {
   if (!c || !X) { set_error("null argument"); return AVD_EINVAL; }
   c->stage = 0;  // a new pass may start at any time
-  AVD_TRY(launch_stats(c, X));
+  AVD_TRY(launch_sample(c, X));
   c->stage = 1;
   return AVD_OK;
 }
 
 avd_status avd_stage_split(avd_ctx* c, const float* X) {
   STAGE_CHECK(c, 1);
-  AVD_TRY(launch_prepare(c));
-  AVD_CUDA(cudaMemcpyAsync(&c->hplan, c->dplan, sizeof(DevPlan), cudaMemcpyDeviceToHost, c->stream));
-  AVD_CUDA(cudaStreamSynchronize(c->stream));
-  if (c->hplan.nonfinite > 0) {
-    set_error(std::to_string(c->hplan.nonfinite) + " non-finite entries in X");
-    c->stage = 0;
-    return AVD_ENONFINITE;
-  }
-  AVD_TRY(launch_split(c, X));
+  if (!X) { set_error("null argument"); return AVD_EINVAL; }
+  AVD_TRY(launch_pass1(c, X, true));
   c->stage = 2;
   return AVD_OK;
 }
 
-avd_status avd_stage_gram(avd_ctx* c) {
+avd_status avd_stage_gram(avd_ctx* c, const float* X) {
   STAGE_CHECK(c, 2);
+  if (!X) { set_error("null argument"); return AVD_EINVAL; }
+  AVD_TRY(launch_finish(c));
+  double ovf = 0.0;
+  AVD_CUDA(cudaMemcpyAsync(&c->hplan, c->dplan, sizeof(DevPlan), cudaMemcpyDeviceToHost, c->stream));
+  AVD_CUDA(cudaMemcpyAsync(&ovf, c->stats + c->cfg.m + 3, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  AVD_CUDA(cudaStreamSynchronize(c->stream));
+  if (c->hplan.nonfinite > 0) {
+    set_error("X has non-finite entries (" + std::to_string(c->hplan.nonfinite) + " non-finite column sums)");
+    c->stage = 0;
+    return AVD_ENONFINITE;
+  }
+  c->requantised = ovf > 0.0 || (c->cfg.flags & AVD_FLAG_EXACT_SCALE);
+  if (c->requantised) AVD_TRY(launch_pass1(c, X, false));  // exact column ranges (k_pass1.cu)
+  AVD_CUDA(cudaMemcpyAsync(c->qsum, c->qsum_local, sizeof(long long) * 2 * c->cfg.m, cudaMemcpyDeviceToDevice, c->stream));
+  AVD_CUDA(cudaMemcpyAsync(c->qerr, c->qerr_local, sizeof(double) * c->m_pad, cudaMemcpyDeviceToDevice, c->stream));
   AVD_TRY(launch_gram(c));
   c->stage = 3;
   return AVD_OK;
@@ -484,6 +515,7 @@ avd_status avd_stage_report(avd_ctx* c, avd_outputs* out) {
   out->max_resid = c->max_resid;
   out->rr_checks = c->rr_count;
   out->jacobi_sweeps = c->jacobi_sweeps;
+  out->requantised = c->requantised ? 1 : 0;
   out->n_top_local = c->hplan.sel_local;
   out->top_offset = c->hplan.top_offset;
   out->n_top_global = c->hplan.n_eff;
@@ -497,7 +529,7 @@ avd_status avd_decompose(avd_ctx* c, const float* X, avd_outputs* out) {
   if ((reinterpret_cast<uintptr_t>(X) & 15) != 0) { set_error("X must be 16-byte aligned"); return AVD_EINVAL; }
   AVD_TRY(avd_stage_stats(c, X));
   AVD_TRY(avd_stage_split(c, X));
-  AVD_TRY(avd_stage_gram(c));
+  AVD_TRY(avd_stage_gram(c, X));
   const avd_status eig = avd_stage_eig(c);
   if (eig != AVD_OK && eig != AVD_ENOCONV) return eig;
   AVD_TRY(avd_stage_project(c, X));

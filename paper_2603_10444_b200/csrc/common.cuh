@@ -52,9 +52,21 @@ struct Ctx {
   float* colmax_part = nullptr;   // [r1][m]
   float* colmin_part = nullptr;   // [r1][m]
   double* sq_part = nullptr;      // [r1 * ncb]
-  double* stats = nullptr;        // [m + 3]: colsum[m], sum x^2, #nonfinite, #nonzero (exchange)
+  double* stats = nullptr;        // [m + 4]: colsum[m], sum x^2, (unused), #nonzero, #overflowing columns (exchange)
+  double* samp = nullptr;         // [m + 1]: row-sample column sums, #sampled rows (exchange SUM)
+  float* smax = nullptr;          // [m] row-sample column max (exchange MAX)
+  float* smin = nullptr;          // [m] row-sample column min (exchange MIN)
+  float* qscale = nullptr;        // [m_pad] 2^shift (fp32)
+  float* mu0 = nullptr;           // [m_pad] quantiser centre (fl32 of the sample mean)
+  float* qoff = nullptr;          // [m_pad] -mu0 * 2^shift (fp32)
+  long long* qsum_part = nullptr; // [r1][m] per-chunk integer column sums of q
+  long long* qsum_local = nullptr;// [2 m]: this rank's column sums of q | sums of q^2
+  long long* qsq_part = nullptr;  // [r1][m] per-chunk sums of q^2
+  float* qerr_part = nullptr;     // [r1][m] per-chunk sums of the squared rounding errors
+  double* qerr_local = nullptr;   // [m_pad] this rank's sums of squared rounding errors
+  double* qerr = nullptr;         // [m_pad] (exchange SUM)
   unsigned long long* hist0 = nullptr;  // [4096] exact first-level histogram over candidates (exchange)
-  float* colmax = nullptr;        // [m] (exchange MAX)
+  float* colmax = nullptr;        // [m] max |x - mu0| (exchange MAX)
   float* colmin = nullptr;        // [m] (exchange MIN)
   unsigned long long* hist1 = nullptr;  // [4096] (exchange SUM)
   // prepare
@@ -71,11 +83,12 @@ struct Ctx {
   int64_t cand_cap = 0;
   long long* cand_x = nullptr;    // [2] exchange SUM: candidate count, overflow flag
   bool cand_overflow = false;     // true -> K6 streams X instead of the candidate list
+  bool requantised = false;       // the sampled digit scales overflowed: requantised with exact ranges
   // K3
   long long* gram_i = nullptr;    // [m_pad * m_pad] int64 (upper tiles) (exchange SUM)
   double* G = nullptr;            // [m_pad][m_pad] fp64 symmetric (zero beyond m)
   float* G32 = nullptr;           // [m_pad][m_pad] fp32 copy (power steps of K4)
-  long long* qsum = nullptr;      // [m_pad] column sums of the quantised operand (exchange SUM)
+  long long* qsum = nullptr;      // [2 m] column sums of the quantised operand | of its squares (exchange SUM)
   CUtensorMap tmap_digits{};
   int gram_split = 1;
   // K4
@@ -160,10 +173,9 @@ __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + 
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
 // ---------------------------------------------------------------- kernels (per file)
-avd_status launch_stats(Ctx* c, const float* X);           // k_stats.cu
-avd_status launch_stats_reduce(Ctx* c);                    // k_stats.cu
-avd_status launch_prepare(Ctx* c);                         // k_stats.cu
-avd_status launch_split(Ctx* c, const float* X);           // k_split.cu
+avd_status launch_sample(Ctx* c, const float* X);          // k_pass1.cu
+avd_status launch_pass1(Ctx* c, const float* X, bool full); // k_pass1.cu
+avd_status launch_finish(Ctx* c);                          // k_pass1.cu
 avd_status launch_gram(Ctx* c);                            // k_gram.cu
 avd_status gram_make_tmap(Ctx* c);                         // k_gram.cu
 avd_status launch_gram_finalize(Ctx* c);                   // k_eig.cu

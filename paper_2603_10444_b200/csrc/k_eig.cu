@@ -36,7 +36,8 @@ namespace {
 // Both with leading dimension m_pad; rows/columns >= m are zero.
 __global__ void gram_finalize_kernel(const long long* __restrict__ Gi, int64_t m, int64_t m_pad,
                                      const int32_t* __restrict__ shift, const long long* __restrict__ qsum,
-                                     double inv_l, double unit, double* __restrict__ G, float* __restrict__ G32) {
+                                     const double* __restrict__ qerr, double inv_l, double unit,
+                                     double* __restrict__ G, float* __restrict__ G32) {
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t a = blockIdx.y;
   if (b >= m_pad) return;
@@ -47,8 +48,12 @@ __global__ void gram_finalize_kernel(const long long* __restrict__ Gi, int64_t m
     const long long v = upper ? Gi[b * m_pad + a] : Gi[a * m_pad + b];
     // exact centring of the quantised matrix: sum_i (q_ia - qbar_a)(q_ib - qbar_b)
     //   = sum_i q_ia q_ib - S_a S_b / l   (S = column sums of q, exact integers)
-    const double corr = qsum ? ((double)qsum[a] * (double)qsum[b]) * inv_l : 0.0;
-    g = ldexp(((double)v - corr) * unit, -(shift[a] + shift[b]));
+    // v unit = sum_i q_ia q_ib; the diagonal is the exact sum_i q_ia^2 of the fused pass
+    // (qsum[m + a]; with 3 digits the Gram drops the two lowest digit-product classes, whose
+    // diagonal part is a positive bias) minus the realised squared rounding errors (unbiased)
+    const double qq = (a == b) ? (double)qsum[m + a] - qerr[a] : (double)v * unit;
+    const double corr = ((double)qsum[a] * (double)qsum[b]) * inv_l;
+    g = ldexp(qq - corr, -(shift[a] + shift[b]));
   }
   G[a * m_pad + b] = g;
   G32[a * m_pad + b] = (float)g;
@@ -762,7 +767,7 @@ avd_status launch_gram_finalize(Ctx* c) {
   const int64_t m = c->cfg.m;
   const double unit = (c->nd == 3) ? 16384.0 : 1.0;
   dim3 grid((unsigned)ceil_div(c->m_pad, 256), (unsigned)c->m_pad);
-  gram_finalize_kernel<<<grid, 256, 0, c->stream>>>(c->gram_i, m, c->m_pad, c->shift, c->qsum,
+  gram_finalize_kernel<<<grid, 256, 0, c->stream>>>(c->gram_i, m, c->m_pad, c->shift, c->qsum, c->qerr,
                                                     1.0 / (double)c->cfg.l_global, unit, c->G, c->G32);
   AVD_LAUNCHED(c);
   trace_kernel<<<1, 256, 0, c->stream>>>(c->G, m, c->m_pad, c->trace, c->gmax);

@@ -2,8 +2,9 @@
 // eigenvectors, sigma^2 its eigenvalues: the truncated SVD of PAPER.md:11-14) as a dense
 // contraction on the 5th-generation tensor cores.
 //
-// Operands: the nd int8 digit planes D_d[j][i] written by K2 (K-major, row j = column j of Xc),
-// q_ij = sum_d 128^(nd-1-d) D_d[j][i].  The Gram of the fixed-point matrix is accumulated
+// Operands: the nd int8 digit planes D_d[i][j] written by the fused pass (k_pass1.cu), row-major
+// like X (MN-major UMMA operands: a 128-row x 128-column TMA box is 128 K-rows of 128 bytes),
+// q_ij = sum_d 128^(nd-1-d) D_d[i][j].  The Gram of the fixed-point matrix is accumulated
 // EXACTLY:  sum_i q_ia q_ib = sum_{d,e} 128^(2nd-2-d-e) sum_i D_d[a][i] D_e[b][i]
 //   nd = 2: all four digit products, classes 2^14 / 2^7 / 2^0           (exact)
 //   nd = 3: classes 2^28 / 2^21 / 2^14 (6 products; classes <= 2^7 dropped, rel. <= 2^-21)
@@ -33,9 +34,10 @@ using namespace sm100;
 constexpr int kGramThreads = 320;
 constexpr uint32_t kBox = 128 * 128;  // bytes of one TMA box (128 rows x 128 int8)
 
-// kind::i8 instruction descriptor: c_format S32 (2), a/b format signed int8 (1), K-major.
+// kind::i8 instruction descriptor: c_format S32 (2), a/b format signed int8 (1), A and B
+// MN-major (bits 15, 16; validated bit-exactly by tools/umma_i8_mn_probe.cu).
 __host__ __device__ constexpr uint32_t idesc_i8(uint32_t M, uint32_t N) {
-  return (2u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
+  return (2u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
 __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -62,7 +64,7 @@ __device__ __forceinline__ void unit_coords(int64_t u, int n_tiles, int T, int S
 
 template <int ND, int NS>
 __global__ void __launch_bounds__(kGramThreads, 1) gram_kernel(const __grid_constant__ CUtensorMap tmap,
-                                                               int64_t m_pad, int64_t NK, int T, int S,
+                                                               int64_t m_pad, int64_t l_pad, int64_t NK, int T, int S,
                                                                long long* __restrict__ G) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -104,12 +106,12 @@ __global__ void __launch_bounds__(kGramThreads, 1) gram_kernel(const __grid_cons
           mbar_arrive_expect_tx(&full_bar[s], diag ? ND * kBox : 2 * ND * kBox);
 #pragma unroll
           for (int d = 0; d < ND; ++d)
-            tma_load_2d(st + d * kBox, &tmap, &full_bar[s], (int32_t)(ks * 128), (int32_t)(d * m_pad + ta * 128));
+            tma_load_2d(st + d * kBox, &tmap, &full_bar[s], (int32_t)(ta * 128), (int32_t)(d * l_pad + ks * 128));
           if (!diag) {
 #pragma unroll
             for (int d = 0; d < ND; ++d)
-              tma_load_2d(st + (ND + d) * kBox, &tmap, &full_bar[s], (int32_t)(ks * 128),
-                          (int32_t)(d * m_pad + tb * 128));
+              tma_load_2d(st + (ND + d) * kBox, &tmap, &full_bar[s], (int32_t)(tb * 128),
+                          (int32_t)(d * l_pad + ks * 128));
           }
         }
       }
@@ -137,8 +139,10 @@ __global__ void __launch_bounds__(kGramThreads, 1) gram_kernel(const __grid_cons
             uint64_t a[ND], b[ND];
 #pragma unroll
             for (int d = 0; d < ND; ++d) {
-              a[d] = smem_desc(abase + d * kBox + kk * 32, 16, 1024, 2);
-              b[d] = smem_desc(bbase + d * kBox + kk * 32, 16, 1024, 2);
+              // MN-major SW128: K rows of 128 B; the K = 32 slice kk starts 32 rows (4 KB) in,
+              // SBO = 1 KB between 8-row groups (LBO unused: M = N = 128 int8 is one 128-B chunk)
+              a[d] = smem_desc(abase + d * kBox + kk * 4096, 16384, 1024, 2);
+              b[d] = smem_desc(bbase + d * kBox + kk * 4096, 16384, 1024, 2);
             }
             const uint32_t acc = (ks > ks0 || kk > 0) ? 1u : 0u;
             if (ND == 2) {
@@ -213,10 +217,11 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 int choose_split(int n_tiles, int64_t NK, int sms) {
-  // balance waves over the SMs; every unit <= 1024 stages (131072 rows: int32-exact bound)
+  // balance waves over the SMs; every unit <= 512 stages (65536 rows): the largest class sum
+  // per row is <= 2*127*64 + 64^2 = 20352 (nd = 3), so the int32 TMEM sums stay exact
   int best = 1;
   double best_eff = -1.0;
-  const int smin = (int)ceil_div(NK, 1024);
+  const int smin = (int)ceil_div(NK, 512);
   for (int S = std::max(1, smin); S <= std::max(smin, 16) && S <= NK; ++S) {
     const int64_t units = (int64_t)n_tiles * S;
     const double waves = (double)ceil_div(units, sms);
@@ -233,8 +238,8 @@ PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() { return get_encode(); }
 avd_status gram_make_tmap(Ctx* c) {
   auto enc = get_encode();
   if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return AVD_ECUDA; }
-  uint64_t dims[2] = {(uint64_t)c->l_pad, (uint64_t)(c->nd * c->m_pad)};
-  uint64_t strides[1] = {(uint64_t)c->l_pad};
+  uint64_t dims[2] = {(uint64_t)c->m_pad, (uint64_t)(c->nd * c->l_pad)};
+  uint64_t strides[1] = {(uint64_t)c->m_pad};
   uint32_t box[2] = {128, 128};
   uint32_t es[2] = {1, 1};
   CUresult r = enc(&c->tmap_digits, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, c->digits, dims, strides, box, es,
@@ -245,7 +250,7 @@ avd_status gram_make_tmap(Ctx* c) {
   c->gram_split = choose_split(T * (T + 1) / 2, c->l_pad / 128, c->num_sms);
   if (const char* e = getenv("AVD_GRAM_SPLIT")) {
     const int v = atoi(e);
-    if (v >= (int)ceil_div(c->l_pad / 128, 1024) && v <= c->l_pad / 128) c->gram_split = v;
+    if (v >= (int)ceil_div(c->l_pad / 128, 512) && v <= c->l_pad / 128) c->gram_split = v;
   }
   return AVD_OK;
 }
@@ -262,12 +267,12 @@ avd_status launch_gram(Ctx* c) {
     constexpr int NS = 3;
     const size_t smem = (size_t)NS * 2 * 2 * kBox + 1024;
     AVD_CUDA(cudaFuncSetAttribute(gram_kernel<2, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    gram_kernel<2, NS><<<grid, kGramThreads, smem, c->stream>>>(c->tmap_digits, c->m_pad, NK, T, S, c->gram_i);
+    gram_kernel<2, NS><<<grid, kGramThreads, smem, c->stream>>>(c->tmap_digits, c->m_pad, c->l_pad, NK, T, S, c->gram_i);
   } else {
     constexpr int NS = 2;
     const size_t smem = (size_t)NS * 2 * 3 * kBox + 1024;
     AVD_CUDA(cudaFuncSetAttribute(gram_kernel<3, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    gram_kernel<3, NS><<<grid, kGramThreads, smem, c->stream>>>(c->tmap_digits, c->m_pad, NK, T, S, c->gram_i);
+    gram_kernel<3, NS><<<grid, kGramThreads, smem, c->stream>>>(c->tmap_digits, c->m_pad, c->l_pad, NK, T, S, c->gram_i);
   }
   AVD_LAUNCHED(c);
   return AVD_OK;

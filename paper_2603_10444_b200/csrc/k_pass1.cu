@@ -1,0 +1,583 @@
+// k_pass1.cu — K1+K2: the single HBM-streaming pass over X that feeds the rest of the path.
+//
+// One read of X (4 B/entry) produces, fused:
+//   * fp64 column sums (mu = (1/l) X^T 1), sum x^2 (||X||_F^2), column
+//     max/min, the exact count of nonzero entries (|E_top| = min(n_top, #nonzero), R4)
+//     and a non-finite check;
+//   * the Gram operand: every entry centred on a PROVISIONAL column centre mu0 (from a row
+//     sample) and scaled by the column's power of two 2^shift_j, rounded with a deterministic
+//     dither d (uniform on a 2^-9 grid in (-1/2, 1/2)):  q = rint((x - mu0_j) 2^shift_j + d) — nd balanced
+//     base-128 int8 digits into ROW-MAJOR planes D_d[i][j] (MN-major operands of the tcgen05
+//     kind::i8 Gram, k_gram.cu); and the exact integer column sums S_j = sum_i q_ij;
+//   * the top-set candidates: entries whose |x| bit pattern falls in a first-level bin >= b0 are
+//     appended as (key, global linear index).
+// The Gram of the quantised matrix is then centred EXACTLY (k_eig.cu gram_finalize):
+//   sum_i (q_ia - S_a/l)(q_ib - S_b/l) = sum_i q_ia q_ib - S_a S_b / l,
+// its diagonal is taken from the exact sum_i q_ia^2 accumulated here (with 3 digits the Gram drops
+// the two lowest digit-product classes, whose diagonal part is a positive bias), and debiased by
+// the realised squared rounding errors E_a = sum_i (q_ia - y_ia)^2
+// (the dithered errors are zero-mean and independent across columns, so only the diagonal
+// carries a bias; with it removed the Gram is unbiased even for columns whose range is set by
+// a massive activation),
+// so X~ = X - 1 mu^T never needs the exact mu before the pass.
+//
+// mu0, shift and b0 come from a 1/s row sample (sample_kernel, s = 16 at large l): shift maps
+// the sampled max |x - mu0| below 2^(7nd-1); the digit range admits twice that.  An entry
+// outside the range is counted (stats[m+3]); if any rank saw one, the quantisation is redone
+// with the exact column ranges (requant path, same kernel without the statistics).
+#include <cfloat>
+#include "common.cuh"
+
+namespace avd {
+
+namespace {
+
+constexpr int kT = 256;  // threads of the streaming kernels
+
+__device__ __forceinline__ uint32_t mix32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7FEB352Du;
+  x ^= x >> 15;
+  x *= 0x846CA68Bu;
+  x ^= x >> 16;
+  return x;
+}
+
+__device__ __forceinline__ void hist_add(unsigned int* sh, uint32_t key, bool valid) {
+  // warp-aggregated shared-memory histogram update (one atomic per distinct bin per warp)
+  const uint32_t bin = valid ? (key >> 19) : 0xFFFFFFFFu;
+  const uint32_t peers = __match_any_sync(0xFFFFFFFFu, bin);
+  const int leader = __ffs(peers) - 1;
+  if (valid && (int)(threadIdx.x & 31) == leader) atomicAdd(&sh[bin], (unsigned)__popc(peers));
+}
+
+// ---------------------------------------------------------------- row sample
+// Rows with global index gi % s == 0: column sums (fp64), max, min, and the 4096-bin histogram
+// of |x| bits [30:19] that seeds the candidate threshold b0.
+constexpr int kHistSub = 4;  // histogram on 1 of kHistSub sampled rows
+template <int VEC>
+__global__ void __launch_bounds__(kT) sample_kernel(const float* __restrict__ X, int64_t l, int64_t m, int64_t i0,
+                                                   int s, int64_t row_offset, int64_t n_rows, int64_t rpc,
+                                                   double* __restrict__ colsum_part,
+                                                   float* __restrict__ colmax_part, float* __restrict__ colmin_part,
+                                                   unsigned long long* __restrict__ hist1) {
+  __shared__ unsigned int sh[kHistBins];
+  for (int b = threadIdx.x; b < kHistBins; b += kT) sh[b] = 0;
+  __syncthreads();
+  const int64_t c0 = ((int64_t)blockIdx.x * kT + threadIdx.x) * VEC;
+  const int64_t j0 = (int64_t)blockIdx.y * rpc, j1 = min(n_rows, j0 + rpc);
+  const bool active = c0 < m;
+  double cs[VEC];
+  float mx[VEC], mn[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) { cs[v] = 0.0; mx[v] = -FLT_MAX; mn[v] = FLT_MAX; }
+  for (int64_t jr = j0; jr < j1; ++jr) {
+    const int64_t i = i0 + jr * s;
+    float x[VEC];
+    if constexpr (VEC == 4) {
+      const float4 t = active ? __ldg(reinterpret_cast<const float4*>(X + i * m + c0)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      x[0] = t.x; x[1] = t.y; x[2] = t.z; x[3] = t.w;
+    } else {
+      x[0] = active ? __ldg(X + i * m + c0) : 0.f;
+    }
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      const uint32_t key = __float_as_uint(x[v]) & 0x7FFFFFFFu;
+      const bool fin = key < 0x7F800000u;
+      if (active && fin) {
+        cs[v] += (double)x[v];
+        mx[v] = fmaxf(mx[v], x[v]);
+        mn[v] = fminf(mn[v], x[v]);
+      }
+    }
+    // the |x| histogram only needs every kHistSub-th sampled row (enough for a top-0.1% bin)
+    if ((((uint64_t)(i0 + jr * s) + row_offset) / s) % kHistSub == 0) {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        const uint32_t key = __float_as_uint(x[v]) & 0x7FFFFFFFu;
+        hist_add(sh, key, active && key < 0x7F800000u && key != 0);
+      }
+    }
+  }
+  if (active)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      colsum_part[(int64_t)blockIdx.y * m + c0 + v] = cs[v];
+      colmax_part[(int64_t)blockIdx.y * m + c0 + v] = mx[v];
+      colmin_part[(int64_t)blockIdx.y * m + c0 + v] = mn[v];
+    }
+  __syncthreads();
+  for (int b = threadIdx.x; b < kHistBins; b += kT)
+    if (sh[b]) atomicAdd(&hist1[b], (unsigned long long)sh[b]);
+}
+
+// fixed-order reduction of the sample partials -> samp[0..m) column sums, samp[m] = #rows
+__global__ void sample_reduce_kernel(int64_t m, int r1, double n_rows, const double* __restrict__ colsum_part,
+                                     const float* __restrict__ colmax_part, const float* __restrict__ colmin_part,
+                                     double* __restrict__ samp, float* __restrict__ smax, float* __restrict__ smin) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < m) {
+    double s = 0.0;
+    float mx = -FLT_MAX, mn = FLT_MAX;
+    for (int r = 0; r < r1; ++r) {
+      s += colsum_part[(int64_t)r * m + j];
+      mx = fmaxf(mx, colmax_part[(int64_t)r * m + j]);
+      mn = fminf(mn, colmin_part[(int64_t)r * m + j]);
+    }
+    samp[j] = s;
+    smax[j] = mx;
+    smin[j] = mn;
+  }
+  if (j == 0) samp[m] = n_rows;
+}
+
+// Quantiser parameters from column centres and ranges:
+//   mu0_j = fl32(centre), shift_j = (7 nd - 1) - (ilogb(a_j) + 1), a_j = max|x - mu0_j| over the
+//   range given, so the range maps below 2^(7nd-1) and the digit range (2^(7nd) - 2^7) admits a
+//   factor 2 beyond it;  qscale = 2^shift (fp32, exact), qoff = -mu0 * 2^shift (exact).
+// exact == 0: centre = sample mean, range = sample max/min; also picks b0 from the sampled
+// histogram: the largest bin whose scaled tail count covers 2 n_top + 256 s (conservative; K6
+// verifies with exact counts and falls back to streaming X when it does not cover |E_top|).
+// exact == 1: the same centre, range = the exact max |x - mu0| of the fused pass (requant path).
+__global__ void prepare_kernel(int64_t m, int64_t m_pad, int nd, int exact, int64_t n_top, int s,
+                               const double* __restrict__ centre_sum, float* __restrict__ mu0,
+                               const float* __restrict__ cmax, const float* __restrict__ cmin,
+                               const unsigned long long* __restrict__ hist1, int32_t* __restrict__ shift,
+                               float* __restrict__ qscale, float* __restrict__ qoff, DevPlan* __restrict__ dp) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < m_pad) {
+    int32_t sh = 0;
+    float sc = 0.f, off = 0.f;
+    if (j < m) {
+      // sample: centre = fl32(sample mean), a = sampled max |x - centre|; exact (requant): the
+      // same centre (kept in mu0) and a = the exact max |x - mu0| measured by the fused pass
+      const float c0 = exact ? mu0[j] : (centre_sum[m] > 0.0 ? (float)(centre_sum[j] / centre_sum[m]) : 0.f);
+      const double a = exact ? (double)cmax[j] : fmax((double)cmax[j] - (double)c0, (double)c0 - (double)cmin[j]);
+      if (!exact) mu0[j] = c0;
+      if (a > 0.0 && a < 1e300) sh = (7 * nd - 1) - (ilogb(a) + 1);
+      else if (!exact) sh = 100;  // no sampled range: any deviation overflows -> exact requant
+      sh = max(-100, min(100, sh));
+      sc = __int_as_float((sh + 127) << 23);
+      off = -c0 * sc;
+    }
+    shift[j] = sh;
+    qscale[j] = sc;
+    qoff[j] = off;
+  }
+  if (exact || blockIdx.x != 0 || threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  const unsigned long long sh = (unsigned long long)s * kHistSub;  // rows per histogrammed row
+  const unsigned long long need = 2ull * (unsigned long long)n_top + 256ull * sh;
+  constexpr int per = kHistBins / 32;
+  const int hi = kHistBins - 1 - lane * per;  // lane covers bins (hi-per, hi]
+  unsigned long long mine = 0;
+  for (int b = hi; b > hi - per; --b) mine += hist1[b] * sh;
+  unsigned long long incl = mine;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const unsigned long long excl = incl - mine;
+  int b0 = -1;
+  if (excl < need && incl >= need) {
+    unsigned long long cum = excl;
+    int b = hi;
+    for (; b > hi - per; --b) {
+      cum += hist1[b] * sh;
+      if (cum >= need) break;
+    }
+    b0 = b;
+  }
+  // lowest lane holding a crossing wins; none -> every nonzero entry is a candidate (b0 = 0)
+  for (int o = 16; o > 0; o >>= 1) b0 = max(b0, __shfl_xor_sync(0xFFFFFFFFu, b0, o));
+  if (lane == 0) {
+    dp->b0 = b0 < 0 ? 0 : b0;
+    dp->b1 = 0;
+    dp->b2 = 0;
+    dp->cnt_gt = 0;
+    dp->cand_count = 0;
+  }
+}
+
+// pack the low bytes of four ints into one word (byte v <- value v)
+__device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
+  return __byte_perm(__byte_perm((uint32_t)a, (uint32_t)b, 0x0040), __byte_perm((uint32_t)c, (uint32_t)d, 0x0040), 0x5410);
+}
+
+// ---------------------------------------------------------------- the fused pass
+// FULL: statistics + candidates + digits; !FULL: digits + S + E only (requant path).
+// Thread: VEC consecutive columns, rows [r0, r1) of its chunk, U rows in flight.  Per entry the
+// hot loop does the dithered rounding, the digit split and packing, the exact integer / error
+// sums, |y| max (the digit-range check and the exact range for a requant), x and x^2 sums, the
+// nonzero count and a candidate flag whose warp-aggregated append runs only when some lane of
+// the warp has one (the top-0.1% candidates are rare).
+template <int ND, int VEC, bool FULL>
+__global__ void __launch_bounds__(kT, 3) pass1_kernel(
+    const float* __restrict__ X, int64_t l, int64_t m, int64_t m_pad, int64_t l_pad, int64_t rpc, int64_t row_offset,
+    const float* __restrict__ qscale, const float* __restrict__ qoff, uint32_t seed32, int8_t* __restrict__ digits,
+    const DevPlan* __restrict__ dp, uint32_t* __restrict__ cand_key, uint64_t* __restrict__ cand_idx,
+    unsigned long long* __restrict__ cand_cnt, int64_t cand_cap, double* __restrict__ colsum_part,
+    float* __restrict__ ymax_part, double* __restrict__ sq_part, long long* __restrict__ qsum_part,
+    long long* __restrict__ qsq_part, float* __restrict__ qerr_part, double* __restrict__ stats) {
+  using QAcc = typename std::conditional<ND == 2, int, long long>::type;
+  constexpr int U = 4;
+  constexpr int DB = ND == 2 ? 9 : 2;           // dither grid bits (see below)
+  __shared__ double sred[kT / 32];
+  __shared__ unsigned long long snz;
+  if (threadIdx.x == 0) snz = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t c0 = ((int64_t)blockIdx.x * kT + threadIdx.x) * VEC;
+  const int64_t r0 = (int64_t)blockIdx.y * rpc;
+  const int64_t r1 = min(l, r0 + rpc);
+  const bool active = c0 < m;
+  const bool writer = c0 < m_pad;
+  float sc[VEC], off[VEC];
+  uint32_t colh[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    sc[v] = active ? qscale[c0 + v] : 0.f;
+    off[v] = active ? qoff[c0 + v] : 0.f;
+    colh[v] = mix32((uint32_t)(c0 + v) ^ 0x68E31DA4u);
+  }
+  // candidate test as one unsigned compare: key in [max(1, b0 << 19), 0x7F800000)
+  const uint32_t klo = FULL ? max(1u, (uint32_t)dp->b0 << 19) : 0u;
+  const uint32_t kspan = 0x7F800000u - klo;
+  double s[VEC];
+  QAcc qs[VEC];
+  long long qq[VEC];  // exact sum of q^2 (the Gram diagonal of the quantised operand)
+  float es[VEC], ym[VEC];  // sum of squared rounding errors (q - y)^2; max |y|
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) { s[v] = 0.0; qs[v] = 0; qq[v] = 0; es[v] = 0.f; ym[v] = 0.f; }
+  double sq = 0.0;
+  unsigned nz = 0;
+  for (int64_t i = r0; i < r1; i += U) {
+    float x[U][VEC];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool ok = active && (i + u < r1);
+      if constexpr (VEC == 4) {
+        const float4 t = ok ? __ldcs(reinterpret_cast<const float4*>(X + (i + u) * m + c0)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        x[u][0] = t.x; x[u][1] = t.y; x[u][2] = t.z; x[u][3] = t.w;
+      } else {
+        x[u][0] = ok ? __ldcs(X + (i + u) * m + c0) : 0.f;
+      }
+    }
+    uint32_t cmask = 0;  // candidate entries (u, v) of this iteration, bit u * VEC + v
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool ok = active && (i + u < r1);
+      const uint32_t srow = (uint32_t)(row_offset + i + u) * 0x9E3779B1u + seed32;
+      int dg[ND][VEC];
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        // dithered rounding: q = rint(y + d), y = (x - mu0) 2^shift, d uniform on the symmetric grid
+        // (k + 1/2) 2^-DB - 1/2, k < 2^DB: y + d is exact in fp32 for integer y (|y| < 2^(7nd)), so
+        // exactly representable data stays exact (tests/test_gpu_parity.py planted case)
+        const uint32_t h = (srow ^ colh[v]) * 0x85EBCA6Bu;
+        const float d = __uint_as_float(0x3F800000u | ((h >> (32 - DB)) << (23 - DB)) | (1u << (22 - DB))) - 1.5f;
+        const float y = ok ? fmaf(x[u][v], sc[v], off[v]) : 0.f;
+        const float t = (y + d) + 12582912.0f;  // 1.5 * 2^23: RN to an integer
+        int q = __float_as_int(t) - 0x4B400000;
+        const float e = (t - 12582912.0f) - y;  // exact: q and y share the fp32 grid
+        es[v] = fmaf(e, e, es[v]);
+        ym[v] = fmaxf(ym[v], fabsf(y));
+        qs[v] += (QAcc)q;
+        qq[v] += (long long)q * (long long)q;
+        // balanced base-128 digits, most significant first
+#pragma unroll
+        for (int dd = ND - 1; dd >= 1; --dd) {
+          const int hi = (q + 64) >> 7;
+          dg[dd][v] = q - (hi << 7);
+          q = hi;
+        }
+        dg[0][v] = q;
+        if (FULL) {
+          const uint32_t key = __float_as_uint(x[u][v]) & 0x7FFFFFFFu;
+          nz += (ok && key != 0u) ? 1u : 0u;
+          cmask |= (ok && (key - klo) < kspan) ? (1u << (u * VEC + v)) : 0u;
+        }
+      }
+      if (writer && i + u < r1) {
+#pragma unroll
+        for (int dd = 0; dd < ND; ++dd) {
+          int8_t* row = digits + ((int64_t)dd * l_pad + i + u) * m_pad + c0;
+          if constexpr (VEC == 4) {
+            __stcs(reinterpret_cast<unsigned int*>(row), pack4(dg[dd][0], dg[dd][1], dg[dd][2], dg[dd][3]));
+          } else {
+            *row = (int8_t)dg[dd][0];
+          }
+        }
+      }
+    }
+    if (FULL) {
+      // candidates: one warp-wide exclusive scan of the per-thread counts and one atomic per warp
+      if (__any_sync(0xFFFFFFFFu, cmask != 0u)) {
+        const uint32_t cnt = __popc(cmask);
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        unsigned long long base = 0;
+        if (lane == 31) base = atomicAdd(cand_cnt, (unsigned long long)total);
+        base = __shfl_sync(0xFFFFFFFFu, base, 31) + (incl - cnt);
+        if (cmask) {
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v)
+              if ((cmask >> (u * VEC + v)) & 1u) {
+                if (base < (unsigned long long)cand_cap) {
+                  cand_key[base] = __float_as_uint(x[u][v]) & 0x7FFFFFFFu;
+                  cand_idx[base] = (uint64_t)(row_offset + i + u) * (uint64_t)m + (uint64_t)(c0 + v);
+                }
+                ++base;
+              }
+        }
+      }
+      // fp64 accumulation of U-row fp32 partial sums (each partial rounds once, ~2^-24 relative)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        float ps = 0.f, pq = 0.f;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          ps += x[u][v];  // rows past r1 / inactive columns were loaded as 0
+          pq = fmaf(x[u][v], x[u][v], pq);
+        }
+        s[v] += (double)ps;
+        sq += (double)pq;
+      }
+    }
+  }
+  if (active) {
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      const int64_t o = (int64_t)blockIdx.y * m + c0 + v;
+      qsum_part[o] = (long long)qs[v];
+      qsq_part[o] = qq[v];
+      qerr_part[o] = es[v];
+      ymax_part[o] = ym[v];
+      if (FULL) colsum_part[o] = s[v];
+    }
+  }
+  if (FULL) {
+    for (int o = 16; o > 0; o >>= 1) {
+      sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o);
+      nz += __shfl_xor_sync(0xFFFFFFFFu, nz, o);
+    }
+    if (lane == 0) {
+      sred[threadIdx.x >> 5] = sq;
+      atomicAdd(&snz, (unsigned long long)nz);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < kT / 32; ++w) t += sred[w];
+      sq_part[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
+      if (snz) atomicAdd(&stats[m + 2], (double)snz);  // integer-valued double: exact, order-free
+    }
+  }
+}
+
+// Fixed-order reduction of the per-chunk partials -> stats[0..m) colsum, stats[m] sum x^2,
+// stats[m+3] = #columns whose digits overflowed, colmax[j] = max |x - mu0_j| (the exact range
+// about the quantiser centre, for a requant), qsum_local / qerr_local.
+template <int ND>
+__global__ void pass1_reduce_kernel(int64_t m, int r1, int nsq, int full, const double* __restrict__ colsum_part,
+                                    const float* __restrict__ ymax_part, const double* __restrict__ sq_part,
+                                    const long long* __restrict__ qsum_part, const long long* __restrict__ qsq_part,
+                                    const float* __restrict__ qerr_part,
+                                    const float* __restrict__ qscale, double* __restrict__ stats,
+                                    float* __restrict__ colmax, long long* __restrict__ qsum_local,
+                                    double* __restrict__ qerr_local) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < m) {
+    long long qs = 0, qq = 0;
+    double qe = 0.0;
+    float ym = 0.f;
+    for (int r = 0; r < r1; ++r) {
+      qs += qsum_part[(int64_t)r * m + j];
+      qq += qsq_part[(int64_t)r * m + j];
+      qe += (double)qerr_part[(int64_t)r * m + j];
+      ym = fmaxf(ym, ymax_part[(int64_t)r * m + j]);
+    }
+    qsum_local[j] = qs;
+    qsum_local[m + j] = qq;  // [S | sum q^2]
+    qerr_local[j] = qe;
+    if (full) {
+      double s = 0.0;
+      for (int r = 0; r < r1; ++r) s += colsum_part[(int64_t)r * m + j];
+      stats[j] = s;
+      // exact max |x - mu0_j| (power-of-two scale: exact), the range of a requant; |y| beyond
+      // the digit range (top digit outside [-127, 127]) counts as an overflow of column j
+      constexpr float kYLim = ND == 2 ? 16319.0f : 2088895.0f;
+      colmax[j] = ym / qscale[j];
+      if (!(ym <= kYLim)) atomicAdd(&stats[m + 3], 1.0);
+    }
+  }
+  if (full && blockIdx.x == 0) {
+    __shared__ double sh[256];
+    double t = 0.0;
+    for (int r = threadIdx.x; r < nsq; r += blockDim.x) t += sq_part[r];
+    sh[threadIdx.x] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double u = 0.0;
+      for (int q = 0; q < (int)blockDim.x; ++q) u += sh[q];
+      stats[m] = u;
+    }
+  }
+}
+
+// After the statistics exchange: mu (fp64) and its fp32 hi/lo pair for the projection pass,
+// |E_top| = min(n_top, #nonzero), the non-finite count.
+__global__ void finish_kernel(int64_t m, int64_t m_pad, int64_t l_global, int64_t n_top,
+                              const double* __restrict__ stats, double* __restrict__ mu, float* __restrict__ mu_hl,
+                              DevPlan* __restrict__ dp) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < m && !isfinite(stats[j])) atomicAdd(reinterpret_cast<unsigned long long*>(&dp->nonfinite), 1ull);
+  if (j < m_pad) {
+    float mh = 0.f, ml = 0.f;
+    if (j < m) {
+      const double mj = stats[j] / (double)l_global;
+      mu[j] = mj;
+      mh = (float)mj;
+      ml = (float)(mj - (double)mh);
+    }
+    mu_hl[j] = mh;
+    mu_hl[m_pad + j] = ml;
+  }
+  if (j == 0) {
+    const long long nonzero = (long long)stats[m + 2];
+    const long long n_eff = min((long long)n_top, nonzero);
+    dp->n_eff = n_eff;
+    dp->empty = n_eff == 0 ? 1 : 0;
+    if (!isfinite(stats[m])) atomicAdd(reinterpret_cast<unsigned long long*>(&dp->nonfinite), 1ull);
+  }
+}
+
+// exchange slot for the global candidate decision: [count, overflowed]
+__global__ void cand_publish_kernel(const unsigned long long* __restrict__ cnt, int64_t cap,
+                                    long long* __restrict__ out) {
+  out[0] = (long long)*cnt;
+  out[1] = (long long)(*cnt > (unsigned long long)cap ? 1 : 0);
+}
+
+bool vec4(const Ctx* c, const float* X) {
+  return (c->cfg.m % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
+}
+
+uint32_t dither_seed(const Ctx* c) {
+  return (uint32_t)(c->cfg.seed * 0x9E3779B97F4A7C15ull >> 32) ^ 0xA5A5A5A5u;
+}
+
+}  // namespace
+
+int stats_sample_step(int64_t l_global) {
+  const int64_t want = std::max<int64_t>(1, std::min<int64_t>(16, l_global / 4096));
+  int s = 1;
+  while (s * 2 <= want) s *= 2;  // power of two
+  return s;
+}
+
+// Stage 1: the row sample -> samp, smax, smin, hist1 (exchange buffers).
+avd_status launch_sample(Ctx* c, const float* X) {
+  const int64_t m = c->cfg.m, l = c->cfg.l_local;
+  const int s = stats_sample_step(c->cfg.l_global);
+  const int64_t i0 = (s - c->cfg.row_offset % s) % s;  // first local row with global index % s == 0
+  const int64_t n_rows = i0 < l ? ceil_div(l - i0, s) : 0;
+  const bool vec = vec4(c, X);
+  const int VEC = vec ? 4 : 1;
+  const int ncb = (int)ceil_div(m, (int64_t)kT * VEC);
+  const int r1 = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>((int64_t)c->r1, ceil_div(4LL * c->num_sms, ncb)), std::max<int64_t>(n_rows, 1)));
+  const int64_t rpc = ceil_div(std::max<int64_t>(n_rows, 1), r1);
+  AVD_CUDA(cudaMemsetAsync(c->hist1, 0, sizeof(unsigned long long) * kHistBins, c->stream));
+  dim3 grid(ncb, r1);
+  if (vec)
+    sample_kernel<4><<<grid, kT, 0, c->stream>>>(X, l, m, i0, s, c->cfg.row_offset, n_rows, rpc, c->colsum_part, c->colmax_part,
+                                                 c->colmin_part, c->hist1);
+  else
+    sample_kernel<1><<<grid, kT, 0, c->stream>>>(X, l, m, i0, s, c->cfg.row_offset, n_rows, rpc, c->colsum_part, c->colmax_part,
+                                                 c->colmin_part, c->hist1);
+  AVD_LAUNCHED(c);
+  sample_reduce_kernel<<<(unsigned)ceil_div(m, 256), 256, 0, c->stream>>>(m, r1, (double)n_rows, c->colsum_part,
+                                                                         c->colmax_part, c->colmin_part, c->samp,
+                                                                         c->smax, c->smin);
+  AVD_LAUNCHED(c);
+  return AVD_OK;
+}
+
+// Stage 2: quantiser parameters from the (exchanged) sample, then the fused pass.
+avd_status launch_pass1(Ctx* c, const float* X, bool full) {
+  const int64_t m = c->cfg.m, l = c->cfg.l_local;
+  const int s = stats_sample_step(c->cfg.l_global);
+  if (full) {
+    prepare_kernel<<<(unsigned)ceil_div(c->m_pad, 256), 256, 0, c->stream>>>(
+        m, c->m_pad, c->nd, 0, c->plan.n_top, s, c->samp, c->mu0, c->smax, c->smin, c->hist1, c->shift, c->qscale,
+        c->qoff, c->dplan);
+    AVD_LAUNCHED(c);
+  } else {
+    prepare_kernel<<<(unsigned)ceil_div(c->m_pad, 256), 256, 0, c->stream>>>(
+        m, c->m_pad, c->nd, 1, c->plan.n_top, s, c->stats, c->mu0, c->colmax, c->colmin, c->hist1,
+        c->shift, c->qscale, c->qoff, c->dplan);
+    AVD_LAUNCHED(c);
+  }
+  const bool vec = vec4(c, X);
+  const int VEC = vec ? 4 : 1;
+  const int ncb = (int)ceil_div(c->m_pad, (int64_t)kT * VEC);
+  const int64_t rpc = round_up(ceil_div(l, c->r1), 4);
+  const int r1 = (int)ceil_div(l, rpc);
+  if (full) {
+    AVD_CUDA(cudaMemsetAsync(c->stats, 0, sizeof(double) * (m + 4), c->stream));
+    AVD_CUDA(cudaMemsetAsync(c->cand_cnt, 0, sizeof(unsigned long long), c->stream));
+  }
+  // digit-plane rows [l_local, l_pad) are zero (the Gram sums over them)
+  if (c->l_pad > l)
+    for (int d = 0; d < c->nd; ++d)
+      AVD_CUDA(cudaMemsetAsync(c->digits + ((int64_t)d * c->l_pad + l) * c->m_pad, 0, (size_t)(c->l_pad - l) * c->m_pad,
+                               c->stream));
+  dim3 grid(ncb, r1);
+  const uint32_t seed32 = dither_seed(c);
+#define LAUNCH(ND, V, F)                                                                                        \
+  pass1_kernel<ND, V, F><<<grid, kT, 0, c->stream>>>(                                                           \
+      X, l, m, c->m_pad, c->l_pad, rpc, c->cfg.row_offset, c->qscale, c->qoff, seed32, c->digits, c->dplan,     \
+      c->cand_key, c->cand_idx, c->cand_cnt, c->cand_cap, c->colsum_part, c->colmax_part, c->sq_part,          \
+      c->qsum_part, c->qsq_part, c->qerr_part, c->stats)
+  if (c->nd == 2) {
+    if (full) { if (vec) LAUNCH(2, 4, true); else LAUNCH(2, 1, true); }
+    else { if (vec) LAUNCH(2, 4, false); else LAUNCH(2, 1, false); }
+  } else {
+    if (full) { if (vec) LAUNCH(3, 4, true); else LAUNCH(3, 1, true); }
+    else { if (vec) LAUNCH(3, 4, false); else LAUNCH(3, 1, false); }
+  }
+#undef LAUNCH
+  AVD_LAUNCHED(c);
+  if (c->nd == 2)
+    pass1_reduce_kernel<2><<<(unsigned)ceil_div(m, 256), 256, 0, c->stream>>>(
+        m, r1, r1 * ncb, full ? 1 : 0, c->colsum_part, c->colmax_part, c->sq_part, c->qsum_part, c->qsq_part,
+        c->qerr_part, c->qscale, c->stats, c->colmax, c->qsum_local, c->qerr_local);
+  else
+    pass1_reduce_kernel<3><<<(unsigned)ceil_div(m, 256), 256, 0, c->stream>>>(
+        m, r1, r1 * ncb, full ? 1 : 0, c->colsum_part, c->colmax_part, c->sq_part, c->qsum_part, c->qsq_part,
+        c->qerr_part, c->qscale, c->stats, c->colmax, c->qsum_local, c->qerr_local);
+  AVD_LAUNCHED(c);
+  if (full) {
+    cand_publish_kernel<<<1, 1, 0, c->stream>>>(c->cand_cnt, c->cand_cap, c->cand_x);
+    AVD_LAUNCHED(c);
+  }
+  return AVD_OK;
+}
+
+avd_status launch_finish(Ctx* c) {
+  AVD_CUDA(cudaMemsetAsync(&c->dplan->nonfinite, 0, sizeof(int64_t), c->stream));
+  finish_kernel<<<(unsigned)ceil_div(c->m_pad, 256), 256, 0, c->stream>>>(c->cfg.m, c->m_pad, c->cfg.l_global,
+                                                                         c->plan.n_top, c->stats, c->mu, c->mu_hl,
+                                                                         c->dplan);
+  AVD_LAUNCHED(c);
+  return AVD_OK;
+}
+
+}  // namespace avd

@@ -5,9 +5,11 @@ order == row order, which makes the tie quota of E_top a rank-ordered prefix).  
 step runs in libavd's kernels through the stage entry points of include/avd.h; between them this
 module all-reduces exactly the exchange buffers the header lists:
 
-  stats   : column sums + sum x^2 + non-finite count (SUM f64), column max (MAX), min (MIN),
-            |x| histogram level 1 (SUM i64)
-  gram    : the exact int64 Gram partials (SUM i64)  -> identical G on every rank
+  stats   : row-sample column sums + #rows (SUM f64), max (MAX), min (MIN), |x| histogram
+            level 1 (SUM i64)  -> identical quantiser centre / scale and candidate bin everywhere
+  split   : column sums + sum x^2 + counts (SUM f64), column range about the quantiser centre (MAX)
+  gram    : the exact int64 Gram partials and integer column sums of the quantised operand
+            (SUM i64)  -> identical exactly-centred G on every rank
   eig     : replicated (same G, same seed -> bit-identical V_k, sigma_k on every rank)
   project : elementwise energy sums + column sums of P (SUM f64)
   gram    : + candidate count / overflow flag (SUM i64) -> same candidate-vs-stream decision
@@ -27,9 +29,11 @@ from .api import Decomposer, Result
 
 # (stage, buffer name, dtype, reduce op) in call order
 EXCHANGES = {
-    "stats": [("STATS", torch.float64, "sum"), ("COLMAX", torch.float32, "max"),
-              ("COLMIN", torch.float32, "min"), ("HIST1", torch.int64, "sum")],
-    "gram": [("GRAM", torch.int64, "sum"), ("CAND", torch.int64, "sum")],
+    "stats": [("SAMPLE", torch.float64, "sum"), ("SMAX", torch.float32, "max"),
+              ("SMIN", torch.float32, "min"), ("HIST1", torch.int64, "sum")],
+    "split": [("STATS", torch.float64, "sum"), ("COLMAX", torch.float32, "max")],
+    "gram": [("GRAM", torch.int64, "sum"), ("CAND", torch.int64, "sum"), ("QSUM", torch.int64, "sum"),
+             ("QERR", torch.float64, "sum")],
     "project": [("ENERGY", torch.float64, "sum")],
     "select0": [("HIST0", torch.int64, "sum")],
     "select1": [("HIST2", torch.int64, "sum")],
@@ -73,7 +77,8 @@ def run_stages(backend, comm, X) -> object:
     backend.stage_stats(X)
     exchange("stats")
     backend.stage_split(X)
-    backend.stage_gram()
+    exchange("split")
+    backend.stage_gram(X)
     exchange("gram")
     backend.stage_eig()
     backend.stage_project(X)
@@ -106,8 +111,8 @@ class _LibBackend:
     def stage_split(self, X):
         L.avd_stage_split(self.h, X.data_ptr())
 
-    def stage_gram(self):
-        L.avd_stage_gram(self.h)
+    def stage_gram(self, X):
+        L.avd_stage_gram(self.h, X.data_ptr())
 
     def stage_eig(self):
         self.eig_status = L.avd_stage_eig(self.h)

@@ -34,37 +34,51 @@ class ModelBackend:
     def exchange_buffer(self, name, dtype):
         return self.buf[name]
 
+    def _sample_step(self):
+        want = max(1, min(16, self.l // 4096))
+        s = 1
+        while s * 2 <= want:
+            s *= 2
+        return s
+
     def stage_stats(self, X):
-        Xd = X.astype(np.float64)
-        key = _keys(X)
-        nz = np.count_nonzero(key)
-        self.buf["STATS"] = torch.tensor(np.concatenate([Xd.sum(0), [np.sum(Xd * Xd), 0.0, nz]]))
-        self.buf["COLMAX"] = torch.tensor(X.max(0))
-        self.buf["COLMIN"] = torch.tensor(X.min(0))
+        s = self._sample_step()
+        rows = np.arange(X.shape[0]) + self.row0
+        Xs = X[rows % s == 0]
+        key = _keys(X[rows % (4 * s) == 0])
+        self.buf["SAMPLE"] = torch.tensor(np.concatenate([Xs.astype(np.float64).sum(0), [len(Xs)]]))
+        self.buf["SMAX"] = torch.tensor(Xs.max(0) if len(Xs) else np.full(self.m, -np.inf, np.float32))
+        self.buf["SMIN"] = torch.tensor(Xs.min(0) if len(Xs) else np.full(self.m, np.inf, np.float32))
         h = np.bincount((key[key != 0] >> 19).ravel(), minlength=4096)
         self.buf["HIST1"] = torch.tensor(h.astype(np.int64))
 
     def stage_split(self, X):
-        st = self.buf["STATS"].numpy()
-        self.mu = st[: self.m] / self.l
-        self.n_eff = int(min(self.n_top, st[self.m + 2]))
+        Xd = X.astype(np.float64)
+        key = _keys(X)
+        self.buf["STATS"] = torch.tensor(np.concatenate([Xd.sum(0), [np.sum(Xd * Xd), 0.0, np.count_nonzero(key), 0.0]]))
+        self.buf["COLMAX"] = torch.tensor(np.abs(X).max(0))
+        s = self._sample_step()
         h = self.buf["HIST1"].numpy()
         cum, b0 = 0, 0
         for b in range(4095, -1, -1):
-            cum += h[b]
-            if cum >= 2 * self.n_eff + 256:
+            cum += h[b] * s * 4
+            if cum >= 2 * self.n_top + 256 * s * 4:
                 b0 = b
                 break
-        key = _keys(X)
         li = np.arange(X.size).reshape(X.shape) + self.row0 * self.m
         sel = (key != 0) & ((key >> 19) >= b0)
         self.ckey, self.cidx = key[sel], li[sel]
         self.buf["CAND"] = torch.tensor([len(self.ckey), 0], dtype=torch.int64)
         self.X = X
 
-    def stage_gram(self):
+    def stage_gram(self, X):
+        st = self.buf["STATS"].numpy()
+        self.mu = st[: self.m] / self.l
+        self.n_eff = int(min(self.n_top, st[self.m + 2]))
         self.Xc = self.X.astype(np.float64) - self.mu
         self.buf["GRAM"] = torch.tensor(self.Xc.T @ self.Xc)
+        self.buf["QSUM"] = torch.zeros(2 * self.m, dtype=torch.int64)
+        self.buf["QERR"] = torch.zeros(self.m, dtype=torch.float64)
 
     def stage_eig(self):
         lam, W = np.linalg.eigh(self.buf["GRAM"].numpy())  # the exchanged (global) Gram

@@ -150,3 +150,35 @@ def test_large_k_parity(cuda_device, k):
     o = O.decompose(X.numpy(), k=k)
     g = _gpu(X, k=k)
     assert_parity(g, o)
+
+
+def test_requantise_forced(cuda_device):
+    """AVD_FLAG_EXACT_SCALE: the Gram operand quantised with the exact column ranges (the
+    fallback path of a digit overflow) gives the same parity."""
+    from paper_2603_10444_b200._lib import AVD_FLAG_EXACT_SCALE
+    X = generate(SynthSpec(3000, 300, seed=12, f_mean=0.8))
+    o = O.decompose(X.numpy())
+    g = _gpu(X, flags=AVD_FLAG_EXACT_SCALE)
+    assert g["res"].requantised == 1
+    assert_parity(g, o)
+
+
+def test_requantise_on_unsampled_outlier(cuda_device):
+    """l = 65536 samples every 16th row for the quantiser scales; a massive activation in an
+    unsampled row overflows the sampled digit range, which must trigger the exact-range
+    re-quantisation.  The single entry then carries ~all of its column's energy, so its
+    quantisation step (2^-13 of the column range with 2 digits) bounds the accuracy of that
+    column's Gram entries: the 2-digit run is checked at 1e-3, the 3-digit run (21-bit operand)
+    at the full tolerances."""
+    X = generate(SynthSpec(65536, 128, seed=13, f_mean=0.8))
+    X[17, 3] = 5000.0   # row 17 is not sampled (17 % 16 != 0)
+    o = O.decompose(X.numpy())
+    g3 = _gpu(X, digits=3)
+    assert g3["res"].requantised == 1
+    assert_parity(g3, o)
+    g2 = _gpu(X, digits=2)
+    assert g2["res"].requantised == 1
+    np.testing.assert_array_equal(g2["top_idx"], o["top_idx"])
+    np.testing.assert_allclose(g2["sigma"], o["sigma"], rtol=1e-3)
+    X2 = generate(SynthSpec(65536, 128, seed=13, f_mean=0.8))
+    assert _gpu(X2)["res"].requantised == 0
