@@ -447,7 +447,8 @@ avd_status avd_stage_select(avd_ctx* c, const float* X, int32_t level, int32_t r
     AVD_CUDA(cudaMemcpyAsync(gx, c->cand_x, sizeof(gx), cudaMemcpyDeviceToHost, c->stream));
     AVD_CUDA(cudaStreamSynchronize(c->stream));
     c->hplan.cand_count = (int64_t)cnt;
-    c->cand_overflow = gx[1] > 0 || gx[0] < c->hplan.n_eff || (c->cfg.flags & AVD_FLAG_STREAM_SELECT);
+    // the candidate list is used only if it holds >= n_top entries (then |E_top| = n_top)
+    c->cand_overflow = gx[1] > 0 || gx[0] < c->plan.n_top || (c->cfg.flags & AVD_FLAG_STREAM_SELECT);
   }
   AVD_TRY(launch_select(c, X, level, rank));
   c->stage = 6 + level;

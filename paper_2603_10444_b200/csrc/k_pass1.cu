@@ -1,9 +1,9 @@
 // k_pass1.cu — K1+K2: the single HBM-streaming pass over X that feeds the rest of the path.
 //
 // One read of X (4 B/entry) produces, fused:
-//   * fp64 column sums (mu = (1/l) X^T 1), sum x^2 (||X||_F^2), column
-//     max/min, the exact count of nonzero entries (|E_top| = min(n_top, #nonzero), R4)
-//     and a non-finite check;
+//   * fp64 column sums (mu = (1/l) X^T 1) and sum x^2 (||X||_F^2), whose
+//     finiteness is the non-finite check; (#nonzero for |E_top| = min(n_top,
+//     #nonzero), R4, comes exactly from the K6 level-0 histogram, k_select.cu);
 //   * the Gram operand: every entry centred on a PROVISIONAL column centre mu0 (from a row
 //     sample) and scaled by the column's power of two 2^shift_j, rounded with a deterministic
 //     dither d (uniform on a 2^-9 grid in (-1/2, 1/2)):  q = rint((x - mu0_j) 2^shift_j + d) — nd balanced
@@ -207,177 +207,201 @@ __device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
 // ---------------------------------------------------------------- the fused pass
 // FULL: statistics + candidates + digits; !FULL: digits + S + E only (requant path).
 // Thread: VEC consecutive columns, rows [r0, r1) of its chunk, U rows in flight.  Per entry the
-// hot loop does the dithered rounding, the digit split and packing, the exact integer / error
-// sums, |y| max (the digit-range check and the exact range for a requant), x and x^2 sums, the
-// nonzero count and a candidate flag whose warp-aggregated append runs only when some lane of
-// the warp has one (the top-0.1% candidates are rare).
+// hot loop does the dithered rounding, the digit split and packing, the exact integer sums of q
+// and q^2, the squared rounding error, |y| max (the digit-range check and the exact range for a
+// requant), the x and x^2 sums and a running max of the |x| bit patterns; only when that max
+// reaches the candidate bin does the warp build candidate masks and append them (one scan and
+// one atomic per warp).  Full U-row groups run without bounds checks; pointers are advanced,
+// not recomputed.
 template <int ND, int VEC, bool FULL>
-__global__ void __launch_bounds__(kT, 3) pass1_kernel(
+__device__ __forceinline__ void pass1_rows(int nrows, const float* __restrict__ xp, int64_t m, int8_t* __restrict__ dp,
+                                           int64_t plane, int64_t m_pad, uint32_t srow0, const float* sc,
+                                           const float* off, const uint32_t* colh, uint32_t klo, uint32_t kspan,
+                                           uint64_t lin0, int lane, uint32_t* __restrict__ cand_key,
+                                           uint64_t* __restrict__ cand_idx, unsigned long long* __restrict__ cand_cnt,
+                                           int64_t cand_cap, double* s, double& sq, int* qs32, long long* qs64,
+                                           long long* qq, float* es, float* ym, bool active, bool writer) {
+  constexpr int U = 4;
+  constexpr int DB = ND == 2 ? 9 : 2;  // dither grid bits (see below)
+  float x[U][VEC];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const bool ok = active && u < nrows;
+    if constexpr (VEC == 4) {
+      const float4 t = ok ? __ldcs(reinterpret_cast<const float4*>(xp + u * m)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      x[u][0] = t.x; x[u][1] = t.y; x[u][2] = t.z; x[u][3] = t.w;
+    } else {
+      x[u][0] = ok ? __ldcs(xp + u * m) : 0.f;
+    }
+  }
+  uint32_t kmax = 0;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    if (u >= nrows) break;
+    const uint32_t srow = srow0 + (uint32_t)u * 0x9E3779B1u;
+    int dg[ND][VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      // dithered rounding: q = rint(y + d), y = (x - mu0) 2^shift, d uniform on the symmetric grid
+      // (k + 1/2) 2^-DB - 1/2, k < 2^DB: y + d is exact in fp32 for integer y (|y| < 2^(7nd)), so
+      // exactly representable data stays exact (tests/test_gpu_parity.py planted case)
+      const uint32_t h = (srow ^ colh[v]) * 0x85EBCA6Bu;
+      const float d = __uint_as_float(0x3F800000u | ((h >> (32 - DB)) << (23 - DB)) | (1u << (22 - DB))) - 1.5f;
+      const float y = fmaf(x[u][v], sc[v], off[v]);
+      const float t = (y + d) + 12582912.0f;  // 1.5 * 2^23: RN to an integer
+      int q = __float_as_int(t) - 0x4B400000;
+      const float e = (t - 12582912.0f) - y;  // exact: q and y share the fp32 grid
+      es[v] = fmaf(e, e, es[v]);
+      ym[v] = fmaxf(ym[v], fabsf(y));
+      if constexpr (ND == 2) qs32[v] += q; else qs64[v] += q;
+      qq[v] += (long long)q * (long long)q;
+      // balanced base-128 digits, most significant first
+#pragma unroll
+      for (int dd = ND - 1; dd >= 1; --dd) {
+        const int hi = (q + 64) >> 7;
+        dg[dd][v] = q - (hi << 7);
+        q = hi;
+      }
+      dg[0][v] = q;
+      if (FULL) kmax = max(kmax, __float_as_uint(x[u][v]) & 0x7FFFFFFFu);
+    }
+    if (writer) {
+#pragma unroll
+      for (int dd = 0; dd < ND; ++dd) {
+        int8_t* row = dp + dd * plane + u * m_pad;
+        if constexpr (VEC == 4) {
+          __stcs(reinterpret_cast<unsigned int*>(row), pack4(dg[dd][0], dg[dd][1], dg[dd][2], dg[dd][3]));
+        } else {
+          *row = (int8_t)dg[dd][0];
+        }
+      }
+    }
+  }
+  if (FULL) {
+    // candidates (key in [klo, 0x7F800000)): rare, so only warps that saw one build masks
+    if (__any_sync(0xFFFFFFFFu, kmax >= klo)) {
+      uint32_t cmask = 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          const uint32_t key = __float_as_uint(x[u][v]) & 0x7FFFFFFFu;
+          cmask |= (u < nrows && (key - klo) < kspan) ? (1u << (u * VEC + v)) : 0u;
+        }
+      const uint32_t cnt = __popc(cmask);
+      uint32_t incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+      unsigned long long base = 0;
+      if (lane == 31 && total) base = atomicAdd(cand_cnt, (unsigned long long)total);
+      base = __shfl_sync(0xFFFFFFFFu, base, 31) + (incl - cnt);
+      if (cmask) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int v = 0; v < VEC; ++v)
+            if ((cmask >> (u * VEC + v)) & 1u) {
+              if (base < (unsigned long long)cand_cap) {
+                cand_key[base] = __float_as_uint(x[u][v]) & 0x7FFFFFFFu;
+                cand_idx[base] = lin0 + (uint64_t)u * (uint64_t)m + (uint64_t)v;
+              }
+              ++base;
+            }
+      }
+    }
+    // fp64 accumulation of U-row fp32 partial sums (each partial rounds once, ~2^-24 relative)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      float ps = 0.f, pq = 0.f;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        ps += x[u][v];  // rows past the end were loaded as 0
+        pq = fmaf(x[u][v], x[u][v], pq);
+      }
+      s[v] += (double)ps;
+      sq += (double)pq;
+    }
+  }
+}
+
+template <int ND, int VEC, bool FULL>
+__global__ void __launch_bounds__(kT, 2) pass1_kernel(
     const float* __restrict__ X, int64_t l, int64_t m, int64_t m_pad, int64_t l_pad, int64_t rpc, int64_t row_offset,
     const float* __restrict__ qscale, const float* __restrict__ qoff, uint32_t seed32, int8_t* __restrict__ digits,
-    const DevPlan* __restrict__ dp, uint32_t* __restrict__ cand_key, uint64_t* __restrict__ cand_idx,
+    const DevPlan* __restrict__ dplan, uint32_t* __restrict__ cand_key, uint64_t* __restrict__ cand_idx,
     unsigned long long* __restrict__ cand_cnt, int64_t cand_cap, double* __restrict__ colsum_part,
     float* __restrict__ ymax_part, double* __restrict__ sq_part, long long* __restrict__ qsum_part,
     long long* __restrict__ qsq_part, float* __restrict__ qerr_part, double* __restrict__ stats) {
-  using QAcc = typename std::conditional<ND == 2, int, long long>::type;
   constexpr int U = 4;
-  constexpr int DB = ND == 2 ? 9 : 2;           // dither grid bits (see below)
   __shared__ double sred[kT / 32];
-  __shared__ unsigned long long snz;
-  if (threadIdx.x == 0) snz = 0;
-  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t c0 = ((int64_t)blockIdx.x * kT + threadIdx.x) * VEC;
   const int64_t r0 = (int64_t)blockIdx.y * rpc;
   const int64_t r1 = min(l, r0 + rpc);
   const bool active = c0 < m;
-  const bool writer = c0 < m_pad;
-  float sc[VEC], off[VEC];
-  uint32_t colh[VEC];
-#pragma unroll
-  for (int v = 0; v < VEC; ++v) {
-    sc[v] = active ? qscale[c0 + v] : 0.f;
-    off[v] = active ? qoff[c0 + v] : 0.f;
-    colh[v] = mix32((uint32_t)(c0 + v) ^ 0x68E31DA4u);
-  }
-  // candidate test as one unsigned compare: key in [max(1, b0 << 19), 0x7F800000)
-  const uint32_t klo = FULL ? max(1u, (uint32_t)dp->b0 << 19) : 0u;
-  const uint32_t kspan = 0x7F800000u - klo;
-  double s[VEC];
-  QAcc qs[VEC];
-  long long qq[VEC];  // exact sum of q^2 (the Gram diagonal of the quantised operand)
-  float es[VEC], ym[VEC];  // sum of squared rounding errors (q - y)^2; max |y|
-#pragma unroll
-  for (int v = 0; v < VEC; ++v) { s[v] = 0.0; qs[v] = 0; qq[v] = 0; es[v] = 0.f; ym[v] = 0.f; }
+  const bool writer = c0 < m_pad;  // digit columns [m, m_pad) come out zero (x = 0, scale 1, centre 0)
+  const int64_t plane = l_pad * m_pad;
   double sq = 0.0;
-  unsigned nz = 0;
-  for (int64_t i = r0; i < r1; i += U) {
-    float x[U][VEC];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const bool ok = active && (i + u < r1);
-      if constexpr (VEC == 4) {
-        const float4 t = ok ? __ldcs(reinterpret_cast<const float4*>(X + (i + u) * m + c0)) : make_float4(0.f, 0.f, 0.f, 0.f);
-        x[u][0] = t.x; x[u][1] = t.y; x[u][2] = t.z; x[u][3] = t.w;
-      } else {
-        x[u][0] = ok ? __ldcs(X + (i + u) * m + c0) : 0.f;
-      }
-    }
-    uint32_t cmask = 0;  // candidate entries (u, v) of this iteration, bit u * VEC + v
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const bool ok = active && (i + u < r1);
-      const uint32_t srow = (uint32_t)(row_offset + i + u) * 0x9E3779B1u + seed32;
-      int dg[ND][VEC];
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) {
-        // dithered rounding: q = rint(y + d), y = (x - mu0) 2^shift, d uniform on the symmetric grid
-        // (k + 1/2) 2^-DB - 1/2, k < 2^DB: y + d is exact in fp32 for integer y (|y| < 2^(7nd)), so
-        // exactly representable data stays exact (tests/test_gpu_parity.py planted case)
-        const uint32_t h = (srow ^ colh[v]) * 0x85EBCA6Bu;
-        const float d = __uint_as_float(0x3F800000u | ((h >> (32 - DB)) << (23 - DB)) | (1u << (22 - DB))) - 1.5f;
-        const float y = ok ? fmaf(x[u][v], sc[v], off[v]) : 0.f;
-        const float t = (y + d) + 12582912.0f;  // 1.5 * 2^23: RN to an integer
-        int q = __float_as_int(t) - 0x4B400000;
-        const float e = (t - 12582912.0f) - y;  // exact: q and y share the fp32 grid
-        es[v] = fmaf(e, e, es[v]);
-        ym[v] = fmaxf(ym[v], fabsf(y));
-        qs[v] += (QAcc)q;
-        qq[v] += (long long)q * (long long)q;
-        // balanced base-128 digits, most significant first
-#pragma unroll
-        for (int dd = ND - 1; dd >= 1; --dd) {
-          const int hi = (q + 64) >> 7;
-          dg[dd][v] = q - (hi << 7);
-          q = hi;
-        }
-        dg[0][v] = q;
-        if (FULL) {
-          const uint32_t key = __float_as_uint(x[u][v]) & 0x7FFFFFFFu;
-          nz += (ok && key != 0u) ? 1u : 0u;
-          cmask |= (ok && (key - klo) < kspan) ? (1u << (u * VEC + v)) : 0u;
-        }
-      }
-      if (writer && i + u < r1) {
-#pragma unroll
-        for (int dd = 0; dd < ND; ++dd) {
-          int8_t* row = digits + ((int64_t)dd * l_pad + i + u) * m_pad + c0;
-          if constexpr (VEC == 4) {
-            __stcs(reinterpret_cast<unsigned int*>(row), pack4(dg[dd][0], dg[dd][1], dg[dd][2], dg[dd][3]));
-          } else {
-            *row = (int8_t)dg[dd][0];
-          }
-        }
-      }
-    }
-    if (FULL) {
-      // candidates: one warp-wide exclusive scan of the per-thread counts and one atomic per warp
-      if (__any_sync(0xFFFFFFFFu, cmask != 0u)) {
-        const uint32_t cnt = __popc(cmask);
-        uint32_t incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-          if (lane >= o) incl += t;
-        }
-        const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-        unsigned long long base = 0;
-        if (lane == 31) base = atomicAdd(cand_cnt, (unsigned long long)total);
-        base = __shfl_sync(0xFFFFFFFFu, base, 31) + (incl - cnt);
-        if (cmask) {
-#pragma unroll
-          for (int u = 0; u < U; ++u)
-#pragma unroll
-            for (int v = 0; v < VEC; ++v)
-              if ((cmask >> (u * VEC + v)) & 1u) {
-                if (base < (unsigned long long)cand_cap) {
-                  cand_key[base] = __float_as_uint(x[u][v]) & 0x7FFFFFFFu;
-                  cand_idx[base] = (uint64_t)(row_offset + i + u) * (uint64_t)m + (uint64_t)(c0 + v);
-                }
-                ++base;
-              }
-        }
-      }
-      // fp64 accumulation of U-row fp32 partial sums (each partial rounds once, ~2^-24 relative)
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) {
-        float ps = 0.f, pq = 0.f;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          ps += x[u][v];  // rows past r1 / inactive columns were loaded as 0
-          pq = fmaf(x[u][v], x[u][v], pq);
-        }
-        s[v] += (double)ps;
-        sq += (double)pq;
-      }
-    }
-  }
-  if (active) {
+  // whole warps take part (the candidate append uses warp collectives); lanes past m load nothing
+  if (__any_sync(0xFFFFFFFFu, writer)) {
+    const int64_t cc = writer ? c0 : 0;
+    float sc[VEC], off[VEC];
+    uint32_t colh[VEC];
 #pragma unroll
     for (int v = 0; v < VEC; ++v) {
-      const int64_t o = (int64_t)blockIdx.y * m + c0 + v;
-      qsum_part[o] = (long long)qs[v];
-      qsq_part[o] = qq[v];
-      qerr_part[o] = es[v];
-      ymax_part[o] = ym[v];
-      if (FULL) colsum_part[o] = s[v];
+      sc[v] = active ? qscale[c0 + v] : 1.f;
+      off[v] = active ? qoff[c0 + v] : 0.f;
+      colh[v] = mix32((uint32_t)(c0 + v) ^ 0x68E31DA4u);
+    }
+    // candidate test as one unsigned compare: key in [max(1, b0 << 19), 0x7F800000)
+    const uint32_t klo = FULL ? max(1u, (uint32_t)dplan->b0 << 19) : 0xFFFFFFFFu;
+    const uint32_t kspan = 0x7F800000u - klo;
+    double s[VEC];
+    int qs32[VEC];
+    long long qs64[VEC], qq[VEC];
+    float es[VEC], ym[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) { s[v] = 0.0; qs32[v] = 0; qs64[v] = 0; qq[v] = 0; es[v] = 0.f; ym[v] = 0.f; }
+    const float* xp = X + r0 * m + (active ? c0 : 0);
+    int8_t* dp = digits + r0 * m_pad + cc;
+    uint32_t srow0 = (uint32_t)(row_offset + r0) * 0x9E3779B1u + seed32;
+    uint64_t lin0 = (uint64_t)(row_offset + r0) * (uint64_t)m + (uint64_t)c0;
+    int64_t i = r0;
+    for (; i + U <= r1; i += U) {
+      pass1_rows<ND, VEC, FULL>(U, xp, m, dp, plane, m_pad, srow0, sc, off, colh, klo, kspan, lin0, lane, cand_key,
+                                cand_idx, cand_cnt, cand_cap, s, sq, qs32, qs64, qq, es, ym, active, writer);
+      xp += U * m;
+      dp += U * m_pad;
+      srow0 += (uint32_t)U * 0x9E3779B1u;
+      lin0 += (uint64_t)U * (uint64_t)m;
+    }
+    if (i < r1)
+      pass1_rows<ND, VEC, FULL>((int)(r1 - i), xp, m, dp, plane, m_pad, srow0, sc, off, colh, klo, kspan, lin0, lane,
+                                cand_key, cand_idx, cand_cnt, cand_cap, s, sq, qs32, qs64, qq, es, ym, active, writer);
+    if (active) {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        const int64_t o = (int64_t)blockIdx.y * m + c0 + v;
+        qsum_part[o] = ND == 2 ? (long long)qs32[v] : qs64[v];
+        qsq_part[o] = qq[v];
+        qerr_part[o] = es[v];
+        ymax_part[o] = ym[v];
+        if (FULL) colsum_part[o] = s[v];
+      }
     }
   }
   if (FULL) {
-    for (int o = 16; o > 0; o >>= 1) {
-      sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o);
-      nz += __shfl_xor_sync(0xFFFFFFFFu, nz, o);
-    }
-    if (lane == 0) {
-      sred[threadIdx.x >> 5] = sq;
-      atomicAdd(&snz, (unsigned long long)nz);
-    }
+    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o);
+    if (lane == 0) sred[threadIdx.x >> 5] = sq;
     __syncthreads();
     if (threadIdx.x == 0) {
       double t = 0.0;
       for (int w = 0; w < kT / 32; ++w) t += sred[w];
       sq_part[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
-      if (snz) atomicAdd(&stats[m + 2], (double)snz);  // integer-valued double: exact, order-free
     }
   }
 }
@@ -450,13 +474,7 @@ __global__ void finish_kernel(int64_t m, int64_t m_pad, int64_t l_global, int64_
     mu_hl[j] = mh;
     mu_hl[m_pad + j] = ml;
   }
-  if (j == 0) {
-    const long long nonzero = (long long)stats[m + 2];
-    const long long n_eff = min((long long)n_top, nonzero);
-    dp->n_eff = n_eff;
-    dp->empty = n_eff == 0 ? 1 : 0;
-    if (!isfinite(stats[m])) atomicAdd(reinterpret_cast<unsigned long long*>(&dp->nonfinite), 1ull);
-  }
+  if (j == 0 && !isfinite(stats[m])) atomicAdd(reinterpret_cast<unsigned long long*>(&dp->nonfinite), 1ull);
 }
 
 // exchange slot for the global candidate decision: [count, overflowed]

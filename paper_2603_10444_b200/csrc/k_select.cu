@@ -62,11 +62,14 @@ __global__ void __launch_bounds__(kSelThreads) hist_kernel(int level, int64_t n,
 }
 
 // Find the bin of radix level `level` that contains the n_eff-th largest key (one warp).
-__global__ void find_bin_kernel(int level, const unsigned long long* __restrict__ h, DevPlan* __restrict__ dp) {
+// Level 0 first sets |E_top| = n_eff = min(n_top, #counted keys): streaming X the level-0
+// histogram counts every nonzero finite entry exactly; the candidate list is only used when it
+// holds >= n_top entries, so there n_eff = n_top (R4).
+__global__ void find_bin_kernel(int level, const unsigned long long* __restrict__ h, int64_t n_top,
+                                DevPlan* __restrict__ dp) {
   const int lane = threadIdx.x;
   const int nb = level < 2 ? kHistBins : kHist3Bins;
   const int per = nb / 32;
-  const long long need = dp->n_eff - dp->cnt_gt;  // rank inside the current prefix (>= 1)
   const int hi = nb - 1 - lane * per;
   unsigned long long mine = 0;
   for (int b = hi; b > hi - per; --b) mine += h[b];
@@ -76,7 +79,19 @@ __global__ void find_bin_kernel(int level, const unsigned long long* __restrict_
     if (lane >= o) incl += t;
   }
   const unsigned long long excl = incl - mine;
+  if (level == 0) {
+    const unsigned long long total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    const long long n_eff = min((long long)n_top, (long long)total);
+    __syncwarp();
+    if (lane == 0) {
+      dp->n_eff = n_eff;
+      dp->empty = n_eff == 0 ? 1 : 0;
+      dp->cnt_gt = 0;
+    }
+    __syncwarp();
+  }
   if (dp->empty) return;
+  const long long need = dp->n_eff - dp->cnt_gt;  // rank inside the current prefix (>= 1)
   if (excl < (unsigned long long)need && incl >= (unsigned long long)need) {
     unsigned long long cum = excl;
     int b = hi;
@@ -329,7 +344,7 @@ avd_status launch_select(Ctx* c, const float* X, int level, int rank) {
   if (level <= 2) {
     unsigned long long* h = level == 0 ? c->hist0 : (level == 1 ? c->hist2 : c->hist3);
     if (level > 0) {
-      find_bin_kernel<<<1, 32, 0, c->stream>>>(level - 1, level == 1 ? c->hist0 : c->hist2, c->dplan);
+      find_bin_kernel<<<1, 32, 0, c->stream>>>(level - 1, level == 1 ? c->hist0 : c->hist2, c->plan.n_top, c->dplan);
       AVD_LAUNCHED(c);
     }
     AVD_CUDA(cudaMemsetAsync(h, 0, sizeof(unsigned long long) * (level < 2 ? kHistBins : kHist3Bins), c->stream));
@@ -337,7 +352,7 @@ avd_status launch_select(Ctx* c, const float* X, int level, int rank) {
     else hist_kernel<false><<<grid, kSelThreads, 0, c->stream>>>(level, n, c->cand_key, c->cand_idx, nullptr, c->dplan, h);
     AVD_LAUNCHED(c);
   } else {
-    find_bin_kernel<<<1, 32, 0, c->stream>>>(2, c->hist3, c->dplan);
+    find_bin_kernel<<<1, 32, 0, c->stream>>>(2, c->hist3, c->plan.n_top, c->dplan);
     AVD_LAUNCHED(c);
     AVD_CUDA(cudaMemsetAsync(c->bm_sel, 0, sizeof(uint32_t) * c->nwords, c->stream));
     AVD_CUDA(cudaMemsetAsync(c->bm_tie, 0, sizeof(uint32_t) * c->nwords, c->stream));
