@@ -265,12 +265,13 @@ __device__ __forceinline__ double rsqrt_fast(double x) {  // 1/sqrt(x), x in the
 // — the rotation only has to shrink a_pq, which a 2^-24-accurate angle does by ~1e-7 per visit —
 // while (c, s) are made orthogonal to fp64 accuracy: c^2 + s^2 = 1 + d from the fp32 pair, scaled by
 // (1 + d)^(-1/2) = 1 - d/2 + 3d^2/8 (|d| <~ 1e-7), so every applied transform is an exact-in-fp64
-// similarity and the eigenvalues keep fp64 accuracy.  Skipped when |a_pq| <= 1e-13 sqrt(a_pp a_qq).
+// similarity and the eigenvalues keep fp64 accuracy.  Skipped when |a_pq| <= 1e-9 sqrt(a_pp a_qq).
 __device__ __forceinline__ void jacobi_rotation(double app, double aqq, double apq, double& c, double& s, bool& rot) {
   c = 1.0;
   s = 0.0;
   rot = false;
-  if (!(apq * apq > 1e-26 * fabs(app * aqq)) || fabs(apq) < 1e-30 || fabs(apq) > 1e30) return;
+  // |a_pq| <= 1e-9 sqrt(a_pp a_qq): eigenvalue error ~1e-18 relative, eigenvector error ~1e-9 / gap
+  if (!(apq * apq > 1e-18 * fabs(app * aqq)) || fabs(apq) < 1e-30 || fabs(apq) > 1e30) return;
   const float th = __fdividef(0.5f * (float)(aqq - app), (float)apq);
   const float ath = fabsf(th);
   if (!(ath < 1e18f)) return;  // |a_pq| below 1e-18 |a_qq - a_pp|: nothing left to rotate

@@ -323,13 +323,14 @@ __global__ void __launch_bounds__(kSelThreads) gather_kernel(const int64_t* __re
   }
 }
 
+// fixed-order sum of the per-CTA partials: 32 lanes stride the partials of each of the 8 sums,
+// then a fixed shuffle tree (deterministic)
 __global__ void agg_reduce_kernel(const double* __restrict__ part, int nparts, double* __restrict__ agg) {
-  const int t = threadIdx.x;
-  if (t < 8) {
-    double s = 0.0;
-    for (int q = 0; q < nparts; ++q) s += part[(int64_t)q * 8 + t];
-    agg[t] = s;
-  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;  // warp w: sum w
+  double s = 0.0;
+  for (int q = lane; q < nparts; q += 32) s += part[(int64_t)q * 8 + w];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+  if (lane == 0) agg[w] = s;
 }
 
 }  // namespace
@@ -392,7 +393,7 @@ avd_status launch_gather(Ctx* c, const float* X, int rank, int64_t* top_idx, dou
   gather_kernel<<<(unsigned)c->n_gather_ctas, kSelThreads, 0, c->stream>>>(top_idx, c->dplan, X, c->cfg.m, c->cfg.row_offset,
                                                                            c->mu, c->P, c->V, c->k, c->k_pad, rho, c->agg_part);
   AVD_LAUNCHED(c);
-  agg_reduce_kernel<<<1, 32, 0, c->stream>>>(c->agg_part, c->n_gather_ctas, c->agg);
+  agg_reduce_kernel<<<1, 256, 0, c->stream>>>(c->agg_part, c->n_gather_ctas, c->agg);
   AVD_LAUNCHED(c);
   return AVD_OK;
 }
