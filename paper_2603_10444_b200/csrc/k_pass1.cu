@@ -117,13 +117,24 @@ __global__ void sample_reduce_kernel(int64_t m, int r1, double n_rows, const dou
                                      double* __restrict__ samp, float* __restrict__ smax, float* __restrict__ smin) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j < m) {
-    double s = 0.0;
+    // 8 independent chains (fixed combination order: deterministic)
+    double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     float mx = -FLT_MAX, mn = FLT_MAX;
-    for (int r = 0; r < r1; ++r) {
-      s += colsum_part[(int64_t)r * m + j];
+    int r = 0;
+    for (; r + 8 <= r1; r += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        a[u] += colsum_part[(int64_t)(r + u) * m + j];
+        mx = fmaxf(mx, colmax_part[(int64_t)(r + u) * m + j]);
+        mn = fminf(mn, colmin_part[(int64_t)(r + u) * m + j]);
+      }
+    }
+    for (; r < r1; ++r) {
+      a[0] += colsum_part[(int64_t)r * m + j];
       mx = fmaxf(mx, colmax_part[(int64_t)r * m + j]);
       mn = fminf(mn, colmin_part[(int64_t)r * m + j]);
     }
+    const double s = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
     samp[j] = s;
     smax[j] = mx;
     smin[j] = mn;
@@ -420,20 +431,36 @@ __global__ void pass1_reduce_kernel(int64_t m, int r1, int nsq, int full, const 
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j < m) {
     long long qs = 0, qq = 0;
-    double qe = 0.0;
+    double e8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     float ym = 0.f;
-    for (int r = 0; r < r1; ++r) {
+    int r = 0;
+    for (; r + 8 <= r1; r += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        qs += qsum_part[(int64_t)(r + u) * m + j];
+        qq += qsq_part[(int64_t)(r + u) * m + j];
+        e8[u] += (double)qerr_part[(int64_t)(r + u) * m + j];
+        ym = fmaxf(ym, ymax_part[(int64_t)(r + u) * m + j]);
+      }
+    }
+    for (; r < r1; ++r) {
       qs += qsum_part[(int64_t)r * m + j];
       qq += qsq_part[(int64_t)r * m + j];
-      qe += (double)qerr_part[(int64_t)r * m + j];
+      e8[0] += (double)qerr_part[(int64_t)r * m + j];
       ym = fmaxf(ym, ymax_part[(int64_t)r * m + j]);
     }
+    const double qe = ((e8[0] + e8[1]) + (e8[2] + e8[3])) + ((e8[4] + e8[5]) + (e8[6] + e8[7]));
     qsum_local[j] = qs;
     qsum_local[m + j] = qq;  // [S | sum q^2]
     qerr_local[j] = qe;
     if (full) {
-      double s = 0.0;
-      for (int r = 0; r < r1; ++r) s += colsum_part[(int64_t)r * m + j];
+      double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      int r2 = 0;
+      for (; r2 + 8 <= r1; r2 += 8)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] += colsum_part[(int64_t)(r2 + u) * m + j];
+      for (; r2 < r1; ++r2) a[0] += colsum_part[(int64_t)r2 * m + j];
+      const double s = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
       stats[j] = s;
       // exact max |x - mu0_j| (power-of-two scale: exact), the range of a requant; |y| beyond
       // the digit range (top digit outside [-127, 127]) counts as an overflow of column j
