@@ -1,0 +1,78 @@
+"""Row-sharded pass on a real GPU: two processes share cuda:0 and exchange the stage buffers of
+include/avd.h with torch.distributed (gloo, which all-reduces CUDA tensors through the host).
+This runs the library's real stage kernels on each shard — the row sample, the fused pass with
+the exchanged quantiser, the integer Gram partials, the replicated eigensolver, the radix
+selection with a tie block straddling the rank boundary — and the concatenated per-rank outputs
+must match the single-process fp64 oracle at the north-star tolerances.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from synth.gen import SynthSpec, generate
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, spec, col_fix, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2603_10444_b200.distributed import ShardedDecomposer, shard_rows
+    r0, lr = shard_rows(spec.l, world, rank)
+    X = generate(spec, r0, lr, device="cuda")
+    if col_fix is not None:
+        X[:, col_fix[0]] = col_fix[1]
+    sd = ShardedDecomposer(spec.l, spec.m)
+    r = sd(X)
+    torch.cuda.synchronize()
+    out[rank] = dict(mu=r.mu.cpu().numpy(), sigma=r.sigma.cpu().numpy(), top=r.top_idx.cpu().numpy(),
+                     rho=r.rho.cpu().numpy(), offset=int(r.top_offset), n_top=int(r.n_top_global),
+                     energy_cf=list(r.energy_cf), energy_el=list(r.energy_el))
+    sd.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _run(spec, col_fix=None, world=2):
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), spec, col_fix, out), nprocs=world, join=True)
+    return [out[r] for r in range(world)]
+
+
+@pytest.mark.parametrize("l,m,col_fix", [(4096, 256, (5, 40.0)), (65536, 128, None)])
+def test_two_ranks_match_oracle(cuda_device, l, m, col_fix):
+    from oracle import oracle as O
+    spec = SynthSpec(l, m, seed=17, f_mean=0.8)
+    res = _run(spec, col_fix)
+    X = generate(spec)
+    if col_fix is not None:
+        X[:, col_fix[0]] = col_fix[1]  # l tied maxima: the tie block straddles the rank boundary
+    o = O.decompose(X.numpy())
+    for r in res:
+        assert np.max(np.abs(r["mu"] - o["mu"])) <= 1e-6 * np.max(np.abs(o["mu"]))
+        np.testing.assert_allclose(r["sigma"], o["sigma"], rtol=1e-4)
+        assert r["n_top"] == o["n_top"]
+        s_g = np.array(r["energy_cf"][1:]) / r["energy_cf"][0]
+        s_o = np.array(o["energy_cf"][1:]) / o["energy_cf"][0]
+        assert np.all(np.abs(s_g - s_o) <= 1e-5 * s_o + 1e-12)
+    assert res[0]["offset"] == 0 and res[1]["offset"] == len(res[0]["top"])
+    np.testing.assert_array_equal(np.concatenate([r["top"] for r in res]), o["top_idx"])
+    rho = np.concatenate([r["rho"] for r in res])
+    assert np.max(np.abs(rho - o["rho"])) <= 1e-3
+    # the replicated eigensolver sees the same exchanged Gram on both ranks
+    np.testing.assert_array_equal(res[0]["sigma"], res[1]["sigma"])
