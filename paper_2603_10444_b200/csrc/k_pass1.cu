@@ -33,6 +33,7 @@ namespace avd {
 namespace {
 
 constexpr int kT = 256;  // threads of the streaming kernels
+constexpr int kNStg = 3;  // cp.async ring depth of the fused pass (U = 4 rows x 16 B per thread and stage)
 
 __device__ __forceinline__ uint32_t mix32(uint32_t x) {
   x ^= x >> 16;
@@ -224,8 +225,8 @@ __device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
 // reaches the candidate bin does the warp build candidate masks and append them (one scan and
 // one atomic per warp).  Full U-row groups run without bounds checks; pointers are advanced,
 // not recomputed.
-template <int ND, int VEC, bool FULL>
-__device__ __forceinline__ void pass1_rows(int nrows, const float* __restrict__ xp, int64_t m, int8_t* __restrict__ dp,
+template <int ND, int VEC, bool FULL, bool SMEM>
+__device__ __forceinline__ void pass1_rows(int nrows, const float* __restrict__ xp, const float4* xs, int64_t m, int8_t* __restrict__ dp,
                                            int64_t plane, int64_t m_pad, uint32_t srow0, const float* sc,
                                            const float* off, const uint32_t* colh, uint32_t klo, uint32_t kspan,
                                            uint64_t lin0, int lane, uint32_t* __restrict__ cand_key,
@@ -238,7 +239,10 @@ __device__ __forceinline__ void pass1_rows(int nrows, const float* __restrict__ 
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const bool ok = active && u < nrows;
-    if constexpr (VEC == 4) {
+    if constexpr (SMEM) {  // prefetched by cp.async (zero-filled past the end)
+      const float4 t = xs[u * kT];
+      x[u][0] = t.x; x[u][1] = t.y; x[u][2] = t.z; x[u][3] = t.w;
+    } else if constexpr (VEC == 4) {
       const float4 t = ok ? __ldcs(reinterpret_cast<const float4*>(xp + u * m)) : make_float4(0.f, 0.f, 0.f, 0.f);
       x[u][0] = t.x; x[u][1] = t.y; x[u][2] = t.z; x[u][3] = t.w;
     } else {
@@ -310,7 +314,20 @@ __device__ __forceinline__ void pass1_rows(int nrows, const float* __restrict__ 
       unsigned long long base = 0;
       if (lane == 31 && total) base = atomicAdd(cand_cnt, (unsigned long long)total);
       base = __shfl_sync(0xFFFFFFFFu, base, 31) + (incl - cnt);
-      if (cmask) {
+      if constexpr (SMEM) {
+        // one step per candidate of this thread; the values are re-read from its ring slot
+        const float* xsf = reinterpret_cast<const float*>(xs);
+        while (cmask) {
+          const int bit = __ffs(cmask) - 1;
+          cmask &= cmask - 1u;
+          const int u = bit / VEC, v = bit % VEC;
+          if (base < (unsigned long long)cand_cap) {
+            cand_key[base] = __float_as_uint(xsf[u * kT * 4 + v]) & 0x7FFFFFFFu;
+            cand_idx[base] = lin0 + (uint64_t)u * (uint64_t)m + (uint64_t)v;
+          }
+          ++base;
+        }
+      } else if (cmask) {
 #pragma unroll
         for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -340,7 +357,7 @@ __device__ __forceinline__ void pass1_rows(int nrows, const float* __restrict__ 
 }
 
 template <int ND, int VEC, bool FULL>
-__global__ void __launch_bounds__(kT, 2) pass1_kernel(
+__global__ void __launch_bounds__(kT, ND == 2 ? 3 : 2) pass1_kernel(
     const float* __restrict__ X, int64_t l, int64_t m, int64_t m_pad, int64_t l_pad, int64_t rpc, int64_t row_offset,
     const float* __restrict__ qscale, const float* __restrict__ qoff, uint32_t seed32, int8_t* __restrict__ digits,
     const DevPlan* __restrict__ dplan, uint32_t* __restrict__ cand_key, uint64_t* __restrict__ cand_idx,
@@ -381,18 +398,57 @@ __global__ void __launch_bounds__(kT, 2) pass1_kernel(
     int8_t* dp = digits + r0 * m_pad + cc;
     uint32_t srow0 = (uint32_t)(row_offset + r0) * 0x9E3779B1u + seed32;
     uint64_t lin0 = (uint64_t)(row_offset + r0) * (uint64_t)m + (uint64_t)c0;
-    int64_t i = r0;
-    for (; i + U <= r1; i += U) {
-      pass1_rows<ND, VEC, FULL>(U, xp, m, dp, plane, m_pad, srow0, sc, off, colh, klo, kspan, lin0, lane, cand_key,
-                                cand_idx, cand_cnt, cand_cap, s, sq, qs32, qs64, qq, es, ym, active, writer);
-      xp += U * m;
-      dp += U * m_pad;
-      srow0 += (uint32_t)U * 0x9E3779B1u;
-      lin0 += (uint64_t)U * (uint64_t)m;
+    if constexpr (VEC == 4) {
+      // cp.async ring: group g (U rows of this thread's 16 B) lands in stage g % kNStg while the
+      // thread computes on group g - kNStg + 1 (memory-level parallelism without registers)
+      extern __shared__ __align__(16) float4 xring[];  // [kNStg][U][kT]
+      const int ng = (int)ceil_div(r1 - r0, U);
+      auto issue = [&](int g) {
+        const int64_t i = r0 + (int64_t)g * U;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const bool ok = active && i + u < r1;
+          const float* src = ok ? X + (i + u) * m + c0 : X;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                           (uint32_t)__cvta_generic_to_shared(&xring[((g % kNStg) * U + u) * kT + threadIdx.x])),
+                       "l"(src), "r"(ok ? 16 : 0)
+                       : "memory");
+        }
+      };
+#pragma unroll
+      for (int g = 0; g < kNStg - 1; ++g) {
+        if (g < ng) issue(g);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      }
+      for (int g = 0; g < ng; ++g) {
+        if (g + kNStg - 1 < ng) issue(g + kNStg - 1);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group %0;" ::"n"(kNStg - 1) : "memory");
+        const int nrows = (int)min((int64_t)U, r1 - (r0 + (int64_t)g * U));
+        pass1_rows<ND, VEC, FULL, true>(nrows, xp, &xring[((g % kNStg) * U) * kT + threadIdx.x], m, dp, plane, m_pad,
+                                        srow0, sc, off, colh, klo, kspan, lin0, lane, cand_key, cand_idx, cand_cnt,
+                                        cand_cap, s, sq, qs32, qs64, qq, es, ym, active, writer);
+        dp += U * m_pad;
+        srow0 += (uint32_t)U * 0x9E3779B1u;
+        lin0 += (uint64_t)U * (uint64_t)m;
+      }
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    } else {
+      int64_t i = r0;
+      for (; i + U <= r1; i += U) {
+        pass1_rows<ND, VEC, FULL, false>(U, xp, nullptr, m, dp, plane, m_pad, srow0, sc, off, colh, klo, kspan, lin0,
+                                         lane, cand_key, cand_idx, cand_cnt, cand_cap, s, sq, qs32, qs64, qq, es, ym,
+                                         active, writer);
+        xp += U * m;
+        dp += U * m_pad;
+        srow0 += (uint32_t)U * 0x9E3779B1u;
+        lin0 += (uint64_t)U * (uint64_t)m;
+      }
+      if (i < r1)
+        pass1_rows<ND, VEC, FULL, false>((int)(r1 - i), xp, nullptr, m, dp, plane, m_pad, srow0, sc, off, colh, klo,
+                                         kspan, lin0, lane, cand_key, cand_idx, cand_cnt, cand_cap, s, sq, qs32, qs64,
+                                         qq, es, ym, active, writer);
     }
-    if (i < r1)
-      pass1_rows<ND, VEC, FULL>((int)(r1 - i), xp, m, dp, plane, m_pad, srow0, sc, off, colh, klo, kspan, lin0, lane,
-                                cand_key, cand_idx, cand_cnt, cand_cap, s, sq, qs32, qs64, qq, es, ym, active, writer);
     if (active) {
 #pragma unroll
       for (int v = 0; v < VEC; ++v) {
@@ -573,7 +629,13 @@ avd_status launch_pass1(Ctx* c, const float* X, bool full) {
   const bool vec = vec4(c, X);
   const int VEC = vec ? 4 : 1;
   const int ncb = (int)ceil_div(c->m_pad, (int64_t)kT * VEC);
-  const int64_t rpc = round_up(ceil_div(l, c->r1), 4);
+  // one full wave: (CTAs resident per SM) x SMs, split over the column blocks (<= c->r1 chunks,
+  // <= 65536 rows per chunk for the int32 sums of q)
+  const int per_sm = (c->nd == 2 && vec) ? 3 : 2;
+  int64_t want = std::max<int64_t>(1, (int64_t)per_sm * c->num_sms / ncb);
+  want = std::min<int64_t>(want, c->r1);
+  want = std::max<int64_t>(want, ceil_div(l, 65536));
+  const int64_t rpc = round_up(ceil_div(l, want), 4);
   const int r1 = (int)ceil_div(l, rpc);
   if (full) {
     AVD_CUDA(cudaMemsetAsync(c->stats, 0, sizeof(double) * (m + 4), c->stream));
@@ -586,17 +648,19 @@ avd_status launch_pass1(Ctx* c, const float* X, bool full) {
                                c->stream));
   dim3 grid(ncb, r1);
   const uint32_t seed32 = dither_seed(c);
+  const int ring = VEC == 4 ? kNStg * 4 * kT * 16 : 0;
 #define LAUNCH(ND, V, F)                                                                                        \
-  pass1_kernel<ND, V, F><<<grid, kT, 0, c->stream>>>(                                                           \
+  AVD_CUDA(cudaFuncSetAttribute(pass1_kernel<ND, V, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, ring));  \
+  pass1_kernel<ND, V, F><<<grid, kT, ring, c->stream>>>(                                                        \
       X, l, m, c->m_pad, c->l_pad, rpc, c->cfg.row_offset, c->qscale, c->qoff, seed32, c->digits, c->dplan,     \
       c->cand_key, c->cand_idx, c->cand_cnt, c->cand_cap, c->colsum_part, c->colmax_part, c->sq_part,          \
       c->qsum_part, c->qsq_part, c->qerr_part, c->stats)
   if (c->nd == 2) {
-    if (full) { if (vec) LAUNCH(2, 4, true); else LAUNCH(2, 1, true); }
-    else { if (vec) LAUNCH(2, 4, false); else LAUNCH(2, 1, false); }
+    if (full) { if (vec) { LAUNCH(2, 4, true); } else { LAUNCH(2, 1, true); } }
+    else { if (vec) { LAUNCH(2, 4, false); } else { LAUNCH(2, 1, false); } }
   } else {
-    if (full) { if (vec) LAUNCH(3, 4, true); else LAUNCH(3, 1, true); }
-    else { if (vec) LAUNCH(3, 4, false); else LAUNCH(3, 1, false); }
+    if (full) { if (vec) { LAUNCH(3, 4, true); } else { LAUNCH(3, 1, true); } }
+    else { if (vec) { LAUNCH(3, 4, false); } else { LAUNCH(3, 1, false); } }
   }
 #undef LAUNCH
   AVD_LAUNCHED(c);
