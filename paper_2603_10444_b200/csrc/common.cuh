@@ -90,6 +90,7 @@ struct Ctx {
   float* G32 = nullptr;           // [m_pad][m_pad] fp32 copy (power steps of K4)
   long long* qsum = nullptr;      // [2 m] column sums of the quantised operand | of its squares (exchange SUM)
   CUtensorMap tmap_digits{};
+  CUtensorMap tmap_digits_b{};    // 64-column SWIZZLE_64B boxes (B halves of the CTA-pair Gram)
   int gram_split = 1;
   // K4
   double *Q = nullptr, *Y = nullptr, *Z = nullptr, *U = nullptr;  // [m][p]

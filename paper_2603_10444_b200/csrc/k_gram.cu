@@ -204,6 +204,224 @@ __global__ void __launch_bounds__(kGramThreads, 1) gram_kernel(const __grid_cons
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
+// ======================================================================= CTA-pair Gram
+// A cluster of two CTAs on one TPC computes a 256-row x 128-column tile with
+// tcgen05.mma.cta_group::2 (M = 256, N = 128, K = 32): each CTA stages its own 128 A-rows (digit
+// columns, SWIZZLE_128B box 128 x 128) and HALF of the 128 B-columns (SWIZZLE_64B box 64 x 128),
+// so per MMA a CTA reads 6 KB of operands from shared memory instead of 8 KB — the single-CTA
+// kernel is bound by that bandwidth (smem-for-tensor ~78%).  Validated bit-exactly by
+// tools/umma_2cta_probe.cu.  Work unit = (256-row block i, 128-column block b >= 2i, K range);
+// the half-tile (2i+1, 2i) below the diagonal is computed but not stored.  The leader CTA
+// (rank 0) issues the MMAs; both CTAs' TMA loads complete on the leader's full barrier, the MMA
+// commits multicast to both CTAs' empty / tfull barriers, and both CTAs' epilogue warps (each
+// reads its own TMEM lanes = its 128 rows) arrive on the leader's tempty barrier.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t caddr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int32_t c0,
+                                                 int32_t c1) {
+  asm volatile("cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+               " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)),
+               "r"(bar_cluster), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void mma_i8_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {  // arrive on `bar` in both CTAs of the pair
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               ::"r"(smem_u32(bar)), "h"((uint16_t)3)
+               : "memory");
+}
+
+__device__ __forceinline__ void unit_coords_pair(int64_t u, int n_pairs, int T, int S, int64_t NK, int& i, int& b,
+                                                 int64_t& ks0, int64_t& ks1) {
+  const int s = (int)(u / n_pairs);
+  int t = (int)(u - (int64_t)s * n_pairs);
+  int ii = 0;
+  while (t >= T - 2 * ii) { t -= T - 2 * ii; ++ii; }
+  i = ii;
+  b = 2 * ii + t;
+  ks0 = NK * s / S;
+  ks1 = NK * (s + 1) / S;
+}
+
+template <int ND, int NS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGramThreads, 1)
+    gram2_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB, int64_t m_pad,
+                 int64_t l_pad, int64_t NK, int T, int S, long long* __restrict__ G) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr uint32_t kABytes = 128 * 128;   // one digit plane of the CTA's 128 A-rows
+  constexpr uint32_t kBBytes = 64 * 128;    // one digit plane of the CTA's 64 B-columns
+  constexpr uint32_t kStageBytes = ND * (kABytes + kBBytes);
+  __shared__ __align__(8) uint64_t full_bar[NS], empty_bar[NS], tfull_bar, tempty_bar;
+  __shared__ uint32_t tmem_base_sh;
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const uint32_t rank = cluster_rank();
+  const int T2 = (T + 1) / 2;
+  const int n_pairs = T2 * T - T2 * (T2 - 1);  // sum_{i < T2} (T - 2i)
+  const int64_t n_units = (int64_t)n_pairs * S;
+  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
+    mbar_init(&tfull_bar, 1);
+    mbar_init(&tempty_bar, 16);  // 8 epilogue warps x 2 CTAs
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) { tma_prefetch(&tmapA); tma_prefetch(&tmapB); }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_sh))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  const uint32_t full0 = mapa_shared(smem_u32(&full_bar[0]), 0);     // leader's full barriers
+  const uint32_t tempty0 = mapa_shared(smem_u32(&tempty_bar), 0);    // leader's tempty barrier
+
+  if (warp == 0) {
+    // ================= TMA producer (both CTAs: own A rows, own half of the B columns)
+    if (elect_one()) {
+      uint32_t it = 0;
+      for (int64_t u = cid; u < n_units; u += ncl) {
+        int i, b;
+        int64_t ks0, ks1;
+        unit_coords_pair(u, n_pairs, T, S, NK, i, b, ks0, ks1);
+        for (int64_t ks = ks0; ks < ks1; ++ks, ++it) {
+          const uint32_t s = it % NS, r = it / NS;
+          mbar_wait(&empty_bar[s], (r & 1) ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[s], 2 * kStageBytes);
+          uint8_t* st = smem + s * kStageBytes;
+          const uint32_t fb = full0 + s * (uint32_t)sizeof(uint64_t);
+#pragma unroll
+          for (int d = 0; d < ND; ++d) {
+            tma_load_2d_pair(st + d * kABytes, &tmapA, fb, (int32_t)((2 * i + (int)rank) * 128),
+                             (int32_t)(d * l_pad + ks * 128));
+            tma_load_2d_pair(st + ND * kABytes + d * kBBytes, &tmapB, fb, (int32_t)(b * 128 + (int)rank * 64),
+                             (int32_t)(d * l_pad + ks * 128));
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer (leader CTA only)
+    if (rank == 0) {
+      constexpr uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) | ((128u >> 3) << 17) |
+                                 ((256u >> 4) << 24);
+      uint32_t it = 0, ui = 0;
+      for (int64_t u = cid; u < n_units; u += ncl, ++ui) {
+        int i, b;
+        int64_t ks0, ks1;
+        unit_coords_pair(u, n_pairs, T, S, NK, i, b, ks0, ks1);
+        mbar_wait(&tempty_bar, (ui & 1) ^ 1);
+        tc_fence_after();
+        for (int64_t ks = ks0; ks < ks1; ++ks, ++it) {
+          const uint32_t s = it % NS, r = it / NS;
+          mbar_wait(&full_bar[s], r & 1);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t abase = smem_u32(smem + s * kStageBytes);
+            const uint32_t bbase = abase + ND * kABytes;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              uint64_t a[ND], bd[ND];
+#pragma unroll
+              for (int d = 0; d < ND; ++d) {
+                a[d] = smem_desc(abase + d * kABytes + kk * 4096, 16384, 1024, 2);  // SW128, MN-major
+                bd[d] = smem_desc(bbase + d * kBBytes + kk * 2048, 8192, 512, 4);   // SW64, MN-major
+              }
+              const uint32_t acc = (ks > ks0 || kk > 0) ? 1u : 0u;
+              if (ND == 2) {
+                mma_i8_pair(tmem + 0, a[0], bd[0], idesc, acc);
+                mma_i8_pair(tmem + 128, a[0], bd[1], idesc, acc);
+                mma_i8_pair(tmem + 128, a[1], bd[0], idesc, 1u);
+                mma_i8_pair(tmem + 256, a[1], bd[1], idesc, acc);
+              } else {
+                mma_i8_pair(tmem + 0, a[0], bd[0], idesc, acc);
+                mma_i8_pair(tmem + 128, a[0], bd[1], idesc, acc);
+                mma_i8_pair(tmem + 128, a[1], bd[0], idesc, 1u);
+                mma_i8_pair(tmem + 256, a[0], bd[ND - 1], idesc, acc);
+                mma_i8_pair(tmem + 256, a[1], bd[1], idesc, 1u);
+                mma_i8_pair(tmem + 256, a[ND - 1], bd[0], idesc, 1u);
+              }
+            }
+            mma_commit_pair(&empty_bar[s]);
+          }
+          __syncwarp();
+        }
+        if (elect_one()) mma_commit_pair(&tfull_bar);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ================= epilogue (both CTAs): warps 2..9 -> TMEM lane quadrant, column half
+    const uint32_t q = warp & 3, h = (warp - 2) >> 2;
+    uint32_t ui = 0;
+    for (int64_t u = cid; u < n_units; u += ncl, ++ui) {
+      int i, b;
+      int64_t ks0, ks1;
+      unit_coords_pair(u, n_pairs, T, S, NK, i, b, ks0, ks1);
+      mbar_wait(&tfull_bar, ui & 1);
+      tc_fence_after();
+      const int ta = 2 * i + (int)rank;  // this CTA's 128-row block
+      if (ta < T && ta <= b) {           // skip the half-tile below the diagonal / past m_pad
+        const int64_t row = (int64_t)ta * 128 + q * 32 + lane;
+        unsigned long long* gcol =
+            reinterpret_cast<unsigned long long*>(G + ((int64_t)b * 128 + h * 64) * m_pad + row);
+        const uint32_t tbase = tmem + ((q * 32) << 16) + h * 64;
+#pragma unroll 1
+        for (int c0 = 0; c0 < 64; c0 += 16) {
+          uint32_t r0[16], r1[16], r2[16];
+          tmem_ld16(tbase + c0, r0);
+          tmem_ld16(tbase + 128 + c0, r1);
+          tmem_ld16(tbase + 256 + c0, r2);
+          tmem_ld_wait();
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            const long long v = ((long long)(int32_t)r0[t] << 14) + ((long long)(int32_t)r1[t] << 7) +
+                                (long long)(int32_t)r2[t];
+            if (v != 0) atomicAdd(gcol + (int64_t)(c0 + t) * m_pad, (unsigned long long)v);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty0);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -235,6 +453,17 @@ int choose_split(int n_tiles, int64_t NK, int sms) {
 
 PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() { return get_encode(); }
 
+bool gram_pair_enabled(const Ctx* c) {
+  if (c->num_sms < 2) return false;
+  const char* e = getenv("AVD_GRAM_1CTA");
+  return !(e && atoi(e) != 0);
+}
+
+int gram_pair_count(int T) {
+  const int T2 = (T + 1) / 2;
+  return T2 * T - T2 * (T2 - 1);
+}
+
 avd_status gram_make_tmap(Ctx* c) {
   auto enc = get_encode();
   if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return AVD_ECUDA; }
@@ -246,8 +475,15 @@ avd_status gram_make_tmap(Ctx* c) {
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r)); return AVD_ECUDA; }
+  // B halves of the CTA-pair kernel: 64 digit columns x 128 K-rows, SWIZZLE_64B
+  uint32_t boxb[2] = {64, 128};
+  r = enc(&c->tmap_digits_b, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, c->digits, dims, strides, boxb, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled (B halves) failed: " + std::to_string((int)r)); return AVD_ECUDA; }
   const int T = (int)(c->m_pad / 128);
-  c->gram_split = choose_split(T * (T + 1) / 2, c->l_pad / 128, c->num_sms);
+  c->gram_split = gram_pair_enabled(c) ? choose_split(gram_pair_count(T), c->l_pad / 128, c->num_sms / 2)
+                                       : choose_split(T * (T + 1) / 2, c->l_pad / 128, c->num_sms);
   if (const char* e = getenv("AVD_GRAM_SPLIT")) {
     const int v = atoi(e);
     if (v >= (int)ceil_div(c->l_pad / 128, 512) && v <= c->l_pad / 128) c->gram_split = v;
@@ -257,12 +493,32 @@ avd_status gram_make_tmap(Ctx* c) {
 
 avd_status launch_gram(Ctx* c) {
   const int T = (int)(c->m_pad / 128);
-  const int n_tiles = T * (T + 1) / 2;
   const int64_t NK = c->l_pad / 128;
   const int S = c->gram_split;
+  AVD_CUDA(cudaMemsetAsync(c->gram_i, 0, sizeof(long long) * c->m_pad * c->m_pad, c->stream));
+  if (gram_pair_enabled(c)) {
+    const int64_t units = (int64_t)gram_pair_count(T) * S;
+    const int clusters = (int)std::min<int64_t>(units, c->num_sms / 2);
+    const int grid = 2 * clusters;
+    if (c->nd == 2) {
+      constexpr int NS = 4;
+      const size_t smem = (size_t)NS * 2 * (128 * 128 + 64 * 128) + 1024;
+      AVD_CUDA(cudaFuncSetAttribute(gram2_kernel<2, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      gram2_kernel<2, NS><<<grid, kGramThreads, smem, c->stream>>>(c->tmap_digits, c->tmap_digits_b, c->m_pad,
+                                                                   c->l_pad, NK, T, S, c->gram_i);
+    } else {
+      constexpr int NS = 3;
+      const size_t smem = (size_t)NS * 3 * (128 * 128 + 64 * 128) + 1024;
+      AVD_CUDA(cudaFuncSetAttribute(gram2_kernel<3, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      gram2_kernel<3, NS><<<grid, kGramThreads, smem, c->stream>>>(c->tmap_digits, c->tmap_digits_b, c->m_pad,
+                                                                   c->l_pad, NK, T, S, c->gram_i);
+    }
+    AVD_LAUNCHED(c);
+    return AVD_OK;
+  }
+  const int n_tiles = T * (T + 1) / 2;
   const int64_t units = (int64_t)n_tiles * S;
   const int grid = (int)std::min<int64_t>(units, c->num_sms);
-  AVD_CUDA(cudaMemsetAsync(c->gram_i, 0, sizeof(long long) * c->m_pad * c->m_pad, c->stream));
   if (c->nd == 2) {
     constexpr int NS = 3;
     const size_t smem = (size_t)NS * 2 * 2 * kBox + 1024;
