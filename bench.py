@@ -363,6 +363,8 @@ def main():
         "roofline": roofline, "stage_ms": stage_ms, "streaming_roofline": stream_roof,
         "eig_iters": res.iters, "eig_max_resid": res.max_resid, "eig_rr_checks": res.rr_checks,
         "eig_jacobi_sweeps": res.jacobi_sweeps,
+        "mean_diagnostics": {"R": res.mean_R, "sign_fraction": res.sign_fraction, "cos_mu_v1": res.cos_mu_v1,
+                             "alpha1": res.alpha1, "sigma1_uncentred": res.sigma1_u, "power_iters": res.iters_u},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(spec, 2048, 512)

@@ -113,6 +113,20 @@ typedef struct {
   int32_t rr_checks;      /* Rayleigh-Ritz checks of the eigensolver (diagnostic)           */
   int32_t jacobi_sweeps;   /* total sweeps of the p x p Jacobi solves (diagnostic)           */
   int32_t requantised;     /* 1 if the Gram operand was re-quantised with exact column ranges */
+  /* mean-bias diagnostics ("Mean bias phenomenon"; Eq. R):
+   *   p_i = x_i^T mu_hat (mu_hat = mu / ||mu||); sign_fraction = max(#p_i > 0, #p_i < 0) / l
+   *   (-1 when unavailable: m % 4 != 0 projection path; 0 when mu = 0);
+   *   R = ||mu|| / sqrt(||X||_F^2 / l);  v_1, sigma_1 = top right singular pair of the UNCENTRED
+   *   X (eigenpair of X^T X = G + l mu mu^T); alpha_1 = (sigma_1 / l) u_1^T 1 = mu . v_1 (sign of
+   *   v_1 chosen so alpha_1 >= 0); cos_mu_v1 = |mu_hat . v_1| (0 when mu = 0)                    */
+  double mean_R;
+  double sign_fraction;
+  int64_t p_pos, p_neg;
+  double cos_mu_v1;
+  double alpha1;
+  double sigma1_u;
+  double resid_u;          /* ||Gu v - lambda v|| / lambda of the uncentred power iteration     */
+  int32_t iters_u;         /* its steps                                                         */
 } avd_outputs;
 
 typedef struct avd_ctx avd_ctx;
@@ -120,7 +134,7 @@ typedef struct avd_ctx avd_ctx;
 /* Sizes and workspace for a configuration (no device work).  AVD_EINVAL when l_global < 2,
  * m < 2, k > min(l, m), a fraction outside (0, 1], p > 112, or the row
  * shard is inconsistent.                                                                    */
-avd_status avd_plan(const avd_config* cfg, avd_plan_t* plan);
+avd_status avd_plan(const avd_config* cfg, avd_plan_t* plan);  /* k <= 95 */
 
 /* Allocate the workspace on cfg->device and bind cfg->stream.  *ctx is NULL on failure.     */
 avd_status avd_create(const avd_config* cfg, avd_ctx** ctx);
@@ -155,9 +169,11 @@ avd_status avd_decompose_host(avd_ctx* ctx, const float* X_host, avd_outputs* ou
  *                       ranges if any rank's digits overflowed; K3 tcgen05 int8 Gram, exact int64)
  *       exchange: AVD_BUF_GRAM (i64, SUM), AVD_BUF_CAND (i64, SUM), AVD_BUF_QSUM (i64, SUM),
  *                 AVD_BUF_QERR (f64, SUM)
- *   avd_stage_eig      (exact centring of the Gram, K4 subspace iteration + Rayleigh-Ritz;
- *                       replicated on every rank)
- *   avd_stage_project  (K5+K8 projections P = Xc V_k and elementwise energies)
+ *   avd_stage_eig      (exact centring of the Gram, K4 subspace iteration + Rayleigh-Ritz, and
+ *                       the top eigenpair of the uncentred Gram G + l mu mu^T; replicated on every
+ *                       rank)
+ *   avd_stage_project  (K5+K8 projections P = Xc V_k and elementwise energies, counts of the
+ *                       signs of p_i = x_i . mu_hat)
  *       exchange: AVD_BUF_ENERGY (f64, SUM)
  *   avd_stage_select(level 0)  (K6 exact |x| histogram, bits 30:19)  exchange: AVD_BUF_HIST0 (i64, SUM)
  *   avd_stage_select(level 1)  (K6 bits 18:7 inside bin b1)          exchange: AVD_BUF_HIST2 (i64, SUM)

@@ -184,6 +184,41 @@ def decompose(X, k: int | None = None, n_top: int | None = None, k_frac: float =
     )
 
 
+def mean_diagnostics(X) -> dict:
+    """Mean-bias diagnostics of the paper's section "Mean bias phenomenon" and
+    Eq. R, in the paper's order and notation, fp64:
+      mu = (1/l) X^T 1; mu_hat = mu / ||mu||; p_i = x_i^T mu_hat (PAPER.md:551);
+      sign fraction = max(#p_i > 0, #p_i < 0) / l ("max fraction of tokens whose
+      x_i^T mu_hat shares one sign"); R = ||mu|| / sqrt(||X||_F^2 / l) (N read as l, SPEC.md:246);
+      X = U S V^T (uncentred): v_1, sigma_1 from the Jacobi eigendecomposition of
+      X^T X; u_1 = X v_1 / sigma_1; alpha_1 = (sigma_1 / l) u_1^T 1 (sign of v_1
+      such that alpha_1 >= 0); cos_mu_v1 = |mu_hat^T v_1| (0 when mu = 0).
+    Readings (R19): with mu = 0 the sign fraction and cos are 0."""
+    X = _f32(X)
+    l, m = X.shape
+    Xd = X.astype(np.float64)
+    mu = column_mean(X)
+    nmu = math.sqrt(float(mu @ mu))
+    if nmu > 0.0:
+        p = Xd @ (mu / nmu)
+        pos, neg = int(np.count_nonzero(p > 0)), int(np.count_nonzero(p < 0))
+        frac = max(pos, neg) / l
+    else:
+        pos = neg = 0
+        frac = 0.0
+    R = nmu / math.sqrt(float(np.sum(Xd * Xd)) / l)
+    lam, V, _ = jacobi_eig(gram(Xd))
+    v1 = V[:, 0].copy()
+    s1 = math.sqrt(max(lam[0], 0.0))
+    u1 = (Xd @ v1) / s1 if s1 > 0 else np.zeros(l)
+    alpha1 = s1 / l * float(np.sum(u1))
+    if alpha1 < 0:
+        v1, u1, alpha1 = -v1, -u1, -alpha1
+    cos = abs(float(mu @ v1)) / nmu if nmu > 0 else 0.0
+    return dict(mu_norm=nmu, p_pos=pos, p_neg=neg, sign_fraction=frac, R=R, sigma1_u=s1, v1=v1,
+                alpha1=alpha1, cos_mu_v1=cos)
+
+
 def host_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))

@@ -53,7 +53,12 @@ class avd_outputs(ctypes.Structure):
                 ("sigma_next", ctypes.c_double), ("trace_g", ctypes.c_double),
                 ("iters", ctypes.c_int32), ("max_resid", ctypes.c_double),
                 ("rr_checks", ctypes.c_int32), ("jacobi_sweeps", ctypes.c_int32),
-                ("requantised", ctypes.c_int32)]
+                ("requantised", ctypes.c_int32),
+                ("mean_R", ctypes.c_double), ("sign_fraction", ctypes.c_double),
+                ("p_pos", ctypes.c_int64), ("p_neg", ctypes.c_int64),
+                ("cos_mu_v1", ctypes.c_double), ("alpha1", ctypes.c_double),
+                ("sigma1_u", ctypes.c_double), ("resid_u", ctypes.c_double),
+                ("iters_u", ctypes.c_int32)]
 
 
 _lib = None

@@ -52,7 +52,7 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   const int64_t k = cfg->k_override > 0 ? cfg->k_override : std::max<int64_t>(1, floor_frac(cfg->k_frac, m));
   if (k > std::min(l, m)) { set_error("k > min(l, m) (SPEC.md:227)"); return AVD_EINVAL; }
   const int64_t p = ((k + 8 + 15) / 16) * 16;
-  if (p > kMaxP || k > 96) { set_error("k too large for this build (p <= 112, k <= 96)"); return AVD_EINVAL; }
+  if (p > kMaxP || k > 95) { set_error("k too large for this build (p <= 112, k <= 95)"); return AVD_EINVAL; }
   const int64_t n_top = cfg->n_top_override > 0 ? cfg->n_top_override : std::max<int64_t>(1, floor_frac(cfg->top_frac, l * m));
   const int nd = cfg->digits == 0 ? 2 : cfg->digits;
   if (nd != 2 && nd != 3) { set_error("digits must be 2 or 3"); return AVD_EINVAL; }
@@ -67,7 +67,7 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   C->cfg.world = world;
   C->k = (int)k;
   C->p = (int)p;
-  C->k_pad = (int)(((k + 15) / 16) * 16);
+  C->k_pad = (int)(((k + 1 + 15) / 16) * 16);  // + one column: the mean direction (diagnostics)
   C->nd = nd;
   C->m_pad = round_up(m, kGramTile);
   C->m_pad32 = round_up(m, 32);
@@ -117,7 +117,7 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   L.add(sizeof(float) * ll * C->k_pad);         // 30 P
   L.add(sizeof(double) * C->n_proj_ctas * 4);   // 31 en_part
   L.add(sizeof(double) * C->n_proj_ctas * C->k_pad);  // 32 colsumP_part
-  L.add(sizeof(double) * (4 + C->k_pad));       // 33 energy
+  L.add(sizeof(double) * (6 + C->k_pad));       // 33 energy (+ #p_i > 0, #p_i < 0)
   L.add(sizeof(unsigned long long) * kHistBins);// 34 hist2
   L.add(sizeof(unsigned long long) * kHist3Bins);// 35 hist3
   L.add(sizeof(long long) * 2 * world);         // 36 ties
@@ -152,6 +152,7 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   L.add(sizeof(double) * C->m_pad);                                      // 65 qerr
   L.add(sizeof(float) * C->m_pad);                                       // 66 mu0
   L.add(sizeof(long long) * C->r1 * m);                                  // 67 qsq_part
+  L.add(sizeof(double) * (4 + 2 * C->m_pad));                            // 68 diag: |mu|, scratch, q, y
   if (L.n >= 128) { set_error("workspace layout table overflow"); return AVD_EINVAL; }
   plan->workspace_bytes = L.total;
   if (lay) *lay = L;
@@ -291,7 +292,7 @@ avd_status avd_create(const avd_config* cfg, avd_ctx** out) {
   BIND(G32, float*); BIND(qsum, long long*); BIND(Q32, float*); BIND(Z32, float*); BIND(ticket, unsigned*); BIND(gmax, double*);
   BIND(samp, double*); BIND(smax, float*); BIND(smin, float*); BIND(qscale, float*); BIND(qoff, float*);
   BIND(qsum_part, long long*); BIND(qsum_local, long long*); BIND(qerr_part, float*); BIND(qerr_local, double*);
-  BIND(qerr, double*); BIND(mu0, float*); BIND(qsq_part, long long*);
+  BIND(qerr, double*); BIND(mu0, float*); BIND(qsq_part, long long*); BIND(diag, double*);
 #undef BIND
   if (cudaMallocHost(&c->eig_host, sizeof(double) * 4 * kMaxP) != cudaSuccess) {
     cudaGetLastError();
@@ -357,7 +358,7 @@ avd_status avd_buffer(avd_ctx* c, int32_t which, void** ptr, size_t* bytes) {
     case AVD_BUF_COLMIN: *ptr = c->colmin; *bytes = sizeof(float) * m; break;
     case AVD_BUF_HIST1: *ptr = c->hist1; *bytes = sizeof(long long) * kHistBins; break;
     case AVD_BUF_GRAM: *ptr = c->gram_i; *bytes = sizeof(long long) * c->m_pad * c->m_pad; break;
-    case AVD_BUF_ENERGY: *ptr = c->energy; *bytes = sizeof(double) * (4 + c->k_pad); break;
+    case AVD_BUF_ENERGY: *ptr = c->energy; *bytes = sizeof(double) * (6 + c->k_pad); break;
     case AVD_BUF_HIST2: *ptr = c->hist2; *bytes = sizeof(long long) * kHistBins; break;
     case AVD_BUF_HIST3: *ptr = c->hist3; *bytes = sizeof(long long) * kHist3Bins; break;
     case AVD_BUF_TIES: *ptr = c->ties; *bytes = sizeof(long long) * 2 * c->cfg.world; break;
@@ -425,6 +426,7 @@ avd_status avd_stage_eig(avd_ctx* c) {
   AVD_TRY(launch_gram_finalize(c));
   avd_status st = run_eig(c);
   if (st != AVD_OK && st != AVD_ENOCONV) return st;
+  AVD_TRY(run_uncentred(c));  // mean-bias diagnostics
   c->stage = 4;
   return st;
 }
@@ -486,6 +488,8 @@ avd_status avd_stage_report(avd_ctx* c, avd_outputs* out) {
   AVD_CUDA(cudaMemcpyAsync(h + 16, c->energy, sizeof(double) * 4, cudaMemcpyDeviceToHost, c->stream));
   AVD_CUDA(cudaMemcpyAsync(h + 20, c->stats + m, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   AVD_CUDA(cudaMemcpyAsync(h + 21, c->trace, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  AVD_CUDA(cudaMemcpyAsync(h + 22, c->energy + 4 + c->k_pad, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  AVD_CUDA(cudaMemcpyAsync(h + 24, c->diag, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   std::vector<double> sig(k);
   AVD_CUDA(cudaMemcpyAsync(sig.data(), c->sigma, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
   AVD_CUDA(cudaMemcpyAsync(&c->hplan, c->dplan, sizeof(DevPlan), cudaMemcpyDeviceToHost, c->stream));
@@ -517,6 +521,17 @@ avd_status avd_stage_report(avd_ctx* c, avd_outputs* out) {
   out->rr_checks = c->rr_count;
   out->jacobi_sweeps = c->jacobi_sweeps;
   out->requantised = c->requantised ? 1 : 0;
+  // mean-bias diagnostics
+  const double lg = (double)c->cfg.l_global;
+  out->mean_R = (total > 0.0) ? h[24] / std::sqrt(total / lg) : 0.0;
+  out->p_pos = (int64_t)h[22];
+  out->p_neg = (int64_t)h[23];
+  out->sign_fraction = c->sign_valid ? (double)std::max(out->p_pos, out->p_neg) / lg : -1.0;
+  out->cos_mu_v1 = c->cos_mu_v1;
+  out->alpha1 = c->alpha1;
+  out->sigma1_u = c->sigma1_u;
+  out->resid_u = c->resid_u;
+  out->iters_u = c->iters_u;
   out->n_top_local = c->hplan.sel_local;
   out->top_offset = c->hplan.top_offset;
   out->n_top_global = c->hplan.n_eff;

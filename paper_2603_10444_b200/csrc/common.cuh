@@ -101,6 +101,12 @@ struct Ctx {
   float *Q32 = nullptr, *Z32 = nullptr;  // [m][p] fp32 mirrors of Q, Z
   unsigned* ticket = nullptr;     // last-CTA ticket of the fused reductions
   double* gmax = nullptr;         // max |G| (fixed-point scale of the Y = G Q accumulation)
+  // mean-bias diagnostics: diag[0] = ||mu||, diag[4..4+m_pad) = q,
+  // diag[4+m_pad..) = y of the uncentred power iteration
+  double* diag = nullptr;
+  double sigma1_u = 0, alpha1 = 0, cos_mu_v1 = 0, resid_u = 0;
+  int iters_u = 0;
+  bool sign_valid = false;        // p_i signs available (tensor-core projection path)
   double* resid = nullptr;        // [p]
   double* trace = nullptr;        // [1]
   double* eig_host = nullptr;     // pinned: theta[p] + resid[p]
@@ -177,6 +183,8 @@ __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_
 avd_status launch_sample(Ctx* c, const float* X);          // k_pass1.cu
 avd_status launch_pass1(Ctx* c, const float* X, bool full); // k_pass1.cu
 avd_status launch_finish(Ctx* c);                          // k_pass1.cu
+avd_status run_uncentred(Ctx* c);                          // k_eig.cu (mean-bias diagnostics)
+avd_status launch_sign_count(Ctx* c);                      // k_project.cu (mean-bias diagnostics)
 avd_status launch_gram(Ctx* c);                            // k_gram.cu
 avd_status gram_make_tmap(Ctx* c);                         // k_gram.cu
 avd_status launch_gram_finalize(Ctx* c);                   // k_eig.cu

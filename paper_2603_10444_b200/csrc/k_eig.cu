@@ -762,6 +762,105 @@ __global__ void finalize_vectors_kernel(const double* __restrict__ U, const doub
   if (threadIdx.x == 0) sigma[r] = sqrt(fmax(theta[r], 0.0));
 }
 
+// ---------------------------------------------------------------- mean-bias diagnostics
+// ("Mean bias phenomenon"): the mean direction mu_hat and the
+// top right singular vector v_1 of the UNCENTRED X, whose Gram is X^T X = G + l mu mu^T.
+// ||mu|| (one CTA, fixed order) -> diag[0]; q_0 = mu / ||mu|| -> diag[4..4+m_pad)
+__global__ void mu_norm_kernel(const double* __restrict__ mu, int64_t m, int64_t m_pad, double* __restrict__ diag) {
+  __shared__ double sh[256];
+  double s = 0.0;
+  for (int64_t j = threadIdx.x; j < m; j += 256) s = fma(mu[j], mu[j], s);
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  const double nrm = sqrt(sh[0]);
+  if (threadIdx.x == 0) diag[0] = nrm;
+  double* q = diag + 4;
+  for (int64_t j = threadIdx.x; j < m_pad; j += 256) q[j] = (j < m && nrm > 0.0) ? mu[j] / nrm : 0.0;
+}
+
+// m-length fixed-order dot products of one CTA (256 threads): returns (a . b, b . b)
+__device__ __forceinline__ double2 cta_dots(const double* __restrict__ a, const double* __restrict__ b, int64_t m,
+                                            double* sh) {
+  double s = 0.0, t = 0.0;
+  for (int64_t j = threadIdx.x; j < m; j += 256) {
+    s = fma(a[j], b[j], s);
+    t = fma(b[j], b[j], t);
+  }
+  sh[threadIdx.x] = s;
+  sh[256 + threadIdx.x] = t;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) {
+      sh[threadIdx.x] += sh[threadIdx.x + w];
+      sh[256 + threadIdx.x] += sh[256 + threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  const double2 r = make_double2(sh[0], sh[256]);
+  __syncthreads();
+  return r;
+}
+
+// One power step on the uncentred Gram:  dst = (G + l mu mu^T) src / ||src||.  Every CTA
+// recomputes mu.src and ||src|| (fixed order) so no inter-CTA reduction is needed; one warp per
+// row of the L2-resident G32, fp64 accumulation.
+__global__ void __launch_bounds__(256) power_u_kernel(const float* __restrict__ G32, int64_t ld,
+                                                      const double* __restrict__ mu, int64_t m, double l,
+                                                      const double* __restrict__ src, double* __restrict__ dst) {
+  __shared__ double sh[512];
+  const double2 d = cta_dots(mu, src, m, sh);
+  const double inv = d.y > 0.0 ? 1.0 / sqrt(d.y) : 0.0;
+  const double lmq = l * d.x * inv;  // l (mu . q)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t a = (int64_t)blockIdx.x * 8 + warp; a < m; a += (int64_t)gridDim.x * 8) {
+    const float* row = G32 + a * ld;
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+    int64_t b = lane;
+    for (; b + 96 < m; b += 128) {
+      acc0 = fma((double)row[b], src[b], acc0);
+      acc1 = fma((double)row[b + 32], src[b + 32], acc1);
+      acc2 = fma((double)row[b + 64], src[b + 64], acc2);
+      acc3 = fma((double)row[b + 96], src[b + 96], acc3);
+    }
+    for (; b < m; b += 32) acc0 = fma((double)row[b], src[b], acc0);
+    double acc = (acc0 + acc1) + (acc2 + acc3);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+    if (lane == 0) dst[a] = acc * inv + lmq * mu[a];
+  }
+}
+
+// q = src / ||src||, y = Gu q (= dst):  diag[1] = q.y (Rayleigh quotient), diag[2] =
+// ||y - (q.y) q|| / (q.y) (residual), diag[3] = mu . q
+__global__ void power_u_stats_kernel(const double* __restrict__ mu, int64_t m, const double* __restrict__ src,
+                                     const double* __restrict__ dst, double* __restrict__ diag) {
+  __shared__ double sh[512];
+  const double2 a = cta_dots(src, dst, m, sh);   // (src . dst, dst . dst)
+  const double2 b = cta_dots(mu, src, m, sh);    // (mu . src, src . src)
+  const double ns = sqrt(b.y);
+  const double lam = ns > 0.0 ? a.x / ns : 0.0;  // q.y with q = src/|src|, y = dst
+  // ||y - lam q||^2 elementwise (no cancellation), fixed order
+  double r = 0.0;
+  for (int64_t j = threadIdx.x; j < m; j += 256) {
+    const double e = dst[j] - (ns > 0.0 ? lam * src[j] / ns : 0.0);
+    r = fma(e, e, r);
+  }
+  sh[threadIdx.x] = r;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    diag[1] = lam;
+    diag[2] = lam > 0.0 ? sqrt(sh[0]) / lam : 0.0;
+    diag[3] = ns > 0.0 ? b.x / ns : 0.0;
+  }
+}
+
 }  // namespace
 
 avd_status launch_gram_finalize(Ctx* c) {
@@ -980,6 +1079,41 @@ avd_status run_eig(Ctx* c) {
   finalize_vectors_kernel<<<k, 256, 0, c->stream>>>(c->U, c->theta, m, p, k, c->k_pad, c->V, c->sigma, c->V32);
   AVD_LAUNCHED(c);
   return conv ? AVD_OK : AVD_ENOCONV;
+}
+
+// Mean-bias diagnostics on the replicated G and mu (no exchange): power iteration on the uncentred
+// Gram from q_0 = mu_hat (already aligned when the mean dominates), in blocks of
+// 4 steps until the residual is <= 1e-8 (at most 64 steps).  Fills c->sigma1_u = sqrt(lambda_1),
+// c->alpha1 = |mu . v_1| (= (sigma_1 / l) u_1^T 1), c->cos_mu_v1 = alpha1 / ||mu||.
+avd_status run_uncentred(Ctx* c) {
+  const int64_t m = c->cfg.m;
+  mu_norm_kernel<<<1, 256, 0, c->stream>>>(c->mu, m, c->m_pad, c->diag);
+  AVD_LAUNCHED(c);
+  double* q = c->diag + 4;
+  double* y = q + c->m_pad;
+  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(m, 8), 4LL * c->num_sms);
+  double h[4] = {0, 0, 0, 0};
+  int it = 0;
+  for (int blk = 0; blk < 16; ++blk) {
+    for (int t = 0; t < 4; ++t, ++it) {
+      power_u_kernel<<<grid, 256, 0, c->stream>>>(c->G32, c->m_pad, c->mu, m, (double)c->cfg.l_global, q, y);
+      AVD_LAUNCHED(c);
+      std::swap(q, y);  // q now holds the unnormalised product
+    }
+    power_u_kernel<<<grid, 256, 0, c->stream>>>(c->G32, c->m_pad, c->mu, m, (double)c->cfg.l_global, q, y);
+    AVD_LAUNCHED(c);
+    power_u_stats_kernel<<<1, 256, 0, c->stream>>>(c->mu, m, q, y, c->diag);
+    AVD_LAUNCHED(c);
+    AVD_CUDA(cudaMemcpyAsync(h, c->diag, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    AVD_CUDA(cudaStreamSynchronize(c->stream));
+    if (!(h[0] > 0.0) || h[2] <= 1e-8) break;
+  }
+  c->iters_u = it;
+  c->sigma1_u = std::sqrt(std::max(h[1], 0.0));
+  c->alpha1 = std::fabs(h[3]);
+  c->cos_mu_v1 = h[0] > 0.0 ? std::min(1.0, std::fabs(h[3]) / h[0]) : 0.0;
+  c->resid_u = h[2];
+  return AVD_OK;
 }
 
 }  // namespace avd

@@ -150,15 +150,50 @@ __global__ void project_reduce_kernel(const double* __restrict__ en_part, const 
   if (threadIdx.x == 0) energy[o] = sh[0];
 }
 
+// p_i = x_i . mu_hat = P[i][k] + ||mu||: counts of p_i > 0 and p_i < 0 added to
+// cnt[0], cnt[1] as integer-valued doubles (exact, order-free; exchanged with the energies)
+__global__ void sign_count_kernel(const float* __restrict__ P, int64_t l, int kpad, int k,
+                                  const double* __restrict__ diag, double* __restrict__ cnt) {
+  __shared__ unsigned int sp, sn;
+  if (threadIdx.x == 0) { sp = 0; sn = 0; }
+  __syncthreads();
+  const double nrm = diag[0];
+  unsigned int pos = 0, neg = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < l; i += (int64_t)gridDim.x * blockDim.x) {
+    const double p = (double)P[i * kpad + k] + nrm;
+    pos += p > 0.0 ? 1u : 0u;
+    neg += p < 0.0 ? 1u : 0u;
+  }
+  if (nrm > 0.0) {
+    atomicAdd(&sp, pos);
+    atomicAdd(&sn, neg);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && (sp || sn)) {
+    atomicAdd(&cnt[0], (double)sp);
+    atomicAdd(&cnt[1], (double)sn);
+  }
+}
+
 }  // namespace
 
+avd_status launch_sign_count(Ctx* c) {
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(c->cfg.l_local, 256), 2LL * c->num_sms));
+  sign_count_kernel<<<grid, 256, 0, c->stream>>>(c->P, c->cfg.l_local, c->k_pad, c->k, c->diag,
+                                                 c->energy + 4 + c->k_pad);
+  AVD_LAUNCHED(c);
+  return AVD_OK;
+}
+
 avd_status launch_project(Ctx* c, const float* X) {
+  AVD_CUDA(cudaMemsetAsync(c->energy + 4 + c->k_pad, 0, 2 * sizeof(double), c->stream));
+  c->sign_valid = project_tc_supported(c, X);
   if (project_tc_supported(c, X)) {
     AVD_TRY(launch_project_tc(c, X));
     project_reduce_kernel<<<4 + c->k_pad, 256, 0, c->stream>>>(c->en_part, c->colsumP_part, c->n_proj_ctas, c->k_pad,
                                                                 c->energy);
     AVD_LAUNCHED(c);
-    return AVD_OK;
+    return launch_sign_count(c);  // P[:, k] = xc . mu_hat (split_v_kernel)
   }
   const unsigned grid = (unsigned)c->n_proj_ctas;
   switch (c->k_pad / 16) {

@@ -37,7 +37,13 @@ __device__ __forceinline__ float rna_tf32(float x) {
 
 // fp64 V (m x k, row-major) -> Vt_hl [2*KP][m_pad32] (hi rows then lo rows) and
 // V_hl [2][m_pad128][KP32] (hi plane then lo plane); padding is zero.
-__global__ void split_v_kernel(const double* __restrict__ V, int64_t m, int k, int KP, int KP32, int64_t m_pad32,
+// fp64 V (m x k, row-major) -> Vt_hl [2*KP][m_pad32] (hi rows then lo rows) and
+// V_hl [2][m_pad128][KP32] (hi plane then lo plane); padding is zero.  Column k of Vt_hl (K5's B
+// operand only) carries the mean direction mu / ||mu||, so P[:, k] = xc_i . mu_hat and
+// p_i = x_i . mu_hat = P[i][k] + ||mu|| come with the projection for free; V_hl
+// (K8's B operand) keeps a zero there, so the spike S = P V_k^T is unaffected.
+__global__ void split_v_kernel(const double* __restrict__ V, const double* __restrict__ mu,
+                               const double* __restrict__ diag, int64_t m, int k, int KP, int KP32, int64_t m_pad32,
                                int64_t m_pad128, float* __restrict__ Vt_hl, float* __restrict__ V_hl) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= m_pad128 * KP32) return;
@@ -48,8 +54,11 @@ __global__ void split_v_kernel(const double* __restrict__ V, int64_t m, int k, i
   V_hl[j * KP32 + r] = hi;
   V_hl[(m_pad128 + j) * KP32 + r] = lo;
   if (r < KP && j < m_pad32) {
-    Vt_hl[(int64_t)r * m_pad32 + j] = hi;
-    Vt_hl[(int64_t)(KP + r) * m_pad32 + j] = lo;
+    float vt = v;
+    if (r == k) vt = (j < m && diag[0] > 0.0) ? (float)(mu[j] / diag[0]) : 0.f;
+    const float th = rna_tf32(vt), tl = rna_tf32(vt - th);
+    Vt_hl[(int64_t)r * m_pad32 + j] = th;
+    Vt_hl[(int64_t)(KP + r) * m_pad32 + j] = tl;
   }
 }
 
@@ -488,8 +497,8 @@ bool project_tc_supported(const Ctx* c, const float* X) {
 avd_status launch_split_v(Ctx* c) {
   const int KP32 = (c->k_pad + 31) / 32 * 32;
   const int64_t n = c->m_pad * KP32;
-  split_v_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c->stream>>>(c->V, c->cfg.m, c->k, c->k_pad, KP32, c->m_pad32,
-                                                                    c->m_pad, c->Vt_hl, c->V_hl);
+  split_v_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c->stream>>>(c->V, c->mu, c->diag, c->cfg.m, c->k, c->k_pad,
+                                                                    KP32, c->m_pad32, c->m_pad, c->Vt_hl, c->V_hl);
   AVD_LAUNCHED(c);
   return AVD_OK;
 }

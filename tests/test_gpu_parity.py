@@ -182,3 +182,19 @@ def test_requantise_on_unsampled_outlier(cuda_device):
     np.testing.assert_allclose(g2["sigma"], o["sigma"], rtol=1e-3)
     X2 = generate(SynthSpec(65536, 128, seed=13, f_mean=0.8))
     assert _gpu(X2)["res"].requantised == 0
+
+
+@pytest.mark.parametrize("l,m,seed,f_mean", [(512, 256, 0, 0.9), (3000, 300, 1, 0.8), (4096, 512, 4, 0.3)])
+def test_mean_diagnostics_parity(cuda_device, l, m, seed, f_mean):
+    """Mean-bias diagnostics against the oracle: R, the p_i sign
+    counts, and the uncentred top singular pair (sigma_1, alpha_1, cos(mu_hat, v_1))."""
+    X = generate(SynthSpec(l, m, seed=seed, f_mean=f_mean))
+    d = O.mean_diagnostics(X.numpy())
+    r = _gpu(X)["res"]
+    assert abs(r.mean_R - d["R"]) <= 1e-9 * d["R"]
+    p = X.numpy().astype(np.float64) @ (np.asarray(O.column_mean(X.numpy())) / d["mu_norm"])
+    near = int(np.count_nonzero(np.abs(p) <= 1e-5 * np.abs(X.numpy()).max() * np.sqrt(m)))
+    assert abs(r.sign_fraction - d["sign_fraction"]) <= near / l + 1e-15
+    assert abs(r.sigma1_u - d["sigma1_u"]) <= 1e-5 * d["sigma1_u"]
+    assert abs(r.alpha1 - d["alpha1"]) <= 1e-5 * d["alpha1"]
+    assert abs(r.cos_mu_v1 - d["cos_mu_v1"]) <= 1e-5

@@ -285,3 +285,63 @@ def test_generator_shard_invariant_and_deterministic():
     assert torch.equal(X, Y)
     assert torch.equal(X, generate(spec))
     assert not torch.equal(X, generate(SynthSpec(300, 70, seed=12)))
+
+
+# ---- mean-bias diagnostics -----------------------
+def test_mean_diagnostics_worked_2x2():
+    """X = [[1,2],[3,4]] by hand: mu = (2,3), ||X||^2 = 30, X^T X = [[10,14],[14,20]] with
+    eigenvalues 15 +- sqrt(221); p = X mu_hat = (8, 18)/sqrt(13) > 0."""
+    d = O.mean_diagnostics(np.array([[1, 2], [3, 4]], np.float32))
+    lam1 = 15 + math.sqrt(221)
+    v1 = np.array([14.0, lam1 - 10.0])
+    v1 /= np.linalg.norm(v1)
+    mu = np.array([2.0, 3.0])
+    assert d["p_pos"] == 2 and d["p_neg"] == 0 and d["sign_fraction"] == 1.0
+    assert abs(d["R"] - math.sqrt(13) / math.sqrt(15)) < 1e-14
+    assert abs(d["sigma1_u"] - math.sqrt(lam1)) < 1e-12
+    assert abs(d["alpha1"] - mu @ v1) < 1e-12
+    assert abs(d["cos_mu_v1"] - (mu @ v1) / math.sqrt(13)) < 1e-12
+
+
+@pytest.mark.parametrize("l,m,rank", [(256, 64, 2), (512, 128, 3)])
+def test_mean_diagnostics_planted_constant_mean(l, m, rank):
+    """X = 1 c 1^T + sum_r c_r h(a_r, .) h(b_r, .)^T with Walsh codes a_r, b_r != 0: every spike
+    direction is orthogonal to 1 (the mean direction), so X^T X = l c^2 1 1^T + sum_r sigma_r^2
+    v_r v_r^T exactly: v_1 = mu_hat when l m c^2 > sigma_r^2, cos = 1, sigma_1 = c sqrt(l m),
+    alpha_1 = ||mu|| = c sqrt(m); p_i = ||mu|| for every row (sign fraction 1); closed-form R."""
+    c = 0.75
+    ii, jj = torch.arange(l), torch.arange(m)
+    X = torch.full((l, m), c, dtype=torch.float64)
+    sig2 = 0.0
+    for r in range(rank):
+        cr = 0.125 * (r + 1)
+        X += cr * torch.outer(walsh(r + 1, ii), walsh(2 * r + 3, jj))
+        sig2 += cr * cr * l * m
+    d = O.mean_diagnostics(X.float().numpy())
+    assert d["sign_fraction"] == 1.0 and d["p_pos"] == l
+    assert abs(d["cos_mu_v1"] - 1.0) < 1e-12
+    assert abs(d["sigma1_u"] - c * math.sqrt(l * m)) < 1e-9 * c * math.sqrt(l * m)
+    assert abs(d["alpha1"] - c * math.sqrt(m)) < 1e-12 * m
+    assert abs(d["R"] - c * math.sqrt(m) / math.sqrt((l * m * c * c + sig2) / l)) < 1e-12
+
+
+def test_mean_diagnostics_vs_numpy_svd():
+    """Library routine: numpy's SVD of the uncentred X gives sigma_1 and v_1."""
+    rng = np.random.default_rng(7)
+    X = (rng.standard_normal((300, 40)) + rng.standard_normal(40) * 3).astype(np.float32)
+    d = O.mean_diagnostics(X)
+    U, S, Vt = np.linalg.svd(X.astype(np.float64), full_matrices=False)
+    mu = X.astype(np.float64).mean(0)
+    assert abs(d["sigma1_u"] - S[0]) < 1e-10 * S[0]
+    assert abs(d["cos_mu_v1"] - abs(mu @ Vt[0]) / np.linalg.norm(mu)) < 1e-10
+    assert abs(d["alpha1"] - abs(S[0] / 300 * U[:, 0].sum())) < 1e-10 * d["alpha1"]
+    p = X.astype(np.float64) @ (mu / np.linalg.norm(mu))  # brute force
+    assert d["p_pos"] == int((p > 0).sum()) and d["p_neg"] == int((p < 0).sum())
+
+
+def test_mean_diagnostics_zero_mean():
+    """Exactly zero column means: no mean direction -> sign fraction 0, cos 0, R 0 (R19)."""
+    ii, jj = torch.arange(64), torch.arange(16)
+    X = torch.outer(walsh(3, ii), walsh(5, jj)).float().numpy()
+    d = O.mean_diagnostics(X)
+    assert d["mu_norm"] == 0.0 and d["sign_fraction"] == 0.0 and d["cos_mu_v1"] == 0.0 and d["R"] == 0.0
