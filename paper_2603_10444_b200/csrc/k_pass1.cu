@@ -112,35 +112,35 @@ __global__ void __launch_bounds__(kT) sample_kernel(const float* __restrict__ X,
     if (sh[b]) atomicAdd(&hist1[b], (unsigned long long)sh[b]);
 }
 
-// fixed-order reduction of the sample partials -> samp[0..m) column sums, samp[m] = #rows
-__global__ void sample_reduce_kernel(int64_t m, int r1, double n_rows, const double* __restrict__ colsum_part,
-                                     const float* __restrict__ colmax_part, const float* __restrict__ colmin_part,
-                                     double* __restrict__ samp, float* __restrict__ smax, float* __restrict__ smin) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j < m) {
-    // 8 independent chains (fixed combination order: deterministic)
-    double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    float mx = -FLT_MAX, mn = FLT_MAX;
-    int r = 0;
-    for (; r + 8 <= r1; r += 8) {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        a[u] += colsum_part[(int64_t)(r + u) * m + j];
-        mx = fmaxf(mx, colmax_part[(int64_t)(r + u) * m + j]);
-        mn = fminf(mn, colmin_part[(int64_t)(r + u) * m + j]);
-      }
-    }
-    for (; r < r1; ++r) {
-      a[0] += colsum_part[(int64_t)r * m + j];
+// fixed-order reduction of the sample partials -> samp[0..m) column sums, samp[m] = #rows;
+// CTA = 32 columns x 8 row groups as in pass1_reduce_kernel
+__global__ void __launch_bounds__(256) sample_reduce_kernel(int64_t m, int r1, double n_rows,
+                                                            const double* __restrict__ colsum_part,
+                                                            const float* __restrict__ colmax_part,
+                                                            const float* __restrict__ colmin_part,
+                                                            double* __restrict__ samp, float* __restrict__ smax,
+                                                            float* __restrict__ smin) {
+  __shared__ double s_s[8][32];
+  __shared__ float s_mx[8][32], s_mn[8][32];
+  const int c = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t j = (int64_t)blockIdx.x * 32 + c;
+  double s = 0.0;
+  float mx = -FLT_MAX, mn = FLT_MAX;
+  if (j < m)
+    for (int r = g; r < r1; r += 8) {
+      s += colsum_part[(int64_t)r * m + j];
       mx = fmaxf(mx, colmax_part[(int64_t)r * m + j]);
       mn = fminf(mn, colmin_part[(int64_t)r * m + j]);
     }
-    const double s = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+  s_s[g][c] = s; s_mx[g][c] = mx; s_mn[g][c] = mn;
+  __syncthreads();
+  if (g == 0 && j < m) {
+    for (int h = 1; h < 8; ++h) { s += s_s[h][c]; mx = fmaxf(mx, s_mx[h][c]); mn = fminf(mn, s_mn[h][c]); }
     samp[j] = s;
     smax[j] = mx;
     smin[j] = mn;
   }
-  if (j == 0) samp[m] = n_rows;
+  if (blockIdx.x == 0 && threadIdx.x == 0) samp[m] = n_rows;
 }
 
 // Quantiser parameters from column centres and ranges:
@@ -476,48 +476,43 @@ __global__ void __launch_bounds__(kT, ND == 2 ? 3 : 2) pass1_kernel(
 // Fixed-order reduction of the per-chunk partials -> stats[0..m) colsum, stats[m] sum x^2,
 // stats[m+3] = #columns whose digits overflowed, colmax[j] = max |x - mu0_j| (the exact range
 // about the quantiser centre, for a requant), qsum_local / qerr_local.
+// CTA = 32 columns x 8 row groups (256 threads): thread (g, c) sums the chunks r = g (mod 8) of
+// column j0 + c (coalesced 32-column rows), the 8 group sums are combined in a fixed order.
 template <int ND>
-__global__ void pass1_reduce_kernel(int64_t m, int r1, int nsq, int full, const double* __restrict__ colsum_part,
-                                    const float* __restrict__ ymax_part, const double* __restrict__ sq_part,
-                                    const long long* __restrict__ qsum_part, const long long* __restrict__ qsq_part,
-                                    const float* __restrict__ qerr_part,
-                                    const float* __restrict__ qscale, double* __restrict__ stats,
-                                    float* __restrict__ colmax, long long* __restrict__ qsum_local,
-                                    double* __restrict__ qerr_local) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) pass1_reduce_kernel(
+    int64_t m, int r1, int nsq, int full, const double* __restrict__ colsum_part, const float* __restrict__ ymax_part,
+    const double* __restrict__ sq_part, const long long* __restrict__ qsum_part, const long long* __restrict__ qsq_part,
+    const float* __restrict__ qerr_part, const float* __restrict__ qscale, double* __restrict__ stats,
+    float* __restrict__ colmax, long long* __restrict__ qsum_local, double* __restrict__ qerr_local) {
+  __shared__ long long s_qs[8][32], s_qq[8][32];
+  __shared__ double s_qe[8][32], s_cs[8][32];
+  __shared__ float s_ym[8][32];
+  const int c = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t j = (int64_t)blockIdx.x * 32 + c;
+  long long qs = 0, qq = 0;
+  double qe = 0.0, cs = 0.0;
+  float ym = 0.f;
   if (j < m) {
-    long long qs = 0, qq = 0;
-    double e8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    float ym = 0.f;
-    int r = 0;
-    for (; r + 8 <= r1; r += 8) {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        qs += qsum_part[(int64_t)(r + u) * m + j];
-        qq += qsq_part[(int64_t)(r + u) * m + j];
-        e8[u] += (double)qerr_part[(int64_t)(r + u) * m + j];
-        ym = fmaxf(ym, ymax_part[(int64_t)(r + u) * m + j]);
-      }
+    for (int r = g; r < r1; r += 8) {
+      const int64_t o = (int64_t)r * m + j;
+      qs += qsum_part[o];
+      qq += qsq_part[o];
+      qe += (double)qerr_part[o];
+      ym = fmaxf(ym, ymax_part[o]);
+      if (full) cs += colsum_part[o];
     }
-    for (; r < r1; ++r) {
-      qs += qsum_part[(int64_t)r * m + j];
-      qq += qsq_part[(int64_t)r * m + j];
-      e8[0] += (double)qerr_part[(int64_t)r * m + j];
-      ym = fmaxf(ym, ymax_part[(int64_t)r * m + j]);
+  }
+  s_qs[g][c] = qs; s_qq[g][c] = qq; s_qe[g][c] = qe; s_cs[g][c] = cs; s_ym[g][c] = ym;
+  __syncthreads();
+  if (g == 0 && j < m) {
+    for (int h = 1; h < 8; ++h) {
+      qs += s_qs[h][c]; qq += s_qq[h][c]; qe += s_qe[h][c]; cs += s_cs[h][c]; ym = fmaxf(ym, s_ym[h][c]);
     }
-    const double qe = ((e8[0] + e8[1]) + (e8[2] + e8[3])) + ((e8[4] + e8[5]) + (e8[6] + e8[7]));
     qsum_local[j] = qs;
     qsum_local[m + j] = qq;  // [S | sum q^2]
     qerr_local[j] = qe;
     if (full) {
-      double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      int r2 = 0;
-      for (; r2 + 8 <= r1; r2 += 8)
-#pragma unroll
-        for (int u = 0; u < 8; ++u) a[u] += colsum_part[(int64_t)(r2 + u) * m + j];
-      for (; r2 < r1; ++r2) a[0] += colsum_part[(int64_t)r2 * m + j];
-      const double s = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
-      stats[j] = s;
+      stats[j] = cs;
       // exact max |x - mu0_j| (power-of-two scale: exact), the range of a requant; |y| beyond
       // the digit range (top digit outside [-127, 127]) counts as an overflow of column j
       constexpr float kYLim = ND == 2 ? 16319.0f : 2088895.0f;
@@ -604,7 +599,7 @@ avd_status launch_sample(Ctx* c, const float* X) {
     sample_kernel<1><<<grid, kT, 0, c->stream>>>(X, l, m, i0, s, c->cfg.row_offset, n_rows, rpc, c->colsum_part, c->colmax_part,
                                                  c->colmin_part, c->hist1);
   AVD_LAUNCHED(c);
-  sample_reduce_kernel<<<(unsigned)ceil_div(m, 256), 256, 0, c->stream>>>(m, r1, (double)n_rows, c->colsum_part,
+  sample_reduce_kernel<<<(unsigned)ceil_div(m, 32), 256, 0, c->stream>>>(m, r1, (double)n_rows, c->colsum_part,
                                                                          c->colmax_part, c->colmin_part, c->samp,
                                                                          c->smax, c->smin);
   AVD_LAUNCHED(c);
@@ -665,11 +660,11 @@ avd_status launch_pass1(Ctx* c, const float* X, bool full) {
 #undef LAUNCH
   AVD_LAUNCHED(c);
   if (c->nd == 2)
-    pass1_reduce_kernel<2><<<(unsigned)ceil_div(m, 256), 256, 0, c->stream>>>(
+    pass1_reduce_kernel<2><<<(unsigned)ceil_div(m, 32), 256, 0, c->stream>>>(
         m, r1, r1 * ncb, full ? 1 : 0, c->colsum_part, c->colmax_part, c->sq_part, c->qsum_part, c->qsq_part,
         c->qerr_part, c->qscale, c->stats, c->colmax, c->qsum_local, c->qerr_local);
   else
-    pass1_reduce_kernel<3><<<(unsigned)ceil_div(m, 256), 256, 0, c->stream>>>(
+    pass1_reduce_kernel<3><<<(unsigned)ceil_div(m, 32), 256, 0, c->stream>>>(
         m, r1, r1 * ncb, full ? 1 : 0, c->colsum_part, c->colmax_part, c->sq_part, c->qsum_part, c->qsq_part,
         c->qerr_part, c->qscale, c->stats, c->colmax, c->qsum_local, c->qerr_local);
   AVD_LAUNCHED(c);
