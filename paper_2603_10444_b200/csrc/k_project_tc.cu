@@ -198,10 +198,10 @@ __global__ void __launch_bounds__(kPThreads, 1) proj_tc_kernel(
           hs[ch] = make_float4(hv[0], hv[1], hv[2], hv[3]);
           ls[ch] = make_float4(lv[0], lv[1], lv[2], lv[3]);
         }
-        sq += (double)s32;
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&conv_bar[s]);
+        sq += (double)s32;  // off the MMA's critical path (after the stage is handed over)
       }
       // ---- epilogue: P row = sum of slots (this warp: half of the KP columns)
       mbar_wait(&tfull_bar, ui & 1);
@@ -461,7 +461,7 @@ CUresult encode2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t o
 template <int KP>
 avd_status launch_k5(Ctx* c, const CUtensorMap& tmX, const CUtensorMap& tmVt, int grid) {
   constexpr uint32_t kStage = 2 * kTile + ((2 * KP * 128 + 1023) / 1024) * 1024;
-  constexpr int NS = (200 * 1024) / kStage;  // 4-5 stages in flight
+  constexpr int NS = (220 * 1024) / kStage;  // 5 stages in flight
   const size_t smem = NS * kStage + 1024;
   AVD_CUDA(cudaFuncSetAttribute(proj_tc_kernel<KP, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   proj_tc_kernel<KP, NS><<<grid, kPThreads, smem, c->stream>>>(tmX, tmVt, c->cfg.l_local, c->cfg.m, c->mu_hl,
@@ -475,7 +475,7 @@ template <int KP32, int NCOL>
 avd_status launch_k8(Ctx* c, const CUtensorMap& tmP, const CUtensorMap& tmV, const CUtensorMap& tmX, int grid) {
   constexpr uint32_t kA = 2 * (KP32 / 32) * kTile;
   constexpr uint32_t kStage = 2 * (KP32 / 32) * NCOL * 128 + (NCOL / 32) * kTile;
-  constexpr int NSF = (int)((200u * 1024u - kA) / kStage);
+  constexpr int NSF = (int)((220u * 1024u - kA) / kStage);
   constexpr int NS = NSF > 6 ? 6 : (NSF < 2 ? 2 : NSF);
   const size_t smem = kA + NS * kStage + 1024;
   AVD_CUDA(cudaFuncSetAttribute(energy_tc_kernel<KP32, NCOL, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
