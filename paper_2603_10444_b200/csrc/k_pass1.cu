@@ -227,14 +227,15 @@ __device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
 // not recomputed.
 template <int ND, int VEC, bool FULL, bool SMEM>
 __device__ __forceinline__ void pass1_rows(int nrows, const float* __restrict__ xp, const float4* xs, int64_t m, int8_t* __restrict__ dp,
-                                           int64_t plane, int64_t m_pad, uint32_t srow0, const float* sc,
+                                           int64_t plane, int64_t m_pad, uint32_t srow0, uint32_t kd, const float* sc,
                                            const float* off, const uint32_t* colh, uint32_t klo, uint32_t kspan,
                                            uint64_t lin0, int lane, uint32_t* __restrict__ cand_key,
                                            uint64_t* __restrict__ cand_idx, unsigned long long* __restrict__ cand_cnt,
-                                           int64_t cand_cap, double* s, double& sq, int* qs32, long long* qs64,
-                                           long long* qq, float* es, float* ym, bool active, bool writer) {
+                                           int64_t cand_cap, double* s, double& sq,
+                                           std::conditional_t<ND == 2, int, long long>* ws, long long* ww, float* es, float* ym, bool active, bool writer) {
   constexpr int U = 4;
   constexpr int DB = ND == 2 ? 9 : 2;  // dither grid bits (see below)
+  constexpr int kW0 = ND == 2 ? 64 : 64 + 64 * 128;
   float x[U][VEC];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
@@ -249,52 +250,71 @@ __device__ __forceinline__ void pass1_rows(int nrows, const float* __restrict__ 
       x[u][0] = ok ? __ldcs(xp + u * m) : 0.f;
     }
   }
-  uint32_t kmax = 0;
+  // kd = 1.0f | (1 << (22 - DB)) (the exponent and the half-step of the dither grid) arrives as a
+  // kernel argument so the mask-and-or below is one LOP3 (two immediates do not fit one)
+  float kmax = 0.f;
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     if (u >= nrows) break;
     const uint32_t srow = srow0 + (uint32_t)u * 0x9E3779B1u;
-    int dg[ND][VEC];
+    int w[VEC];
 #pragma unroll
     for (int v = 0; v < VEC; ++v) {
-      // dithered rounding: q = rint(y + d), y = (x - mu0) 2^shift, d uniform on the symmetric grid
-      // (k + 1/2) 2^-DB - 1/2, k < 2^DB: y + d is exact in fp32 for integer y (|y| < 2^(7nd)), so
+      // dithered rounding: q = floor(y + u) with u = (k + 1/2) 2^-DB uniform, k < 2^DB (unbiased
+      // stochastic rounding), taken as floor(y + D) - 1 with D = 1 + u built from hash bits;
+      // y = (x - mu0) 2^shift.  y + D is exact in fp32 for integer y (|y| < 2^(7nd) - 2), so
       // exactly representable data stays exact (tests/test_gpu_parity.py planted case)
-      const uint32_t h = (srow ^ colh[v]) * 0x85EBCA6Bu;
-      const float d = __uint_as_float(0x3F800000u | ((h >> (32 - DB)) << (23 - DB)) | (1u << (22 - DB))) - 1.5f;
+      // DB bits from the high word of a 32 x 32 multiplicative hash, in place at mantissa bits
+      // 22 .. 23 - DB
+      const uint32_t h = __umulhi(srow ^ colh[v], 0x85EBCA6Bu);
+      const float D = __uint_as_float((h & (((1u << DB) - 1u) << (23 - DB))) | kd);
       const float y = fmaf(x[u][v], sc[v], off[v]);
-      const float t = (y + d) + 12582912.0f;  // 1.5 * 2^23: RN to an integer
-      int q = __float_as_int(t) - 0x4B400000;
-      const float e = (t - 12582912.0f) - y;  // exact: q and y share the fp32 grid
+      const float t = __fadd_rd(y + D, 12582912.0f);  // 1.5 * 2^23 + floor(y + D)
+      // w = q + kW0 (kW0 = 64 sum_{i < nd-1} 128^i): every digit is a plain bit field of w
+      w[v] = __float_as_int(t) - (0x4B400000 + 1 - kW0);
+      const float e = (t - 12582913.0f) - y;  // q - y
       es[v] = fmaf(e, e, es[v]);
       ym[v] = fmaxf(ym[v], fabsf(y));
-      if constexpr (ND == 2) qs32[v] += q; else qs64[v] += q;
-      qq[v] += (long long)q * (long long)q;
-      // balanced base-128 digits, most significant first
-#pragma unroll
-      for (int dd = ND - 1; dd >= 1; --dd) {
-        const int hi = (q + 64) >> 7;
-        dg[dd][v] = q - (hi << 7);
-        q = hi;
-      }
-      dg[0][v] = q;
-      if (FULL) kmax = max(kmax, __float_as_uint(x[u][v]) & 0x7FFFFFFFu);
+      ws[v] += w[v];
+      ww[v] += (long long)w[v] * (long long)w[v];
+      if (FULL) kmax = fmaxf(kmax, fabsf(x[u][v]));
     }
     if (writer) {
+      int8_t* row = dp + u * m_pad;
+      if constexpr (ND == 2 && VEC == 4) {
+        // balanced base-128 digits of q = w - 64, four entries at a time: hi = w >> 7 (bits
+        // 14..7 of w), lo = (w & 127) - 64 (bits 6..0 of w, minus 64 as a byte)
+        const uint32_t A = __byte_perm((uint32_t)w[0], (uint32_t)w[1], 0x5140);
+        const uint32_t B = __byte_perm((uint32_t)w[2], (uint32_t)w[3], 0x5140);
+        const uint32_t P0 = __byte_perm(A, B, 0x5410);  // byte v = bits 7..0 of w[v]
+        const uint32_t P1 = __byte_perm(A, B, 0x7632);  // byte v = bits 15..8 of w[v]
+        const uint32_t hi = ((P1 << 1) & 0xFEFEFEFEu) | ((P0 >> 7) & 0x01010101u);
+        const uint32_t lo = ((P0 & 0x7F7F7F7Fu) | ((P0 << 1) & 0x80808080u)) ^ 0xC0C0C0C0u;
+        __stcs(reinterpret_cast<unsigned int*>(row), hi);
+        __stcs(reinterpret_cast<unsigned int*>(row + plane), lo);
+      } else {
+        // plane 0 = most significant digit w >> 7(nd-1); plane nd-1-i = ((w >> 7i) & 127) - 64
+        int dg[ND][VEC];
 #pragma unroll
-      for (int dd = 0; dd < ND; ++dd) {
-        int8_t* row = dp + dd * plane + u * m_pad;
-        if constexpr (VEC == 4) {
-          __stcs(reinterpret_cast<unsigned int*>(row), pack4(dg[dd][0], dg[dd][1], dg[dd][2], dg[dd][3]));
-        } else {
-          *row = (int8_t)dg[dd][0];
+        for (int v = 0; v < VEC; ++v) {
+          dg[0][v] = w[v] >> (7 * (ND - 1));
+#pragma unroll
+          for (int i = 0; i < ND - 1; ++i) dg[ND - 1 - i][v] = ((w[v] >> (7 * i)) & 127) - 64;
+        }
+#pragma unroll
+        for (int dd = 0; dd < ND; ++dd) {
+          if constexpr (VEC == 4) {
+            __stcs(reinterpret_cast<unsigned int*>(row + dd * plane), pack4(dg[dd][0], dg[dd][1], dg[dd][2], dg[dd][3]));
+          } else {
+            row[dd * plane] = (int8_t)dg[dd][0];
+          }
         }
       }
     }
   }
   if (FULL) {
     // candidates (key in [klo, 0x7F800000)): rare, so only warps that saw one build masks
-    if (__any_sync(0xFFFFFFFFu, kmax >= klo)) {
+    if (__any_sync(0xFFFFFFFFu, __float_as_uint(kmax) >= klo)) {
       uint32_t cmask = 0;
 #pragma unroll
       for (int u = 0; u < U; ++u)
@@ -359,7 +379,8 @@ __device__ __forceinline__ void pass1_rows(int nrows, const float* __restrict__ 
 template <int ND, int VEC, bool FULL>
 __global__ void __launch_bounds__(kT, ND == 2 ? 3 : 2) pass1_kernel(
     const float* __restrict__ X, int64_t l, int64_t m, int64_t m_pad, int64_t l_pad, int64_t rpc, int64_t row_offset,
-    const float* __restrict__ qscale, const float* __restrict__ qoff, uint32_t seed32, int8_t* __restrict__ digits,
+    const float* __restrict__ qscale, const float* __restrict__ qoff, uint32_t seed32, uint32_t kd,
+    int8_t* __restrict__ digits,
     const DevPlan* __restrict__ dplan, uint32_t* __restrict__ cand_key, uint64_t* __restrict__ cand_idx,
     unsigned long long* __restrict__ cand_cnt, int64_t cand_cap, double* __restrict__ colsum_part,
     float* __restrict__ ymax_part, double* __restrict__ sq_part, long long* __restrict__ qsum_part,
@@ -383,17 +404,18 @@ __global__ void __launch_bounds__(kT, ND == 2 ? 3 : 2) pass1_kernel(
     for (int v = 0; v < VEC; ++v) {
       sc[v] = active ? qscale[c0 + v] : 1.f;
       off[v] = active ? qoff[c0 + v] : 0.f;
-      colh[v] = mix32((uint32_t)(c0 + v) ^ 0x68E31DA4u);
+      colh[v] = ((uint32_t)(c0 + v) * 0x2545F491u) ^ 0x68E31DA4u;  // cheap to rematerialise
     }
     // candidate test as one unsigned compare: key in [max(1, b0 << 19), 0x7F800000)
     const uint32_t klo = FULL ? max(1u, (uint32_t)dplan->b0 << 19) : 0xFFFFFFFFu;
     const uint32_t kspan = 0x7F800000u - klo;
     double s[VEC];
-    int qs32[VEC];
-    long long qs64[VEC], qq[VEC];
+    // sums of w = q + kW0 and of w^2 (the digit offset; removed below)
+    std::conditional_t<ND == 2, int, long long> ws[VEC];
+    long long ww[VEC];
     float es[VEC], ym[VEC];
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) { s[v] = 0.0; qs32[v] = 0; qs64[v] = 0; qq[v] = 0; es[v] = 0.f; ym[v] = 0.f; }
+    for (int v = 0; v < VEC; ++v) { s[v] = 0.0; ws[v] = 0; ww[v] = 0; es[v] = 0.f; ym[v] = 0.f; }
     const float* xp = X + r0 * m + (active ? c0 : 0);
     int8_t* dp = digits + r0 * m_pad + cc;
     uint32_t srow0 = (uint32_t)(row_offset + r0) * 0x9E3779B1u + seed32;
@@ -426,8 +448,8 @@ __global__ void __launch_bounds__(kT, ND == 2 ? 3 : 2) pass1_kernel(
         asm volatile("cp.async.wait_group %0;" ::"n"(kNStg - 1) : "memory");
         const int nrows = (int)min((int64_t)U, r1 - (r0 + (int64_t)g * U));
         pass1_rows<ND, VEC, FULL, true>(nrows, xp, &xring[((g % kNStg) * U) * kT + threadIdx.x], m, dp, plane, m_pad,
-                                        srow0, sc, off, colh, klo, kspan, lin0, lane, cand_key, cand_idx, cand_cnt,
-                                        cand_cap, s, sq, qs32, qs64, qq, es, ym, active, writer);
+                                        srow0, kd, sc, off, colh, klo, kspan, lin0, lane, cand_key, cand_idx, cand_cnt,
+                                        cand_cap, s, sq, ws, ww, es, ym, active, writer);
         dp += U * m_pad;
         srow0 += (uint32_t)U * 0x9E3779B1u;
         lin0 += (uint64_t)U * (uint64_t)m;
@@ -436,8 +458,8 @@ __global__ void __launch_bounds__(kT, ND == 2 ? 3 : 2) pass1_kernel(
     } else {
       int64_t i = r0;
       for (; i + U <= r1; i += U) {
-        pass1_rows<ND, VEC, FULL, false>(U, xp, nullptr, m, dp, plane, m_pad, srow0, sc, off, colh, klo, kspan, lin0,
-                                         lane, cand_key, cand_idx, cand_cnt, cand_cap, s, sq, qs32, qs64, qq, es, ym,
+        pass1_rows<ND, VEC, FULL, false>(U, xp, nullptr, m, dp, plane, m_pad, srow0, kd, sc, off, colh, klo, kspan, lin0,
+                                         lane, cand_key, cand_idx, cand_cnt, cand_cap, s, sq, ws, ww, es, ym,
                                          active, writer);
         xp += U * m;
         dp += U * m_pad;
@@ -445,16 +467,18 @@ __global__ void __launch_bounds__(kT, ND == 2 ? 3 : 2) pass1_kernel(
         lin0 += (uint64_t)U * (uint64_t)m;
       }
       if (i < r1)
-        pass1_rows<ND, VEC, FULL, false>((int)(r1 - i), xp, nullptr, m, dp, plane, m_pad, srow0, sc, off, colh, klo,
-                                         kspan, lin0, lane, cand_key, cand_idx, cand_cnt, cand_cap, s, sq, qs32, qs64,
-                                         qq, es, ym, active, writer);
+        pass1_rows<ND, VEC, FULL, false>((int)(r1 - i), xp, nullptr, m, dp, plane, m_pad, srow0, kd, sc, off, colh, klo,
+                                         kspan, lin0, lane, cand_key, cand_idx, cand_cnt, cand_cap, s, sq, ws, ww,
+                                         es, ym, active, writer);
     }
     if (active) {
 #pragma unroll
       for (int v = 0; v < VEC; ++v) {
         const int64_t o = (int64_t)blockIdx.y * m + c0 + v;
-        qsum_part[o] = ND == 2 ? (long long)qs32[v] : qs64[v];
-        qsq_part[o] = qq[v];
+        constexpr long long W0 = ND == 2 ? 64 : 64 + 64 * 128;
+        const long long n = r1 - r0, sw = (long long)ws[v];
+        qsum_part[o] = sw - W0 * n;                     // sum q
+        qsq_part[o] = ww[v] - 2 * W0 * sw + W0 * W0 * n;  // sum (w - W0)^2
         qerr_part[o] = es[v];
         ymax_part[o] = ym[v];
         if (FULL) colsum_part[o] = s[v];
@@ -643,11 +667,12 @@ avd_status launch_pass1(Ctx* c, const float* X, bool full) {
                                c->stream));
   dim3 grid(ncb, r1);
   const uint32_t seed32 = dither_seed(c);
+  const uint32_t kd = 0x3F800000u | (1u << (22 - (c->nd == 2 ? 9 : 2)));  // see pass1_rows
   const int ring = VEC == 4 ? kNStg * 4 * kT * 16 : 0;
 #define LAUNCH(ND, V, F)                                                                                        \
   AVD_CUDA(cudaFuncSetAttribute(pass1_kernel<ND, V, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, ring));  \
   pass1_kernel<ND, V, F><<<grid, kT, ring, c->stream>>>(                                                        \
-      X, l, m, c->m_pad, c->l_pad, rpc, c->cfg.row_offset, c->qscale, c->qoff, seed32, c->digits, c->dplan,     \
+      X, l, m, c->m_pad, c->l_pad, rpc, c->cfg.row_offset, c->qscale, c->qoff, seed32, kd, c->digits, c->dplan, \
       c->cand_key, c->cand_idx, c->cand_cnt, c->cand_cap, c->colsum_part, c->colmax_part, c->sq_part,          \
       c->qsum_part, c->qsq_part, c->qerr_part, c->stats)
   if (c->nd == 2) {
