@@ -76,7 +76,8 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   const int ncb = (int)ceil_div(m, 256LL * ((m % 4 == 0) ? 4 : 1));
   C->r1 = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(4LL * C->num_sms, ncb), ceil_div(ll, 4)));
   C->r1 = (int)std::max<int64_t>(C->r1, ceil_div(ll, 65536));  // int32 per-chunk sums of q (k_pass1.cu)
-  C->cand_cap = std::min<int64_t>(ll * m, std::max<int64_t>(4 * n_top, 1 << 20));
+  // + room for the holes of the per-warp slot blocks (k_pass1.cu kCandBlk)
+  C->cand_cap = std::min<int64_t>(ll * m, std::max<int64_t>(4 * n_top, 1 << 20) + (1 << 18));
   C->n_red = (int)ceil_div(m, kRedRowsC);  // partials of the m-length p x p reductions
   C->n_proj_ctas = (int)ceil_div(ll, 32);
   C->nwords = ceil_div(ll * m, 32);
@@ -98,7 +99,7 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   L.add((size_t)nd * C->m_pad * C->l_pad);      // 11 digits
   L.add(sizeof(uint32_t) * C->cand_cap);        // 12 cand_key
   L.add(sizeof(uint64_t) * C->cand_cap);        // 13 cand_idx
-  L.add(sizeof(unsigned long long));            // 14 cand_cnt
+  L.add(2 * sizeof(unsigned long long));        // 14 cand_cnt [slot cursor, real count]
   L.add(sizeof(long long) * C->m_pad * C->m_pad);// 15 gram_i
   L.add(sizeof(double) * C->m_pad * C->m_pad);  // 16 G
   L.add(sizeof(double) * m * p);                // 17 Q

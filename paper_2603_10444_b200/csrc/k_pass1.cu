@@ -27,13 +27,15 @@
 // with the exact column ranges (requant path, same kernel without the statistics).
 #include <cfloat>
 #include "common.cuh"
+#include "sm100.cuh"
 
 namespace avd {
 
 namespace {
+using namespace sm100;
 
 constexpr int kT = 256;  // threads of the streaming kernels
-constexpr int kNStg = 3;  // cp.async ring depth of the fused pass (U = 4 rows x 16 B per thread and stage)
+constexpr int kNStg = 4;  // bulk-copy ring depth of the fused pass (stage = U = 4 rows x kT x 16 B)
 
 __device__ __forceinline__ uint32_t mix32(uint32_t x) {
   x ^= x >> 16;
@@ -225,11 +227,25 @@ __device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
 // reaches the candidate bin does the warp build candidate masks and append them (one scan and
 // one atomic per warp).  Full U-row groups run without bounds checks; pointers are advanced,
 // not recomputed.
+// Candidate slots: each warp owns a block of slots [base, base + cap) of the candidate list,
+// reserved from the global cursor cand_cnt[0]; unused slots of a closed block are holes with
+// key 0 (never a candidate key, skipped by K6).  cand_cnt[1] counts the real candidates.
+constexpr uint32_t kCandBlk = 64;
+struct CandBlk {
+  unsigned long long base;
+  uint32_t used, cap, real, pad;
+};
+__device__ __forceinline__ void close_cand_block(uint32_t* __restrict__ cand_key, int64_t cand_cap,
+                                                 unsigned long long base, uint32_t used, uint32_t cap, int lane) {
+  for (uint32_t t = used + (uint32_t)lane; t < cap; t += 32)
+    if (base + t < (unsigned long long)cand_cap) cand_key[base + t] = 0u;
+}
+
 template <int ND, int VEC, bool FULL, bool SMEM>
 __device__ __forceinline__ void pass1_rows(int nrows, const float* __restrict__ xp, const float4* xs, int64_t m, int8_t* __restrict__ dp,
                                            int64_t plane, int64_t m_pad, uint32_t srow0, uint32_t kd, const float* sc,
                                            const float* off, const uint32_t* colh, uint32_t klo, uint32_t kspan,
-                                           uint64_t lin0, int lane, uint32_t* __restrict__ cand_key,
+                                           uint64_t lin0, int lane, CandBlk* cb, uint32_t* __restrict__ cand_key,
                                            uint64_t* __restrict__ cand_idx, unsigned long long* __restrict__ cand_cnt,
                                            int64_t cand_cap, double* s, double& sq,
                                            std::conditional_t<ND == 2, int, long long>* ws, long long* ww, float* es, float* ym, bool active, bool writer) {
@@ -241,7 +257,7 @@ __device__ __forceinline__ void pass1_rows(int nrows, const float* __restrict__ 
   for (int u = 0; u < U; ++u) {
     const bool ok = active && u < nrows;
     if constexpr (SMEM) {  // prefetched by cp.async (zero-filled past the end)
-      const float4 t = xs[u * kT];
+      const float4 t = u < nrows ? xs[u * kT] : make_float4(0.f, 0.f, 0.f, 0.f);  // tail: stale slot
       x[u][0] = t.x; x[u][1] = t.y; x[u][2] = t.z; x[u][3] = t.w;
     } else if constexpr (VEC == 4) {
       const float4 t = ok ? __ldcs(reinterpret_cast<const float4*>(xp + u * m)) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -314,14 +330,16 @@ __device__ __forceinline__ void pass1_rows(int nrows, const float* __restrict__ 
   }
   if (FULL) {
     // candidates (key in [klo, 0x7F800000)): rare, so only warps that saw one build masks
-    if (__any_sync(0xFFFFFFFFu, __float_as_uint(kmax) >= klo)) {
+    // (as fp32 compares against thr = float(klo): NaN fails them; an infinity passes, but a
+    // non-finite X ends the call with AVD_ENONFINITE before the candidates are used)
+    const float thr = __uint_as_float(klo);
+    if (__any_sync(0xFFFFFFFFu, kmax >= thr)) {
       uint32_t cmask = 0;
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int v = 0; v < VEC; ++v) {
-          const uint32_t key = __float_as_uint(x[u][v]) & 0x7FFFFFFFu;
-          cmask |= (u < nrows && (key - klo) < kspan) ? (1u << (u * VEC + v)) : 0u;
+          if (fabsf(x[u][v]) >= thr) cmask |= 1u << (u * VEC + v);  // rows past the end hold 0
         }
       const uint32_t cnt = __popc(cmask);
       uint32_t incl = cnt;
@@ -331,9 +349,23 @@ __device__ __forceinline__ void pass1_rows(int nrows, const float* __restrict__ 
         if (lane >= o) incl += t;
       }
       const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-      unsigned long long base = 0;
-      if (lane == 31 && total) base = atomicAdd(cand_cnt, (unsigned long long)total);
-      base = __shfl_sync(0xFFFFFFFFu, base, 31) + (incl - cnt);
+      // slots come from this warp's block (reserved from the global cursor kCandBlk at a time);
+      // only a warp whose block runs out goes to the global atomic
+      unsigned long long bbase = cb->base;
+      uint32_t used = cb->used, bcap = cb->cap;
+      if (used + total > bcap) {
+        close_cand_block(cand_key, cand_cap, bbase, used, bcap, lane);
+        const uint32_t want = max((uint32_t)kCandBlk, total);
+        unsigned long long b = 0;
+        if (lane == 0) b = atomicAdd(cand_cnt, (unsigned long long)want);
+        bbase = __shfl_sync(0xFFFFFFFFu, b, 0);
+        used = 0;
+        bcap = want;
+      }
+      unsigned long long base = bbase + used + (incl - cnt);
+      __syncwarp();
+      if (lane == 0) { cb->base = bbase; cb->used = used + total; cb->cap = bcap; cb->real += total; }
+      __syncwarp();
       if constexpr (SMEM) {
         // one step per candidate of this thread; the values are re-read from its ring slot
         const float* xsf = reinterpret_cast<const float*>(xs);
@@ -395,6 +427,21 @@ __global__ void __launch_bounds__(kT, ND == 2 ? 3 : 2) pass1_kernel(
   const bool writer = c0 < m_pad;  // digit columns [m, m_pad) come out zero (x = 0, scale 1, centre 0)
   const int64_t plane = l_pad * m_pad;
   double sq = 0.0;
+  __shared__ CandBlk cblk[kT / 32];
+  CandBlk* cb = &cblk[threadIdx.x >> 5];
+  if (lane == 0) *cb = CandBlk{0ull, 0u, 0u, 0u, 0u};
+  __syncwarp();
+  // VEC == 4: the bulk-copy ring's barriers; empty_bar counts the warps holding a digit column
+  __shared__ __align__(8) uint64_t full_bar[kNStg], empty_bar[kNStg];
+  if constexpr (VEC == 4) {
+    if (threadIdx.x == 0) {
+      const int64_t cols = m_pad - (int64_t)blockIdx.x * kT * 4;  // > 0 for every launched CTA
+      const uint32_t nw = (uint32_t)min((int64_t)kT / 32, ceil_div(cols, (int64_t)128));
+      for (int t = 0; t < kNStg; ++t) { mbar_init(&full_bar[t], 1); mbar_init(&empty_bar[t], nw); }
+      fence_mbar_init();
+    }
+    __syncthreads();
+  }
   // whole warps take part (the candidate append uses warp collectives); lanes past m load nothing
   if (__any_sync(0xFFFFFFFFu, writer)) {
     const int64_t cc = writer ? c0 : 0;
@@ -421,45 +468,50 @@ __global__ void __launch_bounds__(kT, ND == 2 ? 3 : 2) pass1_kernel(
     uint32_t srow0 = (uint32_t)(row_offset + r0) * 0x9E3779B1u + seed32;
     uint64_t lin0 = (uint64_t)(row_offset + r0) * (uint64_t)m + (uint64_t)c0;
     if constexpr (VEC == 4) {
-      // cp.async ring: group g (U rows of this thread's 16 B) lands in stage g % kNStg while the
-      // thread computes on group g - kNStg + 1 (memory-level parallelism without registers)
+      // bulk-copy ring: thread 0 streams group g (U rows x the CTA's kT * 16 B, contiguous in X)
+      // into stage g % kNStg with cp.async.bulk, kNStg - 1 groups ahead; the warps release a
+      // stage through empty_bar once they have computed on it.  Slots of lanes past m are
+      // zeroed once and never written by the copies.
       extern __shared__ __align__(16) float4 xring[];  // [kNStg][U][kT]
       const int ng = (int)ceil_div(r1 - r0, U);
-      auto issue = [&](int g) {
+      const int64_t cblk = (int64_t)blockIdx.x * kT * 4;
+      const uint32_t row_bytes = (uint32_t)max((int64_t)0, min((int64_t)kT * 4, m - cblk)) * 4u;
+      if (!active)
+        for (int t = 0; t < kNStg * U; ++t) xring[t * kT + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
+      auto issue = [&](int g) {  // thread 0
+        const int st = g % kNStg;
         const int64_t i = r0 + (int64_t)g * U;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const bool ok = active && i + u < r1;
-          const float* src = ok ? X + (i + u) * m + c0 : X;
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
-                           (uint32_t)__cvta_generic_to_shared(&xring[((g % kNStg) * U + u) * kT + threadIdx.x])),
-                       "l"(src), "r"(ok ? 16 : 0)
-                       : "memory");
-        }
+        const int nr = (int)min((int64_t)U, r1 - i);
+        mbar_arrive_expect_tx(&full_bar[st], (uint32_t)nr * row_bytes);
+        if (row_bytes)
+          for (int u = 0; u < nr; ++u)
+            bulk_load_1d(&xring[(st * U + u) * kT], X + (i + u) * m + cblk, row_bytes, &full_bar[st]);
       };
-#pragma unroll
-      for (int g = 0; g < kNStg - 1; ++g) {
-        if (g < ng) issue(g);
-        asm volatile("cp.async.commit_group;" ::: "memory");
-      }
+      if (threadIdx.x == 0)
+        for (int g = 0; g < kNStg - 1 && g < ng; ++g) issue(g);
       for (int g = 0; g < ng; ++g) {
-        if (g + kNStg - 1 < ng) issue(g + kNStg - 1);
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        asm volatile("cp.async.wait_group %0;" ::"n"(kNStg - 1) : "memory");
+        const int st = g % kNStg;
+        if (threadIdx.x == 0 && g + kNStg - 1 < ng) {
+          const int gn = g + kNStg - 1;
+          if (gn >= kNStg) mbar_wait_sleep(&empty_bar[gn % kNStg], (uint32_t)((gn / kNStg) - 1) & 1u);
+          issue(gn);
+        }
+        mbar_wait_sleep(&full_bar[st], (uint32_t)(g / kNStg) & 1u);
         const int nrows = (int)min((int64_t)U, r1 - (r0 + (int64_t)g * U));
-        pass1_rows<ND, VEC, FULL, true>(nrows, xp, &xring[((g % kNStg) * U) * kT + threadIdx.x], m, dp, plane, m_pad,
-                                        srow0, kd, sc, off, colh, klo, kspan, lin0, lane, cand_key, cand_idx, cand_cnt,
+        pass1_rows<ND, VEC, FULL, true>(nrows, xp, &xring[(st * U) * kT + threadIdx.x], m, dp, plane, m_pad,
+                                        srow0, kd, sc, off, colh, klo, kspan, lin0, lane, cb, cand_key, cand_idx, cand_cnt,
                                         cand_cap, s, sq, ws, ww, es, ym, active, writer);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[st]);
         dp += U * m_pad;
         srow0 += (uint32_t)U * 0x9E3779B1u;
         lin0 += (uint64_t)U * (uint64_t)m;
       }
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
     } else {
       int64_t i = r0;
       for (; i + U <= r1; i += U) {
         pass1_rows<ND, VEC, FULL, false>(U, xp, nullptr, m, dp, plane, m_pad, srow0, kd, sc, off, colh, klo, kspan, lin0,
-                                         lane, cand_key, cand_idx, cand_cnt, cand_cap, s, sq, ws, ww, es, ym,
+                                         lane, cb, cand_key, cand_idx, cand_cnt, cand_cap, s, sq, ws, ww, es, ym,
                                          active, writer);
         xp += U * m;
         dp += U * m_pad;
@@ -468,8 +520,14 @@ __global__ void __launch_bounds__(kT, ND == 2 ? 3 : 2) pass1_kernel(
       }
       if (i < r1)
         pass1_rows<ND, VEC, FULL, false>((int)(r1 - i), xp, nullptr, m, dp, plane, m_pad, srow0, kd, sc, off, colh, klo,
-                                         kspan, lin0, lane, cand_key, cand_idx, cand_cnt, cand_cap, s, sq, ws, ww,
+                                         kspan, lin0, lane, cb, cand_key, cand_idx, cand_cnt, cand_cap, s, sq, ws, ww,
                                          es, ym, active, writer);
+    }
+    if (FULL) {  // close this warp's candidate block; publish its real count
+      __syncwarp();
+      const CandBlk st = *cb;
+      close_cand_block(cand_key, cand_cap, st.base, st.used, st.cap, lane);
+      if (lane == 0 && st.real) atomicAdd(cand_cnt + 1, (unsigned long long)st.real);
     }
     if (active) {
 #pragma unroll
@@ -582,8 +640,8 @@ __global__ void finish_kernel(int64_t m, int64_t m_pad, int64_t l_global, int64_
 // exchange slot for the global candidate decision: [count, overflowed]
 __global__ void cand_publish_kernel(const unsigned long long* __restrict__ cnt, int64_t cap,
                                     long long* __restrict__ out) {
-  out[0] = (long long)*cnt;
-  out[1] = (long long)(*cnt > (unsigned long long)cap ? 1 : 0);
+  out[0] = (long long)cnt[1];                                   // real candidates
+  out[1] = (long long)(cnt[0] > (unsigned long long)cap ? 1 : 0);  // slots (with holes) past cap
 }
 
 bool vec4(const Ctx* c, const float* X) {
@@ -658,7 +716,7 @@ avd_status launch_pass1(Ctx* c, const float* X, bool full) {
   const int r1 = (int)ceil_div(l, rpc);
   if (full) {
     AVD_CUDA(cudaMemsetAsync(c->stats, 0, sizeof(double) * (m + 4), c->stream));
-    AVD_CUDA(cudaMemsetAsync(c->cand_cnt, 0, sizeof(unsigned long long), c->stream));
+    AVD_CUDA(cudaMemsetAsync(c->cand_cnt, 0, 2 * sizeof(unsigned long long), c->stream));
   }
   // digit-plane rows [l_local, l_pad) are zero (the Gram sums over them)
   if (c->l_pad > l)

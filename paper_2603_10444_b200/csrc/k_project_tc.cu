@@ -179,9 +179,10 @@ __global__ void __launch_bounds__(kPThreads, 1) proj_tc_kernel(
         const float4* xs = reinterpret_cast<const float4*>(st);
         float4* hs = reinterpret_cast<float4*>(st);          // hi overwrites x in place
         float4* ls = reinterpret_cast<float4*>(st + kTile);
-        float s32 = 0.f;
+        float s32u[4];  // one partial per u: four short FFMA chains instead of one of 16
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
+          float s32 = 0.f;
           const int ch = ct + 256 * u;  // 16-byte chunk index in the tile
           const bool rok = row0 + rbase + 32 * u < l_local;
           const float4 x = xs[ch];
@@ -197,7 +198,9 @@ __global__ void __launch_bounds__(kPThreads, 1) proj_tc_kernel(
           }
           hs[ch] = make_float4(hv[0], hv[1], hv[2], hv[3]);
           ls[ch] = make_float4(lv[0], lv[1], lv[2], lv[3]);
+          s32u[u] = s32;
         }
+        const float s32 = (s32u[0] + s32u[1]) + (s32u[2] + s32u[3]);
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&conv_bar[s]);
@@ -408,16 +411,26 @@ __global__ void __launch_bounds__(kPThreads, 1) energy_tc_kernel(
             xv[4 * u] = v.x; xv[4 * u + 1] = v.y; xv[4 * u + 2] = v.z; xv[4 * u + 3] = v.w;
           }
           tmem_ld_wait();
+          float s2b = 0.f, t2b = 0.f, stb = 0.f;  // two chains per sum (even / odd t)
 #pragma unroll
-          for (int t = 0; t < 16; ++t) {
-            const bool ok = rok && j0 + t < m;
-            const float xc = (xv[t] - mh[t]) - ml[t];
-            const float S = ok ? __uint_as_float(rv[t]) : 0.f;
-            const float T = ok ? xc - S : 0.f;
-            s2 = fmaf(S, S, s2);
-            t2 = fmaf(T, T, t2);
-            st = fmaf(S, T, st);
+          for (int t = 0; t < 16; t += 2) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const bool ok = rok && j0 + t + e < m;
+              const float xc = (xv[t + e] - mh[t + e]) - ml[t + e];
+              const float S = ok ? __uint_as_float(rv[t + e]) : 0.f;
+              const float T = ok ? xc - S : 0.f;
+              float& a2 = e ? s2b : s2;
+              float& b2 = e ? t2b : t2;
+              float& c2 = e ? stb : st;
+              a2 = fmaf(S, S, a2);
+              b2 = fmaf(T, T, b2);
+              c2 = fmaf(S, T, c2);
+            }
           }
+          s2 += s2b;
+          t2 += t2b;
+          st += stb;
         }
         eS += (double)s2;
         eT += (double)t2;

@@ -31,6 +31,7 @@ __device__ __forceinline__ bool fetch(int64_t t, const uint32_t* __restrict__ ck
     return key != 0 && key < 0x7F800000u;
   } else {
     key = ckey[t];
+    if (key == 0) return false;  // a hole of a K2 slot block
     lidx = cidx[t] - (uint64_t)base;
     return true;
   }
