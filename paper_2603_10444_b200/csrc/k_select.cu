@@ -219,11 +219,27 @@ __global__ void __launch_bounds__(1024) blk_scan_kernel(int64_t* __restrict__ bl
   int64_t sel_total = 0;
   for (int which = 0; which < 2; ++which) {
     int64_t* a = blk + which * nblk;
+    // the run is read in batches of 8 independent loads (one latency per batch, not per block)
     int64_t run = 0;
-    for (int64_t i = b0; i < b1; ++i) run += a[i];
+    int64_t i = b0;
+    for (; i + 8 <= b1; i += 8) {
+      int64_t v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = a[i + u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) run += v[u];
+    }
+    for (; i < b1; ++i) run += a[i];
     int64_t total;
     int64_t acc = block_exclusive_scan<int64_t, 1024>(run, wt, total);
-    for (int64_t i = b0; i < b1; ++i) {
+    for (i = b0; i + 8 <= b1; i += 8) {
+      int64_t v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = a[i + u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { a[i + u] = acc; acc += v[u]; }
+    }
+    for (; i < b1; ++i) {
       const int64_t v = a[i];
       a[i] = acc;
       acc += v;
