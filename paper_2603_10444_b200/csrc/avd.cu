@@ -216,6 +216,28 @@ __global__ void copy_outputs_kernel(const double* __restrict__ mu, const double*
   if (sigma_o && t < k) sigma_o[t] = sigma[t];
 }
 
+// gather the report's scalars into one contiguous block (one D2H copy instead of nine):
+// [0,5) report, [8,16) agg, [16,20) energy, 20 sum x^2, 21 trace, [22,24) sign counts,
+// 24 ||mu||, [32, 32+k) sigma, then the DevPlan words
+constexpr int kPackHead = 32;
+constexpr int kPlanWords = (int)((sizeof(DevPlan) + 7) / 8);
+__global__ void report_pack_kernel(const double* __restrict__ report, const double* __restrict__ agg,
+                                   const double* __restrict__ energy, const double* __restrict__ stats,
+                                   const double* __restrict__ trace, const double* __restrict__ diag,
+                                   const double* __restrict__ sigma, const DevPlan* __restrict__ dp, int64_t m,
+                                   int k, int k_pad, double* __restrict__ pack) {
+  const int t = threadIdx.x;
+  if (t < 5) pack[t] = report[t];
+  if (t < 8) pack[8 + t] = agg[t];
+  if (t < 4) pack[16 + t] = energy[t];
+  if (t == 0) { pack[20] = stats[m]; pack[21] = trace[0]; pack[24] = diag[0]; }
+  if (t < 2) pack[22 + t] = energy[4 + k_pad + t];
+  for (int r = t; r < k; r += blockDim.x) pack[kPackHead + r] = sigma[r];
+  const unsigned long long* pw = reinterpret_cast<const unsigned long long*>(dp);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(pack + kPackHead + k);
+  if (t < (int)(sizeof(DevPlan) / 8)) dst[t] = pw[t];
+}
+
 }  // namespace
 }  // namespace avd
 
@@ -482,20 +504,17 @@ avd_status avd_stage_report(avd_ctx* c, avd_outputs* out) {
         c->mu, c->V, c->sigma, m, k, out->mu_dev, out->V_dev, out->sigma_dev);
     AVD_LAUNCHED(c);
   }
-  double h[64];
-  const int kp = c->k_pad;
-  AVD_CUDA(cudaMemcpyAsync(h, c->report, sizeof(double) * 5, cudaMemcpyDeviceToHost, c->stream));
-  AVD_CUDA(cudaMemcpyAsync(h + 8, c->agg, sizeof(double) * 8, cudaMemcpyDeviceToHost, c->stream));
-  AVD_CUDA(cudaMemcpyAsync(h + 16, c->energy, sizeof(double) * 4, cudaMemcpyDeviceToHost, c->stream));
-  AVD_CUDA(cudaMemcpyAsync(h + 20, c->stats + m, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  AVD_CUDA(cudaMemcpyAsync(h + 21, c->trace, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  AVD_CUDA(cudaMemcpyAsync(h + 22, c->energy + 4 + c->k_pad, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  AVD_CUDA(cudaMemcpyAsync(h + 24, c->diag, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  std::vector<double> sig(k);
-  AVD_CUDA(cudaMemcpyAsync(sig.data(), c->sigma, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
-  AVD_CUDA(cudaMemcpyAsync(&c->hplan, c->dplan, sizeof(DevPlan), cudaMemcpyDeviceToHost, c->stream));
+  // one packed D2H copy (pageable copies cost ~10 us each); the tail of the eig scratch is free
+  const int64_t npack = kPackHead + k + kPlanWords;
+  double* pack = c->red_part + ((int64_t)c->n_red * c->p * c->p - npack);
+  report_pack_kernel<<<1, 128, 0, c->stream>>>(c->report, c->agg, c->energy, c->stats, c->trace, c->diag, c->sigma,
+                                               c->dplan, m, k, c->k_pad, pack);
+  AVD_LAUNCHED(c);
+  std::vector<double> h((size_t)npack);
+  AVD_CUDA(cudaMemcpyAsync(h.data(), pack, sizeof(double) * npack, cudaMemcpyDeviceToHost, c->stream));
   AVD_CUDA(cudaStreamSynchronize(c->stream));
-  (void)kp;
+  std::memcpy(&c->hplan, h.data() + kPackHead + k, sizeof(DevPlan));
+  const double* sig = h.data() + kPackHead;
   double spike = 0.0;
   for (int r = 0; r < k; ++r) spike += sig[r] * sig[r];
   const double total = h[20], trace = h[21];
