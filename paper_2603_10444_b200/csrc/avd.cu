@@ -426,10 +426,12 @@ avd_status avd_stage_gram(avd_ctx* c, const float* X) {
   STAGE_CHECK(c, 2);
   if (!X) { set_error("null argument"); return AVD_EINVAL; }
   AVD_TRY(launch_finish(c));
-  double ovf = 0.0;
-  AVD_CUDA(cudaMemcpyAsync(&c->hplan, c->dplan, sizeof(DevPlan), cudaMemcpyDeviceToHost, c->stream));
-  AVD_CUDA(cudaMemcpyAsync(&ovf, c->stats + c->cfg.m + 3, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  double* hs = c->eig_host;  // pinned scratch
+  AVD_CUDA(cudaMemcpyAsync(hs, c->stats + c->cfg.m + 3, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  AVD_CUDA(cudaMemcpyAsync(hs + 1, c->dplan, sizeof(DevPlan), cudaMemcpyDeviceToHost, c->stream));
   AVD_CUDA(cudaStreamSynchronize(c->stream));
+  const double ovf = hs[0];
+  std::memcpy(&c->hplan, hs + 1, sizeof(DevPlan));
   if (c->hplan.nonfinite > 0) {
     set_error("X has non-finite entries (" + std::to_string(c->hplan.nonfinite) + " non-finite column sums)");
     c->stage = 0;
@@ -466,11 +468,12 @@ avd_status avd_stage_select(avd_ctx* c, const float* X, int32_t level, int32_t r
   if (level < 0 || level > 3 || rank < 0 || rank >= c->cfg.world) { set_error("bad level/rank"); return AVD_EINVAL; }
   if (level == 0) {
     // local count + globally exchanged [count, overflow] -> same decision on every rank
-    unsigned long long cnt = 0;
-    long long gx[2] = {0, 0};
-    AVD_CUDA(cudaMemcpyAsync(&cnt, c->cand_cnt, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
-    AVD_CUDA(cudaMemcpyAsync(gx, c->cand_x, sizeof(gx), cudaMemcpyDeviceToHost, c->stream));
+    long long* hs = reinterpret_cast<long long*>(c->eig_host);  // pinned scratch
+    AVD_CUDA(cudaMemcpyAsync(hs, c->cand_cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+    AVD_CUDA(cudaMemcpyAsync(hs + 1, c->cand_x, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
     AVD_CUDA(cudaStreamSynchronize(c->stream));
+    const unsigned long long cnt = (unsigned long long)hs[0];
+    const long long gx[2] = {hs[1], hs[2]};
     c->hplan.cand_count = (int64_t)cnt;
     // the candidate list is used only if it holds >= n_top entries (then |E_top| = n_top)
     c->cand_overflow = gx[1] > 0 || gx[0] < c->plan.n_top || (c->cfg.flags & AVD_FLAG_STREAM_SELECT);
@@ -510,11 +513,12 @@ avd_status avd_stage_report(avd_ctx* c, avd_outputs* out) {
   report_pack_kernel<<<1, 128, 0, c->stream>>>(c->report, c->agg, c->energy, c->stats, c->trace, c->diag, c->sigma,
                                                c->dplan, m, k, c->k_pad, pack);
   AVD_LAUNCHED(c);
-  std::vector<double> h((size_t)npack);
-  AVD_CUDA(cudaMemcpyAsync(h.data(), pack, sizeof(double) * npack, cudaMemcpyDeviceToHost, c->stream));
+  static_assert(kPackHead + 96 + kPlanWords <= 4 * kMaxP, "pinned scratch too small for the report pack");
+  const double* h = c->eig_host;  // pinned scratch (k <= 95)
+  AVD_CUDA(cudaMemcpyAsync(c->eig_host, pack, sizeof(double) * npack, cudaMemcpyDeviceToHost, c->stream));
   AVD_CUDA(cudaStreamSynchronize(c->stream));
-  std::memcpy(&c->hplan, h.data() + kPackHead + k, sizeof(DevPlan));
-  const double* sig = h.data() + kPackHead;
+  std::memcpy(&c->hplan, h + kPackHead + k, sizeof(DevPlan));
+  const double* sig = h + kPackHead;
   double spike = 0.0;
   for (int r = 0; r < k; ++r) spike += sig[r] * sig[r];
   const double total = h[20], trace = h[21];

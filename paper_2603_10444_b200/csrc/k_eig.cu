@@ -1070,8 +1070,8 @@ avd_status run_eig(Ctx* c) {
   c->rr_count = rr_count;
   c->max_resid = maxres;
   c->sigma_next = (k < p) ? std::sqrt(std::max(c->eig_host[k], 0.0)) : 0.0;
-  int sw[16];
-  AVD_CUDA(cudaMemcpyAsync(sw, jstats, sizeof(sw), cudaMemcpyDeviceToHost, c->stream));
+  int* sw = reinterpret_cast<int*>(c->eig_host + 2 * kMaxP);  // pinned scratch, 16 ints
+  AVD_CUDA(cudaMemcpyAsync(sw, jstats, sizeof(int) * 16, cudaMemcpyDeviceToHost, c->stream));
   AVD_CUDA(cudaStreamSynchronize(c->stream));
   c->jacobi_sweeps = 0;
   for (int q = 0; q < std::min(rr_count, 16); ++q) c->jacobi_sweeps += sw[q];  // total over all RR solves
@@ -1092,7 +1092,8 @@ avd_status run_uncentred(Ctx* c) {
   double* q = c->diag + 4;
   double* y = q + c->m_pad;
   const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(m, 8), 4LL * c->num_sms);
-  double h[4] = {0, 0, 0, 0};
+  double* h = c->eig_host + 3 * kMaxP;  // pinned scratch, 4 doubles
+  for (int t = 0; t < 4; ++t) h[t] = 0.0;
   int it = 0;
   for (int blk = 0; blk < 16; ++blk) {
     for (int t = 0; t < 4; ++t, ++it) {
@@ -1104,7 +1105,7 @@ avd_status run_uncentred(Ctx* c) {
     AVD_LAUNCHED(c);
     power_u_stats_kernel<<<1, 256, 0, c->stream>>>(c->mu, m, q, y, c->diag);
     AVD_LAUNCHED(c);
-    AVD_CUDA(cudaMemcpyAsync(h, c->diag, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    AVD_CUDA(cudaMemcpyAsync(h, c->diag, sizeof(double) * 4, cudaMemcpyDeviceToHost, c->stream));
     AVD_CUDA(cudaStreamSynchronize(c->stream));
     if (!(h[0] > 0.0) || h[2] <= 1e-8) break;
   }

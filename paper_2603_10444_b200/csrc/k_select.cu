@@ -11,6 +11,7 @@
 // Rank r takes the ties left after ranks < r (rows are sharded in rank order).
 // The histogram and mark passes read the K2 candidate list (entries with key>>19 >= b1), or,
 // if it overflowed its capacity, stream X directly.
+#include <cstring>
 #include <vector>
 #include "common.cuh"
 
@@ -392,10 +393,13 @@ avd_status launch_select(Ctx* c, const float* X, int level, int rank) {
 avd_status launch_gather(Ctx* c, const float* X, int rank, int64_t* top_idx, double* rho) {
   // exchanged per-rank counts -> this rank's tie quota and global offset (host integer logic)
   const int world = c->cfg.world;
-  std::vector<long long> tc(2 * world);
-  AVD_CUDA(cudaMemcpyAsync(tc.data(), c->ties, sizeof(long long) * 2 * world, cudaMemcpyDeviceToHost, c->stream));
-  AVD_CUDA(cudaMemcpyAsync(&c->hplan, c->dplan, sizeof(DevPlan), cudaMemcpyDeviceToHost, c->stream));
+  // both land in the pinned scratch (pageable D2H copies cost ~10 us each)
+  long long* hs = reinterpret_cast<long long*>(c->eig_host);
+  AVD_CUDA(cudaMemcpyAsync(hs, c->ties, sizeof(long long) * 2 * world, cudaMemcpyDeviceToHost, c->stream));
+  AVD_CUDA(cudaMemcpyAsync(hs + 2 * world, c->dplan, sizeof(DevPlan), cudaMemcpyDeviceToHost, c->stream));
   AVD_CUDA(cudaStreamSynchronize(c->stream));
+  std::vector<long long> tc(hs, hs + 2 * world);
+  std::memcpy(&c->hplan, hs + 2 * world, sizeof(DevPlan));
   std::vector<int64_t> sel(world), tie(world);
   for (int r = 0; r < world; ++r) { sel[r] = tc[r]; tie[r] = tc[world + r]; }
   int64_t quota = 0, offset = 0;
