@@ -224,8 +224,9 @@ constexpr int kPlanWords = (int)((sizeof(DevPlan) + 7) / 8);
 __global__ void report_pack_kernel(const double* __restrict__ report, const double* __restrict__ agg,
                                    const double* __restrict__ energy, const double* __restrict__ stats,
                                    const double* __restrict__ trace, const double* __restrict__ diag,
-                                   const double* __restrict__ sigma, const DevPlan* __restrict__ dp, int64_t m,
-                                   int k, int k_pad, double* __restrict__ pack) {
+                                   const double* __restrict__ sigma, const DevPlan* __restrict__ dp,
+                                   const double* __restrict__ jstats, int64_t m, int k, int k_pad,
+                                   double* __restrict__ pack) {
   const int t = threadIdx.x;
   if (t < 5) pack[t] = report[t];
   if (t < 8) pack[8 + t] = agg[t];
@@ -236,6 +237,7 @@ __global__ void report_pack_kernel(const double* __restrict__ report, const doub
   const unsigned long long* pw = reinterpret_cast<const unsigned long long*>(dp);
   unsigned long long* dst = reinterpret_cast<unsigned long long*>(pack + kPackHead + k);
   if (t < (int)(sizeof(DevPlan) / 8)) dst[t] = pw[t];
+  if (t < 8) pack[kPackHead + k + kPlanWords + t] = jstats[t];  // 16 int sweep counts (run_eig)
 }
 
 }  // namespace
@@ -508,16 +510,22 @@ avd_status avd_stage_report(avd_ctx* c, avd_outputs* out) {
     AVD_LAUNCHED(c);
   }
   // one packed D2H copy (pageable copies cost ~10 us each); the tail of the eig scratch is free
-  const int64_t npack = kPackHead + k + kPlanWords;
+  const int64_t npack = kPackHead + k + kPlanWords + 8;
   double* pack = c->red_part + ((int64_t)c->n_red * c->p * c->p - npack);
   report_pack_kernel<<<1, 128, 0, c->stream>>>(c->report, c->agg, c->energy, c->stats, c->trace, c->diag, c->sigma,
-                                               c->dplan, m, k, c->k_pad, pack);
+                                               c->dplan, c->theta + c->p, m, k, c->k_pad, pack);
   AVD_LAUNCHED(c);
-  static_assert(kPackHead + 96 + kPlanWords <= 4 * kMaxP, "pinned scratch too small for the report pack");
+  static_assert(kPackHead + 96 + kPlanWords + 8 <= 4 * kMaxP, "pinned scratch too small for the report pack");
   const double* h = c->eig_host;  // pinned scratch (k <= 95)
   AVD_CUDA(cudaMemcpyAsync(c->eig_host, pack, sizeof(double) * npack, cudaMemcpyDeviceToHost, c->stream));
   AVD_CUDA(cudaStreamSynchronize(c->stream));
   std::memcpy(&c->hplan, h + kPackHead + k, sizeof(DevPlan));
+  {
+    int sw[16];
+    std::memcpy(sw, h + kPackHead + k + kPlanWords, sizeof(sw));
+    c->jacobi_sweeps = 0;
+    for (int q = 0; q < std::min(c->rr_count, 16); ++q) c->jacobi_sweeps += sw[q];  // over all RR solves
+  }
   const double* sig = h + kPackHead;
   double spike = 0.0;
   for (int r = 0; r < k; ++r) spike += sig[r] * sig[r];

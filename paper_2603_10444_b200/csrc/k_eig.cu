@@ -1070,11 +1070,7 @@ avd_status run_eig(Ctx* c) {
   c->rr_count = rr_count;
   c->max_resid = maxres;
   c->sigma_next = (k < p) ? std::sqrt(std::max(c->eig_host[k], 0.0)) : 0.0;
-  int* sw = reinterpret_cast<int*>(c->eig_host + 2 * kMaxP);  // pinned scratch, 16 ints
-  AVD_CUDA(cudaMemcpyAsync(sw, jstats, sizeof(int) * 16, cudaMemcpyDeviceToHost, c->stream));
-  AVD_CUDA(cudaStreamSynchronize(c->stream));
-  c->jacobi_sweeps = 0;
-  for (int q = 0; q < std::min(rr_count, 16); ++q) c->jacobi_sweeps += sw[q];  // total over all RR solves
+  // the per-solve sweep counts stay at theta + p; the report stage reads them with its packed copy
   AVD_CUDA(cudaMemsetAsync(c->V32, 0, sizeof(float) * m * c->k_pad, c->stream));
   finalize_vectors_kernel<<<k, 256, 0, c->stream>>>(c->U, c->theta, m, p, k, c->k_pad, c->V, c->sigma, c->V32);
   AVD_LAUNCHED(c);
