@@ -121,7 +121,8 @@ __global__ void __launch_bounds__(kSelThreads) mark_kernel(int64_t n, const uint
                                                            const uint64_t* __restrict__ cidx, const float* __restrict__ X,
                                                            int64_t base, const DevPlan* __restrict__ dp,
                                                            uint32_t* __restrict__ bm_sel, uint32_t* __restrict__ bm_tie,
-                                                           unsigned long long* __restrict__ counts) {
+                                                           unsigned long long* __restrict__ counts,
+                                                           unsigned long long* __restrict__ blk, int64_t nblk) {
   __shared__ unsigned int c_sel, c_tie;
   if (threadIdx.x == 0) { c_sel = 0; c_tie = 0; }
   __syncthreads();
@@ -133,11 +134,15 @@ __global__ void __launch_bounds__(kSelThreads) mark_kernel(int64_t n, const uint
       uint32_t key;
       uint64_t li;
       if (!fetch<FROM_X>(t, ckey, cidx, X, base, key, li)) continue;
+      // + the per-compaction-block counts the ordered emit scans (no separate counting pass)
+      const int64_t bk = (int64_t)(li >> 5) / kWordsPerBlk;
       if (key > T) {
         atomicOr(&bm_sel[li >> 5], 1u << (li & 31));
+        atomicAdd(&blk[bk], 1ull);
         ++ns;
       } else if (key == T) {
         atomicOr(&bm_tie[li >> 5], 1u << (li & 31));
+        atomicAdd(&blk[nblk + bk], 1ull);
         ++nt;
       }
     }
@@ -158,25 +163,6 @@ __global__ void publish_counts_kernel(const unsigned long long* __restrict__ cou
   if (t < 2 * world) ties[t] = 0;
   __syncthreads();
   if (t == 0) { ties[rank] = (long long)counts[0]; ties[world + rank] = (long long)counts[1]; }
-}
-
-__global__ void __launch_bounds__(kSelThreads) blk_count_kernel(const uint32_t* __restrict__ bs, const uint32_t* __restrict__ bt,
-                                                                int64_t nwords, int64_t nblk, int64_t* __restrict__ blk) {
-  __shared__ int s1[kSelThreads], s2[kSelThreads];
-  const int64_t w0 = (int64_t)blockIdx.x * kWordsPerBlk;
-  int a = 0, b = 0;
-  for (int64_t w = w0 + threadIdx.x; w < min(nwords, w0 + kWordsPerBlk); w += kSelThreads) {
-    a += __popc(bs[w]);
-    b += __popc(bt[w]);
-  }
-  s1[threadIdx.x] = a;
-  s2[threadIdx.x] = b;
-  __syncthreads();
-  for (int o = kSelThreads / 2; o > 0; o >>= 1) {
-    if ((int)threadIdx.x < o) { s1[threadIdx.x] += s1[threadIdx.x + o]; s2[threadIdx.x] += s2[threadIdx.x + o]; }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) { blk[blockIdx.x] = s1[0]; blk[nblk + blockIdx.x] = s2[0]; }
 }
 
 // exclusive scan of block counts (one CTA); quota / offset come from avd_tie_quota (host)
@@ -377,12 +363,14 @@ avd_status launch_select(Ctx* c, const float* X, int level, int rank) {
     AVD_CUDA(cudaMemsetAsync(c->bm_tie, 0, sizeof(uint32_t) * c->nwords, c->stream));
     unsigned long long* counts = reinterpret_cast<unsigned long long*>(c->blk_cnt + 2 * c->nblk);
     AVD_CUDA(cudaMemsetAsync(counts, 0, 2 * sizeof(unsigned long long), c->stream));
+    unsigned long long* blk = reinterpret_cast<unsigned long long*>(c->blk_cnt);
+    AVD_CUDA(cudaMemsetAsync(blk, 0, 2 * sizeof(unsigned long long) * c->nblk, c->stream));
     if (fromX)
       mark_kernel<true><<<grid, kSelThreads, 0, c->stream>>>(n, nullptr, nullptr, X, base, c->dplan, c->bm_sel,
-                                                             c->bm_tie, counts);
+                                                             c->bm_tie, counts, blk, c->nblk);
     else
       mark_kernel<false><<<grid, kSelThreads, 0, c->stream>>>(n, c->cand_key, c->cand_idx, nullptr, base, c->dplan,
-                                                              c->bm_sel, c->bm_tie, counts);
+                                                              c->bm_sel, c->bm_tie, counts, blk, c->nblk);
     AVD_LAUNCHED(c);
     publish_counts_kernel<<<1, 256, 0, c->stream>>>(counts, c->ties, c->cfg.world, rank);
     AVD_LAUNCHED(c);
@@ -404,8 +392,7 @@ avd_status launch_gather(Ctx* c, const float* X, int rank, int64_t* top_idx, dou
   for (int r = 0; r < world; ++r) { sel[r] = tc[r]; tie[r] = tc[world + r]; }
   int64_t quota = 0, offset = 0;
   AVD_TRY(avd_tie_quota(sel.data(), tie.data(), world, rank, c->hplan.empty ? 0 : c->hplan.q, &quota, &offset));
-  blk_count_kernel<<<(unsigned)c->nblk, kSelThreads, 0, c->stream>>>(c->bm_sel, c->bm_tie, c->nwords, c->nblk, c->blk_cnt);
-  AVD_LAUNCHED(c);
+  // per-block (sel, tie) counts were accumulated by mark_kernel
   blk_scan_kernel<<<1, 1024, 0, c->stream>>>(c->blk_cnt, c->nblk, quota, offset, tie[rank], c->dplan);
   AVD_LAUNCHED(c);
   emit_kernel<<<(unsigned)c->nblk, kSelThreads, 0, c->stream>>>(c->bm_sel, c->bm_tie, c->nwords, c->nblk, c->blk_cnt,
