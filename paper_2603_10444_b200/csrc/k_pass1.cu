@@ -74,31 +74,42 @@ __global__ void __launch_bounds__(kT) sample_kernel(const float* __restrict__ X,
   float mx[VEC], mn[VEC];
 #pragma unroll
   for (int v = 0; v < VEC; ++v) { cs[v] = 0.0; mx[v] = -FLT_MAX; mn[v] = FLT_MAX; }
-  for (int64_t jr = j0; jr < j1; ++jr) {
-    const int64_t i = i0 + jr * s;
-    float x[VEC];
-    if constexpr (VEC == 4) {
-      const float4 t = active ? __ldg(reinterpret_cast<const float4*>(X + i * m + c0)) : make_float4(0.f, 0.f, 0.f, 0.f);
-      x[0] = t.x; x[1] = t.y; x[2] = t.z; x[3] = t.w;
-    } else {
-      x[0] = active ? __ldg(X + i * m + c0) : 0.f;
-    }
+  // sampled row jr has global sampled index gb + jr ((i0 + row_offset) is a multiple of s)
+  const uint64_t gb = ((uint64_t)i0 + (uint64_t)row_offset) / (uint64_t)s;
+  constexpr int R = 4;  // sampled rows in flight per thread
+  for (int64_t jr = j0; jr < j1; jr += R) {
+    float x[R][VEC];
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) {
-      const uint32_t key = __float_as_uint(x[v]) & 0x7FFFFFFFu;
-      const bool fin = key < 0x7F800000u;
-      if (active && fin) {
-        cs[v] += (double)x[v];
-        mx[v] = fmaxf(mx[v], x[v]);
-        mn[v] = fminf(mn[v], x[v]);
+    for (int u = 0; u < R; ++u) {
+      const bool ok = active && jr + u < j1;
+      const int64_t i = i0 + (jr + u) * s;
+      if constexpr (VEC == 4) {
+        const float4 t = ok ? __ldg(reinterpret_cast<const float4*>(X + i * m + c0)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        x[u][0] = t.x; x[u][1] = t.y; x[u][2] = t.z; x[u][3] = t.w;
+      } else {
+        x[u][0] = ok ? __ldg(X + i * m + c0) : 0.f;
       }
     }
-    // the |x| histogram only needs every kHistSub-th sampled row (enough for a top-0.1% bin)
-    if ((((uint64_t)(i0 + jr * s) + row_offset) / s) % kHistSub == 0) {
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      if (jr + u >= j1) break;
 #pragma unroll
       for (int v = 0; v < VEC; ++v) {
-        const uint32_t key = __float_as_uint(x[v]) & 0x7FFFFFFFu;
-        hist_add(sh, key, active && key < 0x7F800000u && key != 0);
+        const uint32_t key = __float_as_uint(x[u][v]) & 0x7FFFFFFFu;
+        const bool fin = key < 0x7F800000u;
+        if (active && fin) {
+          cs[v] += (double)x[u][v];
+          mx[v] = fmaxf(mx[v], x[u][v]);
+          mn[v] = fminf(mn[v], x[u][v]);
+        }
+      }
+      // the |x| histogram only needs every kHistSub-th sampled row (enough for a top-0.1% bin)
+      if ((gb + (uint64_t)(jr + u)) % kHistSub == 0) {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          const uint32_t key = __float_as_uint(x[u][v]) & 0x7FFFFFFFu;
+          hist_add(sh, key, active && key < 0x7F800000u && key != 0);
+        }
       }
     }
   }
