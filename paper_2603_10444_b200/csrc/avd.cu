@@ -326,9 +326,17 @@ avd_status avd_create(const avd_config* cfg, avd_ctx** out) {
     set_error("cudaMallocHost failed");
     return AVD_ENOMEM;
   }
+  if (cudaEventCreateWithFlags(&c->ev_host, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(c->ws);
+    cudaFreeHost(c->eig_host);
+    delete c;
+    set_error("cudaEventCreate failed");
+    return AVD_ECUDA;
+  }
   cudaMemset(c->P_hl, 0, sizeof(float) * 2 * c->l_pad * (((c->k_pad + 31) / 32) * 32));
   st = gram_make_tmap(c);
-  if (st != AVD_OK) { cudaFree(c->ws); cudaFreeHost(c->eig_host); delete c; return st; }
+  if (st != AVD_OK) { cudaFree(c->ws); cudaFreeHost(c->eig_host); cudaEventDestroy(c->ev_host); delete c; return st; }
   c->stage = 0;
   *out = c;
   return AVD_OK;
@@ -338,6 +346,7 @@ void avd_destroy(avd_ctx* c) {
   if (!c) return;
   cudaFree(c->ws);
   cudaFreeHost(c->eig_host);
+  if (c->ev_host) cudaEventDestroy(c->ev_host);
   cudaFree(c->X_stage);
   cudaFree(c->o_mu); cudaFree(c->o_V); cudaFree(c->o_sigma); cudaFree(c->o_rho); cudaFree(c->o_idx);
   delete c;
@@ -431,7 +440,18 @@ avd_status avd_stage_gram(avd_ctx* c, const float* X) {
   double* hs = c->eig_host;  // pinned scratch
   AVD_CUDA(cudaMemcpyAsync(hs, c->stats + c->cfg.m + 3, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   AVD_CUDA(cudaMemcpyAsync(hs + 1, c->dplan, sizeof(DevPlan), cudaMemcpyDeviceToHost, c->stream));
-  AVD_CUDA(cudaStreamSynchronize(c->stream));
+  AVD_CUDA(cudaEventRecord(c->ev_host, c->stream));
+  // speculative: the Gram of the digits as they stand is queued before the host reads the flags,
+  // so the GPU does not idle through the round trip; a requant (or an error) redoes / drops it
+  auto gram = [&]() -> avd_status {
+    AVD_CUDA(cudaMemcpyAsync(c->qsum, c->qsum_local, sizeof(long long) * 2 * c->cfg.m, cudaMemcpyDeviceToDevice,
+                             c->stream));
+    AVD_CUDA(cudaMemcpyAsync(c->qerr, c->qerr_local, sizeof(double) * c->m_pad, cudaMemcpyDeviceToDevice, c->stream));
+    return launch_gram(c);
+  };
+  const bool force_exact = (c->cfg.flags & AVD_FLAG_EXACT_SCALE) != 0;
+  if (!force_exact) AVD_TRY(gram());
+  AVD_CUDA(cudaEventSynchronize(c->ev_host));
   const double ovf = hs[0];
   std::memcpy(&c->hplan, hs + 1, sizeof(DevPlan));
   if (c->hplan.nonfinite > 0) {
@@ -439,11 +459,11 @@ avd_status avd_stage_gram(avd_ctx* c, const float* X) {
     c->stage = 0;
     return AVD_ENONFINITE;
   }
-  c->requantised = ovf > 0.0 || (c->cfg.flags & AVD_FLAG_EXACT_SCALE);
-  if (c->requantised) AVD_TRY(launch_pass1(c, X, false));  // exact column ranges (k_pass1.cu)
-  AVD_CUDA(cudaMemcpyAsync(c->qsum, c->qsum_local, sizeof(long long) * 2 * c->cfg.m, cudaMemcpyDeviceToDevice, c->stream));
-  AVD_CUDA(cudaMemcpyAsync(c->qerr, c->qerr_local, sizeof(double) * c->m_pad, cudaMemcpyDeviceToDevice, c->stream));
-  AVD_TRY(launch_gram(c));
+  c->requantised = ovf > 0.0 || force_exact;
+  if (c->requantised) {
+    AVD_TRY(launch_pass1(c, X, false));  // exact column ranges (k_pass1.cu)
+    AVD_TRY(gram());
+  }
   c->stage = 3;
   return AVD_OK;
 }

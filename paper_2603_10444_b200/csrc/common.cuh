@@ -110,6 +110,7 @@ struct Ctx {
   double* resid = nullptr;        // [p]
   double* trace = nullptr;        // [1]
   double* eig_host = nullptr;     // pinned: theta[p] + resid[p]
+  cudaEvent_t ev_host = nullptr;  // host waits on this instead of the whole stream (stage_gram)
   double* V = nullptr;            // [m][k] output copy (row-major)
   double* sigma = nullptr;        // [k]
   float* V32 = nullptr;           // [m][k_pad] fp32 copy for K5/K8

@@ -127,6 +127,13 @@ __device__ __forceinline__ double fix_scale(const double* gmax, int64_t m, int l
   const double b = level ? g * g : g;
   return ldexp(1.0, 61 - (ilogb(b) + 1));
 }
+// 1 / fix_scale (a power of two, so exact) without an fp64 division
+__device__ __forceinline__ double fix_scale_inv(const double* gmax, int64_t m, int level) {
+  const double g = *gmax * (double)m;
+  if (!(g > 0.0) || !(g < 1e150)) return 1.0;
+  const double b = level ? g * g : g;
+  return ldexp(1.0, (ilogb(b) + 1) - 61);
+}
 
 template <typename T, int NR, int NC>
 __global__ void __launch_bounds__(kSkThreads) gemm_sk_kernel(const T* __restrict__ G, int64_t ldg,
@@ -242,7 +249,7 @@ __global__ void fix_convert_kernel(unsigned long long* __restrict__ Yfix, int64_
                                    float* __restrict__ Y32) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
-  const double inv = 1.0 / fix_scale(gmax, m, level);
+  const double inv = fix_scale_inv(gmax, m, level);
   const double v = (double)(long long)Yfix[t] * inv;
   Yfix[t] = 0ull;
   Y[t] = v;
