@@ -34,29 +34,45 @@ namespace {
 
 // ---------------------------------------------------------------- G_int -> G (fp64), G32 (fp32)
 // Both with leading dimension m_pad; rows/columns >= m are zero.
-__global__ void gram_finalize_kernel(const long long* __restrict__ Gi, int64_t m, int64_t m_pad,
+// 32 x 32 tiles, 32 x 8 threads.  K3 adds tile (A, B), A <= B (128-blocks), transposed: element
+// (a, b) of an upper tile sits at Gi[b][a]; those tiles are read row-wise (coalesced) and
+// transposed through shared memory, so every global access is coalesced.
+__global__ void __launch_bounds__(256) gram_finalize_kernel(const long long* __restrict__ Gi, int64_t m, int64_t m_pad,
                                      const int32_t* __restrict__ shift, const long long* __restrict__ qsum,
                                      const double* __restrict__ qerr, double inv_l, double unit,
                                      double* __restrict__ G, float* __restrict__ G32) {
-  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t a = blockIdx.y;
-  if (b >= m_pad) return;
-  double g = 0.0;
-  if (a < m && b < m) {
-    // K3 adds tile (A, B), A <= B, transposed: element (a, b) of an upper tile sits at Gi[b][a]
-    const bool upper = (a / 128) <= (b / 128);
-    const long long v = upper ? Gi[b * m_pad + a] : Gi[a * m_pad + b];
-    // exact centring of the quantised matrix: sum_i (q_ia - qbar_a)(q_ib - qbar_b)
-    //   = sum_i q_ia q_ib - S_a S_b / l   (S = column sums of q, exact integers)
-    // v unit = sum_i q_ia q_ib; the diagonal is the exact sum_i q_ia^2 of the fused pass
-    // (qsum[m + a]; with 3 digits the Gram drops the two lowest digit-product classes, whose
-    // diagonal part is a positive bias) minus the realised squared rounding errors (unbiased)
-    const double qq = (a == b) ? (double)qsum[m + a] - qerr[a] : (double)v * unit;
-    const double corr = ((double)qsum[a] * (double)qsum[b]) * inv_l;
-    g = ldexp(qq - corr, -(shift[a] + shift[b]));
+  __shared__ long long tile[32][33];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int64_t a0 = (int64_t)blockIdx.y * 32, b0 = (int64_t)blockIdx.x * 32;
+  const bool upper = (a0 / 128) <= (b0 / 128);  // uniform over the 32 x 32 tile
+  if (upper) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int bb = ty + 8 * r;
+      tile[bb][tx] = (b0 + bb < m && a0 + tx < m) ? Gi[(b0 + bb) * m_pad + a0 + tx] : 0ll;
+    }
+    __syncthreads();
   }
-  G[a * m_pad + b] = g;
-  G32[a * m_pad + b] = (float)g;
+  const int64_t b = b0 + tx;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int aa = ty + 8 * r;
+    const int64_t a = a0 + aa;
+    double g = 0.0;
+    if (a < m && b < m) {
+      const long long v = upper ? tile[tx][aa] : Gi[a * m_pad + b];
+      // exact centring of the quantised matrix: sum_i (q_ia - qbar_a)(q_ib - qbar_b)
+      //   = sum_i q_ia q_ib - S_a S_b / l   (S = column sums of q, exact integers)
+      // v unit = sum_i q_ia q_ib; the diagonal is the exact sum_i q_ia^2 of the fused pass
+      // (qsum[m + a]; with 3 digits the Gram drops the two lowest digit-product classes, whose
+      // diagonal part is a positive bias) minus the realised squared rounding errors (unbiased)
+      const double qq = (a == b) ? (double)qsum[m + a] - qerr[a] : (double)v * unit;
+      const double corr = ((double)qsum[a] * (double)qsum[b]) * inv_l;
+      g = ldexp(qq - corr, -(shift[a] + shift[b]));
+    }
+    G[a * m_pad + b] = g;
+    G32[a * m_pad + b] = (float)g;
+  }
 }
 
 // tr(G) and max_a G_aa (= max |G_ab| for the positive semidefinite G)
@@ -873,8 +889,8 @@ __global__ void power_u_stats_kernel(const double* __restrict__ mu, int64_t m, c
 avd_status launch_gram_finalize(Ctx* c) {
   const int64_t m = c->cfg.m;
   const double unit = (c->nd == 3) ? 16384.0 : 1.0;
-  dim3 grid((unsigned)ceil_div(c->m_pad, 256), (unsigned)c->m_pad);
-  gram_finalize_kernel<<<grid, 256, 0, c->stream>>>(c->gram_i, m, c->m_pad, c->shift, c->qsum, c->qerr,
+  dim3 grid((unsigned)(c->m_pad / 32), (unsigned)(c->m_pad / 32));
+  gram_finalize_kernel<<<grid, dim3(32, 8), 0, c->stream>>>(c->gram_i, m, c->m_pad, c->shift, c->qsum, c->qerr,
                                                     1.0 / (double)c->cfg.l_global, unit, c->G, c->G32);
   AVD_LAUNCHED(c);
   trace_kernel<<<1, 256, 0, c->stream>>>(c->G, m, c->m_pad, c->trace, c->gmax);
