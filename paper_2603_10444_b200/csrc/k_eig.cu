@@ -76,21 +76,25 @@ __global__ void __launch_bounds__(256) gram_finalize_kernel(const long long* __r
 }
 
 // tr(G) and max_a G_aa (= max |G_ab| for the positive semidefinite G)
-__global__ void trace_kernel(const double* __restrict__ G, int64_t m, int64_t ld, double* __restrict__ out,
-                             double* __restrict__ gmax) {
-  __shared__ double sh[256], shm[256];
+__global__ void __launch_bounds__(1024) trace_kernel(const double* __restrict__ G, int64_t m, int64_t ld,
+                                                    double* __restrict__ out, double* __restrict__ gmax) {
+  // fixed order: strided per-thread sums, xor-shuffle tree per warp, warp partials in order
+  __shared__ double sh[32], shm[32];
   double s = 0.0, mx = 0.0;
-  for (int64_t j = threadIdx.x; j < m; j += 256) {
+  for (int64_t j = threadIdx.x; j < m; j += 1024) {
     const double g = G[j * ld + j];
     s += g;
     mx = fmax(mx, fabs(g));
   }
-  sh[threadIdx.x] = s;
-  shm[threadIdx.x] = mx;
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+    mx = fmax(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0) { sh[threadIdx.x >> 5] = s; shm[threadIdx.x >> 5] = mx; }
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0, u = 0.0;
-    for (int i = 0; i < 256; ++i) { t += sh[i]; u = fmax(u, shm[i]); }
+    for (int i = 0; i < 32; ++i) { t += sh[i]; u = fmax(u, shm[i]); }
     *out = t;
     *gmax = u;
   }
@@ -893,7 +897,7 @@ avd_status launch_gram_finalize(Ctx* c) {
   gram_finalize_kernel<<<grid, dim3(32, 8), 0, c->stream>>>(c->gram_i, m, c->m_pad, c->shift, c->qsum, c->qerr,
                                                     1.0 / (double)c->cfg.l_global, unit, c->G, c->G32);
   AVD_LAUNCHED(c);
-  trace_kernel<<<1, 256, 0, c->stream>>>(c->G, m, c->m_pad, c->trace, c->gmax);
+  trace_kernel<<<1, 1024, 0, c->stream>>>(c->G, m, c->m_pad, c->trace, c->gmax);
   AVD_LAUNCHED(c);
   return AVD_OK;
 }
