@@ -493,14 +493,16 @@ avd_status avd_stage_select(avd_ctx* c, const float* X, int32_t level, int32_t r
     long long* hs = reinterpret_cast<long long*>(c->eig_host);  // pinned scratch
     AVD_CUDA(cudaMemcpyAsync(hs, c->cand_cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
     AVD_CUDA(cudaMemcpyAsync(hs + 1, c->cand_x, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-    AVD_CUDA(cudaStreamSynchronize(c->stream));
+    AVD_CUDA(cudaEventRecord(c->ev_host, c->stream));
+    AVD_TRY(launch_select0_speculative(c));  // runs while the host reads the counts
+    AVD_CUDA(cudaEventSynchronize(c->ev_host));
     const unsigned long long cnt = (unsigned long long)hs[0];
     const long long gx[2] = {hs[1], hs[2]};
     c->hplan.cand_count = (int64_t)cnt;
     // the candidate list is used only if it holds >= n_top entries (then |E_top| = n_top)
     c->cand_overflow = gx[1] > 0 || gx[0] < c->plan.n_top || (c->cfg.flags & AVD_FLAG_STREAM_SELECT);
   }
-  AVD_TRY(launch_select(c, X, level, rank));
+  if (level != 0 || c->cand_overflow) AVD_TRY(launch_select(c, X, level, rank));  // level 0 from X
   c->stage = 6 + level;
   return AVD_OK;
 }

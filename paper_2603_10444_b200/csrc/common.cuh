@@ -193,6 +193,7 @@ avd_status run_eig(Ctx* c);                                // k_eig.cu
 void gemm_geometry(int64_t m_pad, int p, int num_sms, bool fp32, int* BM, int* ncta, int64_t* U, int* KT);
 size_t gemm_part_bytes(int64_t m_pad, int p, int num_sms);
 avd_status launch_project(Ctx* c, const float* X);         // k_project.cu
+avd_status launch_select0_speculative(Ctx* c);
 avd_status launch_select(Ctx* c, const float* X, int level, int rank);  // k_select.cu
 avd_status launch_gather(Ctx* c, const float* X, int rank, int64_t* top_idx, double* rho);
 avd_status launch_project_reduce(Ctx* c);                  // k_project.cu

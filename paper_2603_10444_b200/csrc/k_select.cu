@@ -43,8 +43,11 @@ __device__ __forceinline__ bool fetch(int64_t t, const uint32_t* __restrict__ ck
 template <bool FROM_X>
 __global__ void __launch_bounds__(kSelThreads) hist_kernel(int level, int64_t n, const uint32_t* __restrict__ ckey,
                                                            const uint64_t* __restrict__ cidx, const float* __restrict__ X,
-                                                           const DevPlan* __restrict__ dp, unsigned long long* __restrict__ out) {
+                                                           const DevPlan* __restrict__ dp, unsigned long long* __restrict__ out,
+                                                           const unsigned long long* __restrict__ n_dev = nullptr,
+                                                           int64_t n_cap = 0) {
   __shared__ unsigned int sh[kHistBins];
+  if (n_dev) n = min((int64_t)*n_dev, n_cap);  // count read on the device (speculative level 0)
   const int nb = level < 2 ? kHistBins : kHist3Bins;
   for (int b = threadIdx.x; b < nb; b += kSelThreads) sh[b] = 0;
   __syncthreads();
@@ -375,6 +378,16 @@ avd_status launch_select(Ctx* c, const float* X, int level, int rank) {
     publish_counts_kernel<<<1, 256, 0, c->stream>>>(counts, c->ties, c->cfg.world, rank);
     AVD_LAUNCHED(c);
   }
+  return AVD_OK;
+}
+
+// Level-0 histogram over the candidate list with the count read on the device, queued before the
+// host learns whether the list is usable (avd_stage_select redoes level 0 from X if it is not).
+avd_status launch_select0_speculative(Ctx* c) {
+  AVD_CUDA(cudaMemsetAsync(c->hist0, 0, sizeof(unsigned long long) * kHistBins, c->stream));
+  hist_kernel<false><<<(unsigned)(4 * c->num_sms), kSelThreads, 0, c->stream>>>(
+      0, 0, c->cand_key, c->cand_idx, nullptr, c->dplan, c->hist0, c->cand_cnt, c->cand_cap);
+  AVD_LAUNCHED(c);
   return AVD_OK;
 }
 
