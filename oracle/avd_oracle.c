@@ -21,8 +21,12 @@
  *   cross    = 1 - sum(rho)  ("minor cross-terms")
  * Readings where the paper is silent are DESIGN.md "Readings" R1..R12 (cited inline).
  *
- * Build: gcc -O2 -fopenmp -ffp-contract=off -fno-fast-math -shared -fPIC (see oracle/build.py).
- * OpenMP is used only across independent outputs; no summation order is changed by it.
+ * Build: gcc -O3 -mavx2 -fopenmp -ffp-contract=off -fno-fast-math -shared -fPIC (oracle/oracle.py).
+ * OpenMP is used only across independent outputs or fixed row blocks whose partial sums are
+ * added in block order, so no result depends on the thread count.  Scale (SURVEY §8(c) steps
+ * 3, 5, 8): the Gram is accumulated from row chunks of Xc (no l x m fp64 copy), the Jacobi
+ * eigensolver uses the parallel round-robin ordering, and E_top of large inputs is selected
+ * with a bounded heap under the same comparator (equality with the full sort is pinned).
  * Parity: pinned by tests/test_oracle_pins.py (worked example, closed forms of the planted
  * generator, numpy SVD on small inputs, brute-force sort, invariants).
  */
@@ -62,32 +66,70 @@ void oracle_center(const float* X, int64_t l, int64_t m, const double* mu, doubl
 
 /* 3. Gram  G = Xc^T Xc  (the right singular vectors of Xc are the eigenvectors of G and
  *    sigma_r^2 its eigenvalues — the SVD of PAPER.md:12-14).  G[a][b] = sum_i Xc[i][a] Xc[i][b],
- *    summed in row order i; computed for b >= a and mirrored (G is symmetric).
- *    XcT is the transpose of Xc (m x l) so each entry is one contiguous dot product. */
-void oracle_gram(const double* Xc, int64_t l, int64_t m, double* G) {
-  double* XcT = (double*)malloc(sizeof(double) * (size_t)(l * m));
-  if (!XcT) return;
-#pragma omp parallel for schedule(static)
-  for (int64_t a = 0; a < m; ++a)
-    for (int64_t i = 0; i < l; ++i) XcT[a * l + i] = Xc[i * m + a];
-#pragma omp parallel for schedule(dynamic, 4)
-  for (int64_t a = 0; a < m; ++a) {
-    const double* xa = XcT + a * l;
-    for (int64_t b = a; b < m; ++b) {
-      const double* xb = XcT + b * l;
-      double s = 0.0;
-      for (int64_t i = 0; i < l; ++i) s = s + xa[i] * xb[i];
-      G[a * m + b] = s;
-      G[b * m + a] = s;
+ *    summed in row order i = 0, 1, ..., l-1 for every entry (b >= a, mirrored: G is symmetric).
+ *    The sum is accumulated row by row (G[a][.] += Xc[i][a] Xc[i][.]): the same per-entry order as
+ *    a dot product over i, without a transposed copy of Xc.  OpenMP splits the ROWS a of G
+ *    (independent outputs); the order of every sum is unchanged by it.                          */
+#define ORACLE_GRAM_RB 64  /* rows of Xc held per chunk */
+#define ORACLE_GRAM_AB 16  /* rows a of G per task      */
+static void gram_chunk(const double* xc, int64_t n, int64_t m, double* G) {
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t a0 = 0; a0 < m; a0 += ORACLE_GRAM_AB) {
+    const int64_t a1 = a0 + ORACLE_GRAM_AB < m ? a0 + ORACLE_GRAM_AB : m;
+    for (int64_t r = 0; r < n; ++r) {
+      const double* xr = xc + r * m;
+      for (int64_t a = a0; a < a1; ++a) {
+        const double xa = xr[a];
+        double* g = G + a * m;
+        for (int64_t b = a; b < m; ++b) g[b] = g[b] + xa * xr[b];
+      }
     }
   }
-  free(XcT);
+}
+static void gram_mirror(int64_t m, double* G) {
+#pragma omp parallel for schedule(static)
+  for (int64_t a = 0; a < m; ++a)
+    for (int64_t b = 0; b < a; ++b) G[a * m + b] = G[b * m + a];
+}
+
+void oracle_gram(const double* Xc, int64_t l, int64_t m, double* G) {
+  memset(G, 0, sizeof(double) * (size_t)(m * m));
+  for (int64_t i0 = 0; i0 < l; i0 += ORACLE_GRAM_RB) {
+    const int64_t n = l - i0 < ORACLE_GRAM_RB ? l - i0 : ORACLE_GRAM_RB;
+    gram_chunk(Xc + i0 * m, n, m, G);
+  }
+  gram_mirror(m, G);
+}
+
+/* Same Gram straight from the fp32 X: the rows of Xc = X - 1 mu^T are formed in
+ * fp64 one chunk at a time (row-blocked Xc, so the l x m fp64 copy never exists — SURVEY §8(c)
+ * step 3).  Bit-identical to oracle_gram(oracle_center(X, mu)).                                */
+int oracle_gram_x(const float* X, int64_t l, int64_t m, const double* mu, double* G) {
+  double* xc = (double*)malloc(sizeof(double) * (size_t)(ORACLE_GRAM_RB * m));
+  if (!xc) return ORACLE_ENOMEM;
+  memset(G, 0, sizeof(double) * (size_t)(m * m));
+  for (int64_t i0 = 0; i0 < l; i0 += ORACLE_GRAM_RB) {
+    const int64_t n = l - i0 < ORACLE_GRAM_RB ? l - i0 : ORACLE_GRAM_RB;
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < n; ++r)
+      for (int64_t j = 0; j < m; ++j) xc[r * m + j] = (double)X[(i0 + r) * m + j] - mu[j];
+    gram_chunk(xc, n, m, G);
+  }
+  gram_mirror(m, G);
+  free(xc);
+  return ORACLE_OK;
 }
 
 /* ------------------------------------------------------------------ */
-/* 4. Symmetric eigendecomposition of G by cyclic-by-row Jacobi        */
+/* 4. Symmetric eigendecomposition of G by Jacobi rotations            */
 /*    (Golub & Van Loan, "Matrix Computations", Alg. 8.5.2 sym.schur2  */
-/*    + Alg. 8.5.3 cyclic Jacobi; Rutishauser's update formulas).      */
+/*    for each rotation; parallel ordering of Sec. 8.5.5: every sweep  */
+/*    visits all pairs (p, q) in m'-1 steps of m'/2 DISJOINT pairs      */
+/*    (round-robin "chess tournament" ordering, m' = m rounded up to   */
+/*    even).  Rotations of one step touch disjoint index pairs, so     */
+/*    J = prod J_u is applied as A <- J^T A J (rows, then columns) —   */
+/*    mathematically the same as applying them one after another.     */
+/*    A sweep with no rotation ends the iteration.                     */
 /*    On return lam[0..m) is descending (ties by original index),      */
 /*    lam_r clamped at 0 is NOT applied here (caller decides), and     */
 /*    V[j*m + r] is component j of eigenvector r, with the sign rule   */
@@ -103,10 +145,28 @@ static int cmp_eig_desc(const void* pa, const void* pb) {
   return (a->idx < b->idx) ? -1 : (a->idx > b->idx);
 }
 
+/* pair u of step s among n (even) indices: index n-1 is fixed, the others rotate */
+static void rr_pair(int64_t n, int64_t s, int64_t u, int64_t* p, int64_t* q) {
+  int64_t a, b;
+  if (u == 0) { a = n - 1; b = s; }
+  else { a = (s + u) % (n - 1); b = (s - u + (n - 1)) % (n - 1); }
+  *p = a < b ? a : b;
+  *q = a < b ? b : a;
+}
+
 int oracle_jacobi_eig(const double* G, int64_t m, double* lam, double* V, int max_sweeps) {
   double* A = (double*)malloc(sizeof(double) * (size_t)(m * m));
   double* W = (double*)malloc(sizeof(double) * (size_t)(m * m)); /* W = V^T: row r = eigvec r */
-  if (!A || !W) { free(A); free(W); return -1; }
+  const int64_t n = (m % 2 == 0) ? m : m + 1;
+  const int64_t half = n / 2;
+  int64_t* pp = (int64_t*)malloc(sizeof(int64_t) * (size_t)half);
+  int64_t* qq = (int64_t*)malloc(sizeof(int64_t) * (size_t)half);
+  double* cc = (double*)malloc(sizeof(double) * (size_t)half);
+  double* ss = (double*)malloc(sizeof(double) * (size_t)half);
+  if (!A || !W || !pp || !qq || !cc || !ss) {
+    free(A); free(W); free(pp); free(qq); free(cc); free(ss);
+    return -1;
+  }
   memcpy(A, G, sizeof(double) * (size_t)(m * m));
   double fro = 0.0;
   for (int64_t i = 0; i < m * m; ++i) fro = fro + A[i] * A[i];
@@ -116,42 +176,56 @@ int oracle_jacobi_eig(const double* G, int64_t m, double* lam, double* V, int ma
     for (int64_t j = 0; j < m; ++j) W[i * m + j] = (i == j) ? 1.0 : 0.0;
 
   int sweep = 0;
-  for (; sweep < max_sweeps; ++sweep) {
+  for (; sweep < max_sweeps && m > 1; ++sweep) {
     int64_t rotations = 0;
-    for (int64_t p = 0; p < m - 1; ++p) {
-      for (int64_t q = p + 1; q < m; ++q) {
-        double apq = A[p * m + q];
-        double app = A[p * m + p], aqq = A[q * m + q];
+    for (int64_t s = 0; s < n - 1; ++s) {
+      /* the rotations of this step, from the current A (sym.schur2) */
+      for (int64_t u = 0; u < half; ++u) {
+        int64_t p, q;
+        rr_pair(n, s, u, &p, &q);
+        pp[u] = p; qq[u] = q; cc[u] = 1.0; ss[u] = 0.0;
+        if (q >= m) continue; /* the padding index of an odd m */
+        const double apq = A[p * m + q], app = A[p * m + p], aqq = A[q * m + q];
         if (fabs(apq) <= abs_floor) continue;
         if (fabs(apq) <= 1e-15 * sqrt(fabs(app) * fabs(aqq))) continue;
-        /* sym.schur2: choose (c, s) so that J^T A J zeroes a_pq */
-        double tau = (aqq - app) / (2.0 * apq);
-        double t = (tau >= 0.0) ? 1.0 / (tau + sqrt(1.0 + tau * tau))
-                                : -1.0 / (-tau + sqrt(1.0 + tau * tau));
-        double c = 1.0 / sqrt(1.0 + t * t);
-        double s = t * c;
-        double* Ap = A + p * m;
-        double* Aq = A + q * m;
-        for (int64_t r = 0; r < m; ++r) {
-          if (r == p || r == q) continue;
-          double arp = Ap[r], arq = Aq[r];
-          double np = c * arp - s * arq;
-          double nq = s * arp + c * arq;
-          Ap[r] = np; A[r * m + p] = np;
-          Aq[r] = nq; A[r * m + q] = nq;
-        }
-        Ap[p] = app - t * apq;
-        Aq[q] = aqq + t * apq;
-        Ap[q] = 0.0; Aq[p] = 0.0;
-        double* Wp = W + p * m;
-        double* Wq = W + q * m;
-        for (int64_t r = 0; r < m; ++r) {
-          double vp = Wp[r], vq = Wq[r];
-          Wp[r] = c * vp - s * vq;
-          Wq[r] = s * vp + c * vq;
-        }
+        const double tau = (aqq - app) / (2.0 * apq);
+        const double t = (tau >= 0.0) ? 1.0 / (tau + sqrt(1.0 + tau * tau))
+                                      : -1.0 / (-tau + sqrt(1.0 + tau * tau));
+        const double c = 1.0 / sqrt(1.0 + t * t);
+        cc[u] = c; ss[u] = t * c;
         ++rotations;
       }
+      /* A <- J^T A (rows p, q of every rotating pair) and W <- J^T W */
+#pragma omp parallel for schedule(static)
+      for (int64_t u = 0; u < half; ++u) {
+        if (ss[u] == 0.0) continue;
+        const double c = cc[u], sn = ss[u];
+        double* Ap = A + pp[u] * m; double* Aq = A + qq[u] * m;
+        double* Wp = W + pp[u] * m; double* Wq = W + qq[u] * m;
+        for (int64_t r = 0; r < m; ++r) {
+          const double x = Ap[r], y = Aq[r];
+          Ap[r] = c * x - sn * y;
+          Aq[r] = sn * x + c * y;
+          const double v = Wp[r], w = Wq[r];
+          Wp[r] = c * v - sn * w;
+          Wq[r] = sn * v + c * w;
+        }
+      }
+      /* A <- A J (columns p, q of every rotating pair), one row at a time */
+#pragma omp parallel for schedule(static)
+      for (int64_t r = 0; r < m; ++r) {
+        double* Ar = A + r * m;
+        for (int64_t u = 0; u < half; ++u) {
+          if (ss[u] == 0.0) continue;
+          const double c = cc[u], sn = ss[u];
+          const double x = Ar[pp[u]], y = Ar[qq[u]];
+          Ar[pp[u]] = c * x - sn * y;
+          Ar[qq[u]] = sn * x + c * y;
+        }
+      }
+      /* the rotated pair's off-diagonal is zero by construction of (c, s) */
+      for (int64_t u = 0; u < half; ++u)
+        if (ss[u] != 0.0) { A[pp[u] * m + qq[u]] = 0.0; A[qq[u] * m + pp[u]] = 0.0; }
     }
     if (rotations == 0) break;
   }
@@ -159,6 +233,7 @@ int oracle_jacobi_eig(const double* G, int64_t m, double* lam, double* V, int ma
   eig_pair* pr = (eig_pair*)malloc(sizeof(eig_pair) * (size_t)m);
   for (int64_t i = 0; i < m; ++i) { pr[i].lam = A[i * m + i]; pr[i].idx = i; }
   qsort(pr, (size_t)m, sizeof(eig_pair), cmp_eig_desc);
+#pragma omp parallel for schedule(static)
   for (int64_t r = 0; r < m; ++r) {
     const double* w = W + pr[r].idx * m;
     int64_t jmax = 0;
@@ -168,8 +243,20 @@ int oracle_jacobi_eig(const double* G, int64_t m, double* lam, double* V, int ma
     lam[r] = pr[r].lam;
     for (int64_t j = 0; j < m; ++j) V[j * m + r] = sg * w[j];
   }
-  free(pr); free(A); free(W);
+  free(pr); free(A); free(W); free(pp); free(qq); free(cc); free(ss);
   return sweep + 1;
+}
+
+/* Sign rule of DESIGN.md R8 applied to k given eigenvectors (V[j*k + r]), for eigenvectors
+ * computed by another routine (the LAPACK step of oracle.decompose(eig="lapack")).          */
+void oracle_sign_fix(double* V, int64_t m, int64_t k) {
+  for (int64_t r = 0; r < k; ++r) {
+    int64_t jmax = 0;
+    for (int64_t j = 1; j < m; ++j)
+      if (fabs(V[j * k + r]) > fabs(V[jmax * k + r])) jmax = j;
+    if (V[jmax * k + r] < 0.0)
+      for (int64_t j = 0; j < m; ++j) V[j * k + r] = -V[j * k + r];
+  }
 }
 
 /* ------------------------------------------------------------------ */
@@ -265,84 +352,110 @@ typedef struct {
   int32_t status;
 } oracle_report;
 
-int oracle_decompose(const float* X, int64_t l, int64_t m, int32_t k, int64_t n_top_req,
-                     int32_t use_heap, double* mu, double* V, double* sigma, double* lam_all,
-                     int64_t* top_idx, double* rho, oracle_report* rep) {
-  memset(rep, 0, sizeof(*rep));
+/* Phase 1 of the pass: validation, mu and G = Xc^T Xc. */
+int oracle_mean_gram(const float* X, int64_t l, int64_t m, int32_t k, double* mu, double* G) {
   /* validation (R1, R5) */
+  if (l < 2 || m < 2 || k < 1 || k > (l < m ? l : m)) return ORACLE_EINVAL;
+  int bad = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad)
+  for (int64_t i = 0; i < l; ++i)
+    for (int64_t j = 0; j < m; ++j)
+      if (!isfinite(X[i * m + j])) bad = 1;
+  if (bad) return ORACLE_ENONFINITE;
+  oracle_column_mean(X, l, m, mu);
+  return oracle_gram_x(X, l, m, mu, G);
+}
+
+/* Phase 3 of the pass, given mu, the eigenvalues lam[0..k] of G (lam[k] only if k < m), the
+ * eigenvectors V_k (V[j*k + r], sign rule applied) and tr(G):
+ *   spike / tail row by row: p_i = xc_i V_k, S_i = p_i V_k^T, T_i = xc_i - S_i,
+ *   elementwise and closed-form energies, E_top, rho and
+ *   cross.
+ * Row sums are taken over fixed blocks of rows (ORACLE_NB blocks, each summed in row order, the
+ * block partials then added in block order), so the result does not depend on the thread count. */
+#define ORACLE_NB 256
+int oracle_finish(const float* X, int64_t l, int64_t m, int32_t k, int64_t n_top_req, int32_t use_heap,
+                  const double* mu, const double* lam, const double* V, double trace, double* sigma,
+                  int64_t* top_idx, double* rho, oracle_report* rep) {
+  memset(rep, 0, sizeof(*rep));
   if (l < 2 || m < 2 || k < 1 || k > (l < m ? l : m) || n_top_req < 1) {
     rep->status = ORACLE_EINVAL; return ORACLE_EINVAL;
   }
-  for (int64_t t = 0; t < l * m; ++t)
-    if (!isfinite(X[t])) { rep->status = ORACLE_ENONFINITE; return ORACLE_ENONFINITE; }
-
-  double* Xc = (double*)malloc(sizeof(double) * (size_t)(l * m));
-  double* G = (double*)malloc(sizeof(double) * (size_t)(m * m));
-  double* Vall = (double*)malloc(sizeof(double) * (size_t)(m * m));
-  double* lam = (double*)malloc(sizeof(double) * (size_t)m);
-  double* P = (double*)malloc(sizeof(double) * (size_t)(l * k));
-  double* csS = (double*)calloc((size_t)m, sizeof(double));
-  double* csT = (double*)calloc((size_t)m, sizeof(double));
-  double* S_row = (double*)malloc(sizeof(double) * (size_t)m);
-  if (!Xc || !G || !Vall || !lam || !P || !csS || !csT || !S_row) {
-    free(Xc); free(G); free(Vall); free(lam); free(P); free(csS); free(csT); free(S_row);
-    rep->status = ORACLE_ENOMEM; return ORACLE_ENOMEM;
-  }
-
-  /* mu, Xc */
-  oracle_column_mean(X, l, m, mu);
-  oracle_center(X, l, m, mu, Xc);
-
-  /* truncated SVD of Xc through G = Xc^T Xc */
-  oracle_gram(Xc, l, m, G);
-  rep->sweeps = oracle_jacobi_eig(G, m, lam, Vall, 60);
-  double trace = 0.0;
-  for (int64_t j = 0; j < m; ++j) trace = trace + G[j * m + j];
   rep->trace_g = trace;
-  for (int64_t r = 0; r < m; ++r)
-    if (lam_all) lam_all[r] = lam[r];
   double sum_lam_k = 0.0;
   for (int32_t r = 0; r < k; ++r) {
     double lr = lam[r] > 0.0 ? lam[r] : 0.0; /* DESIGN.md R9: sigma = sqrt(max(lam, 0)) */
     sigma[r] = sqrt(lr);
     sum_lam_k = sum_lam_k + lr;
-    for (int64_t j = 0; j < m; ++j) V[j * k + r] = Vall[j * m + r];
   }
   rep->sigma_next = (k < m) ? sqrt(lam[k] > 0.0 ? lam[k] : 0.0) : 0.0;
 
-  /* spike / tail row by row: p_i = xc_i V_k, S_i = p_i V_k^T, T_i = xc_i - S_i */
+  const int64_t nb = l < ORACLE_NB ? l : ORACLE_NB;
+  double* P = (double*)malloc(sizeof(double) * (size_t)(l * k));
+  double* part = (double*)calloc((size_t)(nb * 4), sizeof(double));
+  double* csS = (double*)calloc((size_t)(nb * m), sizeof(double));
+  double* csT = (double*)calloc((size_t)(nb * m), sizeof(double));
+  if (!P || !part || !csS || !csT) {
+    free(P); free(part); free(csS); free(csT);
+    rep->status = ORACLE_ENOMEM; return ORACLE_ENOMEM;
+  }
+  int oom = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(| : oom)
+  for (int64_t blk = 0; blk < nb; ++blk) {
+    const int64_t i0 = l * blk / nb, i1 = l * (blk + 1) / nb;
+    double* xc = (double*)malloc(sizeof(double) * (size_t)m);
+    double* S_row = (double*)malloc(sizeof(double) * (size_t)m);
+    if (!xc || !S_row) { free(xc); free(S_row); oom = 1; continue; }
+    double sx2 = 0.0, sS2 = 0.0, sT2 = 0.0, sST = 0.0;
+    double* cS = csS + blk * m;
+    double* cT = csT + blk * m;
+    for (int64_t i = i0; i < i1; ++i) {
+      for (int64_t j = 0; j < m; ++j) xc[j] = (double)X[i * m + j] - mu[j];
+      double* p = P + i * k;
+      for (int32_t r = 0; r < k; ++r) {
+        double s = 0.0;
+        for (int64_t j = 0; j < m; ++j) s = s + xc[j] * V[j * k + r];
+        p[r] = s;
+      }
+      for (int64_t j = 0; j < m; ++j) {
+        double s = 0.0;
+        for (int32_t r = 0; r < k; ++r) s = s + p[r] * V[j * k + r];
+        S_row[j] = s;
+      }
+      for (int64_t j = 0; j < m; ++j) {
+        double x = (double)X[i * m + j];
+        double Sij = S_row[j];
+        double Tij = xc[j] - Sij;
+        sx2 = sx2 + x * x;
+        sS2 = sS2 + Sij * Sij;
+        sT2 = sT2 + Tij * Tij;
+        sST = sST + Sij * Tij;
+        cS[j] = cS[j] + Sij;
+        cT[j] = cT[j] + Tij;
+      }
+    }
+    part[blk * 4 + 0] = sx2; part[blk * 4 + 1] = sS2; part[blk * 4 + 2] = sT2; part[blk * 4 + 3] = sST;
+    free(xc); free(S_row);
+  }
+  if (oom) {
+    free(P); free(part); free(csS); free(csT);
+    rep->status = ORACLE_ENOMEM; return ORACLE_ENOMEM;
+  }
   double sum_x2 = 0.0, sum_S2 = 0.0, sum_T2 = 0.0, sum_ST = 0.0;
-  for (int64_t i = 0; i < l; ++i) {
-    const double* xc = Xc + i * m;
-    double* p = P + i * k;
-    for (int32_t r = 0; r < k; ++r) {
-      double s = 0.0;
-      for (int64_t j = 0; j < m; ++j) s = s + xc[j] * V[j * k + r];
-      p[r] = s;
-    }
-    for (int64_t j = 0; j < m; ++j) {
-      double s = 0.0;
-      for (int32_t r = 0; r < k; ++r) s = s + p[r] * V[j * k + r];
-      S_row[j] = s;
-    }
-    for (int64_t j = 0; j < m; ++j) {
-      double x = (double)X[i * m + j];
-      double Sij = S_row[j];
-      double Tij = xc[j] - Sij;
-      sum_x2 = sum_x2 + x * x;
-      sum_S2 = sum_S2 + Sij * Sij;
-      sum_T2 = sum_T2 + Tij * Tij;
-      sum_ST = sum_ST + Sij * Tij;
-      csS[j] = csS[j] + Sij;
-      csT[j] = csT[j] + Tij;
-    }
+  for (int64_t blk = 0; blk < nb; ++blk) {
+    sum_x2 = sum_x2 + part[blk * 4 + 0];
+    sum_S2 = sum_S2 + part[blk * 4 + 1];
+    sum_T2 = sum_T2 + part[blk * 4 + 2];
+    sum_ST = sum_ST + part[blk * 4 + 3];
   }
   double sum_mu2 = 0.0, MS = 0.0, MT = 0.0, amS = 0.0, amT = 0.0;
   for (int64_t j = 0; j < m; ++j) {
+    double sS = 0.0, sT = 0.0;
+    for (int64_t blk = 0; blk < nb; ++blk) { sS = sS + csS[blk * m + j]; sT = sT + csT[blk * m + j]; }
     sum_mu2 = sum_mu2 + mu[j] * mu[j];
-    MS = MS + mu[j] * csS[j];
-    MT = MT + mu[j] * csT[j];
-    double a = fabs(csS[j] / (double)l), b = fabs(csT[j] / (double)l);
+    MS = MS + mu[j] * sS;
+    MT = MT + mu[j] * sT;
+    double a = fabs(sS / (double)l), b = fabs(sT / (double)l);
     if (a > amS) amS = a;
     if (b > amT) amT = b;
   }
@@ -364,27 +477,72 @@ int oracle_decompose(const float* X, int64_t l, int64_t m, int32_t k, int64_t n_
   int64_t n_top = use_heap ? oracle_top_set_heap(X, l, m, n_top_req, top_idx)
                            : oracle_top_set_sort(X, l, m, n_top_req, top_idx);
   rep->n_top = n_top;
-  double agg[4] = {0, 0, 0, 0}, eM = 0, eS = 0, eT = 0, eX = 0;
+  double* Sv = (double*)malloc(sizeof(double) * (size_t)(n_top > 0 ? 2 * n_top : 1));
+  if (!Sv) {
+    free(P); free(part); free(csS); free(csT);
+    rep->status = ORACLE_ENOMEM; return ORACLE_ENOMEM;
+  }
+#pragma omp parallel for schedule(static)
   for (int64_t t = 0; t < n_top; ++t) {
     int64_t i = top_idx[t] / m, j = top_idx[t] % m;
     double x = (double)X[i * m + j];
     double M = mu[j];
     double Sij = 0.0;
     for (int32_t r = 0; r < k; ++r) Sij = Sij + P[i * k + r] * V[j * k + r];
-    double Tij = Xc[i * m + j] - Sij;
+    double Tij = (x - mu[j]) - Sij;
     double x2 = x * x;
     double rm = M * M / x2, rs = Sij * Sij / x2, rt = Tij * Tij / x2;
     double cr = 1.0 - (rm + rs + rt);
     rho[t * 4 + 0] = rm; rho[t * 4 + 1] = rs; rho[t * 4 + 2] = rt; rho[t * 4 + 3] = cr;
-    agg[0] = agg[0] + rm; agg[1] = agg[1] + rs; agg[2] = agg[2] + rt; agg[3] = agg[3] + cr;
-    eM = eM + M * M; eS = eS + Sij * Sij; eT = eT + Tij * Tij; eX = eX + x2;
+    Sv[2 * t] = Sij; Sv[2 * t + 1] = Tij;
+  }
+  double agg[4] = {0, 0, 0, 0}, eM = 0, eS = 0, eT = 0, eX = 0;
+  for (int64_t t = 0; t < n_top; ++t) {
+    int64_t j = top_idx[t] % m;
+    double x = (double)X[top_idx[t]];
+    double x2 = x * x;
+    agg[0] = agg[0] + rho[t * 4 + 0]; agg[1] = agg[1] + rho[t * 4 + 1];
+    agg[2] = agg[2] + rho[t * 4 + 2]; agg[3] = agg[3] + rho[t * 4 + 3];
+    eM = eM + mu[j] * mu[j]; eS = eS + Sv[2 * t] * Sv[2 * t]; eT = eT + Sv[2 * t + 1] * Sv[2 * t + 1]; eX = eX + x2;
   }
   for (int c = 0; c < 4; ++c) rep->rho_mean_aggr[c] = n_top > 0 ? agg[c] / (double)n_top : 0.0;
   rep->rho_energy_aggr[0] = eX > 0 ? eM / eX : 0.0;
   rep->rho_energy_aggr[1] = eX > 0 ? eS / eX : 0.0;
   rep->rho_energy_aggr[2] = eX > 0 ? eT / eX : 0.0;
 
-  free(Xc); free(G); free(Vall); free(lam); free(P); free(csS); free(csT); free(S_row);
+  free(P); free(part); free(csS); free(csT); free(Sv);
   rep->status = ORACLE_OK;
   return ORACLE_OK;
+}
+
+int oracle_decompose(const float* X, int64_t l, int64_t m, int32_t k, int64_t n_top_req,
+                     int32_t use_heap, double* mu, double* V, double* sigma, double* lam_all,
+                     int64_t* top_idx, double* rho, oracle_report* rep) {
+  memset(rep, 0, sizeof(*rep));
+  if (l < 2 || m < 2 || k < 1 || k > (l < m ? l : m) || n_top_req < 1) {
+    rep->status = ORACLE_EINVAL; return ORACLE_EINVAL;
+  }
+  double* G = (double*)malloc(sizeof(double) * (size_t)(m * m));
+  double* Vall = (double*)malloc(sizeof(double) * (size_t)(m * m));
+  double* lam = (double*)malloc(sizeof(double) * (size_t)m);
+  if (!G || !Vall || !lam) {
+    free(G); free(Vall); free(lam);
+    rep->status = ORACLE_ENOMEM; return ORACLE_ENOMEM;
+  }
+  /* mu, G */
+  int st = oracle_mean_gram(X, l, m, k, mu, G);
+  if (st != ORACLE_OK) { free(G); free(Vall); free(lam); rep->status = st; return st; }
+  /* truncated SVD of Xc through the eigenpairs of G */
+  const int sweeps = oracle_jacobi_eig(G, m, lam, Vall, 60);
+  double trace = 0.0;
+  for (int64_t j = 0; j < m; ++j) trace = trace + G[j * m + j];
+  for (int64_t r = 0; r < m; ++r)
+    if (lam_all) lam_all[r] = lam[r];
+  for (int32_t r = 0; r < k; ++r)
+    for (int64_t j = 0; j < m; ++j) V[j * k + r] = Vall[j * m + r];
+  free(G); free(Vall);
+  st = oracle_finish(X, l, m, k, n_top_req, use_heap, mu, lam, V, trace, sigma, top_idx, rho, rep);
+  rep->sweeps = sweeps;
+  free(lam);
+  return st;
 }

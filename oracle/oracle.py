@@ -29,7 +29,7 @@ def build(force: bool = False) -> str:
     """Compile the oracle (plain C, fp64, IEEE order: -ffp-contract=off, no fast-math)."""
     os.makedirs(os.path.dirname(_LIB), exist_ok=True)
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        cmd = ["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
+        cmd = ["gcc", "-O3", "-mavx2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
                "-shared", _SRC, "-o", _LIB + ".tmp", "-lm"]
         subprocess.check_call(cmd)
         os.replace(_LIB + ".tmp", _LIB)
@@ -71,6 +71,14 @@ def _load():
         lib.oracle_decompose.argtypes = [P, I64, I64, ctypes.c_int32, I64, ctypes.c_int32,
                                          P, P, P, P, P, P, ctypes.POINTER(OracleReport)]
         lib.oracle_decompose.restype = ctypes.c_int
+        lib.oracle_gram_x.argtypes = [P, I64, I64, P, P]
+        lib.oracle_gram_x.restype = ctypes.c_int
+        lib.oracle_mean_gram.argtypes = [P, I64, I64, ctypes.c_int32, P, P]
+        lib.oracle_mean_gram.restype = ctypes.c_int
+        lib.oracle_finish.argtypes = [P, I64, I64, ctypes.c_int32, I64, ctypes.c_int32, P, P, P,
+                                      ctypes.c_double, P, P, P, ctypes.POINTER(OracleReport)]
+        lib.oracle_finish.restype = ctypes.c_int
+        lib.oracle_sign_fix.argtypes = [P, I64, I64]
         _lib = lib
     return _lib
 
@@ -150,8 +158,13 @@ def top_set(X, n_top: int, heap: bool = False) -> np.ndarray:
 
 # ---- the whole pass ----------------------------------------------------------------------
 def decompose(X, k: int | None = None, n_top: int | None = None, k_frac: float = 0.01,
-              top_frac: float = 0.001, heap: bool | None = None) -> dict:
-    """Full mean/spike/tail decomposition + top-0.1% attribution of X (fp32 l x m)."""
+              top_frac: float = 0.001, heap: bool | None = None, eig: str = "jacobi") -> dict:
+    """Full mean/spike/tail decomposition + top-0.1% attribution of X (fp32 l x m).
+
+    eig = "jacobi": the oracle's own parallel cyclic Jacobi eigensolve of G (the default; every
+    pin runs it).  eig = "lapack": the eigen step is numpy.linalg.eigh (LAPACK dsyevd) on the same
+    G — a library primitive serving as that one step, for m in the thousands where
+    the Jacobi sweeps take hours; the Gram, E_top, energies and rho stay the oracle's C code."""
     X = _f32(X)
     l, m = X.shape
     k = rank_k(m, k_frac) if k is None else int(k)
@@ -165,9 +178,26 @@ def decompose(X, k: int | None = None, n_top: int | None = None, k_frac: float =
     idx = np.empty(max(n_top, 1), np.int64)
     rho = np.empty((max(n_top, 1), 4), np.float64)
     rep = OracleReport()
-    st = _load().oracle_decompose(_ptr(X), l, m, k, n_top, int(heap), _ptr(mu), _ptr(V),
+    lib = _load()
+    if eig == "jacobi":
+        st = lib.oracle_decompose(_ptr(X), l, m, k, n_top, int(heap), _ptr(mu), _ptr(V),
                                   _ptr(sigma), _ptr(lam), _ptr(idx), _ptr(rho),
                                   ctypes.byref(rep))
+    elif eig == "lapack":
+        G = np.empty((m, m), np.float64)
+        st = lib.oracle_mean_gram(_ptr(X), l, m, k, _ptr(mu), _ptr(G))
+        if st == 0:
+            trace = float(sum(float(G[j, j]) for j in range(m)))  # row order, as the C pass
+            w, U = np.linalg.eigh(G)
+            order = np.lexsort((np.arange(m), -w))  # descending, ties by index
+            lam[:] = w[order]
+            V[:] = U[:, order[:k]]
+            lib.oracle_sign_fix(_ptr(V), m, k)
+            del G, U
+            st = lib.oracle_finish(_ptr(X), l, m, k, n_top, int(heap), _ptr(mu), _ptr(lam), _ptr(V),
+                                   trace, _ptr(sigma), _ptr(idx), _ptr(rho), ctypes.byref(rep))
+    else:
+        raise ValueError(eig)
     if st != 0:
         raise ValueError(f"oracle_decompose status {st}")
     n = rep.n_top
@@ -180,8 +210,17 @@ def decompose(X, k: int | None = None, n_top: int | None = None, k_frac: float =
         cross_el=np.array(rep.cross_el[:]), colmean_absmax=np.array(rep.colmean_absmax[:]),
         rho_mean_aggr=np.array(rep.rho_mean_aggr[:]),
         rho_energy_aggr=np.array(rep.rho_energy_aggr[:]),
-        trace_g=rep.trace_g, sweeps=rep.sweeps,
+        trace_g=rep.trace_g, sweeps=rep.sweeps, eig=eig,
     )
+
+
+def gram_x(X, mu) -> np.ndarray:
+    """G = Xc^T Xc formed from fp32 X and mu in row chunks (no l x m fp64 copy)."""
+    X = _f32(X)
+    mu = np.ascontiguousarray(mu, np.float64)
+    G = np.empty((X.shape[1], X.shape[1]), np.float64)
+    _load().oracle_gram_x(_ptr(X), X.shape[0], X.shape[1], _ptr(mu), _ptr(G))
+    return G
 
 
 def mean_diagnostics(X) -> dict:

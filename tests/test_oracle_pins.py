@@ -40,6 +40,12 @@ def test_worked_example_2x2():
     np.testing.assert_allclose(r["energy_cf"], g["energy_cf"], rtol=1e-14, atol=1e-13)
     np.testing.assert_array_equal(r["top_idx"], g["top_idx"])
     np.testing.assert_allclose(r["rho"], g["rho"], atol=1e-14)
+    np.testing.assert_allclose(r["rho_mean_aggr"], g["rho_mean_aggr"], atol=1e-14)
+    np.testing.assert_allclose(r["rho_energy_aggr"], g["rho_energy_aggr"], atol=1e-14)
+    np.testing.assert_allclose(r["cross_el"], g["cross_el"], atol=1e-13)
+    np.testing.assert_allclose(r["colmean_absmax"], g["colmean_absmax"], atol=1e-14)
+    np.testing.assert_allclose(r["energy_el"], g["energy_el"], rtol=1e-14, atol=1e-13)
+    assert abs(r["sigma_next"] - g["sigma_next"]) <= 1e-7  # sqrt of a ~1e-16 rounding residue
 
 
 def test_column_mean_and_center_examples():
@@ -240,6 +246,17 @@ def test_decompose_vs_numpy_svd(l, m, k):
     x2 = Xd[i, j] ** 2
     rho = np.stack([mu[j] ** 2 / x2, spike[i, j] ** 2 / x2, tail[i, j] ** 2 / x2], 1)
     np.testing.assert_allclose(r["rho"][:, :3], rho, atol=1e-9)
+    # aggregates over E_top (R10): mean of the per-entry shares, energy-weighted shares
+    np.testing.assert_allclose(r["rho_mean_aggr"][:3], rho.mean(axis=0), atol=1e-10)
+    np.testing.assert_allclose(r["rho_mean_aggr"][3], 1.0 - rho.sum(1).mean(), atol=1e-10)
+    comp = np.stack([mu[j] ** 2, spike[i, j] ** 2, tail[i, j] ** 2], 1)
+    np.testing.assert_allclose(r["rho_energy_aggr"], comp.sum(0) / x2.sum(), rtol=1e-9, atol=1e-12)
+    # cross terms and column means of the spike / tail from the numpy SVD
+    M = np.broadcast_to(mu, Xd.shape)
+    cross = [np.sum(M * spike), np.sum(M * tail), np.sum(spike * tail)]
+    np.testing.assert_allclose(r["cross_el"], cross, atol=1e-9 * e[0])
+    np.testing.assert_allclose(r["colmean_absmax"], [np.abs(spike.mean(0)).max(), np.abs(tail.mean(0)).max()],
+                               atol=1e-10 * np.abs(Xd).max())
     # subspace: V_k spans the top right singular vectors
     np.testing.assert_allclose(np.abs(Vt[:k] @ r["V"]), np.eye(k), atol=1e-8)
 
@@ -345,3 +362,42 @@ def test_mean_diagnostics_zero_mean():
     X = torch.outer(walsh(3, ii), walsh(5, jj)).float().numpy()
     d = O.mean_diagnostics(X)
     assert d["mu_norm"] == 0.0 and d["sign_fraction"] == 0.0 and d["cos_mu_v1"] == 0.0 and d["R"] == 0.0
+
+
+# ---------------------------------------------------------------- scaled oracle
+def test_gram_x_equals_explicit_centring():
+    """The row-chunked Gram from fp32 X (no l x m fp64 copy) is bit-identical to the Gram of
+    the explicit Xc, and both equal numpy's fp64 product to rounding."""
+    X = generate(SynthSpec(700, 96, seed=41)).numpy()
+    mu = O.column_mean(X)
+    G1 = O.gram_x(X, mu)
+    G2 = O.gram(O.center(X, mu))
+    np.testing.assert_array_equal(G1, G2)
+    Xc = X.astype(np.float64) - mu
+    np.testing.assert_allclose(G1, Xc.T @ Xc, rtol=1e-12, atol=1e-12 * np.abs(G1).max())
+
+
+@pytest.mark.parametrize("m", [7, 8, 33])
+def test_parallel_jacobi_odd_even_sizes(m):
+    """Round-robin parallel Jacobi on even and odd m (padding index) against numpy eigh."""
+    rng = np.random.default_rng(m)
+    A = rng.standard_normal((3 * m, m))
+    G = A.T @ A
+    lam, V, sweeps = O.jacobi_eig(G)
+    w = np.linalg.eigvalsh(G)[::-1]
+    np.testing.assert_allclose(lam, w, rtol=1e-12, atol=1e-12 * w[0])
+    np.testing.assert_allclose(V.T @ V, np.eye(m), atol=1e-12)
+    np.testing.assert_allclose(G @ V, V * lam, atol=1e-11 * w[0])
+    assert sweeps < 20
+
+
+def test_lapack_eig_step_matches_jacobi():
+    """decompose(eig="lapack") (numpy eigh as the eigen step) gives the Jacobi oracle's outputs."""
+    X = generate(SynthSpec(2048, 256, seed=43)).numpy()
+    a = O.decompose(X)
+    b = O.decompose(X, eig="lapack")
+    np.testing.assert_allclose(b["sigma"], a["sigma"], rtol=1e-11)
+    np.testing.assert_allclose(b["V"], a["V"], atol=1e-9)
+    np.testing.assert_array_equal(b["top_idx"], a["top_idx"])
+    np.testing.assert_allclose(b["rho"], a["rho"], atol=1e-10)
+    np.testing.assert_allclose(b["energy_cf"], a["energy_cf"], rtol=1e-11)
