@@ -47,7 +47,10 @@ typedef enum {
   AVD_ENOCONV = 3,     /* eigensolver hit max_iters before eig_tol; outputs still written */
   AVD_ECUDA = 4,       /* a CUDA runtime / driver call failed                             */
   AVD_ENOMEM = 6,      /* device allocation failed                                       */
-  AVD_ESTATE = 8       /* stage called out of order                                      */
+  AVD_ESTATE = 8,      /* stage called out of order                                      */
+  AVD_EREPEAT = 9      /* (stage API only) avd_stage_eig raised the Gram operand to 3 digits:
+                          call avd_stage_gram again (exchange GRAM, QSUM, QERR), then
+                          avd_stage_eig; avd_decompose handles this internally              */
 } avd_status;
 
 /* Sizes derived from (l, m, fractions) — DESIGN.md R1, R2:
@@ -58,7 +61,7 @@ typedef struct {
   int32_t k;               /* spike rank                                                    */
   int32_t p;               /* subspace-iteration block size = roundup16(k + 8)              */
   int64_t n_top;           /* |E_top| requested (global)                                    */
-  int32_t digits;          /* int8 digit planes per centred entry in the Gram (2 or 3)      */
+  int32_t digits;          /* int8 digit planes the Gram STARTS with (2 or 3; see avd_config) */
   size_t workspace_bytes;  /* device bytes avd_create will allocate                         */
 } avd_plan_t;
 
@@ -74,7 +77,12 @@ typedef struct {
   uint64_t seed;           /* start block of the subspace iteration + Gram dither            */
   int32_t max_iters;       /* subspace iterations cap (0 -> 200)                             */
   double eig_tol;          /* Ritz residual tolerance relative to lambda_1 (0 -> 1e-6)       */
-  int32_t digits;          /* 0 -> 2; Gram operand = centred X in `digits` int8 digit planes */
+  int32_t digits;          /* Gram operand = centred X in int8 digit planes:
+                              0 (default) = automatic: 2 digits (14 bits of each column's
+                              range), raised to 3 (21 bits) when the a-posteriori bound of the
+                              quantisation error on sigma_k or on the spike/tail energy shares
+                              exceeds half the north-star tolerance (1e-4 on sigma, 1e-5 on
+                              the shares; see precision_sigma / precision_share); 2 or 3 = fixed */
   int32_t world;           /* ranks sharing the rows (1 = single GPU)                        */
   int32_t device;          /* CUDA device ordinal                                            */
   void* stream;            /* cudaStream_t (NULL = legacy default stream)                    */
@@ -113,6 +121,14 @@ typedef struct {
   int32_t rr_checks;      /* Rayleigh-Ritz checks of the eigensolver (diagnostic)           */
   int32_t jacobi_sweeps;   /* total sweeps of the p x p Jacobi solves (diagnostic)           */
   int32_t requantised;     /* 1 if the Gram operand was re-quantised with exact column ranges */
+  int32_t digits_used;     /* digit planes of the final Gram (3 after an automatic escalation) */
+  double precision_sigma;  /* 5-sigma bound of the relative error of sigma_r (max over r < k)
+                              from the operand's quantisation noise: the first-order
+                              perturbation of lambda_r by the dithered rounding errors e_ia
+                              (|E e| = 0, var e <= 1/4 in units of the column step d_a):
+                              std(d lambda_r) <= sigma_r sqrt(sum_a d_a^2 v_ra^2)            */
+  double precision_share;  /* 5-sigma bound of |d share| / share for the spike and tail shares:
+                              std(d E_spike) <= sqrt(sum_a d_a^2 sum_r lambda_r v_ra^2)       */
   /* mean-bias diagnostics ("Mean bias phenomenon"; Eq. R):
    *   p_i = x_i^T mu_hat (mu_hat = mu / ||mu||); sign_fraction = max(#p_i > 0, #p_i < 0) / l
    *   (-1 when unavailable: m % 4 != 0 projection path; 0 when mu = 0);

@@ -13,6 +13,7 @@ LIB_PATH = os.path.join(HERE, "libavd.so")
 
 AVD_FLAG_STREAM_SELECT, AVD_FLAG_EXACT_SCALE = 1, 2
 AVD_OK, AVD_EINVAL, AVD_ENONFINITE, AVD_ENOCONV, AVD_ECUDA, AVD_ENOMEM, AVD_ESTATE = 0, 1, 2, 3, 4, 6, 8
+AVD_EREPEAT = 9
 BUF = dict(STATS=0, COLMAX=1, COLMIN=2, HIST1=3, GRAM=4, ENERGY=5, HIST2=6, HIST3=7, TIES=8, AGG=9,
            HIST0=10, CAND=11, SAMPLE=12, SMAX=13, SMIN=14, QSUM=15, QERR=21,
            MU=16, G=17, P=18, DIGITS=19, SCALE=20)
@@ -53,7 +54,8 @@ class avd_outputs(ctypes.Structure):
                 ("sigma_next", ctypes.c_double), ("trace_g", ctypes.c_double),
                 ("iters", ctypes.c_int32), ("max_resid", ctypes.c_double),
                 ("rr_checks", ctypes.c_int32), ("jacobi_sweeps", ctypes.c_int32),
-                ("requantised", ctypes.c_int32),
+                ("requantised", ctypes.c_int32), ("digits_used", ctypes.c_int32),
+                ("precision_sigma", ctypes.c_double), ("precision_share", ctypes.c_double),
                 ("mean_R", ctypes.c_double), ("sign_fraction", ctypes.c_double),
                 ("p_pos", ctypes.c_int64), ("p_neg", ctypes.c_int64),
                 ("cos_mu_v1", ctypes.c_double), ("alpha1", ctypes.c_double),
@@ -169,7 +171,7 @@ def avd_stage_gram(h, X_dev: int):
 
 
 def avd_stage_eig(h):
-    return check(lib().avd_stage_eig(h), "avd_stage_eig", ok=(AVD_OK, AVD_ENOCONV))
+    return check(lib().avd_stage_eig(h), "avd_stage_eig", ok=(AVD_OK, AVD_ENOCONV, AVD_EREPEAT))
 
 
 def avd_stage_project(h, X_ptr: int):

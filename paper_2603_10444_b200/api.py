@@ -40,6 +40,9 @@ class Result:
     rr_checks: int = 0
     jacobi_sweeps: int = 0
     requantised: int = 0        # 1: Gram operand re-quantised with the exact column ranges
+    digits_used: int = 2        # digit planes of the final Gram (3 after an automatic escalation)
+    precision_sigma: float = 0.0  # 5-sigma bound of the quantisation error on sigma (relative)
+    precision_share: float = 0.0  # 5-sigma bound of the quantisation error on the shares
     # mean-bias diagnostics (include/avd.h)
     mean_R: float = 0.0
     sign_fraction: float = 0.0
@@ -123,7 +126,9 @@ class Decomposer:
                       rho_energy_aggr=_to_list(o.rho_energy_aggr), sigma_next=float(o.sigma_next),
                       trace_g=float(o.trace_g), iters=int(o.iters), max_resid=float(o.max_resid),
                       status=st, rr_checks=int(o.rr_checks), jacobi_sweeps=int(o.jacobi_sweeps),
-                      requantised=int(o.requantised), mean_R=float(o.mean_R),
+                      requantised=int(o.requantised), digits_used=int(o.digits_used),
+                      precision_sigma=float(o.precision_sigma),
+                      precision_share=float(o.precision_share), mean_R=float(o.mean_R),
                       sign_fraction=float(o.sign_fraction), cos_mu_v1=float(o.cos_mu_v1),
                       alpha1=float(o.alpha1), sigma1_u=float(o.sigma1_u), iters_u=int(o.iters_u))
 

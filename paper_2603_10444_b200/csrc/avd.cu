@@ -55,7 +55,8 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   if (p > kMaxP || k > 95) { set_error("k too large for this build (p <= 112, k <= 95)"); return AVD_EINVAL; }
   const int64_t n_top = cfg->n_top_override > 0 ? cfg->n_top_override : std::max<int64_t>(1, floor_frac(cfg->top_frac, l * m));
   const int nd = cfg->digits == 0 ? 2 : cfg->digits;
-  if (nd != 2 && nd != 3) { set_error("digits must be 2 or 3"); return AVD_EINVAL; }
+  if (nd != 2 && nd != 3) { set_error("digits must be 0 (automatic), 2 or 3"); return AVD_EINVAL; }
+  const int nd_max = cfg->digits == 0 ? 3 : nd;
   plan->k = (int32_t)k;
   plan->p = (int32_t)p;
   plan->n_top = n_top;
@@ -69,6 +70,8 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   C->p = (int)p;
   C->k_pad = (int)(((k + 1 + 15) / 16) * 16);  // + one column: the mean direction (diagnostics)
   C->nd = nd;
+  C->nd_max = nd_max;
+  C->auto_digits = cfg->digits == 0;
   C->m_pad = round_up(m, kGramTile);
   C->m_pad32 = round_up(m, 32);
   C->l_pad = round_up(cfg->l_local, kGramK);
@@ -96,7 +99,7 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   L.add(sizeof(double) * m);                    // 8 mu
   L.add(sizeof(int32_t) * C->m_pad);            // 9 shift
   L.add(sizeof(DevPlan));                       // 10 dplan
-  L.add((size_t)nd * C->m_pad * C->l_pad);      // 11 digits
+  L.add((size_t)nd_max * C->m_pad * C->l_pad);  // 11 digits
   L.add(sizeof(uint32_t) * C->cand_cap);        // 12 cand_key
   L.add(sizeof(uint64_t) * C->cand_cap);        // 13 cand_idx
   L.add(2 * sizeof(unsigned long long));        // 14 cand_cnt [slot cursor, real count]
@@ -111,7 +114,7 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   L.add(sizeof(double) * 2 * p);                // 23 theta
   L.add(sizeof(double) * C->n_red * p * p);     // 24 red_part
   L.add(sizeof(double) * 2 * p);                // 25 resid
-  L.add(sizeof(double));                        // 26 trace
+  L.add(sizeof(double) * 4);                    // 26 trace
   L.add(sizeof(double) * m * k);                // 27 V
   L.add(sizeof(double) * k);                    // 28 sigma
   L.add(sizeof(float) * m * C->k_pad);          // 29 V32
@@ -154,6 +157,7 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   L.add(sizeof(float) * C->m_pad);                                       // 66 mu0
   L.add(sizeof(long long) * C->r1 * m);                                  // 67 qsq_part
   L.add(sizeof(double) * (4 + 2 * C->m_pad));                            // 68 diag: |mu|, scratch, q, y
+  L.add(sizeof(double) * kMaxP);                                         // 69 prec
   if (L.n >= 128) { set_error("workspace layout table overflow"); return AVD_EINVAL; }
   plan->workspace_bytes = L.total;
   if (lay) *lay = L;
@@ -264,6 +268,7 @@ const char* avd_strerror(avd_status s) {
     case AVD_ECUDA: return "CUDA error";
     case AVD_ENOMEM: return "out of device memory";
     case AVD_ESTATE: return "stage called out of order";
+    case AVD_EREPEAT: return "repeat avd_stage_gram: the Gram operand was raised to 3 digits";
   }
   return "unknown status";
 }
@@ -318,6 +323,7 @@ avd_status avd_create(const avd_config* cfg, avd_ctx** out) {
   BIND(samp, double*); BIND(smax, float*); BIND(smin, float*); BIND(qscale, float*); BIND(qoff, float*);
   BIND(qsum_part, long long*); BIND(qsum_local, long long*); BIND(qerr_part, float*); BIND(qerr_local, double*);
   BIND(qerr, double*); BIND(mu0, float*); BIND(qsq_part, long long*); BIND(diag, double*);
+  BIND(prec, double*);
 #undef BIND
   if (cudaMallocHost(&c->eig_host, sizeof(double) * 4 * kMaxP) != cudaSuccess) {
     cudaGetLastError();
@@ -400,7 +406,7 @@ avd_status avd_buffer(avd_ctx* c, int32_t which, void** ptr, size_t* bytes) {
     case AVD_BUF_MU: *ptr = c->mu; *bytes = sizeof(double) * m; break;
     case AVD_BUF_G: *ptr = c->G; *bytes = sizeof(double) * c->m_pad * c->m_pad; break;
     case AVD_BUF_P: *ptr = c->P; *bytes = sizeof(float) * c->cfg.l_local * c->k_pad; break;
-    case AVD_BUF_DIGITS: *ptr = c->digits; *bytes = (size_t)c->nd * c->m_pad * c->l_pad; break;
+    case AVD_BUF_DIGITS: *ptr = c->digits; *bytes = (size_t)c->nd_max * c->m_pad * c->l_pad; break;
     case AVD_BUF_SCALE: *ptr = c->shift; *bytes = sizeof(int32_t) * c->m_pad; break;
     default: set_error("unknown buffer id"); return AVD_EINVAL;
   }
@@ -420,6 +426,8 @@ avd_status avd_buffer(avd_ctx* c, int32_t which, void** ptr, size_t* bytes) {
 avd_status avd_stage_stats(avd_ctx* c, const float* X) {
   if (!c || !X) { set_error("null argument"); return AVD_EINVAL; }
   c->stage = 0;  // a new pass may start at any time
+  c->nd = c->plan.digits;  // an automatic escalation lasts for one pass
+  c->escalate = false;
   AVD_TRY(launch_sample(c, X));
   c->stage = 1;
   return AVD_OK;
@@ -436,6 +444,19 @@ avd_status avd_stage_split(avd_ctx* c, const float* X) {
 avd_status avd_stage_gram(avd_ctx* c, const float* X) {
   STAGE_CHECK(c, 2);
   if (!X) { set_error("null argument"); return AVD_EINVAL; }
+  if (c->escalate) {
+    // raised to 3 digits by avd_stage_eig: re-encode with the exact column ranges of the fused
+    // pass (already exchanged) and redo the Gram; every other statistic stands
+    c->escalate = false;
+    AVD_TRY(launch_pass1(c, X, false));
+    AVD_CUDA(cudaMemcpyAsync(c->qsum, c->qsum_local, sizeof(long long) * 2 * c->cfg.m, cudaMemcpyDeviceToDevice,
+                             c->stream));
+    AVD_CUDA(cudaMemcpyAsync(c->qerr, c->qerr_local, sizeof(double) * c->m_pad, cudaMemcpyDeviceToDevice, c->stream));
+    AVD_TRY(launch_gram(c));
+    c->requantised = true;
+    c->stage = 3;
+    return AVD_OK;
+  }
   AVD_TRY(launch_finish(c));
   double* hs = c->eig_host;  // pinned scratch
   AVD_CUDA(cudaMemcpyAsync(hs, c->stats + c->cfg.m + 3, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -473,6 +494,16 @@ avd_status avd_stage_eig(avd_ctx* c) {
   AVD_TRY(launch_gram_finalize(c));
   avd_status st = run_eig(c);
   if (st != AVD_OK && st != AVD_ENOCONV) return st;
+  // automatic digits (avd_config.digits == 0): the quantisation-error bound decides whether the
+  // 2-digit operand meets half the north-star tolerances; if not, redo the Gram with 3 digits.
+  // The decision uses only replicated values (G, V_k, shifts), so every rank takes it alike.
+  if (c->auto_digits && c->nd == 2 && (c->prec_sigma > 5e-5 || c->prec_share > 5e-6)) {
+    c->nd = 3;
+    c->escalate = true;
+    c->stage = 2;
+    set_error("Gram operand raised to 3 digits: call avd_stage_gram again");
+    return AVD_EREPEAT;
+  }
   AVD_TRY(run_uncentred(c));  // mean-bias diagnostics
   c->stage = 4;
   return st;
@@ -575,6 +606,9 @@ avd_status avd_stage_report(avd_ctx* c, avd_outputs* out) {
   out->rr_checks = c->rr_count;
   out->jacobi_sweeps = c->jacobi_sweeps;
   out->requantised = c->requantised ? 1 : 0;
+  out->digits_used = c->nd;
+  out->precision_sigma = c->prec_sigma;
+  out->precision_share = c->prec_share;
   // mean-bias diagnostics
   const double lg = (double)c->cfg.l_global;
   out->mean_R = (total > 0.0) ? h[24] / std::sqrt(total / lg) : 0.0;
@@ -600,7 +634,11 @@ avd_status avd_decompose(avd_ctx* c, const float* X, avd_outputs* out) {
   AVD_TRY(avd_stage_stats(c, X));
   AVD_TRY(avd_stage_split(c, X));
   AVD_TRY(avd_stage_gram(c, X));
-  const avd_status eig = avd_stage_eig(c);
+  avd_status eig = avd_stage_eig(c);
+  if (eig == AVD_EREPEAT) {  // automatic digits: 3-digit Gram
+    AVD_TRY(avd_stage_gram(c, X));
+    eig = avd_stage_eig(c);
+  }
   if (eig != AVD_OK && eig != AVD_ENOCONV) return eig;
   AVD_TRY(avd_stage_project(c, X));
   for (int lv = 0; lv < 4; ++lv) AVD_TRY(avd_stage_select(c, X, lv, 0));

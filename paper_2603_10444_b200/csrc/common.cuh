@@ -44,6 +44,10 @@ struct Ctx {
   int64_t l_pad = 0;     // l_local rounded up to kGramK
   int k = 0, p = 0, k_pad = 0;
   int nd = 3;
+  int nd_max = 3;        // digit planes the workspace holds (3 when digits are automatic)
+  bool auto_digits = false;
+  bool escalate = false; // stage_gram must re-encode with nd = 3 (set by stage_eig)
+  double prec_sigma = 0, prec_share = 0;  // a-posteriori quantisation-error bounds (run_eig)
   int64_t launches = 0;
   int stage = 0;         // last completed stage (ordering check)
   // K1
@@ -108,7 +112,8 @@ struct Ctx {
   int iters_u = 0;
   bool sign_valid = false;        // p_i signs available (tensor-core projection path)
   double* resid = nullptr;        // [p]
-  double* trace = nullptr;        // [1]
+  double* trace = nullptr;        // [4]: tr(G), sum_a d_a^2 G_aa (precision bound), -, -
+  double* prec = nullptr;         // [kMaxP]: t_r = sum_a d_a^2 v_ra^2 (quantisation step d_a)
   double* eig_host = nullptr;     // pinned: theta[p] + resid[p]
   cudaEvent_t ev_host = nullptr;  // host waits on this instead of the whole stream (stage_gram)
   double* V = nullptr;            // [m][k] output copy (row-major)

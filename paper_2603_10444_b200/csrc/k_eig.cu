@@ -75,27 +75,34 @@ __global__ void __launch_bounds__(256) gram_finalize_kernel(const long long* __r
   }
 }
 
-// tr(G) and max_a G_aa (= max |G_ab| for the positive semidefinite G)
+// tr(G), max_a G_aa (= max |G_ab| for the positive semidefinite G), and for the precision bound
+// (run_eig) sum_a d_a^2 G_aa over the columns with a nonzero rounding error (d_a = 2^-shift_a, the
+// quantisation step of column a in units of x)
 __global__ void __launch_bounds__(1024) trace_kernel(const double* __restrict__ G, int64_t m, int64_t ld,
-                                                    double* __restrict__ out, double* __restrict__ gmax) {
+                                                    const int32_t* __restrict__ shift,
+                                                    const double* __restrict__ qerr, double* __restrict__ out,
+                                                    double* __restrict__ gmax) {
   // fixed order: strided per-thread sums, xor-shuffle tree per warp, warp partials in order
-  __shared__ double sh[32], shm[32];
-  double s = 0.0, mx = 0.0;
+  __shared__ double sh[32], shm[32], shd[32];
+  double s = 0.0, mx = 0.0, dg = 0.0;
   for (int64_t j = threadIdx.x; j < m; j += 1024) {
     const double g = G[j * ld + j];
     s += g;
     mx = fmax(mx, fabs(g));
+    if (qerr[j] > 0.0) dg += ldexp(fmax(g, 0.0), -2 * shift[j]);
   }
   for (int o = 16; o > 0; o >>= 1) {
     s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
     mx = fmax(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    dg += __shfl_xor_sync(0xFFFFFFFFu, dg, o);
   }
-  if ((threadIdx.x & 31) == 0) { sh[threadIdx.x >> 5] = s; shm[threadIdx.x >> 5] = mx; }
+  if ((threadIdx.x & 31) == 0) { sh[threadIdx.x >> 5] = s; shm[threadIdx.x >> 5] = mx; shd[threadIdx.x >> 5] = dg; }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double t = 0.0, u = 0.0;
-    for (int i = 0; i < 32; ++i) { t += sh[i]; u = fmax(u, shm[i]); }
-    *out = t;
+    double t = 0.0, u = 0.0, d = 0.0;
+    for (int i = 0; i < 32; ++i) { t += sh[i]; u = fmax(u, shm[i]); d += shd[i]; }
+    out[0] = t;
+    out[1] = d;
     *gmax = u;
   }
 }
@@ -760,22 +767,32 @@ __global__ void resid_kernel(const double* __restrict__ Z, const double* __restr
 
 // V_out[j][r] = sign_r * U[j][r] (r < k), sign making the largest-|.| entry positive
 // (smallest j on ties; R8); sigma_r = sqrt(max(theta_r, 0)); V32 fp32 copy.
+// Also t_r = sum_a d_a^2 v_ra^2 over the columns with rounding errors (precision bound, run_eig).
 __global__ void finalize_vectors_kernel(const double* __restrict__ U, const double* __restrict__ theta, int64_t m,
-                                        int p, int k, int k_pad, double* __restrict__ V, double* __restrict__ sigma,
-                                        float* __restrict__ V32) {
-  __shared__ double sv[256];
+                                        int p, int k, int k_pad, const int32_t* __restrict__ shift,
+                                        const double* __restrict__ qerr, double* __restrict__ V,
+                                        double* __restrict__ sigma, float* __restrict__ V32, double* __restrict__ prec) {
+  __shared__ double sv[256], st[256];
   __shared__ int64_t sj[256];
   const int r = blockIdx.x;
-  double best = -1.0;
+  double best = -1.0, tr = 0.0;
   int64_t bj = 0;
   for (int64_t j = threadIdx.x; j < m; j += 256) {
-    const double a = fabs(U[j * p + r]);
+    const double u = U[j * p + r];
+    const double a = fabs(u);
     if (a > best) { best = a; bj = j; }
+    if (qerr[j] > 0.0) tr += ldexp(u * u, -2 * shift[j]);
   }
   sv[threadIdx.x] = best;
   sj[threadIdx.x] = bj;
+  st[threadIdx.x] = tr;
   __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) st[threadIdx.x] += st[threadIdx.x + o];
+    __syncthreads();
+  }
   if (threadIdx.x == 0) {
+    prec[r] = st[0];
     for (int t = 1; t < 256; ++t)
       if (sv[t] > sv[0] || (sv[t] == sv[0] && sj[t] < sj[0])) { sv[0] = sv[t]; sj[0] = sj[t]; }
   }
@@ -897,7 +914,7 @@ avd_status launch_gram_finalize(Ctx* c) {
   gram_finalize_kernel<<<grid, dim3(32, 8), 0, c->stream>>>(c->gram_i, m, c->m_pad, c->shift, c->qsum, c->qerr,
                                                     1.0 / (double)c->cfg.l_global, unit, c->G, c->G32);
   AVD_LAUNCHED(c);
-  trace_kernel<<<1, 1024, 0, c->stream>>>(c->G, m, c->m_pad, c->trace, c->gmax);
+  trace_kernel<<<1, 1024, 0, c->stream>>>(c->G, m, c->m_pad, c->shift, c->qerr, c->trace, c->gmax);
   AVD_LAUNCHED(c);
   return AVD_OK;
 }
@@ -1031,6 +1048,47 @@ avd_status orth(Ctx* c, const double* Y, uint32_t seed) {
 
 }  // namespace
 
+// A-posteriori bound of the Gram operand's quantisation error (DESIGN.md §8 "Gram precision").
+// The operand is q_ia = y_ia + e_ia, y = (x - mu0) 2^shift, with dithered rounding errors e that
+// are zero-mean, independent and var e <= 1/4 (exactly 0 for a column whose every entry is on the
+// grid: qerr_a = 0).  The centred Gram of q, with the diagonal debiased, is G + E, E_ab =
+// d_a d_b sum_i (e_ia xc_ib + xc_ia e_ib) + O(e^2) off the diagonal (d_a = 2^-shift_a), so to
+// first order
+//   d lambda_r = v_r^T E v_r = 2 sigma_r sum_i u_ri sum_a d_a v_ra e_ia,
+//   std(d lambda_r) <= sigma_r sqrt(t_r),  t_r = sum_a d_a^2 v_ra^2           (finalize kernel)
+//   d E_spike = sum_r d lambda_r = 2 sum_ia d_a e_ia S_ia,  std <= sqrt(sum_r lambda_r t_r)
+//   d tr(G) = 2 sum_ia d_a e_ia xc_ia,                       std <= sqrt(sum_a d_a^2 G_aa)
+// (the spike matrix S_ia = sum_r sigma_r u_ri v_ra).  Reported at 5 sigma:
+//   prec_sigma = max_r 2.5 sqrt(t_r) / sigma_r  (relative error of sigma_r = d lambda / 2 lambda)
+//   prec_share = max(5 std(d E_spike) / E_spike, 5 (std(d E_spike) + std(d tr)) / E_tail)
+// The automatic digit rule raises the operand to 3 digits when prec_sigma > 5e-5 or
+// prec_share > 5e-6 (half the north-star tolerances 1e-4 / 1e-5).
+avd_status precision_bound(Ctx* c) {
+  const int k = c->k;
+  double* h = c->eig_host + 2 * kMaxP;  // pinned scratch: t_r [k <= 95], tr(G), sum d^2 G_aa
+  AVD_CUDA(cudaMemcpyAsync(h, c->prec, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
+  AVD_CUDA(cudaMemcpyAsync(h + k, c->trace, sizeof(double) * 2, cudaMemcpyDeviceToHost, c->stream));
+  AVD_CUDA(cudaStreamSynchronize(c->stream));
+  double ps = 0.0, var_spike = 0.0, e_spike = 0.0;
+  for (int r = 0; r < k; ++r) {
+    const double lam = std::max(c->eig_host[r], 0.0);  // Ritz values of the last check (theta)
+    const double t = std::max(h[r], 0.0);
+    if (lam > 0.0) ps = std::max(ps, 2.5 * std::sqrt(t / lam));
+    else if (t > 0.0) ps = std::max(ps, 0.0);  // sigma_r = 0: no relative error to bound
+    var_spike += lam * t;
+    e_spike += lam;
+  }
+  const double trace = h[k], dg = std::max(h[k + 1], 0.0);
+  const double e_tail = std::max(trace - e_spike, 0.0);
+  const double sd_spike = std::sqrt(var_spike), sd_tr = std::sqrt(dg);
+  double pe = 0.0;
+  if (e_spike > 0.0) pe = std::max(pe, 5.0 * sd_spike / e_spike);
+  if (sd_spike + sd_tr > 0.0) pe = std::max(pe, e_tail > 0.0 ? 5.0 * (sd_spike + sd_tr) / e_tail : HUGE_VAL);
+  c->prec_sigma = ps;
+  c->prec_share = pe;
+  return AVD_OK;
+}
+
 // Subspace iteration: power steps Q <- orth(G^2 Q) in fp32; a Rayleigh-Ritz check (fp64) runs
 // on a schedule predicted from the observed residual decay (at most every 8 steps, always on the
 // last one), so the p x p Jacobi runs ~2-3 times per solve.
@@ -1045,7 +1103,7 @@ avd_status run_eig(Ctx* c) {
   rand_fill_kernel<<<(unsigned)ceil_div(m * p, 256), 256, 0, c->stream>>>(c->Z, nullptr, m, p, seed, nullptr);
   AVD_LAUNCHED(c);
   AVD_TRY(orth(c, c->Z, seed + 1));
-  const int max_it = c->cfg.max_iters > 0 ? c->cfg.max_iters : 100;
+  const int max_it = c->cfg.max_iters > 0 ? c->cfg.max_iters : 200;
   const double tol = c->cfg.eig_tol > 0 ? c->cfg.eig_tol : 1e-6;  // V angle <~ tol * lambda_1 / gap_k
   int it = 0, next_rr = 2, prev_it = 0, rr_count = 0;
   double maxres = 0.0, prev_res = -1.0, pred_res = -1.0;
@@ -1099,8 +1157,10 @@ avd_status run_eig(Ctx* c) {
   c->sigma_next = (k < p) ? std::sqrt(std::max(c->eig_host[k], 0.0)) : 0.0;
   // the per-solve sweep counts stay at theta + p; the report stage reads them with its packed copy
   AVD_CUDA(cudaMemsetAsync(c->V32, 0, sizeof(float) * m * c->k_pad, c->stream));
-  finalize_vectors_kernel<<<k, 256, 0, c->stream>>>(c->U, c->theta, m, p, k, c->k_pad, c->V, c->sigma, c->V32);
+  finalize_vectors_kernel<<<k, 256, 0, c->stream>>>(c->U, c->theta, m, p, k, c->k_pad, c->shift, c->qerr, c->V,
+                                                    c->sigma, c->V32, c->prec);
   AVD_LAUNCHED(c);
+  AVD_TRY(precision_bound(c));
   return conv ? AVD_OK : AVD_ENOCONV;
 }
 

@@ -467,7 +467,7 @@ int gram_pair_count(int T) {
 avd_status gram_make_tmap(Ctx* c) {
   auto enc = get_encode();
   if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return AVD_ECUDA; }
-  uint64_t dims[2] = {(uint64_t)c->m_pad, (uint64_t)(c->nd * c->l_pad)};
+  uint64_t dims[2] = {(uint64_t)c->m_pad, (uint64_t)(c->nd_max * c->l_pad)};
   uint64_t strides[1] = {(uint64_t)c->m_pad};
   uint32_t box[2] = {128, 128};
   uint32_t es[2] = {1, 1};

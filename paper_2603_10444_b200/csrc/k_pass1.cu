@@ -181,7 +181,12 @@ __global__ void prepare_kernel(int64_t m, int64_t m_pad, int nd, int exact, int6
       if (!exact) mu0[j] = c0;
       if (a > 0.0 && a < 1e300) sh = (7 * nd - 1) - (ilogb(a) + 1);
       else if (!exact) sh = 100;  // no sampled range: any deviation overflows -> exact requant
-      sh = max(-100, min(100, sh));
+      // 2^sh stays a normal fp32 and mu0 2^sh stays finite (qoff); a finite fp32 range a < 2^128
+      // gives sh >= 7 nd - 129 > -126, so the exact-range requant can never overflow the digits
+      // (|y| <= a 2^sh < 2^(7 nd - 1)), and for x != mu0, |x - mu0| >= |mu0| 2^-25 keeps
+      // |mu0| 2^sh <= 2^(7 nd + 24) whenever the range is measured
+      sh = max(-126, min(126, sh));
+      if (c0 != 0.f) sh = min(sh, 125 - ilogbf(fabsf(c0)));
       sc = __int_as_float((sh + 127) << 23);
       off = -c0 * sc;
     }

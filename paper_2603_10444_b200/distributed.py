@@ -10,7 +10,8 @@ module all-reduces exactly the exchange buffers the header lists (SURVEY.md §2.
   split   : column sums + sum x^2 + counts (SUM f64), column range about the quantiser centre (MAX)
   gram    : the exact int64 Gram partials and integer column sums of the quantised operand
             (SUM i64)  -> identical exactly-centred G on every rank
-  eig     : replicated (same G, same seed -> bit-identical V_k, sigma_k on every rank)
+  eig     : replicated (same G, same seed -> bit-identical V_k, sigma_k on every rank); may ask
+            for a 3-digit Gram (AVD_EREPEAT) -> gram again, exchange GRAM, QSUM, QERR, eig again
   project : elementwise energy sums + column sums of P (SUM f64)
   gram    : + candidate count / overflow flag (SUM i64) -> same candidate-vs-stream decision
   select  : radix histograms of |x| bits (SUM i64), per-rank sel/tie counts (SUM = all-gather)
@@ -34,6 +35,7 @@ EXCHANGES = {
     "split": [("STATS", torch.float64, "sum"), ("COLMAX", torch.float32, "max")],
     "gram": [("GRAM", torch.int64, "sum"), ("CAND", torch.int64, "sum"), ("QSUM", torch.int64, "sum"),
              ("QERR", torch.float64, "sum")],
+    "regram": [("GRAM", torch.int64, "sum"), ("QSUM", torch.int64, "sum"), ("QERR", torch.float64, "sum")],
     "project": [("ENERGY", torch.float64, "sum")],
     "select0": [("HIST0", torch.int64, "sum")],
     "select1": [("HIST2", torch.int64, "sum")],
@@ -80,7 +82,12 @@ def run_stages(backend, comm, X) -> object:
     exchange("split")
     backend.stage_gram(X)
     exchange("gram")
-    backend.stage_eig()
+    if backend.stage_eig() == L.AVD_EREPEAT:
+        # automatic digits: the replicated precision bound raised the Gram operand to 3 digits
+        # on every rank alike; redo the Gram (the candidate count is already global)
+        backend.stage_gram(X)
+        exchange("regram")
+        backend.stage_eig()
     backend.stage_project(X)
     exchange("project")
     for lv in range(4):
@@ -116,6 +123,7 @@ class _LibBackend:
 
     def stage_eig(self):
         self.eig_status = L.avd_stage_eig(self.h)
+        return self.eig_status
 
     def stage_project(self, X):
         L.avd_stage_project(self.h, X.data_ptr())
