@@ -114,7 +114,10 @@ typedef struct {
   double colmean_absmax[2];/* max_j |mean_i spike_ij|, max_j |mean_i tail_ij|  */
   double rho_mean_aggr[4]; /* mean over E_top of rho_mean, rho_spike, rho_tail, cross (R10)  */
   double rho_energy_aggr[3]; /* sum_E c^2 / sum_E x^2, c = M, spike, tail                    */
-  double sigma_next;       /* sigma_{k+1} (Ritz estimate; 0 when unavailable)                */
+  double sigma_next;       /* sigma_{k+1}: the (k+1)-th Ritz value of the converged p-column
+                              subspace, a LOWER bound of sigma_{k+1} (Cauchy interlacing),
+                              typically within a few % (its residual is not part of the
+                              convergence test); 0 when unavailable                          */
   double trace_g;          /* tr(G) = ||Xc||_F^2                                             */
   int32_t iters;           /* subspace iterations used                                       */
   double max_resid;        /* max_r<k ||G v_r - lambda_r v_r|| / lambda_1                     */

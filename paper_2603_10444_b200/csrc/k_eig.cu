@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(256) gram_finalize_kernel(const long long* __r
       //   = sum_i q_ia q_ib - S_a S_b / l   (S = column sums of q, exact integers)
       // v unit = sum_i q_ia q_ib; the diagonal is the exact sum_i q_ia^2 of the fused pass
       // (qsum[m + a]; with 3 digits the Gram drops the two lowest digit-product classes, whose
-      // diagonal part is a positive bias) minus the realised squared rounding errors (unbiased)
+      // diagonal part is a positive bias) minus qerr_a = sum_i (q_ia^2 - y_ia^2): sum_i y_ia^2
       const double qq = (a == b) ? (double)qsum[m + a] - qerr[a] : (double)v * unit;
       const double corr = ((double)qsum[a] * (double)qsum[b]) * inv_l;
       g = ldexp(qq - corr, -(shift[a] + shift[b]));
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(1024) trace_kernel(const double* __restrict__ 
     const double g = G[j * ld + j];
     s += g;
     mx = fmax(mx, fabs(g));
-    if (qerr[j] > 0.0) dg += ldexp(fmax(g, 0.0), -2 * shift[j]);
+    if (qerr[j] != 0.0) dg += ldexp(fmax(g, 0.0), -2 * shift[j]);
   }
   for (int o = 16; o > 0; o >>= 1) {
     s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
@@ -781,7 +781,7 @@ __global__ void finalize_vectors_kernel(const double* __restrict__ U, const doub
     const double u = U[j * p + r];
     const double a = fabs(u);
     if (a > best) { best = a; bj = j; }
-    if (qerr[j] > 0.0) tr += ldexp(u * u, -2 * shift[j]);
+    if (qerr[j] != 0.0) tr += ldexp(u * u, -2 * shift[j]);
   }
   sv[threadIdx.x] = best;
   sj[threadIdx.x] = bj;
@@ -1057,10 +1057,11 @@ avd_status orth(Ctx* c, const double* Y, uint32_t seed) {
 //   d lambda_r = v_r^T E v_r = 2 sigma_r sum_i u_ri sum_a d_a v_ra e_ia,
 //   std(d lambda_r) <= sigma_r sqrt(t_r),  t_r = sum_a d_a^2 v_ra^2           (finalize kernel)
 //   d E_spike = sum_r d lambda_r = 2 sum_ia d_a e_ia S_ia,  std <= sqrt(sum_r lambda_r t_r)
-//   d tr(G) = 2 sum_ia d_a e_ia xc_ia,                       std <= sqrt(sum_a d_a^2 G_aa)
-// (the spike matrix S_ia = sum_r sigma_r u_ri v_ra).  Reported at 5 sigma:
+// (the spike matrix S_ia = sum_r sigma_r u_ri v_ra).  The diagonal of G is the centred energy
+// sum y^2 - S^2/l itself (k_pass1.cu), so tr(G) carries only the fp32 rounding of y (<= 2^-24
+// relative, counted as 6e-8 tr(G)) and E_tail = tr(G) - E_spike inherits d E_spike.  At 5 sigma:
 //   prec_sigma = max_r 2.5 sqrt(t_r) / sigma_r  (relative error of sigma_r = d lambda / 2 lambda)
-//   prec_share = max(5 std(d E_spike) / E_spike, 5 (std(d E_spike) + std(d tr)) / E_tail)
+//   prec_share = max(5 std(d E_spike) / E_spike, (5 std(d E_spike) + 6e-8 tr(G)) / E_tail)
 // The automatic digit rule raises the operand to 3 digits when prec_sigma > 5e-5 or
 // prec_share > 5e-6 (half the north-star tolerances 1e-4 / 1e-5).
 avd_status precision_bound(Ctx* c) {
@@ -1078,12 +1079,13 @@ avd_status precision_bound(Ctx* c) {
     var_spike += lam * t;
     e_spike += lam;
   }
-  const double trace = h[k], dg = std::max(h[k + 1], 0.0);
+  const double trace = h[k];
   const double e_tail = std::max(trace - e_spike, 0.0);
-  const double sd_spike = std::sqrt(var_spike), sd_tr = std::sqrt(dg);
+  const double sd_spike = std::sqrt(var_spike);
   double pe = 0.0;
   if (e_spike > 0.0) pe = std::max(pe, 5.0 * sd_spike / e_spike);
-  if (sd_spike + sd_tr > 0.0) pe = std::max(pe, e_tail > 0.0 ? 5.0 * (sd_spike + sd_tr) / e_tail : HUGE_VAL);
+  if (sd_spike > 0.0 && e_tail > 0.0) pe = std::max(pe, (5.0 * sd_spike + 6e-8 * trace) / e_tail);
+  else if (sd_spike > 0.0) pe = HUGE_VAL;
   c->prec_sigma = ps;
   c->prec_share = pe;
   return AVD_OK;

@@ -14,11 +14,11 @@
 // The Gram of the quantised matrix is then centred EXACTLY (k_eig.cu gram_finalize):
 //   sum_i (q_ia - S_a/l)(q_ib - S_b/l) = sum_i q_ia q_ib - S_a S_b / l,
 // its diagonal is taken from the exact sum_i q_ia^2 accumulated here (with 3 digits the Gram drops
-// the two lowest digit-product classes, whose diagonal part is a positive bias), and debiased by
-// the realised squared rounding errors E_a = sum_i (q_ia - y_ia)^2
-// (the dithered errors are zero-mean and independent across columns, so only the diagonal
-// carries a bias; with it removed the Gram is unbiased even for columns whose range is set by
-// a massive activation),
+// the two lowest digit-product classes, whose diagonal part is a positive bias) minus
+// E_a = sum_i (q_ia^2 - y_ia^2) = sum_i e_ia (e_ia + 2 y_ia), e = q - y the rounding error, so the
+// diagonal is the centred energy sum_i y_ia^2 - S_a^2 / l itself, free of the dither's noise
+// (which would otherwise put an error of ~2 |x| d e on the energy of a column holding a massive
+// activation x); the off-diagonal dither noise is zero-mean and independent across columns,
 // so X~ = X - 1 mu^T never needs the exact mu before the pass.
 //
 // mu0, shift and b0 come from a 1/s row sample (sample_kernel, s = 16 at large l): shift maps
@@ -238,7 +238,7 @@ __device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
 // FULL: statistics + candidates + digits; !FULL: digits + S + E only (requant path).
 // Thread: VEC consecutive columns, rows [r0, r1) of its chunk, U rows in flight.  Per entry the
 // hot loop does the dithered rounding, the digit split and packing, the exact integer sums of q
-// and q^2, the squared rounding error, |y| max (the digit-range check and the exact range for a
+// and q^2, the rounding-error term q^2 - y^2, |y| max (the digit-range check and the exact range for a
 // requant), the x and x^2 sums and a running max of the |x| bit patterns; only when that max
 // reaches the candidate bin does the warp build candidate masks and append them (one scan and
 // one atomic per warp).  Full U-row groups run without bounds checks; pointers are advanced,
@@ -305,7 +305,7 @@ __device__ __forceinline__ void pass1_rows(int nrows, const float* __restrict__ 
       // w = q + kW0 (kW0 = 64 sum_{i < nd-1} 128^i): every digit is a plain bit field of w
       w[v] = __float_as_int(t) - (0x4B400000 + 1 - kW0);
       const float e = (t - 12582913.0f) - y;  // q - y
-      es[v] = fmaf(e, e, es[v]);
+      es[v] = fmaf(e, fmaf(2.f, y, e), es[v]);  // q^2 - y^2 = e (e + 2 y)
       ym[v] = fmaxf(ym[v], fabsf(y));
       ws[v] += w[v];
       ww[v] += (long long)w[v] * (long long)w[v];

@@ -48,8 +48,10 @@ def assert_parity(g, o, sigma_tol=1e-4, share_tol=1e-5, rho_tol=1e-3, check_sigm
         # V_k: the spanned subspace (sign / rotation inside degenerate blocks is free, R8, c-10)
         if o["sigma"][-1] > 1e-6 * o["sigma"][0]:
             assert subspace_sin(g["V"], o["V"]) <= 1e-3
-        # sigma_{k+1}: the Ritz estimate of the (k+1)-th direction (not part of the residual test)
-        assert abs(r.sigma_next - o["sigma_next"]) <= 1e-3 * o["sigma_next"] + 1e-6 * o["sigma"][0]
+        # sigma_{k+1}: the (k+1)-th Ritz value of the p-dimensional subspace, a lower bound of
+        # sigma_{k+1} (Cauchy interlacing) that the residual test does not converge (include/avd.h)
+        so = o["sigma_next"]
+        assert 0.9 * so - 1e-6 * o["sigma"][0] <= r.sigma_next <= so * (1 + 1e-4) + 1e-6 * o["sigma"][0]
     s_g = np.array(r.energy_cf[1:]) / r.energy_cf[0]
     s_o = np.array(o["energy_cf"][1:]) / o["energy_cf"][0]
     assert np.all(np.abs(s_g - s_o) <= share_tol * s_o + 1e-12), (s_g, s_o)
