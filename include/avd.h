@@ -94,6 +94,9 @@ typedef struct {
 /* avd_config.flags: quantise the Gram operand with the exact column ranges (the fallback taken
  * when the row-sampled ranges overflow the digit range; forced here for tests)               */
 #define AVD_FLAG_EXACT_SCALE 2
+/* avd_config.flags (tests): with automatic digits, take the 3-digit escalation (AVD_EREPEAT and
+ * the re-encoded Gram) whatever the precision bound says                                      */
+#define AVD_FLAG_FORCE_ESCALATE 4
 
 /* Outputs.  Device arrays caller-owned, sized from the plan (cap = n_top). */
 typedef struct {
@@ -183,7 +186,8 @@ avd_status avd_decompose_host(avd_ctx* ctx, const float* X_host, avd_outputs* ou
  *                       column range about the quantiser centre, the centred int8 digit planes of
  *                       the Gram operand with their integer column sums and squared rounding
  *                       errors, the top-set candidates)
- *       exchange: AVD_BUF_STATS (f64, SUM), AVD_BUF_COLMAX (f32, MAX: max |x - quantiser centre|)
+ *       exchange: AVD_BUF_STATS (f64, SUM), AVD_BUF_COLMAX (f32, MAX: max |x - quantiser centre|),
+                 AVD_BUF_DIAG (f64, SUM: sum_i (x_ij - centre_j)^2, the exact diagonal of G)
  *   avd_stage_gram     (mu; AVD_ENONFINITE if X has NaN/Inf; re-quantisation with the exact
  *                       ranges if any rank's digits overflowed; K3 tcgen05 int8 Gram, exact int64)
  *       exchange: AVD_BUF_GRAM (i64, SUM), AVD_BUF_CAND (i64, SUM), AVD_BUF_QSUM (i64, SUM),
@@ -209,6 +213,7 @@ typedef enum {
   AVD_BUF_GRAM = 4, AVD_BUF_ENERGY = 5, AVD_BUF_HIST2 = 6, AVD_BUF_HIST3 = 7,
   AVD_BUF_TIES = 8, AVD_BUF_AGG = 9, AVD_BUF_HIST0 = 10, AVD_BUF_CAND = 11,
   AVD_BUF_SAMPLE = 12, AVD_BUF_SMAX = 13, AVD_BUF_SMIN = 14, AVD_BUF_QSUM = 15, AVD_BUF_QERR = 21,
+  AVD_BUF_DIAG = 22,
   /* read-only views for tests / diagnostics (not exchanged) */
   AVD_BUF_MU = 16, AVD_BUF_G = 17, AVD_BUF_P = 18, AVD_BUF_DIGITS = 19, AVD_BUF_SCALE = 20
 } avd_buffer_id;

@@ -4,7 +4,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <new>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -14,6 +16,17 @@ namespace avd {
 
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
+
+cudaError_t smem_attr_impl(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> set;  // one process drives one device
+  std::lock_guard<std::mutex> lk(mu);
+  int& cur = set[fn];
+  if (bytes <= cur) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) cur = bytes;
+  return e;
+}
 
 namespace {
 
@@ -133,7 +146,7 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   L.add(sizeof(double) * 16);                   // 42 report
   L.add(sizeof(unsigned long long) * kHistBins);// 43 hist0
   L.add(sizeof(long long) * 2);                 // 44 cand_x
-  L.add(gemm_part_bytes(C->m_pad, (int)p, C->num_sms));  // 45 gemm_part
+  L.add(gemm_part_bytes(m, C->m_pad, (int)p, C->num_sms));  // 45 gemm_part
   L.add(sizeof(float) * 2 * C->l_pad * (((C->k_pad + 31) / 32) * 32));   // 46 P_hl
   L.add(sizeof(float) * 2 * C->k_pad * round_up(m, 32));                 // 47 Vt_hl
   L.add(sizeof(float) * 2 * C->m_pad * (((C->k_pad + 31) / 32) * 32));   // 48 V_hl
@@ -158,6 +171,7 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   L.add(sizeof(long long) * C->r1 * m);                                  // 67 qsq_part
   L.add(sizeof(double) * (4 + 2 * C->m_pad));                            // 68 diag: |mu|, scratch, q, y
   L.add(sizeof(double) * kMaxP);                                         // 69 prec
+  L.add(sizeof(double) * m);                                             // 70 ysq
   if (L.n >= 128) { set_error("workspace layout table overflow"); return AVD_EINVAL; }
   plan->workspace_bytes = L.total;
   if (lay) *lay = L;
@@ -323,7 +337,7 @@ avd_status avd_create(const avd_config* cfg, avd_ctx** out) {
   BIND(samp, double*); BIND(smax, float*); BIND(smin, float*); BIND(qscale, float*); BIND(qoff, float*);
   BIND(qsum_part, long long*); BIND(qsum_local, long long*); BIND(qerr_part, float*); BIND(qerr_local, double*);
   BIND(qerr, double*); BIND(mu0, float*); BIND(qsq_part, long long*); BIND(diag, double*);
-  BIND(prec, double*);
+  BIND(prec, double*); BIND(ysq, double*);
 #undef BIND
   if (cudaMallocHost(&c->eig_host, sizeof(double) * 4 * kMaxP) != cudaSuccess) {
     cudaGetLastError();
@@ -392,6 +406,7 @@ avd_status avd_buffer(avd_ctx* c, int32_t which, void** ptr, size_t* bytes) {
     case AVD_BUF_SMIN: *ptr = c->smin; *bytes = sizeof(float) * m; break;
     case AVD_BUF_QSUM: *ptr = c->qsum; *bytes = sizeof(long long) * 2 * m; break;
     case AVD_BUF_QERR: *ptr = c->qerr; *bytes = sizeof(double) * m; break;
+    case AVD_BUF_DIAG: *ptr = c->ysq; *bytes = sizeof(double) * m; break;
     case AVD_BUF_HIST0: *ptr = c->hist0; *bytes = sizeof(long long) * kHistBins; break;
     case AVD_BUF_CAND: *ptr = c->cand_x; *bytes = sizeof(long long) * 2; break;
     case AVD_BUF_COLMAX: *ptr = c->colmax; *bytes = sizeof(float) * m; break;
@@ -497,7 +512,8 @@ avd_status avd_stage_eig(avd_ctx* c) {
   // automatic digits (avd_config.digits == 0): the quantisation-error bound decides whether the
   // 2-digit operand meets half the north-star tolerances; if not, redo the Gram with 3 digits.
   // The decision uses only replicated values (G, V_k, shifts), so every rank takes it alike.
-  if (c->auto_digits && c->nd == 2 && (c->prec_sigma > 5e-5 || c->prec_share > 5e-6)) {
+  const bool force = (c->cfg.flags & AVD_FLAG_FORCE_ESCALATE) != 0;
+  if (c->auto_digits && c->nd == 2 && (force || c->prec_sigma > 5e-5 || c->prec_share > 5e-6)) {
     c->nd = 3;
     c->escalate = true;
     c->stage = 2;

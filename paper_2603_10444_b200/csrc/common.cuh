@@ -56,7 +56,7 @@ struct Ctx {
   float* colmax_part = nullptr;   // [r1][m]
   float* colmin_part = nullptr;   // [r1][m]
   double* sq_part = nullptr;      // [r1 * ncb]
-  double* stats = nullptr;        // [m + 4]: colsum[m], sum x^2, (unused), #nonzero, #overflowing columns (exchange)
+  double* stats = nullptr;        // [m + 4]: colsum[m], sum x^2 (set by the trace kernel from ysq), -, #nonzero, #overflowing columns (exchange)
   double* samp = nullptr;         // [m + 1]: row-sample column sums, #sampled rows (exchange SUM)
   float* smax = nullptr;          // [m] row-sample column max (exchange MAX)
   float* smin = nullptr;          // [m] row-sample column min (exchange MIN)
@@ -69,6 +69,7 @@ struct Ctx {
   float* qerr_part = nullptr;     // [r1][m] per-chunk sums of the squared rounding errors
   double* qerr_local = nullptr;   // [m_pad] this rank's sums of squared rounding errors
   double* qerr = nullptr;         // [m_pad] (exchange SUM)
+  double* ysq = nullptr;          // [m] sum_i (x_ij - mu0_j)^2, fp64 (exchange SUM): diag of G, ||X||^2
   unsigned long long* hist0 = nullptr;  // [4096] exact first-level histogram over candidates (exchange)
   float* colmax = nullptr;        // [m] max |x - mu0| (exchange MAX)
   float* colmin = nullptr;        // [m] (exchange MIN)
@@ -101,7 +102,7 @@ struct Ctx {
   double *H = nullptr, *W = nullptr, *theta = nullptr;          // [p][p], [p][p], [p]
   double* red_part = nullptr;     // [n_red_chunks][p*p]
   int n_red = 1;
-  void* gemm_part = nullptr;      // Yfix: int64 [m_pad][p] fixed-point accumulator of Y = G Q
+  void* gemm_part = nullptr;      // split-K partials of Y = G Q [RB][KS][BM][p] + row-block tickets
   float *Q32 = nullptr, *Z32 = nullptr;  // [m][p] fp32 mirrors of Q, Z
   unsigned* ticket = nullptr;     // last-CTA ticket of the fused reductions
   double* gmax = nullptr;         // max |G| (fixed-point scale of the Y = G Q accumulation)
@@ -182,6 +183,12 @@ void set_error(const std::string& msg);
     if (s__ != AVD_OK) return s__;           \
   } while (0)
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when a kernel needs more than it was last
+// given (a host API call per launch costs microseconds; the eigensolver launches ~100 kernels)
+cudaError_t smem_attr_impl(const void* fn, int bytes);
+template <typename F>
+inline cudaError_t smem_attr(F* fn, int bytes) { return smem_attr_impl(reinterpret_cast<const void*>(fn), bytes); }
+
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
@@ -195,8 +202,8 @@ avd_status launch_gram(Ctx* c);                            // k_gram.cu
 avd_status gram_make_tmap(Ctx* c);                         // k_gram.cu
 avd_status launch_gram_finalize(Ctx* c);                   // k_eig.cu
 avd_status run_eig(Ctx* c);                                // k_eig.cu
-void gemm_geometry(int64_t m_pad, int p, int num_sms, bool fp32, int* BM, int* ncta, int64_t* U, int* KT);
-size_t gemm_part_bytes(int64_t m_pad, int p, int num_sms);
+void gemm_geometry(int64_t m, int64_t m_pad, int p, int num_sms, bool fp32, int* BM, int* KS, int* RB, int* KT);
+size_t gemm_part_bytes(int64_t m, int64_t m_pad, int p, int num_sms);
 avd_status launch_project(Ctx* c, const float* X);         // k_project.cu
 avd_status launch_select0_speculative(Ctx* c);
 avd_status launch_select(Ctx* c, const float* X, int level, int rank);  // k_select.cu

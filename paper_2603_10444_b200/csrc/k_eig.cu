@@ -39,7 +39,8 @@ namespace {
 // transposed through shared memory, so every global access is coalesced.
 __global__ void __launch_bounds__(256) gram_finalize_kernel(const long long* __restrict__ Gi, int64_t m, int64_t m_pad,
                                      const int32_t* __restrict__ shift, const long long* __restrict__ qsum,
-                                     const double* __restrict__ qerr, double inv_l, double unit,
+                                     const double* __restrict__ ysq, const double* __restrict__ mu,
+                                     const float* __restrict__ mu0, double l, double inv_l, double unit,
                                      double* __restrict__ G, float* __restrict__ G32) {
   __shared__ long long tile[32][33];
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -63,24 +64,28 @@ __global__ void __launch_bounds__(256) gram_finalize_kernel(const long long* __r
       const long long v = upper ? tile[tx][aa] : Gi[a * m_pad + b];
       // exact centring of the quantised matrix: sum_i (q_ia - qbar_a)(q_ib - qbar_b)
       //   = sum_i q_ia q_ib - S_a S_b / l   (S = column sums of q, exact integers)
-      // v unit = sum_i q_ia q_ib; the diagonal is the exact sum_i q_ia^2 of the fused pass
-      // (qsum[m + a]; with 3 digits the Gram drops the two lowest digit-product classes, whose
-      // diagonal part is a positive bias) minus qerr_a = sum_i (q_ia^2 - y_ia^2): sum_i y_ia^2
-      const double qq = (a == b) ? (double)qsum[m + a] - qerr[a] : (double)v * unit;
-      const double corr = ((double)qsum[a] * (double)qsum[b]) * inv_l;
-      g = ldexp(qq - corr, -(shift[a] + shift[b]));
+      // v unit = sum_i q_ia q_ib.  The diagonal is the centred energy itself, from the fp64
+      // sums of the fused pass: sum_i (x_ia - mu_a)^2 = sum_i (x_ia - mu0_a)^2 - l (mu_a - mu0_a)^2
+      // (no dither noise, no cancellation: mu0 is the sampled centre)
+      if (a == b) {
+        const double dm = mu[a] - (double)mu0[a];
+        g = ysq[a] - l * dm * dm;
+      } else {
+        const double corr = ((double)qsum[a] * (double)qsum[b]) * inv_l;
+        g = ldexp((double)v * unit - corr, -(shift[a] + shift[b]));
+      }
     }
     G[a * m_pad + b] = g;
     G32[a * m_pad + b] = (float)g;
   }
 }
 
-// tr(G), max_a G_aa (= max |G_ab| for the positive semidefinite G), and for the precision bound
-// (run_eig) sum_a d_a^2 G_aa over the columns with a nonzero rounding error (d_a = 2^-shift_a, the
-// quantisation step of column a in units of x)
+// tr(G), max_a G_aa (= max |G_ab| for the positive semidefinite G), and
+// ||X||_F^2 = sum_a [sum_i (x_ia - mu0_a)^2 + 2 mu0_a sum_i x_ia - l mu0_a^2] -> stats[m] (every
+// term is a nonnegative-dominated fp64 sum; PAPER.md:15 total energy)
 __global__ void __launch_bounds__(1024) trace_kernel(const double* __restrict__ G, int64_t m, int64_t ld,
-                                                    const int32_t* __restrict__ shift,
-                                                    const double* __restrict__ qerr, double* __restrict__ out,
+                                                    const double* __restrict__ ysq, const float* __restrict__ mu0,
+                                                    double l, double* __restrict__ stats, double* __restrict__ out,
                                                     double* __restrict__ gmax) {
   // fixed order: strided per-thread sums, xor-shuffle tree per warp, warp partials in order
   __shared__ double sh[32], shm[32], shd[32];
@@ -89,7 +94,8 @@ __global__ void __launch_bounds__(1024) trace_kernel(const double* __restrict__ 
     const double g = G[j * ld + j];
     s += g;
     mx = fmax(mx, fabs(g));
-    if (qerr[j] != 0.0) dg += ldexp(fmax(g, 0.0), -2 * shift[j]);
+    const double c0 = (double)mu0[j];
+    dg += ysq[j] + c0 * (2.0 * stats[j] - l * c0);
   }
   for (int o = 16; o > 0; o >>= 1) {
     s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
@@ -102,7 +108,7 @@ __global__ void __launch_bounds__(1024) trace_kernel(const double* __restrict__ 
     double t = 0.0, u = 0.0, d = 0.0;
     for (int i = 0; i < 32; ++i) { t += sh[i]; u = fmax(u, shm[i]); d += shd[i]; }
     out[0] = t;
-    out[1] = d;
+    stats[m] = d;
     *gmax = u;
   }
 }
@@ -128,11 +134,13 @@ __global__ void rand_fill_kernel(double* __restrict__ Q, float* __restrict__ Q32
   if (Q32) Q32[t] = (float)v;
 }
 
-// ---------------------------------------------------------------- Y = G Q, stream-K
-// Unit = (row block rb of BM rows, K tile kt of 32).  U = RB * KT units are split evenly over
-// ncta CTAs (CTA c: [c U / n, (c+1) U / n)); a CTA's range covers at most two row blocks
-// (ncta >= RB), each written as a partial segment part[c][seg][BM][p].  G is symmetric, so the
-// (rows r0.., K k0..) tile is read as G[k][r0..] (contiguous rows, no transpose).
+// ---------------------------------------------------------------- Y = G Q, split-K
+// Unit = (row block rb of BM rows, K range ks of the KS equal slices of the 32-row K tiles):
+// CTA rb * KS + ks computes the BM x p partial product of its K range (fp32 or fp64 FMA in
+// registers) and stores it to part[rb][ks]; the LAST CTA of a row block (acq_rel ticket) sums
+// the KS partials in ks order in fp64 and writes Y (fp64) and its optional fp32 mirror — one
+// kernel, no atomics on data, bit-deterministic.  G is symmetric, so the (rows r0.., K k0..)
+// tile is read as G[k][r0..] (contiguous rows, no transpose).
 // 128 threads: ty = tid / 8 owns rows ty*NR .. +NR, tx = tid % 8 owns column pairs 16 c2 + 2 tx.
 constexpr int kSkBK = 32;
 constexpr int kSkThreads = 128;
@@ -145,45 +153,37 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// Fixed-point scale of the Y accumulation: |partial sums of Y = G In| <= ||G||_inf max|In| <=
-// (m max|G|)^(level+1) =: Bnd for In orthonormal-ish (level 0) or In = G * orthonormal (level 1);
-// scale = 2^(61 - e), 2^e >= Bnd, so every running sum fits an int64 with resolution Bnd 2^-60.
-__device__ __forceinline__ double fix_scale(const double* gmax, int64_t m, int level) {
-  const double g = *gmax * (double)m;
-  if (!(g > 0.0) || !(g < 1e150)) return 1.0;
-  const double b = level ? g * g : g;
-  return ldexp(1.0, 61 - (ilogb(b) + 1));
-}
-// 1 / fix_scale (a power of two, so exact) without an fp64 division
-__device__ __forceinline__ double fix_scale_inv(const double* gmax, int64_t m, int level) {
-  const double g = *gmax * (double)m;
-  if (!(g > 0.0) || !(g < 1e150)) return 1.0;
-  const double b = level ? g * g : g;
-  return ldexp(1.0, (ilogb(b) + 1) - 61);
+// ticket += 1 with acq_rel semantics at GPU scope (no full sequentially-consistent fence)
+__device__ __forceinline__ unsigned ticket_acq_rel(unsigned* t) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(t) : "memory");
+  return old;
 }
 
 template <typename T, int NR, int NC>
-__global__ void __launch_bounds__(kSkThreads) gemm_sk_kernel(const T* __restrict__ G, int64_t ldg,
-                                                             const T* __restrict__ Qin, int64_t m, int64_t U,
-                                                             int KT, int ncta, unsigned long long* __restrict__ Yfix,
-                                                             const double* __restrict__ gmax, int level) {
+__global__ void __launch_bounds__(kSkThreads) gemm_kernel(const T* __restrict__ G, int64_t ldg,
+                                                          const T* __restrict__ Qin, int64_t m, int KT, int KS,
+                                                          T* __restrict__ part, unsigned* __restrict__ tickets,
+                                                          double* __restrict__ Y, float* __restrict__ Y32) {
   constexpr int BM = 16 * NR;
   constexpr int p = 8 * NC;
   constexpr int SG = kSkBK * BM;          // elements of one G stage
   constexpr int SQ = kSkBK * p;           // elements of one Q stage
   constexpr int EPC = 16 / sizeof(T);     // elements per 16-B chunk
   extern __shared__ __align__(16) unsigned char sk_raw[];
+  __shared__ unsigned last_sh;
   T* sm = reinterpret_cast<T*>(sk_raw);
   const int tid = threadIdx.x;
   const int ty = tid >> 3, tx = tid & 7;
-  const int c = blockIdx.x;
-  const int64_t u0 = ((int64_t)c * U) / ncta, u1 = ((int64_t)(c + 1) * U) / ncta;
+  const int rb = blockIdx.x / KS, ks = blockIdx.x % KS;
+  const int kt0 = (int)(((int64_t)KT * ks) / KS), kt1 = (int)(((int64_t)KT * (ks + 1)) / KS);
+  const int n = kt1 - kt0;
 
-  auto load_stage = [&](int slot, int64_t rb, int kt) {
+  auto load_stage = [&](int slot, int kt) {
     T* sG = sm + slot * (SG + SQ);
     T* sQ = sG + SG;
     const int64_t k0 = (int64_t)kt * kSkBK;
-    const int64_t r0 = rb * BM;
+    const int64_t r0 = (int64_t)rb * BM;
     constexpr int GCH = SG / EPC;  // 16-B chunks of the G tile
     for (int ch = tid; ch < GCH; ch += kSkThreads) {
       const int kk = ch / (BM / EPC), cc = ch % (BM / EPC);
@@ -200,87 +200,89 @@ __global__ void __launch_bounds__(kSkThreads) gemm_sk_kernel(const T* __restrict
     }
   };
 
-  int seg = 0;
-  for (int64_t u = u0; u < u1; ++seg) {
-    const int64_t rb = u / KT;
-    const int64_t uend = min(u1, (rb + 1) * KT);
-    const int n = (int)(uend - u);
-    const int kt0 = (int)(u - rb * KT);
-    T acc[NR][NC];
+  T acc[NR][NC];
 #pragma unroll
-    for (int r = 0; r < NR; ++r)
+  for (int r = 0; r < NR; ++r)
 #pragma unroll
-      for (int q = 0; q < NC; ++q) acc[r][q] = T(0);
-    __syncthreads();  // previous segment's readers are done with every slot
+    for (int q = 0; q < NC; ++q) acc[r][q] = T(0);
 #pragma unroll
-    for (int s = 0; s < kSkStages - 1; ++s) {
-      if (s < n) load_stage(s, rb, kt0 + s);
-      cp_commit();
-    }
-    for (int i = 0; i < n; ++i) {
-      cp_wait<kSkStages - 2>();
-      __syncthreads();
-      if (i + kSkStages - 1 < n) load_stage((i + kSkStages - 1) % kSkStages, rb, kt0 + i + kSkStages - 1);
-      cp_commit();
-      const T* sG = sm + (i % kSkStages) * (SG + SQ);
-      const T* sQ = sG + SG;
+  for (int s = 0; s < kSkStages - 1; ++s) {
+    if (s < n) load_stage(s, kt0 + s);
+    cp_commit();
+  }
+  for (int i = 0; i < n; ++i) {
+    cp_wait<kSkStages - 2>();
+    __syncthreads();
+    if (i + kSkStages - 1 < n) load_stage((i + kSkStages - 1) % kSkStages, kt0 + i + kSkStages - 1);
+    cp_commit();
+    const T* sG = sm + (i % kSkStages) * (SG + SQ);
+    const T* sQ = sG + SG;
 #pragma unroll 4
-      for (int kk = 0; kk < kSkBK; ++kk) {
-        T g[NR], q[NC];
+    for (int kk = 0; kk < kSkBK; ++kk) {
+      T g[NR], q[NC];
 #pragma unroll
-        for (int r = 0; r < NR; r += EPC) {
-          if constexpr (sizeof(T) == 4) {
-            const float4 v = *reinterpret_cast<const float4*>(sG + kk * BM + ty * NR + r);
-            g[r] = v.x; g[r + 1] = v.y; g[r + 2] = v.z; g[r + 3] = v.w;
-          } else {
-            const double2 v = *reinterpret_cast<const double2*>(sG + kk * BM + ty * NR + r);
-            g[r] = v.x; g[r + 1] = v.y;
-          }
+      for (int r = 0; r < NR; r += EPC) {
+        if constexpr (sizeof(T) == 4) {
+          const float4 v = *reinterpret_cast<const float4*>(sG + kk * BM + ty * NR + r);
+          g[r] = v.x; g[r + 1] = v.y; g[r + 2] = v.z; g[r + 3] = v.w;
+        } else {
+          const double2 v = *reinterpret_cast<const double2*>(sG + kk * BM + ty * NR + r);
+          g[r] = v.x; g[r + 1] = v.y;
         }
+      }
 #pragma unroll
-        for (int c2 = 0; c2 < NC / 2; ++c2) {
-          if constexpr (sizeof(T) == 4) {
-            const float2 v = *reinterpret_cast<const float2*>(sQ + kk * p + 16 * c2 + 2 * tx);
-            q[2 * c2] = v.x; q[2 * c2 + 1] = v.y;
-          } else {
-            const double2 v = *reinterpret_cast<const double2*>(sQ + kk * p + 16 * c2 + 2 * tx);
-            q[2 * c2] = v.x; q[2 * c2 + 1] = v.y;
-          }
+      for (int c2 = 0; c2 < NC / 2; ++c2) {
+        if constexpr (sizeof(T) == 4) {
+          const float2 v = *reinterpret_cast<const float2*>(sQ + kk * p + 16 * c2 + 2 * tx);
+          q[2 * c2] = v.x; q[2 * c2 + 1] = v.y;
+        } else {
+          const double2 v = *reinterpret_cast<const double2*>(sQ + kk * p + 16 * c2 + 2 * tx);
+          q[2 * c2] = v.x; q[2 * c2 + 1] = v.y;
         }
+      }
 #pragma unroll
-        for (int r = 0; r < NR; ++r)
+      for (int r = 0; r < NR; ++r)
 #pragma unroll
-          for (int q2 = 0; q2 < NC; ++q2) acc[r][q2] = fma(g[r], q[q2], acc[r][q2]);
+        for (int q2 = 0; q2 < NC; ++q2) acc[r][q2] = fma(g[r], q[q2], acc[r][q2]);
+    }
+  }
+  cp_wait<0>();
+  // partial product of this K slice -> part[rb][ks] (BM x p, row-major)
+  T* pp = part + ((int64_t)rb * KS + ks) * (BM * p);
+#pragma unroll
+  for (int r = 0; r < NR; ++r)
+#pragma unroll
+    for (int c2 = 0; c2 < NC / 2; ++c2) {
+      T* d = pp + (ty * NR + r) * p + 16 * c2 + 2 * tx;
+      if constexpr (sizeof(T) == 4) *reinterpret_cast<float2*>(d) = make_float2(acc[r][2 * c2], acc[r][2 * c2 + 1]);
+      else *reinterpret_cast<double2*>(d) = make_double2(acc[r][2 * c2], acc[r][2 * c2 + 1]);
+    }
+  __syncthreads();
+  if (tid == 0) last_sh = (ticket_acq_rel(&tickets[rb]) == (unsigned)(KS - 1)) ? 1u : 0u;
+  __syncthreads();
+  if (!last_sh) return;
+  // the row block's last CTA: fixed-order sum of the KS partials
+  const T* base = part + (int64_t)rb * KS * (BM * p);
+  for (int e = tid * 2; e < BM * p; e += kSkThreads * 2) {
+    double s0 = 0.0, s1 = 0.0;
+    for (int q = 0; q < KS; ++q) {
+      const T* src = base + (int64_t)q * (BM * p) + e;
+      if constexpr (sizeof(T) == 4) {
+        const float2 v = __ldcg(reinterpret_cast<const float2*>(src));
+        s0 += (double)v.x; s1 += (double)v.y;
+      } else {
+        const double2 v = __ldcg(reinterpret_cast<const double2*>(src));
+        s0 += v.x; s1 += v.y;
       }
     }
-    cp_wait<0>();
-    // exact integer accumulation of this segment into Yfix (order-independent, deterministic)
-    const double scale = fix_scale(gmax, m, level);
-#pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      const int64_t row = rb * BM + ty * NR + r;
-      if (row < m)
-#pragma unroll
-        for (int q2 = 0; q2 < NC; ++q2) {
-          const long long v = __double2ll_rn((double)acc[r][q2] * scale);
-          if (v) atomicAdd(Yfix + row * p + 16 * (q2 / 2) + 2 * tx + (q2 & 1), (unsigned long long)v);
-        }
+    const int64_t row = (int64_t)rb * BM + e / p;
+    if (row < m) {
+      const int64_t o = row * p + e % p;
+      *reinterpret_cast<double2*>(Y + o) = make_double2(s0, s1);
+      if (Y32) *reinterpret_cast<float2*>(Y32 + o) = make_float2((float)s0, (float)s1);
     }
-    u = uend;
   }
-}
-
-// Y = Yfix / scale (fp64, optional fp32 mirror); Yfix re-zeroed for the next product
-__global__ void fix_convert_kernel(unsigned long long* __restrict__ Yfix, int64_t n, int64_t m,
-                                   const double* __restrict__ gmax, int level, double* __restrict__ Y,
-                                   float* __restrict__ Y32) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  const double inv = fix_scale_inv(gmax, m, level);
-  const double v = (double)(long long)Yfix[t] * inv;
-  Yfix[t] = 0ull;
-  Y[t] = v;
-  if (Y32) Y32[t] = (float)v;
+  if (tid == 0) tickets[rb] = 0u;  // re-armed for the next launch (stream-ordered)
 }
 
 // ---------------------------------------------------------------- p x p helpers (one CTA)
@@ -471,12 +473,6 @@ __device__ void chol_block(double* B, double* dinv, int* bad) {
 }
 
 // ---------------------------------------------------------------- fused m-length reduction
-// ticket += 1 with acq_rel semantics at GPU scope (no full sequentially-consistent fence)
-__device__ __forceinline__ unsigned ticket_acq_rel(unsigned* t) {
-  unsigned old;
-  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(t) : "memory");
-  return old;
-}
 constexpr int kRedRows = kRedRowsC;  // rows per partial
 template <int PC>
 struct RedCfg {
@@ -767,21 +763,27 @@ __global__ void resid_kernel(const double* __restrict__ Z, const double* __restr
 
 // V_out[j][r] = sign_r * U[j][r] (r < k), sign making the largest-|.| entry positive
 // (smallest j on ties; R8); sigma_r = sqrt(max(theta_r, 0)); V32 fp32 copy.
-// Also t_r = sum_a d_a^2 v_ra^2 over the columns with rounding errors (precision bound, run_eig).
+// Also t_r = sum_a d_a^2 v_ra^2 (lambda_r (1 - 2 v_ra^2) + v_ra^2 G_aa) over the columns with
+// rounding errors (precision bound, run_eig).
 __global__ void finalize_vectors_kernel(const double* __restrict__ U, const double* __restrict__ theta, int64_t m,
                                         int p, int k, int k_pad, const int32_t* __restrict__ shift,
-                                        const double* __restrict__ qerr, double* __restrict__ V,
-                                        double* __restrict__ sigma, float* __restrict__ V32, double* __restrict__ prec) {
+                                        const double* __restrict__ qerr, const double* __restrict__ G, int64_t ldg,
+                                        double* __restrict__ V, double* __restrict__ sigma, float* __restrict__ V32,
+                                        double* __restrict__ prec) {
   __shared__ double sv[256], st[256];
   __shared__ int64_t sj[256];
   const int r = blockIdx.x;
   double best = -1.0, tr = 0.0;
   int64_t bj = 0;
+  const double lam = fmax(theta[r], 0.0);
   for (int64_t j = threadIdx.x; j < m; j += 256) {
     const double u = U[j * p + r];
     const double a = fabs(u);
     if (a > best) { best = a; bj = j; }
-    if (qerr[j] != 0.0) tr += ldexp(u * u, -2 * shift[j]);
+    if (qerr[j] != 0.0) {
+      const double u2 = u * u;
+      tr += ldexp(u2 * fmax(lam * (1.0 - 2.0 * u2) + u2 * G[j * ldg + j], 0.0), -2 * shift[j]);
+    }
   }
   sv[threadIdx.x] = best;
   sj[threadIdx.x] = bj;
@@ -804,6 +806,35 @@ __global__ void finalize_vectors_kernel(const double* __restrict__ U, const doub
     V32[j * k_pad + r] = (float)v;
   }
   if (threadIdx.x == 0) sigma[r] = sqrt(fmax(theta[r], 0.0));
+}
+
+// Bound of the spike-energy error (run_eig): var(d E_spike) <= sum_a d_a^2 (w_a (1 - 2 P_aa) +
+// P_aa^2 G_aa), w_a = sum_r lambda_r v_ra^2, P_aa = sum_r v_ra^2 -> prec[k]; one CTA, fixed order
+__global__ void __launch_bounds__(1024) prec_energy_kernel(const double* __restrict__ V, const double* __restrict__ theta,
+                                                           int64_t m, int k, const int32_t* __restrict__ shift,
+                                                           const double* __restrict__ qerr,
+                                                           const double* __restrict__ G, int64_t ldg,
+                                                           double* __restrict__ prec) {
+  __shared__ double sh[32];
+  double acc = 0.0;
+  for (int64_t j = threadIdx.x; j < m; j += 1024) {
+    if (qerr[j] == 0.0) continue;
+    double P = 0.0, w = 0.0;
+    for (int r = 0; r < k; ++r) {
+      const double v2 = V[j * k + r] * V[j * k + r];
+      P += v2;
+      w = fma(fmax(theta[r], 0.0), v2, w);
+    }
+    acc += ldexp(fmax(w * (1.0 - 2.0 * P) + P * P * G[j * ldg + j], 0.0), -2 * shift[j]);
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < 32; ++i) t += sh[i];
+    prec[k] = t;
+  }
 }
 
 // ---------------------------------------------------------------- mean-bias diagnostics
@@ -911,64 +942,67 @@ avd_status launch_gram_finalize(Ctx* c) {
   const int64_t m = c->cfg.m;
   const double unit = (c->nd == 3) ? 16384.0 : 1.0;
   dim3 grid((unsigned)(c->m_pad / 32), (unsigned)(c->m_pad / 32));
-  gram_finalize_kernel<<<grid, dim3(32, 8), 0, c->stream>>>(c->gram_i, m, c->m_pad, c->shift, c->qsum, c->qerr,
-                                                    1.0 / (double)c->cfg.l_global, unit, c->G, c->G32);
+  gram_finalize_kernel<<<grid, dim3(32, 8), 0, c->stream>>>(c->gram_i, m, c->m_pad, c->shift, c->qsum, c->ysq, c->mu,
+                                                            c->mu0, (double)c->cfg.l_global,
+                                                            1.0 / (double)c->cfg.l_global, unit, c->G, c->G32);
   AVD_LAUNCHED(c);
-  trace_kernel<<<1, 1024, 0, c->stream>>>(c->G, m, c->m_pad, c->shift, c->qerr, c->trace, c->gmax);
+  trace_kernel<<<1, 1024, 0, c->stream>>>(c->G, m, c->m_pad, c->ysq, c->mu0, (double)c->cfg.l_global, c->stats,
+                                          c->trace, c->gmax);
   AVD_LAUNCHED(c);
   return AVD_OK;
 }
 
-// stream-K geometry shared by the plan (workspace) and the launches
-void gemm_geometry(int64_t m_pad, int p, int num_sms, bool fp32, int* BM, int* ncta, int64_t* U, int* KT) {
+// split-K geometry shared by the plan (workspace) and the launches
+void gemm_geometry(int64_t m, int64_t m_pad, int p, int num_sms, bool fp32, int* BM, int* KS, int* RB, int* KT) {
   *BM = (fp32 && p <= 64) ? 128 : 64;  // = 16 * NR of the gemm32 / gemm64 instantiations
-  const int64_t RB = m_pad / *BM;
-  *KT = (int)ceil_div(m_pad, kSkBK);
-  *U = RB * (int64_t)(*KT);
-  int64_t n = (int64_t)num_sms * (fp32 ? 3 : 2);
-  n = std::max<int64_t>(n, RB);
-  n = std::min<int64_t>(n, *U);
-  *ncta = (int)n;
+  *RB = (int)(m_pad / *BM);
+  *KT = (int)ceil_div(m, kSkBK);
+  const int64_t want = (int64_t)num_sms * (fp32 ? 3 : 2);  // resident CTAs (smem-bound)
+  *KS = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(want, *RB), *KT));
 }
-size_t gemm_part_bytes(int64_t m_pad, int p, int num_sms) {
-  (void)num_sms;
-  return sizeof(unsigned long long) * (size_t)m_pad * p;  // Yfix
+size_t gemm_part_bytes(int64_t m, int64_t m_pad, int p, int num_sms) {
+  size_t best = 0;
+  for (int f = 0; f < 2; ++f) {
+    int BM, KS, RB, KT;
+    gemm_geometry(m, m_pad, p, num_sms, f == 0, &BM, &KS, &RB, &KT);
+    best = std::max(best, (size_t)RB * KS * BM * p * (f == 0 ? sizeof(float) : sizeof(double)));
+  }
+  return (size_t)round_up((int64_t)best, 256) + sizeof(unsigned) * (size_t)(m_pad / 64 + 1);  // partials + tickets
 }
 
 namespace {
 
 // Y = G In (fp64 G, fp64 math) or Y = G32 In32 (fp32); Y fp64 (+ optional fp32 mirror)
 template <typename T, int NR, int NC>
-avd_status gemm_launch(Ctx* c, const T* Gm, const T* In, int level, double* Y, float* Y32) {
-  int BM, ncta, KT;
-  int64_t U;
+avd_status gemm_launch(Ctx* c, const T* Gm, const T* In, double* Y, float* Y32) {
+  int BM, KS, RB, KT;
   const int p = 8 * NC;
-  gemm_geometry(c->m_pad, p, c->num_sms, sizeof(T) == 4, &BM, &ncta, &U, &KT);
+  gemm_geometry(c->cfg.m, c->m_pad, p, c->num_sms, sizeof(T) == 4, &BM, &KS, &RB, &KT);
   if (BM != 16 * NR) { set_error("gemm geometry mismatch"); return AVD_EINVAL; }
   const int sm = kSkStages * (kSkBK * BM + kSkBK * p) * (int)sizeof(T);
-  AVD_CUDA(cudaFuncSetAttribute(gemm_sk_kernel<T, NR, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-  auto* yfix = reinterpret_cast<unsigned long long*>(c->gemm_part);
-  gemm_sk_kernel<T, NR, NC><<<ncta, kSkThreads, sm, c->stream>>>(Gm, c->m_pad, In, c->cfg.m, U, KT, ncta, yfix,
-                                                                  c->gmax, level);
-  AVD_LAUNCHED(c);
-  const int64_t n = c->cfg.m * p;
-  fix_convert_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c->stream>>>(yfix, n, c->cfg.m, c->gmax, level, Y, Y32);
+  AVD_CUDA(smem_attr(gemm_kernel<T, NR, NC>, sm));
+  const size_t pb = gemm_part_bytes(c->cfg.m, c->m_pad, c->p, c->num_sms);
+  T* part = reinterpret_cast<T*>(c->gemm_part);
+  unsigned* tickets = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(c->gemm_part) + pb -
+                                                  sizeof(unsigned) * (size_t)(c->m_pad / 64 + 1));
+  gemm_kernel<T, NR, NC><<<RB * KS, kSkThreads, sm, c->stream>>>(Gm, c->m_pad, In, c->cfg.m, KT, KS, part, tickets, Y,
+                                                                 Y32);
   AVD_LAUNCHED(c);
   return AVD_OK;
 }
 
-avd_status gemm64(Ctx* c, const double* In, int level, double* Y, float* Y32) {
+avd_status gemm64(Ctx* c, const double* In, double* Y, float* Y32) {
   switch (c->p / 16) {
-#define CASE(PC) case PC: return gemm_launch<double, 4, 2 * PC>(c, c->G, In, level, Y, Y32);
+#define CASE(PC) case PC: return gemm_launch<double, 4, 2 * PC>(c, c->G, In, Y, Y32);
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
   }
   set_error("unsupported p");
   return AVD_EINVAL;
 }
-avd_status gemm32(Ctx* c, const float* In, int level, double* Y, float* Y32) {
+avd_status gemm32(Ctx* c, const float* In, double* Y, float* Y32) {
   switch (c->p / 16) {
-#define CASE(PC) case PC: return gemm_launch<float, (PC <= 4 ? 8 : 4), 2 * PC>(c, c->G32, In, level, Y, Y32);
+#define CASE(PC) case PC: return gemm_launch<float, (PC <= 4 ? 8 : 4), 2 * PC>(c, c->G32, In, Y, Y32);
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
   }
@@ -986,7 +1020,7 @@ avd_status atb_fused(Ctx* c, const double* A, const double* B, double* out0, dou
   switch (p / 16) {
 #define CASE(PC)                                                                                                \
   case PC:                                                                                                      \
-    AVD_CUDA(cudaFuncSetAttribute(atb_fused_kernel<MODE, PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+    AVD_CUDA(smem_attr(atb_fused_kernel<MODE, PC>, (int)sm)); \
     atb_fused_kernel<MODE, PC><<<n_red, RedCfg<PC>::threads, sm, c->stream>>>(A, B, c->cfg.m, c->red_part, c->ticket, out0, out1,  \
                                                               ibad, stats, gate, max_sweeps);                   \
     break;
@@ -1002,7 +1036,7 @@ avd_status matpp(Ctx* c, const double* In0, double* Out0, float* Out0f, const do
                  float* Out1f, const double* M) {
   const int p = c->p;
   const size_t sm = ((size_t)p * p + 16 * p) * sizeof(double);
-  AVD_CUDA(cudaFuncSetAttribute(matpp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  AVD_CUDA(smem_attr(matpp_kernel, (int)sm));
   matpp_kernel<<<(unsigned)ceil_div(c->cfg.m, 16), 256, sm, c->stream>>>(In0, Out0, Out0f, In1, Out1, Out1f, M,
                                                                          c->cfg.m, p);
   AVD_LAUNCHED(c);
@@ -1014,7 +1048,7 @@ avd_status trsm(Ctx* c, const double* Y, const double* R, const double* dinv, co
   switch (c->p / 16) {
 #define CASE(PC)                                                                                              \
   case PC:                                                                                                    \
-    AVD_CUDA(cudaFuncSetAttribute(trsm_kernel<16 * PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * PC * PC * 8)); \
+    AVD_CUDA(smem_attr(trsm_kernel<16 * PC>, 256 * PC * PC * 8)); \
     trsm_kernel<16 * PC><<<grid, 32, 256 * PC * PC * 8, c->stream>>>(Y, R, dinv, bad, gate, c->cfg.m, c->Q, c->Q32); \
     break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
@@ -1051,40 +1085,39 @@ avd_status orth(Ctx* c, const double* Y, uint32_t seed) {
 // A-posteriori bound of the Gram operand's quantisation error (DESIGN.md §8 "Gram precision").
 // The operand is q_ia = y_ia + e_ia, y = (x - mu0) 2^shift, with dithered rounding errors e that
 // are zero-mean, independent and var e <= 1/4 (exactly 0 for a column whose every entry is on the
-// grid: qerr_a = 0).  The centred Gram of q, with the diagonal debiased, is G + E, E_ab =
-// d_a d_b sum_i (e_ia xc_ib + xc_ia e_ib) + O(e^2) off the diagonal (d_a = 2^-shift_a), so to
-// first order
-//   d lambda_r = v_r^T E v_r = 2 sigma_r sum_i u_ri sum_a d_a v_ra e_ia,
-//   std(d lambda_r) <= sigma_r sqrt(t_r),  t_r = sum_a d_a^2 v_ra^2           (finalize kernel)
-//   d E_spike = sum_r d lambda_r = 2 sum_ia d_a e_ia S_ia,  std <= sqrt(sum_r lambda_r t_r)
-// (the spike matrix S_ia = sum_r sigma_r u_ri v_ra).  The diagonal of G is the centred energy
-// sum y^2 - S^2/l itself (k_pass1.cu), so tr(G) carries only the fp32 rounding of y (<= 2^-24
-// relative, counted as 6e-8 tr(G)) and E_tail = tr(G) - E_spike inherits d E_spike.  At 5 sigma:
-//   prec_sigma = max_r 2.5 sqrt(t_r) / sigma_r  (relative error of sigma_r = d lambda / 2 lambda)
-//   prec_share = max(5 std(d E_spike) / E_spike, (5 std(d E_spike) + 6e-8 tr(G)) / E_tail)
+// grid: qerr_a = 0).  The diagonal of G is the exact centred energy (fp64 sums of the fused pass),
+// the off-diagonal is E_ab = d_a d_b sum_i (e_ia xc_ib + xc_ia e_ib) + O(e^2) (d_a = 2^-shift_a),
+// so to first order, with X~ v_r = sigma_r u_r and X~^T u_r = sigma_r v_r,
+//   d lambda_r = v_r^T E v_r = 2 sum_ia d_a v_ra e_ia (sigma_r u_ri - v_ra xc_ia),
+//   var <= t_r = sum_a d_a^2 v_ra^2 (lambda_r (1 - 2 v_ra^2) + v_ra^2 G_aa)      (finalize kernel)
+//   d E_spike = sum_r d lambda_r = 2 sum_ia d_a e_ia (S_ia - P_aa xc_ia),  P = V_k V_k^T,
+//   var <= sum_a d_a^2 (w_a (1 - 2 P_aa) + P_aa^2 G_aa),  w_a = sum_r lambda_r v_ra^2 (prec kernel)
+// (S the spike matrix).  A column carried by one massive entry (v_r ~ e_a) drops out, as it
+// should: its diagonal is exact.  E_tail = tr(G) - E_spike inherits d E_spike (tr(G) is exact up
+// to the fp32 rounding of y, counted as 1e-9 tr(G)).  At 5 sigma:
+//   prec_sigma = max_r 2.5 sqrt(t_r) / lambda_r  (relative error of sigma_r = d lambda / 2 lambda)
+//   prec_share = max(5 std(d E_spike) / E_spike, (5 std(d E_spike) + 1e-9 tr(G)) / E_tail)
 // The automatic digit rule raises the operand to 3 digits when prec_sigma > 5e-5 or
 // prec_share > 5e-6 (half the north-star tolerances 1e-4 / 1e-5).
 avd_status precision_bound(Ctx* c) {
   const int k = c->k;
-  double* h = c->eig_host + 2 * kMaxP;  // pinned scratch: t_r [k <= 95], tr(G), sum d^2 G_aa
-  AVD_CUDA(cudaMemcpyAsync(h, c->prec, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
-  AVD_CUDA(cudaMemcpyAsync(h + k, c->trace, sizeof(double) * 2, cudaMemcpyDeviceToHost, c->stream));
+  double* h = c->eig_host + 2 * kMaxP;  // pinned scratch: t_r [k <= 95], var(d E_spike), tr(G)
+  AVD_CUDA(cudaMemcpyAsync(h, c->prec, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, c->stream));
+  AVD_CUDA(cudaMemcpyAsync(h + k + 1, c->trace, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   AVD_CUDA(cudaStreamSynchronize(c->stream));
-  double ps = 0.0, var_spike = 0.0, e_spike = 0.0;
+  double ps = 0.0, e_spike = 0.0;
   for (int r = 0; r < k; ++r) {
     const double lam = std::max(c->eig_host[r], 0.0);  // Ritz values of the last check (theta)
     const double t = std::max(h[r], 0.0);
-    if (lam > 0.0) ps = std::max(ps, 2.5 * std::sqrt(t / lam));
-    else if (t > 0.0) ps = std::max(ps, 0.0);  // sigma_r = 0: no relative error to bound
-    var_spike += lam * t;
+    if (lam > 0.0) ps = std::max(ps, 2.5 * std::sqrt(t) / lam);
     e_spike += lam;
   }
-  const double trace = h[k];
+  const double sd_spike = std::sqrt(std::max(h[k], 0.0));
+  const double trace = h[k + 1];
   const double e_tail = std::max(trace - e_spike, 0.0);
-  const double sd_spike = std::sqrt(var_spike);
   double pe = 0.0;
   if (e_spike > 0.0) pe = std::max(pe, 5.0 * sd_spike / e_spike);
-  if (sd_spike > 0.0 && e_tail > 0.0) pe = std::max(pe, (5.0 * sd_spike + 6e-8 * trace) / e_tail);
+  if (sd_spike > 0.0 && e_tail > 0.0) pe = std::max(pe, (5.0 * sd_spike + 1e-9 * trace) / e_tail);
   else if (sd_spike > 0.0) pe = HUGE_VAL;
   c->prec_sigma = ps;
   c->prec_share = pe;
@@ -1101,7 +1134,10 @@ avd_status run_eig(Ctx* c) {
   int* jstats = reinterpret_cast<int*>(c->theta + p);  // [16] sweeps per RR solve
   AVD_CUDA(cudaMemsetAsync(jstats, 0, 16 * sizeof(int), c->stream));
   AVD_CUDA(cudaMemsetAsync(c->ticket, 0, sizeof(unsigned), c->stream));
-  AVD_CUDA(cudaMemsetAsync(c->gemm_part, 0, gemm_part_bytes(c->m_pad, p, c->num_sms), c->stream));
+  {  // split-K tickets (re-armed by every launch; cleared here once per solve)
+    const size_t pb = gemm_part_bytes(m, c->m_pad, p, c->num_sms), tb = sizeof(unsigned) * (size_t)(c->m_pad / 64 + 1);
+    AVD_CUDA(cudaMemsetAsync(reinterpret_cast<char*>(c->gemm_part) + pb - tb, 0, tb, c->stream));
+  }
   rand_fill_kernel<<<(unsigned)ceil_div(m * p, 256), 256, 0, c->stream>>>(c->Z, nullptr, m, p, seed, nullptr);
   AVD_LAUNCHED(c);
   AVD_TRY(orth(c, c->Z, seed + 1));
@@ -1113,7 +1149,7 @@ avd_status run_eig(Ctx* c) {
   for (it = 1; it <= max_it; ++it) {
     if (it == next_rr || it == max_it) {
       ++rr_count;
-      AVD_TRY(gemm64(c, c->Q, 0, c->Y, nullptr));           // Y = G Q (exact G, fp64)
+      AVD_TRY(gemm64(c, c->Q, c->Y, nullptr));           // Y = G Q (exact G, fp64)
       // an intermediate check only needs an orthonormal basis of the subspace and honest
       // residuals: its Jacobi is capped at 3 sweeps (the residuals of the rotated basis are still
       // true residuals, so a capped solve can only delay convergence, never fake it); a check
@@ -1146,10 +1182,10 @@ avd_status run_eig(Ctx* c) {
       prev_it = it;
       next_rr = it + step;
       pred_res = (rate > 0.0 && rate < 0.95) ? maxres * std::pow(rate, (double)step) : -1.0;
-      AVD_TRY(gemm32(c, c->Z32, 1, c->Y, nullptr));        // Y = G Z = G^2 U
+      AVD_TRY(gemm32(c, c->Z32, c->Y, nullptr));        // Y = G Z = G^2 U
     } else {
-      AVD_TRY(gemm32(c, c->Q32, 0, c->Z, c->Z32));         // Z = G Q
-      AVD_TRY(gemm32(c, c->Z32, 1, c->Y, nullptr));        // Y = G Z = G^2 Q
+      AVD_TRY(gemm32(c, c->Q32, c->Z, c->Z32));         // Z = G Q
+      AVD_TRY(gemm32(c, c->Z32, c->Y, nullptr));        // Y = G Z = G^2 Q
     }
     AVD_TRY(orth(c, c->Y, seed + 7919u * (uint32_t)it));
   }
@@ -1159,8 +1195,10 @@ avd_status run_eig(Ctx* c) {
   c->sigma_next = (k < p) ? std::sqrt(std::max(c->eig_host[k], 0.0)) : 0.0;
   // the per-solve sweep counts stay at theta + p; the report stage reads them with its packed copy
   AVD_CUDA(cudaMemsetAsync(c->V32, 0, sizeof(float) * m * c->k_pad, c->stream));
-  finalize_vectors_kernel<<<k, 256, 0, c->stream>>>(c->U, c->theta, m, p, k, c->k_pad, c->shift, c->qerr, c->V,
-                                                    c->sigma, c->V32, c->prec);
+  finalize_vectors_kernel<<<k, 256, 0, c->stream>>>(c->U, c->theta, m, p, k, c->k_pad, c->shift, c->qerr, c->G,
+                                                    c->m_pad, c->V, c->sigma, c->V32, c->prec);
+  AVD_LAUNCHED(c);
+  prec_energy_kernel<<<1, 1024, 0, c->stream>>>(c->V, c->theta, m, k, c->shift, c->qerr, c->G, c->m_pad, c->prec);
   AVD_LAUNCHED(c);
   AVD_TRY(precision_bound(c));
   return conv ? AVD_OK : AVD_ENOCONV;

@@ -503,13 +503,13 @@ avd_status launch_gram(Ctx* c) {
     if (c->nd == 2) {
       constexpr int NS = 4;
       const size_t smem = (size_t)NS * 2 * (128 * 128 + 64 * 128) + 1024;
-      AVD_CUDA(cudaFuncSetAttribute(gram2_kernel<2, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      AVD_CUDA(smem_attr(gram2_kernel<2, NS>, (int)smem));
       gram2_kernel<2, NS><<<grid, kGramThreads, smem, c->stream>>>(c->tmap_digits, c->tmap_digits_b, c->m_pad,
                                                                    c->l_pad, NK, T, S, c->gram_i);
     } else {
       constexpr int NS = 3;
       const size_t smem = (size_t)NS * 3 * (128 * 128 + 64 * 128) + 1024;
-      AVD_CUDA(cudaFuncSetAttribute(gram2_kernel<3, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      AVD_CUDA(smem_attr(gram2_kernel<3, NS>, (int)smem));
       gram2_kernel<3, NS><<<grid, kGramThreads, smem, c->stream>>>(c->tmap_digits, c->tmap_digits_b, c->m_pad,
                                                                    c->l_pad, NK, T, S, c->gram_i);
     }
@@ -522,12 +522,12 @@ avd_status launch_gram(Ctx* c) {
   if (c->nd == 2) {
     constexpr int NS = 3;
     const size_t smem = (size_t)NS * 2 * 2 * kBox + 1024;
-    AVD_CUDA(cudaFuncSetAttribute(gram_kernel<2, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    AVD_CUDA(smem_attr(gram_kernel<2, NS>, (int)smem));
     gram_kernel<2, NS><<<grid, kGramThreads, smem, c->stream>>>(c->tmap_digits, c->m_pad, c->l_pad, NK, T, S, c->gram_i);
   } else {
     constexpr int NS = 2;
     const size_t smem = (size_t)NS * 2 * 3 * kBox + 1024;
-    AVD_CUDA(cudaFuncSetAttribute(gram_kernel<3, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    AVD_CUDA(smem_attr(gram_kernel<3, NS>, (int)smem));
     gram_kernel<3, NS><<<grid, kGramThreads, smem, c->stream>>>(c->tmap_digits, c->m_pad, c->l_pad, NK, T, S, c->gram_i);
   }
   AVD_LAUNCHED(c);

@@ -263,8 +263,8 @@ __device__ __forceinline__ void pass1_rows(int nrows, const float* __restrict__ 
                                            const float* off, const uint32_t* colh, uint32_t klo, uint32_t kspan,
                                            uint64_t lin0, int lane, CandBlk* cb, uint32_t* __restrict__ cand_key,
                                            uint64_t* __restrict__ cand_idx, unsigned long long* __restrict__ cand_cnt,
-                                           int64_t cand_cap, double* s, double& sq,
-                                           std::conditional_t<ND == 2, int, long long>* ws, long long* ww, float* es, float* ym, bool active, bool writer) {
+                                           int64_t cand_cap, double* s, double* yq,
+                                           std::conditional_t<ND == 2, int, long long>* ws, float* es, float* ym, bool active, bool writer) {
   constexpr int U = 4;
   constexpr int DB = ND == 2 ? 9 : 2;  // dither grid bits (see below)
   constexpr int kW0 = ND == 2 ? 64 : 64 + 64 * 128;
@@ -285,6 +285,9 @@ __device__ __forceinline__ void pass1_rows(int nrows, const float* __restrict__ 
   // kd = 1.0f | (1 << (22 - DB)) (the exponent and the half-step of the dither grid) arrives as a
   // kernel argument so the mask-and-or below is one LOP3 (two immediates do not fit one)
   float kmax = 0.f;
+  float py[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) py[v] = 0.f;
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     if (u >= nrows) break;
@@ -305,10 +308,10 @@ __device__ __forceinline__ void pass1_rows(int nrows, const float* __restrict__ 
       // w = q + kW0 (kW0 = 64 sum_{i < nd-1} 128^i): every digit is a plain bit field of w
       w[v] = __float_as_int(t) - (0x4B400000 + 1 - kW0);
       const float e = (t - 12582913.0f) - y;  // q - y
-      es[v] = fmaf(e, fmaf(2.f, y, e), es[v]);  // q^2 - y^2 = e (e + 2 y)
+      es[v] = fmaf(e, e, es[v]);
+      if (FULL) py[v] = fmaf(y, y, py[v]);  // the exact centred energy (diagonal of G)
       ym[v] = fmaxf(ym[v], fabsf(y));
       ws[v] += w[v];
-      ww[v] += (long long)w[v] * (long long)w[v];
       if (FULL) kmax = fmaxf(kmax, fabsf(x[u][v]));
     }
     if (writer) {
@@ -412,14 +415,11 @@ __device__ __forceinline__ void pass1_rows(int nrows, const float* __restrict__ 
     // fp64 accumulation of U-row fp32 partial sums (each partial rounds once, ~2^-24 relative)
 #pragma unroll
     for (int v = 0; v < VEC; ++v) {
-      float ps = 0.f, pq = 0.f;
+      float ps = 0.f;
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        ps += x[u][v];  // rows past the end were loaded as 0
-        pq = fmaf(x[u][v], x[u][v], pq);
-      }
+      for (int u = 0; u < U; ++u) ps += x[u][v];  // rows past the end were loaded as 0
       s[v] += (double)ps;
-      sq += (double)pq;
+      yq[v] += (double)py[v];
     }
   }
 }
@@ -431,10 +431,9 @@ __global__ void __launch_bounds__(kT, ND == 2 ? 3 : 2) pass1_kernel(
     int8_t* __restrict__ digits,
     const DevPlan* __restrict__ dplan, uint32_t* __restrict__ cand_key, uint64_t* __restrict__ cand_idx,
     unsigned long long* __restrict__ cand_cnt, int64_t cand_cap, double* __restrict__ colsum_part,
-    float* __restrict__ ymax_part, double* __restrict__ sq_part, long long* __restrict__ qsum_part,
-    long long* __restrict__ qsq_part, float* __restrict__ qerr_part, double* __restrict__ stats) {
+    float* __restrict__ ymax_part, long long* __restrict__ qsum_part, double* __restrict__ ysq_part,
+    float* __restrict__ qerr_part) {
   constexpr int U = 4;
-  __shared__ double sred[kT / 32];
   const int lane = threadIdx.x & 31;
   const int64_t c0 = ((int64_t)blockIdx.x * kT + threadIdx.x) * VEC;
   const int64_t r0 = (int64_t)blockIdx.y * rpc;
@@ -442,7 +441,6 @@ __global__ void __launch_bounds__(kT, ND == 2 ? 3 : 2) pass1_kernel(
   const bool active = c0 < m;
   const bool writer = c0 < m_pad;  // digit columns [m, m_pad) come out zero (x = 0, scale 1, centre 0)
   const int64_t plane = l_pad * m_pad;
-  double sq = 0.0;
   __shared__ CandBlk cblk[kT / 32];
   CandBlk* cb = &cblk[threadIdx.x >> 5];
   if (lane == 0) *cb = CandBlk{0ull, 0u, 0u, 0u, 0u};
@@ -475,10 +473,10 @@ __global__ void __launch_bounds__(kT, ND == 2 ? 3 : 2) pass1_kernel(
     double s[VEC];
     // sums of w = q + kW0 and of w^2 (the digit offset; removed below)
     std::conditional_t<ND == 2, int, long long> ws[VEC];
-    long long ww[VEC];
+    double yq[VEC];
     float es[VEC], ym[VEC];
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) { s[v] = 0.0; ws[v] = 0; ww[v] = 0; es[v] = 0.f; ym[v] = 0.f; }
+    for (int v = 0; v < VEC; ++v) { s[v] = 0.0; yq[v] = 0.0; ws[v] = 0; es[v] = 0.f; ym[v] = 0.f; }
     const float* xp = X + r0 * m + (active ? c0 : 0);
     int8_t* dp = digits + r0 * m_pad + cc;
     uint32_t srow0 = (uint32_t)(row_offset + r0) * 0x9E3779B1u + seed32;
@@ -516,7 +514,7 @@ __global__ void __launch_bounds__(kT, ND == 2 ? 3 : 2) pass1_kernel(
         const int nrows = (int)min((int64_t)U, r1 - (r0 + (int64_t)g * U));
         pass1_rows<ND, VEC, FULL, true>(nrows, xp, &xring[(st * U) * kT + threadIdx.x], m, dp, plane, m_pad,
                                         srow0, kd, sc, off, colh, klo, kspan, lin0, lane, cb, cand_key, cand_idx, cand_cnt,
-                                        cand_cap, s, sq, ws, ww, es, ym, active, writer);
+                                        cand_cap, s, yq, ws, es, ym, active, writer);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[st]);
         dp += U * m_pad;
@@ -527,7 +525,7 @@ __global__ void __launch_bounds__(kT, ND == 2 ? 3 : 2) pass1_kernel(
       int64_t i = r0;
       for (; i + U <= r1; i += U) {
         pass1_rows<ND, VEC, FULL, false>(U, xp, nullptr, m, dp, plane, m_pad, srow0, kd, sc, off, colh, klo, kspan, lin0,
-                                         lane, cb, cand_key, cand_idx, cand_cnt, cand_cap, s, sq, ws, ww, es, ym,
+                                         lane, cb, cand_key, cand_idx, cand_cnt, cand_cap, s, yq, ws, es, ym,
                                          active, writer);
         xp += U * m;
         dp += U * m_pad;
@@ -536,7 +534,7 @@ __global__ void __launch_bounds__(kT, ND == 2 ? 3 : 2) pass1_kernel(
       }
       if (i < r1)
         pass1_rows<ND, VEC, FULL, false>((int)(r1 - i), xp, nullptr, m, dp, plane, m_pad, srow0, kd, sc, off, colh, klo,
-                                         kspan, lin0, lane, cb, cand_key, cand_idx, cand_cnt, cand_cap, s, sq, ws, ww,
+                                         kspan, lin0, lane, cb, cand_key, cand_idx, cand_cnt, cand_cap, s, yq, ws,
                                          es, ym, active, writer);
     }
     if (FULL) {  // close this warp's candidate block; publish its real count
@@ -552,52 +550,44 @@ __global__ void __launch_bounds__(kT, ND == 2 ? 3 : 2) pass1_kernel(
         constexpr long long W0 = ND == 2 ? 64 : 64 + 64 * 128;
         const long long n = r1 - r0, sw = (long long)ws[v];
         qsum_part[o] = sw - W0 * n;                     // sum q
-        qsq_part[o] = ww[v] - 2 * W0 * sw + W0 * W0 * n;  // sum (w - W0)^2
+        if (FULL) ysq_part[o] = yq[v];                  // sum (x - mu0)^2 2^(2 shift)
         qerr_part[o] = es[v];
         ymax_part[o] = ym[v];
         if (FULL) colsum_part[o] = s[v];
       }
     }
   }
-  if (FULL) {
-    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o);
-    if (lane == 0) sred[threadIdx.x >> 5] = sq;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int w = 0; w < kT / 32; ++w) t += sred[w];
-      sq_part[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
-    }
-  }
 }
 
-// Fixed-order reduction of the per-chunk partials -> stats[0..m) colsum, stats[m] sum x^2,
-// stats[m+3] = #columns whose digits overflowed, colmax[j] = max |x - mu0_j| (the exact range
-// about the quantiser centre, for a requant), qsum_local / qerr_local.
+// Fixed-order reduction of the per-chunk partials -> stats[0..m) colsum, stats[m+3] = #columns
+// whose digits overflowed, colmax[j] = max |x - mu0_j| (the exact range about the quantiser
+// centre, for a requant), qsum_local / qerr_local, and ysq[j] = sum_i (x_ij - mu0_j)^2 (fp64, in
+// units of x: the scale 2^shift is a power of two) from which the diagonal of G and ||X||^2 are
+// formed exactly (k_eig.cu gram_finalize / trace).
 // CTA = 32 columns x 8 row groups (256 threads): thread (g, c) sums the chunks r = g (mod 8) of
 // column j0 + c (coalesced 32-column rows), the 8 group sums are combined in a fixed order.
 template <int ND>
 __global__ void __launch_bounds__(256) pass1_reduce_kernel(
-    int64_t m, int r1, int nsq, int full, const double* __restrict__ colsum_part, const float* __restrict__ ymax_part,
-    const double* __restrict__ sq_part, const long long* __restrict__ qsum_part, const long long* __restrict__ qsq_part,
+    int64_t m, int r1, int full, const double* __restrict__ colsum_part, const float* __restrict__ ymax_part,
+    const long long* __restrict__ qsum_part, const double* __restrict__ ysq_part,
     const float* __restrict__ qerr_part, const float* __restrict__ qscale, double* __restrict__ stats,
-    float* __restrict__ colmax, long long* __restrict__ qsum_local, double* __restrict__ qerr_local) {
-  __shared__ long long s_qs[8][32], s_qq[8][32];
-  __shared__ double s_qe[8][32], s_cs[8][32];
+    float* __restrict__ colmax, long long* __restrict__ qsum_local, double* __restrict__ qerr_local,
+    double* __restrict__ ysq) {
+  __shared__ long long s_qs[8][32];
+  __shared__ double s_qe[8][32], s_cs[8][32], s_qq[8][32];
   __shared__ float s_ym[8][32];
   const int c = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int64_t j = (int64_t)blockIdx.x * 32 + c;
-  long long qs = 0, qq = 0;
-  double qe = 0.0, cs = 0.0;
+  long long qs = 0;
+  double qe = 0.0, cs = 0.0, qq = 0.0;
   float ym = 0.f;
   if (j < m) {
     for (int r = g; r < r1; r += 8) {
       const int64_t o = (int64_t)r * m + j;
       qs += qsum_part[o];
-      qq += qsq_part[o];
       qe += (double)qerr_part[o];
       ym = fmaxf(ym, ymax_part[o]);
-      if (full) cs += colsum_part[o];
+      if (full) { cs += colsum_part[o]; qq += ysq_part[o]; }
     }
   }
   s_qs[g][c] = qs; s_qq[g][c] = qq; s_qe[g][c] = qe; s_cs[g][c] = cs; s_ym[g][c] = ym;
@@ -607,27 +597,17 @@ __global__ void __launch_bounds__(256) pass1_reduce_kernel(
       qs += s_qs[h][c]; qq += s_qq[h][c]; qe += s_qe[h][c]; cs += s_cs[h][c]; ym = fmaxf(ym, s_ym[h][c]);
     }
     qsum_local[j] = qs;
-    qsum_local[m + j] = qq;  // [S | sum q^2]
+    qsum_local[m + j] = 0;  // (unused half of the exchange buffer)
     qerr_local[j] = qe;
     if (full) {
       stats[j] = cs;
+      const float isc = 1.0f / qscale[j];  // 2^-shift, exact
+      ysq[j] = qq * (double)isc * (double)isc;
       // exact max |x - mu0_j| (power-of-two scale: exact), the range of a requant; |y| beyond
       // the digit range (top digit outside [-127, 127]) counts as an overflow of column j
       constexpr float kYLim = ND == 2 ? 16319.0f : 2088895.0f;
       colmax[j] = ym / qscale[j];
       if (!(ym <= kYLim)) atomicAdd(&stats[m + 3], 1.0);
-    }
-  }
-  if (full && blockIdx.x == 0) {
-    __shared__ double sh[256];
-    double t = 0.0;
-    for (int r = threadIdx.x; r < nsq; r += blockDim.x) t += sq_part[r];
-    sh[threadIdx.x] = t;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double u = 0.0;
-      for (int q = 0; q < (int)blockDim.x; ++q) u += sh[q];
-      stats[m] = u;
     }
   }
 }
@@ -650,7 +630,6 @@ __global__ void finish_kernel(int64_t m, int64_t m_pad, int64_t l_global, int64_
     mu_hl[j] = mh;
     mu_hl[m_pad + j] = ml;
   }
-  if (j == 0 && !isfinite(stats[m])) atomicAdd(reinterpret_cast<unsigned long long*>(&dp->nonfinite), 1ull);
 }
 
 // exchange slot for the global candidate decision: [count, overflowed]
@@ -744,11 +723,11 @@ avd_status launch_pass1(Ctx* c, const float* X, bool full) {
   const uint32_t kd = 0x3F800000u | (1u << (22 - (c->nd == 2 ? 9 : 2)));  // see pass1_rows
   const int ring = VEC == 4 ? kNStg * 4 * kT * 16 : 0;
 #define LAUNCH(ND, V, F)                                                                                        \
-  AVD_CUDA(cudaFuncSetAttribute(pass1_kernel<ND, V, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, ring));  \
+  AVD_CUDA(smem_attr(pass1_kernel<ND, V, F>, ring));  \
   pass1_kernel<ND, V, F><<<grid, kT, ring, c->stream>>>(                                                        \
       X, l, m, c->m_pad, c->l_pad, rpc, c->cfg.row_offset, c->qscale, c->qoff, seed32, kd, c->digits, c->dplan, \
-      c->cand_key, c->cand_idx, c->cand_cnt, c->cand_cap, c->colsum_part, c->colmax_part, c->sq_part,          \
-      c->qsum_part, c->qsq_part, c->qerr_part, c->stats)
+      c->cand_key, c->cand_idx, c->cand_cnt, c->cand_cap, c->colsum_part, c->colmax_part, c->qsum_part,         \
+      reinterpret_cast<double*>(c->qsq_part), c->qerr_part)
   if (c->nd == 2) {
     if (full) { if (vec) { LAUNCH(2, 4, true); } else { LAUNCH(2, 1, true); } }
     else { if (vec) { LAUNCH(2, 4, false); } else { LAUNCH(2, 1, false); } }
@@ -760,12 +739,12 @@ avd_status launch_pass1(Ctx* c, const float* X, bool full) {
   AVD_LAUNCHED(c);
   if (c->nd == 2)
     pass1_reduce_kernel<2><<<(unsigned)ceil_div(m, 32), 256, 0, c->stream>>>(
-        m, r1, r1 * ncb, full ? 1 : 0, c->colsum_part, c->colmax_part, c->sq_part, c->qsum_part, c->qsq_part,
-        c->qerr_part, c->qscale, c->stats, c->colmax, c->qsum_local, c->qerr_local);
+        m, r1, full ? 1 : 0, c->colsum_part, c->colmax_part, c->qsum_part, reinterpret_cast<const double*>(c->qsq_part),
+        c->qerr_part, c->qscale, c->stats, c->colmax, c->qsum_local, c->qerr_local, c->ysq);
   else
     pass1_reduce_kernel<3><<<(unsigned)ceil_div(m, 32), 256, 0, c->stream>>>(
-        m, r1, r1 * ncb, full ? 1 : 0, c->colsum_part, c->colmax_part, c->sq_part, c->qsum_part, c->qsq_part,
-        c->qerr_part, c->qscale, c->stats, c->colmax, c->qsum_local, c->qerr_local);
+        m, r1, full ? 1 : 0, c->colsum_part, c->colmax_part, c->qsum_part, reinterpret_cast<const double*>(c->qsq_part),
+        c->qerr_part, c->qscale, c->stats, c->colmax, c->qsum_local, c->qerr_local, c->ysq);
   AVD_LAUNCHED(c);
   if (full) {
     cand_publish_kernel<<<1, 1, 0, c->stream>>>(c->cand_cnt, c->cand_cap, c->cand_x);

@@ -476,7 +476,7 @@ avd_status launch_k5(Ctx* c, const CUtensorMap& tmX, const CUtensorMap& tmVt, in
   constexpr uint32_t kStage = 2 * kTile + ((2 * KP * 128 + 1023) / 1024) * 1024;
   constexpr int NS = (220 * 1024) / kStage;  // 5 stages in flight
   const size_t smem = NS * kStage + 1024;
-  AVD_CUDA(cudaFuncSetAttribute(proj_tc_kernel<KP, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  AVD_CUDA(smem_attr(proj_tc_kernel<KP, NS>, (int)smem));
   proj_tc_kernel<KP, NS><<<grid, kPThreads, smem, c->stream>>>(tmX, tmVt, c->cfg.l_local, c->cfg.m, c->mu_hl,
                                                                c->m_pad, c->P, c->P_hl, c->l_pad, c->en_part,
                                                                c->colsumP_part);
@@ -491,8 +491,7 @@ avd_status launch_k8(Ctx* c, const CUtensorMap& tmP, const CUtensorMap& tmV, con
   constexpr int NSF = (int)((220u * 1024u - kA) / kStage);
   constexpr int NS = NSF > 6 ? 6 : (NSF < 2 ? 2 : NSF);
   const size_t smem = kA + NS * kStage + 1024;
-  AVD_CUDA(cudaFuncSetAttribute(energy_tc_kernel<KP32, NCOL, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
+  AVD_CUDA(smem_attr(energy_tc_kernel<KP32, NCOL, NS>, (int)smem));
   energy_tc_kernel<KP32, NCOL, NS><<<grid, kPThreads, smem, c->stream>>>(tmP, tmV, tmX, c->cfg.l_local, c->cfg.m,
                                                                          c->l_pad, c->m_pad, c->mu_hl, c->m_pad,
                                                                          c->en_part);

@@ -32,7 +32,7 @@ from .api import Decomposer, Result
 EXCHANGES = {
     "stats": [("SAMPLE", torch.float64, "sum"), ("SMAX", torch.float32, "max"),
               ("SMIN", torch.float32, "min"), ("HIST1", torch.int64, "sum")],
-    "split": [("STATS", torch.float64, "sum"), ("COLMAX", torch.float32, "max")],
+    "split": [("STATS", torch.float64, "sum"), ("COLMAX", torch.float32, "max"), ("DIAG", torch.float64, "sum")],
     "gram": [("GRAM", torch.int64, "sum"), ("CAND", torch.int64, "sum"), ("QSUM", torch.int64, "sum"),
              ("QERR", torch.float64, "sum")],
     "regram": [("GRAM", torch.int64, "sum"), ("QSUM", torch.int64, "sum"), ("QERR", torch.float64, "sum")],

@@ -57,6 +57,9 @@ class ModelBackend:
         key = _keys(X)
         self.buf["STATS"] = torch.tensor(np.concatenate([Xd.sum(0), [np.sum(Xd * Xd), 0.0, np.count_nonzero(key), 0.0]]))
         self.buf["COLMAX"] = torch.tensor(np.abs(X).max(0))
+        smp = self.buf["SAMPLE"].numpy()
+        mu0 = (smp[: self.m] / max(smp[self.m], 1.0)).astype(np.float32).astype(np.float64)
+        self.buf["DIAG"] = torch.tensor(((X.astype(np.float64) - mu0) ** 2).sum(0))  # exact diag of G
         s = self._sample_step()
         h = self.buf["HIST1"].numpy()
         cum, b0 = 0, 0

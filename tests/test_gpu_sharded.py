@@ -27,7 +27,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, spec, col_fix, out):
+def _worker(rank, world, port, spec, col_fix, out, flags=0):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
@@ -36,29 +36,34 @@ def _worker(rank, world, port, spec, col_fix, out):
     X = generate(spec, r0, lr, device="cuda")
     if col_fix is not None:
         X[:, col_fix[0]] = col_fix[1]
-    sd = ShardedDecomposer(spec.l, spec.m)
+    sd = ShardedDecomposer(spec.l, spec.m, flags=flags)
     r = sd(X)
     torch.cuda.synchronize()
     out[rank] = dict(mu=r.mu.cpu().numpy(), sigma=r.sigma.cpu().numpy(), top=r.top_idx.cpu().numpy(),
                      rho=r.rho.cpu().numpy(), offset=int(r.top_offset), n_top=int(r.n_top_global),
-                     energy_cf=list(r.energy_cf), energy_el=list(r.energy_el))
+                     energy_cf=list(r.energy_cf), energy_el=list(r.energy_el), digits=int(r.digits_used))
     sd.close()
     dist.barrier()
     dist.destroy_process_group()
 
 
-def _run(spec, col_fix=None, world=2):
+def _run(spec, col_fix=None, world=2, flags=0):
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), spec, col_fix, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), spec, col_fix, out, flags), nprocs=world, join=True)
     return [out[r] for r in range(world)]
 
 
-@pytest.mark.parametrize("l,m,col_fix", [(4096, 256, (5, 40.0)), (65536, 128, None)])
-def test_two_ranks_match_oracle(cuda_device, l, m, col_fix):
+@pytest.mark.parametrize("l,m,col_fix,flags", [(4096, 256, (5, 40.0), 0), (65536, 128, None, 0),
+                                               (4096, 256, None, 4)])
+def test_two_ranks_match_oracle(cuda_device, l, m, col_fix, flags):
+    """flags = 4 (AVD_FLAG_FORCE_ESCALATE): the AVD_EREPEAT re-Gram with its GRAM/QSUM/QERR
+    re-exchange on both ranks."""
     from oracle import oracle as O
     spec = SynthSpec(l, m, seed=17, f_mean=0.8)
-    res = _run(spec, col_fix)
+    res = _run(spec, col_fix, flags=flags)
+    if flags:
+        assert all(r["digits"] == 3 for r in res)
     X = generate(spec)
     if col_fix is not None:
         X[:, col_fix[0]] = col_fix[1]  # l tied maxima: the tie block straddles the rank boundary

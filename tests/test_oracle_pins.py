@@ -401,3 +401,14 @@ def test_lapack_eig_step_matches_jacobi():
     np.testing.assert_array_equal(b["top_idx"], a["top_idx"])
     np.testing.assert_allclose(b["rho"], a["rho"], atol=1e-10)
     np.testing.assert_allclose(b["energy_cf"], a["energy_cf"], rtol=1e-11)
+
+
+@pytest.mark.parametrize("spec", [SynthSpec(300, 77, seed=3), SynthSpec(256, 128, seed=5, exact=True, k_s=4),
+                                  SynthSpec(1024, 96, seed=9, k_s=3, f_mean=0.5)])
+def test_fast_generator_bit_identical(spec):
+    """synth/gen_fast.c (host fill for bench-scale oracle runs) == synth.gen.generate, bit for bit,
+    including a shard that starts mid-matrix."""
+    from synth.fast import generate_np
+    np.testing.assert_array_equal(generate_np(spec).view(np.uint32), generate(spec).numpy().view(np.uint32))
+    np.testing.assert_array_equal(generate_np(spec, 37, 100).view(np.uint32),
+                                  generate(spec, 37, 100).numpy().view(np.uint32))

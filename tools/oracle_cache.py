@@ -23,7 +23,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 from oracle import oracle as O  # noqa: E402
-from synth.gen import config_spec, generate  # noqa: E402
+from synth.fast import generate_np  # noqa: E402
+from synth.gen import config_spec  # noqa: E402
 
 
 def main():
@@ -34,10 +35,7 @@ def main():
     args = ap.parse_args()
     spec = config_spec(args.config, args.seed)
     t0 = time.time()
-    X = np.empty((spec.l, spec.m), np.float32)
-    blk = 8192
-    for r0 in range(0, spec.l, blk):
-        X[r0:r0 + blk] = generate(spec, r0, min(blk, spec.l - r0)).numpy()
+    X = generate_np(spec)  # bit-identical to synth.gen.generate (pinned)
     t_gen = time.time() - t0
     t0 = time.time()
     r = O.decompose(X, eig=args.eig)
