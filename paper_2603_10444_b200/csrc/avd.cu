@@ -172,6 +172,7 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   L.add(sizeof(double) * (4 + 2 * C->m_pad));                            // 68 diag: |mu|, scratch, q, y
   L.add(sizeof(double) * kMaxP);                                         // 69 prec
   L.add(sizeof(double) * m);                                             // 70 ysq
+  L.add(kEigCtlBytes);                                                   // 71 eig_ctl
   if (L.n >= 128) { set_error("workspace layout table overflow"); return AVD_EINVAL; }
   plan->workspace_bytes = L.total;
   if (lay) *lay = L;
@@ -243,13 +244,15 @@ __global__ void report_pack_kernel(const double* __restrict__ report, const doub
                                    const double* __restrict__ energy, const double* __restrict__ stats,
                                    const double* __restrict__ trace, const double* __restrict__ diag,
                                    const double* __restrict__ sigma, const DevPlan* __restrict__ dp,
-                                   const double* __restrict__ jstats, int64_t m, int k, int k_pad,
-                                   double* __restrict__ pack) {
+                                   const double* __restrict__ jstats, const int* __restrict__ uctl, int64_t m,
+                                   int k, int k_pad, double* __restrict__ pack) {
   const int t = threadIdx.x;
   if (t < 5) pack[t] = report[t];
   if (t < 8) pack[8 + t] = agg[t];
   if (t < 4) pack[16 + t] = energy[t];
   if (t == 0) { pack[20] = stats[m]; pack[21] = trace[0]; pack[24] = diag[0]; }
+  if (t < 3) pack[25 + t] = diag[1 + t];  // uncentred lambda_1, residual, mu . v_1
+  if (t < 2) pack[28 + t] = (double)uctl[t];  // blocks, steps of the uncentred power iteration
   if (t < 2) pack[22 + t] = energy[4 + k_pad + t];
   for (int r = t; r < k; r += blockDim.x) pack[kPackHead + r] = sigma[r];
   const unsigned long long* pw = reinterpret_cast<const unsigned long long*>(dp);
@@ -337,9 +340,9 @@ avd_status avd_create(const avd_config* cfg, avd_ctx** out) {
   BIND(samp, double*); BIND(smax, float*); BIND(smin, float*); BIND(qscale, float*); BIND(qoff, float*);
   BIND(qsum_part, long long*); BIND(qsum_local, long long*); BIND(qerr_part, float*); BIND(qerr_local, double*);
   BIND(qerr, double*); BIND(mu0, float*); BIND(qsq_part, long long*); BIND(diag, double*);
-  BIND(prec, double*); BIND(ysq, double*);
+  BIND(prec, double*); BIND(ysq, double*); BIND(eig_ctl, void*);
 #undef BIND
-  if (cudaMallocHost(&c->eig_host, sizeof(double) * 4 * kMaxP) != cudaSuccess) {
+  if (cudaMallocHost(&c->eig_host, sizeof(double) * kHostScratch) != cudaSuccess) {
     cudaGetLastError();
     cudaFree(c->ws);
     delete c;
@@ -364,6 +367,7 @@ avd_status avd_create(const avd_config* cfg, avd_ctx** out) {
 
 void avd_destroy(avd_ctx* c) {
   if (!c) return;
+  destroy_graphs(c);
   cudaFree(c->ws);
   cudaFreeHost(c->eig_host);
   if (c->ev_host) cudaEventDestroy(c->ev_host);
@@ -507,7 +511,9 @@ avd_status avd_stage_gram(avd_ctx* c, const float* X) {
 avd_status avd_stage_eig(avd_ctx* c) {
   STAGE_CHECK(c, 3);
   AVD_TRY(launch_gram_finalize(c));
+  AVD_TRY(launch_uncentred(c));  // mean-bias diagnostics, side stream
   avd_status st = run_eig(c);
+  AVD_TRY(join_uncentred(c));    // (stream order only; G32 is not rewritten before the join)
   if (st != AVD_OK && st != AVD_ENOCONV) return st;
   // automatic digits (avd_config.digits == 0): the quantisation-error bound decides whether the
   // 2-digit operand meets half the north-star tolerances; if not, redo the Gram with 3 digits.
@@ -520,7 +526,6 @@ avd_status avd_stage_eig(avd_ctx* c) {
     set_error("Gram operand raised to 3 digits: call avd_stage_gram again");
     return AVD_EREPEAT;
   }
-  AVD_TRY(run_uncentred(c));  // mean-bias diagnostics
   c->stage = 4;
   return st;
 }
@@ -582,7 +587,9 @@ avd_status avd_stage_report(avd_ctx* c, avd_outputs* out) {
   const int64_t npack = kPackHead + k + kPlanWords + 8;
   double* pack = c->red_part + ((int64_t)c->n_red * c->p * c->p - npack);
   report_pack_kernel<<<1, 128, 0, c->stream>>>(c->report, c->agg, c->energy, c->stats, c->trace, c->diag, c->sigma,
-                                               c->dplan, c->theta + c->p, m, k, c->k_pad, pack);
+                                               c->dplan, c->theta + c->p,
+                                               reinterpret_cast<const int*>(c->eig_ctl) + kCtlBlocksU, m, k,
+                                               c->k_pad, pack);
   AVD_LAUNCHED(c);
   static_assert(kPackHead + 96 + kPlanWords + 8 <= 4 * kMaxP, "pinned scratch too small for the report pack");
   const double* h = c->eig_host;  // pinned scratch (k <= 95)
@@ -631,6 +638,15 @@ avd_status avd_stage_report(avd_ctx* c, avd_outputs* out) {
   out->p_pos = (int64_t)h[22];
   out->p_neg = (int64_t)h[23];
   out->sign_fraction = c->sign_valid ? (double)std::max(out->p_pos, out->p_neg) / lg : -1.0;
+  {  // uncentred top pair (k_eig.cu launch_uncentred): diag[0] = ||mu||, lambda_1, residual, mu . v_1
+    const double nmu = h[24];
+    c->sigma1_u = std::sqrt(std::max(h[25], 0.0));
+    c->alpha1 = std::fabs(h[27]);
+    c->cos_mu_v1 = nmu > 0.0 ? std::min(1.0, std::fabs(h[27]) / nmu) : 0.0;
+    c->resid_u = h[26];
+    c->iters_u = (int)h[29];
+    c->launches += (int64_t)c->n_u_nodes * (int64_t)h[28];
+  }
   out->cos_mu_v1 = c->cos_mu_v1;
   out->alpha1 = c->alpha1;
   out->sigma1_u = c->sigma1_u;

@@ -16,6 +16,9 @@ constexpr int kGramTile = 128;    // Gram tile edge (rows of A / B panels)
 constexpr int kGramK = 128;       // K rows per pipeline stage (one 128-byte swizzle row of int8)
 constexpr int kMaxP = 112;        // subspace block size cap (two p x p fp64 matrices in smem)
 constexpr int kRedRowsC = 128;    // rows per partial of the m-length p x p reductions (k_eig.cu)
+constexpr int kEigCtlBytes = 256; // device-resident loop state of the eigensolver graph (k_eig.cu)
+constexpr int kCtlBlocksU = 10;   // int index of EigCtl::blocks_u (then iters_u), read by the report
+constexpr int kHostScratch = 8 * kMaxP;  // doubles of the pinned host scratch (eig_host)
 
 // Device-side "plan2": values decided on the device after the stats exchange.
 struct DevPlan {
@@ -106,6 +109,13 @@ struct Ctx {
   float *Q32 = nullptr, *Z32 = nullptr;  // [m][p] fp32 mirrors of Q, Z
   unsigned* ticket = nullptr;     // last-CTA ticket of the fused reductions
   double* gmax = nullptr;         // max |G| (fixed-point scale of the Y = G Q accumulation)
+  void* eig_ctl = nullptr;        // [kEigCtlBytes] loop state of the eigensolver graph
+  cudaGraphExec_t eig_exec = nullptr;   // subspace-iteration loop (built once per context)
+  cudaGraphExec_t unc_exec = nullptr;   // uncentred power iteration loop (diagnostics)
+  cudaStream_t cap_stream = nullptr;    // private stream the graphs are captured on
+  cudaStream_t side_stream = nullptr;   // the uncentred loop runs here, concurrent with the eig
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int n_begin_nodes = 0, n_rr_nodes = 0, n_pow_nodes = 0, n_u_nodes = 0;  // kernels per graph body
   // mean-bias diagnostics: diag[0] = ||mu||, diag[4..4+m_pad) = q,
   // diag[4+m_pad..) = y of the uncentred power iteration
   double* diag = nullptr;
@@ -196,7 +206,9 @@ __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_
 avd_status launch_sample(Ctx* c, const float* X);          // k_pass1.cu
 avd_status launch_pass1(Ctx* c, const float* X, bool full); // k_pass1.cu
 avd_status launch_finish(Ctx* c);                          // k_pass1.cu
-avd_status run_uncentred(Ctx* c);                          // k_eig.cu (mean-bias diagnostics)
+avd_status launch_uncentred(Ctx* c);                       // k_eig.cu (mean-bias diagnostics, side stream)
+avd_status join_uncentred(Ctx* c);                         // k_eig.cu
+void destroy_graphs(Ctx* c);                               // k_eig.cu
 avd_status launch_sign_count(Ctx* c);                      // k_project.cu (mean-bias diagnostics)
 avd_status launch_gram(Ctx* c);                            // k_gram.cu
 avd_status gram_make_tmap(Ctx* c);                         // k_gram.cu

@@ -19,6 +19,8 @@
 // Rank deficiency (G = 0, rank(G) < p, m < p) flags the failing columns, which are re-drawn at
 // random and re-orthonormalised (R11).  Deterministic: no floating-point atomics.
 #include <cfloat>
+#include <cstdlib>
+#include <cstddef>
 #include "common.cuh"
 
 namespace avd {
@@ -123,12 +125,14 @@ __device__ __forceinline__ double rnd_sym(uint32_t seed, uint32_t a, uint32_t b)
 }
 
 // Q[j][c] = U(-1,1) for columns with flag (or all when flags == nullptr); Q32 mirrors it
+// (seed + 7919 * *itp when itp != nullptr: the iteration counter of the device-resident loop)
 __global__ void rand_fill_kernel(double* __restrict__ Q, float* __restrict__ Q32, int64_t m, int p, uint32_t seed,
-                                 const int* __restrict__ flags) {
+                                 const int* __restrict__ flags, const int* __restrict__ itp) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= m * p) return;
   const int c = (int)(t % p);
   if (flags && !flags[c]) return;
+  if (itp) seed += 7919u * (uint32_t)(*itp);
   const double v = rnd_sym(seed, (uint32_t)(t / p), (uint32_t)c);
   Q[t] = v;
   if (Q32) Q32[t] = (float)v;
@@ -164,7 +168,9 @@ template <typename T, int NR, int NC>
 __global__ void __launch_bounds__(kSkThreads) gemm_kernel(const T* __restrict__ G, int64_t ldg,
                                                           const T* __restrict__ Qin, int64_t m, int KT, int KS,
                                                           T* __restrict__ part, unsigned* __restrict__ tickets,
-                                                          double* __restrict__ Y, float* __restrict__ Y32) {
+                                                          double* __restrict__ Y, float* __restrict__ Y32,
+                                                          const int* __restrict__ skip) {
+  if (skip && *skip) return;  // device-side gate (eigensolver graph: Z comes from the RR check)
   constexpr int BM = 16 * NR;
   constexpr int p = 8 * NC;
   constexpr int SG = kSkBK * BM;          // elements of one G stage
@@ -264,8 +270,27 @@ __global__ void __launch_bounds__(kSkThreads) gemm_kernel(const T* __restrict__ 
   // the row block's last CTA: fixed-order sum of the KS partials
   const T* base = part + (int64_t)rb * KS * (BM * p);
   for (int e = tid * 2; e < BM * p; e += kSkThreads * 2) {
+    // the KS partials in order; loads batched 8 at a time so they are in flight together (the
+    // sum is still the sequential q order)
     double s0 = 0.0, s1 = 0.0;
-    for (int q = 0; q < KS; ++q) {
+    int q = 0;
+    for (; q + 8 <= KS; q += 8) {
+      double a0[8], a1[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const T* src = base + (int64_t)(q + u) * (BM * p) + e;
+        if constexpr (sizeof(T) == 4) {
+          const float2 v = __ldcg(reinterpret_cast<const float2*>(src));
+          a0[u] = (double)v.x; a1[u] = (double)v.y;
+        } else {
+          const double2 v = __ldcg(reinterpret_cast<const double2*>(src));
+          a0[u] = v.x; a1[u] = v.y;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { s0 += a0[u]; s1 += a1[u]; }
+    }
+    for (; q < KS; ++q) {
       const T* src = base + (int64_t)q * (BM * p) + e;
       if constexpr (sizeof(T) == 4) {
         const float2 v = __ldcg(reinterpret_cast<const float2*>(src));
@@ -302,16 +327,17 @@ __device__ __forceinline__ double rsqrt_fast(double x) {  // 1/sqrt(x), x in the
 // while (c, s) are made orthogonal to fp64 accuracy: c^2 + s^2 = 1 + d from the fp32 pair, scaled by
 // (1 + d)^(-1/2) = 1 - d/2 + 3d^2/8 (|d| <~ 1e-7), so every applied transform is an exact-in-fp64
 // similarity and the eigenvalues keep fp64 accuracy.  Skipped when |a_pq| <= 1e-9 sqrt(a_pp a_qq).
-__device__ __forceinline__ void jacobi_rotation(double app, double aqq, double apq, double& c, double& s, bool& rot) {
+__device__ __forceinline__ void jacobi_rotation(double app, double aqq, double apq, double& c, double& s, bool& rot,
+                                                double thr2 = 1e-18) {
   c = 1.0;
   s = 0.0;
   rot = false;
   // |a_pq| <= 1e-9 sqrt(a_pp a_qq): eigenvalue error ~1e-18 relative, eigenvector error ~1e-9 / gap
-  if (!(apq * apq > 1e-18 * fabs(app * aqq)) || fabs(apq) < 1e-30 || fabs(apq) > 1e30) return;
+  if (!(apq * apq > thr2 * fabs(app * aqq)) || fabs(apq) < 1e-30 || fabs(apq) > 1e30) return;
   const float th = __fdividef(0.5f * (float)(aqq - app), (float)apq);
   const float ath = fabsf(th);
   if (!(ath < 1e18f)) return;  // |a_pq| below 1e-18 |a_qq - a_pp|: nothing left to rotate
-  float t = __frcp_rn(ath + sqrtf(fmaf(th, th, 1.0f)));
+  float t = __fdividef(1.0f, ath + sqrtf(fmaf(th, th, 1.0f)));
   t = th >= 0.f ? t : -t;
   const float c32 = rsqrtf(fmaf(t, t, 1.0f));
   const double c0 = (double)c32, s0 = (double)(t * c32);
@@ -329,83 +355,70 @@ __device__ __forceinline__ void rr_pair(int p, int step, int i, int& P, int& Q) 
   Q = max(a, b);
 }
 
-// Parallel (round-robin) Jacobi on the symmetric A (P x P, ld LDA, scaled so max|a_ii| ~ 1) with
-// V^T (ld P).  Per step: warp u computes the rotation J_u of its pair (P_u, Q_u) (lane 0), then,
-// after one barrier, rewrites ITS two rows of A as rows of J_u^T A J (lane w takes the column
-// pair (P_w, Q_w) of the step, so each 2x2 block sees both rotations) and its two rows of
-// V^T (V <- V J).  Every row belongs to exactly one pair: no two warps touch the same element.
-// Two barriers per step.  Returns the number of sweeps.
+// One-sided (Hestenes) Jacobi on the symmetric positive semidefinite A (P x P, ld LDA): rotate
+// column pairs of A (A <- A J) and of V (rows of V^T) until every pair of columns is orthogonal;
+// then A = H V has orthogonal columns, ||A_j|| = lambda_j and V holds the eigenvectors (for PSD H the
+// singular and eigen decompositions coincide).  The rotation of a pair comes from its Gram entries
+// (alpha = |a_p|^2, beta = |a_q|^2, gamma = a_p . a_q) by the same Rutishauser formula as the
+// two-sided method; stop when gamma^2 <= 1e-20 alpha beta for every pair.  Step s rotates the P/2
+// disjoint pairs of the round-robin ordering; warp u owns pair u (its two columns of A and two rows
+// of V^T), so a step needs no synchronisation inside, only one barrier before the next step.
+// kfix < P: the basis is ordered (columns >= kfix span the unconverged tail of the spectrum) and
+// rotations between two tail columns are skipped — they only mix tail vectors among themselves, so
+// the leading kfix pairs are exact eigenpairs of A once the coupling pairs are orthogonal, and the
+// tail block (whose Ritz vectors are not converged anyway) costs no sweeps.  Returns the sweeps.
 template <int P, int LDA>
-__device__ int jacobi_block(double* A, double* Vt, double* rc, double* rs, int* rp, int* rq, int* flag, int max_sweeps) {
+__device__ int jacobi_onesided(double* A, double* Vt, int* fl, int max_sweeps, int kfix) {
   constexpr int half = P / 2;
+  constexpr int E = (P + 31) / 32;  // column elements per lane
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
   int sweep = 0;
   for (; sweep < max_sweeps; ++sweep) {
-    if (threadIdx.x == 0) *flag = 0;
+    if (threadIdx.x == 0) fl[sweep & 1] = 0;  // read after this sweep's last barrier
+    __syncthreads();
     for (int step = 0; step < P - 1; ++step) {
-      __syncthreads();
-#ifdef AVD_EIG_PROBE
-      long long t_a = clock64();
-#endif
-      if (warp == 0) {
-        bool any = false;
-        for (int u = lane; u < half; u += 32) {  // all rotations of the step, one lane each
-          int p0, q0;
-          rr_pair(P, step, u, p0, q0);
-          double c, s;
-          bool rot;
-          jacobi_rotation(A[p0 * LDA + p0], A[q0 * LDA + q0], A[p0 * LDA + q0], c, s, rot);
-          rc[u] = c;
-          rs[u] = s;
-          rp[u] = p0;
-          rq[u] = q0;
-          any |= rot;
-        }
-        if (__any_sync(0xFFFFFFFFu, any) && lane == 0) *flag = 1;
-      }
-#ifdef AVD_EIG_PROBE
-      long long t_b = clock64();
-#endif
-      __syncthreads();
-#ifdef AVD_EIG_PROBE
-      long long t_c = clock64();
-      if (threadIdx.x == 0) { g_probe_clk[8] += t_b - t_a; g_probe_clk[9] += t_c - t_b; }
-#endif
       for (int u = warp; u < half; u += nwarps) {
-        const double cu = rc[u], su = rs[u];
-        const int p1 = rp[u], q1 = rq[u];
-        for (int w = lane; w < half; w += 32) {
-          const double cw = rc[w], sw = rs[w];
-          if (su == 0.0 && sw == 0.0) continue;
-          const int p2 = rp[w], q2 = rq[w];
-          const double a = A[p1 * LDA + p2], b = A[p1 * LDA + q2], c_ = A[q1 * LDA + p2], d = A[q1 * LDA + q2];
-          // rows: J_u^T, then columns: J_w
-          const double a1 = cu * a - su * c_, b1 = cu * b - su * d;
-          const double c1 = su * a + cu * c_, d1 = su * b + cu * d;
-          const double a2 = cw * a1 - sw * b1, b2 = sw * a1 + cw * b1;
-          const double c2 = cw * c1 - sw * d1, d2 = sw * c1 + cw * d1;
-          A[p1 * LDA + p2] = a2;
-          A[p1 * LDA + q2] = b2;
-          A[q1 * LDA + p2] = c2;
-          A[q1 * LDA + q2] = d2;
+        int pc, qc;
+        rr_pair(P, step, u, pc, qc);
+        if (pc >= kfix) continue;  // tail-tail pair (pc < qc)
+        double ap[E], aq[E];
+        double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+        for (int t = 0; t < E; ++t) {
+          const int i = lane + 32 * t;
+          ap[t] = i < P ? A[i * LDA + pc] : 0.0;
+          aq[t] = i < P ? A[i * LDA + qc] : 0.0;
+          al = fma(ap[t], ap[t], al);
+          be = fma(aq[t], aq[t], be);
+          ga = fma(ap[t], aq[t], ga);
         }
-        if (su != 0.0) {
-          // V <- V J_u: rows p1, q1 of V^T, two columns per lane
-          for (int j = 2 * lane; j < P; j += 64) {
-            double2* vp = reinterpret_cast<double2*>(Vt + p1 * P + j);
-            double2* vq = reinterpret_cast<double2*>(Vt + q1 * P + j);
-            const double2 x = *vp, y = *vq;
-            *vp = make_double2(cu * x.x - su * y.x, cu * x.y - su * y.y);
-            *vq = make_double2(su * x.x + cu * y.x, su * x.y + cu * y.y);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xFFFFFFFFu, al, o);
+          be += __shfl_xor_sync(0xFFFFFFFFu, be, o);
+          ga += __shfl_xor_sync(0xFFFFFFFFu, ga, o);
+        }
+        double c, sn;
+        bool rot;
+        jacobi_rotation(al, be, ga, c, sn, rot, 1e-20);  // identical in every lane
+        if (!rot) continue;
+        if (lane == 0) fl[sweep & 1] = 1;
+#pragma unroll
+        for (int t = 0; t < E; ++t) {
+          const int i = lane + 32 * t;
+          if (i < P) {
+            A[i * LDA + pc] = c * ap[t] - sn * aq[t];
+            A[i * LDA + qc] = sn * ap[t] + c * aq[t];
+            const double vp = Vt[pc * P + i], vq = Vt[qc * P + i];
+            Vt[pc * P + i] = c * vp - sn * vq;
+            Vt[qc * P + i] = sn * vp + c * vq;
           }
         }
       }
+      __syncthreads();
     }
-    __syncthreads();
-    const int any = *flag;
-    __syncthreads();
-    if (!any) break;
+    if (!fl[sweep & 1]) break;
   }
   return sweep + 1;
 }
@@ -492,7 +505,7 @@ template <int MODE, int PC>
 __global__ void __launch_bounds__(RedCfg<PC>::threads) atb_fused_kernel(
     const double* __restrict__ A, const double* __restrict__ B, int64_t m, double* __restrict__ part,
     unsigned* __restrict__ ticket, double* __restrict__ out0, double* __restrict__ out1, int* __restrict__ ibad,
-    int* __restrict__ stats, const int* __restrict__ gate, int max_sweeps) {
+    int* __restrict__ stats, const int* __restrict__ gate, int max_sweeps, const int* __restrict__ msw) {
   constexpr int p = PC * 16;
   constexpr int NT = RedCfg<PC>::threads;
   constexpr int kRedChunk = RedCfg<PC>::chunk;
@@ -560,9 +573,8 @@ __global__ void __launch_bounds__(RedCfg<PC>::threads) atb_fused_kernel(
   double* S = fsm;            // p x ld
   double* X = fsm + p * ld;   // p x p (V^T for MODE 2)
   __shared__ double aux[p];
-  __shared__ double rcs[2][p / 2];
-  __shared__ int rpq[2][p / 2];
-  __shared__ int flag_sh, badsh[p], rank_sh[p], escale;
+  __shared__ int jfl[2];         // per-sweep "any rotation" flag
+  __shared__ int badsh[p], rank_sh[p], escale;
   // fixed-order sum of the partials: thread t owns the element pair (2t, 2t+1), all loads of a
   // batch of 8 partials in flight at once
   for (int t = threadIdx.x; t < p * p / 2; t += NT) {
@@ -646,9 +658,16 @@ __global__ void __launch_bounds__(RedCfg<PC>::threads) atb_fused_kernel(
   // MODE 2: Rayleigh-Ritz eigensolve (X holds V^T, ld p)
   for (int t = threadIdx.x; t < p * p; t += NT) X[t] = (t / p == t % p) ? 1.0 : 0.0;
   PROBE(4);
-  const int sweeps = jacobi_block<p, ld>(S, X, rcs[0], rcs[1], rpq[0], rpq[1], &flag_sh, max_sweeps);
+  // msw[0]: sweep cap, msw[1]: leading block of an ordered basis (p: none)
+  const int sweeps = jacobi_onesided<p, ld>(S, X, jfl, msw ? msw[0] : max_sweeps, msw ? msw[1] : p);
+  // lambda_j = ||A e_j||, A = H V (fixed-order per-warp sums)
+  for (int j = threadIdx.x >> 5; j < p; j += NT / 32) {
+    double t = 0.0;
+    for (int i = threadIdx.x & 31; i < p; i += 32) t = fma(S[i * ld + j], S[i * ld + j], t);
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xFFFFFFFFu, t, o);
+    if ((threadIdx.x & 31) == 0) aux[j] = sqrt(t);
+  }
   PROBE(5);
-  if (threadIdx.x < p) aux[threadIdx.x] = S[threadIdx.x * ld + threadIdx.x];
   __syncthreads();
   if (threadIdx.x < p) {
     int rk = 0;
@@ -763,77 +782,117 @@ __global__ void resid_kernel(const double* __restrict__ Z, const double* __restr
 
 // V_out[j][r] = sign_r * U[j][r] (r < k), sign making the largest-|.| entry positive
 // (smallest j on ties; R8); sigma_r = sqrt(max(theta_r, 0)); V32 fp32 copy.
-// Also t_r = sum_a d_a^2 v_ra^2 (lambda_r (1 - 2 v_ra^2) + v_ra^2 G_aa) over the columns with
-// rounding errors (precision bound, run_eig).
-__global__ void finalize_vectors_kernel(const double* __restrict__ U, const double* __restrict__ theta, int64_t m,
-                                        int p, int k, int k_pad, const int32_t* __restrict__ shift,
-                                        const double* __restrict__ qerr, const double* __restrict__ G, int64_t ldg,
-                                        double* __restrict__ V, double* __restrict__ sigma, float* __restrict__ V32,
-                                        double* __restrict__ prec) {
-  __shared__ double sv[256], st[256];
-  __shared__ int64_t sj[256];
-  const int r = blockIdx.x;
-  double best = -1.0, tr = 0.0;
-  int64_t bj = 0;
-  const double lam = fmax(theta[r], 0.0);
-  for (int64_t j = threadIdx.x; j < m; j += 256) {
-    const double u = U[j * p + r];
-    const double a = fabs(u);
-    if (a > best) { best = a; bj = j; }
-    if (qerr[j] != 0.0) {
-      const double u2 = u * u;
-      tr += ldexp(u2 * fmax(lam * (1.0 - 2.0 * u2) + u2 * G[j * ldg + j], 0.0), -2 * shift[j]);
+// Also the precision-bound sums (run_eig): t_r = sum_a d_a^2 v_ra^2 (lambda_r (1 - 2 v_ra^2) +
+// v_ra^2 G_aa) and sum_a d_a^2 (w_a (1 - 2 P_aa) + P_aa^2 G_aa), w_a = sum_r lambda_r v_ra^2,
+// P_aa = sum_r v_ra^2, over the columns with rounding errors (qerr != 0).
+// Three kernels: per-block partials (one thread per row j of U, coalesced row reads), one CTA
+// combining the partials in block order, and the sign-applied copy.
+constexpr int kFinThreads = 128;
+constexpr int kFinKMax = 96;
+__global__ void __launch_bounds__(kFinThreads) fin_part_kernel(const double* __restrict__ U,
+                                                              const double* __restrict__ theta, int64_t m, int p,
+                                                              int k, const int32_t* __restrict__ shift,
+                                                              const double* __restrict__ qerr,
+                                                              const double* __restrict__ G, int64_t ldg,
+                                                              double* __restrict__ part) {
+  constexpr int NW = kFinThreads / 32;
+  __shared__ double sv[NW][kFinKMax], st[NW][kFinKMax + 1];
+  __shared__ int64_t sj[NW][kFinKMax];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t j = (int64_t)blockIdx.x * kFinThreads + threadIdx.x;
+  const bool ok = j < m;
+  const bool err = ok && qerr[j] != 0.0;
+  const double gjj = err ? G[j * ldg + j] : 0.0;
+  const double d2 = err ? ldexp(1.0, -2 * shift[j]) : 0.0;
+  double Pjj = 0.0, wj = 0.0;
+  for (int r = 0; r < k; ++r) {
+    const double u = ok ? U[j * p + r] : 0.0;
+    const double lam = fmax(theta[r], 0.0);
+    const double u2 = u * u;
+    Pjj += u2;
+    wj = fma(lam, u2, wj);
+    double best = ok ? fabs(u) : -1.0;
+    int64_t bj = j;
+    double t = err ? d2 * u2 * fmax(lam * (1.0 - 2.0 * u2) + u2 * gjj, 0.0) : 0.0;
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xFFFFFFFFu, best, o);
+      const int64_t oj = __shfl_xor_sync(0xFFFFFFFFu, bj, o);
+      if (ob > best || (ob == best && oj < bj)) { best = ob; bj = oj; }
+      t += __shfl_xor_sync(0xFFFFFFFFu, t, o);
     }
+    if (lane == 0) { sv[warp][r] = best; sj[warp][r] = bj; st[warp][r] = t; }
   }
-  sv[threadIdx.x] = best;
-  sj[threadIdx.x] = bj;
-  st[threadIdx.x] = tr;
+  double e = err ? d2 * fmax(wj * (1.0 - 2.0 * Pjj) + Pjj * Pjj * gjj, 0.0) : 0.0;
+  for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xFFFFFFFFu, e, o);
+  if (lane == 0) st[warp][kFinKMax] = e;
   __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if ((int)threadIdx.x < o) st[threadIdx.x] += st[threadIdx.x + o];
-    __syncthreads();
+  double* out = part + (int64_t)blockIdx.x * (3 * k + 1);
+  for (int r = threadIdx.x; r <= k; r += kFinThreads) {
+    if (r == k) {
+      double tt = 0.0;
+      for (int w = 0; w < NW; ++w) tt += st[w][kFinKMax];
+      out[3 * k] = tt;
+      continue;
+    }
+    double b = sv[0][r], tt = st[0][r];
+    int64_t jj = sj[0][r];
+    for (int w = 1; w < NW; ++w) {
+      if (sv[w][r] > b || (sv[w][r] == b && sj[w][r] < jj)) { b = sv[w][r]; jj = sj[w][r]; }
+      tt += st[w][r];
+    }
+    out[r] = b;
+    out[k + r] = (double)jj;
+    out[2 * k + r] = tt;
   }
-  if (threadIdx.x == 0) {
-    prec[r] = st[0];
-    for (int t = 1; t < 256; ++t)
-      if (sv[t] > sv[0] || (sv[t] == sv[0] && sj[t] < sj[0])) { sv[0] = sv[t]; sj[0] = sj[t]; }
-  }
-  __syncthreads();
-  const double sg = U[sj[0] * p + r] < 0.0 ? -1.0 : 1.0;
-  for (int64_t j = threadIdx.x; j < m; j += 256) {
-    const double v = sg * U[j * p + r];
-    V[j * k + r] = v;
-    V32[j * k_pad + r] = (float)v;
-  }
-  if (threadIdx.x == 0) sigma[r] = sqrt(fmax(theta[r], 0.0));
 }
-
-// Bound of the spike-energy error (run_eig): var(d E_spike) <= sum_a d_a^2 (w_a (1 - 2 P_aa) +
-// P_aa^2 G_aa), w_a = sum_r lambda_r v_ra^2, P_aa = sum_r v_ra^2 -> prec[k]; one CTA, fixed order
-__global__ void __launch_bounds__(1024) prec_energy_kernel(const double* __restrict__ V, const double* __restrict__ theta,
-                                                           int64_t m, int k, const int32_t* __restrict__ shift,
-                                                           const double* __restrict__ qerr,
-                                                           const double* __restrict__ G, int64_t ldg,
-                                                           double* __restrict__ prec) {
-  __shared__ double sh[32];
-  double acc = 0.0;
-  for (int64_t j = threadIdx.x; j < m; j += 1024) {
-    if (qerr[j] == 0.0) continue;
-    double P = 0.0, w = 0.0;
-    for (int r = 0; r < k; ++r) {
-      const double v2 = V[j * k + r] * V[j * k + r];
-      P += v2;
-      w = fma(fmax(theta[r], 0.0), v2, w);
-    }
-    acc += ldexp(fmax(w * (1.0 - 2.0 * P) + P * P * G[j * ldg + j], 0.0), -2 * shift[j]);
-  }
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
+// one warp per r (block r < k) plus one for the energy bound (block k): lanes take the block
+// partials q = lane, lane + 32, ... (fixed order), then a fixed xor tree
+__global__ void __launch_bounds__(32) fin_final_kernel(const double* __restrict__ part, int nb, int k,
+                                                      const double* __restrict__ theta, const double* __restrict__ U,
+                                                      int p, double* __restrict__ sigma, double* __restrict__ sgn,
+                                                      double* __restrict__ prec) {
+  const int r = blockIdx.x, lane = threadIdx.x;
+  const int stride = 3 * k + 1;
+  if (r == k) {
     double t = 0.0;
-    for (int i = 0; i < 32; ++i) t += sh[i];
-    prec[k] = t;
+    for (int q = lane; q < nb; q += 32) t += part[(int64_t)q * stride + 3 * k];
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xFFFFFFFFu, t, o);
+    if (lane == 0) prec[k] = t;
+    return;
+  }
+  double b = -1.0, t = 0.0;
+  int64_t jj = INT64_MAX;
+  for (int q = lane; q < nb; q += 32) {
+    const double* pq = part + (int64_t)q * stride;
+    const double v = pq[r];
+    const int64_t vj = (int64_t)pq[k + r];
+    if (v > b || (v == b && vj < jj)) { b = v; jj = vj; }
+    t += pq[2 * k + r];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xFFFFFFFFu, b, o);
+    const int64_t oj = __shfl_xor_sync(0xFFFFFFFFu, jj, o);
+    if (ob > b || (ob == b && oj < jj)) { b = ob; jj = oj; }
+    t += __shfl_xor_sync(0xFFFFFFFFu, t, o);
+  }
+  if (lane == 0) {
+    sgn[r] = U[jj * p + r] < 0.0 ? -1.0 : 1.0;
+    sigma[r] = sqrt(fmax(theta[r], 0.0));
+    prec[r] = t;
+  }
+}
+__global__ void fin_write_kernel(const double* __restrict__ U, const double* __restrict__ sgn, int64_t m, int p, int k,
+                                 int k_pad, double* __restrict__ V, float* __restrict__ V32) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m * k_pad) return;
+  const int64_t j = t / k_pad;
+  const int r = (int)(t % k_pad);
+  if (r < k) {
+    const double v = sgn[r] * U[j * p + r];
+    V[j * k + r] = v;
+    V32[t] = (float)v;
+  } else {
+    V32[t] = 0.f;
   }
 }
 
@@ -936,29 +995,134 @@ __global__ void power_u_stats_kernel(const double* __restrict__ mu, int64_t m, c
   }
 }
 
-}  // namespace
+// ---------------------------------------------------------------- device-resident loop control
+// The subspace iteration runs as ONE CUDA graph: WHILE(loop) { begin; IF(rr) {RR check; ctl_rr};
+// IF(pow) {power step; orth; ctl_end} } — every decision the host used to take between launches
+// (when to run a Rayleigh-Ritz check, how many Jacobi sweeps it may take, convergence) is taken
+// here, on the device, from the same quantities and with the same rules.
+struct EigCtl {
+  int it;           // current iteration (1-based)
+  int next_rr;      // iteration of the next Rayleigh-Ritz check
+  int prev_it;      // iteration of the previous check
+  int rr_count;     // checks so far
+  int conv;         // 1: converged
+  int max_it;
+  int msw;          // Jacobi sweep cap of the current check (3 intermediate, 40 final)
+  int kfix;         // (must follow msw) leading block of the check's ordered basis, p if unordered
+  int last_sweeps;  // sweeps of the last check's Jacobi (atb_fused MODE 2 writes it)
+  int rr_now;       // this iteration ran a check (the power step starts from its Z = G U)
+  int blocks_u;     // uncentred power iteration: blocks of 4 steps
+  int iters_u;
+  int stop;         // the last check ended the loop
+  int stop_u;       // the uncentred loop is done
+  int k, p;
+  double tol, prev_res, pred_res, maxres;
+};
+static_assert(sizeof(EigCtl) <= kEigCtlBytes, "EigCtl too large");
+static_assert(offsetof(EigCtl, blocks_u) == 4 * kCtlBlocksU && offsetof(EigCtl, iters_u) == 4 * kCtlBlocksU + 4,
+              "report reads blocks_u / iters_u by index");
 
-avd_status launch_gram_finalize(Ctx* c) {
-  const int64_t m = c->cfg.m;
-  const double unit = (c->nd == 3) ? 16384.0 : 1.0;
-  dim3 grid((unsigned)(c->m_pad / 32), (unsigned)(c->m_pad / 32));
-  gram_finalize_kernel<<<grid, dim3(32, 8), 0, c->stream>>>(c->gram_i, m, c->m_pad, c->shift, c->qsum, c->ysq, c->mu,
-                                                            c->mu0, (double)c->cfg.l_global,
-                                                            1.0 / (double)c->cfg.l_global, unit, c->G, c->G32);
-  AVD_LAUNCHED(c);
-  trace_kernel<<<1, 1024, 0, c->stream>>>(c->G, m, c->m_pad, c->ysq, c->mu0, (double)c->cfg.l_global, c->stats,
-                                          c->trace, c->gmax);
-  AVD_LAUNCHED(c);
-  return AVD_OK;
+__global__ void ctl_init_kernel(EigCtl* ctl, int max_it, double tol, int k, int p) {
+  if (threadIdx.x != 0) return;
+  ctl->k = k;
+  ctl->p = p;
+  ctl->kfix = p;
+  ctl->it = 1;
+  ctl->next_rr = 2;
+  ctl->prev_it = 0;
+  ctl->rr_count = 0;
+  ctl->conv = 0;
+  ctl->max_it = max_it;
+  ctl->msw = 3;
+  ctl->last_sweeps = 0;
+  ctl->rr_now = 0;
+  ctl->stop = 0;
+  ctl->tol = tol;
+  ctl->prev_res = -1.0;
+  ctl->pred_res = -1.0;
+  ctl->maxres = 0.0;
+}
+// top of the loop body: does this iteration run a check?  (sets both IF handles every iteration)
+__global__ void ctl_begin_kernel(EigCtl* ctl, cudaGraphConditionalHandle h_rr, cudaGraphConditionalHandle h_pow) {
+  if (threadIdx.x != 0) return;
+  const int it = ctl->it;
+  const bool rr = it == ctl->next_rr || it == ctl->max_it;
+  // an intermediate check only needs an orthonormal basis of the subspace and honest residuals:
+  // its Jacobi is capped at 3 sweeps (the residuals of the rotated basis are still true
+  // residuals, so a capped solve can only delay convergence, never fake it); a check that could
+  // end the solve (predicted residual within 10x of tol, or the last iteration) runs to full
+  // convergence.
+  const bool final_ish = it == ctl->max_it || (ctl->pred_res >= 0.0 && ctl->pred_res <= 10.0 * ctl->tol);
+  ctl->msw = final_ish ? 40 : 3;
+  // after a check, the power steps keep Q's columns in Ritz order (CholQR of G^2 Z, Z = Y W sorted),
+  // so the tail-tail rotations can be skipped (jacobi_block)
+  ctl->kfix = ctl->rr_count > 0 ? ctl->k : ctl->p;
+  ctl->rr_now = rr ? 1 : 0;
+  if (h_rr) cudaGraphSetConditional(h_rr, rr ? 1u : 0u);  // 0 handles: host-driven profiling mode
+  if (h_pow) cudaGraphSetConditional(h_pow, 1u);
+}
+// after a check: convergence, else the next check predicted from the observed residual decay
+// per G^2 step (or (theta_p / theta_k)^2 before two checks exist), at most 8 steps ahead
+__global__ void ctl_rr_kernel(EigCtl* ctl, const double* __restrict__ theta, const double* __restrict__ resid, int p,
+                              int k, int* __restrict__ jstats, cudaGraphConditionalHandle h_loop,
+                              cudaGraphConditionalHandle h_pow) {
+  if (threadIdx.x != 0) return;
+  const int it = ctl->it;
+  const int rc = ctl->rr_count++;
+  jstats[rc < 15 ? rc : 15] = ctl->last_sweeps;
+  double maxres = 0.0;
+  for (int r = 0; r < k; ++r) maxres = fmax(maxres, resid[r]);
+  bool stop = false;
+  if (!(theta[0] > 0.0)) { maxres = 0.0; ctl->conv = 1; stop = true; }  // G == 0: nothing to iterate
+  else if (maxres <= ctl->tol) { ctl->conv = 1; stop = true; }
+  else if (it == ctl->max_it) { stop = true; }
+  ctl->maxres = maxres;
+  if (!stop) {
+    double rate = -1.0;
+    if (ctl->prev_res > 0.0 && maxres < ctl->prev_res) rate = pow(maxres / ctl->prev_res, 1.0 / (double)(it - ctl->prev_it));
+    else if (theta[k - 1] > 0.0) rate = pow(fmax(theta[p - 1], 0.0) / theta[k - 1], 2.0);
+    int step = 1;
+    if (rate > 0.0 && rate < 0.95) {
+      const double need = log(ctl->tol / maxres) / log(rate);
+      step = (int)fmax(1.0, fmin(8.0, ceil(need)));
+    }
+    ctl->prev_res = maxres;
+    ctl->prev_it = it;
+    ctl->next_rr = it + step;
+    ctl->pred_res = (rate > 0.0 && rate < 0.95) ? maxres * pow(rate, (double)step) : -1.0;
+  }
+  ctl->stop = stop ? 1 : 0;
+  if (stop && h_loop) cudaGraphSetConditional(h_loop, 0u);
+  if (h_pow) cudaGraphSetConditional(h_pow, stop ? 0u : 1u);
+}
+__global__ void ctl_end_kernel(EigCtl* ctl) {
+  if (threadIdx.x == 0) ctl->it += 1;
+}
+// uncentred power iteration: stop after the residual reaches 1e-8 (or mu = 0), at most 16 blocks
+__global__ void ctl_u_init_kernel(EigCtl* ctl) {
+  if (threadIdx.x == 0) { ctl->blocks_u = 0; ctl->iters_u = 0; ctl->stop_u = 0; }
+}
+__global__ void ctl_u_kernel(EigCtl* ctl, const double* __restrict__ diag, cudaGraphConditionalHandle h_u) {
+  if (threadIdx.x != 0) return;
+  ctl->blocks_u += 1;
+  ctl->iters_u += 4;
+  if (!(diag[0] > 0.0) || diag[2] <= 1e-8 || ctl->blocks_u >= 16) {
+    ctl->stop_u = 1;
+    if (h_u) cudaGraphSetConditional(h_u, 0u);
+  }
 }
 
-// split-K geometry shared by the plan (workspace) and the launches
+}  // namespace
+
+// split-K geometry shared by the plan (workspace) and the launches: as many K slices as fill
+// ONE wave of resident CTAs (3 fp32 / 2 fp64 CTAs per SM, smem-bound) — a partial second wave
+// would double the kernel's time
 void gemm_geometry(int64_t m, int64_t m_pad, int p, int num_sms, bool fp32, int* BM, int* KS, int* RB, int* KT) {
   *BM = (fp32 && p <= 64) ? 128 : 64;  // = 16 * NR of the gemm32 / gemm64 instantiations
   *RB = (int)(m_pad / *BM);
   *KT = (int)ceil_div(m, kSkBK);
   const int64_t want = (int64_t)num_sms * (fp32 ? 3 : 2);  // resident CTAs (smem-bound)
-  *KS = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(want, *RB), *KT));
+  *KS = (int)std::max<int64_t>(1, std::min<int64_t>(want / *RB, *KT));
 }
 size_t gemm_part_bytes(int64_t m, int64_t m_pad, int p, int num_sms) {
   size_t best = 0;
@@ -974,7 +1138,7 @@ namespace {
 
 // Y = G In (fp64 G, fp64 math) or Y = G32 In32 (fp32); Y fp64 (+ optional fp32 mirror)
 template <typename T, int NR, int NC>
-avd_status gemm_launch(Ctx* c, const T* Gm, const T* In, double* Y, float* Y32) {
+avd_status gemm_launch(Ctx* c, const T* Gm, const T* In, double* Y, float* Y32, const int* skip) {
   int BM, KS, RB, KT;
   const int p = 8 * NC;
   gemm_geometry(c->cfg.m, c->m_pad, p, c->num_sms, sizeof(T) == 4, &BM, &KS, &RB, &KT);
@@ -986,23 +1150,23 @@ avd_status gemm_launch(Ctx* c, const T* Gm, const T* In, double* Y, float* Y32) 
   unsigned* tickets = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(c->gemm_part) + pb -
                                                   sizeof(unsigned) * (size_t)(c->m_pad / 64 + 1));
   gemm_kernel<T, NR, NC><<<RB * KS, kSkThreads, sm, c->stream>>>(Gm, c->m_pad, In, c->cfg.m, KT, KS, part, tickets, Y,
-                                                                 Y32);
+                                                                 Y32, skip);
   AVD_LAUNCHED(c);
   return AVD_OK;
 }
 
 avd_status gemm64(Ctx* c, const double* In, double* Y, float* Y32) {
   switch (c->p / 16) {
-#define CASE(PC) case PC: return gemm_launch<double, 4, 2 * PC>(c, c->G, In, Y, Y32);
+#define CASE(PC) case PC: return gemm_launch<double, 4, 2 * PC>(c, c->G, In, Y, Y32, nullptr);
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
   }
   set_error("unsupported p");
   return AVD_EINVAL;
 }
-avd_status gemm32(Ctx* c, const float* In, double* Y, float* Y32) {
+avd_status gemm32(Ctx* c, const float* In, double* Y, float* Y32, const int* skip = nullptr) {
   switch (c->p / 16) {
-#define CASE(PC) case PC: return gemm_launch<float, (PC <= 4 ? 8 : 4), 2 * PC>(c, c->G32, In, Y, Y32);
+#define CASE(PC) case PC: return gemm_launch<float, (PC <= 4 ? 8 : 4), 2 * PC>(c, c->G32, In, Y, Y32, skip);
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
   }
@@ -1012,7 +1176,7 @@ avd_status gemm32(Ctx* c, const float* In, double* Y, float* Y32) {
 
 template <int MODE>
 avd_status atb_fused(Ctx* c, const double* A, const double* B, double* out0, double* out1, int* ibad, int* stats,
-                     const int* gate = nullptr, int max_sweeps = 40) {
+                     const int* gate = nullptr, int max_sweeps = 40, const int* msw = nullptr) {
   const int p = c->p;
   const int n_red = (int)ceil_div(c->cfg.m, kRedRows);
   const int chunk = p <= 48 ? kRedRows : 64;
@@ -1022,7 +1186,7 @@ avd_status atb_fused(Ctx* c, const double* A, const double* B, double* out0, dou
   case PC:                                                                                                      \
     AVD_CUDA(smem_attr(atb_fused_kernel<MODE, PC>, (int)sm)); \
     atb_fused_kernel<MODE, PC><<<n_red, RedCfg<PC>::threads, sm, c->stream>>>(A, B, c->cfg.m, c->red_part, c->ticket, out0, out1,  \
-                                                              ibad, stats, gate, max_sweeps);                   \
+                                                              ibad, stats, gate, max_sweeps, msw);              \
     break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
@@ -1062,8 +1226,8 @@ avd_status trsm(Ctx* c, const double* Y, const double* R, const double* dinv, co
 // Q <- orth(Y) by Cholesky-QR (Q32 mirrors Q).  The second pass (CholQR2) runs only when the
 // first one flagged it (a rank-deficient column, re-drawn at random in between, or
 // cond(R)^2 > 1e6, where one pass leaves orthogonality errors above ~1e-10); otherwise its two
-// kernels exit at once.
-avd_status orth(Ctx* c, const double* Y, uint32_t seed) {
+// kernels exit at once.  itp: device iteration counter mixed into the re-draw seed.
+avd_status orth(Ctx* c, const double* Y, uint32_t seed, const int* itp) {
   int* bad = reinterpret_cast<int*>(c->resid + c->p);
   int* need2 = bad + c->p;
   const int p = c->p;
@@ -1073,14 +1237,190 @@ avd_status orth(Ctx* c, const double* Y, uint32_t seed) {
     AVD_TRY(atb_fused<1>(c, src, src, c->W, c->H, bad, pass == 0 ? need2 : nullptr, gate));  // R -> W, 1/R_jj -> H
     AVD_TRY(trsm(c, src, c->W, c->H, bad, gate));                   // in place allowed (row-wise)
     if (pass == 0) {
-      rand_fill_kernel<<<(unsigned)ceil_div(c->cfg.m * p, 256), 256, 0, c->stream>>>(c->Q, c->Q32, c->cfg.m, p, seed, bad);
+      rand_fill_kernel<<<(unsigned)ceil_div(c->cfg.m * p, 256), 256, 0, c->stream>>>(c->Q, c->Q32, c->cfg.m, p, seed,
+                                                                                     bad, itp);
       AVD_LAUNCHED(c);
     }
   }
   return AVD_OK;
 }
 
+uint32_t eig_seed(const Ctx* c) { return (uint32_t)(c->cfg.seed ^ (c->cfg.seed >> 32)) * 2654435761u + 12345u; }
+
+// Capture the launches `fn` makes on c->stream into `g` (an empty conditional body graph); the
+// host-side launch counter is restored (graph kernels are counted per executed iteration) and the
+// number of kernels captured is returned in *nodes.
+template <typename F>
+avd_status capture_into(Ctx* c, cudaGraph_t g, int* nodes, F&& fn) {
+  cudaStream_t user = c->stream;
+  c->stream = c->cap_stream;
+  const int64_t l0 = c->launches;
+  avd_status st = AVD_OK;
+  cudaError_t e = cudaStreamBeginCaptureToGraph(c->cap_stream, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
+  if (e == cudaSuccess) {
+    st = fn();
+    cudaGraph_t out = g;
+    const cudaError_t e2 = cudaStreamEndCapture(c->cap_stream, &out);
+    if (st == AVD_OK && e2 != cudaSuccess) e = e2;
+  }
+  c->stream = user;
+  *nodes = (int)(c->launches - l0);
+  c->launches = l0;
+  if (st != AVD_OK) return st;
+  if (e != cudaSuccess) {
+    set_error(std::string("graph capture failed: ") + cudaGetErrorString(e));
+    return AVD_ECUDA;
+  }
+  return AVD_OK;
+}
+
+avd_status add_cond(cudaGraph_t g, const cudaGraphNode_t* deps, size_t ndeps, cudaGraphConditionalHandle h,
+                    cudaGraphConditionalNodeType type, cudaGraphNode_t* node, cudaGraph_t* body) {
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h;
+  np.conditional.type = type;
+  np.conditional.size = 1;
+  AVD_CUDA(cudaGraphAddNode(node, g, deps, ndeps, &np));
+  *body = np.conditional.phGraph_out[0];
+  return AVD_OK;
+}
+
+// Loop bodies (graph bodies, or launched one by one by the host-driven profiling mode)
+avd_status enqueue_rr(Ctx* c, cudaGraphConditionalHandle h_loop, cudaGraphConditionalHandle h_pow) {
+  const int64_t m = c->cfg.m;
+  const int p = c->p, k = c->k;
+  EigCtl* ctl = reinterpret_cast<EigCtl*>(c->eig_ctl);
+  int* jstats = reinterpret_cast<int*>(c->theta + p);
+  AVD_TRY(gemm64(c, c->Q, c->Y, nullptr));  // Y = G Q (exact G, fp64)
+  AVD_TRY(atb_fused<2>(c, c->Q, c->Y, c->W, c->theta, nullptr, &ctl->last_sweeps, nullptr, 40, &ctl->msw));
+  AVD_TRY(matpp(c, c->Y, c->Z, c->Z32, c->Q, c->U, nullptr, c->W));  // Z = Y W, U = Q W (Ritz vectors)
+  resid_kernel<<<k, 256, 0, c->stream>>>(c->Z, c->U, c->theta, m, p, c->resid);
+  AVD_LAUNCHED(c);
+  ctl_rr_kernel<<<1, 32, 0, c->stream>>>(ctl, c->theta, c->resid, p, k, jstats, h_loop, h_pow);
+  AVD_LAUNCHED(c);
+  return AVD_OK;
+}
+avd_status enqueue_pow(Ctx* c) {
+  EigCtl* ctl = reinterpret_cast<EigCtl*>(c->eig_ctl);
+  AVD_TRY(gemm32(c, c->Q32, c->Z, c->Z32, &ctl->rr_now));  // Z = G Q (a check already made Z = G U)
+  AVD_TRY(gemm32(c, c->Z32, c->Y, nullptr));                // Y = G Z = G^2 Q
+  AVD_TRY(orth(c, c->Y, eig_seed(c), &ctl->it));
+  ctl_end_kernel<<<1, 32, 0, c->stream>>>(ctl);
+  AVD_LAUNCHED(c);
+  return AVD_OK;
+}
+avd_status enqueue_unc(Ctx* c, cudaGraphConditionalHandle h_u) {
+  const int64_t m = c->cfg.m;
+  EigCtl* ctl = reinterpret_cast<EigCtl*>(c->eig_ctl);
+  double* q = c->diag + 4;
+  double* y = q + c->m_pad;
+  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(m, 8), 4LL * c->num_sms);
+  const double lg = (double)c->cfg.l_global;
+  for (int t = 0; t < 4; ++t) {
+    power_u_kernel<<<grid, 256, 0, c->stream>>>(c->G32, c->m_pad, c->mu, m, lg, (t & 1) ? y : q, (t & 1) ? q : y);
+    AVD_LAUNCHED(c);
+  }
+  power_u_kernel<<<grid, 256, 0, c->stream>>>(c->G32, c->m_pad, c->mu, m, lg, q, y);
+  AVD_LAUNCHED(c);
+  power_u_stats_kernel<<<1, 256, 0, c->stream>>>(c->mu, m, q, y, c->diag);
+  AVD_LAUNCHED(c);
+  ctl_u_kernel<<<1, 32, 0, c->stream>>>(ctl, c->diag, h_u);
+  AVD_LAUNCHED(c);
+  return AVD_OK;
+}
+
+// The eigensolver loop as one graph (built once per context; every pointer it uses is fixed):
+//   WHILE(loop) { ctl_begin; IF(rr) { Y = G Q (fp64); Jacobi RR; Z = Y W, U = Q W; residuals;
+//                 ctl_rr }; IF(pow) { Z = G32 Q32 (skipped after a check); Y = G32 Z32;
+//                 Q = orth(Y); ctl_end } }
+avd_status build_eig_graph(Ctx* c) {
+  EigCtl* ctl = reinterpret_cast<EigCtl*>(c->eig_ctl);
+  cudaGraph_t g;
+  AVD_CUDA(cudaGraphCreate(&g, 0));
+  avd_status st = [&]() -> avd_status {
+    cudaGraphConditionalHandle h_loop;
+    AVD_CUDA(cudaGraphConditionalHandleCreate(&h_loop, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNode_t wnode;
+    cudaGraph_t body;
+    AVD_TRY(add_cond(g, nullptr, 0, h_loop, cudaGraphCondTypeWhile, &wnode, &body));
+    cudaGraphConditionalHandle h_rr, h_pow;
+    AVD_CUDA(cudaGraphConditionalHandleCreate(&h_rr, body, 0, 0));
+    AVD_CUDA(cudaGraphConditionalHandleCreate(&h_pow, body, 0, 0));
+    int nb = 0;
+    AVD_TRY(capture_into(c, body, &nb, [&]() -> avd_status {
+      ctl_begin_kernel<<<1, 32, 0, c->stream>>>(ctl, h_rr, h_pow);
+      AVD_LAUNCHED(c);
+      return AVD_OK;
+    }));
+    cudaGraphNode_t begin_node;
+    size_t n1 = 1;
+    AVD_CUDA(cudaGraphGetNodes(body, &begin_node, &n1));
+    cudaGraphNode_t rr_node, pow_node;
+    cudaGraph_t rr_body, pow_body;
+    AVD_TRY(add_cond(body, &begin_node, 1, h_rr, cudaGraphCondTypeIf, &rr_node, &rr_body));
+    AVD_TRY(add_cond(body, &rr_node, 1, h_pow, cudaGraphCondTypeIf, &pow_node, &pow_body));
+    AVD_TRY(capture_into(c, rr_body, &c->n_rr_nodes, [&]() { return enqueue_rr(c, h_loop, h_pow); }));
+    AVD_TRY(capture_into(c, pow_body, &c->n_pow_nodes, [&]() { return enqueue_pow(c); }));
+    c->n_begin_nodes = nb;
+    AVD_CUDA(cudaGraphInstantiate(&c->eig_exec, g, 0));
+    return AVD_OK;
+  }();
+  cudaGraphDestroy(g);
+  return st;
+}
+
+// Uncentred power iteration (mean-bias diagnostics) as one graph on the side stream:
+//   WHILE(u) { 4 power steps (q -> y -> q -> y -> q); y = Gu q; stats(q, y); ctl_u }
+avd_status build_unc_graph(Ctx* c) {
+  cudaGraph_t g;
+  AVD_CUDA(cudaGraphCreate(&g, 0));
+  avd_status st = [&]() -> avd_status {
+    cudaGraphConditionalHandle h_u;
+    AVD_CUDA(cudaGraphConditionalHandleCreate(&h_u, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNode_t wnode;
+    cudaGraph_t body;
+    AVD_TRY(add_cond(g, nullptr, 0, h_u, cudaGraphCondTypeWhile, &wnode, &body));
+    AVD_TRY(capture_into(c, body, &c->n_u_nodes, [&]() { return enqueue_unc(c, h_u); }));
+    AVD_CUDA(cudaGraphInstantiate(&c->unc_exec, g, 0));
+    return AVD_OK;
+  }();
+  cudaGraphDestroy(g);
+  return st;
+}
+
+// AVD_EIG_NOGRAPH=1: the same loop bodies launched one by one by the host with a synchronisation
+// per decision (profiling: ncu sees every kernel; numerically identical)
+bool eig_nograph() {
+  static const bool v = [] { const char* e = std::getenv("AVD_EIG_NOGRAPH"); return e && e[0] == '1'; }();
+  return v;
+}
+
+avd_status ensure_graphs(Ctx* c) {
+  if (!c->side_stream) AVD_CUDA(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
+  if (c->eig_exec || eig_nograph()) return AVD_OK;
+  if (!c->cap_stream) AVD_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  if (!c->ev_fork) AVD_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  if (!c->ev_join) AVD_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  AVD_TRY(build_unc_graph(c));
+  return build_eig_graph(c);
+}
+
 }  // namespace
+
+avd_status launch_gram_finalize(Ctx* c) {
+  const int64_t m = c->cfg.m;
+  const double unit = (c->nd == 3) ? 16384.0 : 1.0;
+  dim3 grid((unsigned)(c->m_pad / 32), (unsigned)(c->m_pad / 32));
+  gram_finalize_kernel<<<grid, dim3(32, 8), 0, c->stream>>>(c->gram_i, m, c->m_pad, c->shift, c->qsum, c->ysq, c->mu,
+                                                            c->mu0, (double)c->cfg.l_global,
+                                                            1.0 / (double)c->cfg.l_global, unit, c->G, c->G32);
+  AVD_LAUNCHED(c);
+  trace_kernel<<<1, 1024, 0, c->stream>>>(c->G, m, c->m_pad, c->ysq, c->mu0, (double)c->cfg.l_global, c->stats,
+                                          c->trace, c->gmax);
+  AVD_LAUNCHED(c);
+  return AVD_OK;
+}
 
 // A-posteriori bound of the Gram operand's quantisation error (DESIGN.md §8 "Gram precision").
 // The operand is q_ia = y_ia + e_ia, y = (x - mu0) 2^shift, with dithered rounding errors e that
@@ -1089,9 +1429,9 @@ avd_status orth(Ctx* c, const double* Y, uint32_t seed) {
 // the off-diagonal is E_ab = d_a d_b sum_i (e_ia xc_ib + xc_ia e_ib) + O(e^2) (d_a = 2^-shift_a),
 // so to first order, with X~ v_r = sigma_r u_r and X~^T u_r = sigma_r v_r,
 //   d lambda_r = v_r^T E v_r = 2 sum_ia d_a v_ra e_ia (sigma_r u_ri - v_ra xc_ia),
-//   var <= t_r = sum_a d_a^2 v_ra^2 (lambda_r (1 - 2 v_ra^2) + v_ra^2 G_aa)      (finalize kernel)
+//   var <= t_r = sum_a d_a^2 v_ra^2 (lambda_r (1 - 2 v_ra^2) + v_ra^2 G_aa)      (fin kernels)
 //   d E_spike = sum_r d lambda_r = 2 sum_ia d_a e_ia (S_ia - P_aa xc_ia),  P = V_k V_k^T,
-//   var <= sum_a d_a^2 (w_a (1 - 2 P_aa) + P_aa^2 G_aa),  w_a = sum_r lambda_r v_ra^2 (prec kernel)
+//   var <= sum_a d_a^2 (w_a (1 - 2 P_aa) + P_aa^2 G_aa),  w_a = sum_r lambda_r v_ra^2 (fin kernels)
 // (S the spike matrix).  A column carried by one massive entry (v_r ~ e_a) drops out, as it
 // should: its diagonal is exact.  E_tail = tr(G) - E_spike inherits d E_spike (tr(G) is exact up
 // to the fp32 rounding of y, counted as 1e-9 tr(G)).  At 5 sigma:
@@ -1099,15 +1439,12 @@ avd_status orth(Ctx* c, const double* Y, uint32_t seed) {
 //   prec_share = max(5 std(d E_spike) / E_spike, (5 std(d E_spike) + 1e-9 tr(G)) / E_tail)
 // The automatic digit rule raises the operand to 3 digits when prec_sigma > 5e-5 or
 // prec_share > 5e-6 (half the north-star tolerances 1e-4 / 1e-5).
-avd_status precision_bound(Ctx* c) {
+// h: the pinned copy of [theta (p) | t_r (k) | var(d E_spike) | tr(G)].
+static void precision_bound(Ctx* c, const double* theta, const double* h) {
   const int k = c->k;
-  double* h = c->eig_host + 2 * kMaxP;  // pinned scratch: t_r [k <= 95], var(d E_spike), tr(G)
-  AVD_CUDA(cudaMemcpyAsync(h, c->prec, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, c->stream));
-  AVD_CUDA(cudaMemcpyAsync(h + k + 1, c->trace, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  AVD_CUDA(cudaStreamSynchronize(c->stream));
   double ps = 0.0, e_spike = 0.0;
   for (int r = 0; r < k; ++r) {
-    const double lam = std::max(c->eig_host[r], 0.0);  // Ritz values of the last check (theta)
+    const double lam = std::max(theta[r], 0.0);
     const double t = std::max(h[r], 0.0);
     if (lam > 0.0) ps = std::max(ps, 2.5 * std::sqrt(t) / lam);
     e_spike += lam;
@@ -1121,16 +1458,21 @@ avd_status precision_bound(Ctx* c) {
   else if (sd_spike > 0.0) pe = HUGE_VAL;
   c->prec_sigma = ps;
   c->prec_share = pe;
-  return AVD_OK;
 }
 
-// Subspace iteration: power steps Q <- orth(G^2 Q) in fp32; a Rayleigh-Ritz check (fp64) runs
-// on a schedule predicted from the observed residual decay (at most every 8 steps, always on the
-// last one), so the p x p Jacobi runs ~2-3 times per solve.
+// Subspace iteration (device-resident): power steps Q <- orth(G^2 Q) in fp32; a Rayleigh-Ritz
+// check (fp64) runs on a schedule predicted from the observed residual decay (at most every 8
+// steps, always on the last one), so the p x p Jacobi runs ~2 times per solve.  The whole loop is
+// one graph launch (build_eig_graph); the host synchronises once, after the final vectors and the
+// precision bound, and meanwhile the uncentred power iteration runs on the side stream.
 avd_status run_eig(Ctx* c) {
   const int64_t m = c->cfg.m;
   const int p = c->p, k = c->k;
-  const uint32_t seed = (uint32_t)(c->cfg.seed ^ (c->cfg.seed >> 32)) * 2654435761u + 12345u;
+  AVD_TRY(ensure_graphs(c));
+  EigCtl* ctl = reinterpret_cast<EigCtl*>(c->eig_ctl);
+  const uint32_t seed = eig_seed(c);
+  const int max_it = std::max(2, c->cfg.max_iters > 0 ? c->cfg.max_iters : 200);
+  const double tol = c->cfg.eig_tol > 0 ? c->cfg.eig_tol : 1e-6;  // V angle <~ tol * lambda_1 / gap_k
   int* jstats = reinterpret_cast<int*>(c->theta + p);  // [16] sweeps per RR solve
   AVD_CUDA(cudaMemsetAsync(jstats, 0, 16 * sizeof(int), c->stream));
   AVD_CUDA(cudaMemsetAsync(c->ticket, 0, sizeof(unsigned), c->stream));
@@ -1138,106 +1480,112 @@ avd_status run_eig(Ctx* c) {
     const size_t pb = gemm_part_bytes(m, c->m_pad, p, c->num_sms), tb = sizeof(unsigned) * (size_t)(c->m_pad / 64 + 1);
     AVD_CUDA(cudaMemsetAsync(reinterpret_cast<char*>(c->gemm_part) + pb - tb, 0, tb, c->stream));
   }
-  rand_fill_kernel<<<(unsigned)ceil_div(m * p, 256), 256, 0, c->stream>>>(c->Z, nullptr, m, p, seed, nullptr);
+  ctl_init_kernel<<<1, 32, 0, c->stream>>>(ctl, max_it, tol, k, p);
   AVD_LAUNCHED(c);
-  AVD_TRY(orth(c, c->Z, seed + 1));
-  const int max_it = c->cfg.max_iters > 0 ? c->cfg.max_iters : 200;
-  const double tol = c->cfg.eig_tol > 0 ? c->cfg.eig_tol : 1e-6;  // V angle <~ tol * lambda_1 / gap_k
-  int it = 0, next_rr = 2, prev_it = 0, rr_count = 0;
-  double maxres = 0.0, prev_res = -1.0, pred_res = -1.0;
-  bool conv = false;
-  for (it = 1; it <= max_it; ++it) {
-    if (it == next_rr || it == max_it) {
-      ++rr_count;
-      AVD_TRY(gemm64(c, c->Q, c->Y, nullptr));           // Y = G Q (exact G, fp64)
-      // an intermediate check only needs an orthonormal basis of the subspace and honest
-      // residuals: its Jacobi is capped at 3 sweeps (the residuals of the rotated basis are still
-      // true residuals, so a capped solve can only delay convergence, never fake it); a check
-      // that could end the solve (predicted residual within 10x of tol, or the last iteration)
-      // runs to full convergence.
-      const bool final_ish = it == max_it || (pred_res >= 0.0 && pred_res <= 10.0 * tol);
-      AVD_TRY(atb_fused<2>(c, c->Q, c->Y, c->W, c->theta, nullptr, jstats + std::min(rr_count - 1, 15), nullptr,
-                           final_ish ? 40 : 3));
-      AVD_TRY(matpp(c, c->Y, c->Z, c->Z32, c->Q, c->U, nullptr, c->W));  // Z = Y W, U = Q W (Ritz vectors)
-      resid_kernel<<<k, 256, 0, c->stream>>>(c->Z, c->U, c->theta, m, p, c->resid);
+  rand_fill_kernel<<<(unsigned)ceil_div(m * p, 256), 256, 0, c->stream>>>(c->Z, nullptr, m, p, seed, nullptr, nullptr);
+  AVD_LAUNCHED(c);
+  AVD_TRY(orth(c, c->Z, seed + 1, nullptr));
+  EigCtl* hc = reinterpret_cast<EigCtl*>(c->eig_host + 6 * kMaxP);
+  static_assert(6 * kMaxP + kEigCtlBytes / 8 <= kHostScratch, "pinned scratch too small");
+  const bool nograph = eig_nograph();
+  if (nograph) {
+    for (;;) {
+      ctl_begin_kernel<<<1, 32, 0, c->stream>>>(ctl, 0, 0);
       AVD_LAUNCHED(c);
-      AVD_CUDA(cudaMemcpyAsync(c->eig_host, c->theta, sizeof(double) * p, cudaMemcpyDeviceToHost, c->stream));
-      AVD_CUDA(cudaMemcpyAsync(c->eig_host + p, c->resid, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
+      AVD_CUDA(cudaMemcpyAsync(hc, ctl, sizeof(EigCtl), cudaMemcpyDeviceToHost, c->stream));
       AVD_CUDA(cudaStreamSynchronize(c->stream));
-      maxres = 0.0;
-      for (int r = 0; r < k; ++r) maxres = std::max(maxres, c->eig_host[p + r]);
-      if (!(c->eig_host[0] > 0.0)) { maxres = 0.0; conv = true; break; }  // G == 0: nothing to iterate
-      if (maxres <= tol) { conv = true; break; }
-      if (it == max_it) break;
-      // predicted residual decay per G^2 step: observed, else (theta_p / theta_k)^2
-      double rate = -1.0;
-      if (prev_res > 0.0 && maxres < prev_res) rate = std::pow(maxres / prev_res, 1.0 / (double)(it - prev_it));
-      else if (c->eig_host[k - 1] > 0.0) rate = std::pow(std::max(c->eig_host[p - 1], 0.0) / c->eig_host[k - 1], 2.0);
-      int step = 1;
-      if (rate > 0.0 && rate < 0.95) {
-        const double need = std::log(tol / maxres) / std::log(rate);
-        step = (int)std::max(1.0, std::min(8.0, std::ceil(need)));
+      if (hc->rr_now) {
+        AVD_TRY(enqueue_rr(c, 0, 0));
+        AVD_CUDA(cudaMemcpyAsync(hc, ctl, sizeof(EigCtl), cudaMemcpyDeviceToHost, c->stream));
+        AVD_CUDA(cudaStreamSynchronize(c->stream));
+        if (hc->stop) break;
       }
-      prev_res = maxres;
-      prev_it = it;
-      next_rr = it + step;
-      pred_res = (rate > 0.0 && rate < 0.95) ? maxres * std::pow(rate, (double)step) : -1.0;
-      AVD_TRY(gemm32(c, c->Z32, c->Y, nullptr));        // Y = G Z = G^2 U
-    } else {
-      AVD_TRY(gemm32(c, c->Q32, c->Z, c->Z32));         // Z = G Q
-      AVD_TRY(gemm32(c, c->Z32, c->Y, nullptr));        // Y = G Z = G^2 Q
+      AVD_TRY(enqueue_pow(c));
     }
-    AVD_TRY(orth(c, c->Y, seed + 7919u * (uint32_t)it));
+  } else {
+    AVD_CUDA(cudaGraphLaunch(c->eig_exec, c->stream));
   }
+  // final vectors, sigma, the precision-bound sums
+  const int nb = (int)ceil_div(m, kFinThreads);
+  fin_part_kernel<<<nb, kFinThreads, 0, c->stream>>>(c->U, c->theta, m, p, k, c->shift, c->qerr, c->G, c->m_pad,
+                                                      c->red_part);
+  AVD_LAUNCHED(c);
+  fin_final_kernel<<<k + 1, 32, 0, c->stream>>>(c->red_part, nb, k, c->theta, c->U, p, c->sigma, c->H, c->prec);
+  AVD_LAUNCHED(c);
+  fin_write_kernel<<<(unsigned)ceil_div(m * c->k_pad, 256), 256, 0, c->stream>>>(c->U, c->H, m, p, k, c->k_pad, c->V,
+                                                                                 c->V32);
+  AVD_LAUNCHED(c);
+  // one pinned copy: theta [p] | t_r [k], var(d E_spike) | tr(G) | ctl
+  double* h = c->eig_host + 4 * kMaxP;
+  AVD_CUDA(cudaMemcpyAsync(h, c->theta, sizeof(double) * p, cudaMemcpyDeviceToHost, c->stream));
+  AVD_CUDA(cudaMemcpyAsync(h + p, c->prec, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, c->stream));
+  AVD_CUDA(cudaMemcpyAsync(h + p + k + 1, c->trace, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  AVD_CUDA(cudaMemcpyAsync(hc, ctl, sizeof(EigCtl), cudaMemcpyDeviceToHost, c->stream));
+  AVD_CUDA(cudaStreamSynchronize(c->stream));
+  const int it = hc->it, rr = hc->rr_count;
+  if (!nograph)
+    c->launches += (int64_t)c->n_begin_nodes * it + (int64_t)c->n_rr_nodes * rr + (int64_t)c->n_pow_nodes * (it - 1);
   c->iters = std::min(it, max_it);
-  c->rr_count = rr_count;
-  c->max_resid = maxres;
-  c->sigma_next = (k < p) ? std::sqrt(std::max(c->eig_host[k], 0.0)) : 0.0;
-  // the per-solve sweep counts stay at theta + p; the report stage reads them with its packed copy
-  AVD_CUDA(cudaMemsetAsync(c->V32, 0, sizeof(float) * m * c->k_pad, c->stream));
-  finalize_vectors_kernel<<<k, 256, 0, c->stream>>>(c->U, c->theta, m, p, k, c->k_pad, c->shift, c->qerr, c->G,
-                                                    c->m_pad, c->V, c->sigma, c->V32, c->prec);
-  AVD_LAUNCHED(c);
-  prec_energy_kernel<<<1, 1024, 0, c->stream>>>(c->V, c->theta, m, k, c->shift, c->qerr, c->G, c->m_pad, c->prec);
-  AVD_LAUNCHED(c);
-  AVD_TRY(precision_bound(c));
-  return conv ? AVD_OK : AVD_ENOCONV;
+  c->rr_count = rr;
+  c->max_resid = hc->maxres;
+  c->sigma_next = (k < p) ? std::sqrt(std::max(h[k], 0.0)) : 0.0;
+  for (int r = 0; r < p; ++r) c->eig_host[r] = h[r];  // Ritz values of the last check
+  precision_bound(c, h, h + p);
+  return hc->conv ? AVD_OK : AVD_ENOCONV;
 }
 
 // Mean-bias diagnostics on the replicated G and mu (no exchange): power iteration on the uncentred
 // Gram from q_0 = mu_hat (already aligned when the mean dominates), in blocks of
-// 4 steps until the residual is <= 1e-8 (at most 64 steps).  Fills c->sigma1_u = sqrt(lambda_1),
-// c->alpha1 = |mu . v_1| (= (sigma_1 / l) u_1^T 1), c->cos_mu_v1 = alpha1 / ||mu||.
-avd_status run_uncentred(Ctx* c) {
-  const int64_t m = c->cfg.m;
-  mu_norm_kernel<<<1, 256, 0, c->stream>>>(c->mu, m, c->m_pad, c->diag);
-  AVD_LAUNCHED(c);
-  double* q = c->diag + 4;
-  double* y = q + c->m_pad;
-  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(m, 8), 4LL * c->num_sms);
-  double* h = c->eig_host + 3 * kMaxP;  // pinned scratch, 4 doubles
-  for (int t = 0; t < 4; ++t) h[t] = 0.0;
-  int it = 0;
-  for (int blk = 0; blk < 16; ++blk) {
-    for (int t = 0; t < 4; ++t, ++it) {
-      power_u_kernel<<<grid, 256, 0, c->stream>>>(c->G32, c->m_pad, c->mu, m, (double)c->cfg.l_global, q, y);
-      AVD_LAUNCHED(c);
-      std::swap(q, y);  // q now holds the unnormalised product
+// 4 steps until the residual is <= 1e-8 (at most 64 steps), as one graph on the side stream,
+// concurrent with the subspace iteration (both only read G32 and mu).  diag[0] = ||mu||,
+// diag[1] = lambda_1 (Rayleigh quotient), diag[2] = residual, diag[3] = mu . q; the report stage
+// turns them into sigma1_u = sqrt(lambda_1), alpha1 = |mu . v_1| (= (sigma_1 / l) u_1^T 1,
+// PAPER.md:559-561), cos_mu_v1 = alpha1 / ||mu||.
+avd_status launch_uncentred(Ctx* c) {
+  AVD_TRY(ensure_graphs(c));
+  if (eig_nograph()) {
+    EigCtl* ctl = reinterpret_cast<EigCtl*>(c->eig_ctl);
+    EigCtl* hc = reinterpret_cast<EigCtl*>(c->eig_host + 6 * kMaxP);
+    ctl_u_init_kernel<<<1, 32, 0, c->stream>>>(ctl);
+    AVD_LAUNCHED(c);
+    mu_norm_kernel<<<1, 256, 0, c->stream>>>(c->mu, c->cfg.m, c->m_pad, c->diag);
+    AVD_LAUNCHED(c);
+    for (;;) {
+      AVD_TRY(enqueue_unc(c, 0));
+      AVD_CUDA(cudaMemcpyAsync(hc, ctl, sizeof(EigCtl), cudaMemcpyDeviceToHost, c->stream));
+      AVD_CUDA(cudaStreamSynchronize(c->stream));
+      if (hc->stop_u) break;
     }
-    power_u_kernel<<<grid, 256, 0, c->stream>>>(c->G32, c->m_pad, c->mu, m, (double)c->cfg.l_global, q, y);
-    AVD_LAUNCHED(c);
-    power_u_stats_kernel<<<1, 256, 0, c->stream>>>(c->mu, m, q, y, c->diag);
-    AVD_LAUNCHED(c);
-    AVD_CUDA(cudaMemcpyAsync(h, c->diag, sizeof(double) * 4, cudaMemcpyDeviceToHost, c->stream));
-    AVD_CUDA(cudaStreamSynchronize(c->stream));
-    if (!(h[0] > 0.0) || h[2] <= 1e-8) break;
+    c->launches -= (int64_t)c->n_u_nodes * hc->blocks_u;  // the report adds them for the graph mode
+    return AVD_OK;
   }
-  c->iters_u = it;
-  c->sigma1_u = std::sqrt(std::max(h[1], 0.0));
-  c->alpha1 = std::fabs(h[3]);
-  c->cos_mu_v1 = h[0] > 0.0 ? std::min(1.0, std::fabs(h[3]) / h[0]) : 0.0;
-  c->resid_u = h[2];
+  AVD_CUDA(cudaEventRecord(c->ev_fork, c->stream));
+  AVD_CUDA(cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
+  cudaStream_t user = c->stream;
+  c->stream = c->side_stream;
+  ctl_u_init_kernel<<<1, 32, 0, c->stream>>>(reinterpret_cast<EigCtl*>(c->eig_ctl));
+  mu_norm_kernel<<<1, 256, 0, c->stream>>>(c->mu, c->cfg.m, c->m_pad, c->diag);
+  c->stream = user;
+  AVD_LAUNCHED(c);
+  AVD_LAUNCHED(c);
+  AVD_CUDA(cudaGraphLaunch(c->unc_exec, c->side_stream));
+  AVD_CUDA(cudaEventRecord(c->ev_join, c->side_stream));
   return AVD_OK;
+}
+avd_status join_uncentred(Ctx* c) {
+  if (eig_nograph()) return AVD_OK;
+  AVD_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+  return AVD_OK;
+}
+
+void destroy_graphs(Ctx* c) {
+  if (c->eig_exec) cudaGraphExecDestroy(c->eig_exec);
+  if (c->unc_exec) cudaGraphExecDestroy(c->unc_exec);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  if (c->side_stream) cudaStreamDestroy(c->side_stream);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  c->eig_exec = c->unc_exec = nullptr;
 }
 
 }  // namespace avd
