@@ -490,7 +490,12 @@ avd_status avd_stage_gram(avd_ctx* c, const float* X) {
     return launch_gram(c);
   };
   const bool force_exact = (c->cfg.flags & AVD_FLAG_EXACT_SCALE) != 0;
-  if (!force_exact) AVD_TRY(gram());
+  if (!force_exact) {  // gated on the device: skipped when an entry overflowed the sampled range
+    AVD_CUDA(cudaMemcpyAsync(c->qsum, c->qsum_local, sizeof(long long) * 2 * c->cfg.m, cudaMemcpyDeviceToDevice,
+                             c->stream));
+    AVD_CUDA(cudaMemcpyAsync(c->qerr, c->qerr_local, sizeof(double) * c->m_pad, cudaMemcpyDeviceToDevice, c->stream));
+    AVD_TRY(launch_gram(c, c->stats + c->cfg.m + 3));
+  }
   AVD_CUDA(cudaEventSynchronize(c->ev_host));
   const double ovf = hs[0];
   std::memcpy(&c->hplan, hs + 1, sizeof(DevPlan));
@@ -501,6 +506,10 @@ avd_status avd_stage_gram(avd_ctx* c, const float* X) {
   }
   c->requantised = ovf > 0.0 || force_exact;
   if (c->requantised) {
+    // automatic digits: an exact-range requant that costs a column >= 3 bits of its planned
+    // 14-bit resolution (a massive activation the row sample missed) goes to
+    // 3 digits at once instead of through a 2-digit Gram and the a-posteriori escalation
+    if (c->auto_digits && c->nd == 2 && c->hplan.range_bits >= 3) c->nd = 3;
     AVD_TRY(launch_pass1(c, X, false));  // exact column ranges (k_pass1.cu)
     AVD_TRY(gram());
   }

@@ -36,6 +36,8 @@ struct DevPlan {
   int64_t quota;        // ties this rank takes
   int64_t sel_local;    // entries of E_top held by this rank
   int64_t top_offset;   // global position of this rank's first entry
+  int32_t range_bits;   // max_j ceil(log2(max|y_j| / planned range)): bits an exact-range requant loses
+  int32_t pad0;
 };
 
 struct Ctx {
@@ -210,7 +212,7 @@ avd_status launch_uncentred(Ctx* c);                       // k_eig.cu (mean-bia
 avd_status join_uncentred(Ctx* c);                         // k_eig.cu
 void destroy_graphs(Ctx* c);                               // k_eig.cu
 avd_status launch_sign_count(Ctx* c);                      // k_project.cu (mean-bias diagnostics)
-avd_status launch_gram(Ctx* c);                            // k_gram.cu
+avd_status launch_gram(Ctx* c, const double* skip = nullptr);  // k_gram.cu (skip: device gate)
 avd_status gram_make_tmap(Ctx* c);                         // k_gram.cu
 avd_status launch_gram_finalize(Ctx* c);                   // k_eig.cu
 avd_status run_eig(Ctx* c);                                // k_eig.cu

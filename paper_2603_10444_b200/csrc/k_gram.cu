@@ -65,7 +65,8 @@ __device__ __forceinline__ void unit_coords(int64_t u, int n_tiles, int T, int S
 template <int ND, int NS>
 __global__ void __launch_bounds__(kGramThreads, 1) gram_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                int64_t m_pad, int64_t l_pad, int64_t NK, int T, int S,
-                                                               long long* __restrict__ G) {
+                                                               long long* __restrict__ G, const double* __restrict__ skip) {
+  if (skip && *skip > 0.0) return;  // see gram2_kernel
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr uint32_t kStageBytes = 2 * ND * kBox;
@@ -268,7 +269,10 @@ __device__ __forceinline__ void unit_coords_pair(int64_t u, int n_pairs, int T, 
 template <int ND, int NS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGramThreads, 1)
     gram2_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB, int64_t m_pad,
-                 int64_t l_pad, int64_t NK, int T, int S, long long* __restrict__ G) {
+                 int64_t l_pad, int64_t NK, int T, int S, long long* __restrict__ G, const double* __restrict__ skip) {
+  // speculative launch (queued before the host reads the fused pass's flags): an entry outside the
+  // sampled digit range means the operand is re-encoded, so this Gram would be discarded
+  if (skip && *skip > 0.0) return;  // uniform over the grid: no CTA reaches a cluster barrier
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr uint32_t kABytes = 128 * 128;   // one digit plane of the CTA's 128 A-rows
@@ -491,7 +495,7 @@ avd_status gram_make_tmap(Ctx* c) {
   return AVD_OK;
 }
 
-avd_status launch_gram(Ctx* c) {
+avd_status launch_gram(Ctx* c, const double* skip) {
   const int T = (int)(c->m_pad / 128);
   const int64_t NK = c->l_pad / 128;
   const int S = c->gram_split;
@@ -505,13 +509,13 @@ avd_status launch_gram(Ctx* c) {
       const size_t smem = (size_t)NS * 2 * (128 * 128 + 64 * 128) + 1024;
       AVD_CUDA(smem_attr(gram2_kernel<2, NS>, (int)smem));
       gram2_kernel<2, NS><<<grid, kGramThreads, smem, c->stream>>>(c->tmap_digits, c->tmap_digits_b, c->m_pad,
-                                                                   c->l_pad, NK, T, S, c->gram_i);
+                                                                   c->l_pad, NK, T, S, c->gram_i, skip);
     } else {
       constexpr int NS = 3;
       const size_t smem = (size_t)NS * 3 * (128 * 128 + 64 * 128) + 1024;
       AVD_CUDA(smem_attr(gram2_kernel<3, NS>, (int)smem));
       gram2_kernel<3, NS><<<grid, kGramThreads, smem, c->stream>>>(c->tmap_digits, c->tmap_digits_b, c->m_pad,
-                                                                   c->l_pad, NK, T, S, c->gram_i);
+                                                                   c->l_pad, NK, T, S, c->gram_i, skip);
     }
     AVD_LAUNCHED(c);
     return AVD_OK;
@@ -523,12 +527,12 @@ avd_status launch_gram(Ctx* c) {
     constexpr int NS = 3;
     const size_t smem = (size_t)NS * 2 * 2 * kBox + 1024;
     AVD_CUDA(smem_attr(gram_kernel<2, NS>, (int)smem));
-    gram_kernel<2, NS><<<grid, kGramThreads, smem, c->stream>>>(c->tmap_digits, c->m_pad, c->l_pad, NK, T, S, c->gram_i);
+    gram_kernel<2, NS><<<grid, kGramThreads, smem, c->stream>>>(c->tmap_digits, c->m_pad, c->l_pad, NK, T, S, c->gram_i, skip);
   } else {
     constexpr int NS = 2;
     const size_t smem = (size_t)NS * 2 * 3 * kBox + 1024;
     AVD_CUDA(smem_attr(gram_kernel<3, NS>, (int)smem));
-    gram_kernel<3, NS><<<grid, kGramThreads, smem, c->stream>>>(c->tmap_digits, c->m_pad, c->l_pad, NK, T, S, c->gram_i);
+    gram_kernel<3, NS><<<grid, kGramThreads, smem, c->stream>>>(c->tmap_digits, c->m_pad, c->l_pad, NK, T, S, c->gram_i, skip);
   }
   AVD_LAUNCHED(c);
   return AVD_OK;

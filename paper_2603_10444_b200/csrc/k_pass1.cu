@@ -616,9 +616,16 @@ __global__ void __launch_bounds__(256) pass1_reduce_kernel(
 // |E_top| = min(n_top, #nonzero), the non-finite count.
 __global__ void finish_kernel(int64_t m, int64_t m_pad, int64_t l_global, int64_t n_top,
                               const double* __restrict__ stats, double* __restrict__ mu, float* __restrict__ mu_hl,
-                              DevPlan* __restrict__ dp) {
+                              DevPlan* __restrict__ dp, const float* __restrict__ colmax,
+                              const int32_t* __restrict__ shift, int nd) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j < m && !isfinite(stats[j])) atomicAdd(reinterpret_cast<unsigned long long*>(&dp->nonfinite), 1ull);
+  // bits of resolution an exact-range re-quantisation would cost column j: the measured
+  // max |x - mu0| against the range the sampled scale planned for (2^(7nd-1) in y units)
+  if (j < m) {
+    const double r = ldexp((double)colmax[j], shift[j] - (7 * nd - 1));
+    if (r > 1.0 && r < 1e300) atomicMax(&dp->range_bits, ilogb(r) + 1);
+  }
   if (j < m_pad) {
     float mh = 0.f, ml = 0.f;
     if (j < m) {
@@ -755,9 +762,10 @@ avd_status launch_pass1(Ctx* c, const float* X, bool full) {
 
 avd_status launch_finish(Ctx* c) {
   AVD_CUDA(cudaMemsetAsync(&c->dplan->nonfinite, 0, sizeof(int64_t), c->stream));
+  AVD_CUDA(cudaMemsetAsync(&c->dplan->range_bits, 0, sizeof(int32_t), c->stream));
   finish_kernel<<<(unsigned)ceil_div(c->m_pad, 256), 256, 0, c->stream>>>(c->cfg.m, c->m_pad, c->cfg.l_global,
                                                                          c->plan.n_top, c->stats, c->mu, c->mu_hl,
-                                                                         c->dplan);
+                                                                         c->dplan, c->colmax, c->shift, c->nd);
   AVD_LAUNCHED(c);
   return AVD_OK;
 }
