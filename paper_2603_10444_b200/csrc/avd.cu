@@ -148,7 +148,7 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   L.add(sizeof(long long) * 2);                 // 44 cand_x
   L.add(gemm_part_bytes(m, C->m_pad, (int)p, C->num_sms));  // 45 gemm_part
   L.add(sizeof(float) * 2 * C->l_pad * (((C->k_pad + 31) / 32) * 32));   // 46 P_hl
-  L.add(sizeof(float) * 2 * C->k_pad * round_up(m, 32));                 // 47 Vt_hl
+  L.add(std::max<size_t>(sizeof(float) * 2 * C->k_pad * round_up(m, 32), (size_t)4 * C->k_pad * C->m_pad));  // 47 Vt_hl / W digits
   L.add(sizeof(float) * 2 * C->m_pad * (((C->k_pad + 31) / 32) * 32));   // 48 V_hl
   L.add(sizeof(float) * 2 * C->m_pad);                                   // 49 mu_hl
   L.add(sizeof(float) * C->m_pad * C->m_pad);                            // 50 G32
@@ -173,6 +173,7 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   L.add(sizeof(double) * kMaxP);                                         // 69 prec
   L.add(sizeof(double) * m);                                             // 70 ysq
   L.add(kEigCtlBytes);                                                   // 71 eig_ctl
+  L.add(sizeof(double) * 512);                                           // 72 wsc (+ spiky list at 384)
   if (L.n >= 128) { set_error("workspace layout table overflow"); return AVD_EINVAL; }
   plan->workspace_bytes = L.total;
   if (lay) *lay = L;
@@ -340,7 +341,7 @@ avd_status avd_create(const avd_config* cfg, avd_ctx** out) {
   BIND(samp, double*); BIND(smax, float*); BIND(smin, float*); BIND(qscale, float*); BIND(qoff, float*);
   BIND(qsum_part, long long*); BIND(qsum_local, long long*); BIND(qerr_part, float*); BIND(qerr_local, double*);
   BIND(qerr, double*); BIND(mu0, float*); BIND(qsq_part, long long*); BIND(diag, double*);
-  BIND(prec, double*); BIND(ysq, double*); BIND(eig_ctl, void*);
+  BIND(prec, double*); BIND(ysq, double*); BIND(eig_ctl, void*); BIND(wsc, double*);
 #undef BIND
   if (cudaMallocHost(&c->eig_host, sizeof(double) * kHostScratch) != cudaSuccess) {
     cudaGetLastError();

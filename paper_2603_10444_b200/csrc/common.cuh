@@ -140,7 +140,8 @@ struct Ctx {
   // K5/K8
   float* P = nullptr;             // [l_local][k_pad]
   float* P_hl = nullptr;          // [2][l_pad][KP32] tf32 hi / lo planes of P (K8 A operand)
-  float* Vt_hl = nullptr;         // [2*k_pad][m_pad32] tf32 hi / lo of V^T (K5 B operand)
+  float* Vt_hl = nullptr;         // [2*k_pad][m_pad32] fp32 words; holds K5's int8 W digit planes [4][k_pad][m_pad]
+  double* wsc = nullptr;          // [512]: K5 column scales t_r | corrections corr_r | (int) spiky columns at 384
   float* V_hl = nullptr;          // [2][m_pad][KP32] tf32 hi / lo of V (K8 B operand)
   int64_t m_pad32 = 0;
   double* en_part = nullptr;      // [n_proj_ctas][4]

@@ -68,7 +68,9 @@ __global__ void __launch_bounds__(kGramThreads, 1) gram_kernel(const __grid_cons
                                                                long long* __restrict__ G, const double* __restrict__ skip) {
   if (skip && *skip > 0.0) return;  // see gram2_kernel
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned in the shared window; derived from smem_raw by an offset so the compiler keeps
+  // the shared address space (LDS/STS instead of generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr uint32_t kStageBytes = 2 * ND * kBox;
   __shared__ uint64_t full_bar[NS], empty_bar[NS], tfull_bar, tempty_bar;
   __shared__ uint32_t tmem_base_sh;
@@ -274,7 +276,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGramThreads, 1)
   // sampled digit range means the operand is re-encoded, so this Gram would be discarded
   if (skip && *skip > 0.0) return;  // uniform over the grid: no CTA reaches a cluster barrier
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned in the shared window; derived from smem_raw by an offset so the compiler keeps
+  // the shared address space (LDS/STS instead of generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr uint32_t kABytes = 128 * 128;   // one digit plane of the CTA's 128 A-rows
   constexpr uint32_t kBBytes = 64 * 128;    // one digit plane of the CTA's 64 B-columns
   constexpr uint32_t kStageBytes = ND * (kABytes + kBBytes);
