@@ -48,9 +48,10 @@ typedef enum {
   AVD_ECUDA = 4,       /* a CUDA runtime / driver call failed                             */
   AVD_ENOMEM = 6,      /* device allocation failed                                       */
   AVD_ESTATE = 8,      /* stage called out of order                                      */
-  AVD_EREPEAT = 9      /* (stage API only) avd_stage_eig raised the Gram operand to 3 digits:
+  AVD_EREPEAT = 9,     /* (stage API only) avd_stage_eig raised the Gram operand to 3 digits:
                           call avd_stage_gram again (exchange GRAM, QSUM, QERR), then
                           avd_stage_eig; avd_decompose handles this internally              */
+  AVD_EEXCHANGE = 10   /* an exchange callback (avd_exchange_fn) returned nonzero            */
 } avd_status;
 
 /* Sizes derived from (l, m, fractions) — DESIGN.md R1, R2:
@@ -189,9 +190,10 @@ avd_status avd_decompose_host(avd_ctx* ctx, const float* X_host, avd_outputs* ou
  *       exchange: AVD_BUF_STATS (f64, SUM), AVD_BUF_COLMAX (f32, MAX: max |x - quantiser centre|),
                  AVD_BUF_DIAG (f64, SUM: sum_i (x_ij - centre_j)^2, the exact diagonal of G)
  *   avd_stage_gram     (mu; AVD_ENONFINITE if X has NaN/Inf; re-quantisation with the exact
- *                       ranges if any rank's digits overflowed; K3 tcgen05 int8 Gram, exact int64)
- *       exchange: AVD_BUF_GRAM (i64, SUM), AVD_BUF_CAND (i64, SUM), AVD_BUF_QSUM (i64, SUM),
- *                 AVD_BUF_QERR (f64, SUM)
+ *                       ranges if any rank's digits overflowed; K3 tcgen05 int8 Gram, exact int64;
+ *                       with world > 1 its upper 128-tiles are also packed into AVD_BUF_GRAMP)
+ *       exchange: AVD_BUF_GRAMP (i64, SUM; world > 1 — avd_stage_eig unpacks it),
+ *                 AVD_BUF_CAND (i64, SUM), AVD_BUF_QSUM (i64, SUM), AVD_BUF_QERR (f64, SUM)
  *   avd_stage_eig      (exact centring of the Gram, K4 subspace iteration + Rayleigh-Ritz, and
  *                       the top eigenpair of the uncentred Gram G + l mu mu^T; replicated on every
  *                       rank)
@@ -214,6 +216,10 @@ typedef enum {
   AVD_BUF_TIES = 8, AVD_BUF_AGG = 9, AVD_BUF_HIST0 = 10, AVD_BUF_CAND = 11,
   AVD_BUF_SAMPLE = 12, AVD_BUF_SMAX = 13, AVD_BUF_SMIN = 14, AVD_BUF_QSUM = 15, AVD_BUF_QERR = 21,
   AVD_BUF_DIAG = 22,
+  AVD_BUF_GRAMP = 25,  /* the Gram's upper 128-tiles, packed (i64, SUM): what world > 1 exchanges
+                          after avd_stage_gram (half the bytes of AVD_BUF_GRAM)               */
+  AVD_BUF_EIGZ = 23,   /* distributed eigensolve: Z = G Q, m x p f32 (SUM of row blocks)     */
+  AVD_BUF_EIGY = 24,   /* distributed eigensolve: Y = G Z or G Q, m x p f64 (SUM of row blocks) */
   /* read-only views for tests / diagnostics (not exchanged) */
   AVD_BUF_MU = 16, AVD_BUF_G = 17, AVD_BUF_P = 18, AVD_BUF_DIGITS = 19, AVD_BUF_SCALE = 20
 } avd_buffer_id;
@@ -229,6 +235,39 @@ avd_status avd_stage_project(avd_ctx* ctx, const float* X_dev);
 avd_status avd_stage_select(avd_ctx* ctx, const float* X_dev, int32_t level, int32_t rank);
 avd_status avd_stage_gather(avd_ctx* ctx, const float* X_dev, int32_t rank, avd_outputs* out);
 avd_status avd_stage_report(avd_ctx* ctx, avd_outputs* out);
+
+/* ---- library-driven exchanges (row-sharded, world >= 1) --------------------------------
+ * An exchange callback all-reduces IN PLACE, over all ranks, `count` elements of type `dtype`
+ * at buf_dev (device; the workspace buffer `which`, avd_buffer_id) with `op`, stream-ordered
+ * after the library's work on the context's stream (e.g. ncclAllReduce on that stream, or a
+ * synchronous host-staged all-reduce).  Returns 0 on success; anything else aborts the call with
+ * AVD_EEXCHANGE.                                                                              */
+typedef enum { AVD_DT_F64 = 0, AVD_DT_F32 = 1, AVD_DT_I64 = 2 } avd_dtype;
+typedef enum { AVD_OP_SUM = 0, AVD_OP_MAX = 1, AVD_OP_MIN = 2 } avd_op;
+typedef int (*avd_exchange_fn)(int32_t which, void* buf_dev, int32_t dtype, int32_t op, size_t count,
+                               void* user);
+
+/* Distributed eigensolve: avd_stage_eig with every G Q product split by row
+ * blocks over the ranks (rank r computes rows [r0, r1) of its share of the 128-row blocks); the
+ * zero-padded products are exchanged through fn as SUMs (AVD_BUF_EIGZ, f32; AVD_BUF_EIGY, f64 —
+ * i.e. all-gathers), twice per power step and once per Rayleigh-Ritz check; the p x p work is
+ * replicated.  Same results as avd_stage_eig up to the row blocking of the GEMM partial sums.
+ * world == 1 or fn == NULL: exactly avd_stage_eig.  May return AVD_EREPEAT like avd_stage_eig. */
+avd_status avd_stage_eig_dist(avd_ctx* ctx, int32_t rank, avd_exchange_fn fn, void* user);
+
+/* The whole row-sharded pass for a C caller: every stage in order, every exchange listed above
+ * through fn (with world > 1 the Gram goes as AVD_BUF_GRAMP), the distributed eigensolve, the
+ * 3-digit repeat.  X_dev: this rank's rows (cfg.l_local x m).  world == 1 with fn == NULL is
+ * avd_decompose.                                                                              */
+avd_status avd_decompose_sharded(avd_ctx* ctx, const float* X_dev, int32_t rank, avd_outputs* out,
+                                 avd_exchange_fn fn, void* user);
+
+/* A ready-made avd_exchange_fn over NCCL: user = &(avd_nccl_comm){comm, stream}, comm an
+ * ncclComm_t of the `world` ranks in row order, stream the context's cudaStream_t.  Issues
+ * ncclAllReduce(buf, buf, count, type, op, comm, stream) (libnccl.so.2 is loaded at first use;
+ * returns nonzero when it cannot be loaded or the call fails).                                */
+typedef struct { void* comm; void* stream; } avd_nccl_comm;
+int avd_exchange_nccl(int32_t which, void* buf_dev, int32_t dtype, int32_t op, size_t count, void* user);
 
 /* Tie quota of `rank` (R3): E_top takes the first q entries with key == T in global
  * linear order and rows are sharded in rank order, so rank r takes

@@ -13,17 +13,24 @@ LIB_PATH = os.path.join(HERE, "libavd.so")
 
 AVD_FLAG_STREAM_SELECT, AVD_FLAG_EXACT_SCALE, AVD_FLAG_FORCE_ESCALATE = 1, 2, 4
 AVD_OK, AVD_EINVAL, AVD_ENONFINITE, AVD_ENOCONV, AVD_ECUDA, AVD_ENOMEM, AVD_ESTATE = 0, 1, 2, 3, 4, 6, 8
-AVD_EREPEAT = 9
+AVD_EREPEAT, AVD_EEXCHANGE = 9, 10
 BUF = dict(STATS=0, COLMAX=1, COLMIN=2, HIST1=3, GRAM=4, ENERGY=5, HIST2=6, HIST3=7, TIES=8, AGG=9,
            HIST0=10, CAND=11, SAMPLE=12, SMAX=13, SMIN=14, QSUM=15, QERR=21, DIAG=22,
+           GRAMP=25, EIGZ=23, EIGY=24,
            MU=16, G=17, P=18, DIGITS=19, SCALE=20)
+BUF_NAME = {v: k for k, v in BUF.items()}
+AVD_DT_F64, AVD_DT_F32, AVD_DT_I64 = 0, 1, 2
+AVD_OP_SUM, AVD_OP_MAX, AVD_OP_MIN = 0, 1, 2
+# int (*avd_exchange_fn)(int32_t which, void* buf_dev, int32_t dtype, int32_t op, size_t count, void* user)
+EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
+                               ctypes.c_size_t, ctypes.c_void_p)
 
 # every symbol include/avd.h declares
 EXPORTS = ["avd_plan", "avd_create", "avd_destroy", "avd_get_plan", "avd_decompose",
            "avd_decompose_host", "avd_buffer", "avd_stage_stats", "avd_stage_split",
            "avd_stage_gram", "avd_stage_eig", "avd_stage_project", "avd_stage_select",
            "avd_stage_gather", "avd_stage_report", "avd_tie_quota", "avd_launch_count", "avd_strerror",
-           "avd_last_error"]
+           "avd_last_error", "avd_stage_eig_dist", "avd_decompose_sharded", "avd_exchange_nccl"]
 
 
 class avd_plan_t(ctypes.Structure):
@@ -93,6 +100,9 @@ def lib() -> ctypes.CDLL:
         L.avd_stage_split.argtypes = [P, P]
         L.avd_stage_gram.argtypes = [P, P]
         L.avd_stage_eig.argtypes = [P]
+        L.avd_stage_eig_dist.argtypes = [P, I32, EXCHANGE_FN, P]
+        L.avd_decompose_sharded.argtypes = [P, P, I32, ctypes.POINTER(avd_outputs), EXCHANGE_FN, P]
+        L.avd_exchange_nccl.argtypes = [I32, P, I32, I32, ctypes.c_size_t, P]
         L.avd_stage_project.argtypes = [P, P]
         L.avd_stage_select.argtypes = [P, P, I32, I32]
         L.avd_stage_gather.argtypes = [P, P, I32, ctypes.POINTER(avd_outputs)]
@@ -172,6 +182,17 @@ def avd_stage_gram(h, X_dev: int):
 
 def avd_stage_eig(h):
     return check(lib().avd_stage_eig(h), "avd_stage_eig", ok=(AVD_OK, AVD_ENOCONV, AVD_EREPEAT))
+
+
+def avd_stage_eig_dist(h, rank: int, fn, user=None):
+    """fn: an EXCHANGE_FN (keep a reference alive for the call)."""
+    return check(lib().avd_stage_eig_dist(h, rank, fn, user), "avd_stage_eig_dist",
+                 ok=(AVD_OK, AVD_ENOCONV, AVD_EREPEAT))
+
+
+def avd_decompose_sharded(h, X_ptr: int, rank: int, out: avd_outputs, fn, user=None):
+    return check(lib().avd_decompose_sharded(h, ctypes.c_void_p(X_ptr), rank, ctypes.byref(out), fn, user),
+                 "avd_decompose_sharded", ok=(AVD_OK, AVD_ENOCONV))
 
 
 def avd_stage_project(h, X_ptr: int):

@@ -10,6 +10,9 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include "common.cuh"
 
 namespace avd {
@@ -174,6 +177,10 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   L.add(sizeof(double) * m);                                             // 70 ysq
   L.add(kEigCtlBytes);                                                   // 71 eig_ctl
   L.add(sizeof(double) * 512);                                           // 72 wsc (+ spiky list at 384)
+  {
+    const int64_t T = C->m_pad / 128;
+    L.add(world > 1 ? sizeof(long long) * (size_t)(T * (T + 1) / 2) * 128 * 128 : 0);  // 73 gram_p
+  }
   if (L.n >= 128) { set_error("workspace layout table overflow"); return AVD_EINVAL; }
   plan->workspace_bytes = L.total;
   if (lay) *lay = L;
@@ -287,6 +294,7 @@ const char* avd_strerror(avd_status s) {
     case AVD_ENOMEM: return "out of device memory";
     case AVD_ESTATE: return "stage called out of order";
     case AVD_EREPEAT: return "repeat avd_stage_gram: the Gram operand was raised to 3 digits";
+    case AVD_EEXCHANGE: return "exchange callback failed";
   }
   return "unknown status";
 }
@@ -341,7 +349,8 @@ avd_status avd_create(const avd_config* cfg, avd_ctx** out) {
   BIND(samp, double*); BIND(smax, float*); BIND(smin, float*); BIND(qscale, float*); BIND(qoff, float*);
   BIND(qsum_part, long long*); BIND(qsum_local, long long*); BIND(qerr_part, float*); BIND(qerr_local, double*);
   BIND(qerr, double*); BIND(mu0, float*); BIND(qsq_part, long long*); BIND(diag, double*);
-  BIND(prec, double*); BIND(ysq, double*); BIND(eig_ctl, void*); BIND(wsc, double*);
+  BIND(prec, double*); BIND(ysq, double*); BIND(eig_ctl, void*); BIND(wsc, double*); BIND(gram_p, long long*);
+  if (c->cfg.world <= 1) c->gram_p = nullptr;
 #undef BIND
   if (cudaMallocHost(&c->eig_host, sizeof(double) * kHostScratch) != cudaSuccess) {
     cudaGetLastError();
@@ -428,6 +437,15 @@ avd_status avd_buffer(avd_ctx* c, int32_t which, void** ptr, size_t* bytes) {
     case AVD_BUF_P: *ptr = c->P; *bytes = sizeof(float) * c->cfg.l_local * c->k_pad; break;
     case AVD_BUF_DIGITS: *ptr = c->digits; *bytes = (size_t)c->nd_max * c->m_pad * c->l_pad; break;
     case AVD_BUF_SCALE: *ptr = c->shift; *bytes = sizeof(int32_t) * c->m_pad; break;
+    case AVD_BUF_GRAMP: {
+      if (!c->gram_p) { set_error("AVD_BUF_GRAMP exists with world > 1 only"); return AVD_EINVAL; }
+      const int64_t T = c->m_pad / 128;
+      *ptr = c->gram_p;
+      *bytes = sizeof(long long) * (size_t)(T * (T + 1) / 2) * 128 * 128;
+      break;
+    }
+    case AVD_BUF_EIGZ: *ptr = c->Z32; *bytes = sizeof(float) * m * c->p; break;
+    case AVD_BUF_EIGY: *ptr = c->Y; *bytes = sizeof(double) * m * c->p; break;
     default: set_error("unknown buffer id"); return AVD_EINVAL;
   }
   return AVD_OK;
@@ -473,6 +491,7 @@ avd_status avd_stage_gram(avd_ctx* c, const float* X) {
                              c->stream));
     AVD_CUDA(cudaMemcpyAsync(c->qerr, c->qerr_local, sizeof(double) * c->m_pad, cudaMemcpyDeviceToDevice, c->stream));
     AVD_TRY(launch_gram(c));
+    if (c->gram_p) AVD_TRY(launch_gram_pack(c, false));  // world > 1: the exchanged form
     c->requantised = true;
     c->stage = 3;
     return AVD_OK;
@@ -514,15 +533,17 @@ avd_status avd_stage_gram(avd_ctx* c, const float* X) {
     AVD_TRY(launch_pass1(c, X, false));  // exact column ranges (k_pass1.cu)
     AVD_TRY(gram());
   }
+  if (c->gram_p) AVD_TRY(launch_gram_pack(c, false));  // world > 1: the exchanged form
   c->stage = 3;
   return AVD_OK;
 }
 
-avd_status avd_stage_eig(avd_ctx* c) {
+static avd_status stage_eig_impl(avd_ctx* c, int32_t rank, avd_exchange_fn fn, void* user) {
   STAGE_CHECK(c, 3);
+  if (c->gram_p) AVD_TRY(launch_gram_pack(c, true));  // the exchanged packed tiles back into G_int
   AVD_TRY(launch_gram_finalize(c));
   AVD_TRY(launch_uncentred(c));  // mean-bias diagnostics, side stream
-  avd_status st = run_eig(c);
+  avd_status st = fn ? run_eig_dist(c, rank, fn, user) : run_eig(c);
   AVD_TRY(join_uncentred(c));    // (stream order only; G32 is not rewritten before the join)
   if (st != AVD_OK && st != AVD_ENOCONV) return st;
   // automatic digits (avd_config.digits == 0): the quantisation-error bound decides whether the
@@ -538,6 +559,13 @@ avd_status avd_stage_eig(avd_ctx* c) {
   }
   c->stage = 4;
   return st;
+}
+
+avd_status avd_stage_eig(avd_ctx* c) { return stage_eig_impl(c, 0, nullptr, nullptr); }
+
+avd_status avd_stage_eig_dist(avd_ctx* c, int32_t rank, avd_exchange_fn fn, void* user) {
+  if (!c) { set_error("null ctx"); return AVD_EINVAL; }
+  return stage_eig_impl(c, rank, c->cfg.world > 1 ? fn : nullptr, user);
 }
 
 avd_status avd_stage_project(avd_ctx* c, const float* X) {
@@ -687,6 +715,88 @@ avd_status avd_decompose(avd_ctx* c, const float* X, avd_outputs* out) {
   AVD_TRY(avd_stage_gather(c, X, 0, out));
   AVD_TRY(avd_stage_report(c, out));
   return eig;
+}
+
+// The exchange table of the stage API (include/avd.h), in call order
+namespace {
+struct Exch { int32_t which, dtype, op; };
+avd_status run_exchanges(avd_ctx* c, const Exch* tab, int n, avd_exchange_fn fn, void* user) {
+  for (int i = 0; i < n; ++i) {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    AVD_TRY(avd_buffer(c, tab[i].which, &ptr, &bytes));
+    const size_t es = tab[i].dtype == AVD_DT_F32 ? 4 : 8;
+    if (fn(tab[i].which, ptr, tab[i].dtype, tab[i].op, bytes / es, user) != 0) {
+      set_error("exchange callback failed (buffer " + std::to_string(tab[i].which) + ")");
+      return AVD_EEXCHANGE;
+    }
+  }
+  return AVD_OK;
+}
+}  // namespace
+
+avd_status avd_decompose_sharded(avd_ctx* c, const float* X, int32_t rank, avd_outputs* out, avd_exchange_fn fn,
+                                 void* user) {
+  if (!c || !X || !out) { set_error("null argument"); return AVD_EINVAL; }
+  if (c->cfg.world == 1 && !fn) return avd_decompose(c, X, out);
+  if (!fn) { set_error("world > 1 needs an exchange callback"); return AVD_EINVAL; }
+  const bool w = c->cfg.world > 1;
+  static const Exch kStats[] = {{AVD_BUF_SAMPLE, AVD_DT_F64, AVD_OP_SUM}, {AVD_BUF_SMAX, AVD_DT_F32, AVD_OP_MAX},
+                                {AVD_BUF_SMIN, AVD_DT_F32, AVD_OP_MIN}, {AVD_BUF_HIST1, AVD_DT_I64, AVD_OP_SUM}};
+  static const Exch kSplit[] = {{AVD_BUF_STATS, AVD_DT_F64, AVD_OP_SUM}, {AVD_BUF_COLMAX, AVD_DT_F32, AVD_OP_MAX},
+                                {AVD_BUF_DIAG, AVD_DT_F64, AVD_OP_SUM}};
+  static const Exch kGram[] = {{AVD_BUF_GRAMP, AVD_DT_I64, AVD_OP_SUM}, {AVD_BUF_CAND, AVD_DT_I64, AVD_OP_SUM},
+                               {AVD_BUF_QSUM, AVD_DT_I64, AVD_OP_SUM}, {AVD_BUF_QERR, AVD_DT_F64, AVD_OP_SUM}};
+  static const Exch kRegram[] = {{AVD_BUF_GRAMP, AVD_DT_I64, AVD_OP_SUM}, {AVD_BUF_QSUM, AVD_DT_I64, AVD_OP_SUM},
+                                 {AVD_BUF_QERR, AVD_DT_F64, AVD_OP_SUM}};
+  static const Exch kProj[] = {{AVD_BUF_ENERGY, AVD_DT_F64, AVD_OP_SUM}};
+  static const Exch kSel[4] = {{AVD_BUF_HIST0, AVD_DT_I64, AVD_OP_SUM}, {AVD_BUF_HIST2, AVD_DT_I64, AVD_OP_SUM},
+                               {AVD_BUF_HIST3, AVD_DT_I64, AVD_OP_SUM}, {AVD_BUF_TIES, AVD_DT_I64, AVD_OP_SUM}};
+  static const Exch kAgg[] = {{AVD_BUF_AGG, AVD_DT_F64, AVD_OP_SUM}};
+  AVD_TRY(avd_stage_stats(c, X));
+  AVD_TRY(run_exchanges(c, kStats, 4, fn, user));
+  AVD_TRY(avd_stage_split(c, X));
+  AVD_TRY(run_exchanges(c, kSplit, 3, fn, user));
+  AVD_TRY(avd_stage_gram(c, X));
+  if (w) AVD_TRY(run_exchanges(c, kGram, 4, fn, user));
+  else AVD_TRY(run_exchanges(c, kGram + 1, 3, fn, user));
+  avd_status eig = avd_stage_eig_dist(c, rank, fn, user);
+  if (eig == AVD_EREPEAT) {
+    AVD_TRY(avd_stage_gram(c, X));
+    if (w) AVD_TRY(run_exchanges(c, kRegram, 3, fn, user));
+    else AVD_TRY(run_exchanges(c, kRegram + 1, 2, fn, user));
+    eig = avd_stage_eig_dist(c, rank, fn, user);
+  }
+  if (eig != AVD_OK && eig != AVD_ENOCONV) return eig;
+  AVD_TRY(avd_stage_project(c, X));
+  AVD_TRY(run_exchanges(c, kProj, 1, fn, user));
+  for (int lv = 0; lv < 4; ++lv) {
+    AVD_TRY(avd_stage_select(c, X, lv, rank));
+    AVD_TRY(run_exchanges(c, kSel + lv, 1, fn, user));
+  }
+  AVD_TRY(avd_stage_gather(c, X, rank, out));
+  AVD_TRY(run_exchanges(c, kAgg, 1, fn, user));
+  AVD_TRY(avd_stage_report(c, out));
+  return eig;
+}
+
+// ---- NCCL exchange (libnccl.so.2 loaded at first use; types from nccl.h)
+typedef ncclResult_t (*nccl_allreduce_t)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                         cudaStream_t);
+int avd_exchange_nccl(int32_t which, void* buf, int32_t dtype, int32_t op, size_t count, void* user) {
+  (void)which;
+  static nccl_allreduce_t fn = [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    return h ? reinterpret_cast<nccl_allreduce_t>(dlsym(h, "ncclAllReduce")) : nullptr;
+  }();
+  const avd_nccl_comm* nc = static_cast<const avd_nccl_comm*>(user);
+  if (!fn || !nc || !nc->comm) return 1;
+  const ncclDataType_t t = dtype == AVD_DT_F64 ? ncclFloat64 : (dtype == AVD_DT_F32 ? ncclFloat32 : ncclInt64);
+  const ncclRedOp_t o = op == AVD_OP_MAX ? ncclMax : (op == AVD_OP_MIN ? ncclMin : ncclSum);
+  return fn(buf, buf, count, t, o, static_cast<ncclComm_t>(nc->comm), static_cast<cudaStream_t>(nc->stream)) ==
+                 ncclSuccess
+             ? 0
+             : 1;
 }
 
 avd_status avd_decompose_host(avd_ctx* c, const float* X_host, avd_outputs* out) {

@@ -96,6 +96,7 @@ struct Ctx {
   bool requantised = false;       // the sampled digit scales overflowed: requantised with exact ranges
   // K3
   long long* gram_i = nullptr;    // [m_pad * m_pad] int64 (upper tiles) (exchange SUM)
+  long long* gram_p = nullptr;    // world > 1: the upper 128-tiles packed [T(T+1)/2][128][128] (exchange SUM)
   double* G = nullptr;            // [m_pad][m_pad] fp64 symmetric (zero beyond m)
   float* G32 = nullptr;           // [m_pad][m_pad] fp32 copy (power steps of K4)
   long long* qsum = nullptr;      // [2 m] column sums of the quantised operand | of its squares (exchange SUM)
@@ -217,6 +218,8 @@ avd_status launch_gram(Ctx* c, const double* skip = nullptr);  // k_gram.cu (ski
 avd_status gram_make_tmap(Ctx* c);                         // k_gram.cu
 avd_status launch_gram_finalize(Ctx* c);                   // k_eig.cu
 avd_status run_eig(Ctx* c);                                // k_eig.cu
+avd_status run_eig_dist(Ctx* c, int rank, avd_exchange_fn fn, void* user);  // k_eig.cu
+avd_status launch_gram_pack(Ctx* c, bool unpack);          // k_gram.cu (world > 1 exchange)
 void gemm_geometry(int64_t m, int64_t m_pad, int p, int num_sms, bool fp32, int* BM, int* KS, int* RB, int* KT);
 size_t gemm_part_bytes(int64_t m, int64_t m_pad, int p, int num_sms);
 avd_status launch_project(Ctx* c, const float* X);         // k_project.cu

@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(kSkThreads) gemm_kernel(const T* __restrict__ 
                                                           const T* __restrict__ Qin, int64_t m, int KT, int KS,
                                                           T* __restrict__ part, unsigned* __restrict__ tickets,
                                                           double* __restrict__ Y, float* __restrict__ Y32,
-                                                          const int* __restrict__ skip) {
+                                                          const int* __restrict__ skip, int rb0) {
   if (skip && *skip) return;  // device-side gate (eigensolver graph: Z comes from the RR check)
   constexpr int BM = 16 * NR;
   constexpr int p = 8 * NC;
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(kSkThreads) gemm_kernel(const T* __restrict__ 
   T* sm = reinterpret_cast<T*>(sk_raw);
   const int tid = threadIdx.x;
   const int ty = tid >> 3, tx = tid & 7;
-  const int rb = blockIdx.x / KS, ks = blockIdx.x % KS;
+  const int rb = rb0 + (int)(blockIdx.x / KS), ks = (int)(blockIdx.x % KS);
   const int kt0 = (int)(((int64_t)KT * ks) / KS), kt1 = (int)(((int64_t)KT * (ks + 1)) / KS);
   const int n = kt1 - kt0;
 
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kSkThreads) gemm_kernel(const T* __restrict__ 
   }
   cp_wait<0>();
   // partial product of this K slice -> part[rb][ks] (BM x p, row-major)
-  T* pp = part + ((int64_t)rb * KS + ks) * (BM * p);
+  T* pp = part + ((int64_t)(rb - rb0) * KS + ks) * (BM * p);
 #pragma unroll
   for (int r = 0; r < NR; ++r)
 #pragma unroll
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kSkThreads) gemm_kernel(const T* __restrict__ 
   __syncthreads();
   if (!last_sh) return;
   // the row block's last CTA: fixed-order sum of the KS partials
-  const T* base = part + (int64_t)rb * KS * (BM * p);
+  const T* base = part + (int64_t)(rb - rb0) * KS * (BM * p);
   for (int e = tid * 2; e < BM * p; e += kSkThreads * 2) {
     // the KS partials in order; loads batched 8 at a time so they are in flight together (the
     // sum is still the sequential q order)
@@ -1126,10 +1126,12 @@ void gemm_geometry(int64_t m, int64_t m_pad, int p, int num_sms, bool fp32, int*
 }
 size_t gemm_part_bytes(int64_t m, int64_t m_pad, int p, int num_sms) {
   size_t best = 0;
-  for (int f = 0; f < 2; ++f) {
+  for (int f = 0; f < 2; ++f) {  // RB x KS <= the resident-CTA count for any row range (gemm_launch)
     int BM, KS, RB, KT;
     gemm_geometry(m, m_pad, p, num_sms, f == 0, &BM, &KS, &RB, &KT);
-    best = std::max(best, (size_t)RB * KS * BM * p * (f == 0 ? sizeof(float) : sizeof(double)));
+    const int64_t want = (int64_t)num_sms * (f == 0 ? 3 : 2);
+    best = std::max(best, (size_t)std::max<int64_t>(want, (int64_t)RB * KS) * BM * p *
+                              (f == 0 ? sizeof(float) : sizeof(double)));
   }
   return (size_t)round_up((int64_t)best, 256) + sizeof(unsigned) * (size_t)(m_pad / 64 + 1);  // partials + tickets
 }
@@ -1137,12 +1139,21 @@ size_t gemm_part_bytes(int64_t m, int64_t m_pad, int p, int num_sms) {
 namespace {
 
 // Y = G In (fp64 G, fp64 math) or Y = G32 In32 (fp32); Y fp64 (+ optional fp32 mirror)
+// rows [r0, r1) of Y only (multiples of 128; all rows when r1 <= r0): the distributed eigensolve
 template <typename T, int NR, int NC>
-avd_status gemm_launch(Ctx* c, const T* Gm, const T* In, double* Y, float* Y32, const int* skip) {
+avd_status gemm_launch(Ctx* c, const T* Gm, const T* In, double* Y, float* Y32, const int* skip, int64_t r0 = 0,
+                       int64_t r1 = 0) {
   int BM, KS, RB, KT;
   const int p = 8 * NC;
   gemm_geometry(c->cfg.m, c->m_pad, p, c->num_sms, sizeof(T) == 4, &BM, &KS, &RB, &KT);
   if (BM != 16 * NR) { set_error("gemm geometry mismatch"); return AVD_EINVAL; }
+  int rb0 = 0;
+  if (r1 > r0) {  // a row range: fewer row blocks, more K slices (same partial-buffer bound)
+    rb0 = (int)(r0 / BM);
+    RB = (int)ceil_div(r1 - r0, BM);
+    const int64_t want = (int64_t)c->num_sms * (sizeof(T) == 4 ? 3 : 2);
+    KS = (int)std::max<int64_t>(1, std::min<int64_t>(want / RB, KT));
+  }
   const int sm = kSkStages * (kSkBK * BM + kSkBK * p) * (int)sizeof(T);
   AVD_CUDA(smem_attr(gemm_kernel<T, NR, NC>, sm));
   const size_t pb = gemm_part_bytes(c->cfg.m, c->m_pad, c->p, c->num_sms);
@@ -1150,23 +1161,24 @@ avd_status gemm_launch(Ctx* c, const T* Gm, const T* In, double* Y, float* Y32, 
   unsigned* tickets = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(c->gemm_part) + pb -
                                                   sizeof(unsigned) * (size_t)(c->m_pad / 64 + 1));
   gemm_kernel<T, NR, NC><<<RB * KS, kSkThreads, sm, c->stream>>>(Gm, c->m_pad, In, c->cfg.m, KT, KS, part, tickets, Y,
-                                                                 Y32, skip);
+                                                                 Y32, skip, rb0);
   AVD_LAUNCHED(c);
   return AVD_OK;
 }
 
-avd_status gemm64(Ctx* c, const double* In, double* Y, float* Y32) {
+avd_status gemm64(Ctx* c, const double* In, double* Y, float* Y32, int64_t r0 = 0, int64_t r1 = 0) {
   switch (c->p / 16) {
-#define CASE(PC) case PC: return gemm_launch<double, 4, 2 * PC>(c, c->G, In, Y, Y32, nullptr);
+#define CASE(PC) case PC: return gemm_launch<double, 4, 2 * PC>(c, c->G, In, Y, Y32, nullptr, r0, r1);
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
   }
   set_error("unsupported p");
   return AVD_EINVAL;
 }
-avd_status gemm32(Ctx* c, const float* In, double* Y, float* Y32, const int* skip = nullptr) {
+avd_status gemm32(Ctx* c, const float* In, double* Y, float* Y32, const int* skip = nullptr, int64_t r0 = 0,
+                  int64_t r1 = 0) {
   switch (c->p / 16) {
-#define CASE(PC) case PC: return gemm_launch<float, (PC <= 4 ? 8 : 4), 2 * PC>(c, c->G32, In, Y, Y32, skip);
+#define CASE(PC) case PC: return gemm_launch<float, (PC <= 4 ? 8 : 4), 2 * PC>(c, c->G32, In, Y, Y32, skip, r0, r1);
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
   }
@@ -1460,15 +1472,11 @@ static void precision_bound(Ctx* c, const double* theta, const double* h) {
   c->prec_share = pe;
 }
 
-// Subspace iteration (device-resident): power steps Q <- orth(G^2 Q) in fp32; a Rayleigh-Ritz
-// check (fp64) runs on a schedule predicted from the observed residual decay (at most every 8
-// steps, always on the last one), so the p x p Jacobi runs ~2 times per solve.  The whole loop is
-// one graph launch (build_eig_graph); the host synchronises once, after the final vectors and the
-// precision bound, and meanwhile the uncentred power iteration runs on the side stream.
-avd_status run_eig(Ctx* c) {
+namespace {
+// start block: Q_0 = orth(random), loop state reset (shared by every mode of the solve)
+avd_status eig_prologue(Ctx* c) {
   const int64_t m = c->cfg.m;
   const int p = c->p, k = c->k;
-  AVD_TRY(ensure_graphs(c));
   EigCtl* ctl = reinterpret_cast<EigCtl*>(c->eig_ctl);
   const uint32_t seed = eig_seed(c);
   const int max_it = std::max(2, c->cfg.max_iters > 0 ? c->cfg.max_iters : 200);
@@ -1484,28 +1492,14 @@ avd_status run_eig(Ctx* c) {
   AVD_LAUNCHED(c);
   rand_fill_kernel<<<(unsigned)ceil_div(m * p, 256), 256, 0, c->stream>>>(c->Z, nullptr, m, p, seed, nullptr, nullptr);
   AVD_LAUNCHED(c);
-  AVD_TRY(orth(c, c->Z, seed + 1, nullptr));
-  EigCtl* hc = reinterpret_cast<EigCtl*>(c->eig_host + 6 * kMaxP);
-  static_assert(6 * kMaxP + kEigCtlBytes / 8 <= kHostScratch, "pinned scratch too small");
-  const bool nograph = eig_nograph();
-  if (nograph) {
-    for (;;) {
-      ctl_begin_kernel<<<1, 32, 0, c->stream>>>(ctl, 0, 0);
-      AVD_LAUNCHED(c);
-      AVD_CUDA(cudaMemcpyAsync(hc, ctl, sizeof(EigCtl), cudaMemcpyDeviceToHost, c->stream));
-      AVD_CUDA(cudaStreamSynchronize(c->stream));
-      if (hc->rr_now) {
-        AVD_TRY(enqueue_rr(c, 0, 0));
-        AVD_CUDA(cudaMemcpyAsync(hc, ctl, sizeof(EigCtl), cudaMemcpyDeviceToHost, c->stream));
-        AVD_CUDA(cudaStreamSynchronize(c->stream));
-        if (hc->stop) break;
-      }
-      AVD_TRY(enqueue_pow(c));
-    }
-  } else {
-    AVD_CUDA(cudaGraphLaunch(c->eig_exec, c->stream));
-  }
-  // final vectors, sigma, the precision-bound sums
+  return orth(c, c->Z, seed + 1, nullptr);
+}
+
+// final vectors, sigma, the precision-bound sums; one synchronisation; fills the host fields
+avd_status eig_epilogue(Ctx* c, bool count_graph) {
+  const int64_t m = c->cfg.m;
+  const int p = c->p, k = c->k;
+  EigCtl* ctl = reinterpret_cast<EigCtl*>(c->eig_ctl);
   const int nb = (int)ceil_div(m, kFinThreads);
   fin_part_kernel<<<nb, kFinThreads, 0, c->stream>>>(c->U, c->theta, m, p, k, c->shift, c->qerr, c->G, c->m_pad,
                                                       c->red_part);
@@ -1517,21 +1511,122 @@ avd_status run_eig(Ctx* c) {
   AVD_LAUNCHED(c);
   // one pinned copy: theta [p] | t_r [k], var(d E_spike) | tr(G) | ctl
   double* h = c->eig_host + 4 * kMaxP;
+  EigCtl* hc = reinterpret_cast<EigCtl*>(c->eig_host + 6 * kMaxP);
+  static_assert(6 * kMaxP + kEigCtlBytes / 8 <= kHostScratch, "pinned scratch too small");
   AVD_CUDA(cudaMemcpyAsync(h, c->theta, sizeof(double) * p, cudaMemcpyDeviceToHost, c->stream));
   AVD_CUDA(cudaMemcpyAsync(h + p, c->prec, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, c->stream));
   AVD_CUDA(cudaMemcpyAsync(h + p + k + 1, c->trace, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   AVD_CUDA(cudaMemcpyAsync(hc, ctl, sizeof(EigCtl), cudaMemcpyDeviceToHost, c->stream));
   AVD_CUDA(cudaStreamSynchronize(c->stream));
   const int it = hc->it, rr = hc->rr_count;
-  if (!nograph)
+  if (count_graph)
     c->launches += (int64_t)c->n_begin_nodes * it + (int64_t)c->n_rr_nodes * rr + (int64_t)c->n_pow_nodes * (it - 1);
-  c->iters = std::min(it, max_it);
+  c->iters = std::min(it, hc->max_it);
   c->rr_count = rr;
   c->max_resid = hc->maxres;
   c->sigma_next = (k < p) ? std::sqrt(std::max(h[k], 0.0)) : 0.0;
   for (int r = 0; r < p; ++r) c->eig_host[r] = h[r];  // Ritz values of the last check
   precision_bound(c, h, h + p);
   return hc->conv ? AVD_OK : AVD_ENOCONV;
+}
+
+// host-driven loop (profiling mode, and the distributed solve): the same kernels and the same
+// device control decisions as the graph, one synchronisation per decision
+template <typename RR, typename POW>
+avd_status eig_host_loop(Ctx* c, RR&& rr_body, POW&& pow_body) {
+  EigCtl* ctl = reinterpret_cast<EigCtl*>(c->eig_ctl);
+  EigCtl* hc = reinterpret_cast<EigCtl*>(c->eig_host + 6 * kMaxP);
+  for (;;) {
+    ctl_begin_kernel<<<1, 32, 0, c->stream>>>(ctl, 0, 0);
+    AVD_LAUNCHED(c);
+    AVD_CUDA(cudaMemcpyAsync(hc, ctl, sizeof(EigCtl), cudaMemcpyDeviceToHost, c->stream));
+    AVD_CUDA(cudaStreamSynchronize(c->stream));
+    const bool rr = hc->rr_now != 0;
+    if (rr) {
+      AVD_TRY(rr_body());
+      AVD_CUDA(cudaMemcpyAsync(hc, ctl, sizeof(EigCtl), cudaMemcpyDeviceToHost, c->stream));
+      AVD_CUDA(cudaStreamSynchronize(c->stream));
+      if (hc->stop) break;
+    }
+    AVD_TRY(pow_body(rr));
+  }
+  return AVD_OK;
+}
+}  // namespace
+
+// Subspace iteration (device-resident): power steps Q <- orth(G^2 Q) in fp32; a Rayleigh-Ritz
+// check (fp64) runs on a schedule predicted from the observed residual decay (at most every 8
+// steps, always on the last one), so the p x p Jacobi runs ~2 times per solve.  The whole loop is
+// one graph launch (build_eig_graph); the host synchronises once, after the final vectors and the
+// precision bound, and meanwhile the uncentred power iteration runs on the side stream.
+avd_status run_eig(Ctx* c) {
+  AVD_TRY(ensure_graphs(c));
+  AVD_TRY(eig_prologue(c));
+  const bool nograph = eig_nograph();
+  if (nograph) {
+    AVD_TRY(eig_host_loop(c, [&]() { return enqueue_rr(c, 0, 0); }, [&](bool) { return enqueue_pow(c); }));
+  } else {
+    AVD_CUDA(cudaGraphLaunch(c->eig_exec, c->stream));
+  }
+  return eig_epilogue(c, !nograph);
+}
+
+// Distributed eigensolve: every rank holds the exchanged G, and each G Q product
+// is split by rows — rank r computes the rows [r0, r1) of its share of the 128-row blocks; the
+// other rows of the product are zero, so a SUM exchange of the whole m x p block is the
+// all-gather (EIGZ: the fp32 Z = G Q of a power step, EIGY: the fp64 Y = G Z or the Rayleigh-Ritz
+// product).  The p x p work, the orthonormalisation and the control decisions are replicated
+// (identical inputs -> identical results on every rank).  Exchanges per power step: 2 (1.2 MB
+// at c4), per check: 1.
+avd_status run_eig_dist(Ctx* c, int rank, avd_exchange_fn fn, void* user) {
+  const int world = c->cfg.world;
+  if (world <= 1 || !fn) return run_eig(c);
+  if (rank < 0 || rank >= world) { set_error("bad rank"); return AVD_EINVAL; }
+  AVD_TRY(ensure_graphs(c));
+  const int64_t m = c->cfg.m;
+  const int p = c->p;
+  const int64_t U = c->m_pad / 128;
+  const int64_t r0 = 128 * (U * rank / world), r1 = 128 * (U * (rank + 1) / world);
+  EigCtl* ctl = reinterpret_cast<EigCtl*>(c->eig_ctl);
+  auto exch = [&](int which, void* ptr, int dt) -> avd_status {
+    if (fn(which, ptr, dt, AVD_OP_SUM, (size_t)(m * p), user) != 0) {
+      set_error("exchange callback failed (buffer " + std::to_string(which) + ")");
+      return AVD_EEXCHANGE;
+    }
+    return AVD_OK;
+  };
+  AVD_TRY(eig_prologue(c));
+  // (r1 <= r0 when there are more ranks than row blocks: the rank contributes zeros)
+  auto rows_y = [&](auto&& gemm) -> avd_status {
+    AVD_CUDA(cudaMemsetAsync(c->Y, 0, sizeof(double) * m * p, c->stream));
+    if (r1 > r0) AVD_TRY(gemm());
+    return exch(AVD_BUF_EIGY, c->Y, AVD_DT_F64);
+  };
+  auto rr_body = [&]() -> avd_status {
+    AVD_TRY(rows_y([&]() { return gemm64(c, c->Q, c->Y, nullptr, r0, r1); }));  // Y = G Q (fp64)
+    int* jstats = reinterpret_cast<int*>(c->theta + p);
+    AVD_TRY(atb_fused<2>(c, c->Q, c->Y, c->W, c->theta, nullptr, &ctl->last_sweeps, nullptr, 40, &ctl->msw));
+    AVD_TRY(matpp(c, c->Y, c->Z, c->Z32, c->Q, c->U, nullptr, c->W));
+    resid_kernel<<<c->k, 256, 0, c->stream>>>(c->Z, c->U, c->theta, m, p, c->resid);
+    AVD_LAUNCHED(c);
+    ctl_rr_kernel<<<1, 32, 0, c->stream>>>(ctl, c->theta, c->resid, p, c->k, jstats, 0, 0);
+    AVD_LAUNCHED(c);
+    return AVD_OK;
+  };
+  auto pow_body = [&](bool after_rr) -> avd_status {
+    if (!after_rr) {  // Z = G Q (a check already made Z = G U on every rank)
+      AVD_CUDA(cudaMemsetAsync(c->Z32, 0, sizeof(float) * m * p, c->stream));
+      if (r1 > r0) AVD_TRY(gemm32(c, c->Q32, c->Z, c->Z32, nullptr, r0, r1));
+      AVD_TRY(exch(AVD_BUF_EIGZ, c->Z32, AVD_DT_F32));
+    }
+    AVD_TRY(rows_y([&]() { return gemm32(c, c->Z32, c->Y, nullptr, nullptr, r0, r1); }));  // Y = G Z
+    AVD_TRY(orth(c, c->Y, eig_seed(c), &ctl->it));
+    ctl_end_kernel<<<1, 32, 0, c->stream>>>(ctl);
+    AVD_LAUNCHED(c);
+    return AVD_OK;
+  };
+  AVD_TRY(eig_host_loop(c, rr_body, pow_body));
+  return eig_epilogue(c, false);
 }
 
 // Mean-bias diagnostics on the replicated G and mu (no exchange): power iteration on the uncentred

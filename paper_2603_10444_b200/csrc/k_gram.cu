@@ -499,6 +499,34 @@ avd_status gram_make_tmap(Ctx* c) {
   return AVD_OK;
 }
 
+namespace {
+// world > 1: the Gram's upper 128-tiles (A <= B; tile (A, B) sits at rows B, columns A of G_int,
+// element (a, b) at Gi[b][a]) packed in row-major upper-triangle order, so the exchange moves
+// T(T+1)/2 instead of T^2 tiles; unpack = the inverse copy after the all-reduce
+__global__ void __launch_bounds__(256) gram_pack_kernel(long long* __restrict__ Gi, int64_t m_pad, int T,
+                                                        long long* __restrict__ Gp, int unpack) {
+  const int t = blockIdx.x;
+  int A = 0, rem = t;
+  while (rem >= T - A) { rem -= T - A; ++A; }
+  const int B = A + rem;
+  long long* tile = Gi + (int64_t)B * 128 * m_pad + (int64_t)A * 128;
+  long long* pk = Gp + (int64_t)t * 128 * 128;
+  for (int e = threadIdx.x; e < 128 * 128; e += 256) {
+    const int r = e >> 7, cc = e & 127;
+    if (unpack) tile[(int64_t)r * m_pad + cc] = pk[e];
+    else pk[e] = tile[(int64_t)r * m_pad + cc];
+  }
+}
+}  // namespace
+
+avd_status launch_gram_pack(Ctx* c, bool unpack) {
+  const int T = (int)(c->m_pad / 128);
+  if (!c->gram_p) { set_error("packed Gram buffer needs world > 1"); return AVD_EINVAL; }
+  gram_pack_kernel<<<T * (T + 1) / 2, 256, 0, c->stream>>>(c->gram_i, c->m_pad, T, c->gram_p, unpack ? 1 : 0);
+  AVD_LAUNCHED(c);
+  return AVD_OK;
+}
+
 avd_status launch_gram(Ctx* c, const double* skip) {
   const int T = (int)(c->m_pad / 128);
   const int64_t NK = c->l_pad / 128;

@@ -8,10 +8,14 @@ module all-reduces exactly the exchange buffers the header lists (SURVEY.md §2.
   stats   : row-sample column sums + #rows (SUM f64), max (MAX), min (MIN), |x| histogram
             level 1 (SUM i64)  -> identical quantiser centre / scale and candidate bin everywhere
   split   : column sums + sum x^2 + counts (SUM f64), column range about the quantiser centre (MAX)
-  gram    : the exact int64 Gram partials and integer column sums of the quantised operand
-            (SUM i64)  -> identical exactly-centred G on every rank
-  eig     : replicated (same G, same seed -> bit-identical V_k, sigma_k on every rank); may ask
-            for a 3-digit Gram (AVD_EREPEAT) -> gram again, exchange GRAM, QSUM, QERR, eig again
+  gram    : the exact int64 Gram partials — their upper 128-tiles, packed (GRAMP) — and integer
+            column sums of the quantised operand (SUM i64)  -> identical exactly-centred G on
+            every rank
+  eig     : distributed: every G Q product of the subspace iteration is split by
+            row blocks over the ranks and all-gathered (EIGZ f32 / EIGY f64, SUM of zero-padded
+            blocks) through a callback the library calls; the p x p work is replicated (same G,
+            same seed -> identical V_k, sigma_k on every rank); may ask for a 3-digit Gram
+            (AVD_EREPEAT) -> gram again, exchange GRAMP, QSUM, QERR, eig again
   project : elementwise energy sums + column sums of P (SUM f64)
   gram    : + candidate count / overflow flag (SUM i64) -> same candidate-vs-stream decision
   select  : radix histograms of |x| bits (SUM i64), per-rank sel/tie counts (SUM = all-gather)
@@ -33,9 +37,11 @@ EXCHANGES = {
     "stats": [("SAMPLE", torch.float64, "sum"), ("SMAX", torch.float32, "max"),
               ("SMIN", torch.float32, "min"), ("HIST1", torch.int64, "sum")],
     "split": [("STATS", torch.float64, "sum"), ("COLMAX", torch.float32, "max"), ("DIAG", torch.float64, "sum")],
-    "gram": [("GRAM", torch.int64, "sum"), ("CAND", torch.int64, "sum"), ("QSUM", torch.int64, "sum"),
+    "gram": [("GRAMP", torch.int64, "sum"), ("CAND", torch.int64, "sum"), ("QSUM", torch.int64, "sum"),
              ("QERR", torch.float64, "sum")],
-    "regram": [("GRAM", torch.int64, "sum"), ("QSUM", torch.int64, "sum"), ("QERR", torch.float64, "sum")],
+    "regram": [("GRAMP", torch.int64, "sum"), ("QSUM", torch.int64, "sum"), ("QERR", torch.float64, "sum")],
+    # called back by the library from inside the distributed eigensolve
+    "eig": [("EIGZ", torch.float32, "sum"), ("EIGY", torch.float64, "sum")],
     "project": [("ENERGY", torch.float64, "sum")],
     "select0": [("HIST0", torch.int64, "sum")],
     "select1": [("HIST2", torch.int64, "sum")],
@@ -66,9 +72,36 @@ class TorchComm:
         dist.all_reduce(t, op=_OPS[op], group=self.group)
 
 
+class StageFailed(RuntimeError):
+    """A stage failed on some rank; every rank raises it (the first failing rank's message)."""
+
+
 def run_stages(backend, comm, X) -> object:
-    """The sharded pass: stage calls of `backend` interleaved with `comm` exchanges."""
+    """The sharded pass: stage calls of `backend` interleaved with `comm` exchanges.  With
+    world > 1 every stage is followed by a status all-reduce (MAX), so a stage that fails on one
+    rank (a CUDA error, AVD_ESTATE, ...) makes every rank raise instead of leaving the others
+    blocked in the next collective."""
     rank = comm.rank
+    status = None
+    if comm.world > 1:
+        dev = X.device if torch.is_tensor(X) else torch.device("cpu")
+        status = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def guarded(fn, *a):
+        if comm.world == 1:
+            return fn(*a)
+        err, res = None, None
+        try:
+            res = fn(*a)
+        except Exception as e:  # noqa: BLE001 - re-raised below on every rank
+            err = e
+        status.fill_(0 if err is None else 1)
+        comm.all_reduce(status, "max")
+        if err is not None:
+            raise err
+        if int(status.item()) != 0:
+            raise StageFailed(f"{getattr(fn, '__name__', 'stage')} failed on another rank")
+        return res
 
     def exchange(stage):
         if comm.world == 1:
@@ -76,26 +109,36 @@ def run_stages(backend, comm, X) -> object:
         for name, dtype, op in EXCHANGES[stage]:
             comm.all_reduce(backend.exchange_buffer(name, dtype), op)
 
-    backend.stage_stats(X)
+    guarded(backend.stage_stats, X)
     exchange("stats")
-    backend.stage_split(X)
+    guarded(backend.stage_split, X)
     exchange("split")
-    backend.stage_gram(X)
+    guarded(backend.stage_gram, X)
     exchange("gram")
-    if backend.stage_eig() == L.AVD_EREPEAT:
+
+    def eig():
+        if comm.world == 1:
+            return backend.stage_eig()
+        dtypes = {name: dt for name, dt, _ in EXCHANGES["eig"]}
+
+        def eig_exchange(name):  # the library's all-gather of a row-split product
+            comm.all_reduce(backend.exchange_buffer(name, dtypes[name]), "sum")
+        return backend.stage_eig_dist(rank, eig_exchange)
+
+    if guarded(eig) == L.AVD_EREPEAT:
         # automatic digits: the replicated precision bound raised the Gram operand to 3 digits
         # on every rank alike; redo the Gram (the candidate count is already global)
-        backend.stage_gram(X)
+        guarded(backend.stage_gram, X)
         exchange("regram")
-        backend.stage_eig()
-    backend.stage_project(X)
+        guarded(eig)
+    guarded(backend.stage_project, X)
     exchange("project")
     for lv in range(4):
-        backend.stage_select(X, lv, rank)
+        guarded(backend.stage_select, X, lv, rank)
         exchange(f"select{lv}")
-    backend.stage_gather(X, rank)
+    guarded(backend.stage_gather, X, rank)
     exchange("gather")
-    return backend.stage_report()
+    return guarded(backend.stage_report)
 
 
 class _LibBackend:
@@ -123,6 +166,19 @@ class _LibBackend:
 
     def stage_eig(self):
         self.eig_status = L.avd_stage_eig(self.h)
+        return self.eig_status
+
+    def stage_eig_dist(self, rank, exchange):
+        """exchange(name): all-reduce (SUM) the named exchange buffer over the ranks; the library
+        calls it back (through an avd_exchange_fn) from inside the distributed eigensolve."""
+        def cb(which, ptr, dtype, op, count, user):
+            try:
+                exchange(L.BUF_NAME[which])
+                return 0
+            except Exception:  # noqa: BLE001 - reported to the library as AVD_EEXCHANGE
+                return 1
+        fn = L.EXCHANGE_FN(cb)  # kept alive for the duration of the call
+        self.eig_status = L.avd_stage_eig_dist(self.h, rank, fn, None)
         return self.eig_status
 
     def stage_project(self, X):

@@ -79,12 +79,46 @@ class ModelBackend:
         self.mu = st[: self.m] / self.l
         self.n_eff = int(min(self.n_top, st[self.m + 2]))
         self.Xc = self.X.astype(np.float64) - self.mu
-        self.buf["GRAM"] = torch.tensor(self.Xc.T @ self.Xc)
+        self.buf["GRAMP"] = torch.tensor(self.Xc.T @ self.Xc)  # (the model keeps it unpacked)
         self.buf["QSUM"] = torch.zeros(2 * self.m, dtype=torch.int64)
         self.buf["QERR"] = torch.zeros(self.m, dtype=torch.float64)
 
+    def stage_eig_dist(self, rank, exchange):
+        """Model of avd_stage_eig_dist: block power iterations whose G Q products are split by
+        row blocks over the ranks, each rank's rows written into a zero-padded m x p block that
+        `exchange` all-reduces (EIGZ in fp32, EIGY in fp64, like the library), then Rayleigh-Ritz
+        on the replicated orthonormal basis."""
+        G = self.buf["GRAMP"].numpy()
+        m, p = self.m, self.k + 6
+        r0, r1 = m * rank // self.world, m * (rank + 1) // self.world
+        Q = np.linalg.qr(np.random.default_rng(7).standard_normal((m, p)))[0]
+        for _ in range(60):
+            Z = np.zeros((m, p), np.float32)
+            Z[r0:r1] = G[r0:r1] @ Q
+            self.buf["EIGZ"] = torch.tensor(Z)
+            exchange("EIGZ")
+            Z = self.buf["EIGZ"].numpy().astype(np.float64)
+            Y = np.zeros((m, p))
+            Y[r0:r1] = G[r0:r1] @ Z
+            self.buf["EIGY"] = torch.tensor(Y)
+            exchange("EIGY")
+            Q = np.linalg.qr(self.buf["EIGY"].numpy())[0]
+        Y = np.zeros((m, p))
+        Y[r0:r1] = G[r0:r1] @ Q
+        self.buf["EIGY"] = torch.tensor(Y)
+        exchange("EIGY")
+        H = Q.T @ self.buf["EIGY"].numpy()
+        th, W = np.linalg.eigh(0.5 * (H + H.T))
+        U = Q @ W[:, ::-1][:, : self.k]
+        for r in range(self.k):
+            j = np.argmax(np.abs(U[:, r]))
+            if U[j, r] < 0:
+                U[:, r] *= -1
+        self.V, self.sigma = U, np.sqrt(np.maximum(th[::-1][: self.k], 0))
+        return 0
+
     def stage_eig(self):
-        lam, W = np.linalg.eigh(self.buf["GRAM"].numpy())  # the exchanged (global) Gram
+        lam, W = np.linalg.eigh(self.buf["GRAMP"].numpy())  # the exchanged (global) Gram
         lam, W = lam[::-1][: self.k], W[:, ::-1][:, : self.k]
         for r in range(self.k):
             j = np.argmax(np.abs(W[:, r]))
@@ -228,3 +262,35 @@ def test_gram_allreduce_is_exact():
     p1, t1 = out[1]
     np.testing.assert_array_equal(t0, t1)
     np.testing.assert_array_equal(t0, p0 + p1)
+
+
+class _FailingBackend(ModelBackend):
+    def stage_split(self, X):
+        if self.rank == 1:
+            raise RuntimeError("injected failure on rank 1")
+        return super().stage_split(X)
+
+
+def _fail_worker(rank, world, port, X, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2603_10444_b200.distributed import TorchComm, run_stages, shard_rows
+    r0, lr = shard_rows(X.shape[0], world, rank)
+    be = _FailingBackend(X.shape[0], X.shape[1], 2, 32, r0, world, rank)
+    try:
+        run_stages(be, TorchComm(), X[r0:r0 + lr])
+        out[rank] = "no error"
+    except Exception as e:  # noqa: BLE001
+        out[rank] = type(e).__name__ + ": " + str(e)
+    dist.destroy_process_group()
+
+
+def test_stage_failure_reaches_every_rank():
+    """a stage failing on one rank makes every rank raise (status all-reduce after each
+    stage) instead of leaving the others blocked in the next collective."""
+    X = generate(SynthSpec(512, 64, seed=3, k_s=2, f_mean=0.8)).numpy()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_fail_worker, args=(2, _free_port(), X, out), nprocs=2, join=True)
+    assert out[1].startswith("RuntimeError: injected failure")
+    assert out[0].startswith("StageFailed")
