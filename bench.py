@@ -27,13 +27,15 @@ import torch
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from synth.gen import config_spec, generate  # noqa: E402
+from synth.gen import config_spec, generate, sweep_specs  # noqa: E402
 
 METRIC = "activation entries decomposed/sec (l*m/s)"
 UNIT = "entries/s"
 WORKLOADS = {
     "c1": "c1: single matrix l=512, m=256 (k=2, |E_top|=131)",
     "c2": "c2: single layer l=8192, m=2048 (k=20)",
+    "c3": "c3: 29-module sweep (embedding + 28 layers) x early/late mean-bias strength = 58 matrices "
+          "of l=32768, m=2048 (k=20)",
     "c4": "c4: single matrix l=131072, m=4096 (k=40), row-sharded over the GPUs",
     "c5": "c5: single matrix l=1048576, m=8192 (k=81), row-sharded over the GPUs",
 }
@@ -210,6 +212,119 @@ def plant_massive(X, row0, m):
             X[i - row0, j] = v
 
 
+# ------------------------------------------------------------------ c3: the 58-matrix sweep
+def run_c3(args, rank, world, local):
+    """BASELINE.json configs[2]: one step = the whole pass over each of the 58 matrices of the
+    sweep (synth.gen.sweep_specs).  Two contexts on two CUDA streams, each
+    driven by its own host thread (the C calls release the GIL), so matrix i+1's fused pass /
+    Gram run while matrix i is in its eigensolve.  N > 1: the matrices are dealt round-robin to
+    the ranks (independent problems, no collective)."""
+    import torch.distributed as dist
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_2603_10444_b200.api import Decomposer
+    specs = sweep_specs(0)
+    mine = [i for i in range(len(specs)) if i % world == rank]
+    l, m = specs[0].l, specs[0].m
+    Xs = [generate(specs[i], device="cuda") for i in mine]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    decs = [Decomposer(l, m, seed=0, stream=st) for st in streams]
+
+    def worker(w, mats, host=None):
+        out = []
+        with torch.cuda.stream(streams[w]):
+            for j in range(w, len(mats), 2):
+                out.append(decs[w](mats[j]) if host is None else decs[w].run_host(host[j]))
+        return out
+
+    pool = ThreadPoolExecutor(2)
+
+    def step(mats, host=None):
+        fut = [pool.submit(worker, w, mats, host) for w in range(2)]
+        return [r for f in fut for r in f.result()]
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    for _ in range(args.warmup):
+        res = step(Xs)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.15)
+    l0 = sum(d.launches() for d in decs)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(streams[0])
+    streams[1].wait_event(ev0)
+    for _ in range(args.steps):
+        res = step(Xs)
+    ev_b = torch.cuda.Event()
+    ev_b.record(streams[1])
+    streams[0].wait_event(ev_b)
+    ev1.record(streams[0])
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    launches = sum(d.launches() for d in decs) - l0
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    n_all = len(specs)
+    entries = n_all * l * m
+    bad = [f"matrix {mine[i]}: status {r.status}, residual {r.max_resid}" for i, r in enumerate(res)
+           if r.status != 0 or not (r.max_resid <= 1e-6)]
+    # e2e: host buffers through avd_decompose_host (H2D of X and D2H of the results inside), on
+    # the first 8 of this rank's matrices, both threads
+    ne = min(8, len(Xs))
+    Xh = [x.cpu().pin_memory() for x in Xs[:ne]]
+    step(Xs[:ne], Xh)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(max(1, args.e2e_steps)):
+        step(Xs[:ne], Xh)
+    torch.cuda.synchronize()
+    e_ms = (time.perf_counter() - t0) * 1e3 / max(1, args.e2e_steps)
+    k = decs[0].k
+    d2h = ne * (8 * (m + m * k + k) + 40 * decs[0].n_top)
+    line = {
+        "metric": METRIC, "value": entries / (ms_step * 1e-3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "i8/i32 Gram + f64 eig + i8/f32 projection", "data":
+            "synthetic (synth/gen.py sweep_specs: 29 modules x early/late, invented monotone schedule)",
+        "matrices_per_s": n_all / (ms_step * 1e-3),
+        "config": {"workload": WORKLOADS["c3"], "matrices": n_all, "l": l, "m": m, "k": k,
+                   "streams": 2, "l2": "each matrix (268 MB) is larger than L2; no flush",
+                   "parallelism": f"matrices dealt round-robin to {world} rank(s)"},
+        "clocks": clocks, "gpu_launches": int(launches),
+        "e2e": {"value": ne * l * m / (e_ms * 1e-3), "unit": UNIT, "matrices_per_s": ne / (e_ms * 1e-3),
+                "h2d_bytes_per_step": ne * l * m * 4, "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms,
+                "sample": f"the first {ne} matrices of this rank, pinned host buffers"},
+        "eig_iters": [r.iters for r in res[:4]], "digits_used": sorted({r.digits_used for r in res}),
+    }
+    if bad:
+        line["invalid"] = "; ".join(bad[:4])
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(specs[0], min(l, 8192), args.cpu_baseline_eig)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    for d in decs:
+        d.close()
+    pool.shutdown()
+    if world > 1:
+        dist.destroy_process_group()
+    if bad:
+        print("bench: INVALID run: " + "; ".join(bad[:4]), file=sys.stderr)
+        sys.exit(3)
+
+
 # ------------------------------------------------------------------ main
 def main():
     ap = argparse.ArgumentParser()
@@ -242,6 +357,9 @@ def main():
     import torch.distributed as dist
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.config == "c3":
+        run_c3(args, rank, world, local)
+        return
     from paper_2603_10444_b200.distributed import ShardedDecomposer, TorchComm, _LibBackend, run_stages, shard_rows
     from paper_2603_10444_b200.api import Decomposer
 

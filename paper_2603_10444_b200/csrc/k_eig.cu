@@ -1118,11 +1118,19 @@ __global__ void ctl_u_kernel(EigCtl* ctl, const double* __restrict__ diag, cudaG
 // ONE wave of resident CTAs (3 fp32 / 2 fp64 CTAs per SM, smem-bound) — a partial second wave
 // would double the kernel's time
 void gemm_geometry(int64_t m, int64_t m_pad, int p, int num_sms, bool fp32, int* BM, int* KS, int* RB, int* KT) {
-  *BM = (fp32 && p <= 64) ? 128 : 64;  // = 16 * NR of the gemm32 / gemm64 instantiations
-  *RB = (int)(m_pad / *BM);
   *KT = (int)ceil_div(m, kSkBK);
   const int64_t want = (int64_t)num_sms * (fp32 ? 3 : 2);  // resident CTAs (smem-bound)
-  *KS = (int)std::max<int64_t>(1, std::min<int64_t>(want / *RB, *KT));
+  // the largest row block (register tile) that still leaves every CTA >= 8 K tiles of work:
+  // small m (c1, c2) takes 32-row blocks so the grid fills without slivers of K per CTA
+  const int big = (fp32 && p <= 64) ? 128 : 64;
+  *BM = big;
+  for (int bm = big; bm >= 32; bm /= 2) {
+    *BM = bm;
+    const int64_t rb = m_pad / bm;
+    if (std::min<int64_t>(want / rb, *KT) * 8 <= *KT || want / rb < 1) break;
+  }
+  *RB = (int)(m_pad / *BM);
+  *KS = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(want / *RB, *KT), std::max<int64_t>(1, *KT / 8)));
 }
 size_t gemm_part_bytes(int64_t m, int64_t m_pad, int p, int num_sms) {
   size_t best = 0;
@@ -1133,7 +1141,7 @@ size_t gemm_part_bytes(int64_t m, int64_t m_pad, int p, int num_sms) {
     best = std::max(best, (size_t)std::max<int64_t>(want, (int64_t)RB * KS) * BM * p *
                               (f == 0 ? sizeof(float) : sizeof(double)));
   }
-  return (size_t)round_up((int64_t)best, 256) + sizeof(unsigned) * (size_t)(m_pad / 64 + 1);  // partials + tickets
+  return (size_t)round_up((int64_t)best, 256) + sizeof(unsigned) * (size_t)(m_pad / 32 + 1);  // partials + tickets
 }
 
 namespace {
@@ -1159,16 +1167,25 @@ avd_status gemm_launch(Ctx* c, const T* Gm, const T* In, double* Y, float* Y32, 
   const size_t pb = gemm_part_bytes(c->cfg.m, c->m_pad, c->p, c->num_sms);
   T* part = reinterpret_cast<T*>(c->gemm_part);
   unsigned* tickets = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(c->gemm_part) + pb -
-                                                  sizeof(unsigned) * (size_t)(c->m_pad / 64 + 1));
+                                                  sizeof(unsigned) * (size_t)(c->m_pad / 32 + 1));
   gemm_kernel<T, NR, NC><<<RB * KS, kSkThreads, sm, c->stream>>>(Gm, c->m_pad, In, c->cfg.m, KT, KS, part, tickets, Y,
                                                                  Y32, skip, rb0);
   AVD_LAUNCHED(c);
   return AVD_OK;
 }
 
+int gemm_bm(const Ctx* c, bool fp32) {
+  int BM, KS, RB, KT;
+  gemm_geometry(c->cfg.m, c->m_pad, c->p, c->num_sms, fp32, &BM, &KS, &RB, &KT);
+  return BM;
+}
 avd_status gemm64(Ctx* c, const double* In, double* Y, float* Y32, int64_t r0 = 0, int64_t r1 = 0) {
+  const int bm = gemm_bm(c, false);
   switch (c->p / 16) {
-#define CASE(PC) case PC: return gemm_launch<double, 4, 2 * PC>(c, c->G, In, Y, Y32, nullptr, r0, r1);
+#define CASE(PC)                                                                                        \
+  case PC:                                                                                              \
+    return bm == 64 ? gemm_launch<double, 4, 2 * PC>(c, c->G, In, Y, Y32, nullptr, r0, r1)                \
+                    : gemm_launch<double, 2, 2 * PC>(c, c->G, In, Y, Y32, nullptr, r0, r1);
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
   }
@@ -1177,8 +1194,13 @@ avd_status gemm64(Ctx* c, const double* In, double* Y, float* Y32, int64_t r0 = 
 }
 avd_status gemm32(Ctx* c, const float* In, double* Y, float* Y32, const int* skip = nullptr, int64_t r0 = 0,
                   int64_t r1 = 0) {
+  const int bm = gemm_bm(c, true);
   switch (c->p / 16) {
-#define CASE(PC) case PC: return gemm_launch<float, (PC <= 4 ? 8 : 4), 2 * PC>(c, c->G32, In, Y, Y32, skip, r0, r1);
+#define CASE(PC)                                                                                        \
+  case PC:                                                                                              \
+    if (bm == 128 && PC <= 4) return gemm_launch<float, 8, 2 * PC>(c, c->G32, In, Y, Y32, skip, r0, r1);   \
+    if (bm == 64) return gemm_launch<float, 4, 2 * PC>(c, c->G32, In, Y, Y32, skip, r0, r1);                \
+    return gemm_launch<float, 2, 2 * PC>(c, c->G32, In, Y, Y32, skip, r0, r1);
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
   }
@@ -1485,7 +1507,7 @@ avd_status eig_prologue(Ctx* c) {
   AVD_CUDA(cudaMemsetAsync(jstats, 0, 16 * sizeof(int), c->stream));
   AVD_CUDA(cudaMemsetAsync(c->ticket, 0, sizeof(unsigned), c->stream));
   {  // split-K tickets (re-armed by every launch; cleared here once per solve)
-    const size_t pb = gemm_part_bytes(m, c->m_pad, p, c->num_sms), tb = sizeof(unsigned) * (size_t)(c->m_pad / 64 + 1);
+    const size_t pb = gemm_part_bytes(m, c->m_pad, p, c->num_sms), tb = sizeof(unsigned) * (size_t)(c->m_pad / 32 + 1);
     AVD_CUDA(cudaMemsetAsync(reinterpret_cast<char*>(c->gemm_part) + pb - tb, 0, tb, c->stream));
   }
   ctl_init_kernel<<<1, 32, 0, c->stream>>>(ctl, max_it, tol, k, p);

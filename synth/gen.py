@@ -192,6 +192,8 @@ def config_spec(name: str, seed: int = 0) -> SynthSpec:
         return SynthSpec(512, 256, seed=seed, f_mean=0.9)
     if name == "c2":
         return SynthSpec(8192, 2048, seed=seed, f_mean=0.9)
+    if name == "c3":  # the first matrix of the 58-matrix sweep (embedding, early); see sweep_specs
+        return sweep_specs(seed)[0]
     if name == "c4":
         return SynthSpec(131072, 4096, seed=seed, f_mean=0.9)
     if name == "c5":
