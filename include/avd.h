@@ -98,6 +98,10 @@ typedef struct {
 /* avd_config.flags (tests): with automatic digits, take the 3-digit escalation (AVD_EREPEAT and
  * the re-encoded Gram) whatever the precision bound says                                      */
 #define AVD_FLAG_FORCE_ESCALATE 4
+/* avd_config.flags (tests / profiling): run the eigensolver's loop from the host, one kernel
+ * launch and one synchronisation per decision, instead of the device-resident CUDA graph (the
+ * same kernels in the same order: bit-identical results; env AVD_EIG_NOGRAPH=1 does the same)  */
+#define AVD_FLAG_EIG_HOST_LOOP 8
 
 /* Outputs.  Device arrays caller-owned, sized from the plan (cap = n_top). */
 typedef struct {

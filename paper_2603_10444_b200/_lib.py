@@ -11,7 +11,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libavd.so")
 
-AVD_FLAG_STREAM_SELECT, AVD_FLAG_EXACT_SCALE, AVD_FLAG_FORCE_ESCALATE = 1, 2, 4
+AVD_FLAG_STREAM_SELECT, AVD_FLAG_EXACT_SCALE, AVD_FLAG_FORCE_ESCALATE, AVD_FLAG_EIG_HOST_LOOP = 1, 2, 4, 8
 AVD_OK, AVD_EINVAL, AVD_ENONFINITE, AVD_ENOCONV, AVD_ECUDA, AVD_ENOMEM, AVD_ESTATE = 0, 1, 2, 3, 4, 6, 8
 AVD_EREPEAT, AVD_EEXCHANGE = 9, 10
 BUF = dict(STATS=0, COLMAX=1, COLMIN=2, HIST1=3, GRAM=4, ENERGY=5, HIST2=6, HIST3=7, TIES=8, AGG=9,

@@ -1425,14 +1425,16 @@ avd_status build_unc_graph(Ctx* c) {
 
 // AVD_EIG_NOGRAPH=1: the same loop bodies launched one by one by the host with a synchronisation
 // per decision (profiling: ncu sees every kernel; numerically identical)
-bool eig_nograph() {
+bool eig_nograph_env() {
   static const bool v = [] { const char* e = std::getenv("AVD_EIG_NOGRAPH"); return e && e[0] == '1'; }();
   return v;
 }
 
+bool eig_nograph(const Ctx* c) { return eig_nograph_env() || (c->cfg.flags & AVD_FLAG_EIG_HOST_LOOP) != 0; }
+
 avd_status ensure_graphs(Ctx* c) {
   if (!c->side_stream) AVD_CUDA(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
-  if (c->eig_exec || eig_nograph()) return AVD_OK;
+  if (c->eig_exec || eig_nograph(c)) return AVD_OK;
   if (!c->cap_stream) AVD_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
   if (!c->ev_fork) AVD_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   if (!c->ev_join) AVD_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
@@ -1584,7 +1586,7 @@ avd_status eig_host_loop(Ctx* c, RR&& rr_body, POW&& pow_body) {
 avd_status run_eig(Ctx* c) {
   AVD_TRY(ensure_graphs(c));
   AVD_TRY(eig_prologue(c));
-  const bool nograph = eig_nograph();
+  const bool nograph = eig_nograph(c);
   if (nograph) {
     AVD_TRY(eig_host_loop(c, [&]() { return enqueue_rr(c, 0, 0); }, [&](bool) { return enqueue_pow(c); }));
   } else {
@@ -1660,7 +1662,7 @@ avd_status run_eig_dist(Ctx* c, int rank, avd_exchange_fn fn, void* user) {
 // PAPER.md:559-561), cos_mu_v1 = alpha1 / ||mu||.
 avd_status launch_uncentred(Ctx* c) {
   AVD_TRY(ensure_graphs(c));
-  if (eig_nograph()) {
+  if (eig_nograph(c)) {
     EigCtl* ctl = reinterpret_cast<EigCtl*>(c->eig_ctl);
     EigCtl* hc = reinterpret_cast<EigCtl*>(c->eig_host + 6 * kMaxP);
     ctl_u_init_kernel<<<1, 32, 0, c->stream>>>(ctl);
@@ -1676,21 +1678,24 @@ avd_status launch_uncentred(Ctx* c) {
     c->launches -= (int64_t)c->n_u_nodes * hc->blocks_u;  // the report adds them for the graph mode
     return AVD_OK;
   }
+  // AVD_UNC_SERIAL=1 (diagnostics): the uncentred loop on the context's own stream
+  static const bool serial = [] { const char* e = std::getenv("AVD_UNC_SERIAL"); return e && e[0] == '1'; }();
+  cudaStream_t side = serial ? c->stream : c->side_stream;
   AVD_CUDA(cudaEventRecord(c->ev_fork, c->stream));
-  AVD_CUDA(cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
+  AVD_CUDA(cudaStreamWaitEvent(side, c->ev_fork, 0));
   cudaStream_t user = c->stream;
-  c->stream = c->side_stream;
+  c->stream = side;
   ctl_u_init_kernel<<<1, 32, 0, c->stream>>>(reinterpret_cast<EigCtl*>(c->eig_ctl));
   mu_norm_kernel<<<1, 256, 0, c->stream>>>(c->mu, c->cfg.m, c->m_pad, c->diag);
   c->stream = user;
   AVD_LAUNCHED(c);
   AVD_LAUNCHED(c);
-  AVD_CUDA(cudaGraphLaunch(c->unc_exec, c->side_stream));
-  AVD_CUDA(cudaEventRecord(c->ev_join, c->side_stream));
+  AVD_CUDA(cudaGraphLaunch(c->unc_exec, side));
+  AVD_CUDA(cudaEventRecord(c->ev_join, side));
   return AVD_OK;
 }
 avd_status join_uncentred(Ctx* c) {
-  if (eig_nograph()) return AVD_OK;
+  if (eig_nograph(c)) return AVD_OK;
   AVD_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
   return AVD_OK;
 }
