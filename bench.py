@@ -495,7 +495,9 @@ def main():
     streams = {
         "row sample (K1s, 1/%d of the rows)" % samp: (lloc * m * 4 // samp, lloc * m * 4 // samp, stage_ms.get("stats")),
         "fused pass (K1+K2: read X 4 B; writes nd digit bytes)": (lloc * m * 4, lloc * m * (4 + nd), stage_ms.get("split")),
-        "project+energy (K5/K8: read X twice)": (2 * lloc * m * 4, 2 * lloc * m * 4, stage_ms.get("project")),
+        # K5 reads the nd digit planes of the Gram operand, K8 reads X
+        "project+energy (K5/K8: two passes over X; K5 reads the digit planes)": (2 * lloc * m * 4, lloc * m * (nd + 4),
+                                                                               stage_ms.get("project")),
     }
     stream_roof = {k: {"alg_GB/s": a / (t * 1e-3) / 1e9, "frac_hbm": a / (t * 1e-3) / 1e9 / hbm,
                        "exec_GB/s": b / (t * 1e-3) / 1e9, "exec_frac_hbm": b / (t * 1e-3) / 1e9 / hbm}
