@@ -222,7 +222,7 @@ typedef enum {
   AVD_BUF_DIAG = 22,
   AVD_BUF_GRAMP = 25,  /* the Gram's upper 128-tiles, packed (i64, SUM): what world > 1 exchanges
                           after avd_stage_gram (half the bytes of AVD_BUF_GRAM)               */
-  AVD_BUF_EIGZ = 23,   /* distributed eigensolve: Z = G Q, m x p f32 (SUM of row blocks)     */
+  AVD_BUF_EIGZ = 23,   /* distributed eigensolve: Z = G Q, m x p f64 (SUM of row blocks)     */
   AVD_BUF_EIGY = 24,   /* distributed eigensolve: Y = G Z or G Q, m x p f64 (SUM of row blocks) */
   /* read-only views for tests / diagnostics (not exchanged) */
   AVD_BUF_MU = 16, AVD_BUF_G = 17, AVD_BUF_P = 18, AVD_BUF_DIGITS = 19, AVD_BUF_SCALE = 20
@@ -253,7 +253,7 @@ typedef int (*avd_exchange_fn)(int32_t which, void* buf_dev, int32_t dtype, int3
 
 /* Distributed eigensolve: avd_stage_eig with every G Q product split by row
  * blocks over the ranks (rank r computes rows [r0, r1) of its share of the 128-row blocks); the
- * zero-padded products are exchanged through fn as SUMs (AVD_BUF_EIGZ, f32; AVD_BUF_EIGY, f64 —
+ * zero-padded products are exchanged through fn as SUMs (AVD_BUF_EIGZ, AVD_BUF_EIGY, both f64 —
  * i.e. all-gathers), twice per power step and once per Rayleigh-Ritz check; the p x p work is
  * replicated.  Same results as avd_stage_eig up to the row blocking of the GEMM partial sums.
  * world == 1 or fn == NULL: exactly avd_stage_eig.  May return AVD_EREPEAT like avd_stage_eig. */

@@ -181,6 +181,13 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
     const int64_t T = C->m_pad / 128;
     L.add(world > 1 ? sizeof(long long) * (size_t)(T * (T + 1) / 2) * 128 * 128 : 0);  // 73 gram_p
   }
+  L.add((size_t)4 * C->m_pad * C->m_pad);                               // 74 gd
+  L.add(sizeof(double) * C->m_pad);                                      // 75 gsc
+  L.add((size_t)3 * kMaxP * C->m_pad);                                   // 76 qd
+  L.add(sizeof(double) * kMaxP);                                         // 77 qsc
+  L.add(gemm_i8_part_bytes(C->m_pad, (int)p, C->num_sms));               // 78 g8_part
+  L.add(sizeof(unsigned) * (size_t)(C->m_pad / 128 + 1));                // 79 g8_tickets
+  L.add(2 * sizeof(CUtensorMap));                                        // 80 tm_dev
   if (L.n >= 128) { set_error("workspace layout table overflow"); return AVD_EINVAL; }
   plan->workspace_bytes = L.total;
   if (lay) *lay = L;
@@ -350,6 +357,8 @@ avd_status avd_create(const avd_config* cfg, avd_ctx** out) {
   BIND(qsum_part, long long*); BIND(qsum_local, long long*); BIND(qerr_part, float*); BIND(qerr_local, double*);
   BIND(qerr, double*); BIND(mu0, float*); BIND(qsq_part, long long*); BIND(diag, double*);
   BIND(prec, double*); BIND(ysq, double*); BIND(eig_ctl, void*); BIND(wsc, double*); BIND(gram_p, long long*);
+  BIND(gd, int8_t*); BIND(gsc, double*); BIND(qd, int8_t*); BIND(qsc, double*); BIND(g8_part, double*);
+  BIND(g8_tickets, unsigned*); BIND(tm_dev, CUtensorMap*);
   if (c->cfg.world <= 1) c->gram_p = nullptr;
 #undef BIND
   if (cudaMallocHost(&c->eig_host, sizeof(double) * kHostScratch) != cudaSuccess) {
@@ -368,6 +377,7 @@ avd_status avd_create(const avd_config* cfg, avd_ctx** out) {
     return AVD_ECUDA;
   }
   cudaMemset(c->P_hl, 0, sizeof(float) * 2 * c->l_pad * (((c->k_pad + 31) / 32) * 32));
+  cudaMemset(c->g8_tickets, 0, sizeof(unsigned) * (size_t)(c->m_pad / 128 + 1));
   st = gram_make_tmap(c);
   if (st != AVD_OK) { cudaFree(c->ws); cudaFreeHost(c->eig_host); cudaEventDestroy(c->ev_host); delete c; return st; }
   c->stage = 0;
@@ -444,7 +454,7 @@ avd_status avd_buffer(avd_ctx* c, int32_t which, void** ptr, size_t* bytes) {
       *bytes = sizeof(long long) * (size_t)(T * (T + 1) / 2) * 128 * 128;
       break;
     }
-    case AVD_BUF_EIGZ: *ptr = c->Z32; *bytes = sizeof(float) * m * c->p; break;
+    case AVD_BUF_EIGZ: *ptr = c->Z; *bytes = sizeof(double) * m * c->p; break;
     case AVD_BUF_EIGY: *ptr = c->Y; *bytes = sizeof(double) * m * c->p; break;
     default: set_error("unknown buffer id"); return AVD_EINVAL;
   }

@@ -113,6 +113,15 @@ struct Ctx {
   unsigned* ticket = nullptr;     // last-CTA ticket of the fused reductions
   double* gmax = nullptr;         // max |G| (fixed-point scale of the Y = G Q accumulation)
   void* eig_ctl = nullptr;        // [kEigCtlBytes] loop state of the eigensolver graph
+  int8_t* gd = nullptr;           // [4][m_pad][m_pad] G in balanced base-128 digits (k_eig_i8.cu)
+  double* gsc = nullptr;          // [m_pad] row scales of gd
+  int8_t* qd = nullptr;           // [3][p][m_pad] the product's input block in digits (transposed)
+  double* qsc = nullptr;          // [kMaxP] its column scales
+  double* g8_part = nullptr;      // split-K partials of the int8 products
+  unsigned* g8_tickets = nullptr; // [m_pad / 128] last-CTA tickets
+  CUtensorMap tm_gd{}, tm_qd{};
+  CUtensorMap* tm_dev = nullptr;  // [2] device copies of tm_gd, tm_qd (64-B aligned; graph kernels read them)
+  bool tm_gd_ready = false;
   cudaGraphExec_t eig_exec = nullptr;   // subspace-iteration loop (built once per context)
   cudaGraphExec_t unc_exec = nullptr;   // uncentred power iteration loop (diagnostics)
   cudaStream_t cap_stream = nullptr;    // private stream the graphs are captured on
@@ -220,6 +229,10 @@ avd_status launch_gram_finalize(Ctx* c);                   // k_eig.cu
 avd_status run_eig(Ctx* c);                                // k_eig.cu
 avd_status run_eig_dist(Ctx* c, int rank, avd_exchange_fn fn, void* user);  // k_eig.cu
 avd_status launch_gram_pack(Ctx* c, bool unpack);          // k_gram.cu (world > 1 exchange)
+bool eig_i8_enabled(const Ctx* c);                         // k_eig_i8.cu
+avd_status eig_i8_prepare(Ctx* c);                         // k_eig_i8.cu (once per solve)
+avd_status gemm_i8(Ctx* c, const double* In, double* Y, float* Y32, const int* skip, int64_t r0, int64_t r1);
+size_t gemm_i8_part_bytes(int64_t m_pad, int p, int num_sms);
 void gemm_geometry(int64_t m, int64_t m_pad, int p, int num_sms, bool fp32, int* BM, int* KS, int* RB, int* KT);
 size_t gemm_part_bytes(int64_t m, int64_t m_pad, int p, int num_sms);
 avd_status launch_project(Ctx* c, const float* X);         // k_project.cu

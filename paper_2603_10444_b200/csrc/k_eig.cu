@@ -995,6 +995,11 @@ __global__ void power_u_stats_kernel(const double* __restrict__ mu, int64_t m, c
   }
 }
 
+__global__ void f64_to_f32_kernel(const double* __restrict__ a, float* __restrict__ b, int64_t n) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) b[t] = (float)a[t];
+}
+
 // ---------------------------------------------------------------- device-resident loop control
 // The subspace iteration runs as ONE CUDA graph: WHILE(loop) { begin; IF(rr) {RR check; ctl_rr};
 // IF(pow) {power step; orth; ctl_end} } — every decision the host used to take between launches
@@ -1337,8 +1342,13 @@ avd_status enqueue_rr(Ctx* c, cudaGraphConditionalHandle h_loop, cudaGraphCondit
 }
 avd_status enqueue_pow(Ctx* c) {
   EigCtl* ctl = reinterpret_cast<EigCtl*>(c->eig_ctl);
-  AVD_TRY(gemm32(c, c->Q32, c->Z, c->Z32, &ctl->rr_now));  // Z = G Q (a check already made Z = G U)
-  AVD_TRY(gemm32(c, c->Z32, c->Y, nullptr));                // Y = G Z = G^2 Q
+  if (eig_i8_enabled(c)) {  // int8 tensor-core products (k_eig_i8.cu)
+    AVD_TRY(gemm_i8(c, c->Q, c->Z, c->Z32, &ctl->rr_now, 0, 0));  // Z = G Q (a check already made Z = G U)
+    AVD_TRY(gemm_i8(c, c->Z, c->Y, nullptr, nullptr, 0, 0));       // Y = G Z = G^2 Q
+  } else {
+    AVD_TRY(gemm32(c, c->Q32, c->Z, c->Z32, &ctl->rr_now));  // Z = G Q (a check already made Z = G U)
+    AVD_TRY(gemm32(c, c->Z32, c->Y, nullptr));                // Y = G Z = G^2 Q
+  }
   AVD_TRY(orth(c, c->Y, eig_seed(c), &ctl->it));
   ctl_end_kernel<<<1, 32, 0, c->stream>>>(ctl);
   AVD_LAUNCHED(c);
@@ -1514,6 +1524,7 @@ avd_status eig_prologue(Ctx* c) {
   }
   ctl_init_kernel<<<1, 32, 0, c->stream>>>(ctl, max_it, tol, k, p);
   AVD_LAUNCHED(c);
+  if (eig_i8_enabled(c)) AVD_TRY(eig_i8_prepare(c));  // G in digits for the power steps
   rand_fill_kernel<<<(unsigned)ceil_div(m * p, 256), 256, 0, c->stream>>>(c->Z, nullptr, m, p, seed, nullptr, nullptr);
   AVD_LAUNCHED(c);
   return orth(c, c->Z, seed + 1, nullptr);
@@ -1637,13 +1648,23 @@ avd_status run_eig_dist(Ctx* c, int rank, avd_exchange_fn fn, void* user) {
     AVD_LAUNCHED(c);
     return AVD_OK;
   };
+  const bool i8 = eig_i8_enabled(c);
   auto pow_body = [&](bool after_rr) -> avd_status {
     if (!after_rr) {  // Z = G Q (a check already made Z = G U on every rank)
-      AVD_CUDA(cudaMemsetAsync(c->Z32, 0, sizeof(float) * m * p, c->stream));
-      if (r1 > r0) AVD_TRY(gemm32(c, c->Q32, c->Z, c->Z32, nullptr, r0, r1));
-      AVD_TRY(exch(AVD_BUF_EIGZ, c->Z32, AVD_DT_F32));
+      AVD_CUDA(cudaMemsetAsync(c->Z, 0, sizeof(double) * m * p, c->stream));
+      if (r1 > r0) {
+        if (i8) AVD_TRY(gemm_i8(c, c->Q, c->Z, nullptr, nullptr, r0, r1));
+        else AVD_TRY(gemm32(c, c->Q32, c->Z, nullptr, nullptr, r0, r1));
+      }
+      AVD_TRY(exch(AVD_BUF_EIGZ, c->Z, AVD_DT_F64));
+      if (!i8) {  // the SIMT product reads the fp32 mirror of the exchanged Z
+        f64_to_f32_kernel<<<(unsigned)ceil_div(m * p, 256), 256, 0, c->stream>>>(c->Z, c->Z32, m * p);
+        AVD_LAUNCHED(c);
+      }
     }
-    AVD_TRY(rows_y([&]() { return gemm32(c, c->Z32, c->Y, nullptr, nullptr, r0, r1); }));  // Y = G Z
+    AVD_TRY(rows_y([&]() {  // Y = G Z
+      return i8 ? gemm_i8(c, c->Z, c->Y, nullptr, nullptr, r0, r1) : gemm32(c, c->Z32, c->Y, nullptr, nullptr, r0, r1);
+    }));
     AVD_TRY(orth(c, c->Y, eig_seed(c), &ctl->it));
     ctl_end_kernel<<<1, 32, 0, c->stream>>>(ctl);
     AVD_LAUNCHED(c);

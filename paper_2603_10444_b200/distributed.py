@@ -12,7 +12,7 @@ module all-reduces exactly the exchange buffers the header lists (SURVEY.md §2.
             column sums of the quantised operand (SUM i64)  -> identical exactly-centred G on
             every rank
   eig     : distributed: every G Q product of the subspace iteration is split by
-            row blocks over the ranks and all-gathered (EIGZ f32 / EIGY f64, SUM of zero-padded
+            row blocks over the ranks and all-gathered (EIGZ / EIGY f64, SUM of zero-padded
             blocks) through a callback the library calls; the p x p work is replicated (same G,
             same seed -> identical V_k, sigma_k on every rank); may ask for a 3-digit Gram
             (AVD_EREPEAT) -> gram again, exchange GRAMP, QSUM, QERR, eig again
@@ -41,7 +41,7 @@ EXCHANGES = {
              ("QERR", torch.float64, "sum")],
     "regram": [("GRAMP", torch.int64, "sum"), ("QSUM", torch.int64, "sum"), ("QERR", torch.float64, "sum")],
     # called back by the library from inside the distributed eigensolve
-    "eig": [("EIGZ", torch.float32, "sum"), ("EIGY", torch.float64, "sum")],
+    "eig": [("EIGZ", torch.float64, "sum"), ("EIGY", torch.float64, "sum")],
     "project": [("ENERGY", torch.float64, "sum")],
     "select0": [("HIST0", torch.int64, "sum")],
     "select1": [("HIST2", torch.int64, "sum")],

@@ -86,18 +86,18 @@ class ModelBackend:
     def stage_eig_dist(self, rank, exchange):
         """Model of avd_stage_eig_dist: block power iterations whose G Q products are split by
         row blocks over the ranks, each rank's rows written into a zero-padded m x p block that
-        `exchange` all-reduces (EIGZ in fp32, EIGY in fp64, like the library), then Rayleigh-Ritz
+        `exchange` all-reduces (EIGZ, EIGY in fp64, like the library), then Rayleigh-Ritz
         on the replicated orthonormal basis."""
         G = self.buf["GRAMP"].numpy()
         m, p = self.m, self.k + 6
         r0, r1 = m * rank // self.world, m * (rank + 1) // self.world
         Q = np.linalg.qr(np.random.default_rng(7).standard_normal((m, p)))[0]
         for _ in range(60):
-            Z = np.zeros((m, p), np.float32)
+            Z = np.zeros((m, p))
             Z[r0:r1] = G[r0:r1] @ Q
             self.buf["EIGZ"] = torch.tensor(Z)
             exchange("EIGZ")
-            Z = self.buf["EIGZ"].numpy().astype(np.float64)
+            Z = self.buf["EIGZ"].numpy()
             Y = np.zeros((m, p))
             Y[r0:r1] = G[r0:r1] @ Z
             self.buf["EIGY"] = torch.tensor(Y)
