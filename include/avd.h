@@ -102,6 +102,10 @@ typedef struct {
  * launch and one synchronisation per decision, instead of the device-resident CUDA graph (the
  * same kernels in the same order: bit-identical results; env AVD_EIG_NOGRAPH=1 does the same)  */
 #define AVD_FLAG_EIG_HOST_LOOP 8
+/* avd_config.flags: also compute the top-k singular pairs of the UNCENTRED X (eigenpairs of
+ * X^T X = G + l mu mu^T) and alpha_i = |mu . v_i| into
+ * avd_outputs.mean_sigma_dev / mean_alpha_dev — about one eigensolve of extra work          */
+#define AVD_FLAG_MEAN_TOPK 16
 
 /* Outputs.  Device arrays caller-owned, sized from the plan (cap = n_top). */
 typedef struct {
@@ -154,6 +158,13 @@ typedef struct {
   double sigma1_u;
   double resid_u;          /* ||Gu v - lambda v|| / lambda of the uncentred power iteration     */
   int32_t iters_u;         /* its steps                                                         */
+  /* AVD_FLAG_MEAN_TOPK: the top k uncentred pairs (caller-owned [k] arrays, device — host for
+   * avd_decompose_host —, NULL = not wanted): sigma_i of X and alpha_i = |mu . v_i|, the
+   * coefficients of mu = sum_i alpha_i v_i (cos(mu_hat, v_i) = alpha_i/||mu||) */
+  double* mean_sigma_dev;
+  double* mean_alpha_dev;
+  int32_t iters_uk;        /* subspace steps of that solve (0 when not requested)              */
+  double resid_uk;         /* its max_i<k ||Gu v_i - lambda_i v_i|| / lambda_1                  */
 } avd_outputs;
 
 typedef struct avd_ctx avd_ctx;

@@ -223,7 +223,7 @@ def gram_x(X, mu) -> np.ndarray:
     return G
 
 
-def mean_diagnostics(X) -> dict:
+def mean_diagnostics(X, k=None) -> dict:
     """Mean-bias diagnostics of the paper's section "Mean bias phenomenon" and
     Eq. R, in the paper's order and notation, fp64:
       mu = (1/l) X^T 1; mu_hat = mu / ||mu||; p_i = x_i^T mu_hat (PAPER.md:551);
@@ -232,6 +232,7 @@ def mean_diagnostics(X) -> dict:
       X = U S V^T (uncentred): v_1, sigma_1 from the Jacobi eigendecomposition of
       X^T X; u_1 = X v_1 / sigma_1; alpha_1 = (sigma_1 / l) u_1^T 1 (sign of v_1
       such that alpha_1 >= 0); cos_mu_v1 = |mu_hat^T v_1| (0 when mu = 0).
+    Top k (default all m) uncentred pairs: sigma_u[i], alpha[i] = |mu . v_i|, cos[i] = alpha[i]/||mu||.
     Readings (R19): with mu = 0 the sign fraction and cos are 0."""
     X = _f32(X)
     l, m = X.shape
@@ -254,8 +255,15 @@ def mean_diagnostics(X) -> dict:
     if alpha1 < 0:
         v1, u1, alpha1 = -v1, -u1, -alpha1
     cos = abs(float(mu @ v1)) / nmu if nmu > 0 else 0.0
+    # the top-k uncentred pairs ("the other right singular directions"):
+    # sigma_i = sqrt(lambda_i(X^T X)), alpha_i = |mu . v_i| (the coefficients of mu = sum_i
+    # alpha_i v_i, sign-free), cos_i = alpha_i / ||mu||
+    kk = m if k is None else min(int(k), m)
+    sig_u = np.sqrt(np.maximum(lam[:kk], 0.0))
+    alpha = np.abs(mu @ V[:, :kk])
+    cos_k = alpha / nmu if nmu > 0 else np.zeros(kk)
     return dict(mu_norm=nmu, p_pos=pos, p_neg=neg, sign_fraction=frac, R=R, sigma1_u=s1, v1=v1,
-                alpha1=alpha1, cos_mu_v1=cos)
+                alpha1=alpha1, cos_mu_v1=cos, sigma_u=sig_u, alpha=alpha, cos=cos_k)
 
 
 def host_cores() -> int:

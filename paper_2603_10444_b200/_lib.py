@@ -12,6 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libavd.so")
 
 AVD_FLAG_STREAM_SELECT, AVD_FLAG_EXACT_SCALE, AVD_FLAG_FORCE_ESCALATE, AVD_FLAG_EIG_HOST_LOOP = 1, 2, 4, 8
+AVD_FLAG_MEAN_TOPK = 16
 AVD_OK, AVD_EINVAL, AVD_ENONFINITE, AVD_ENOCONV, AVD_ECUDA, AVD_ENOMEM, AVD_ESTATE = 0, 1, 2, 3, 4, 6, 8
 AVD_EREPEAT, AVD_EEXCHANGE = 9, 10
 BUF = dict(STATS=0, COLMAX=1, COLMIN=2, HIST1=3, GRAM=4, ENERGY=5, HIST2=6, HIST3=7, TIES=8, AGG=9,
@@ -67,7 +68,9 @@ class avd_outputs(ctypes.Structure):
                 ("p_pos", ctypes.c_int64), ("p_neg", ctypes.c_int64),
                 ("cos_mu_v1", ctypes.c_double), ("alpha1", ctypes.c_double),
                 ("sigma1_u", ctypes.c_double), ("resid_u", ctypes.c_double),
-                ("iters_u", ctypes.c_int32)]
+                ("iters_u", ctypes.c_int32),
+                ("mean_sigma_dev", ctypes.c_void_p), ("mean_alpha_dev", ctypes.c_void_p),
+                ("iters_uk", ctypes.c_int32), ("resid_uk", ctypes.c_double)]
 
 
 _lib = None

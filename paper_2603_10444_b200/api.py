@@ -50,6 +50,11 @@ class Result:
     alpha1: float = 0.0
     sigma1_u: float = 0.0
     iters_u: int = 0
+    # AVD_FLAG_MEAN_TOPK: top-k singular values of the uncentred X and alpha_i = |mu . v_i|
+    mean_sigma: torch.Tensor | None = None
+    mean_alpha: torch.Tensor | None = None
+    iters_uk: int = 0
+    resid_uk: float = 0.0
 
     @property
     def shares_cf(self):
@@ -96,6 +101,9 @@ class Decomposer:
         self.sigma = torch.empty(self.k, dtype=torch.float64, device=dev)
         self.top_idx = torch.empty(max(self.n_top, 1), dtype=torch.int64, device=dev)
         self.rho = torch.empty((max(self.n_top, 1), 4), dtype=torch.float64, device=dev)
+        self.topk_u = bool(int(flags) & L.AVD_FLAG_MEAN_TOPK)  # uncentred top-k pairs requested
+        self.mean_sigma = torch.empty(self.k, dtype=torch.float64, device=dev) if self.topk_u else None
+        self.mean_alpha = torch.empty(self.k, dtype=torch.float64, device=dev) if self.topk_u else None
 
     def close(self):
         if getattr(self, "h", None):
@@ -112,6 +120,8 @@ class Decomposer:
         o = L.avd_outputs()
         o.mu_dev, o.V_dev, o.sigma_dev = self.mu.data_ptr(), self.V.data_ptr(), self.sigma.data_ptr()
         o.top_idx_dev, o.rho_dev = self.top_idx.data_ptr(), self.rho.data_ptr()
+        if self.topk_u:
+            o.mean_sigma_dev, o.mean_alpha_dev = self.mean_sigma.data_ptr(), self.mean_alpha.data_ptr()
         return o
 
     def _result(self, o: L.avd_outputs, st: int, host=None) -> Result:
@@ -130,7 +140,10 @@ class Decomposer:
                       precision_sigma=float(o.precision_sigma),
                       precision_share=float(o.precision_share), mean_R=float(o.mean_R),
                       sign_fraction=float(o.sign_fraction), cos_mu_v1=float(o.cos_mu_v1),
-                      alpha1=float(o.alpha1), sigma1_u=float(o.sigma1_u), iters_u=int(o.iters_u))
+                      alpha1=float(o.alpha1), sigma1_u=float(o.sigma1_u), iters_u=int(o.iters_u),
+                      mean_sigma=self.mean_sigma if host is None else None,
+                      mean_alpha=self.mean_alpha if host is None else None,
+                      iters_uk=int(o.iters_uk), resid_uk=float(o.resid_uk))
 
     def _check_X(self, X: torch.Tensor):
         if not (X.is_cuda and X.dtype == torch.float32 and X.is_contiguous()):

@@ -129,7 +129,7 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   L.add(sizeof(double) * p * p);                // 22 W
   L.add(sizeof(double) * 2 * p);                // 23 theta
   L.add(sizeof(double) * C->n_red * p * p);     // 24 red_part
-  L.add(sizeof(double) * 2 * p);                // 25 resid
+  L.add(sizeof(double) * (4 * p + 8));          // 25 resid (+ flags, + scratch of the uncentred top-k)
   L.add(sizeof(double) * 4);                    // 26 trace
   L.add(sizeof(double) * m * k);                // 27 V
   L.add(sizeof(double) * k);                    // 28 sigma
@@ -188,6 +188,7 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   L.add(gemm_i8_part_bytes(C->m_pad, (int)p, C->num_sms));               // 78 g8_part
   L.add(sizeof(unsigned) * (size_t)(C->m_pad / 128 + 1));                // 79 g8_tickets
   L.add(2 * sizeof(CUtensorMap));                                        // 80 tm_dev
+  L.add(sizeof(double) * 2 * kMaxP);                                     // 81 unc_topk
   if (L.n >= 128) { set_error("workspace layout table overflow"); return AVD_EINVAL; }
   plan->workspace_bytes = L.total;
   if (lay) *lay = L;
@@ -358,7 +359,7 @@ avd_status avd_create(const avd_config* cfg, avd_ctx** out) {
   BIND(qerr, double*); BIND(mu0, float*); BIND(qsq_part, long long*); BIND(diag, double*);
   BIND(prec, double*); BIND(ysq, double*); BIND(eig_ctl, void*); BIND(wsc, double*); BIND(gram_p, long long*);
   BIND(gd, int8_t*); BIND(gsc, double*); BIND(qd, int8_t*); BIND(qsc, double*); BIND(g8_part, double*);
-  BIND(g8_tickets, unsigned*); BIND(tm_dev, CUtensorMap*);
+  BIND(g8_tickets, unsigned*); BIND(tm_dev, CUtensorMap*); BIND(unc_topk, double*);
   if (c->cfg.world <= 1) c->gram_p = nullptr;
 #undef BIND
   if (cudaMallocHost(&c->eig_host, sizeof(double) * kHostScratch) != cudaSuccess) {
@@ -567,6 +568,7 @@ static avd_status stage_eig_impl(avd_ctx* c, int32_t rank, avd_exchange_fn fn, v
     set_error("Gram operand raised to 3 digits: call avd_stage_gram again");
     return AVD_EREPEAT;
   }
+  if (c->cfg.flags & AVD_FLAG_MEAN_TOPK) AVD_TRY(run_uncentred_topk(c, c->unc_topk));
   c->stage = 4;
   return st;
 }
@@ -626,6 +628,13 @@ avd_status avd_stage_report(avd_ctx* c, avd_outputs* out) {
   AVD_LAUNCHED(c);
   report_final_kernel<<<1, 32, 0, c->stream>>>(c->red_part, nrep, c->cfg.l_global, c->report);
   AVD_LAUNCHED(c);
+  if (c->cfg.flags & AVD_FLAG_MEAN_TOPK) {  // uncentred sigma_i, alpha_i (i < k)
+    if (out->mean_sigma_dev)
+      AVD_CUDA(cudaMemcpyAsync(out->mean_sigma_dev, c->unc_topk, sizeof(double) * k, cudaMemcpyDeviceToDevice, c->stream));
+    if (out->mean_alpha_dev)
+      AVD_CUDA(cudaMemcpyAsync(out->mean_alpha_dev, c->unc_topk + k, sizeof(double) * k, cudaMemcpyDeviceToDevice,
+                               c->stream));
+  }
   if (out->mu_dev || out->V_dev || out->sigma_dev) {
     copy_outputs_kernel<<<(unsigned)ceil_div(std::max<int64_t>(m * k, m), 256), 256, 0, c->stream>>>(
         c->mu, c->V, c->sigma, m, k, out->mu_dev, out->V_dev, out->sigma_dev);
@@ -700,6 +709,8 @@ avd_status avd_stage_report(avd_ctx* c, avd_outputs* out) {
   out->sigma1_u = c->sigma1_u;
   out->resid_u = c->resid_u;
   out->iters_u = c->iters_u;
+  out->iters_uk = (c->cfg.flags & AVD_FLAG_MEAN_TOPK) ? c->iters_uk : 0;
+  out->resid_uk = (c->cfg.flags & AVD_FLAG_MEAN_TOPK) ? c->resid_uk : 0.0;
   out->n_top_local = c->hplan.sel_local;
   out->top_offset = c->hplan.top_offset;
   out->n_top_global = c->hplan.n_eff;
@@ -823,6 +834,7 @@ avd_status avd_decompose_host(avd_ctx* c, const float* X_host, avd_outputs* out)
   AVD_CUDA(cudaMemcpyAsync(c->X_stage, X_host, sizeof(float) * l * m, cudaMemcpyHostToDevice, c->stream));
   avd_outputs d = *out;
   d.mu_dev = c->o_mu; d.V_dev = c->o_V; d.sigma_dev = c->o_sigma; d.top_idx_dev = c->o_idx; d.rho_dev = c->o_rho;
+  d.mean_sigma_dev = nullptr; d.mean_alpha_dev = nullptr;  // host arrays here: copied below
   const avd_status st = avd_decompose(c, c->X_stage, &d);
   if (st != AVD_OK && st != AVD_ENOCONV) return st;
   if (out->mu_dev) AVD_CUDA(cudaMemcpyAsync(out->mu_dev, c->o_mu, sizeof(double) * m, cudaMemcpyDeviceToHost, c->stream));
@@ -830,11 +842,16 @@ avd_status avd_decompose_host(avd_ctx* c, const float* X_host, avd_outputs* out)
   if (out->sigma_dev) AVD_CUDA(cudaMemcpyAsync(out->sigma_dev, c->o_sigma, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
   if (out->top_idx_dev) AVD_CUDA(cudaMemcpyAsync(out->top_idx_dev, c->o_idx, sizeof(int64_t) * d.n_top_local, cudaMemcpyDeviceToHost, c->stream));
   if (out->rho_dev) AVD_CUDA(cudaMemcpyAsync(out->rho_dev, c->o_rho, sizeof(double) * 4 * d.n_top_local, cudaMemcpyDeviceToHost, c->stream));
+  if ((c->cfg.flags & AVD_FLAG_MEAN_TOPK) && out->mean_sigma_dev)
+    AVD_CUDA(cudaMemcpyAsync(out->mean_sigma_dev, c->unc_topk, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
+  if ((c->cfg.flags & AVD_FLAG_MEAN_TOPK) && out->mean_alpha_dev)
+    AVD_CUDA(cudaMemcpyAsync(out->mean_alpha_dev, c->unc_topk + k, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
   AVD_CUDA(cudaStreamSynchronize(c->stream));
-  double* keep[5] = {out->mu_dev, out->V_dev, out->sigma_dev, out->rho_dev, nullptr};
+  double* keep[6] = {out->mu_dev, out->V_dev, out->sigma_dev, out->rho_dev, out->mean_sigma_dev, out->mean_alpha_dev};
   int64_t* keep_idx = out->top_idx_dev;
   *out = d;
   out->mu_dev = keep[0]; out->V_dev = keep[1]; out->sigma_dev = keep[2]; out->rho_dev = keep[3];
+  out->mean_sigma_dev = keep[4]; out->mean_alpha_dev = keep[5];
   out->top_idx_dev = keep_idx;
   return st;
 }

@@ -132,6 +132,9 @@ struct Ctx {
   // diag[4+m_pad..) = y of the uncentred power iteration
   double* diag = nullptr;
   double sigma1_u = 0, alpha1 = 0, cos_mu_v1 = 0, resid_u = 0;
+  double* unc_topk = nullptr;     // [2 * kMaxP]: uncentred sigma_i | alpha_i, i < k (AVD_FLAG_MEAN_TOPK)
+  int iters_uk = 0;
+  double resid_uk = 0;
   int iters_u = 0;
   bool sign_valid = false;        // p_i signs available (tensor-core projection path)
   double* resid = nullptr;        // [p]
@@ -222,6 +225,7 @@ avd_status launch_finish(Ctx* c);                          // k_pass1.cu
 avd_status launch_uncentred(Ctx* c);                       // k_eig.cu (mean-bias diagnostics, side stream)
 avd_status join_uncentred(Ctx* c);                         // k_eig.cu
 void destroy_graphs(Ctx* c);                               // k_eig.cu
+avd_status run_uncentred_topk(Ctx* c, double* out);        // k_eig.cu (optional)
 avd_status launch_sign_count(Ctx* c);                      // k_project.cu (mean-bias diagnostics)
 avd_status launch_gram(Ctx* c, const double* skip = nullptr);  // k_gram.cu (skip: device gate)
 avd_status gram_make_tmap(Ctx* c);                         // k_gram.cu

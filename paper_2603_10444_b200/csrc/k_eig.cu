@@ -1000,6 +1000,46 @@ __global__ void f64_to_f32_kernel(const double* __restrict__ a, float* __restric
   if (t < n) b[t] = (float)a[t];
 }
 
+// ---------------------------------------------------------------- uncentred top-k (f2)
+// w_r = mu . Q_r (fixed order; one warp per column r)
+__global__ void mu_dot_cols_kernel(const double* __restrict__ mu, const double* __restrict__ Q, int64_t m, int p,
+                                   double* __restrict__ w) {
+  const int r = blockIdx.x, lane = threadIdx.x;
+  double s = 0.0;
+  for (int64_t j = lane; j < m; j += 32) s = fma(mu[j], Q[j * p + r], s);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+  if (lane == 0) w[r] = s;
+}
+// Y += l mu w^T (the rank-one term of the uncentred Gram X^T X = G + l mu mu^T)
+__global__ void rank1_kernel(double* __restrict__ Y, const double* __restrict__ mu, const double* __restrict__ w,
+                             int64_t m, int p, double l) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m * p) return;
+  Y[t] = fma(l * mu[t / p], w[t % p], Y[t]);
+}
+// start block of the uncentred solve: column 0 = mu_hat (diag + 4), columns 1.. = the centred
+// Ritz vectors U[:, 0 .. p-2]
+__global__ void unc_start_kernel(const double* __restrict__ U, const double* __restrict__ muhat, int64_t m, int p,
+                                 double* __restrict__ Z) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m * p) return;
+  const int64_t j = t / p;
+  const int r = (int)(t % p);
+  Z[t] = r == 0 ? muhat[j] : U[j * p + (r - 1)];
+}
+// sigma_i = sqrt(theta_i), alpha_i = |mu . u_i| of the Ritz vectors U (i < k); one warp per i
+__global__ void unc_out_kernel(const double* __restrict__ U, const double* __restrict__ theta,
+                               const double* __restrict__ mu, int64_t m, int p, int k, double* __restrict__ out) {
+  const int i = blockIdx.x, lane = threadIdx.x;
+  double s = 0.0;
+  for (int64_t j = lane; j < m; j += 32) s = fma(mu[j], U[j * p + i], s);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+  if (lane == 0) {
+    out[i] = sqrt(fmax(theta[i], 0.0));
+    out[k + i] = fabs(s);
+  }
+}
+
 // ---------------------------------------------------------------- device-resident loop control
 // The subspace iteration runs as ONE CUDA graph: WHILE(loop) { begin; IF(rr) {RR check; ctl_rr};
 // IF(pow) {power step; orth; ctl_end} } — every decision the host used to take between launches
@@ -1718,6 +1758,51 @@ avd_status launch_uncentred(Ctx* c) {
 avd_status join_uncentred(Ctx* c) {
   if (eig_nograph(c)) return AVD_OK;
   AVD_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+  return AVD_OK;
+}
+
+// Uncentred top-k: the top k right singular pairs of the
+// UNCENTRED X, i.e. eigenpairs of X^T X = G + l mu mu^T, and alpha_i = mu . v_i (the expansion
+// mu = sum_i alpha_i v_i, |.|: sign-free), by subspace iteration on G + l mu mu^T (fp64 products
+// with the exact G plus the rank-one term) from the start block [mu_hat, U_{p-1}] — already close
+// to the answer — with a Rayleigh-Ritz check after every step, until the top-k residuals are
+// <= tol (at most 30 steps).  Writes out[0..k) = sigma_i, out[k..2k) = alpha_i.  Optional
+// (AVD_FLAG_MEAN_TOPK): about one eigensolve of extra work.  Reuses the solve's scratch (V_k and
+// sigma_k are already final).
+avd_status run_uncentred_topk(Ctx* c, double* out) {
+  const int64_t m = c->cfg.m;
+  const int p = c->p, k = c->k;
+  const double l = (double)c->cfg.l_global;
+  const double tol = c->cfg.eig_tol > 0 ? c->cfg.eig_tol : 1e-6;
+  double* w = c->resid + 3 * p;  // [p] scratch (resid holds 2p + flags)
+  int* sweeps = reinterpret_cast<int*>(c->theta + p) + 15;
+  const unsigned g = (unsigned)ceil_div(m * p, 256);
+  unc_start_kernel<<<g, 256, 0, c->stream>>>(c->U, c->diag + 4, m, p, c->Z);
+  AVD_LAUNCHED(c);
+  AVD_TRY(orth(c, c->Z, eig_seed(c) + 977u, nullptr));
+  double* h = c->eig_host + 4 * kMaxP;
+  c->iters_uk = 0;
+  for (int it = 1; it <= 30; ++it) {
+    AVD_TRY(gemm64(c, c->Q, c->Y, nullptr));  // Y = G Q + l mu (mu^T Q)
+    mu_dot_cols_kernel<<<p, 32, 0, c->stream>>>(c->mu, c->Q, m, p, w);
+    AVD_LAUNCHED(c);
+    rank1_kernel<<<g, 256, 0, c->stream>>>(c->Y, c->mu, w, m, p, l);
+    AVD_LAUNCHED(c);
+    AVD_TRY(atb_fused<2>(c, c->Q, c->Y, c->W, c->theta, nullptr, sweeps, nullptr, 40, nullptr));
+    AVD_TRY(matpp(c, c->Y, c->Z, nullptr, c->Q, c->U, nullptr, c->W));  // Z = Gu U, U = Q W
+    resid_kernel<<<k, 256, 0, c->stream>>>(c->Z, c->U, c->theta, m, p, c->resid);
+    AVD_LAUNCHED(c);
+    AVD_CUDA(cudaMemcpyAsync(h, c->resid, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
+    AVD_CUDA(cudaStreamSynchronize(c->stream));
+    double mr = 0.0;
+    for (int r = 0; r < k; ++r) mr = std::max(mr, h[r]);
+    c->iters_uk = it;
+    c->resid_uk = mr;
+    if (mr <= tol) break;
+    AVD_TRY(orth(c, c->Z, eig_seed(c) + 977u * (uint32_t)it, nullptr));  // Q = orth(Gu U)
+  }
+  unc_out_kernel<<<k, 32, 0, c->stream>>>(c->U, c->theta, c->mu, m, p, k, out);
+  AVD_LAUNCHED(c);
   return AVD_OK;
 }
 

@@ -264,3 +264,31 @@ def test_graph_loop_matches_host_loop(cuda_device, l, m, seed):
             np.testing.assert_array_equal(g[key], ref[key])
         for f in ("energy_cf", "energy_el", "sigma_next", "iters", "max_resid", "sigma1_u", "alpha1", "iters_u"):
             assert getattr(g["res"], f) == getattr(ref["res"], f), f
+
+
+@pytest.mark.parametrize("l,m,seed,f_mean", [(512, 256, 0, 0.9), (3000, 300, 1, 0.8), (4096, 512, 4, 0.3)])
+def test_mean_topk_parity(cuda_device, l, m, seed, f_mean):
+    """AVD_FLAG_MEAN_TOPK: the top-k singular values of the UNCENTRED X and alpha_i = |mu . v_i|
+     against the oracle (full Jacobi of X^T X)."""
+    from paper_2603_10444_b200 import Decomposer
+    from paper_2603_10444_b200._lib import AVD_FLAG_MEAN_TOPK
+    X = generate(SynthSpec(l, m, seed=seed, f_mean=f_mean))
+    dec = Decomposer(l, m, flags=AVD_FLAG_MEAN_TOPK)
+    r = dec(X.cuda())
+    torch.cuda.synchronize()
+    k = dec.k
+    d = O.mean_diagnostics(X.numpy(), k=k + 1)
+    sig = r.mean_sigma.cpu().numpy()
+    alpha = r.mean_alpha.cpu().numpy()
+    assert r.iters_uk >= 1 and r.resid_uk <= 1e-6
+    # a planted gap between the k-th and (k+1)-th uncentred pairs is not guaranteed: sigma_i to
+    # 1e-6 relative of sigma_1 (Rayleigh-Ritz values), alpha_i where the pair is separated
+    np.testing.assert_allclose(sig, d["sigma_u"][:k], rtol=0, atol=1e-6 * d["sigma_u"][0])
+    sep = np.ones(k, bool)
+    su = d["sigma_u"]
+    for i in range(k):
+        gaps = [abs(su[i] - su[j]) for j in range(k + 1) if j != i]
+        sep[i] = min(gaps) > 1e-3 * su[0]
+    np.testing.assert_allclose(alpha[sep], d["alpha"][:k][sep], rtol=0, atol=1e-5 * max(d["mu_norm"], 1e-300))
+    assert abs(sig[0] - r.sigma1_u) <= 1e-6 * sig[0]
+    dec.close()

@@ -356,6 +356,39 @@ def test_mean_diagnostics_vs_numpy_svd():
     assert d["p_pos"] == int((p > 0).sum()) and d["p_neg"] == int((p < 0).sum())
 
 
+@pytest.mark.parametrize("l,m,rank", [(256, 64, 2), (512, 128, 3)])
+def test_mean_topk_planted_closed_forms(l, m, rank):
+    """Top-k uncentred pairs on the planted constant-mean data: X^T X =
+    l m c^2 (1/sqrt(m))(1/sqrt(m))^T + sum_r sigma_r^2 v_r v_r^T with v_r (Walsh) orthogonal to the
+    mean direction, so the pairs are (c sqrt(l m), mu_hat) then (sigma_r, v_r): alpha = (||mu||,
+    0, ..., 0) exactly and cos = (1, 0, ..., 0); sigma_i in descending order."""
+    c = 0.75
+    ii, jj = torch.arange(l), torch.arange(m)
+    X = torch.full((l, m), c, dtype=torch.float64)
+    sig = []
+    for r in range(rank):
+        cr = 0.125 * (r + 1)
+        X += cr * torch.outer(walsh(r + 1, ii), walsh(2 * r + 3, jj))
+        sig.append(cr * math.sqrt(l * m))
+    d = O.mean_diagnostics(X.float().numpy(), k=rank + 1)
+    want_sig = np.array([c * math.sqrt(l * m)] + sorted(sig, reverse=True))
+    np.testing.assert_allclose(d["sigma_u"], want_sig, rtol=1e-12)
+    np.testing.assert_allclose(d["alpha"], [c * math.sqrt(m)] + [0.0] * rank, atol=1e-10 * m)
+    np.testing.assert_allclose(d["cos"], [1.0] + [0.0] * rank, atol=1e-10)
+
+
+def test_mean_topk_vs_numpy_svd():
+    """Library routine: numpy's SVD of the uncentred X gives every sigma_i and |mu . v_i|."""
+    rng = np.random.default_rng(8)
+    X = (rng.standard_normal((400, 50)) * np.linspace(3, 0.5, 50) + rng.standard_normal(50) * 2).astype(np.float32)
+    d = O.mean_diagnostics(X, k=6)
+    _, S, Vt = np.linalg.svd(X.astype(np.float64), full_matrices=False)
+    mu = X.astype(np.float64).mean(0)
+    np.testing.assert_allclose(d["sigma_u"], S[:6], rtol=1e-10)
+    np.testing.assert_allclose(d["alpha"], np.abs(Vt[:6] @ mu), rtol=1e-8, atol=1e-12)
+    np.testing.assert_allclose(d["cos"], np.abs(Vt[:6] @ mu) / np.linalg.norm(mu), rtol=1e-8, atol=1e-12)
+
+
 def test_mean_diagnostics_zero_mean():
     """Exactly zero column means: no mean direction -> sign fraction 0, cos 0, R 0 (R19)."""
     ii, jj = torch.arange(64), torch.arange(16)
