@@ -184,7 +184,7 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   L.add((size_t)4 * C->m_pad * C->m_pad);                               // 74 gd
   L.add(sizeof(double) * C->m_pad);                                      // 75 gsc
   L.add((size_t)3 * kMaxP * C->m_pad);                                   // 76 qd
-  L.add(sizeof(double) * kMaxP);                                         // 77 qsc
+  L.add(sizeof(double) * 2 * kMaxP);                                     // 77 qsc (+ column maxima)
   L.add(gemm_i8_part_bytes(C->m_pad, (int)p, C->num_sms));               // 78 g8_part
   L.add(sizeof(unsigned) * (size_t)(C->m_pad / 128 + 1));                // 79 g8_tickets
   L.add(2 * sizeof(CUtensorMap));                                        // 80 tm_dev

@@ -116,7 +116,7 @@ struct Ctx {
   int8_t* gd = nullptr;           // [4][m_pad][m_pad] G in balanced base-128 digits (k_eig_i8.cu)
   double* gsc = nullptr;          // [m_pad] row scales of gd
   int8_t* qd = nullptr;           // [3][p][m_pad] the product's input block in digits (transposed)
-  double* qsc = nullptr;          // [kMaxP] its column scales
+  double* qsc = nullptr;          // [2 kMaxP] its column scales | column maxima (bit patterns)
   double* g8_part = nullptr;      // split-K partials of the int8 products
   unsigned* g8_tickets = nullptr; // [m_pad / 128] last-CTA tickets
   CUtensorMap tm_gd{}, tm_qd{};

@@ -74,37 +74,48 @@ __global__ void __launch_bounds__(256) gdig_kernel(const double* __restrict__ G,
   }
 }
 
-// Q (fp64, m x p row-major) -> Qd [3][p][m_pad] int8 (transposed: K-major B operand),
-// tQ[r] = 2^(e_r - 19) from the column max (colmax != nullptr: a bound given by the producer,
-// else measured here); one CTA per column r
-__global__ void __launch_bounds__(256) qdig_kernel(const double* __restrict__ Q, int64_t m, int64_t m_pad, int p,
-                                                   const double* __restrict__ colmax, int8_t* __restrict__ Qd,
-                                                   double* __restrict__ tQ) {
-  __shared__ double sh[256];
-  const int r = blockIdx.x;
-  double qmax;
-  if (colmax) {
-    qmax = colmax[r];
-  } else {
+// Q (fp64, m x p row-major) -> Qd [3][p][m_pad] int8 (transposed: K-major B operand) with
+// tQ[r] = 2^(e_r - 19) from the column max.  Two coalesced kernels: per 64-row tile column maxima
+// (atomicMax on the bit patterns of |.|: order-free, deterministic), then per 128-row tile the
+// digits, written transposed through shared memory.
+constexpr int kQdTile = 64;
+__global__ void __launch_bounds__(256) qmax_kernel(const double* __restrict__ Q, int64_t m, int p,
+                                                   unsigned long long* __restrict__ qmax) {
+  extern __shared__ double tq[];  // [kQdTile][p]
+  const int64_t b0 = (int64_t)blockIdx.x * kQdTile;
+  const int rows = (int)(m - b0 < kQdTile ? m - b0 : kQdTile);
+  for (int t = threadIdx.x; t < rows * p; t += 256) tq[t] = fabs(Q[b0 * p + t]);
+  __syncthreads();
+  for (int r = threadIdx.x; r < p; r += 256) {
     double mx = 0.0;
-    for (int64_t b = threadIdx.x; b < m; b += 256) mx = fmax(mx, fabs(Q[b * p + r]));
-    sh[threadIdx.x] = mx;
-    __syncthreads();
-    for (int o = 128; o > 0; o >>= 1) {
-      if ((int)threadIdx.x < o) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + o]);
-      __syncthreads();
-    }
-    qmax = sh[0];
+    for (int i = 0; i < rows; ++i) mx = fmax(mx, tq[i * p + r]);
+    atomicMax(qmax + r, (unsigned long long)__double_as_longlong(mx));
   }
-  const int e = (qmax > 0.0 && qmax < 1e300) ? ilogb(qmax) + 1 : 0;
-  if (threadIdx.x == 0) tQ[r] = ldexp(1.0, e - 19);
+}
+constexpr int kQdRows = 32;  // rows per CTA of the digit kernel
+__global__ void __launch_bounds__(256) qdig_kernel(const double* __restrict__ Q, int64_t m, int64_t m_pad, int p,
+                                                   const unsigned long long* __restrict__ qmax,
+                                                   int8_t* __restrict__ Qd, double* __restrict__ tQ) {
+  extern __shared__ double tq[];  // [kQdRows][p] + [p] scales
+  double* sc = tq + kQdRows * p;
+  const int64_t b0 = (int64_t)blockIdx.x * kQdRows;
+  const int rows = (int)(m - b0 <= 0 ? 0 : (m - b0 < kQdRows ? m - b0 : kQdRows));
+  for (int t = threadIdx.x; t < kQdRows * p; t += 256) tq[t] = t < rows * p ? Q[b0 * p + t] : 0.0;
+  for (int r = threadIdx.x; r < p; r += 256) {
+    const double mx = __longlong_as_double((long long)qmax[r]);
+    const int e = (mx > 0.0 && mx < 1e300) ? ilogb(mx) + 1 : 0;
+    sc[r] = mx > 0.0 ? ldexp(1.0, 19 - e) : 0.0;
+    if (blockIdx.x == 0) tQ[r] = ldexp(1.0, e - 19);
+  }
+  __syncthreads();
   const int64_t plane = (int64_t)p * m_pad;
-  for (int64_t b = threadIdx.x; b < m_pad; b += 256) {
-    const long long z = (b < m && qmax > 0.0) ? llrint(ldexp(Q[b * p + r], 19 - e)) : 0ll;
+  for (int t = threadIdx.x; t < kQdRows * p; t += 256) {
+    const int r = t / kQdRows, i = t % kQdRows;  // consecutive threads: consecutive rows of column r
+    const long long z = llrint(tq[i * p + r] * sc[r]);
     int8_t d[kQDig];
     digits_of<kQDig>(z, d);
 #pragma unroll
-    for (int i = 0; i < kQDig; ++i) Qd[i * plane + (int64_t)r * m_pad + b] = d[i];
+    for (int di = 0; di < kQDig; ++di) Qd[di * plane + (int64_t)r * m_pad + b0 + i] = d[di];
   }
 }
 
@@ -281,7 +292,8 @@ __global__ void __launch_bounds__(kG8Threads, 1) gemm_i8_kernel(
 // ---------------------------------------------------------------- host side
 bool eig_i8_enabled(const Ctx* c) {
   static const bool off = [] { const char* e = std::getenv("AVD_EIG_SIMT"); return e && e[0] == '1'; }();
-  return !off && c->p <= 112 && c->gd != nullptr;
+  // small m (c1, c2): the SIMT product's latency beats the digit conversions' fixed cost
+  return !off && c->p <= 112 && c->gd != nullptr && c->cfg.m >= 3072;
 }
 
 // stage bytes and ring depth of one instantiation (<= ~200 KB of dynamic shared memory)
@@ -334,7 +346,13 @@ avd_status eig_i8_prepare(Ctx* c) {  // once per solve: G -> digits; the tensor 
 // Y = G In (In fp64 m x p; Y fp64 + optional fp32 mirror); rows [r0, r1) only when r1 > r0
 avd_status gemm_i8(Ctx* c, const double* In, double* Y, float* Y32, const int* skip, int64_t r0, int64_t r1) {
   const int p = c->p;
-  qdig_kernel<<<p, 256, 0, c->stream>>>(In, c->cfg.m, c->m_pad, p, nullptr, c->qd, c->qsc);
+  unsigned long long* qmax = reinterpret_cast<unsigned long long*>(c->qsc + kMaxP);
+  AVD_CUDA(cudaMemsetAsync(qmax, 0, sizeof(unsigned long long) * p, c->stream));
+  qmax_kernel<<<(unsigned)ceil_div(c->cfg.m, kQdTile), 256, sizeof(double) * kQdTile * p, c->stream>>>(
+      In, c->cfg.m, p, qmax);
+  AVD_LAUNCHED(c);
+  qdig_kernel<<<(unsigned)(c->m_pad / kQdRows), 256, sizeof(double) * (kQdRows + 1) * p, c->stream>>>(
+      In, c->cfg.m, c->m_pad, p, qmax, c->qd, c->qsc);
   AVD_LAUNCHED(c);
   double* out_colmax = nullptr;
   int RB, KS, rb0;
