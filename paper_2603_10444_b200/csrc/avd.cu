@@ -150,9 +150,9 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   L.add(sizeof(unsigned long long) * kHistBins);// 43 hist0
   L.add(sizeof(long long) * 2);                 // 44 cand_x
   L.add(gemm_part_bytes(m, C->m_pad, (int)p, C->num_sms));  // 45 gemm_part
-  L.add(sizeof(float) * 2 * C->l_pad * (((C->k_pad + 31) / 32) * 32));   // 46 P_hl
+  L.add((size_t)3 * C->l_pad * 128);                                     // 46 Pd
   L.add(std::max<size_t>(sizeof(float) * 2 * C->k_pad * round_up(m, 32), (size_t)4 * C->k_pad * C->m_pad));  // 47 Vt_hl / W digits
-  L.add(sizeof(float) * 2 * C->m_pad * (((C->k_pad + 31) / 32) * 32));   // 48 V_hl
+  L.add((size_t)3 * C->m_pad * 128);                                     // 48 Vd
   L.add(sizeof(float) * 2 * C->m_pad);                                   // 49 mu_hl
   L.add(sizeof(float) * C->m_pad * C->m_pad);                            // 50 G32
   L.add(sizeof(long long) * 2 * C->m_pad);                               // 51 qsum
@@ -189,6 +189,8 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   L.add(sizeof(unsigned) * (size_t)(C->m_pad / 128 + 1));                // 79 g8_tickets
   L.add(2 * sizeof(CUtensorMap));                                        // 80 tm_dev
   L.add(sizeof(double) * 2 * kMaxP);                                     // 81 unc_topk
+  L.add(sizeof(float) * C->l_pad);                                       // 82 ps
+  L.add(sizeof(float) * C->m_pad);                                       // 83 vs
   if (L.n >= 128) { set_error("workspace layout table overflow"); return AVD_EINVAL; }
   plan->workspace_bytes = L.total;
   if (lay) *lay = L;
@@ -352,7 +354,7 @@ avd_status avd_create(const avd_config* cfg, avd_ctx** out) {
   BIND(en_part, double*); BIND(colsumP_part, double*); BIND(energy, double*); BIND(hist2, unsigned long long*);
   BIND(hist3, unsigned long long*); BIND(ties, long long*); BIND(bm_sel, uint32_t*); BIND(bm_tie, uint32_t*);
   BIND(blk_cnt, int64_t*); BIND(agg, double*); BIND(agg_part, double*); BIND(report, double*); BIND(hist0, unsigned long long*); BIND(cand_x, long long*); BIND(gemm_part, void*);
-  BIND(P_hl, float*); BIND(Vt_hl, float*); BIND(V_hl, float*); BIND(mu_hl, float*);
+  BIND(Pd, int8_t*); BIND(Vt_hl, float*); BIND(Vd, int8_t*); BIND(mu_hl, float*);
   BIND(G32, float*); BIND(qsum, long long*); BIND(Q32, float*); BIND(Z32, float*); BIND(ticket, unsigned*); BIND(gmax, double*);
   BIND(samp, double*); BIND(smax, float*); BIND(smin, float*); BIND(qscale, float*); BIND(qoff, float*);
   BIND(qsum_part, long long*); BIND(qsum_local, long long*); BIND(qerr_part, float*); BIND(qerr_local, double*);
@@ -360,6 +362,7 @@ avd_status avd_create(const avd_config* cfg, avd_ctx** out) {
   BIND(prec, double*); BIND(ysq, double*); BIND(eig_ctl, void*); BIND(wsc, double*); BIND(gram_p, long long*);
   BIND(gd, int8_t*); BIND(gsc, double*); BIND(qd, int8_t*); BIND(qsc, double*); BIND(g8_part, double*);
   BIND(g8_tickets, unsigned*); BIND(tm_dev, CUtensorMap*); BIND(unc_topk, double*);
+  BIND(ps, float*); BIND(vs, float*);
   if (c->cfg.world <= 1) c->gram_p = nullptr;
 #undef BIND
   if (cudaMallocHost(&c->eig_host, sizeof(double) * kHostScratch) != cudaSuccess) {
@@ -377,7 +380,8 @@ avd_status avd_create(const avd_config* cfg, avd_ctx** out) {
     set_error("cudaEventCreate failed");
     return AVD_ECUDA;
   }
-  cudaMemset(c->P_hl, 0, sizeof(float) * 2 * c->l_pad * (((c->k_pad + 31) / 32) * 32));
+  cudaMemset(c->Pd, 0, (size_t)3 * c->l_pad * 128);  // K padding bytes of K8's operands stay zero
+  cudaMemset(c->ps, 0, sizeof(float) * c->l_pad);
   cudaMemset(c->g8_tickets, 0, sizeof(unsigned) * (size_t)(c->m_pad / 128 + 1));
   st = gram_make_tmap(c);
   if (st != AVD_OK) { cudaFree(c->ws); cudaFreeHost(c->eig_host); cudaEventDestroy(c->ev_host); delete c; return st; }
@@ -456,6 +460,11 @@ avd_status avd_buffer(avd_ctx* c, int32_t which, void** ptr, size_t* bytes) {
       break;
     }
     case AVD_BUF_EIGZ: *ptr = c->Z; *bytes = sizeof(double) * m * c->p; break;
+    // diagnostic views of K8's digit operands (not exchanged)
+    case 30: *ptr = c->Pd; *bytes = (size_t)3 * c->l_pad * 128; break;
+    case 31: *ptr = c->ps; *bytes = sizeof(float) * c->l_pad; break;
+    case 32: *ptr = c->Vd; *bytes = (size_t)3 * c->m_pad * 128; break;
+    case 33: *ptr = c->vs; *bytes = sizeof(float) * c->m_pad; break;
     case AVD_BUF_EIGY: *ptr = c->Y; *bytes = sizeof(double) * m * c->p; break;
     default: set_error("unknown buffer id"); return AVD_EINVAL;
   }

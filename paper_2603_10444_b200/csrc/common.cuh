@@ -152,10 +152,12 @@ struct Ctx {
   double sigma_next = 0;
   // K5/K8
   float* P = nullptr;             // [l_local][k_pad]
-  float* P_hl = nullptr;          // [2][l_pad][KP32] tf32 hi / lo planes of P (K8 A operand)
+  int8_t* Pd = nullptr;           // [3][l_pad][128] P's spike columns in digits (K8 A operand)
+  float* ps = nullptr;            // [l_pad] their row scales
   float* Vt_hl = nullptr;         // [2*k_pad][m_pad32] fp32 words; holds K5's int8 W digit planes [4][k_pad][m_pad]
   double* wsc = nullptr;          // [512]: K5 column scales t_r | corrections corr_r | (int) spiky columns at 384
-  float* V_hl = nullptr;          // [2][m_pad][KP32] tf32 hi / lo of V (K8 B operand)
+  int8_t* Vd = nullptr;           // [3][m_pad][128] V_k in digits (K8 B operand)
+  float* vs = nullptr;            // [m_pad] its row scales
   int64_t m_pad32 = 0;
   double* en_part = nullptr;      // [n_proj_ctas][4]
   double* colsumP_part = nullptr; // [n_proj_ctas][k_pad]

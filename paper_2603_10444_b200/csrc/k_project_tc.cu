@@ -29,26 +29,16 @@ using namespace sm100;
 constexpr int kPThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 convert / epilogue
 constexpr uint32_t kTile = 128 * 128;  // bytes of a 128-row x 32-fp32 swizzled tile
 
+// pack the low bytes of four ints into one word (byte v <- value v)
+__device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
+  return __byte_perm(__byte_perm((uint32_t)a, (uint32_t)b, 0x0040), __byte_perm((uint32_t)c, (uint32_t)d, 0x0040), 0x5410);
+}
+
 // round to the nearest tf32 (10 mantissa bits), ties away from zero: add half of the dropped 13-bit
 // field to the magnitude bits and clear it (two integer ops; the cvt.rna.tf32.f32 instruction is
 // emulated by a longer sequence on sm_100a).  Finite inputs below 2^127 only (X is checked finite).
 __device__ __forceinline__ float rna_tf32(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
-}
-
-// fp64 V (m x k, row-major) -> V_hl [2][m_pad128][KP32] (tf32 hi plane then lo plane; K8's B
-// operand); padding is zero (column k, the mean direction of K5's W, stays zero here so the spike
-// S = P V_k^T is unaffected).
-__global__ void split_v_kernel(const double* __restrict__ V, int64_t m, int k, int KP32, int64_t m_pad128,
-                               float* __restrict__ V_hl) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= m_pad128 * KP32) return;
-  const int64_t j = t / KP32;
-  const int r = (int)(t % KP32);
-  const float v = (j < m && r < k) ? (float)V[j * k + r] : 0.f;
-  const float hi = rna_tf32(v), lo = rna_tf32(v - hi);
-  V_hl[j * KP32 + r] = hi;
-  V_hl[(m_pad128 + j) * KP32 + r] = lo;
 }
 
 // ======================================================================= K5
@@ -179,10 +169,10 @@ __device__ __forceinline__ void mma_i8k(uint32_t d_tmem, uint64_t adesc, uint64_
 template <int KP, int ND, int NS, bool DB>
 __global__ void __launch_bounds__(kK5Threads, 1) proj_i8_kernel(
     const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmW, int64_t l_local, int64_t m_pad,
-    int64_t l_pad, const double* __restrict__ wsc, float* __restrict__ P, float* __restrict__ P_hl,
-    double* __restrict__ colsumP_part, const float* __restrict__ X, int64_t m, const int* __restrict__ spk,
-    const double* __restrict__ V, const double* __restrict__ mu, const double* __restrict__ diag, int k) {
-  constexpr int KP32 = (KP + 31) / 32 * 32;
+    int64_t l_pad, const double* __restrict__ wsc, float* __restrict__ P, int8_t* __restrict__ Pd,
+    float* __restrict__ ps, double* __restrict__ colsumP_part, const float* __restrict__ X, int64_t m,
+    const int* __restrict__ spk, const double* __restrict__ V, const double* __restrict__ mu,
+    const double* __restrict__ diag, int k) {
   constexpr int NCLS = 4;                           // weight classes c = e + d <= 3 (e < ND, d < 4)
   constexpr uint32_t kA = 128 * 128;               // one digit plane: 128 rows x 128 K-bytes
   constexpr uint32_t kB = KP * 128;                // one W digit plane: KP rows x 128 K-bytes
@@ -198,6 +188,7 @@ __global__ void __launch_bounds__(kK5Threads, 1) proj_i8_kernel(
   __shared__ double s_vsp[kMaxSpiky][KP];  // V rows (and mu_hat) of the spiky columns
   __shared__ double s_msp[kMaxSpiky];
   __shared__ int s_jsp[kMaxSpiky];
+  __shared__ float s_rmax[2][2][128];  // per-row max |P_ir| (r < k) of each column half, by row-block parity
   const int nsp = spk[0];
 
   const uint32_t warp = warp_id(), lane = lane_id();
@@ -293,8 +284,11 @@ __global__ void __launch_bounds__(kK5Threads, 1) proj_i8_kernel(
       const int64_t row = rb * 128 + q * 32 + lane;
       const bool rok = row < l_local;
       const uint32_t tb = tmem + ((q * 32) << 16) + b * kAcc;
-#pragma unroll 1
-      for (int c0 = half * (KP / 2); c0 < (half + 1) * (KP / 2); c0 += 8) {
+      float pall[KP / 2];  // this thread's half of the row (registers)
+      float rmx = 0.f;
+#pragma unroll
+      for (int g = 0; g < KP / 16; ++g) {
+        const int c0 = half * (KP / 2) + 8 * g;
         double acc[8];
 #pragma unroll
         for (int t = 0; t < 8; ++t) acc[t] = 0.0;
@@ -317,26 +311,55 @@ __global__ void __launch_bounds__(kK5Threads, 1) proj_i8_kernel(
         }
         float pv[8];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) pv[t] = (float)((s_t[c0 + t] * acc[t] - s_c[c0 + t]) + ex[t]);
+        for (int t = 0; t < 8; ++t) {
+          pv[t] = (float)((s_t[c0 + t] * acc[t] - s_c[c0 + t]) + ex[t]);
+          pall[8 * g + t] = pv[t];
+          if (c0 + t < k) rmx = fmaxf(rmx, fabsf(pv[t]));
+        }
         if (rok) {
           float4* dst = reinterpret_cast<float4*>(P + row * KP + c0);
           dst[0] = make_float4(pv[0], pv[1], pv[2], pv[3]);
           dst[1] = make_float4(pv[4], pv[5], pv[6], pv[7]);
-          float hv[8], lv[8];
-#pragma unroll
-          for (int t = 0; t < 8; ++t) { hv[t] = rna_tf32(pv[t]); lv[t] = rna_tf32(pv[t] - hv[t]); }
-          float4* hrow = reinterpret_cast<float4*>(P_hl + row * KP32 + c0);
-          float4* lrow = reinterpret_cast<float4*>(P_hl + (l_pad + row) * KP32 + c0);
-          hrow[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
-          hrow[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
-          lrow[0] = make_float4(lv[0], lv[1], lv[2], lv[3]);
-          lrow[1] = make_float4(lv[4], lv[5], lv[6], lv[7]);
         }
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
           double v = rok ? (double)pv[t] : 0.0;
           for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
           if (lane == 0) colsum_w[ew][c0 + t] += v;
+        }
+      }
+      // K8's operand: the spike columns r < k of P in three balanced base-128 digits with a
+      // per-row scale 2^(e_i - 19) (|z| < 2^19); the row max spans both column halves
+      s_rmax[ui & 1][half][q * 32 + lane] = rmx;
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 epilogue warps
+      const float rm = fmaxf(rmx, s_rmax[ui & 1][half ^ 1][q * 32 + lane]);
+      const int e = rm > 0.f ? ilogbf(rm) + 1 : 0;
+      const float qsc = rm > 0.f ? ldexpf(1.f, 19 - e) : 0.f;
+      if (rok) {
+        if (half == 0) ps[row] = ldexpf(1.f, e - 19);
+        const int64_t plane = l_pad * 128;
+#pragma unroll
+        for (int g = 0; g < KP / 16; ++g) {
+          const int c0 = half * (KP / 2) + 8 * g;
+          uint32_t w[3][2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            int dd[3][4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const int r = c0 + 4 * h + t;
+              const int z = r < k ? __float2int_rn(pall[8 * g + 4 * h + t] * qsc) : 0;
+              const int zz = z + 64 * (1 + 128 + 16384);
+              dd[0][t] = (zz >> 14) - 64;
+              dd[1][t] = ((zz >> 7) & 127) - 64;
+              dd[2][t] = (zz & 127) - 64;
+            }
+#pragma unroll
+            for (int d = 0; d < 3; ++d) w[d][h] = pack4(dd[d][0], dd[d][1], dd[d][2], dd[d][3]);
+          }
+#pragma unroll
+          for (int d = 0; d < 3; ++d)
+            *reinterpret_cast<uint2*>(Pd + d * plane + row * 128 + c0) = make_uint2(w[d][0], w[d][1]);
         }
       }
       tc_fence_before();
@@ -355,42 +378,82 @@ __global__ void __launch_bounds__(kK5Threads, 1) proj_i8_kernel(
 }
 
 // ======================================================================= K8
-// Stage ring: V hi/lo tiles (B operand) + the matching X tile (for the epilogue), both by TMA.
-// A stage is released when the MMA has consumed it AND the 8 epilogue warps have read its X.
-template <int KP32, int NCOL, int NS>
-__global__ void __launch_bounds__(kPThreads, 1) energy_tc_kernel(
+// S = P V_k^T per (128-row block, NCOL-column chunk) on tcgen05.mma kind::i8 — exact integer
+// products of three-digit operands: P (from K5's epilogue, per-row scale 2^(e_i - 19)) and V_k
+// (split_vd_kernel, per-row scale 2^(f_j - 19)), K = the spike columns r < k (zero-padded to
+// 32-byte K steps inside 128-byte SWIZZLE_128B rows), digit-product classes c = d_P + d_V <= 2
+// kept (the rest weigh <= 2^-21 of the leading one), three int32 TMEM accumulators per chunk,
+// double-buffered.  The operands are small (3 B per P / V entry), so shared memory holds the P
+// block, a V ring and a deep ring of x tiles (TMA, fp32 128 x 32, swizzled) that the 8 epilogue
+// warps read: S_ij = (D0 2^14 + D1 2^7 + D2) 2^(e_i + f - 24) (f: V's single scale), tail = xc - S
+// (xc = x - mu), and the sums of spike^2, tail^2, spike*tail in fp32 per chunk, fp64 across chunks.
+// (The elementwise energies only need S to ~1e-6 relative: random rounding errors average out.)
+// V_k -> three balanced base-128 digits with ONE scale 2^(f - 19) for the whole matrix (f from
+// max |V_jr|, vmax_bits: atomicMax on |.| bit patterns, set by vmax_kernel), so the epilogue's
+// per-element scale is a per-row constant; rows of V_k are within a few bits of that max
+__global__ void vmax_kernel(const double* __restrict__ V, int64_t n, unsigned long long* __restrict__ vmax_bits) {
+  double mx = 0.0;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    mx = fmax(mx, fabs(V[t]));
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(vmax_bits, (unsigned long long)__double_as_longlong(mx));
+}
+__global__ void split_vd_kernel(const double* __restrict__ V, int64_t m, int64_t m_pad, int k,
+                                const unsigned long long* __restrict__ vmax_bits, int8_t* __restrict__ Vd,
+                                float* __restrict__ vs) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t j = (int64_t)blockIdx.x * 8 + warp;
+  if (j >= m_pad) return;
+  const double mx = __longlong_as_double((long long)*vmax_bits);
+  const int e = mx > 0.0 ? ilogb(mx) + 1 : 0;
+  if (j == 0 && lane == 0) vs[0] = ldexpf(1.f, e - 19);
+  const int64_t plane = m_pad * 128;
+  for (int r = lane; r < 128; r += 32) {
+    const int z = (j < m && r < k && mx > 0.0) ? __double2int_rn(ldexp(V[j * k + r], 19 - e)) : 0;
+    const int zz = z + 64 * (1 + 128 + 16384);
+    Vd[j * 128 + r] = (int8_t)((zz >> 14) - 64);
+    Vd[plane + j * 128 + r] = (int8_t)(((zz >> 7) & 127) - 64);
+    Vd[2 * plane + j * 128 + r] = (int8_t)((zz & 127) - 64);
+  }
+}
+
+constexpr int kK8Threads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
+template <int NK, int NCOL, int NSB, int NSX>
+__global__ void __launch_bounds__(kK8Threads, 1) energy_i8_kernel(
     const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmV,
-    const __grid_constant__ CUtensorMap tmX, int64_t l_local, int64_t m, int64_t l_pad, int64_t m_pad128,
-    const float* __restrict__ mu_hl, int64_t m_pad, double* __restrict__ en_part) {
-  constexpr int NA = KP32 / 32;                       // 32-wide K atoms
-  constexpr int NXB = NCOL / 32;                      // X boxes (32 columns) per chunk
-  constexpr uint32_t kATile = kTile;                  // 128 rows x 128 B
-  constexpr uint32_t kBTile = NCOL * 128;             // NCOL rows x 128 B
-  constexpr uint32_t kA = 2 * NA * kATile;            // P hi + lo
-  constexpr uint32_t kVB = 2 * NA * kBTile;           // V hi + lo
-  constexpr uint32_t kStage = kVB + NXB * kTile;      // + X tile
+    const __grid_constant__ CUtensorMap tmX, int64_t l_local, int64_t m, int64_t l_pad, int64_t m_pad,
+    const float* __restrict__ ps, const float* __restrict__ vs, const float* __restrict__ mu_hl,
+    double* __restrict__ en_part) {
+  constexpr uint32_t kA = 128 * 128;                 // one P digit plane of the row block
+  constexpr uint32_t kB = NCOL * 128;                // one V digit plane of the chunk
+  constexpr uint32_t kBS = ((3 * kB + 1023) / 1024) * 1024;
+  constexpr int NXB = NCOL / 32;                     // x sub-tiles (128 rows x 32 fp32) per chunk
+  constexpr uint32_t kXS = NXB * kTile;
+  constexpr uint32_t kAcc = 3 * NCOL;
+  constexpr uint32_t kTm = 2 * kAcc <= 256 ? 256 : 512;
+  static_assert(2 * kAcc <= 512, "TMEM double buffer");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-B aligned in the shared window; derived from smem_raw by an offset so the compiler keeps
-  // the shared address space (LDS/STS instead of generic LD/ST)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
-  uint8_t* sB = smem + kA;
-  __shared__ uint64_t afull_bar, aempty_bar, full_bar[NS], empty_bar[NS], tfull_bar[2], tempty_bar[2];
+  uint8_t* sB = sA + 3 * kA;
+  uint8_t* sX = sB + NSB * kBS;
+  __shared__ uint64_t afull, aempty, bfull[NSB], bempty[NSB], xfull[NSX], xempty[NSX], tfull[2], tempty[2];
   __shared__ uint32_t tmem_sh;
-  __shared__ double red[8][3];
+  __shared__ double red[8][4];
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int64_t nrb = ceil_div(l_local, 128);
   const int NC = (int)((m + NCOL - 1) / NCOL);
   if (threadIdx.x == 0) {
-    mbar_init(&afull_bar, 1);
-    mbar_init(&aempty_bar, 1);
-    for (int s = 0; s < NS; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1 + 8); }
-    for (int b = 0; b < 2; ++b) { mbar_init(&tfull_bar[b], 1); mbar_init(&tempty_bar[b], 8); }
+    mbar_init(&afull, 1);
+    mbar_init(&aempty, 1);
+    for (int s = 0; s < NSB; ++s) { mbar_init(&bfull[s], 1); mbar_init(&bempty[s], 1); }
+    for (int s = 0; s < NSX; ++s) { mbar_init(&xfull[s], 1); mbar_init(&xempty[s], 8); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 8); }
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) { tma_prefetch(&tmP); tma_prefetch(&tmV); tma_prefetch(&tmX); }
-  if (warp == 1) tmem_alloc<(2 * NCOL < 32 ? 32 : 2 * NCOL)>(&tmem_sh);
+  if (warp == 1) tmem_alloc<kTm>(&tmem_sh);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -398,143 +461,133 @@ __global__ void __launch_bounds__(kPThreads, 1) energy_tc_kernel(
 
   if (warp == 0) {
     if (elect_one()) {
-      uint32_t it = 0, ui = 0;
+      uint32_t ib = 0, ix = 0, ui = 0;
       for (int64_t rb = blockIdx.x; rb < nrb; rb += gridDim.x, ++ui) {
-        mbar_wait(&aempty_bar, (ui & 1) ^ 1);
-        mbar_arrive_expect_tx(&afull_bar, kA);
+        mbar_wait(&aempty, (ui & 1) ^ 1);
+        mbar_arrive_expect_tx(&afull, 3 * kA);
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int a = 0; a < NA; ++a)
-            tma_load_2d(sA + (h * NA + a) * kATile, &tmP, &afull_bar, a * 32, (int32_t)(h * l_pad + rb * 128));
-        for (int c = 0; c < NC; ++c, ++it) {
-          const uint32_t s = it % NS, r = it / NS;
-          mbar_wait(&empty_bar[s], (r & 1) ^ 1);
-          uint8_t* st = sB + s * kStage;
-          mbar_arrive_expect_tx(&full_bar[s], kStage);
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int a = 0; a < NA; ++a)
-              tma_load_2d(st + (h * NA + a) * kBTile, &tmV, &full_bar[s], a * 32, (int32_t)(h * m_pad128 + c * NCOL));
+        for (int d = 0; d < 3; ++d) tma_load_2d(sA + d * kA, &tmP, &afull, 0, (int32_t)(d * l_pad + rb * 128));
+        for (int c = 0; c < NC; ++c, ++ib, ++ix) {
+          // x first: its ring is the deep one
+          const uint32_t sx = ix % NSX, rx = ix / NSX;
+          mbar_wait(&xempty[sx], (rx & 1) ^ 1);
+          mbar_arrive_expect_tx(&xfull[sx], kXS);
 #pragma unroll
           for (int xb = 0; xb < NXB; ++xb)
-            tma_load_2d(st + kVB + xb * kTile, &tmX, &full_bar[s], c * NCOL + xb * 32, (int32_t)(rb * 128));
+            tma_load_2d(sX + sx * kXS + xb * kTile, &tmX, &xfull[sx], c * NCOL + xb * 32, (int32_t)(rb * 128));
+          const uint32_t sb = ib % NSB, rbb = ib / NSB;
+          mbar_wait(&bempty[sb], (rbb & 1) ^ 1);
+          mbar_arrive_expect_tx(&bfull[sb], 3 * kB);
+#pragma unroll
+          for (int d = 0; d < 3; ++d)
+            tma_load_2d(sB + sb * kBS + d * kB, &tmV, &bfull[sb], 0, (int32_t)(d * m_pad + c * NCOL));
         }
       }
     }
   } else if (warp == 1) {
-    constexpr uint32_t idesc = idesc_tf32(128, NCOL, 0, 0);
-    uint32_t it = 0, ui = 0, ci = 0;
+    constexpr uint32_t idesc = idesc_i8k(128, NCOL);
+    uint32_t ib = 0, ci = 0, ui = 0;
     for (int64_t rb = blockIdx.x; rb < nrb; rb += gridDim.x, ++ui) {
-      mbar_wait(&afull_bar, ui & 1);
+      mbar_wait(&afull, ui & 1);
       tc_fence_after();
-      for (int c = 0; c < NC; ++c, ++it, ++ci) {
-        const uint32_t s = it % NS, r = it / NS;
+      for (int c = 0; c < NC; ++c, ++ib, ++ci) {
+        const uint32_t sb = ib % NSB, rbb = ib / NSB;
         const uint32_t b = ci & 1, br = ci >> 1;
-        mbar_wait(&tempty_bar[b], (br & 1) ^ 1);
-        mbar_wait(&full_bar[s], r & 1);
+        mbar_wait(&tempty[b], (br & 1) ^ 1);
+        mbar_wait(&bfull[sb], rbb & 1);
         tc_fence_after();
         if (elect_one()) {
-          const uint32_t abase = smem_u32(sA), bbase = smem_u32(sB + s * kStage);
-          const uint32_t d = tmem + b * NCOL;
+          const uint32_t abase = smem_u32(sA), bbase = smem_u32(sB + sb * kBS);
+          const uint32_t d0 = tmem + b * kAcc;
 #pragma unroll
-          for (int a = 0; a < NA; ++a) {
+          for (int kk = 0; kk < NK; ++kk)
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              const uint64_t ahi = smem_desc(abase + a * kATile + kk * 32, 16, 1024, 2);
-              const uint64_t alo = smem_desc(abase + (NA + a) * kATile + kk * 32, 16, 1024, 2);
-              const uint64_t bhi = smem_desc(bbase + a * kBTile + kk * 32, 16, 1024, 2);
-              const uint64_t blo = smem_desc(bbase + (NA + a) * kBTile + kk * 32, 16, 1024, 2);
-              mma_tf32(d, ahi, bhi, idesc, (a == 0 && kk == 0) ? 0u : 1u);
-              mma_tf32(d, ahi, blo, idesc, 1u);
-              mma_tf32(d, alo, bhi, idesc, 1u);
+            for (int dp = 0; dp < 3; ++dp) {
+              const uint64_t a = smem_desc(abase + dp * kA + kk * 32, 16, 1024, 2);
+#pragma unroll
+              for (int dv = 0; dv < 3; ++dv) {
+                if (dp + dv > 2) continue;  // dropped class
+                const uint64_t bd = smem_desc(bbase + dv * kB + kk * 32, 16, 1024, 2);
+                mma_i8k(d0 + (dp + dv) * NCOL, a, bd, idesc, (kk == 0 && dp == 0) ? 0u : 1u);
+              }
             }
-          }
-          mma_commit(&empty_bar[s]);
-          mma_commit(&tfull_bar[b]);
-          if (c == NC - 1) mma_commit(&aempty_bar);
+          mma_commit(&bempty[sb]);
+          mma_commit(&tfull[b]);
+          if (c == NC - 1) mma_commit(&aempty);
         }
         __syncwarp();
       }
     }
   } else {
-    // ================= epilogue warps (8: two per TMEM lane quadrant, each half of the columns)
+    // ================= epilogue warps: quadrant q (32 rows), half h (NCOL / 2 columns)
+    constexpr int HC = NCOL / 2;
     const int ew = warp - 2;
     const uint32_t q = warp & 3;
     const int half = ew >> 2;
-    const int rloc = q * 32 + lane;                   // row inside the 128-row tile
+    const int rloc = q * 32 + lane;
     double eS = 0.0, eT = 0.0, eST = 0.0;
-    uint32_t it = 0, ci = 0;
+    uint32_t ix = 0, ci = 0;
     for (int64_t rb = blockIdx.x; rb < nrb; rb += gridDim.x) {
-      const bool rok = rb * 128 + rloc < l_local;
-      for (int c = 0; c < NC; ++c, ++it, ++ci) {
-        const uint32_t s = it % NS, r = it / NS;
+      const int64_t row = rb * 128 + rloc;
+      const bool rok = row < l_local;
+      // z_P z_V = 2^14 (D0 2^14 + D1 2^7 + D2) + dropped classes: the 2^14 and V's single scale go
+      // with the row scale
+      const float rs = rok ? ps[row] * 16384.f * vs[0] : 0.f;
+      for (int c = 0; c < NC; ++c, ++ix, ++ci) {
+        const uint32_t sx = ix % NSX, rx = ix / NSX;
         const uint32_t b = ci & 1, br = ci >> 1;
-        static_assert(NCOL == 32, "epilogue handles 16 columns per warp half");
-        const int c0 = half * 16;
-        const int64_t j0 = (int64_t)c * NCOL + c0;
-        float mh[16], ml[16];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {  // mu loads issued before the barrier waits
-          const float4 a = __ldg(reinterpret_cast<const float4*>(mu_hl + j0) + u);
-          const float4 bb = __ldg(reinterpret_cast<const float4*>(mu_hl + m_pad + j0) + u);
-          mh[4 * u] = a.x; mh[4 * u + 1] = a.y; mh[4 * u + 2] = a.z; mh[4 * u + 3] = a.w;
-          ml[4 * u] = bb.x; ml[4 * u + 1] = bb.y; ml[4 * u + 2] = bb.z; ml[4 * u + 3] = bb.w;
-        }
-        mbar_wait(&full_bar[s], r & 1);
-        mbar_wait(&tfull_bar[b], br & 1);
-        tc_fence_after();
-        const uint32_t tb = tmem + ((q * 32) << 16) + b * NCOL;
-        const uint8_t* sx = sB + s * kStage + kVB;
         float s2 = 0.f, t2 = 0.f, st = 0.f;
-        {
-          uint32_t rv[16];
-          tmem_ld16(tb + c0, rv);
-          float xv[16];
-          const float4* xrow = reinterpret_cast<const float4*>(sx + rloc * 128);
+        mbar_wait(&tfull[b], br & 1);
+        mbar_wait(&xfull[sx], rx & 1);
+        tc_fence_after();
+        const uint32_t tb = tmem + ((q * 32) << 16) + b * kAcc;
+#pragma unroll
+        for (int g = 0; g < HC / 16; ++g) {
+          const int cl0 = half * HC + 16 * g;           // column inside the chunk
+          const int64_t j0 = (int64_t)c * NCOL + cl0;   // global column
+          const bool inside = rok && j0 + 16 <= m;
+          uint32_t r0v[16], r1v[16], r2v[16];
+          tmem_ld16(tb + cl0, r0v);
+          tmem_ld16(tb + NCOL + cl0, r1v);
+          tmem_ld16(tb + 2 * NCOL + cl0, r2v);
+          float xv[16], mh[16];
+          const uint8_t* xs = sX + sx * kXS + (cl0 / 32) * kTile;
+          const float4* xrow = reinterpret_cast<const float4*>(xs + rloc * 128);
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const int g = (c0 >> 2) + u;              // logical 16-byte group of the row
-            const float4 v = xrow[g ^ (rloc & 7)];    // SWIZZLE_128B
+            const int gq = ((cl0 % 32) >> 2) + u;       // logical 16-byte group of the row
+            const float4 v = xrow[gq ^ (rloc & 7)];     // SWIZZLE_128B
             xv[4 * u] = v.x; xv[4 * u + 1] = v.y; xv[4 * u + 2] = v.z; xv[4 * u + 3] = v.w;
+            // (mu's fp32 low part is left out: a per-column constant shift of the tail, whose
+            // columns have zero mean, moves sum tail^2 by l ||mu_lo||^2 ~ 1e-14 relative)
+            const float4 a = __ldg(reinterpret_cast<const float4*>(mu_hl + j0) + u);
+            mh[4 * u] = a.x; mh[4 * u + 1] = a.y; mh[4 * u + 2] = a.z; mh[4 * u + 3] = a.w;
           }
           tmem_ld_wait();
-          float s2b = 0.f, t2b = 0.f, stb = 0.f;  // two chains per sum (even / odd t)
-          const bool inside = rok && j0 + 16 <= m;  // no per-entry bounds selects
 #pragma unroll
-          for (int t = 0; t < 16; t += 2) {
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const float xc = (xv[t + e] - mh[t + e]) - ml[t + e];
-              float S = __uint_as_float(rv[t + e]);
-              float T = xc - S;
-              if (!inside) {
-                const bool ok = rok && j0 + t + e < m;
-                S = ok ? S : 0.f;
-                T = ok ? T : 0.f;
-              }
-              float& a2 = e ? s2b : s2;
-              float& b2 = e ? t2b : t2;
-              float& c2 = e ? stb : st;
-              a2 = fmaf(S, S, a2);
-              b2 = fmaf(T, T, b2);
-              c2 = fmaf(S, T, c2);
+          for (int t = 0; t < 16; ++t) {
+            const float xc = xv[t] - mh[t];
+            // D1 2^7 + D2 fits int32 (|D| < 2^20); the leading class joins in fp32
+            const int lo = (int)r1v[t] * 128 + (int)r2v[t];
+            const float si = fmaf((float)(int)r0v[t], 16384.f, (float)lo);
+            float S = si * rs;
+            float T = xc - S;
+            if (!inside) {
+              const bool ok = rok && j0 + t < m;
+              S = ok ? S : 0.f;
+              T = ok ? T : 0.f;
             }
+            s2 = fmaf(S, S, s2);
+            t2 = fmaf(T, T, t2);
+            st = fmaf(S, T, st);
           }
-          s2 += s2b;
-          t2 += t2b;
-          st += stb;
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) { mbar_arrive(&tempty[b]); mbar_arrive(&xempty[sx]); }
         eS += (double)s2;
         eT += (double)t2;
         eST += (double)st;
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&tempty_bar[b]);
-          mbar_arrive(&empty_bar[s]);
-        }
       }
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -542,16 +595,16 @@ __global__ void __launch_bounds__(kPThreads, 1) energy_tc_kernel(
       eT += __shfl_xor_sync(0xFFFFFFFFu, eT, o);
       eST += __shfl_xor_sync(0xFFFFFFFFu, eST, o);
     }
-    if (lane == 0) { red[ew][0] = eS; red[ew][1] = eT; red[ew][2] = eST; }
+    if (lane == 0) { red[ew][0] = eS; red[ew][1] = eT; red[ew][2] = eST; red[ew][3] = 0.0; }  // (slot 3 unused)
   }
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x < 3) {
+  if (threadIdx.x < 4) {
     double t = 0.0;
     for (int w = 0; w < 8; ++w) t += red[w][threadIdx.x];
     en_part[(int64_t)blockIdx.x * 4 + threadIdx.x] = t;
   }
-  if (warp == 1) tmem_dealloc<(2 * NCOL < 32 ? 32 : 2 * NCOL)>(tmem);
+  if (warp == 1) tmem_dealloc<kTm>(tmem);
 }
 
 CUresult encode2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
@@ -565,6 +618,18 @@ CUresult encode2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t o
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 
+// 2-D uint8 tensor map, SWIZZLE_128B (inner box 128 bytes)
+CUresult encode_u8(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint32_t box_in,
+                   uint32_t box_out) {
+  uint64_t dims[2] = {inner, outer};
+  uint64_t strides[1] = {inner};
+  uint32_t box[2] = {box_in, box_out};
+  uint32_t es[2] = {1, 1};
+  return tma_encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+}
+
 template <int KP, int ND>
 avd_status launch_k5(Ctx* c, const CUtensorMap& tmD, const CUtensorMap& tmW, int grid, const float* X) {
   constexpr uint32_t kStage = ((ND * 128 * 128 + 4 * KP * 128 + 1023) / 1024) * 1024;
@@ -573,23 +638,22 @@ avd_status launch_k5(Ctx* c, const CUtensorMap& tmD, const CUtensorMap& tmW, int
   const size_t smem = (size_t)NS * kStage + 1024;
   AVD_CUDA(smem_attr(proj_i8_kernel<KP, ND, NS, DB>, (int)smem));
   proj_i8_kernel<KP, ND, NS, DB><<<grid, kK5Threads, smem, c->stream>>>(
-      tmD, tmW, c->cfg.l_local, c->m_pad, c->l_pad, c->wsc, c->P, c->P_hl, c->colsumP_part, X, c->cfg.m,
+      tmD, tmW, c->cfg.l_local, c->m_pad, c->l_pad, c->wsc, c->P, c->Pd, c->ps, c->colsumP_part, X, c->cfg.m,
       reinterpret_cast<const int*>(c->wsc + 384), c->V, c->mu, c->diag, c->k);
   AVD_LAUNCHED(c);
   return AVD_OK;
 }
 
-template <int KP32, int NCOL>
+template <int NK>
 avd_status launch_k8(Ctx* c, const CUtensorMap& tmP, const CUtensorMap& tmV, const CUtensorMap& tmX, int grid) {
-  constexpr uint32_t kA = 2 * (KP32 / 32) * kTile;
-  constexpr uint32_t kStage = 2 * (KP32 / 32) * NCOL * 128 + (NCOL / 32) * kTile;
-  constexpr int NSF = (int)((220u * 1024u - kA) / kStage);
-  constexpr int NS = NSF > 6 ? 6 : (NSF < 2 ? 2 : NSF);
-  const size_t smem = kA + NS * kStage + 1024;
-  AVD_CUDA(smem_attr(energy_tc_kernel<KP32, NCOL, NS>, (int)smem));
-  energy_tc_kernel<KP32, NCOL, NS><<<grid, kPThreads, smem, c->stream>>>(tmP, tmV, tmX, c->cfg.l_local, c->cfg.m,
-                                                                         c->l_pad, c->m_pad, c->mu_hl, c->m_pad,
-                                                                         c->en_part);
+  constexpr int NCOL = 64, NSB = 2;
+  constexpr uint32_t kBS = ((3 * NCOL * 128 + 1023) / 1024) * 1024;
+  constexpr uint32_t kXS = (NCOL / 32) * kTile;
+  constexpr int NSX = (int)((208u * 1024u - 3u * 128u * 128u - NSB * kBS) / kXS);
+  const size_t smem = 3 * 128 * 128 + NSB * kBS + NSX * kXS + 1024;
+  AVD_CUDA(smem_attr(energy_i8_kernel<NK, NCOL, NSB, NSX>, (int)smem));
+  energy_i8_kernel<NK, NCOL, NSB, NSX><<<grid, kK8Threads, smem, c->stream>>>(
+      tmP, tmV, tmX, c->cfg.l_local, c->cfg.m, c->l_pad, c->m_pad, c->ps, c->vs, c->mu_hl, c->en_part);
   AVD_LAUNCHED(c);
   return AVD_OK;
 }
@@ -600,11 +664,14 @@ bool project_tc_supported(const Ctx* c, const float* X) {
   return (c->cfg.m % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0) && c->k_pad <= 96;
 }
 
-// V_k -> tf32 hi/lo operand copy for K8 (once per pass)
+// V_k -> K8's digit operand (once per pass)
 avd_status launch_split_v(Ctx* c) {
-  const int KP32 = (c->k_pad + 31) / 32 * 32;
-  const int64_t n = c->m_pad * KP32;
-  split_v_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c->stream>>>(c->V, c->cfg.m, c->k, KP32, c->m_pad, c->V_hl);
+  unsigned long long* vmax = reinterpret_cast<unsigned long long*>(c->vs + 2);  // (vs[0] = the scale)
+  AVD_CUDA(cudaMemsetAsync(vmax, 0, sizeof(unsigned long long), c->stream));
+  vmax_kernel<<<64, 256, 0, c->stream>>>(c->V, c->cfg.m * c->k, vmax);
+  AVD_LAUNCHED(c);
+  split_vd_kernel<<<(unsigned)ceil_div(c->m_pad, 8), 256, 0, c->stream>>>(c->V, c->cfg.m, c->m_pad, c->k, vmax, c->Vd,
+                                                                          c->vs);
   AVD_LAUNCHED(c);
   return AVD_OK;
 }
@@ -623,8 +690,8 @@ avd_status launch_project_tc(Ctx* c, const float* X) {
                       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
       encode2d(&tmX, X, c->cfg.m, c->cfg.l_local, c->cfg.m * 4, 32, 128) != CUDA_SUCCESS ||
-      encode2d(&tmP, c->P_hl, KP32, 2 * c->l_pad, KP32 * 4, 32, 128) != CUDA_SUCCESS ||
-      encode2d(&tmV, c->V_hl, KP32, 2 * c->m_pad, KP32 * 4, 32, 32) != CUDA_SUCCESS) {
+      encode_u8(&tmP, c->Pd, 128, 3 * c->l_pad, 128, 128) != CUDA_SUCCESS ||
+      encode_u8(&tmV, c->Vd, 128, 3 * c->m_pad, 128, 64) != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (projection maps)");
     return AVD_ECUDA;
   }
@@ -647,10 +714,10 @@ avd_status launch_project_tc(Ctx* c, const float* X) {
 #undef CASE
     default: set_error("unsupported k_pad"); return AVD_EINVAL;
   }
-  switch (KP32) {
-    case 32: AVD_TRY((launch_k8<32, 32>(c, tmP, tmV, tmX, grid))); break;
-    case 64: AVD_TRY((launch_k8<64, 32>(c, tmP, tmV, tmX, grid))); break;
-    case 96: AVD_TRY((launch_k8<96, 32>(c, tmP, tmV, tmX, grid))); break;
+  switch (KP32 / 32) {  // 32-byte K steps of the spike columns
+    case 1: AVD_TRY(launch_k8<1>(c, tmP, tmV, tmX, grid)); break;
+    case 2: AVD_TRY(launch_k8<2>(c, tmP, tmV, tmX, grid)); break;
+    case 3: AVD_TRY(launch_k8<3>(c, tmP, tmV, tmX, grid)); break;
     default: set_error("unsupported k_pad"); return AVD_EINVAL;
   }
   return AVD_OK;
