@@ -32,6 +32,17 @@ EXPORTS = ["avd_plan", "avd_create", "avd_destroy", "avd_get_plan", "avd_decompo
            "avd_stage_gram", "avd_stage_eig", "avd_stage_project", "avd_stage_select",
            "avd_stage_gather", "avd_stage_report", "avd_tie_quota", "avd_launch_count", "avd_strerror",
            "avd_last_error", "avd_stage_eig_dist", "avd_decompose_sharded", "avd_exchange_nccl"]
+# every symbol include/avd_averis.h declares
+EXPORTS_AVERIS = ["avd_averis_create", "avd_averis_destroy", "avd_averis_set_weight", "avd_averis_forward",
+                  "avd_averis_forward_host", "avd_averis_buffer", "avd_averis_launch_count"]
+AVD_AVERIS_STOCHASTIC, AVD_AVERIS_VANILLA = 1, 2
+AV_BUF = dict(MU=0, XCODES=1, XSF=2, WCODES=3, WSF=4, MUCODES=5, MUSF=6, GSCALE=7, BIAS=8)
+
+
+class avd_averis_config(ctypes.Structure):
+    _fields_ = [("l", ctypes.c_int64), ("m", ctypes.c_int64), ("n", ctypes.c_int64),
+                ("flags", ctypes.c_int32), ("seed", ctypes.c_uint64), ("device", ctypes.c_int32),
+                ("stream", ctypes.c_void_p)]
 
 
 class avd_plan_t(ctypes.Structure):
@@ -117,6 +128,17 @@ def lib() -> ctypes.CDLL:
         L.avd_strerror.restype = ctypes.c_char_p
         L.avd_last_error.argtypes = []
         L.avd_last_error.restype = ctypes.c_char_p
+        L.avd_averis_create.argtypes = [ctypes.POINTER(avd_averis_config), ctypes.POINTER(P)]
+        L.avd_averis_destroy.argtypes = [P]
+        L.avd_averis_set_weight.argtypes = [P, P]
+        L.avd_averis_forward.argtypes = [P, P, P]
+        L.avd_averis_forward_host.argtypes = [P, P, P]
+        L.avd_averis_buffer.argtypes = [P, I32, ctypes.POINTER(P), ctypes.POINTER(ctypes.c_size_t)]
+        L.avd_averis_launch_count.argtypes = [P]
+        L.avd_averis_launch_count.restype = I64
+        for name in EXPORTS_AVERIS:
+            if name != "avd_averis_launch_count":
+                getattr(L, name).restype = ctypes.c_int
         for name in EXPORTS:
             if name not in ("avd_destroy", "avd_launch_count", "avd_strerror", "avd_last_error"):
                 getattr(L, name).restype = ctypes.c_int
@@ -228,3 +250,38 @@ def avd_tie_quota(sel_counts, tie_counts, rank: int, q: int):
     check(lib().avd_tie_quota(S, T, world, rank, int(q), ctypes.byref(quota), ctypes.byref(off)),
           "avd_tie_quota")
     return quota.value, off.value
+
+
+# ---- Averis NVFP4 forward GeMM (include/avd_averis.h) ---------------------------------------
+def avd_averis_create(cfg: avd_averis_config) -> ctypes.c_void_p:
+    h = ctypes.c_void_p()
+    check(lib().avd_averis_create(ctypes.byref(cfg), ctypes.byref(h)), "avd_averis_create")
+    return h
+
+
+def avd_averis_destroy(h) -> None:
+    check(lib().avd_averis_destroy(h), "avd_averis_destroy")
+
+
+def avd_averis_set_weight(h, W_ptr: int):
+    return check(lib().avd_averis_set_weight(h, ctypes.c_void_p(W_ptr)), "avd_averis_set_weight")
+
+
+def avd_averis_forward(h, X_ptr: int, Y_ptr: int):
+    return check(lib().avd_averis_forward(h, ctypes.c_void_p(X_ptr), ctypes.c_void_p(Y_ptr)), "avd_averis_forward")
+
+
+def avd_averis_forward_host(h, X_ptr: int, Y_ptr: int):
+    return check(lib().avd_averis_forward_host(h, ctypes.c_void_p(X_ptr), ctypes.c_void_p(Y_ptr)),
+                 "avd_averis_forward_host")
+
+
+def avd_averis_buffer(h, which: int):
+    p = ctypes.c_void_p()
+    n = ctypes.c_size_t()
+    check(lib().avd_averis_buffer(h, which, ctypes.byref(p), ctypes.byref(n)), "avd_averis_buffer")
+    return p.value, n.value
+
+
+def avd_averis_launch_count(h) -> int:
+    return int(lib().avd_averis_launch_count(h))

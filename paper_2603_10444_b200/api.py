@@ -192,7 +192,7 @@ class _CudaArray:
 
 
 _TYPESTR = {torch.float64: "<f8", torch.float32: "<f4", torch.int64: "<i8", torch.int32: "<i4",
-            torch.int8: "|i1"}
+            torch.int8: "|i1", torch.uint8: "|u1"}
 
 
 def _view(ptr: int, nbytes: int, dtype: torch.dtype, device: int, shape=None) -> torch.Tensor:

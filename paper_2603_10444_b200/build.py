@@ -26,7 +26,8 @@ def sources():
 
 def _deps():
     hdr = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
-    hdr.append(os.path.join(HERE, "..", "include", "avd.h"))
+    inc = os.path.join(HERE, "..", "include")
+    hdr += [os.path.join(inc, f) for f in os.listdir(inc) if f.endswith(".h")]
     return max(os.path.getmtime(h) for h in hdr)
 
 

@@ -216,3 +216,17 @@ def sweep_specs(seed: int = 0) -> list[SynthSpec]:
             out.append(SynthSpec(32768, 2048, seed=seed * 1000 + 2 * d + stage, f_mean=f,
                                  theta_1=th))
     return out
+
+
+def generate_weight(m: int, n: int, seed: int = 0, device: str | torch.device = "cpu") -> torch.Tensor:
+    """W [m, n] fp32 for the Averis GeMM: Irwin-Hall-12 entries / sqrt(m) (mean 0,
+    variance 1/m: a random-init linear layer), a pure function of (seed, k, j) like generate()."""
+    dev = torch.device(device)
+    kk = torch.arange(m, dtype=torch.int64, device=dev)
+    jj = torch.arange(n, dtype=torch.int64, device=dev)
+    base = hash32(hash32(kk ^ ((seed * 0x2545F491 + 0x68E31DA4) & M32)).unsqueeze(1) ^ hash32(jj ^ 0x5BD1E995).unsqueeze(0))
+    z = torch.zeros((m, n), dtype=torch.float64, device=dev)
+    for t in range(12):
+        z = z + _u24(hash32(base ^ ((0x1B873593 * (t + 1)) & M32))).to(torch.float64)
+    z = z / float(1 << 24) - 6.0
+    return (z / math.sqrt(m)).to(torch.float32)

@@ -12,16 +12,17 @@ from paper_2603_10444_b200 import _lib as L
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _header_functions():
-    src = open(os.path.join(ROOT, "include", "avd.h")).read()
+def _header_functions(name="avd.h"):
+    src = open(os.path.join(ROOT, "include", name)).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(avd_[a-z_0-9]+)\s*\(", src)))
 
 
-def test_exports_match_header():
+@pytest.mark.parametrize("header,exports", [("avd.h", L.EXPORTS), ("avd_averis.h", L.EXPORTS_AVERIS)])
+def test_exports_match_header(header, exports):
     lib = L.lib()
-    declared = _header_functions()
-    assert set(declared) == set(L.EXPORTS), (declared, L.EXPORTS)
+    declared = _header_functions(header)
+    assert set(declared) == set(exports), (declared, exports)
     for name in declared:
         assert hasattr(lib, name), name
 
