@@ -38,7 +38,11 @@ WORKLOADS = {
           "of l=32768, m=2048 (k=20)",
     "c4": "c4: single matrix l=131072, m=4096 (k=40), row-sharded over the GPUs",
     "c5": "c5: single matrix l=1048576, m=8192 (k=81), row-sharded over the GPUs",
+    "averis": "f3: Averis mean-residual NVFP4 forward GeMM, X l=131072 x m=4096 (the c4 activations) "
+              "times W m=4096 x n=4096 (PAPER.md:391-429)",
 }
+AVERIS_SHAPE = (131072, 4096, 4096)
+AVERIS_METRIC = "Averis NVFP4 forward GeMM throughput (2*l*m*n flop/s, mean split + quantisation inside)"
 
 
 def _peaks():
@@ -170,10 +174,42 @@ def cpu_baseline(spec, rows: int, eig: str):
                       f"{dt:.2f} s", "seconds": dt}
 
 
+def averis_cpu_baseline(rows: int):
+    """oracle/averis.py as it stands (numpy: fp32 quantiser decisions, fp64 GeMM) on rows
+    [0, rows) of the bench X with the full W."""
+    from oracle import averis as A
+    from oracle import oracle as O
+    from synth.gen import generate_weight
+    l, m, n = AVERIS_SHAPE
+    Xs = generate(config_spec("c4"), 0, rows).numpy()
+    W = generate_weight(m, n, seed=0).numpy()
+    t0 = time.perf_counter()
+    A.averis_forward(Xs, W)
+    dt = time.perf_counter() - t0
+    return {"value": 2.0 * rows * m * n / dt / 1e12, "unit": "TFLOP/s", "cores": O.host_cores(), "kind": "oracle",
+            "sample": f"rows [0,{rows}) of X x the full {m}x{n} W (quantise W, mu of the sample, X_R, fp64 "
+                      f"GeMM); {dt:.2f} s", "seconds": dt}
+
+
 def run_reference(args):
     """--impl reference: the fp64 CPU oracle as it stands, on a bounded sample per step."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
+        return
+    if args.config == "averis":
+        for _ in range(args.warmup):
+            averis_cpu_baseline(256)
+        cb = [averis_cpu_baseline(512) for _ in range(args.steps)]
+        v = statistics.median(c["value"] for c in cb)
+        line = {"impl": "reference", "metric": AVERIS_METRIC, "value": v, "unit": "TFLOP/s",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": statistics.median(c["seconds"] for c in cb) * 1e3, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": WORKLOADS["averis"], "sample_rows": 512},
+                "cpu_baseline": {k: cb[0][k] for k in ("unit", "cores", "kind", "sample")} | {"value": v},
+                "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "gpu_launches": 0}
+        print(json.dumps(line), flush=True)
         return
     from oracle import oracle as O
     O.build()
@@ -325,6 +361,105 @@ def run_c3(args, rank, world, local):
         sys.exit(3)
 
 
+# ------------------------------------------------------------------ f3: Averis NVFP4 GeMM
+def run_averis(args, rank, world, local):
+    """one step = avd_averis_forward on the c4 activations X (131072 x 4096) with a
+    4096 x 4096 weight: column statistics, mu_bar and mu_bar W_bar, NVFP4 quantisation of X_R, the
+    block-scaled tcgen05 GeMM and its epilogue (W quantised once, outside the step, as a weight
+    is between optimizer updates).  N > 1: replicas only — every rank runs its own micro-batch
+    (the split's mean is per micro-batch, the GeMM is local to the data-parallel rank)."""
+    import torch.distributed as dist
+    from paper_2603_10444_b200.averis import AverisGemm
+    from synth.gen import generate_weight
+    l, m, n = AVERIS_SHAPE
+    X = generate(config_spec("c4"), device="cuda")
+    W = generate_weight(m, n, seed=0, device="cuda")
+    Y = torch.empty(l, n, dtype=torch.float32, device="cuda")
+    g = AverisGemm(l, m, n, timing=True)
+    g.set_weight(W)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    for _ in range(args.warmup):
+        g(X, Y)
+    torch.cuda.synchronize()
+    # per-stage times (events inside the library, on its stream), one synchronised step at a time
+    st = []
+    for _ in range(max(3, args.steps // 2)):
+        g(X, Y)
+        st.append(g.stage_ms())
+    stage = [statistics.median(s[i] for s in st) for i in range(3)]
+    barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.15)
+    l0 = g.launches()
+    t_s, t_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_s.record()
+    for _ in range(args.steps):
+        g(X, Y)
+    t_e.record()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    launches = g.launches() - l0
+    ms = t_s.elapsed_time(t_e)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    flops = 2.0 * l * m * n
+    value = world * flops / (ms_step * 1e-3) / 1e12
+    e2e = None
+    if not args.no_e2e:
+        Xh = X.cpu().pin_memory()
+        Yh = torch.empty(l, n, dtype=torch.float32).pin_memory()
+        g.forward_host(Xh, Yh)
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            g.forward_host(Xh, Yh)
+        e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
+        e2e = {"value": world * flops / (e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": l * m * 4,
+               "d2h_bytes_per_step": l * n * 4, "ms_per_step": e_ms}
+    peaks, which = _peaks()
+    fp4_peak = 4.0 * peaks.get("bf16_tflops")
+    t_gemm = stage[2] * 1e-3
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    line = {
+        "metric": AVERIS_METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "nvfp4 (e2m1 + ue4m3/16) x nvfp4 -> f32",
+        "data": "synthetic (X: synth/gen.py c4 seed 0, mean-biased with massive columns; W: generate_weight seed 0)",
+        "config": {"workload": WORKLOADS["averis"], "l": l, "m": m, "n": n, "rounding": "nearest",
+                   "l2": "X (2.1 GB) and Y (2.1 GB) larger than L2; no flush", "parallelism": f"replicas x{world}"},
+        "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches),
+        "stage_ms": {"stats+mu_bar+bias": stage[0], "quantise X_R": stage[1], "gemm": stage[2]},
+        "roofline": {"bound": "tensor", "kernel": "av_gemm_kernel (tcgen05.mma kind::mxf4nvf4 block16)",
+                     "achieved": flops / t_gemm / 1e12, "peak": fp4_peak, "unit": "TFLOP/s",
+                     "frac": flops / t_gemm / 1e12 / fp4_peak, "traffic": None,
+                     "peak_source": f"{which}: 4 x bf16_tflops (burst; fp4 dense = 4x bf16 nominal)",
+                     "algorithmic_flops_per_launch": flops, "launch_ms": stage[2]},
+        "streaming_roofline": {
+            "column stats (read X 4 B/entry)": {"alg_GB/s": l * m * 4 / (stage[0] * 1e-3) / 1e9,
+                                                "frac_hbm": l * m * 4 / (stage[0] * 1e-3) / 1e9 / hbm},
+            "quantise X_R (read 4 B, write 0.5625 B/entry)": {
+                "alg_GB/s": l * m * 4.5625 / (stage[1] * 1e-3) / 1e9,
+                "frac_hbm": l * m * 4.5625 / (stage[1] * 1e-3) / 1e9 / hbm}},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = averis_cpu_baseline(1024)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    g.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
 # ------------------------------------------------------------------ main
 def main():
     ap = argparse.ArgumentParser()
@@ -359,6 +494,9 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if args.config == "c3":
         run_c3(args, rank, world, local)
+        return
+    if args.config == "averis":
+        run_averis(args, rank, world, local)
         return
     from paper_2603_10444_b200.distributed import ShardedDecomposer, TorchComm, _LibBackend, run_stages, shard_rows
     from paper_2603_10444_b200.api import Decomposer

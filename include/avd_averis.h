@@ -34,6 +34,8 @@ extern "C" {
                                    by default"; A3: counter hash of (seed, tensor, index));
                                    default: nearest, ties to the even grid index */
 #define AVD_AVERIS_VANILLA 2    /* no split: Y = Q_b(X) Q_b(W) (the paper's "Vanilla FP4")          */
+#define AVD_AVERIS_TIMING 4     /* record CUDA events at the stage boundaries of each forward
+                                   (read with avd_averis_stage_ms)                                  */
 
 typedef struct {
   int64_t l;       /* tokens (rows of X and Y), >= 1                                     */
@@ -82,7 +84,7 @@ avd_status avd_averis_forward_host(avd_averis_handle h, const float* X_host, flo
  *   AVD_AV_MUSF    u8  [m/16]    UE4M3 scales of mu_bar, plain order
  *   AVD_AV_GSCALE  f32 [4]       g of X_R, W, mu_bar, and the tensor amax of X_R
  *   AVD_AV_BIAS    f32 [n]       mu_bar W_bar (zero with AVD_AVERIS_VANILLA)
- * l_pad = 128 * ceil(l / 128), n_pad = 128 * ceil(n / 128).  EINVAL: unknown id. */
+ * l_pad = 256 * ceil(l / 256), n_pad = 256 * ceil(n / 256).  EINVAL: unknown id. */
 #define AVD_AV_MU 0
 #define AVD_AV_XCODES 1
 #define AVD_AV_XSF 2
@@ -96,6 +98,11 @@ avd_status avd_averis_buffer(avd_averis_handle h, int32_t which, void** dev, siz
 
 /* Kernels this context has launched so far (for the bench's gpu_launches). */
 int64_t avd_averis_launch_count(avd_averis_handle h);
+
+/* Stage times of the last avd_averis_forward (needs AVD_AVERIS_TIMING; waits for its end), ms:
+ * ms[0] column statistics + mu_bar + bias, ms[1] quantisation of X_R, ms[2] the NVFP4 GeMM.
+ * EINVAL: no AVD_AVERIS_TIMING. */
+avd_status avd_averis_stage_ms(avd_averis_handle h, float* ms);
 
 #ifdef __cplusplus
 }

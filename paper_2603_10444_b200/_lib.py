@@ -34,8 +34,9 @@ EXPORTS = ["avd_plan", "avd_create", "avd_destroy", "avd_get_plan", "avd_decompo
            "avd_last_error", "avd_stage_eig_dist", "avd_decompose_sharded", "avd_exchange_nccl"]
 # every symbol include/avd_averis.h declares
 EXPORTS_AVERIS = ["avd_averis_create", "avd_averis_destroy", "avd_averis_set_weight", "avd_averis_forward",
-                  "avd_averis_forward_host", "avd_averis_buffer", "avd_averis_launch_count"]
-AVD_AVERIS_STOCHASTIC, AVD_AVERIS_VANILLA = 1, 2
+                  "avd_averis_forward_host", "avd_averis_buffer", "avd_averis_launch_count",
+                  "avd_averis_stage_ms"]
+AVD_AVERIS_STOCHASTIC, AVD_AVERIS_VANILLA, AVD_AVERIS_TIMING = 1, 2, 4
 AV_BUF = dict(MU=0, XCODES=1, XSF=2, WCODES=3, WSF=4, MUCODES=5, MUSF=6, GSCALE=7, BIAS=8)
 
 
@@ -136,6 +137,7 @@ def lib() -> ctypes.CDLL:
         L.avd_averis_buffer.argtypes = [P, I32, ctypes.POINTER(P), ctypes.POINTER(ctypes.c_size_t)]
         L.avd_averis_launch_count.argtypes = [P]
         L.avd_averis_launch_count.restype = I64
+        L.avd_averis_stage_ms.argtypes = [P, P]
         for name in EXPORTS_AVERIS:
             if name != "avd_averis_launch_count":
                 getattr(L, name).restype = ctypes.c_int
@@ -285,3 +287,9 @@ def avd_averis_buffer(h, which: int):
 
 def avd_averis_launch_count(h) -> int:
     return int(lib().avd_averis_launch_count(h))
+
+
+def avd_averis_stage_ms(h):
+    ms = (ctypes.c_float * 3)()
+    check(lib().avd_averis_stage_ms(h, ctypes.cast(ms, ctypes.c_void_p)), "avd_averis_stage_ms")
+    return list(ms)

@@ -17,12 +17,14 @@ class AverisGemm:
     baseline Q(X) Q(W) without the split."""
 
     def __init__(self, l: int, m: int, n: int, stochastic: bool = False, vanilla: bool = False,
-                 seed: int = 0, device: int = 0, stream: torch.cuda.Stream | None = None):
+                 seed: int = 0, device: int = 0, stream: torch.cuda.Stream | None = None,
+                 timing: bool = False):
         self.l, self.m, self.n = l, m, n
         self.stream = stream or torch.cuda.current_stream(device)
         cfg = L.avd_averis_config()
         cfg.l, cfg.m, cfg.n = l, m, n
-        cfg.flags = (L.AVD_AVERIS_STOCHASTIC if stochastic else 0) | (L.AVD_AVERIS_VANILLA if vanilla else 0)
+        cfg.flags = (L.AVD_AVERIS_STOCHASTIC if stochastic else 0) | (L.AVD_AVERIS_VANILLA if vanilla else 0) | \
+            (L.AVD_AVERIS_TIMING if timing else 0)
         cfg.seed, cfg.device, cfg.stream = seed, device, self.stream.cuda_stream
         self.device = torch.device("cuda", device)
         self.h = L.avd_averis_create(cfg)
@@ -51,6 +53,10 @@ class AverisGemm:
         ptr, nbytes = L.avd_averis_buffer(self.h, L.AV_BUF[name])
         dt = {"MU": torch.float64, "GSCALE": torch.float32, "BIAS": torch.float32}.get(name, torch.uint8)
         return _view(ptr, nbytes, dt, self.device.index)
+
+    def stage_ms(self) -> list[float]:
+        """[stats + mu_bar + bias, quantise X_R, GeMM] of the last forward (timing=True)."""
+        return L.avd_averis_stage_ms(self.h)
 
     def launches(self) -> int:
         return L.avd_averis_launch_count(self.h)

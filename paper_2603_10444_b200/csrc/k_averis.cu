@@ -52,10 +52,13 @@ struct AvCtx {
   uint8_t* musf = nullptr;       // [m/16]
   float* gsc = nullptr;          // [8]: g_X, g_W, g_mu, amax_X, amax_W, amax_mu
   float* bias = nullptr;         // [n]
-  CUtensorMap tmA{}, tmB{};
+  CUtensorMap tmA{}, tmB{}, tmSA{}, tmSB{};
   float* X_stage = nullptr;
   float* Y_stage = nullptr;
   std::vector<void*> allocs;
+  bool timing = false;
+  int dbg = 0;  // AVD_AV_DBG (timing experiments only): 1 no stores, 2 no epilogue, 4 no scale copies
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // AVD_AVERIS_TIMING: stage boundaries
 };
 
 namespace {
@@ -191,50 +194,74 @@ __global__ void __launch_bounds__(256) av_amax_kernel(const float* __restrict__ 
 }
 
 // ---------------------------------------------------------------- quantiser Q_b
-// Rows of a K-contiguous source (X_R, mu): four threads per 16-block, one float4 each (a warp reads
-// 512 contiguous bytes).  sf_plain: scales in plain order (mu) instead of the tensor-core layout.
+// Rows of a K-contiguous source (X_R, mu).  A CTA walks whole rows (grid-stride); per pass over a
+// row its 256 threads cover 256 blocks of 16: four threads per block (one float4 each) and kU
+// blocks per thread whose loads are issued first (a warp reads 512 contiguous bytes per load
+// instruction).  The per-block scale decision (an IEEE division and reciprocal) is taken once per
+// block: quad member u decides block u of the quad's kU blocks and broadcasts it.  sf_plain: scales
+// in plain order (mu) instead of the tensor-core layout.
+constexpr int kU = 4;
 template <bool SR>
 __global__ void __launch_bounds__(256) av_quant_rows_kernel(const float* __restrict__ src, int64_t rows, int64_t K,
                                                             const float* __restrict__ mu_f, const float* __restrict__ amax_p,
                                                             float* __restrict__ g_out, uint8_t* __restrict__ codes,
                                                             uint8_t* __restrict__ sf, int64_t kb4, int sf_plain,
                                                             uint64_t seed, uint64_t tid) {
-  const int64_t t = (int64_t)blockIdx.x * 256 + threadIdx.x;
-  const int64_t nb = K >> 4;
-  const int64_t blk = t >> 2;
-  const int qd = (int)(t & 3);
-  const bool ok = blk < rows * nb;
-  const int64_t r = ok ? blk / nb : 0, b = ok ? blk - r * nb : 0;
-  const int64_t k0 = b * 16 + qd * 4;
+  static_assert(kU == 4, "one quad member per block of the quad");
+  const int nb = (int)(K >> 4);
+  const int lane = threadIdx.x & 31, qd = lane & 3;
+  const int bw = (int)(threadIdx.x >> 5) * 32 + (lane >> 2);  // + 8 u: this thread's blocks in a pass
   const float g = tensor_g(*amax_p);
-  if (t == 0 && g_out) *g_out = g;
-  float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (ok) {
-    x = __ldcs(reinterpret_cast<const float4*>(src + r * K + k0));
-    if (mu_f) {
-      const float4 u = __ldg(reinterpret_cast<const float4*>(mu_f + k0));
-      x.x = __fsub_rn(x.x, u.x); x.y = __fsub_rn(x.y, u.y); x.z = __fsub_rn(x.z, u.z); x.w = __fsub_rn(x.w, u.w);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && g_out) *g_out = g;
+  const float d6 = __fmul_rn(6.f, g);
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const float* xr = src + r * K;
+    for (int b0 = 0; b0 < nb; b0 += 256) {
+      float4 x[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int b = b0 + bw + 8 * u;
+        x[u] = b < nb ? __ldcs(reinterpret_cast<const float4*>(xr + b * 16 + qd * 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      float am[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int b = b0 + bw + 8 * u;
+        if (mu_f && b < nb) {
+          const float4 mu = __ldg(reinterpret_cast<const float4*>(mu_f + b * 16 + qd * 4));
+          x[u].x = __fsub_rn(x[u].x, mu.x); x[u].y = __fsub_rn(x[u].y, mu.y);
+          x[u].z = __fsub_rn(x[u].z, mu.z); x[u].w = __fsub_rn(x[u].w, mu.w);
+        }
+        float a = fmaxf(fmaxf(fabsf(x[u].x), fabsf(x[u].y)), fmaxf(fabsf(x[u].z), fabsf(x[u].w)));
+        a = fmaxf(a, __shfl_xor_sync(0xFFFFFFFFu, a, 1));
+        am[u] = fmaxf(a, __shfl_xor_sync(0xFFFFFFFFu, a, 2));
+      }
+      // quad member qd decides block u = qd
+      const float amine = qd == 0 ? am[0] : (qd == 1 ? am[1] : (qd == 2 ? am[2] : am[3]));
+      const uint32_t scm = e4m3_rn(__fdiv_rn(amine, d6));
+      const float Rm = scm ? __frcp_rn(__fmul_rn(e4m3_val(scm), g)) : 0.f;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int b = b0 + bw + 8 * u;
+        const int src_lane = (lane & ~3) | u;
+        const uint32_t sc = __shfl_sync(0xFFFFFFFFu, scm, src_lane);
+        const float R = __shfl_sync(0xFFFFFFFFu, Rm, src_lane);
+        const float v0 = __fmul_rn(x[u].x, R), v1 = __fmul_rn(x[u].y, R), v2 = __fmul_rn(x[u].z, R), v3 = __fmul_rn(x[u].w, R);
+        uint32_t out;
+        if (SR) {
+          const uint64_t li = (uint64_t)(r * K + b * 16 + qd * 4);
+          out = e2m1_sr(v0, ctr_u24(seed, tid, li)) | (e2m1_sr(v1, ctr_u24(seed, tid, li + 1)) << 4) |
+                (e2m1_sr(v2, ctr_u24(seed, tid, li + 2)) << 8) | (e2m1_sr(v3, ctr_u24(seed, tid, li + 3)) << 12);
+        } else {
+          out = e2m1x2_rn(v0, v1) | (e2m1x2_rn(v2, v3) << 8);
+        }
+        if (sc == 0) out = 0;  // all-zero block (A7)
+        if (b < nb) {
+          *reinterpret_cast<uint16_t*>(codes + r * (K >> 1) + b * 8 + qd * 2) = (uint16_t)out;
+          if (qd == 0) sf[sf_plain ? (int64_t)b : sf_off(r, b, kb4)] = (uint8_t)sc;
+        }
+      }
     }
-  }
-  float a = fmaxf(fmaxf(fabsf(x.x), fabsf(x.y)), fmaxf(fabsf(x.z), fabsf(x.w)));
-  a = fmaxf(a, __shfl_xor_sync(0xFFFFFFFFu, a, 1));
-  a = fmaxf(a, __shfl_xor_sync(0xFFFFFFFFu, a, 2));
-  const uint32_t sc = e4m3_rn(__fdiv_rn(a, __fmul_rn(6.f, g)));
-  uint32_t out = 0;
-  if (sc != 0) {
-    const float R = __frcp_rn(__fmul_rn(e4m3_val(sc), g));
-    const float v0 = __fmul_rn(x.x, R), v1 = __fmul_rn(x.y, R), v2 = __fmul_rn(x.z, R), v3 = __fmul_rn(x.w, R);
-    if (SR) {
-      const uint64_t li = (uint64_t)(r * K + k0);
-      out = e2m1_sr(v0, ctr_u24(seed, tid, li)) | (e2m1_sr(v1, ctr_u24(seed, tid, li + 1)) << 4) |
-            (e2m1_sr(v2, ctr_u24(seed, tid, li + 2)) << 8) | (e2m1_sr(v3, ctr_u24(seed, tid, li + 3)) << 12);
-    } else {
-      out = e2m1x2_rn(v0, v1) | (e2m1x2_rn(v2, v3) << 8);
-    }
-  }
-  if (ok) {
-    *reinterpret_cast<uint16_t*>(codes + r * (K >> 1) + (k0 >> 1)) = (uint16_t)out;
-    if (qd == 0) sf[sf_plain ? b : sf_off(r, b, kb4)] = (uint8_t)sc;
   }
 }
 
@@ -311,141 +338,235 @@ __global__ void __launch_bounds__(256) av_bias_kernel(const uint8_t* __restrict_
 
 // ---------------------------------------------------------------- NVFP4 GeMM on tcgen05
 // Y[i][j] = g_X g_W sum_k xr_ik w_kj + bias_j: A = X_R codes [l][m/2] (K-major), B = W codes
-// [n][m/2] (K-major), one 128 x 128 output tile per unit, persistent CTAs (one per SM), K in
+// [n][m/2] (K-major).  CTA pairs (cluster 2x1) own 256 x 256 output blocks with
+// tcgen05.mma.cta_group::2.kind::mxf4nvf4 (M = 256: 128 A rows per CTA; N = 256: each CTA stages
+// one 128-row half of B, so no operand byte is held twice), issued by the leader CTA.  K advances in
 // stages of 256 elements (128 B of codes per row: one SWIZZLE_128B atom), 4 MMAs of K = 64 per
-// stage.  Per stage the TMA brings A (16 KB), B (16 KB) and the stage's scale chunks (2 x 2 KB,
-// 1-D bulk copies: the quantiser wrote them in the tensor-core layout); the MMA warp copies the
-// scales to TMEM (tcgen05.cp 32x128b.warpx4: 32 lanes x 16 B broadcast to the four lane quarters)
-// and issues the block-scaled MMAs, which execute after the copies in issue order.  Two fp32
-// accumulators (TMEM columns 0-127, 128-255) let the epilogue of one tile overlap the next.
-constexpr int kAvNS = 5;
-constexpr uint32_t kAvA = 128 * 128, kAvB = 128 * 128, kAvSF = 2048;
-constexpr uint32_t kAvStage = kAvA + kAvB + 2 * kAvSF;  // 36 KB (multiple of 1 KB)
-constexpr int kAvGemmThreads = 192;                    // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+// stage; per stage each CTA receives 38 KB (A 16, B half 16, its A scales 2, all 256 B-row scales
+// 4 — the scale chunks come as 2 KB TMA boxes of the quantiser's tensor-core layout) and every TMA
+// completes on the leader's barrier.  The leader copies each CTA's scales to its own TMEM
+// (tcgen05.cp.cta_group::2 32x128b.warpx4: 32 lanes x 16 B broadcast to the four lane quarters)
+// ahead of the MMAs in issue order, and its commits arrive on both CTAs' barriers.  One fp32
+// accumulator of 256 columns per CTA: eight epilogue warps per CTA drain it to registers (128
+// values per thread), release it, apply y = acc * g_X g_W + bias_j while the next tile's MMAs run,
+// and write Y by TMA bulk stores of 32 x 32 blocks staged in a 128B-swizzled buffer per warp
+// (row-per-thread global stores cost about as much as the MMAs in L2 sector traffic).
+constexpr uint32_t kAvA = 128 * 128, kAvB = 128 * 128, kAvSFA = 2048, kAvSFB = 4096;
+constexpr uint32_t kAvStage = kAvA + kAvB + kAvSFA + kAvSFB;  // 38 KB per CTA (multiple of 1 KB)
+constexpr uint32_t kAvOut = 32 * 128;                         // per epilogue warp: 32 rows x 32 fp32 (SW128)
+constexpr int kAvGemmThreads = 320;                           // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
 
-// kind::mxf4nvf4, A/B E2M1 (format 1), UE4M3 scales (bit 23 = 0), K-major, M = 128, N = 128, K = 64
+// kind::mxf4nvf4, A/B E2M1 (format 1), UE4M3 scales (bit 23 = 0), K-major, K = 64
 __host__ __device__ constexpr uint32_t idesc_nvf4(uint32_t M, uint32_t N) {
   return (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
-__device__ __forceinline__ void mma_nvf4(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t sfa,
-                                         uint32_t sfb, uint32_t accumulate) {
+__device__ __forceinline__ void mma_nvf4_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t sfa,
+                                              uint32_t sfb, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::mxf4nvf4.block_scale.scale_vec::4X [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(d),
+      "tcgen05.mma.cta_group::2.kind::mxf4nvf4.block_scale.scale_vec::4X [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(d),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb)
       : "memory");
 }
-__device__ __forceinline__ void tmem_cp_sf(uint32_t taddr, uint64_t sdesc) {
-  asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+__device__ __forceinline__ void tmem_cp_sf_pair(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::2.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
+__device__ __forceinline__ uint32_t av_cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void av_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t av_mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void av_arrive_remote(uint32_t caddr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
+// 2-D TMA load into this CTA's shared memory, completion counted on the leader's barrier
+__device__ __forceinline__ void tma_load_2d_p(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int32_t c0,
+                                              int32_t c1) {
+  asm volatile("cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+               " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)),
+               "r"(bar_cluster), "r"(c0), "r"(c1)
+               : "memory");
+}
+// arrive on `bar` in both CTAs of the pair once the leader's previously issued MMAs completed
+__device__ __forceinline__ void mma_commit_pair_mc(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               ::"r"(smem_u32(bar)), "h"((uint16_t)3)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%"
+      "29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
 }
 
-__global__ void __launch_bounds__(kAvGemmThreads, 1) av_gemm_kernel(
-    const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const uint8_t* __restrict__ sfa,
-    const uint8_t* __restrict__ sfb, int64_t l, int64_t n, int KB, int64_t MT, int64_t NT, int64_t kb4,
-    const float* __restrict__ gsc, const float* __restrict__ bias, float* __restrict__ Y) {
+constexpr int kAvNS = 5;
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kAvGemmThreads, 1) av_gemm_kernel(
+    const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+    const __grid_constant__ CUtensorMap tmSA, const __grid_constant__ CUtensorMap tmSB,
+    const __grid_constant__ CUtensorMap tmY, int64_t l, int64_t n, int KB, int64_t MT2, int64_t NT, int64_t kb4,
+    const float* __restrict__ gsc, const float* __restrict__ bias, int dbg) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t full_bar[kAvNS], empty_bar[kAvNS], tfull_bar[2], tempty_bar[2];
+  __shared__ uint64_t full_bar[kAvNS], empty_bar[kAvNS], tfull_bar, tempty_bar;
   __shared__ uint32_t tmem_sh;
   const uint32_t warp = warp_id(), lane = lane_id();
-  const int64_t tiles = MT * NT;
+  const uint32_t rank = av_cluster_rank();
+  const int64_t pairs = MT2 * NT;
+  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int64_t st4 = kb4 / 4;  // 2 KB scale chunks per 128-row tile
   if (threadIdx.x == 0) {
     for (int s = 0; s < kAvNS; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(&tfull_bar[b], 1); mbar_init(&tempty_bar[b], 128); }
+    mbar_init(&tfull_bar, 1);
+    mbar_init(&tempty_bar, 16);  // 8 epilogue warps x 2 CTAs (on the leader)
     fence_mbar_init();
   }
-  if (warp == 0 && lane == 0) { tma_prefetch(&tmA); tma_prefetch(&tmB); }
-  if (warp == 1) tmem_alloc<512>(&tmem_sh);
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA); tma_prefetch(&tmB); tma_prefetch(&tmSA); tma_prefetch(&tmSB); tma_prefetch(&tmY);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_sh))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
   tc_fence_before();
   __syncthreads();
+  av_cluster_sync();
   tc_fence_after();
   const uint32_t tmem = tmem_sh;
+  const uint32_t full0 = av_mapa(smem_u32(&full_bar[0]), 0);   // the leader's full barriers
+  const uint32_t tempty0 = av_mapa(smem_u32(&tempty_bar), 0);  // the leader's tempty barrier
 
   if (warp == 0) {
     if (elect_one()) {
       uint32_t it = 0;
-      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int64_t mt = t / NT, nt = t - (t / NT) * NT;
+      for (int64_t pt = cid; pt < pairs; pt += ncl) {
+        const int64_t mt = 2 * (pt / NT) + rank, nt = pt % NT;
         for (int kb = 0; kb < KB; ++kb, ++it) {
           const uint32_t s = it % kAvNS, ph = (it / kAvNS) & 1;
           mbar_wait(&empty_bar[s], ph ^ 1);
           uint8_t* st = smem + s * kAvStage;
-          mbar_arrive_expect_tx(&full_bar[s], kAvStage);
-          tma_load_2d(st, &tmA, &full_bar[s], kb * 128, (int32_t)(mt * 128));
-          tma_load_2d(st + kAvA, &tmB, &full_bar[s], kb * 128, (int32_t)(nt * 128));
-          bulk_load_1d(st + kAvA + kAvB, sfa + (mt * kb4 + kb * 4) * 512, kAvSF, &full_bar[s]);
-          bulk_load_1d(st + kAvA + kAvB + kAvSF, sfb + (nt * kb4 + kb * 4) * 512, kAvSF, &full_bar[s]);
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[s], 2 * kAvStage);
+          const uint32_t fb = full0 + s * (uint32_t)sizeof(uint64_t);
+          tma_load_2d_p(st, &tmA, fb, kb * 128, (int32_t)(mt * 128));
+          tma_load_2d_p(st + kAvA, &tmB, fb, kb * 128, (int32_t)(nt * 256 + rank * 128));
+          tma_load_2d_p(st + kAvA + kAvB, &tmSA, fb, 0, (int32_t)(mt * st4 + kb));
+          tma_load_2d_p(st + kAvA + kAvB + kAvSFA, &tmSB, fb, 0, (int32_t)(2 * nt * st4 + kb));
+          tma_load_2d_p(st + kAvA + kAvB + 2 * kAvSFA, &tmSB, fb, 0, (int32_t)((2 * nt + 1) * st4 + kb));
         }
       }
     }
   } else if (warp == 1) {
-    constexpr uint32_t idesc = idesc_nvf4(128, 128);
-    uint32_t it = 0, ui = 0;
-    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++ui) {
-      const uint32_t b = ui & 1, br = ui >> 1;
-      mbar_wait(&tempty_bar[b], (br & 1) ^ 1);
-      tc_fence_after();
-      const uint32_t d = tmem + b * 128;
-      for (int kb = 0; kb < KB; ++kb, ++it) {
-        const uint32_t s = it % kAvNS, ph = (it / kAvNS) & 1;
-        mbar_wait(&full_bar[s], ph);
+    if (rank == 0) {
+      constexpr uint32_t idesc = idesc_nvf4(256, 256);
+      uint32_t it = 0, ui = 0;
+      for (int64_t pt = cid; pt < pairs; pt += ncl, ++ui) {
+        if (!(dbg & 2)) mbar_wait(&tempty_bar, (ui & 1) ^ 1);
         tc_fence_after();
-        if (elect_one()) {
-          const uint32_t base = smem_u32(smem + s * kAvStage);
-          const uint32_t tsf = tmem + 256 + (it & 3) * 32;  // 4 rotating scale slots: SFA 16 cols, SFB 16
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const uint32_t s = it % kAvNS, ph = (it / kAvNS) & 1;
+          mbar_wait(&full_bar[s], ph);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t base = smem_u32(smem + s * kAvStage);
+            const uint32_t sfa_s = base + kAvA + kAvB, sfb_s = sfa_s + kAvSFA;
+            const uint32_t tsf = tmem + 256 + (it & 3) * 48;  // 4 rotating slots: SFA 16 columns, SFB 32
+            if (!(dbg & 4)) {
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            tmem_cp_sf(tsf + kk * 4, smem_desc(base + kAvA + kAvB + kk * 512, 0, 128, 0));
-            tmem_cp_sf(tsf + 16 + kk * 4, smem_desc(base + kAvA + kAvB + kAvSF + kk * 512, 0, 128, 0));
-          }
+              for (int kk = 0; kk < 4; ++kk) {
+                tmem_cp_sf_pair(tsf + kk * 4, smem_desc(sfa_s + kk * 512, 0, 128, 0));
+                tmem_cp_sf_pair(tsf + 16 + kk * 8, smem_desc(sfb_s + kk * 512, 0, 128, 0));
+                tmem_cp_sf_pair(tsf + 16 + kk * 8 + 4, smem_desc(sfb_s + kAvSFA + kk * 512, 0, 128, 0));
+              }
+            }
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint64_t ad = smem_desc(base + kk * 32, 16, 1024, 2);
-            const uint64_t bd = smem_desc(base + kAvA + kk * 32, 16, 1024, 2);
-            mma_nvf4(d, ad, bd, idesc, tsf + kk * 4, tsf + 16 + kk * 4, (kb | kk) ? 1u : 0u);
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint64_t ad = smem_desc(base + kk * 32, 16, 1024, 2);
+              const uint64_t bd = smem_desc(base + kAvA + kk * 32, 16, 1024, 2);
+              mma_nvf4_pair(tmem, ad, bd, idesc, tsf + kk * 4, tsf + 16 + kk * 8, (kb | kk) ? 1u : 0u);
+            }
+            mma_commit_pair_mc(&empty_bar[s]);
           }
-          mma_commit(&empty_bar[s]);
+          __syncwarp();
         }
+        if (elect_one()) mma_commit_pair_mc(&tfull_bar);
         __syncwarp();
       }
-      if (elect_one()) mma_commit(&tfull_bar[b]);
-      __syncwarp();
     }
   } else {
-    const uint32_t q = warp & 3;
+    const uint32_t q = warp & 3, h = (warp - 2) >> 2;
     const float gxw = __fmul_rn(gsc[0], gsc[1]);
     uint32_t ui = 0;
-    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++ui) {
-      const uint32_t b = ui & 1, br = ui >> 1;
-      const int64_t mt = t / NT, nt = t - (t / NT) * NT;
-      mbar_wait(&tfull_bar[b], br & 1);
+    for (int64_t pt = cid; pt < pairs; pt += ncl, ++ui) {
+      const int64_t mt = 2 * (pt / NT) + rank, nt = pt % NT;
+      if (dbg & 2) continue;
+      mbar_wait(&tfull_bar, ui & 1);
       tc_fence_after();
-      const int64_t row = mt * 128 + q * 32 + lane;
-      const uint32_t tb = tmem + ((q * 32) << 16) + b * 128;
-#pragma unroll 1
-      for (int c = 0; c < 128; c += 16) {
-        uint32_t rv[16];
-        tmem_ld16(tb + c, rv);
-        tmem_ld_wait();
-        const int64_t col = nt * 128 + c;
-        if (row < l && col < n) {
-          float y[16];
+      uint32_t v[128];
+      const uint32_t tb = tmem + ((q * 32) << 16) + h * 128;
 #pragma unroll
-          for (int u = 0; u < 16; ++u) y[u] = __fmaf_rn(__uint_as_float(rv[u]), gxw, __ldg(bias + col + u));
-          float4* dst = reinterpret_cast<float4*>(Y + row * n + col);
+      for (int c = 0; c < 4; ++c) tmem_ld32(tb + c * 32, v + c * 32);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) av_arrive_remote(tempty0);
+      const int64_t row0 = mt * 128 + q * 32;
+      const int64_t col0 = nt * 256 + h * 128;
+      if (row0 < l && !(dbg & 1)) {
+        const uint32_t sw = lane & 7;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) __stcs(dst + u, make_float4(y[4 * u], y[4 * u + 1], y[4 * u + 2], y[4 * u + 3]));
+        for (int c = 0; c < 4; ++c) {
+          if (col0 + 32 * c >= n) break;
+          uint8_t* ob = smem + kAvNS * kAvStage + (warp - 2) * kAvOut;
+          if (lane == 0) bulk_wait_read0();  // the previous block's bulk store has read the buffer
+          __syncwarp();
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int cc = 32 * c + 4 * k;
+            const float4 bb = col0 + cc < n ? __ldg(reinterpret_cast<const float4*>(bias + col0 + cc))
+                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 y = make_float4(__fmaf_rn(__uint_as_float(v[cc]), gxw, bb.x),
+                                         __fmaf_rn(__uint_as_float(v[cc + 1]), gxw, bb.y),
+                                         __fmaf_rn(__uint_as_float(v[cc + 2]), gxw, bb.z),
+                                         __fmaf_rn(__uint_as_float(v[cc + 3]), gxw, bb.w));
+            *reinterpret_cast<float4*>(ob + lane * 128 + ((k ^ sw) << 4)) = y;
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) tma_store_2d(&tmY, ob, (int32_t)(col0 + 32 * c), (int32_t)row0);
         }
       }
-      tc_fence_before();
-      mbar_arrive(&tempty_bar[b]);
     }
+    if (lane == 0) bulk_wait0();
   }
   tc_fence_before();
   __syncthreads();
-  tc_fence_after();
-  if (warp == 1) tmem_dealloc<512>(tmem);
+  av_cluster_sync();  // no CTA leaves while its peer may still load into it / arrive on it
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
 
 avd_status make_maps(AvCtx* c) {
@@ -462,6 +583,17 @@ avd_status make_maps(AvCtx* c) {
   r = enc(&c->tmB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, c->wcodes, db, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled (Averis B) failed: " + std::to_string((int)r)); return AVD_ECUDA; }
+  // scale chunks: 2 KB boxes (256 x u64) of the tensor-core layout, one per (128-row tile, stage)
+  uint32_t sbox[2] = {256, 1};
+  uint64_t sstr[1] = {2048};
+  uint64_t dsa[2] = {256, (uint64_t)(c->l_pad / 128 * (c->kb4 / 4))};
+  r = enc(&c->tmSA, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, c->xsf, dsa, sstr, sbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled (Averis SFA) failed: " + std::to_string((int)r)); return AVD_ECUDA; }
+  uint64_t dsb[2] = {256, (uint64_t)(c->n_pad / 128 * (c->kb4 / 4))};
+  r = enc(&c->tmSB, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, c->wsf, dsb, sstr, sbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled (Averis SFB) failed: " + std::to_string((int)r)); return AVD_ECUDA; }
   return AVD_OK;
 }
 
@@ -486,6 +618,7 @@ avd_status av_forward(AvCtx* c, const float* X, float* Y) {
     return AVD_EINVAL;
   }
   const int64_t l = c->l, m = c->m, n = c->n;
+  if (c->timing) AVD_CUDA(cudaEventRecord(c->ev[0], c->stream));
   AVD_CUDA(cudaMemsetAsync(c->gsc + 3, 0, sizeof(float), c->stream));
   AVD_CUDA(cudaMemsetAsync(c->gsc + 5, 0, sizeof(float), c->stream));
   const int64_t rows_per = ceil_div(l, c->R);
@@ -497,7 +630,7 @@ avd_status av_forward(AvCtx* c, const float* X, float* Y) {
   AVD_LAUNCHED(c);
   const uint64_t seed = c->cfg.seed;
   if (!c->vanilla) {
-    const unsigned gmu = (unsigned)ceil_div(m / 16 * 4, 256);
+    const unsigned gmu = 1;
     if (c->sr)
       av_quant_rows_kernel<true><<<gmu, 256, 0, c->stream>>>(c->mu_f, 1, m, nullptr, c->gsc + 5, c->gsc + 2, c->mucodes,
                                                              c->musf, 0, 1, seed, 2);
@@ -509,7 +642,8 @@ avd_status av_forward(AvCtx* c, const float* X, float* Y) {
                                                                     c->kb4, c->bias);
     AVD_LAUNCHED(c);
   }
-  const unsigned gx = (unsigned)ceil_div(l * (m / 16) * 4, 256);
+  if (c->timing) AVD_CUDA(cudaEventRecord(c->ev[1], c->stream));
+  const unsigned gx = (unsigned)std::min<int64_t>(l, 16 * c->num_sms);  // CTAs walk rows
   const float* muf = c->vanilla ? nullptr : c->mu_f;
   if (c->sr)
     av_quant_rows_kernel<true><<<gx, 256, 0, c->stream>>>(X, l, m, muf, c->gsc + 3, c->gsc + 0, c->xcodes, c->xsf, c->kb4,
@@ -518,14 +652,26 @@ avd_status av_forward(AvCtx* c, const float* X, float* Y) {
     av_quant_rows_kernel<false><<<gx, 256, 0, c->stream>>>(X, l, m, muf, c->gsc + 3, c->gsc + 0, c->xcodes, c->xsf, c->kb4,
                                                            0, seed, 1);
   AVD_LAUNCHED(c);
-  const int64_t MT = c->l_pad / 128, NT = c->n_pad / 128;
+  if (c->timing) AVD_CUDA(cudaEventRecord(c->ev[2], c->stream));
+  const int64_t MT2 = c->l_pad / 256, NT = c->n_pad / 256;
   const int KB = (int)ceil_div(m, 256);
-  const int smem = kAvNS * kAvStage + 1024;
+  const int smem = kAvNS * kAvStage + 8 * kAvOut + 1024;
   AVD_CUDA(smem_attr(av_gemm_kernel, smem));
-  const int grid = (int)std::min<int64_t>(MT * NT, c->num_sms);
-  av_gemm_kernel<<<grid, kAvGemmThreads, smem, c->stream>>>(c->tmA, c->tmB, c->xsf, c->wsf, l, n, KB, MT, NT, c->kb4,
-                                                            c->gsc, c->bias, Y);
+  CUtensorMap tmY;
+  {
+    auto enc = tma_encode_fn();
+    uint64_t dims[2] = {(uint64_t)n, (uint64_t)l}, strides[1] = {(uint64_t)n * 4};
+    uint32_t box[2] = {32, 32}, es[2] = {1, 1};
+    const CUresult r = enc(&tmY, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Y, dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled (Averis Y) failed: " + std::to_string((int)r)); return AVD_ECUDA; }
+  }
+  const int grid = 2 * (int)std::min<int64_t>(MT2 * NT, c->num_sms / 2);
+  av_gemm_kernel<<<grid, kAvGemmThreads, smem, c->stream>>>(c->tmA, c->tmB, c->tmSA, c->tmSB, tmY, l, n, KB, MT2, NT,
+                                                            c->kb4, c->gsc, c->bias, c->dbg);
   AVD_LAUNCHED(c);
+  if (c->timing) AVD_CUDA(cudaEventRecord(c->ev[3], c->stream));
   return AVD_OK;
 }
 
@@ -560,11 +706,15 @@ avd_status avd_averis_create(const avd_averis_config* cfg, avd_averis_handle* ou
   c->stream = static_cast<cudaStream_t>(cfg->stream);
   c->num_sms = prop.multiProcessorCount;
   c->l = cfg->l; c->m = cfg->m; c->n = cfg->n;
-  c->l_pad = avd::round_up(c->l, 128);
-  c->n_pad = avd::round_up(c->n, 128);
+  c->l_pad = avd::round_up(c->l, 256);  // cluster pairs of 128-row tiles
+  c->n_pad = avd::round_up(c->n, 256);
   c->kb4 = 4 * avd::ceil_div(c->m, 256);
   c->vanilla = (cfg->flags & AVD_AVERIS_VANILLA) != 0;
   c->sr = (cfg->flags & AVD_AVERIS_STOCHASTIC) != 0;
+  c->timing = (cfg->flags & AVD_AVERIS_TIMING) != 0;
+  if (const char* e = getenv("AVD_AV_DBG")) c->dbg = atoi(e);
+  for (int i = 0; i < 4 && c->timing; ++i)
+    if (cudaEventCreate(&c->ev[i]) != cudaSuccess) { cudaGetLastError(); avd::set_error("cudaEventCreate failed"); delete h; return AVD_ECUDA; }
   c->R = (int)std::max<int64_t>(1, std::min<int64_t>(c->l, 4 * c->num_sms / std::max<int64_t>(1, avd::ceil_div(c->m, 1024))));
   const int64_t m = c->m;
   avd_status st = AVD_OK;
@@ -597,6 +747,8 @@ avd_status avd_averis_destroy(avd_averis_handle h) {
   for (void* p : h->c.allocs) cudaFree(p);
   if (h->c.X_stage) cudaFree(h->c.X_stage);
   if (h->c.Y_stage) cudaFree(h->c.Y_stage);
+  for (cudaEvent_t e : h->c.ev)
+    if (e) cudaEventDestroy(e);
   delete h;
   return AVD_OK;
 }
@@ -667,5 +819,15 @@ avd_status avd_averis_buffer(avd_averis_handle h, int32_t which, void** dev, siz
 }
 
 int64_t avd_averis_launch_count(avd_averis_handle h) { return h ? h->c.launches : 0; }
+
+avd_status avd_averis_stage_ms(avd_averis_handle h, float* ms) {
+  if (!h || !ms || !h->c.timing) {
+    avd::set_error("avd_averis_stage_ms: null argument or context created without AVD_AVERIS_TIMING");
+    return AVD_EINVAL;
+  }
+  AVD_CUDA(cudaEventSynchronize(h->c.ev[3]));
+  for (int i = 0; i < 3; ++i) AVD_CUDA(cudaEventElapsedTime(ms + i, h->c.ev[i], h->c.ev[i + 1]));
+  return AVD_OK;
+}
 
 }  // extern "C"
