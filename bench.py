@@ -474,10 +474,11 @@ def main():
     ap.add_argument("--cpu-baseline-rows", type=int, default=0,
                     help="rows of the oracle sample (0: 8192 for c4/c5, all rows below; -1: all rows)")
     ap.add_argument("--cpu-baseline-eig", default="lapack", choices=["lapack", "jacobi"])
-    ap.add_argument("--variant", default="base", choices=["base", "massive"],
+    ap.add_argument("--variant", default="base", choices=["base", "massive", "gramfree"],
                     help="massive: plant single-token massive activations (PAPER.md:245-246) in an "
                          "unsampled row, which forces the exact-range requantisation and exercises "
-                         "the automatic digit escalation inside the timed region")
+                         "the automatic digit escalation inside the timed region; gramfree: the "
+                         "Gram-free eigensolve (AVD_FLAG_GRAM_FREE, SURVEY 8(f4))")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (huge configs)")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -509,8 +510,12 @@ def main():
         plant_massive(X, r0, m)
     torch.cuda.synchronize()
 
+    flags = 0
+    if args.variant == "gramfree":
+        from paper_2603_10444_b200._lib import AVD_FLAG_GRAM_FREE
+        flags = AVD_FLAG_GRAM_FREE
     if world == 1:
-        dec = Decomposer(l, m, digits=args.digits, seed=0)
+        dec = Decomposer(l, m, digits=args.digits, seed=0, flags=flags)
         comm = LocalComm()
     else:
         sd = ShardedDecomposer(l, m, digits=args.digits, seed=0)
@@ -652,7 +657,7 @@ def main():
                    f"{l * m * 4 / 1e9:.2f} GB > 126 MB); no flush",
                    "parallelism": f"row-shard x{world}"},
         "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches),
-        "roofline": roofline, "stage_ms": stage_ms, "streaming_roofline": stream_roof,
+        "roofline": roofline if args.variant != "gramfree" else None, "stage_ms": stage_ms, "streaming_roofline": stream_roof,
         "eig_iters": res.iters, "eig_max_resid": res.max_resid, "eig_rr_checks": res.rr_checks,
         "eig_jacobi_sweeps": res.jacobi_sweeps, "eig_status": res.status,
         "requantised": res.requantised, "digits_used": res.digits_used,
@@ -662,7 +667,9 @@ def main():
     }
     if args.variant != "base":
         line["config"]["variant"] = {"massive": f"single-token massive activations {list(MASSIVE)} "
-                                                f"(row, col, value) in an unsampled row"}[args.variant]
+                                                f"(row, col, value) in an unsampled row",
+                                     "gramfree": "AVD_FLAG_GRAM_FREE: no Gram; every G Q of the eigensolve as "
+                                                 "Xhat^T (Xhat Q) by two tensor-core passes (SURVEY 8(f4))"}[args.variant]
     bad = []
     if res.status != 0:
         bad.append(f"eigensolver status {res.status} (AVD_ENOCONV = 3): not converged")

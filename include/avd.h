@@ -106,6 +106,13 @@ typedef struct {
  * X^T X = G + l mu mu^T) and alpha_i = |mu . v_i| into
  * avd_outputs.mean_sigma_dev / mean_alpha_dev — about one eigensolve of extra work          */
 #define AVD_FLAG_MEAN_TOPK 16
+/* Gram-free eigensolve: the m x m Gram is never
+ * formed; every product G Q of the subspace iteration is evaluated as Xhat^T (Xhat Q) by two
+ * streaming tensor-core passes over the Gram operand's digit planes.  Same outputs and tolerances.
+ * Single GPU only (world 1; EINVAL otherwise); not combinable with AVD_FLAG_MEAN_TOPK, and the
+ * uncentred top pair of the mean-bias diagnostics (cos_mu_v1, alpha1, sigma1_u, resid_u,
+ * iters_u) is not computed (NaN). */
+#define AVD_FLAG_GRAM_FREE 32
 
 /* Outputs.  Device arrays caller-owned, sized from the plan (cap = n_top). */
 typedef struct {
@@ -292,6 +299,14 @@ int avd_exchange_nccl(int32_t which, void* buf_dev, int32_t dtype, int32_t op, s
  * Host-only integer logic (no device work); used by avd_stage_gather.                       */
 avd_status avd_tie_quota(const int64_t* sel_counts, const int64_t* tie_counts, int32_t world,
                          int32_t rank, int64_t q, int64_t* quota, int64_t* offset);
+
+/* Y_dev = G In_dev for the context's Gram operand G = Xhat^T Xhat (Xhat: the quantised, exactly
+ * centred matrix the eigensolve used): the formed fp64 G, or with
+ * AVD_FLAG_GRAM_FREE the two streaming tensor-core passes Xhat^T (Xhat In).
+ * In_dev, Y_dev: device fp64 row-major [m][p] (p from the plan), caller-owned.  Valid after the
+ * eigen stage (or avd_decompose) of this context; synchronises.  ESTATE before that.  For checks
+ * of the product itself (tests) and callers that reuse the operand for further subspace work. */
+avd_status avd_gram_product(avd_ctx* ctx, const double* In_dev, double* Y_dev);
 
 /* Number of kernels this context launched since creation (for the bench's gpu_launches). */
 int64_t avd_launch_count(const avd_ctx* ctx);

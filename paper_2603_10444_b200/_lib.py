@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libavd.so")
 
 AVD_FLAG_STREAM_SELECT, AVD_FLAG_EXACT_SCALE, AVD_FLAG_FORCE_ESCALATE, AVD_FLAG_EIG_HOST_LOOP = 1, 2, 4, 8
-AVD_FLAG_MEAN_TOPK = 16
+AVD_FLAG_MEAN_TOPK, AVD_FLAG_GRAM_FREE = 16, 32
 AVD_OK, AVD_EINVAL, AVD_ENONFINITE, AVD_ENOCONV, AVD_ECUDA, AVD_ENOMEM, AVD_ESTATE = 0, 1, 2, 3, 4, 6, 8
 AVD_EREPEAT, AVD_EEXCHANGE = 9, 10
 BUF = dict(STATS=0, COLMAX=1, COLMIN=2, HIST1=3, GRAM=4, ENERGY=5, HIST2=6, HIST3=7, TIES=8, AGG=9,
@@ -31,7 +31,7 @@ EXPORTS = ["avd_plan", "avd_create", "avd_destroy", "avd_get_plan", "avd_decompo
            "avd_decompose_host", "avd_buffer", "avd_stage_stats", "avd_stage_split",
            "avd_stage_gram", "avd_stage_eig", "avd_stage_project", "avd_stage_select",
            "avd_stage_gather", "avd_stage_report", "avd_tie_quota", "avd_launch_count", "avd_strerror",
-           "avd_last_error", "avd_stage_eig_dist", "avd_decompose_sharded", "avd_exchange_nccl"]
+           "avd_last_error", "avd_stage_eig_dist", "avd_decompose_sharded", "avd_exchange_nccl", "avd_gram_product"]
 # every symbol include/avd_averis.h declares
 EXPORTS_AVERIS = ["avd_averis_create", "avd_averis_destroy", "avd_averis_set_weight", "avd_averis_forward",
                   "avd_averis_forward_host", "avd_averis_buffer", "avd_averis_launch_count",
@@ -118,6 +118,7 @@ def lib() -> ctypes.CDLL:
         L.avd_stage_eig_dist.argtypes = [P, I32, EXCHANGE_FN, P]
         L.avd_decompose_sharded.argtypes = [P, P, I32, ctypes.POINTER(avd_outputs), EXCHANGE_FN, P]
         L.avd_exchange_nccl.argtypes = [I32, P, I32, I32, ctypes.c_size_t, P]
+        L.avd_gram_product.argtypes = [P, P, P]
         L.avd_stage_project.argtypes = [P, P]
         L.avd_stage_select.argtypes = [P, P, I32, I32]
         L.avd_stage_gather.argtypes = [P, P, I32, ctypes.POINTER(avd_outputs)]
@@ -293,3 +294,7 @@ def avd_averis_stage_ms(h):
     ms = (ctypes.c_float * 3)()
     check(lib().avd_averis_stage_ms(h, ctypes.cast(ms, ctypes.c_void_p)), "avd_averis_stage_ms")
     return list(ms)
+
+
+def avd_gram_product(h, In_ptr: int, Y_ptr: int):
+    return check(lib().avd_gram_product(h, ctypes.c_void_p(In_ptr), ctypes.c_void_p(Y_ptr)), "avd_gram_product")

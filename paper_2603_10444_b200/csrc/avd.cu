@@ -73,6 +73,10 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   const int nd = cfg->digits == 0 ? 2 : cfg->digits;
   if (nd != 2 && nd != 3) { set_error("digits must be 0 (automatic), 2 or 3"); return AVD_EINVAL; }
   const int nd_max = cfg->digits == 0 ? 3 : nd;
+  if ((cfg->flags & AVD_FLAG_GRAM_FREE) && (world > 1 || (cfg->flags & AVD_FLAG_MEAN_TOPK))) {
+    set_error("AVD_FLAG_GRAM_FREE needs world == 1 and excludes AVD_FLAG_MEAN_TOPK");
+    return AVD_EINVAL;
+  }
   plan->k = (int32_t)k;
   plan->p = (int32_t)p;
   plan->n_top = n_top;
@@ -88,6 +92,7 @@ avd_status make_plan(const avd_config* cfg, avd_plan_t* plan, Ctx* c, Layout* la
   C->nd = nd;
   C->nd_max = nd_max;
   C->auto_digits = cfg->digits == 0;
+  C->gram_free = (cfg->flags & AVD_FLAG_GRAM_FREE) != 0;
   C->m_pad = round_up(m, kGramTile);
   C->m_pad32 = round_up(m, 32);
   C->l_pad = round_up(cfg->l_local, kGramK);
@@ -398,6 +403,7 @@ void avd_destroy(avd_ctx* c) {
   if (c->ev_host) cudaEventDestroy(c->ev_host);
   cudaFree(c->X_stage);
   cudaFree(c->o_mu); cudaFree(c->o_V); cudaFree(c->o_sigma); cudaFree(c->o_rho); cudaFree(c->o_idx);
+  for (void* q : c->gf_allocs) cudaFree(q);
   delete c;
 }
 
@@ -510,7 +516,7 @@ avd_status avd_stage_gram(avd_ctx* c, const float* X) {
     AVD_CUDA(cudaMemcpyAsync(c->qsum, c->qsum_local, sizeof(long long) * 2 * c->cfg.m, cudaMemcpyDeviceToDevice,
                              c->stream));
     AVD_CUDA(cudaMemcpyAsync(c->qerr, c->qerr_local, sizeof(double) * c->m_pad, cudaMemcpyDeviceToDevice, c->stream));
-    AVD_TRY(launch_gram(c));
+    if (!c->gram_free) AVD_TRY(launch_gram(c));
     if (c->gram_p) AVD_TRY(launch_gram_pack(c, false));  // world > 1: the exchanged form
     c->requantised = true;
     c->stage = 3;
@@ -527,14 +533,14 @@ avd_status avd_stage_gram(avd_ctx* c, const float* X) {
     AVD_CUDA(cudaMemcpyAsync(c->qsum, c->qsum_local, sizeof(long long) * 2 * c->cfg.m, cudaMemcpyDeviceToDevice,
                              c->stream));
     AVD_CUDA(cudaMemcpyAsync(c->qerr, c->qerr_local, sizeof(double) * c->m_pad, cudaMemcpyDeviceToDevice, c->stream));
-    return launch_gram(c);
+    return c->gram_free ? AVD_OK : launch_gram(c);  // Gram-free: no Gram
   };
   const bool force_exact = (c->cfg.flags & AVD_FLAG_EXACT_SCALE) != 0;
   if (!force_exact) {  // gated on the device: skipped when an entry overflowed the sampled range
     AVD_CUDA(cudaMemcpyAsync(c->qsum, c->qsum_local, sizeof(long long) * 2 * c->cfg.m, cudaMemcpyDeviceToDevice,
                              c->stream));
     AVD_CUDA(cudaMemcpyAsync(c->qerr, c->qerr_local, sizeof(double) * c->m_pad, cudaMemcpyDeviceToDevice, c->stream));
-    AVD_TRY(launch_gram(c, c->stats + c->cfg.m + 3));
+    if (!c->gram_free) AVD_TRY(launch_gram(c, c->stats + c->cfg.m + 3));
   }
   AVD_CUDA(cudaEventSynchronize(c->ev_host));
   const double ovf = hs[0];
@@ -560,11 +566,19 @@ avd_status avd_stage_gram(avd_ctx* c, const float* X) {
 
 static avd_status stage_eig_impl(avd_ctx* c, int32_t rank, avd_exchange_fn fn, void* user) {
   STAGE_CHECK(c, 3);
-  if (c->gram_p) AVD_TRY(launch_gram_pack(c, true));  // the exchanged packed tiles back into G_int
-  AVD_TRY(launch_gram_finalize(c));
-  AVD_TRY(launch_uncentred(c));  // mean-bias diagnostics, side stream
-  avd_status st = fn ? run_eig_dist(c, rank, fn, user) : run_eig(c);
-  AVD_TRY(join_uncentred(c));    // (stream order only; G32 is not rewritten before the join)
+  avd_status st;
+  if (c->gram_free) {  // no Gram; tr(G) and diag(G) from the fused pass's sums
+    AVD_TRY(gf_prepare(c));
+    AVD_TRY(gf_diag(c));
+    AVD_TRY(launch_trace(c));
+    st = run_eig(c);
+  } else {
+    if (c->gram_p) AVD_TRY(launch_gram_pack(c, true));  // the exchanged packed tiles back into G_int
+    AVD_TRY(launch_gram_finalize(c));
+    AVD_TRY(launch_uncentred(c));  // mean-bias diagnostics, side stream
+    st = fn ? run_eig_dist(c, rank, fn, user) : run_eig(c);
+    AVD_TRY(join_uncentred(c));    // (stream order only; G32 is not rewritten before the join)
+  }
   if (st != AVD_OK && st != AVD_ENOCONV) return st;
   // automatic digits (avd_config.digits == 0): the quantisation-error bound decides whether the
   // 2-digit operand meets half the north-star tolerances; if not, redo the Gram with 3 digits.
@@ -623,6 +637,14 @@ avd_status avd_stage_gather(avd_ctx* c, const float* X, int32_t rank, avd_output
   if (!out || !out->top_idx_dev || !out->rho_dev) { set_error("null output arrays"); return AVD_EINVAL; }
   AVD_TRY(launch_gather(c, X, rank, out->top_idx_dev, out->rho_dev));
   c->stage = 10;
+  return AVD_OK;
+}
+
+avd_status avd_gram_product(avd_ctx* c, const double* In, double* Y) {
+  if (!c || !In || !Y) { set_error("null argument"); return AVD_EINVAL; }
+  if (c->stage < 4) { set_error("avd_gram_product needs a completed eigen stage (or avd_decompose)"); return AVD_ESTATE; }
+  AVD_TRY(gram_product(c, In, Y));
+  AVD_CUDA(cudaStreamSynchronize(c->stream));
   return AVD_OK;
 }
 
@@ -711,7 +733,11 @@ avd_status avd_stage_report(avd_ctx* c, avd_outputs* out) {
     c->cos_mu_v1 = nmu > 0.0 ? std::min(1.0, std::fabs(h[27]) / nmu) : 0.0;
     c->resid_u = h[26];
     c->iters_u = (int)h[29];
-    c->launches += (int64_t)c->n_u_nodes * (int64_t)h[28];
+    if (!c->gram_free) c->launches += (int64_t)c->n_u_nodes * (int64_t)h[28];
+    if (c->gram_free) {  // the uncentred pair needs G (not formed)
+      c->sigma1_u = c->alpha1 = c->cos_mu_v1 = c->resid_u = std::nan("");
+      c->iters_u = 0;
+    }
   }
   out->cos_mu_v1 = c->cos_mu_v1;
   out->alpha1 = c->alpha1;

@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "../../include/avd.h"
 
@@ -179,6 +180,21 @@ struct Ctx {
   // host path
   float* X_stage = nullptr;             // device copy for avd_decompose_host
   size_t ws_bytes = 0;
+  // Gram-free products (AVD_FLAG_GRAM_FREE; k_gramfree.cu), allocated on first use
+  bool gram_free = false;
+  int8_t* gf_wd = nullptr;        // [4][KQ][m_pad] digits of 2^-s In
+  double* gf_wsc = nullptr;       // [2 KQ]: column scales t_r | centring terms corr_r
+  double* gf_tq = nullptr;        // [KQ] scales of P's digits
+  unsigned* gf_pmax = nullptr;    // [KQ] column max |P| (fp32 bit patterns)
+  long long* gf_zsum = nullptr;   // [KQ] column sums of P's integer codes
+  float* gf_P = nullptr;          // [l_pad][KQ] P = Xhat In
+  int8_t* gf_pd = nullptr;        // [4][l_pad][KQ] digits of P
+  long long* gf_zi = nullptr;     // [m_pad][KQ] Xq^T Pd, high word (weight 2^28; reset after each product)
+  long long* gf_zlo = nullptr;    // [m_pad][KQ] low word
+  double* gf_dd = nullptr;        // [m_pad] exact minus quantised diagonal of Xhat^T Xhat
+  long long* gf_qsq = nullptr;    // [m_pad] sum_i q_ij^2 of the digit planes
+  CUtensorMap* gf_tm = nullptr;   // [3] device-resident tensor maps (X digits, W digits, P digits)
+  std::vector<void*> gf_allocs;
 };
 
 // ---------------------------------------------------------------- errors
@@ -249,5 +265,10 @@ avd_status launch_project_reduce(Ctx* c);                  // k_project.cu
 bool project_tc_supported(const Ctx* c, const float* X); // k_project_tc.cu
 avd_status launch_project_tc(Ctx* c, const float* X);    // k_project_tc.cu
 avd_status launch_agg_reduce(Ctx* c);                      // k_select.cu
+avd_status gf_prepare(Ctx* c);                             // k_gramfree.cu
+avd_status gf_product(Ctx* c, const double* In, double* Y, float* Y32, const int* skip);
+avd_status gf_diag(Ctx* c);
+avd_status launch_trace(Ctx* c);                           // k_eig.cu
+avd_status gram_product(Ctx* c, const double* In, double* Y);  // k_eig.cu
 
 }  // namespace avd

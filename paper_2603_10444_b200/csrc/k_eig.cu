@@ -1,3 +1,4 @@
+#include <vector>
 // k_eig.cu — K4: top-k eigenpairs of the centred Gram G (on device) by block subspace iteration
 // with Rayleigh-Ritz: V_k, sigma_k = sqrt(lambda_k) are the right singular vectors / values of
 // Xc that define the rank-k spike.
@@ -1371,7 +1372,10 @@ avd_status enqueue_rr(Ctx* c, cudaGraphConditionalHandle h_loop, cudaGraphCondit
   const int p = c->p, k = c->k;
   EigCtl* ctl = reinterpret_cast<EigCtl*>(c->eig_ctl);
   int* jstats = reinterpret_cast<int*>(c->theta + p);
-  AVD_TRY(gemm64(c, c->Q, c->Y, nullptr));  // Y = G Q (exact G, fp64)
+  if (c->gram_free)
+    AVD_TRY(gf_product(c, c->Q, c->Y, nullptr, nullptr));  // Y = Xhat^T (Xhat Q)
+  else
+    AVD_TRY(gemm64(c, c->Q, c->Y, nullptr));  // Y = G Q (exact G, fp64)
   AVD_TRY(atb_fused<2>(c, c->Q, c->Y, c->W, c->theta, nullptr, &ctl->last_sweeps, nullptr, 40, &ctl->msw));
   AVD_TRY(matpp(c, c->Y, c->Z, c->Z32, c->Q, c->U, nullptr, c->W));  // Z = Y W, U = Q W (Ritz vectors)
   resid_kernel<<<k, 256, 0, c->stream>>>(c->Z, c->U, c->theta, m, p, c->resid);
@@ -1382,7 +1386,10 @@ avd_status enqueue_rr(Ctx* c, cudaGraphConditionalHandle h_loop, cudaGraphCondit
 }
 avd_status enqueue_pow(Ctx* c) {
   EigCtl* ctl = reinterpret_cast<EigCtl*>(c->eig_ctl);
-  if (eig_i8_enabled(c)) {  // int8 tensor-core products (k_eig_i8.cu)
+  if (c->gram_free) {  // Gram-free: G Q = Xhat^T (Xhat Q), two streaming passes (k_gramfree.cu)
+    AVD_TRY(gf_product(c, c->Q, c->Z, c->Z32, &ctl->rr_now));
+    AVD_TRY(gf_product(c, c->Z, c->Y, nullptr, nullptr));
+  } else if (eig_i8_enabled(c)) {  // int8 tensor-core products (k_eig_i8.cu)
     AVD_TRY(gemm_i8(c, c->Q, c->Z, c->Z32, &ctl->rr_now, 0, 0));  // Z = G Q (a check already made Z = G U)
     AVD_TRY(gemm_i8(c, c->Z, c->Y, nullptr, nullptr, 0, 0));       // Y = G Z = G^2 Q
   } else {
@@ -1480,7 +1487,12 @@ bool eig_nograph_env() {
   return v;
 }
 
-bool eig_nograph(const Ctx* c) { return eig_nograph_env() || (c->cfg.flags & AVD_FLAG_EIG_HOST_LOOP) != 0; }
+// The Gram-free products are templated on the digit count, which the automatic
+// escalation can change after the graph was captured, and each costs two passes over the operand,
+// so their loop is host-driven (one synchronisation per decision is noise next to a product).
+bool eig_nograph(const Ctx* c) {
+  return eig_nograph_env() || (c->cfg.flags & AVD_FLAG_EIG_HOST_LOOP) != 0 || c->gram_free;
+}
 
 avd_status ensure_graphs(Ctx* c) {
   if (!c->side_stream) AVD_CUDA(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
@@ -1493,6 +1505,13 @@ avd_status ensure_graphs(Ctx* c) {
 }
 
 }  // namespace
+
+avd_status launch_trace(Ctx* c) {
+  trace_kernel<<<1, 1024, 0, c->stream>>>(c->G, c->cfg.m, c->m_pad, c->ysq, c->mu0, (double)c->cfg.l_global, c->stats,
+                                          c->trace, c->gmax);
+  AVD_LAUNCHED(c);
+  return AVD_OK;
+}
 
 avd_status launch_gram_finalize(Ctx* c) {
   const int64_t m = c->cfg.m;
@@ -1644,6 +1663,17 @@ avd_status run_eig(Ctx* c) {
     AVD_CUDA(cudaGraphLaunch(c->eig_exec, c->stream));
   }
   return eig_epilogue(c, !nograph);
+}
+
+// Y = G In for the context's current Gram operand (avd_gram_product): the formed fp64 G, or with
+// AVD_FLAG_GRAM_FREE the two streaming passes Xhat^T (Xhat In)
+avd_status gram_product(Ctx* c, const double* In, double* Y) {
+  if (c->gram_free) {
+    AVD_TRY(gf_prepare(c));
+    AVD_TRY(gf_product(c, In, Y, nullptr, nullptr));
+    return AVD_OK;
+  }
+  return gemm64(c, In, Y, nullptr);
 }
 
 // Distributed eigensolve: every rank holds the exchanged G, and each G Q product

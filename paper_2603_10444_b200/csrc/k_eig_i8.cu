@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(kG8Threads, 1) gemm_i8_kernel(
 bool eig_i8_enabled(const Ctx* c) {
   static const bool off = [] { const char* e = std::getenv("AVD_EIG_SIMT"); return e && e[0] == '1'; }();
   // small m (c1, c2): the SIMT product's latency beats the digit conversions' fixed cost
-  return !off && c->p <= 112 && c->gd != nullptr && c->cfg.m >= 3072;
+  return !off && !c->gram_free && c->p <= 112 && c->gd != nullptr && c->cfg.m >= 3072;
 }
 
 // stage bytes and ring depth of one instantiation (<= ~200 KB of dynamic shared memory)
