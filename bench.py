@@ -45,6 +45,14 @@ AVERIS_SHAPE = (131072, 4096, 4096)
 AVERIS_METRIC = "Averis NVFP4 forward GeMM throughput (2*l*m*n flop/s, mean split + quantisation inside)"
 
 
+def _traffic(key):
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(key)
+    except OSError:
+        return None
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -439,9 +447,10 @@ def run_averis(args, rank, world, local):
                    "l2": "X (2.1 GB) and Y (2.1 GB) larger than L2; no flush", "parallelism": f"replicas x{world}"},
         "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches),
         "stage_ms": {"stats+mu_bar+bias": stage[0], "quantise X_R": stage[1], "gemm": stage[2]},
-        "roofline": {"bound": "tensor", "kernel": "av_gemm_kernel (tcgen05.mma kind::mxf4nvf4 block16)",
+        "roofline": {"bound": "tensor", "kernel": "av_gemm_kernel (tcgen05.mma.cta_group::2 kind::mxf4nvf4 block16)",
                      "achieved": flops / t_gemm / 1e12, "peak": fp4_peak, "unit": "TFLOP/s",
-                     "frac": flops / t_gemm / 1e12 / fp4_peak, "traffic": None,
+                     "frac": flops / t_gemm / 1e12 / fp4_peak, "traffic": _traffic("averis_gemm"),
+                     "traffic_note": "ncu dram bytes of one launch: X_R codes + W codes read, Y (fp32, 2.15 GB) written",
                      "peak_source": f"{which}: 4 x bf16_tflops (burst; fp4 dense = 4x bf16 nominal)",
                      "algorithmic_flops_per_launch": flops, "launch_ms": stage[2]},
         "streaming_roofline": {

@@ -575,9 +575,18 @@ avd_status gf_product(Ctx* c, const double* In, double* Y, float* Y32, const int
   const int64_t grid1 = std::min<int64_t>(ceil_div(c->cfg.l_local, 128) * NH, c->num_sms);
   const int T = (int)(c->m_pad / 128);
   const int64_t NK = c->l_pad / 128;
-  // row-range splits: fill the SMs, every unit <= 256 stages (int32 class sums stay exact)
-  int S = (int)std::max<int64_t>(ceil_div(NK, 256), ceil_div(c->num_sms, (int64_t)T * NH));
-  S = (int)std::min<int64_t>(S, NK);
+  // row-range splits: every unit <= 256 stages (int32 class sums stay exact); among those, the S
+  // whose whole waves of units finish first (time ~ waves x stages per unit, plus a small
+  // per-unit epilogue cost)
+  int S = 1;
+  {
+    double best = 1e300;
+    const int64_t tiles = (int64_t)T * NH;
+    for (int64_t s = std::max<int64_t>(1, ceil_div(NK, 256)); s <= std::min<int64_t>(NK, 64); ++s) {
+      const double t = (double)ceil_div(tiles * s, c->num_sms) * ((double)ceil_div(NK, s) + 4.0);
+      if (t < best - 1e-9) { best = t; S = (int)s; }
+    }
+  }
   const int grid3 = (int)std::min<int64_t>((int64_t)T * S * NH, c->num_sms);
   const bool nd3 = c->nd == 3;
   AVD_TRY(nd3 ? launch_gf<3>(c, KQ, grid1, T, S, grid3, skip) : launch_gf<2>(c, KQ, grid1, T, S, grid3, skip));
@@ -588,27 +597,44 @@ avd_status gf_product(Ctx* c, const double* In, double* Y, float* Y32, const int
   return AVD_OK;
 }
 
-// Sum_i q_ij^2 from the digit planes (the fused pass does not carry it): four columns per thread,
-// a row chunk per CTA row, exact int64 atomics (order-free)
+// Sum_i q_ij^2 from the digit planes (the fused pass does not carry it): sixteen columns per
+// thread (one 16-byte load per plane and row, four rows in flight), a row chunk per CTA row,
+// exact int64 atomics (order-free)
 __global__ void __launch_bounds__(256) gf_qsq_kernel(const int8_t* __restrict__ digits, int nd, int64_t l_local,
                                                      int64_t l_pad, int64_t m, int64_t m_pad, int64_t rows_per,
                                                      unsigned long long* __restrict__ qsq) {
-  const int64_t j = ((int64_t)blockIdx.x * 256 + threadIdx.x) * 4;
+  const int64_t j = ((int64_t)blockIdx.x * 256 + threadIdx.x) * 16;
   if (j >= m_pad) return;
   const int64_t r0 = (int64_t)blockIdx.y * rows_per, r1 = min(l_local, r0 + rows_per);
-  long long s[4] = {0, 0, 0, 0};
-  for (int64_t r = r0; r < r1; ++r) {
-    int q[4] = {0, 0, 0, 0};
-    for (int e = 0; e < nd; ++e) {
-      const uint32_t w = *reinterpret_cast<const uint32_t*>(digits + ((int64_t)e * l_pad + r) * m_pad + j);
+  long long s[16];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) q[t] = q[t] * 128 + (int)(int8_t)(w >> (8 * t));
+  for (int t = 0; t < 16; ++t) s[t] = 0;
+  for (int64_t r = r0; r < r1; r += 4) {
+    uint4 w[3][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int e = 0; e < 3; ++e)
+        w[e][u] = (e < nd && r + u < r1)
+                      ? __ldcs(reinterpret_cast<const uint4*>(digits + ((int64_t)e * l_pad + r + u) * m_pad + j))
+                      : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        int q = 0;
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+          if (e >= nd) break;
+          const uint32_t word = t < 4 ? w[e][u].x : (t < 8 ? w[e][u].y : (t < 12 ? w[e][u].z : w[e][u].w));
+          q = q * 128 + (int)(int8_t)(word >> (8 * (t & 3)));
+        }
+        s[t] += (long long)q * q;
+      }
     }
-#pragma unroll
-    for (int t = 0; t < 4; ++t) s[t] += (long long)q[t] * q[t];
   }
 #pragma unroll
-  for (int t = 0; t < 4; ++t)
+  for (int t = 0; t < 16; ++t)
     if (j + t < m && s[t]) atomicAdd(qsq + j + t, (unsigned long long)s[t]);
 }
 
@@ -629,9 +655,9 @@ __global__ void gf_diag_kernel(int64_t m, int64_t m_pad, const double* __restric
   dd[j] = g - ldexp((double)(long long)qsq[j] - S * S / l, -2 * shift[j]);
 }
 avd_status gf_diag(Ctx* c) {
-  const int64_t rows_per = 1024;
+  const int64_t rows_per = 256;
   AVD_CUDA(cudaMemsetAsync(c->gf_qsq, 0, sizeof(long long) * c->m_pad, c->stream));
-  dim3 grid((unsigned)ceil_div(c->m_pad, 1024), (unsigned)ceil_div(c->cfg.l_local, rows_per));
+  dim3 grid((unsigned)ceil_div(c->m_pad, 4096), (unsigned)ceil_div(c->cfg.l_local, rows_per));
   gf_qsq_kernel<<<grid, 256, 0, c->stream>>>(c->digits, c->nd, c->cfg.l_local, c->l_pad, c->cfg.m, c->m_pad, rows_per,
                                              reinterpret_cast<unsigned long long*>(c->gf_qsq));
   AVD_LAUNCHED(c);
