@@ -149,21 +149,32 @@ __global__ void __launch_bounds__(256) av_colstats_kernel(const float* __restric
   *reinterpret_cast<float4*>(cmin + o) = mn;
 }
 
-// mu (fixed-order sum of the row-chunk partials), mu_f, and the tensor amax of X_R and of mu_f
+// mu (fixed-order sum of the row-chunk partials), mu_f, and the tensor amax of X_R and of mu_f.
+// CTA = 32 columns x 8 partial-row groups: thread (g, c) sums the partials y = g (mod 8) of column
+// c (coalesced 32-column rows), the 8 group sums are combined in a fixed order in shared memory.
 __global__ void __launch_bounds__(256) av_reduce_kernel(const double* __restrict__ csum, const float* __restrict__ cmax,
                                                         const float* __restrict__ cmin, int R, int64_t l, int64_t m,
                                                         int vanilla, double* __restrict__ mu, float* __restrict__ mu_f,
                                                         float* __restrict__ gsc) {
-  const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
-  float a = 0.f, am = 0.f;
+  __shared__ double s_s[8][32];
+  __shared__ float s_x[8][32], s_n[8][32];
+  const int c = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t j = (int64_t)blockIdx.x * 32 + c;
+  double s = 0;
+  float mx = -INFINITY, mn = INFINITY;
   if (j < m) {
-    double s = 0;
-    float mx = -INFINITY, mn = INFINITY;
-    for (int y = 0; y < R; ++y) {
+    for (int y = g; y < R; y += 8) {
       s += csum[(int64_t)y * m + j];
       mx = fmaxf(mx, cmax[(int64_t)y * m + j]);
       mn = fminf(mn, cmin[(int64_t)y * m + j]);
     }
+  }
+  s_s[g][c] = s; s_x[g][c] = mx; s_n[g][c] = mn;
+  __syncthreads();
+  if (g != 0) return;
+  float a = 0.f, am = 0.f;
+  if (j < m) {
+    for (int h = 1; h < 8; ++h) { s += s_s[h][c]; mx = fmaxf(mx, s_x[h][c]); mn = fminf(mn, s_n[h][c]); }
     const double u = vanilla ? 0.0 : s / (double)l;
     const float uf = (float)u;
     mu[j] = u;
@@ -176,7 +187,7 @@ __global__ void __launch_bounds__(256) av_reduce_kernel(const double* __restrict
     a = fmaxf(a, __shfl_xor_sync(0xFFFFFFFFu, a, o));
     am = fmaxf(am, __shfl_xor_sync(0xFFFFFFFFu, am, o));
   }
-  if ((threadIdx.x & 31) == 0) {
+  if (c == 0) {
     atomicMax(reinterpret_cast<unsigned*>(gsc + 3), __float_as_uint(a));
     atomicMax(reinterpret_cast<unsigned*>(gsc + 5), __float_as_uint(am));
   }
@@ -625,8 +636,8 @@ avd_status av_forward(AvCtx* c, const float* X, float* Y) {
   av_colstats_kernel<<<dim3((unsigned)ceil_div(m, 1024), (unsigned)c->R), 256, 0, c->stream>>>(
       X, l, m, rows_per, c->csum_part, c->cmax_part, c->cmin_part);
   AVD_LAUNCHED(c);
-  av_reduce_kernel<<<(unsigned)ceil_div(m, 256), 256, 0, c->stream>>>(c->csum_part, c->cmax_part, c->cmin_part, c->R,
-                                                                       l, m, c->vanilla ? 1 : 0, c->mu, c->mu_f, c->gsc);
+  av_reduce_kernel<<<(unsigned)ceil_div(m, 32), 256, 0, c->stream>>>(c->csum_part, c->cmax_part, c->cmin_part, c->R,
+                                                                      l, m, c->vanilla ? 1 : 0, c->mu, c->mu_f, c->gsc);
   AVD_LAUNCHED(c);
   const uint64_t seed = c->cfg.seed;
   if (!c->vanilla) {
