@@ -382,8 +382,9 @@ def run_averis(args, rank, world, local):
     l, m, n = AVERIS_SHAPE
     X = generate(config_spec("c4"), device="cuda")
     W = generate_weight(m, n, seed=0, device="cuda")
-    Y = torch.empty(l, n, dtype=torch.float32, device="cuda")
-    g = AverisGemm(l, m, n, timing=True)
+    bf = args.variant == "bf16"
+    Y = torch.empty(l, n, dtype=torch.bfloat16 if bf else torch.float32, device="cuda")
+    g = AverisGemm(l, m, n, timing=True, bf16_out=bf)
     g.set_weight(W)
 
     def barrier():
@@ -426,14 +427,14 @@ def run_averis(args, rank, world, local):
     e2e = None
     if not args.no_e2e:
         Xh = X.cpu().pin_memory()
-        Yh = torch.empty(l, n, dtype=torch.float32).pin_memory()
+        Yh = torch.empty(l, n, dtype=Y.dtype).pin_memory()
         g.forward_host(Xh, Yh)
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             g.forward_host(Xh, Yh)
         e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
         e2e = {"value": world * flops / (e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": l * m * 4,
-               "d2h_bytes_per_step": l * n * 4, "ms_per_step": e_ms}
+               "d2h_bytes_per_step": l * n * Y.element_size(), "ms_per_step": e_ms}
     peaks, which = _peaks()
     fp4_peak = 4.0 * peaks.get("bf16_tflops")
     t_gemm = stage[2] * 1e-3
@@ -441,7 +442,7 @@ def run_averis(args, rank, world, local):
     line = {
         "metric": AVERIS_METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "nvfp4 (e2m1 + ue4m3/16) x nvfp4 -> f32",
+        "vs_baseline": None, "dtype": "nvfp4 (e2m1 + ue4m3/16) x nvfp4 -> " + ("bf16" if bf else "f32"),
         "data": "synthetic (X: synth/gen.py c4 seed 0, mean-biased with massive columns; W: generate_weight seed 0)",
         "config": {"workload": WORKLOADS["averis"], "l": l, "m": m, "n": n, "rounding": "nearest",
                    "l2": "X (2.1 GB) and Y (2.1 GB) larger than L2; no flush", "parallelism": f"replicas x{world}"},
@@ -450,7 +451,7 @@ def run_averis(args, rank, world, local):
         "roofline": {"bound": "tensor", "kernel": "av_gemm_kernel (tcgen05.mma.cta_group::2 kind::mxf4nvf4 block16)",
                      "achieved": flops / t_gemm / 1e12, "peak": fp4_peak, "unit": "TFLOP/s",
                      "frac": flops / t_gemm / 1e12 / fp4_peak, "traffic": _traffic("averis_gemm"),
-                     "traffic_note": "ncu dram bytes of one launch: X_R codes + W codes read, Y (fp32, 2.15 GB) written",
+                     "traffic_note": "ncu dram bytes of one launch (fp32 Y): X_R codes + W codes read, Y (2.15 GB) written",
                      "peak_source": f"{which}: 4 x bf16_tflops (burst; fp4 dense = 4x bf16 nominal)",
                      "algorithmic_flops_per_launch": flops, "launch_ms": stage[2]},
         "streaming_roofline": {
@@ -483,11 +484,12 @@ def main():
     ap.add_argument("--cpu-baseline-rows", type=int, default=0,
                     help="rows of the oracle sample (0: 8192 for c4/c5, all rows below; -1: all rows)")
     ap.add_argument("--cpu-baseline-eig", default="lapack", choices=["lapack", "jacobi"])
-    ap.add_argument("--variant", default="base", choices=["base", "massive", "gramfree"],
+    ap.add_argument("--variant", default="base", choices=["base", "massive", "gramfree", "bf16"],
                     help="massive: plant single-token massive activations (PAPER.md:245-246) in an "
                          "unsampled row, which forces the exact-range requantisation and exercises "
                          "the automatic digit escalation inside the timed region; gramfree: the "
-                         "Gram-free eigensolve (AVD_FLAG_GRAM_FREE, SURVEY 8(f4))")
+                         "Gram-free eigensolve (AVD_FLAG_GRAM_FREE, SURVEY 8(f4)); bf16 (--config averis): "
+                         "Y in bf16")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (huge configs)")
     args = ap.parse_args()
     if args.impl == "reference":

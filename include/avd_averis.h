@@ -36,6 +36,8 @@ extern "C" {
 #define AVD_AVERIS_VANILLA 2    /* no split: Y = Q_b(X) Q_b(W) (the paper's "Vanilla FP4")          */
 #define AVD_AVERIS_TIMING 4     /* record CUDA events at the stage boundaries of each forward
                                    (read with avd_averis_stage_ms)                                  */
+#define AVD_AVERIS_BF16_OUT 8   /* Y in bf16 (round to nearest even of the fp32 epilogue value: the
+                                   output type of the paper's FP4 training GeMMs); default fp32     */
 
 typedef struct {
   int64_t l;       /* tokens (rows of X and Y), >= 1                                     */
@@ -60,15 +62,15 @@ avd_status avd_averis_destroy(avd_averis_handle h);
  * work completes (stream-ordered). */
 avd_status avd_averis_set_weight(avd_averis_handle h, const float* W_dev);
 
-/* Y_dev (fp32, row-major [l][n], caller-owned) = Eq. averis_forward for X_dev (fp32, row-major
- * [l][m], 16-byte aligned, finite).  Stream-ordered, returns without synchronising.
- * ESTATE: no weight set. */
-avd_status avd_averis_forward(avd_averis_handle h, const float* X_dev, float* Y_dev);
+/* Y_dev (row-major [l][n], fp32 — or bf16 with AVD_AVERIS_BF16_OUT —, caller-owned) = Eq.
+ * averis_forward for X_dev (fp32, row-major [l][m], 16-byte aligned, finite).  Stream-ordered,
+ * returns without synchronising.  ESTATE: no weight set. */
+avd_status avd_averis_forward(avd_averis_handle h, const float* X_dev, void* Y_dev);
 
 /* The same from host memory: copies X_host (l*m fp32) in, runs avd_averis_forward, copies Y
- * (l*n fp32) out to Y_host; synchronises the stream before returning.  Pinned host buffers
- * are copied asynchronously, pageable ones synchronously. */
-avd_status avd_averis_forward_host(avd_averis_handle h, const float* X_host, float* Y_host);
+ * (l*n fp32 or bf16) out to Y_host; synchronises the stream before returning.  Pinned host
+ * buffers are copied asynchronously, pageable ones synchronously. */
+avd_status avd_averis_forward_host(avd_averis_handle h, const float* X_host, void* Y_host);
 
 /* Workspace buffers for checks (device pointer and byte size; valid until destroy):
  *   AVD_AV_MU      f64 [m]   mu_X (zero with AVD_AVERIS_VANILLA)

@@ -36,7 +36,7 @@ EXPORTS = ["avd_plan", "avd_create", "avd_destroy", "avd_get_plan", "avd_decompo
 EXPORTS_AVERIS = ["avd_averis_create", "avd_averis_destroy", "avd_averis_set_weight", "avd_averis_forward",
                   "avd_averis_forward_host", "avd_averis_buffer", "avd_averis_launch_count",
                   "avd_averis_stage_ms"]
-AVD_AVERIS_STOCHASTIC, AVD_AVERIS_VANILLA, AVD_AVERIS_TIMING = 1, 2, 4
+AVD_AVERIS_STOCHASTIC, AVD_AVERIS_VANILLA, AVD_AVERIS_TIMING, AVD_AVERIS_BF16_OUT = 1, 2, 4, 8
 AV_BUF = dict(MU=0, XCODES=1, XSF=2, WCODES=3, WSF=4, MUCODES=5, MUSF=6, GSCALE=7, BIAS=8)
 
 

@@ -18,15 +18,16 @@ class AverisGemm:
 
     def __init__(self, l: int, m: int, n: int, stochastic: bool = False, vanilla: bool = False,
                  seed: int = 0, device: int = 0, stream: torch.cuda.Stream | None = None,
-                 timing: bool = False):
+                 timing: bool = False, bf16_out: bool = False):
         self.l, self.m, self.n = l, m, n
         self.stream = stream or torch.cuda.current_stream(device)
         cfg = L.avd_averis_config()
         cfg.l, cfg.m, cfg.n = l, m, n
         cfg.flags = (L.AVD_AVERIS_STOCHASTIC if stochastic else 0) | (L.AVD_AVERIS_VANILLA if vanilla else 0) | \
-            (L.AVD_AVERIS_TIMING if timing else 0)
+            (L.AVD_AVERIS_TIMING if timing else 0) | (L.AVD_AVERIS_BF16_OUT if bf16_out else 0)
         cfg.seed, cfg.device, cfg.stream = seed, device, self.stream.cuda_stream
         self.device = torch.device("cuda", device)
+        self.out_dtype = torch.bfloat16 if bf16_out else torch.float32
         self.h = L.avd_averis_create(cfg)
 
     def set_weight(self, W: torch.Tensor) -> None:
@@ -37,7 +38,7 @@ class AverisGemm:
     def forward(self, X: torch.Tensor, Y: torch.Tensor | None = None) -> torch.Tensor:
         assert X.dtype == torch.float32 and X.is_contiguous() and tuple(X.shape) == (self.l, self.m)
         if Y is None:
-            Y = torch.empty(self.l, self.n, dtype=torch.float32, device=self.device)
+            Y = torch.empty(self.l, self.n, dtype=self.out_dtype, device=self.device)
         L.avd_averis_forward(self.h, X.data_ptr(), Y.data_ptr())
         return Y
 

@@ -38,7 +38,7 @@ struct AvCtx {
   int R = 1;        // row chunks of the column statistics
   int64_t launches = 0;
   bool weight_set = false;
-  bool vanilla = false, sr = false;
+  bool vanilla = false, sr = false, bf16_out = false;
   double* csum_part = nullptr;   // [R][m]
   float* cmax_part = nullptr;    // [R][m]
   float* cmin_part = nullptr;    // [R][m]
@@ -54,7 +54,7 @@ struct AvCtx {
   float* bias = nullptr;         // [n]
   CUtensorMap tmA{}, tmB{}, tmSA{}, tmSB{};
   float* X_stage = nullptr;
-  float* Y_stage = nullptr;
+  void* Y_stage = nullptr;
   std::vector<void*> allocs;
   bool timing = false;
   int dbg = 0;  // AVD_AV_DBG (timing experiments only): 1 no stores, 2 no epilogue, 4 no scale copies
@@ -420,6 +420,11 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
                : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+__device__ __forceinline__ uint32_t bf16x2(float lo, float hi) {  // RNE, lo in the low half
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
@@ -435,6 +440,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
 }
 
 constexpr int kAvNS = 5;
+template <bool BF>  // BF: Y in bf16 (RNE), else fp32
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kAvGemmThreads, 1) av_gemm_kernel(
     const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
     const __grid_constant__ CUtensorMap tmSA, const __grid_constant__ CUtensorMap tmSB,
@@ -548,26 +554,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kAvGemmThreads, 1) a
       const int64_t col0 = nt * 256 + h * 128;
       if (row0 < l && !(dbg & 1)) {
         const uint32_t sw = lane & 7;
+        // per store: 32 rows x 128 B (32 fp32 or 64 bf16 columns), 128B-swizzled
+        constexpr int CW = BF ? 64 : 32;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (col0 + 32 * c >= n) break;
+        for (int c = 0; c < 128 / CW; ++c) {
+          if (col0 + CW * c >= n) break;
           uint8_t* ob = smem + kAvNS * kAvStage + (warp - 2) * kAvOut;
           if (lane == 0) bulk_wait_read0();  // the previous block's bulk store has read the buffer
           __syncwarp();
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
-            const int cc = 32 * c + 4 * k;
-            const float4 bb = col0 + cc < n ? __ldg(reinterpret_cast<const float4*>(bias + col0 + cc))
-                                            : make_float4(0.f, 0.f, 0.f, 0.f);
-            const float4 y = make_float4(__fmaf_rn(__uint_as_float(v[cc]), gxw, bb.x),
-                                         __fmaf_rn(__uint_as_float(v[cc + 1]), gxw, bb.y),
-                                         __fmaf_rn(__uint_as_float(v[cc + 2]), gxw, bb.z),
-                                         __fmaf_rn(__uint_as_float(v[cc + 3]), gxw, bb.w));
-            *reinterpret_cast<float4*>(ob + lane * 128 + ((k ^ sw) << 4)) = y;
+            if constexpr (BF) {
+              const int cc = 64 * c + 8 * k;
+              float y[8];
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {
+                const float4 bb = col0 + cc + 4 * hh < n ? __ldg(reinterpret_cast<const float4*>(bias + col0 + cc + 4 * hh))
+                                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+                y[4 * hh] = __fmaf_rn(__uint_as_float(v[cc + 4 * hh]), gxw, bb.x);
+                y[4 * hh + 1] = __fmaf_rn(__uint_as_float(v[cc + 4 * hh + 1]), gxw, bb.y);
+                y[4 * hh + 2] = __fmaf_rn(__uint_as_float(v[cc + 4 * hh + 2]), gxw, bb.z);
+                y[4 * hh + 3] = __fmaf_rn(__uint_as_float(v[cc + 4 * hh + 3]), gxw, bb.w);
+              }
+              uint4 pk;
+              pk.x = bf16x2(y[0], y[1]); pk.y = bf16x2(y[2], y[3]); pk.z = bf16x2(y[4], y[5]); pk.w = bf16x2(y[6], y[7]);
+              *reinterpret_cast<uint4*>(ob + lane * 128 + ((k ^ sw) << 4)) = pk;
+            } else {
+              const int cc = 32 * c + 4 * k;
+              const float4 bb = col0 + cc < n ? __ldg(reinterpret_cast<const float4*>(bias + col0 + cc))
+                                              : make_float4(0.f, 0.f, 0.f, 0.f);
+              const float4 y = make_float4(__fmaf_rn(__uint_as_float(v[cc]), gxw, bb.x),
+                                           __fmaf_rn(__uint_as_float(v[cc + 1]), gxw, bb.y),
+                                           __fmaf_rn(__uint_as_float(v[cc + 2]), gxw, bb.z),
+                                           __fmaf_rn(__uint_as_float(v[cc + 3]), gxw, bb.w));
+              *reinterpret_cast<float4*>(ob + lane * 128 + ((k ^ sw) << 4)) = y;
+            }
           }
           fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0) tma_store_2d(&tmY, ob, (int32_t)(col0 + 32 * c), (int32_t)row0);
+          if (lane == 0) tma_store_2d(&tmY, ob, (int32_t)(col0 + CW * c), (int32_t)row0);
         }
       }
     }
@@ -622,7 +647,7 @@ avd_status av_alloc(AvCtx* c, T** p, size_t bytes) {
   return AVD_OK;
 }
 
-avd_status av_forward(AvCtx* c, const float* X, float* Y) {
+avd_status av_forward(AvCtx* c, const float* X, void* Y) {
   if (!c->weight_set) { set_error("avd_averis_forward: no weight (call avd_averis_set_weight first)"); return AVD_ESTATE; }
   if (!X || !Y || (reinterpret_cast<uintptr_t>(X) & 15) || (reinterpret_cast<uintptr_t>(Y) & 15)) {
     set_error("avd_averis_forward: X / Y must be non-null and 16-byte aligned");
@@ -667,19 +692,22 @@ avd_status av_forward(AvCtx* c, const float* X, float* Y) {
   const int64_t MT2 = c->l_pad / 256, NT = c->n_pad / 256;
   const int KB = (int)ceil_div(m, 256);
   const int smem = kAvNS * kAvStage + 8 * kAvOut + 1024;
-  AVD_CUDA(smem_attr(av_gemm_kernel, smem));
+  auto kern = c->bf16_out ? av_gemm_kernel<true> : av_gemm_kernel<false>;
+  AVD_CUDA(smem_attr(kern, smem));
   CUtensorMap tmY;
   {
     auto enc = tma_encode_fn();
-    uint64_t dims[2] = {(uint64_t)n, (uint64_t)l}, strides[1] = {(uint64_t)n * 4};
-    uint32_t box[2] = {32, 32}, es[2] = {1, 1};
-    const CUresult r = enc(&tmY, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Y, dims, strides, box, es,
+    const bool bf = c->bf16_out;
+    uint64_t dims[2] = {(uint64_t)n, (uint64_t)l}, strides[1] = {(uint64_t)n * (bf ? 2 : 4)};
+    uint32_t box[2] = {bf ? 64u : 32u, 32}, es[2] = {1, 1};
+    const CUresult r = enc(&tmY, bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Y, dims,
+                           strides, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled (Averis Y) failed: " + std::to_string((int)r)); return AVD_ECUDA; }
   }
   const int grid = 2 * (int)std::min<int64_t>(MT2 * NT, c->num_sms / 2);
-  av_gemm_kernel<<<grid, kAvGemmThreads, smem, c->stream>>>(c->tmA, c->tmB, c->tmSA, c->tmSB, tmY, l, n, KB, MT2, NT,
+  kern<<<grid, kAvGemmThreads, smem, c->stream>>>(c->tmA, c->tmB, c->tmSA, c->tmSB, tmY, l, n, KB, MT2, NT,
                                                             c->kb4, c->gsc, c->bias, c->dbg);
   AVD_LAUNCHED(c);
   if (c->timing) AVD_CUDA(cudaEventRecord(c->ev[3], c->stream));
@@ -722,6 +750,7 @@ avd_status avd_averis_create(const avd_averis_config* cfg, avd_averis_handle* ou
   c->kb4 = 4 * avd::ceil_div(c->m, 256);
   c->vanilla = (cfg->flags & AVD_AVERIS_VANILLA) != 0;
   c->sr = (cfg->flags & AVD_AVERIS_STOCHASTIC) != 0;
+  c->bf16_out = (cfg->flags & AVD_AVERIS_BF16_OUT) != 0;
   c->timing = (cfg->flags & AVD_AVERIS_TIMING) != 0;
   if (const char* e = getenv("AVD_AV_DBG")) c->dbg = atoi(e);
   for (int i = 0; i < 4 && c->timing; ++i)
@@ -787,15 +816,15 @@ avd_status avd_averis_set_weight(avd_averis_handle h, const float* W) {
   return AVD_OK;
 }
 
-avd_status avd_averis_forward(avd_averis_handle h, const float* X, float* Y) {
+avd_status avd_averis_forward(avd_averis_handle h, const float* X, void* Y) {
   if (!h) { avd::set_error("avd_averis_forward: null handle"); return AVD_EINVAL; }
   return avd::av_forward(&h->c, X, Y);
 }
 
-avd_status avd_averis_forward_host(avd_averis_handle h, const float* Xh, float* Yh) {
+avd_status avd_averis_forward_host(avd_averis_handle h, const float* Xh, void* Yh) {
   if (!h || !Xh || !Yh) { avd::set_error("avd_averis_forward_host: null argument"); return AVD_EINVAL; }
   AvCtx* c = &h->c;
-  const size_t xb = sizeof(float) * c->l * c->m, yb = sizeof(float) * c->l * c->n;
+  const size_t xb = sizeof(float) * c->l * c->m, yb = (c->bf16_out ? 2 : 4) * (size_t)c->l * c->n;
   if (!c->X_stage) {
     if (cudaMalloc(&c->X_stage, xb) != cudaSuccess || cudaMalloc(&c->Y_stage, yb) != cudaSuccess) {
       cudaGetLastError();

@@ -143,3 +143,27 @@ def test_full_size_sampled_rows(cuda_device):
     bound = (m * 2.0 ** -23 + 2.0 ** -20) * absY + 2.0 ** -20 * np.abs(bias)[None, :]
     assert np.all(np.abs(Yg - Yo) <= bound)
     g.close()
+
+
+@pytest.mark.parametrize("l,m,n", [(300, 320, 144), (1024, 1024, 512)])
+def test_averis_bf16_output(cuda_device, l, m, n):
+    """AVD_AVERIS_BF16_OUT: the same fp32 epilogue value rounded to bf16 (RNE): within A9's bound
+    plus half a bf16 ulp (2^-8 relative: 8 significant bits), and equal to torch's RNE cast of the fp32 path's Y."""
+    from paper_2603_10444_b200.averis import AverisGemm
+    X = generate(SynthSpec(l, m, seed=4))
+    W = generate_weight(m, n, seed=4)
+    o = A.averis_forward(X.numpy(), W.numpy())
+    g32 = AverisGemm(l, m, n)
+    g32.set_weight(W.cuda())
+    Y32 = g32(X.cuda())
+    g16 = AverisGemm(l, m, n, bf16_out=True)
+    g16.set_weight(W.cuda())
+    Y16 = g16(X.cuda())
+    torch.cuda.synchronize()
+    assert Y16.dtype == torch.bfloat16
+    assert torch.equal(Y16, Y32.to(torch.bfloat16))
+    Yg = Y16.float().cpu().numpy().astype(np.float64)
+    bound = (m * 2.0 ** -23 + 2.0 ** -20) * o["absY"] + 2.0 ** -20 * np.abs(o["bias"])[None, :] + 2.0 ** -8 * np.abs(o["Y"]) + 1e-30
+    assert np.all(np.abs(Yg - o["Y"]) <= bound)
+    g32.close()
+    g16.close()
