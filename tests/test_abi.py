@@ -57,6 +57,32 @@ def test_plan_rejects_bad_arguments():
     assert msg
 
 
+def test_gram_free_plan_rules():
+    """AVD_FLAG_GRAM_FREE is single-GPU and excludes AVD_FLAG_MEAN_TOPK (include/avd.h)."""
+    pl = L.avd_plan(_cfg(4096, 512, flags=L.AVD_FLAG_GRAM_FREE))
+    assert (pl.k, pl.p) == (5, 16)
+    for cfg in (_cfg(4096, 512, flags=L.AVD_FLAG_GRAM_FREE, world=2, l_local=2048),
+                _cfg(4096, 512, flags=L.AVD_FLAG_GRAM_FREE | L.AVD_FLAG_MEAN_TOPK)):
+        with pytest.raises(L.AvdError) as e:
+            L.avd_plan(cfg)
+        assert e.value.status == L.AVD_EINVAL
+
+
+def test_averis_create_validates():
+    """avd_averis_create: m a multiple of 32, n of 16, l >= 1 (EINVAL), and no device -> ECUDA."""
+    import torch
+    for l, m, n in ((0, 64, 16), (16, 48, 16), (16, 64, 24)):
+        c = L.avd_averis_config()
+        c.l, c.m, c.n = l, m, n
+        h = ctypes.c_void_p()
+        assert L.lib().avd_averis_create(ctypes.byref(c), ctypes.byref(h)) == L.AVD_EINVAL and not h.value
+    if not torch.cuda.is_available():
+        c = L.avd_averis_config()
+        c.l, c.m, c.n = 16, 64, 16
+        h = ctypes.c_void_p()
+        assert L.lib().avd_averis_create(ctypes.byref(c), ctypes.byref(h)) == L.AVD_ECUDA and not h.value
+
+
 def test_tie_quota():
     # q = 4 ties to take; ranks hold 2, 3, 10 ties and 5, 3, 4 strictly-greater entries
     assert L.avd_tie_quota([5, 3, 4], [2, 3, 10], 0, 4) == (2, 0)
