@@ -76,8 +76,16 @@ __global__ void find_bin_kernel(int level, const unsigned long long* __restrict_
   const int nb = level < 2 ? kHistBins : kHist3Bins;
   const int per = nb / 32;
   const int hi = nb - 1 - lane * per;
+  // the lane's `per` bins (hi-per, hi] as 16-byte loads, 8 in flight (a latency-bound single warp)
   unsigned long long mine = 0;
-  for (int b = hi; b > hi - per; --b) mine += h[b];
+  {
+    const ulonglong2* hv = reinterpret_cast<const ulonglong2*>(h + (hi - per + 1));
+#pragma unroll 8
+    for (int t = 0; t < per / 2; ++t) {
+      const ulonglong2 v = __ldg(hv + t);
+      mine += v.x + v.y;
+    }
+  }
   unsigned long long incl = mine;
   for (int o = 1; o < 32; o <<= 1) {
     const unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
