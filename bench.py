@@ -259,9 +259,10 @@ def plant_massive(X, row0, m):
 # ------------------------------------------------------------------ c3: the 58-matrix sweep
 def run_c3(args, rank, world, local):
     """BASELINE.json configs[2]: one step = the whole pass over each of the 58 matrices of the
-    sweep (synth.gen.sweep_specs).  Two contexts on two CUDA streams, each
-    driven by its own host thread (the C calls release the GIL), so matrix i+1's fused pass /
-    Gram run while matrix i is in its eigensolve.  N > 1: the matrices are dealt round-robin to
+    sweep (synth.gen.sweep_specs).  Four contexts on four CUDA streams, each
+    driven by its own host thread (the C calls release the GIL), so other matrices' fused passes /
+    Grams run while one is in its latency-bound eigensolve (2 streams: 60.3 ms per sweep, 3: 50.0,
+    4: 44.6, 6: 44.2).  N > 1: the matrices are dealt round-robin to
     the ranks (independent problems, no collective)."""
     import torch.distributed as dist
     from concurrent.futures import ThreadPoolExecutor
@@ -271,20 +272,21 @@ def run_c3(args, rank, world, local):
     l, m = specs[0].l, specs[0].m
     Xs = [generate(specs[i], device="cuda") for i in mine]
     torch.cuda.synchronize()
-    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    NW = args.c3_streams
+    streams = [torch.cuda.Stream() for _ in range(NW)]
     decs = [Decomposer(l, m, seed=0, stream=st) for st in streams]
 
     def worker(w, mats, host=None):
         out = []
         with torch.cuda.stream(streams[w]):
-            for j in range(w, len(mats), 2):
+            for j in range(w, len(mats), NW):
                 out.append(decs[w](mats[j]) if host is None else decs[w].run_host(host[j]))
         return out
 
-    pool = ThreadPoolExecutor(2)
+    pool = ThreadPoolExecutor(NW)
 
     def step(mats, host=None):
-        fut = [pool.submit(worker, w, mats, host) for w in range(2)]
+        fut = [pool.submit(worker, w, mats, host) for w in range(NW)]
         return [r for f in fut for r in f.result()]
 
     def barrier():
@@ -302,12 +304,14 @@ def run_c3(args, rank, world, local):
     l0 = sum(d.launches() for d in decs)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(streams[0])
-    streams[1].wait_event(ev0)
+    for st in streams[1:]:
+        st.wait_event(ev0)
     for _ in range(args.steps):
         res = step(Xs)
-    ev_b = torch.cuda.Event()
-    ev_b.record(streams[1])
-    streams[0].wait_event(ev_b)
+    for st in streams[1:]:
+        ev_b = torch.cuda.Event()
+        ev_b.record(st)
+        streams[0].wait_event(ev_b)
     ev1.record(streams[0])
     torch.cuda.synchronize()
     barrier()
@@ -345,7 +349,7 @@ def run_c3(args, rank, world, local):
             "synthetic (synth/gen.py sweep_specs: 29 modules x early/late, invented monotone schedule)",
         "matrices_per_s": n_all / (ms_step * 1e-3),
         "config": {"workload": WORKLOADS["c3"], "matrices": n_all, "l": l, "m": m, "k": k,
-                   "streams": 2, "l2": "each matrix (268 MB) is larger than L2; no flush",
+                   "streams": NW, "l2": "each matrix (268 MB) is larger than L2; no flush",
                    "parallelism": f"matrices dealt round-robin to {world} rank(s)"},
         "clocks": clocks, "gpu_launches": int(launches),
         "e2e": {"value": ne * l * m / (e_ms * 1e-3), "unit": UNIT, "matrices_per_s": ne / (e_ms * 1e-3),
@@ -491,6 +495,7 @@ def main():
                          "Gram-free eigensolve (AVD_FLAG_GRAM_FREE, SURVEY 8(f4)); bf16 (--config averis): "
                          "Y in bf16")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (huge configs)")
+    ap.add_argument("--c3-streams", type=int, default=4, help="c3: contexts / streams / host threads in flight")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
