@@ -60,6 +60,15 @@ def test_gram_free_deterministic(cuda_device):
     np.testing.assert_array_equal(a["sigma"], b["sigma"])
     np.testing.assert_array_equal(a["V"], b["V"])
     np.testing.assert_array_equal(a["rho"], b["rho"])
+    # the host entry point (avd_decompose_host: H2D and D2H inside) gives the same bits
+    from paper_2603_10444_b200 import Decomposer
+    from paper_2603_10444_b200._lib import AVD_FLAG_GRAM_FREE
+    dec = Decomposer(4096, 512, flags=AVD_FLAG_GRAM_FREE)
+    r = dec.run_host(X.pin_memory())
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(np.asarray(r.sigma.cpu()), a["sigma"])
+    np.testing.assert_array_equal(np.asarray(r.top_idx.cpu()), a["top_idx"])
+    dec.close()
 
 
 def test_gram_free_c4_against_cached_oracle(cuda_device):
