@@ -1061,6 +1061,8 @@ struct EigCtl {
   int iters_u;
   int stop;         // the last check ended the loop
   int stop_u;       // the uncentred loop is done
+  int rr_fast;      // this check is intermediate: its G Q product may be the fp32/int8 one
+  int rr_exact;     // 1 - rr_fast (the gate of the other product)
   int k, p;
   double tol, prev_res, pred_res, maxres;
 };
@@ -1082,6 +1084,8 @@ __global__ void ctl_init_kernel(EigCtl* ctl, int max_it, double tol, int k, int 
   ctl->msw = 3;
   ctl->last_sweeps = 0;
   ctl->rr_now = 0;
+  ctl->rr_fast = 0;
+  ctl->rr_exact = 1;
   ctl->stop = 0;
   ctl->tol = tol;
   ctl->prev_res = -1.0;
@@ -1104,6 +1108,10 @@ __global__ void ctl_begin_kernel(EigCtl* ctl, cudaGraphConditionalHandle h_rr, c
   // so the tail-tail rotations can be skipped (jacobi_block)
   ctl->kfix = ctl->rr_count > 0 ? ctl->k : ctl->p;
   ctl->rr_now = rr ? 1 : 0;
+  // an intermediate check only steers the basis and predicts the schedule: its product need not be
+  // the fp64 one (a check that could end the solve always is)
+  ctl->rr_fast = (rr && !final_ish) ? 1 : 0;
+  ctl->rr_exact = 1 - ctl->rr_fast;
   if (h_rr) cudaGraphSetConditional(h_rr, rr ? 1u : 0u);  // 0 handles: host-driven profiling mode
   if (h_pow) cudaGraphSetConditional(h_pow, 1u);
 }
@@ -1120,6 +1128,7 @@ __global__ void ctl_rr_kernel(EigCtl* ctl, const double* __restrict__ theta, con
   for (int r = 0; r < k; ++r) maxres = fmax(maxres, resid[r]);
   bool stop = false;
   if (!(theta[0] > 0.0)) { maxres = 0.0; ctl->conv = 1; stop = true; }  // G == 0: nothing to iterate
+  else if (maxres <= ctl->tol && ctl->rr_fast) { maxres = 2.0 * ctl->tol; }  // confirm with an exact check
   else if (maxres <= ctl->tol) { ctl->conv = 1; stop = true; }
   else if (it == ctl->max_it) { stop = true; }
   ctl->maxres = maxres;
@@ -1225,13 +1234,14 @@ int gemm_bm(const Ctx* c, bool fp32) {
   gemm_geometry(c->cfg.m, c->m_pad, c->p, c->num_sms, fp32, &BM, &KS, &RB, &KT);
   return BM;
 }
-avd_status gemm64(Ctx* c, const double* In, double* Y, float* Y32, int64_t r0 = 0, int64_t r1 = 0) {
+avd_status gemm64(Ctx* c, const double* In, double* Y, float* Y32, int64_t r0 = 0, int64_t r1 = 0,
+                  const int* skip = nullptr) {
   const int bm = gemm_bm(c, false);
   switch (c->p / 16) {
 #define CASE(PC)                                                                                        \
   case PC:                                                                                              \
-    return bm == 64 ? gemm_launch<double, 4, 2 * PC>(c, c->G, In, Y, Y32, nullptr, r0, r1)                \
-                    : gemm_launch<double, 2, 2 * PC>(c, c->G, In, Y, Y32, nullptr, r0, r1);
+    return bm == 64 ? gemm_launch<double, 4, 2 * PC>(c, c->G, In, Y, Y32, skip, r0, r1)                   \
+                    : gemm_launch<double, 2, 2 * PC>(c, c->G, In, Y, Y32, skip, r0, r1);
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
   }
@@ -1372,10 +1382,14 @@ avd_status enqueue_rr(Ctx* c, cudaGraphConditionalHandle h_loop, cudaGraphCondit
   const int p = c->p, k = c->k;
   EigCtl* ctl = reinterpret_cast<EigCtl*>(c->eig_ctl);
   int* jstats = reinterpret_cast<int*>(c->theta + p);
-  if (c->gram_free)
+  if (c->gram_free) {
     AVD_TRY(gf_product(c, c->Q, c->Y, nullptr, nullptr));  // Y = Xhat^T (Xhat Q)
-  else
-    AVD_TRY(gemm64(c, c->Q, c->Y, nullptr));  // Y = G Q (exact G, fp64)
+  } else {
+    AVD_TRY(gemm64(c, c->Q, c->Y, nullptr, 0, 0, &ctl->rr_fast));  // Y = G Q (exact G, fp64)
+    // intermediate checks: the power steps' product (gated on the device)
+    if (eig_i8_enabled(c)) AVD_TRY(gemm_i8(c, c->Q, c->Y, nullptr, &ctl->rr_exact, 0, 0));
+    else AVD_TRY(gemm32(c, c->Q32, c->Y, nullptr, &ctl->rr_exact));
+  }
   AVD_TRY(atb_fused<2>(c, c->Q, c->Y, c->W, c->theta, nullptr, &ctl->last_sweeps, nullptr, 40, &ctl->msw));
   AVD_TRY(matpp(c, c->Y, c->Z, c->Z32, c->Q, c->U, nullptr, c->W));  // Z = Y W, U = Q W (Ritz vectors)
   resid_kernel<<<k, 256, 0, c->stream>>>(c->Z, c->U, c->theta, m, p, c->resid);
