@@ -101,35 +101,37 @@ __global__ void __launch_bounds__(256) gf_w_kernel(const double* __restrict__ In
 }
 
 // ---------------------------------------------------------------- F1: P = Xhat Q
-// unit = (128-row block, 64-column slice h of P; persistent CTAs): K = m in 128-column stages,
-// A = ND digit planes (K-major, SWIZZLE_128B), B = the 4 W digit planes' rows h*64 .. +64; EVERY
+// unit = (128-row block, N-column slice h of P; persistent CTAs): K = m in 128-column stages,
+// A = ND digit planes (K-major, SWIZZLE_128B), B = the 4 W digit planes' rows h*N .. +N; EVERY
 // digit-product class c = e + d (0 .. ND+2, weight 128^(ND+2-c)) has its own int32 TMEM accumulator:
 // the low classes cannot be dropped — in a column whose scale a massive activation sets, the other
-// rows live in the low digits only.  Epilogue: P_ir = t_r sum_c acc_c 128^(ND+2-c) - corr_r (fp64,
-// stored fp32, rows >= l zero) and per-column max |P| (atomicMax on the bit patterns).
-template <int ND, int NS>
+// rows live in the low digits only.  N = p when the (ND + 3) classes fit TMEM (one slice, X read
+// once), else 64; DB: two accumulators (the epilogue of one unit overlaps the next) when 2 (ND+3) N
+// <= 512.  Epilogue: P_ir = t_r sum_c acc_c 128^(ND+2-c) - corr_r (fp64, stored fp32, rows >= l
+// zero) and per-column max |P| (atomicMax on the bit patterns).
+template <int ND, int NS, int N, bool DB>
 __global__ void __launch_bounds__(kGfThreads, 1) gf_xq_kernel(const CUtensorMap* __restrict__ tms, int64_t l_local,
-                                                              int64_t m_pad, int64_t l_pad, int KQ,
+                                                              int64_t m_pad, int64_t l_pad, int KQ, int NH,
                                                               const double* __restrict__ wsc, float* __restrict__ P,
                                                               unsigned* __restrict__ pmax, const int* __restrict__ skip) {
   if (skip && *skip) return;
   constexpr int NCLS = ND + 3;
-  constexpr uint32_t kB = 64 * 128;
-  constexpr uint32_t kStage = ND * kBox + 4 * kB;
+  constexpr uint32_t kAcc = NCLS * N;  // TMEM columns of one accumulator set
+  static_assert((DB ? 2 : 1) * kAcc <= 512, "TMEM");
+  constexpr uint32_t kB = N * 128;
+  constexpr uint32_t kStage = ((ND * kBox + 4 * kB + 1023) / 1024) * 1024;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t full_bar[NS], empty_bar[NS], tfull_bar, tempty_bar;
+  __shared__ uint64_t full_bar[NS], empty_bar[NS], tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_sh;
   const CUtensorMap* tmD = tms;
-  const CUtensorMap* tmW = tms + 1;
+  const CUtensorMap* tmW = tms + (ND == 2 ? 3 : 4);  // W digits in N-row boxes
   const uint32_t warp = warp_id(), lane = lane_id();
-  const int NH = KQ / 64;
   const int64_t n_units = ceil_div(l_local, 128) * NH;
   const int NC = (int)(m_pad / 128);
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
-    mbar_init(&tfull_bar, 1);
-    mbar_init(&tempty_bar, 8);
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull_bar[b], 1); mbar_init(&tempty_bar[b], 8); }
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) { tma_prefetch(tmD); tma_prefetch(tmW); }
@@ -149,20 +151,22 @@ __global__ void __launch_bounds__(kGfThreads, 1) gf_xq_kernel(const CUtensorMap*
           const uint32_t s = it % NS, ph = (it / NS) & 1;
           mbar_wait(&empty_bar[s], ph ^ 1);
           uint8_t* st = smem + s * kStage;
-          mbar_arrive_expect_tx(&full_bar[s], kStage);
+          mbar_arrive_expect_tx(&full_bar[s], ND * kBox + 4 * kB);
 #pragma unroll
           for (int e = 0; e < ND; ++e) tma_load_2d(st + e * kBox, tmD, &full_bar[s], c * 128, (int32_t)(e * l_pad + rb * 128));
 #pragma unroll
-          for (int d = 0; d < 4; ++d) tma_load_2d(st + ND * kBox + d * kB, tmW, &full_bar[s], c * 128, d * KQ + h * 64);
+          for (int d = 0; d < 4; ++d) tma_load_2d(st + ND * kBox + d * kB, tmW, &full_bar[s], c * 128, d * KQ + h * N);
         }
       }
     }
   } else if (warp == 1) {
-    constexpr uint32_t idesc = idesc_gf(128, 64, 0);
+    constexpr uint32_t idesc = idesc_gf(128, N, 0);
     uint32_t it = 0, ui = 0;
     for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++ui) {
-      mbar_wait(&tempty_bar, (ui & 1) ^ 1);
+      const uint32_t b = DB ? (ui & 1) : 0, br = DB ? (ui >> 1) : ui;
+      mbar_wait(&tempty_bar[b], (br & 1) ^ 1);
       tc_fence_after();
+      const uint32_t d0 = tmem + b * kAcc;
       for (int c = 0; c < NC; ++c, ++it) {
         const uint32_t s = it % NS, ph = (it / NS) & 1;
         mbar_wait(&full_bar[s], ph);
@@ -176,10 +180,10 @@ __global__ void __launch_bounds__(kGfThreads, 1) gf_xq_kernel(const CUtensorMap*
               const uint64_t a = smem_desc(base + e * kBox + kk * 32, 16, 1024, 2);
 #pragma unroll
               for (int d = 0; d < 4; ++d) {
-                const uint64_t b = smem_desc(base + ND * kBox + d * kB + kk * 32, 16, 1024, 2);
+                const uint64_t bd = smem_desc(base + ND * kBox + d * kB + kk * 32, 16, 1024, 2);
                 // first product of each class in the unit: e = 0 (classes 0..3), d = 3 (classes 4..)
                 const bool first = c == 0 && kk == 0 && (e == 0 || d == 3);
-                mma_i8x(tmem + (e + d) * 64, a, b, idesc, first ? 0u : 1u);
+                mma_i8x(d0 + (e + d) * N, a, bd, idesc, first ? 0u : 1u);
               }
             }
           }
@@ -187,7 +191,7 @@ __global__ void __launch_bounds__(kGfThreads, 1) gf_xq_kernel(const CUtensorMap*
         }
         __syncwarp();
       }
-      if (elect_one()) mma_commit(&tfull_bar);
+      if (elect_one()) mma_commit(&tfull_bar[b]);
       __syncwarp();
     }
   } else {
@@ -195,24 +199,25 @@ __global__ void __launch_bounds__(kGfThreads, 1) gf_xq_kernel(const CUtensorMap*
     const int half = (int)(warp - 2) >> 2;
     uint32_t ui = 0;
     for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++ui) {
+      const uint32_t b = DB ? (ui & 1) : 0, br = DB ? (ui >> 1) : ui;
       const int64_t rb = u / NH;
       const int h = (int)(u - rb * NH);
-      mbar_wait(&tfull_bar, ui & 1);
+      mbar_wait(&tfull_bar[b], br & 1);
       tc_fence_after();
       const int64_t row = rb * 128 + q * 32 + lane;
       const bool rok = row < l_local;
-      const uint32_t tb = tmem + ((q * 32) << 16);
+      const uint32_t tb = tmem + ((q * 32) << 16) + b * kAcc;
 #pragma unroll 1
-      for (int g = 0; g < 4; ++g) {
-        const int t0 = half * 32 + 8 * g;  // TMEM column in the slice
-        const int c0 = h * 64 + t0;         // column of P
+      for (int g = 0; g < N / 16; ++g) {
+        const int t0 = half * (N / 2) + 8 * g;  // TMEM column in the slice
+        const int c0 = h * N + t0;              // column of P
         double acc[8];
 #pragma unroll
         for (int t = 0; t < 8; ++t) acc[t] = 0.0;
 #pragma unroll
         for (int cl = 0; cl < NCLS; ++cl) {
           uint32_t rv[8];
-          tmem_ld8(tb + cl * 64 + t0, rv);
+          tmem_ld8(tb + cl * N + t0, rv);
           tmem_ld_wait();
           const double wgt = (double)(1ll << (7 * (ND + 2 - cl)));
 #pragma unroll
@@ -233,7 +238,7 @@ __global__ void __launch_bounds__(kGfThreads, 1) gf_xq_kernel(const CUtensorMap*
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar);
+      if (lane == 0) mbar_arrive(&tempty_bar[b]);
     }
   }
   tc_fence_before();
@@ -479,18 +484,46 @@ __global__ void __launch_bounds__(256) gf_fin_kernel(long long* __restrict__ Zhi
 
 int gf_kq(int p) { return p <= 64 ? 64 : 128; }
 
-template <int ND>
-avd_status launch_gf(Ctx* c, int KQ, int64_t grid1, int T, int S, int grid3, const int* skip) {
-  constexpr int NS = ND == 2 ? 3 : 2;  // <= 227 KB of shared memory (64 / 80 KB stages)
-  constexpr uint32_t st = ND * kBox + 4 * 64 * 128;
+// F1's slice width for (ND, p): p itself when the ND + 3 classes fit TMEM, else 64
+int gf_n1(int nd, int p) {
+  const int n = ((p + 15) / 16) * 16;
+  return (nd + 3) * n <= 512 ? n : 64;
+}
+
+template <int ND, int N>
+avd_status launch_xq(Ctx* c, int KQ, const int* skip) {
+  if constexpr ((ND + 3) * N > 512) {  // never chosen by gf_n1
+    set_error("Gram-free slice width exceeds TMEM");
+    return AVD_EINVAL;
+  } else {
+  constexpr bool DB = 2 * (ND + 3) * N <= 512;
+  constexpr uint32_t st = ((ND * kBox + 4 * N * 128 + 1023) / 1024) * 1024;
+  constexpr int NS = (int)std::min<uint32_t>(4, (220 * 1024) / st);
   const int sm = NS * (int)st + 1024;
-  AVD_CUDA(smem_attr(gf_xq_kernel<ND, NS>, sm));
-  gf_xq_kernel<ND, NS><<<(unsigned)grid1, kGfThreads, sm, c->stream>>>(c->gf_tm, c->cfg.l_local, c->m_pad, c->l_pad, KQ,
-                                                                     c->gf_wsc, c->gf_P, c->gf_pmax, skip);
+  const int NH = (c->p + N - 1) / N;
+  const int64_t grid = std::min<int64_t>(ceil_div(c->cfg.l_local, 128) * NH, c->num_sms);
+  AVD_CUDA(smem_attr(gf_xq_kernel<ND, NS, N, DB>, sm));
+  gf_xq_kernel<ND, NS, N, DB><<<(unsigned)grid, kGfThreads, sm, c->stream>>>(
+      c->gf_tm, c->cfg.l_local, c->m_pad, c->l_pad, KQ, NH, c->gf_wsc, c->gf_P, c->gf_pmax, skip);
   AVD_LAUNCHED(c);
+  return AVD_OK;
+  }
+}
+
+template <int ND>
+avd_status launch_gf(Ctx* c, int KQ, int T, int S, int grid3, const int* skip) {
+  switch (gf_n1(ND, c->p)) {
+#define CASE(NN) case NN: AVD_TRY((launch_xq<ND, NN>(c, KQ, skip))); break;
+    CASE(16) CASE(32) CASE(48) CASE(64) CASE(80) CASE(96)
+#undef CASE
+    default: set_error("unsupported Gram-free slice width"); return AVD_EINVAL;
+  }
   gf_pq_kernel<<<(unsigned)std::min<int64_t>(4 * c->num_sms, ceil_div(c->l_pad, 256 / (KQ / 4))), 256, 0, c->stream>>>(
       c->gf_P, c->l_pad, KQ, c->gf_pmax, c->gf_pd, c->gf_zsum, c->gf_tq, skip);
   AVD_LAUNCHED(c);
+  constexpr int NS = ND == 2 ? 3 : 2;  // <= 227 KB of shared memory (64 / 80 KB stages)
+  constexpr uint32_t st = ND * kBox + 4 * 64 * 128;
+  const int sm = NS * (int)st + 1024;
   AVD_CUDA(smem_attr(gf_xtp_kernel<ND, NS>, sm));
   gf_xtp_kernel<ND, NS><<<(unsigned)grid3, kGfThreads, sm, c->stream>>>(c->gf_tm, c->m_pad, c->l_pad, KQ, c->l_pad / 128,
                                                                       T, S, c->gf_zi, c->gf_zlo, skip);
@@ -527,8 +560,8 @@ avd_status gf_prepare(Ctx* c) {
   AVD_TRY(alloc(&c->gf_zlo, sizeof(long long) * c->m_pad * KQ));
   AVD_TRY(alloc(&c->gf_dd, sizeof(double) * c->m_pad));
   AVD_TRY(alloc(&c->gf_qsq, sizeof(long long) * c->m_pad));
-  AVD_TRY(alloc(&c->gf_tm, 3 * sizeof(CUtensorMap)));
-  CUtensorMap tm[3];
+  AVD_TRY(alloc(&c->gf_tm, 5 * sizeof(CUtensorMap)));
+  CUtensorMap tm[5];
   auto enc = tma_encode_fn();
   uint32_t es[2] = {1, 1};
   {  // X digit planes [nd_max][l_pad][m_pad], 128 x 128 boxes (K-major for F1, MN-major for F3)
@@ -559,6 +592,15 @@ avd_status gf_prepare(Ctx* c) {
       return AVD_ECUDA;
     }
   }
+  for (int nd = 2; nd <= 3; ++nd) {  // W digits in F1's N-row boxes (tm[3]: 2 digits, tm[4]: 3)
+    uint64_t dims[2] = {(uint64_t)c->m_pad, (uint64_t)(4 * KQ)}, str[1] = {(uint64_t)c->m_pad};
+    uint32_t box[2] = {128, (uint32_t)gf_n1(nd, c->p)};
+    if (enc(&tm[1 + nd], CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, c->gf_wd, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      set_error("cuTensorMapEncodeTiled failed (Gram-free W slice map)");
+      return AVD_ECUDA;
+    }
+  }
   AVD_CUDA(cudaMemcpyAsync(c->gf_tm, tm, sizeof(tm), cudaMemcpyHostToDevice, c->stream));
   return AVD_OK;
 }
@@ -571,8 +613,7 @@ avd_status gf_product(Ctx* c, const double* In, double* Y, float* Y32, const int
   gf_w_kernel<<<KQ, 256, 0, c->stream>>>(In, c->p, m, c->m_pad, c->shift, c->qsum, inv_l, KQ, c->gf_wd, c->gf_wsc,
                                           c->gf_pmax, c->gf_zsum, skip);
   AVD_LAUNCHED(c);
-  const int NH = KQ / 64;
-  const int64_t grid1 = std::min<int64_t>(ceil_div(c->cfg.l_local, 128) * NH, c->num_sms);
+  const int NH = KQ / 64;  // F3's 64-column slices
   const int T = (int)(c->m_pad / 128);
   const int64_t NK = c->l_pad / 128;
   // row-range splits: every unit <= 256 stages (int32 class sums stay exact); among those, the S
@@ -589,7 +630,7 @@ avd_status gf_product(Ctx* c, const double* In, double* Y, float* Y32, const int
   }
   const int grid3 = (int)std::min<int64_t>((int64_t)T * S * NH, c->num_sms);
   const bool nd3 = c->nd == 3;
-  AVD_TRY(nd3 ? launch_gf<3>(c, KQ, grid1, T, S, grid3, skip) : launch_gf<2>(c, KQ, grid1, T, S, grid3, skip));
+  AVD_TRY(nd3 ? launch_gf<3>(c, KQ, T, S, grid3, skip) : launch_gf<2>(c, KQ, T, S, grid3, skip));
   gf_fin_kernel<<<(unsigned)ceil_div(m * KQ, 256), 256, 0, c->stream>>>(c->gf_zi, c->gf_zlo, KQ, c->p, m, c->shift,
                                                                         c->qsum, inv_l, c->gf_tq, c->gf_zsum, c->gf_dd, In,
                                                                         Y, Y32, skip);
