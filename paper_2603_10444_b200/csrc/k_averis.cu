@@ -57,7 +57,6 @@ struct AvCtx {
   void* Y_stage = nullptr;
   std::vector<void*> allocs;
   bool timing = false;
-  int dbg = 0;  // AVD_AV_DBG (timing experiments only): 1 no stores, 2 no epilogue, 4 no scale copies
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // AVD_AVERIS_TIMING: stage boundaries
 };
 
@@ -445,7 +444,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kAvGemmThreads, 1) a
     const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
     const __grid_constant__ CUtensorMap tmSA, const __grid_constant__ CUtensorMap tmSB,
     const __grid_constant__ CUtensorMap tmY, int64_t l, int64_t n, int KB, int64_t MT2, int64_t NT, int64_t kb4,
-    const float* __restrict__ gsc, const float* __restrict__ bias, int dbg) {
+    const float* __restrict__ gsc, const float* __restrict__ bias) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t full_bar[kAvNS], empty_bar[kAvNS], tfull_bar, tempty_bar;
@@ -501,7 +500,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kAvGemmThreads, 1) a
       constexpr uint32_t idesc = idesc_nvf4(256, 256);
       uint32_t it = 0, ui = 0;
       for (int64_t pt = cid; pt < pairs; pt += ncl, ++ui) {
-        if (!(dbg & 2)) mbar_wait(&tempty_bar, (ui & 1) ^ 1);
+        mbar_wait(&tempty_bar, (ui & 1) ^ 1);
         tc_fence_after();
         for (int kb = 0; kb < KB; ++kb, ++it) {
           const uint32_t s = it % kAvNS, ph = (it / kAvNS) & 1;
@@ -511,13 +510,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kAvGemmThreads, 1) a
             const uint32_t base = smem_u32(smem + s * kAvStage);
             const uint32_t sfa_s = base + kAvA + kAvB, sfb_s = sfa_s + kAvSFA;
             const uint32_t tsf = tmem + 256 + (it & 3) * 48;  // 4 rotating slots: SFA 16 columns, SFB 32
-            if (!(dbg & 4)) {
 #pragma unroll
-              for (int kk = 0; kk < 4; ++kk) {
-                tmem_cp_sf_pair(tsf + kk * 4, smem_desc(sfa_s + kk * 512, 0, 128, 0));
-                tmem_cp_sf_pair(tsf + 16 + kk * 8, smem_desc(sfb_s + kk * 512, 0, 128, 0));
-                tmem_cp_sf_pair(tsf + 16 + kk * 8 + 4, smem_desc(sfb_s + kAvSFA + kk * 512, 0, 128, 0));
-              }
+            for (int kk = 0; kk < 4; ++kk) {
+              tmem_cp_sf_pair(tsf + kk * 4, smem_desc(sfa_s + kk * 512, 0, 128, 0));
+              tmem_cp_sf_pair(tsf + 16 + kk * 8, smem_desc(sfb_s + kk * 512, 0, 128, 0));
+              tmem_cp_sf_pair(tsf + 16 + kk * 8 + 4, smem_desc(sfb_s + kAvSFA + kk * 512, 0, 128, 0));
             }
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
@@ -539,7 +536,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kAvGemmThreads, 1) a
     uint32_t ui = 0;
     for (int64_t pt = cid; pt < pairs; pt += ncl, ++ui) {
       const int64_t mt = 2 * (pt / NT) + rank, nt = pt % NT;
-      if (dbg & 2) continue;
       mbar_wait(&tfull_bar, ui & 1);
       tc_fence_after();
       uint32_t v[128];
@@ -552,7 +548,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kAvGemmThreads, 1) a
       if (lane == 0) av_arrive_remote(tempty0);
       const int64_t row0 = mt * 128 + q * 32;
       const int64_t col0 = nt * 256 + h * 128;
-      if (row0 < l && !(dbg & 1)) {
+      if (row0 < l) {
         const uint32_t sw = lane & 7;
         // per store: 32 rows x 128 B (32 fp32 or 64 bf16 columns), 128B-swizzled
         constexpr int CW = BF ? 64 : 32;
@@ -708,7 +704,7 @@ avd_status av_forward(AvCtx* c, const float* X, void* Y) {
   }
   const int grid = 2 * (int)std::min<int64_t>(MT2 * NT, c->num_sms / 2);
   kern<<<grid, kAvGemmThreads, smem, c->stream>>>(c->tmA, c->tmB, c->tmSA, c->tmSB, tmY, l, n, KB, MT2, NT,
-                                                            c->kb4, c->gsc, c->bias, c->dbg);
+                                                            c->kb4, c->gsc, c->bias);
   AVD_LAUNCHED(c);
   if (c->timing) AVD_CUDA(cudaEventRecord(c->ev[3], c->stream));
   return AVD_OK;
@@ -752,7 +748,6 @@ avd_status avd_averis_create(const avd_averis_config* cfg, avd_averis_handle* ou
   c->sr = (cfg->flags & AVD_AVERIS_STOCHASTIC) != 0;
   c->bf16_out = (cfg->flags & AVD_AVERIS_BF16_OUT) != 0;
   c->timing = (cfg->flags & AVD_AVERIS_TIMING) != 0;
-  if (const char* e = getenv("AVD_AV_DBG")) c->dbg = atoi(e);
   for (int i = 0; i < 4 && c->timing; ++i)
     if (cudaEventCreate(&c->ev[i]) != cudaSuccess) { cudaGetLastError(); avd::set_error("cudaEventCreate failed"); delete h; return AVD_ECUDA; }
   c->R = (int)std::max<int64_t>(1, std::min<int64_t>(c->l, 4 * c->num_sms / std::max<int64_t>(1, avd::ceil_div(c->m, 1024))));
