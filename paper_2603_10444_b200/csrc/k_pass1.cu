@@ -139,12 +139,26 @@ __global__ void __launch_bounds__(256) sample_reduce_kernel(int64_t m, int r1, d
   const int64_t j = (int64_t)blockIdx.x * 32 + c;
   double s = 0.0;
   float mx = -FLT_MAX, mn = FLT_MAX;
-  if (j < m)
-    for (int r = g; r < r1; r += 8) {
-      s += colsum_part[(int64_t)r * m + j];
+  if (j < m) {
+    // four partial rows in flight (independent accumulators, combined in a fixed order)
+    double s4[4] = {0.0, 0.0, 0.0, 0.0};
+    int r = g;
+    for (; r + 24 < r1; r += 32) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t o = (int64_t)(r + 8 * u) * m + j;
+        s4[u] += colsum_part[o];
+        mx = fmaxf(mx, colmax_part[o]);
+        mn = fminf(mn, colmin_part[o]);
+      }
+    }
+    for (; r < r1; r += 8) {
+      s4[0] += colsum_part[(int64_t)r * m + j];
       mx = fmaxf(mx, colmax_part[(int64_t)r * m + j]);
       mn = fminf(mn, colmin_part[(int64_t)r * m + j]);
     }
+    s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+  }
   s_s[g][c] = s; s_mx[g][c] = mx; s_mn[g][c] = mn;
   __syncthreads();
   if (g == 0 && j < m) {
@@ -582,13 +596,29 @@ __global__ void __launch_bounds__(256) pass1_reduce_kernel(
   double qe = 0.0, cs = 0.0, qq = 0.0;
   float ym = 0.f;
   if (j < m) {
-    for (int r = g; r < r1; r += 8) {
+    // four partial rows in flight (independent accumulators, combined in a fixed order)
+    double qe4[4] = {0, 0, 0, 0}, cs4[4] = {0, 0, 0, 0}, qq4[4] = {0, 0, 0, 0};
+    int r = g;
+    for (; r + 24 < r1; r += 32) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t o = (int64_t)(r + 8 * u) * m + j;
+        qs += qsum_part[o];
+        qe4[u] += (double)qerr_part[o];
+        ym = fmaxf(ym, ymax_part[o]);
+        if (full) { cs4[u] += colsum_part[o]; qq4[u] += ysq_part[o]; }
+      }
+    }
+    for (; r < r1; r += 8) {
       const int64_t o = (int64_t)r * m + j;
       qs += qsum_part[o];
-      qe += (double)qerr_part[o];
+      qe4[0] += (double)qerr_part[o];
       ym = fmaxf(ym, ymax_part[o]);
-      if (full) { cs += colsum_part[o]; qq += ysq_part[o]; }
+      if (full) { cs4[0] += colsum_part[o]; qq4[0] += ysq_part[o]; }
     }
+    qe = (qe4[0] + qe4[1]) + (qe4[2] + qe4[3]);
+    cs = (cs4[0] + cs4[1]) + (cs4[2] + cs4[3]);
+    qq = (qq4[0] + qq4[1]) + (qq4[2] + qq4[3]);
   }
   s_qs[g][c] = qs; s_qq[g][c] = qq; s_qe[g][c] = qe; s_cs[g][c] = cs; s_ym[g][c] = ym;
   __syncthreads();
