@@ -209,8 +209,16 @@ __device__ __forceinline__ T block_exclusive_scan(T v, T* warp_tot, T& total) {
 
 // exclusive scan of the per-block (sel, tie) counts in one CTA (each thread owns a contiguous
 // run of blocks); quota / offset come from avd_tie_quota (host)
+// ties_dev != nullptr (one rank): the tie quota is taken on the device — every tie of the threshold
+// key up to q (clamped to the ties held), offset 0 — with no host round trip
 __global__ void __launch_bounds__(1024) blk_scan_kernel(int64_t* __restrict__ blk, int64_t nblk, int64_t quota,
-                                                        int64_t offset, int64_t ties_local, DevPlan* __restrict__ dp) {
+                                                        int64_t offset, int64_t ties_local, DevPlan* __restrict__ dp,
+                                                        const long long* __restrict__ ties_dev) {
+  if (ties_dev) {
+    ties_local = ties_dev[1];
+    quota = dp->empty ? 0 : max((int64_t)0, min((int64_t)dp->q, ties_local));
+    offset = 0;
+  }
   __shared__ int64_t wt[1024 / 32 + 1];
   const int64_t per = (nblk + 1023) / 1024;
   const int64_t b0 = threadIdx.x * per, b1 = min(nblk, b0 + per);
@@ -403,19 +411,25 @@ avd_status launch_gather(Ctx* c, const float* X, int rank, int64_t* top_idx, dou
   // exchanged per-rank counts -> this rank's tie quota and global offset (host integer logic)
   const int world = c->cfg.world;
   // both land in the pinned scratch (pageable D2H copies cost ~10 us each)
-  long long* hs = reinterpret_cast<long long*>(c->eig_host);
-  AVD_CUDA(cudaMemcpyAsync(hs, c->ties, sizeof(long long) * 2 * world, cudaMemcpyDeviceToHost, c->stream));
-  AVD_CUDA(cudaMemcpyAsync(hs + 2 * world, c->dplan, sizeof(DevPlan), cudaMemcpyDeviceToHost, c->stream));
-  AVD_CUDA(cudaStreamSynchronize(c->stream));
-  std::vector<long long> tc(hs, hs + 2 * world);
-  std::memcpy(&c->hplan, hs + 2 * world, sizeof(DevPlan));
-  std::vector<int64_t> sel(world), tie(world);
-  for (int r = 0; r < world; ++r) { sel[r] = tc[r]; tie[r] = tc[world + r]; }
-  int64_t quota = 0, offset = 0;
-  AVD_TRY(avd_tie_quota(sel.data(), tie.data(), world, rank, c->hplan.empty ? 0 : c->hplan.q, &quota, &offset));
-  // per-block (sel, tie) counts were accumulated by mark_kernel
-  blk_scan_kernel<<<1, 1024, 0, c->stream>>>(c->blk_cnt, c->nblk, quota, offset, tie[rank], c->dplan);
-  AVD_LAUNCHED(c);
+  if (world == 1) {  // the quota is taken on the device (no host round trip)
+    blk_scan_kernel<<<1, 1024, 0, c->stream>>>(c->blk_cnt, c->nblk, 0, 0, 0, c->dplan,
+                                               reinterpret_cast<const long long*>(c->ties));
+    AVD_LAUNCHED(c);
+  } else {
+    long long* hs = reinterpret_cast<long long*>(c->eig_host);
+    AVD_CUDA(cudaMemcpyAsync(hs, c->ties, sizeof(long long) * 2 * world, cudaMemcpyDeviceToHost, c->stream));
+    AVD_CUDA(cudaMemcpyAsync(hs + 2 * world, c->dplan, sizeof(DevPlan), cudaMemcpyDeviceToHost, c->stream));
+    AVD_CUDA(cudaStreamSynchronize(c->stream));
+    std::vector<long long> tc(hs, hs + 2 * world);
+    std::memcpy(&c->hplan, hs + 2 * world, sizeof(DevPlan));
+    std::vector<int64_t> sel(world), tie(world);
+    for (int r = 0; r < world; ++r) { sel[r] = tc[r]; tie[r] = tc[world + r]; }
+    int64_t quota = 0, offset = 0;
+    AVD_TRY(avd_tie_quota(sel.data(), tie.data(), world, rank, c->hplan.empty ? 0 : c->hplan.q, &quota, &offset));
+    // per-block (sel, tie) counts were accumulated by mark_kernel
+    blk_scan_kernel<<<1, 1024, 0, c->stream>>>(c->blk_cnt, c->nblk, quota, offset, tie[rank], c->dplan, nullptr);
+    AVD_LAUNCHED(c);
+  }
   emit_kernel<<<(unsigned)c->nblk, kSelThreads, 0, c->stream>>>(c->bm_sel, c->bm_tie, c->nwords, c->nblk, c->blk_cnt,
                                                                  c->dplan, c->cfg.row_offset * c->cfg.m, top_idx);
   AVD_LAUNCHED(c);
