@@ -362,8 +362,10 @@ __device__ __forceinline__ void rr_pair(int p, int step, int i, int& P, int& Q) 
 // singular and eigen decompositions coincide).  The rotation of a pair comes from its Gram entries
 // (alpha = |a_p|^2, beta = |a_q|^2, gamma = a_p . a_q) by the same Rutishauser formula as the
 // two-sided method; stop when gamma^2 <= 1e-20 alpha beta for every pair.  Step s rotates the P/2
-// disjoint pairs of the round-robin ordering; warp u owns pair u (its two columns of A and two rows
-// of V^T), so a step needs no synchronisation inside, only one barrier before the next step.
+// disjoint pairs of the round-robin ordering; half-warp u owns pair u (its two columns of A and two
+// rows of V^T), so a step needs no synchronisation inside, only one barrier before the next step.
+// Half-warps rather than warps: the step is bound by the shuffle pipe (three fp64 butterflies per
+// pair), and a 16-lane butterfly serves two pairs per warp instruction with one level fewer.
 // kfix < P: the basis is ordered (columns >= kfix span the unconverged tail of the spectrum) and
 // rotations between two tail columns are skipped — they only mix tail vectors among themselves, so
 // the leading kfix pairs are exact eigenpairs of A once the coupling pairs are orthogonal, and the
@@ -371,15 +373,16 @@ __device__ __forceinline__ void rr_pair(int p, int step, int i, int& P, int& Q) 
 template <int P, int LDA>
 __device__ int jacobi_onesided(double* A, double* Vt, int* fl, int max_sweeps, int kfix) {
   constexpr int half = P / 2;
-  constexpr int E = (P + 31) / 32;  // column elements per lane
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nwarps = blockDim.x >> 5;
+  constexpr int E = (P + 15) / 16;  // column elements per lane
+  const int hw = threadIdx.x >> 4, hl = threadIdx.x & 15;
+  const int nhw = blockDim.x >> 4;
+  const unsigned hmask = (threadIdx.x & 16) ? 0xFFFF0000u : 0x0000FFFFu;
   int sweep = 0;
   for (; sweep < max_sweeps; ++sweep) {
     if (threadIdx.x == 0) fl[sweep & 1] = 0;  // read after this sweep's last barrier
     __syncthreads();
     for (int step = 0; step < P - 1; ++step) {
-      for (int u = warp; u < half; u += nwarps) {
+      for (int u = hw; u < half; u += nhw) {
         int pc, qc;
         rr_pair(P, step, u, pc, qc);
         if (pc >= kfix) continue;  // tail-tail pair (pc < qc)
@@ -387,7 +390,7 @@ __device__ int jacobi_onesided(double* A, double* Vt, int* fl, int max_sweeps, i
         double al = 0.0, be = 0.0, ga = 0.0;
 #pragma unroll
         for (int t = 0; t < E; ++t) {
-          const int i = lane + 32 * t;
+          const int i = hl + 16 * t;
           ap[t] = i < P ? A[i * LDA + pc] : 0.0;
           aq[t] = i < P ? A[i * LDA + qc] : 0.0;
           al = fma(ap[t], ap[t], al);
@@ -395,19 +398,19 @@ __device__ int jacobi_onesided(double* A, double* Vt, int* fl, int max_sweeps, i
           ga = fma(ap[t], aq[t], ga);
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          al += __shfl_xor_sync(0xFFFFFFFFu, al, o);
-          be += __shfl_xor_sync(0xFFFFFFFFu, be, o);
-          ga += __shfl_xor_sync(0xFFFFFFFFu, ga, o);
+        for (int o = 8; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(hmask, al, o);
+          be += __shfl_xor_sync(hmask, be, o);
+          ga += __shfl_xor_sync(hmask, ga, o);
         }
         double c, sn;
         bool rot;
-        jacobi_rotation(al, be, ga, c, sn, rot, 1e-20);  // identical in every lane
+        jacobi_rotation(al, be, ga, c, sn, rot, 1e-20);  // identical in every lane of the half
         if (!rot) continue;
-        if (lane == 0) fl[sweep & 1] = 1;
+        if (hl == 0) fl[sweep & 1] = 1;
 #pragma unroll
         for (int t = 0; t < E; ++t) {
-          const int i = lane + 32 * t;
+          const int i = hl + 16 * t;
           if (i < P) {
             A[i * LDA + pc] = c * ap[t] - sn * aq[t];
             A[i * LDA + qc] = sn * ap[t] + c * aq[t];
