@@ -1175,6 +1175,14 @@ __global__ void ctl_u_kernel(EigCtl* ctl, const double* __restrict__ diag, cudaG
 // split-K geometry shared by the plan (workspace) and the launches: as many K slices as fill
 // ONE wave of resident CTAs (3 fp32 / 2 fp64 CTAs per SM, smem-bound) — a partial second wave
 // would double the kernel's time
+// CTAs of the split-K GEMM resident at once: 3 (fp32) / 2 (fp64) per SM for the register-tiled
+// row blocks, and for the 32-row blocks of small m (c1, c2: a 16 MB G32 in L2, every product
+// latency-bound) as many as shared memory holds, up to 8 per SM
+int64_t gemm_resident(int num_sms, bool fp32, int BM, int p) {
+  if (!(fp32 && BM <= 32)) return (int64_t)num_sms * (fp32 ? 3 : 2);
+  const int64_t sm = (int64_t)kSkStages * (kSkBK * BM + kSkBK * p) * 4 + 2064;  // + static + reserved
+  return (int64_t)num_sms * std::max<int64_t>(3, std::min<int64_t>(8, (228 * 1024) / sm));
+}
 void gemm_geometry(int64_t m, int64_t m_pad, int p, int num_sms, bool fp32, int* BM, int* KS, int* RB, int* KT) {
   *KT = (int)ceil_div(m, kSkBK);
   const int64_t want = (int64_t)num_sms * (fp32 ? 3 : 2);  // resident CTAs (smem-bound)
@@ -1188,14 +1196,17 @@ void gemm_geometry(int64_t m, int64_t m_pad, int p, int num_sms, bool fp32, int*
     if (std::min<int64_t>(want / rb, *KT) * 8 <= *KT || want / rb < 1) break;
   }
   *RB = (int)(m_pad / *BM);
-  *KS = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(want / *RB, *KT), std::max<int64_t>(1, *KT / 8)));
+  // 32-row blocks: more CTAs in flight and >= 4 K tiles each (the K loop is latency-bound there)
+  const bool small = fp32 && *BM <= 32;
+  const int64_t res = gemm_resident(num_sms, fp32, *BM, p);
+  *KS = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(res / *RB, *KT), std::max<int64_t>(1, *KT / (small ? 4 : 8))));
 }
 size_t gemm_part_bytes(int64_t m, int64_t m_pad, int p, int num_sms) {
   size_t best = 0;
   for (int f = 0; f < 2; ++f) {  // RB x KS <= the resident-CTA count for any row range (gemm_launch)
     int BM, KS, RB, KT;
     gemm_geometry(m, m_pad, p, num_sms, f == 0, &BM, &KS, &RB, &KT);
-    const int64_t want = (int64_t)num_sms * (f == 0 ? 3 : 2);
+    const int64_t want = gemm_resident(num_sms, f == 0, BM, p);
     best = std::max(best, (size_t)std::max<int64_t>(want, (int64_t)RB * KS) * BM * p *
                               (f == 0 ? sizeof(float) : sizeof(double)));
   }
@@ -1217,7 +1228,7 @@ avd_status gemm_launch(Ctx* c, const T* Gm, const T* In, double* Y, float* Y32, 
   if (r1 > r0) {  // a row range: fewer row blocks, more K slices (same partial-buffer bound)
     rb0 = (int)(r0 / BM);
     RB = (int)ceil_div(r1 - r0, BM);
-    const int64_t want = (int64_t)c->num_sms * (sizeof(T) == 4 ? 3 : 2);
+    const int64_t want = gemm_resident(c->num_sms, sizeof(T) == 4, BM, p);
     KS = (int)std::max<int64_t>(1, std::min<int64_t>(want / RB, KT));
   }
   const int sm = kSkStages * (kSkBK * BM + kSkBK * p) * (int)sizeof(T);
