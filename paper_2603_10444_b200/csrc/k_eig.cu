@@ -1179,6 +1179,10 @@ __global__ void ctl_u_kernel(EigCtl* ctl, const double* __restrict__ diag, cudaG
 // row blocks, and for the 32-row blocks of small m (c1, c2: a 16 MB G32 in L2, every product
 // latency-bound) as many as shared memory holds, up to 8 per SM
 int64_t gemm_resident(int num_sms, bool fp32, int BM, int p) {
+  if (!fp32 && BM == 128) {  // fp64 128-row register tiles (p <= 48): shared memory allows one per SM
+    const int64_t sm = (int64_t)kSkStages * (kSkBK * BM + kSkBK * p) * 8 + 2064;
+    return (int64_t)num_sms * std::max<int64_t>(1, (228 * 1024) / sm);
+  }
   if (!(fp32 && BM <= 32)) return (int64_t)num_sms * (fp32 ? 3 : 2);
   const int64_t sm = (int64_t)kSkStages * (kSkBK * BM + kSkBK * p) * 4 + 2064;  // + static + reserved
   return (int64_t)num_sms * std::max<int64_t>(3, std::min<int64_t>(8, (228 * 1024) / sm));
@@ -1188,7 +1192,9 @@ void gemm_geometry(int64_t m, int64_t m_pad, int p, int num_sms, bool fp32, int*
   const int64_t want = (int64_t)num_sms * (fp32 ? 3 : 2);  // resident CTAs (smem-bound)
   // the largest row block (register tile) that still leaves every CTA >= 8 K tiles of work:
   // small m (c1, c2) takes 32-row blocks so the grid fills without slivers of K per CTA
-  const int big = (fp32 && p <= 64) ? 128 : 64;
+  // fp64 (the Rayleigh-Ritz product): 8 x 6 register tiles for p <= 48 halve the shared-memory
+  // operand bytes per DFMA (a 4 x 6 tile needs ~1.7x the SM's shared-memory bandwidth)
+  const int big = ((fp32 && p <= 64) || (!fp32 && p <= 48 && m >= 4096)) ? 128 : 64;
   *BM = big;
   for (int bm = big; bm >= 32; bm /= 2) {
     *BM = bm;
@@ -1254,6 +1260,7 @@ avd_status gemm64(Ctx* c, const double* In, double* Y, float* Y32, int64_t r0 = 
   switch (c->p / 16) {
 #define CASE(PC)                                                                                        \
   case PC:                                                                                              \
+    if constexpr (PC <= 3) if (bm == 128) return gemm_launch<double, 8, 2 * PC>(c, c->G, In, Y, Y32, skip, r0, r1); \
     return bm == 64 ? gemm_launch<double, 4, 2 * PC>(c, c->G, In, Y, Y32, skip, r0, r1)                   \
                     : gemm_launch<double, 2, 2 * PC>(c, c->G, In, Y, Y32, skip, r0, r1);
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
